@@ -1,0 +1,184 @@
+/*
+ * sknr_gpu.h -- C ABI of the B200-native SK-NR(ell) core (libsknr_b200.so).
+ *
+ * Drop-in boundary for the reference's C++ solver API in namespace sknr
+ * (/root/reference/proj/include/sknr/{types,core,objective,spectral,solver}.hpp).
+ * Plain pointers and sizes only; all matrices are COLUMN-MAJOR doubles exactly
+ * like the reference's Eigen::MatrixXd (types.hpp:10-12), so an Eigen caller
+ * passes .data() zero-copy. Host buffers are owned by the caller; device
+ * memory is owned by the problem handle. A handle owns one CUDA stream and is
+ * not thread-safe; concurrent solves use separate handles (the reference's
+ * "concurrent solves on a shared read-only problem", maps to
+ * one handle per thread).
+ *
+ * Every entry point returns an sknr_status. On failure sknr_last_error()
+ * returns the message (thread-local). Invalid-argument messages repeat the
+ * reference's std::invalid_argument texts verbatim so the C++ facade
+ * (include/sknr_b200.hpp) can rethrow the same exception with the same what().
+ * There is no CPU fallback: without a usable sm_100 device every compute call
+ * fails with SKNR_ECUDA.
+ */
+#ifndef SKNR_GPU_H
+#define SKNR_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SKNR_OK = 0,
+    SKNR_EINVAL = 1,   /* std::invalid_argument in the reference            */
+    SKNR_EEIGEN = 2,   /* EigensolverError (spectral.hpp:60-68)              */
+    SKNR_ECUDA = 3,    /* CUDA failure / no device / extension unusable      */
+    SKNR_ENCCL = 4,    /* NCCL failure (multi-GPU row sharding)              */
+    SKNR_ERUNTIME = 5, /* std::runtime_error (e.g. anneal stage wrapping)    */
+    SKNR_EINTERNAL = 9
+} sknr_status;
+
+typedef struct sknr_problem_s* sknr_problem;
+
+/* Last error message of the calling thread ("" if none). */
+const char* sknr_last_error(void);
+/* best_residual carried by the last SKNR_EEIGEN (EigensolverError::best_residual). */
+double sknr_last_best_residual(void);
+/* Library / device description, e.g. "sknr_b200 0.1.0 sm_100a (NVIDIA B200, 148 SMs)". */
+int sknr_version(char* buf, int cap);
+/* Number of kernel launches this process issued (evidence for bench "gpu_launches"). */
+int64_t sknr_kernel_launch_count(void);
+
+/* ---------------------------------------------------------------- problems
+ * sknr_problem_create_dense replaces EotProblem(CostMatrix, DiscreteMeasure,
+ * DiscreteMeasure, eps) (types.hpp:47-69, types.cpp:7-43): validates weights
+ * (w>0 finite, |sum-1|<=1e-12), cost finiteness and eps>0 with the same
+ * messages, and uploads cost (n x m col-major) once.
+ *
+ * sknr_problem_create_points is the on-the-fly variant the north star asks
+ * for: C_ij = cost_scale * ||x_i - y_j||^2 (sq_euclidean_cost,
+ * generators.cpp:94-103) is never stored; x is n x d, y is m x d (col-major,
+ * like harness::PointCloud::points, generators.hpp:12-19). cost_scale=1/maxC
+ * reproduces BASELINE C2's max-normalised cost.
+ *
+ * Row sharding (north star): with a communicator attached
+ * (sknr_problem_attach_comm) the handle holds only rows [row_begin, row_end)
+ * of the source side; the C ABI still takes and returns FULL-length host
+ * vectors (every rank passes identical inputs and receives identical outputs).
+ */
+int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const double* alpha,
+                              const double* beta, double epsilon, sknr_problem* out);
+int sknr_problem_create_points(const double* x, const double* y, int64_t n, int64_t m,
+                               int64_t d, double cost_scale, const double* alpha,
+                               const double* beta, double epsilon, sknr_problem* out);
+/* EotProblem::with_epsilon (types.hpp:60-62) without the dense-cost copy. */
+int sknr_problem_set_epsilon(sknr_problem p, double epsilon);
+int sknr_problem_info(sknr_problem p, int64_t* n, int64_t* m, int64_t* d, double* epsilon,
+                      int* kind /* 0 dense, 1 points */);
+int sknr_problem_destroy(sknr_problem p);
+
+/* ---------------------------------------------------------------- core.hpp
+ * core.hpp:16-43 / core.cpp:35-150 on host buffers (upload, device kernels,
+ * download). */
+int sknr_ctransform_of_f(sknr_problem p, const double* f, double* g);
+int sknr_ctransform_of_g(sknr_problem p, const double* g, double* f);
+int sknr_plan_marginals(sknr_problem p, const double* f, const double* g, double* row,
+                        double* col, double* gap_l2, double* gap_inf);
+/* coupling_from (core.cpp:84-103): n x m col-major into a host buffer. */
+int sknr_coupling(sknr_problem p, const double* f, const double* g, double* plan);
+
+/* ---------------------------------------------------------------- objective.hpp */
+int sknr_semi_dual_value(sknr_problem p, const double* f, double* value);
+/* restricted_derivatives_with_transform (objective.cpp:110-142); g = f^{C,eps}. */
+int sknr_restricted_derivatives(sknr_problem p, const double* f, const double* g,
+                                const double* vectors /* n x ell */, int64_t ell,
+                                double* grad /* ell */, double* hess /* ell x ell */);
+
+/* ---------------------------------------------------------------- spectral.hpp
+ * SinkhornOperator::apply_sym_block / apply_sym_t_block (spectral.cpp:68-102)
+ * and top_modes (spectral.cpp:125-193). Returns SKNR_EEIGEN with
+ * sknr_last_best_residual() when the residual target is not met. */
+int sknr_apply_sym_block(sknr_problem p, const double* f, const double* g,
+                         const double* v /* m x k */, int64_t k, double* out /* n x k */);
+int sknr_apply_sym_t_block(sknr_problem p, const double* f, const double* g,
+                           const double* u /* n x k */, int64_t k, double* out /* m x k */);
+int sknr_top_modes(sknr_problem p, const double* f, const double* g, int64_t ell, double tol,
+                   int64_t max_power_iters /* -1: 500*ell */, double* vectors /* n x ell */,
+                   double* vectors_sym /* n x ell */, double* rhos /* ell */,
+                   int64_t* sweeps /* may be NULL */);
+
+/* ---------------------------------------------------------------- solver.hpp */
+typedef struct {
+    double tol_omega;      /* 1e-9   (SolverConfig, solver.hpp:13-19) */
+    int64_t max_iter;      /* 100000 */
+    int64_t ell;           /* 0 = vanilla SK */
+    int32_t newton_enabled;/* 1 */
+    int32_t trace_enabled; /* 1 */
+    int32_t exact_marginals; /* 0: column marginal from the fused transform
+                                (beta_j expm1((g_j-h_j)/eps)); 1: explicit
+                                plan-sum passes as core.cpp:120-143 */
+    int32_t reserved;
+} sknr_config;
+
+void sknr_config_default(sknr_config* c);
+
+typedef struct {
+    int64_t index;
+    double marginal_error;      /* L2-sum rule, core.cpp:145-150 */
+    double marginal_error_inf;
+    double semi_dual_value;
+    int32_t newton_attempted;
+    int32_t newton_accepted;
+    double wall_time_ms;        /* device globaltimer per iteration */
+} sknr_record;
+
+/* solve (solver.cpp:71-156). basis: n x ell potential-coordinate vectors
+ * (SpectralBasis::vectors) or NULL; init_f/init_g both NULL or both set.
+ * trace may be NULL (trace_cap 0); trace_len returns the full length. */
+int sknr_solve(sknr_problem p, const sknr_config* cfg, const double* basis, int64_t basis_ell,
+               const double* init_f, const double* init_g, double* f_out, double* g_out,
+               int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
+               int64_t* trace_len);
+
+/* anneal (solver.cpp:158-222). warm_mode 0 none, 1 potentials, 2 spectral.
+ * Per stage s: f_out[s*n ..], g_out[s*m ..], iterations[s], converged[s];
+ * trace records are concatenated, stage s starting at trace_offsets[s]. */
+int sknr_anneal(sknr_problem p, const double* epsilons, int64_t stages, int warm_mode,
+                int refresh_basis, const sknr_config* cfg, double* f_out, double* g_out,
+                int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
+                int64_t* trace_offsets, int64_t* trace_len);
+
+/* ---------------------------------------------------------------- measurement
+ * Runs `passes` back-to-back transforms on device-resident data (no host
+ * copies) and reports the mean device time per pass (CUDA events on the
+ * handle's stream). which: 0 column LSE (ctransform_of_f), 1 row LSE
+ * (ctransform_of_g), 2 fixed-shift column sum pass (the steady-state kernel),
+ * 3 Newton restricted-derivative pass, 4 top_modes block pass. */
+int sknr_bench_pass(sknr_problem p, int which, int64_t ell, int passes, double* ms_per_pass,
+                    double* kernel_ms_per_pass);
+/* Runs `iters` SK-NR iterations (stopping test disabled) on device-resident
+ * state, one CUDA graph per iteration, and returns device ms per iteration and
+ * the number of kernels in one iteration's graph; bench.py's "value" leg. */
+int sknr_bench_iterations(sknr_problem p, const sknr_config* cfg, const double* basis,
+                          int64_t basis_ell, int64_t iters, double* ms_per_iter,
+                          int64_t* kernels_per_iter);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU. Rank 0 calls sknr_comm_unique_id, the id travels over
+ * any side channel (torch.distributed in bench.py), every rank calls
+ * sknr_comm_init with the same id. Problems created afterwards with
+ * sknr_problem_shard() keep only their row block; column (max,sum) partials,
+ * Krylov inner products and the gauge scalar are merged with NCCL over
+ * NVLink. NCCL is loaded with dlopen at sknr_comm_init (RTLD_NOLOAD first, so
+ * the copy torch already mapped is reused). */
+int sknr_comm_unique_id(unsigned char id[128]);
+int sknr_comm_init(int rank, int world, const unsigned char id[128], int device);
+int sknr_comm_destroy(void);
+/* Restrict a freshly created problem to rows [row_begin,row_end) of this rank
+ * under the attached communicator. */
+int sknr_problem_shard(sknr_problem p, int64_t row_begin, int64_t row_end);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKNR_GPU_H */

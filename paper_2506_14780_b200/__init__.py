@@ -1,0 +1,594 @@
+"""B200-native SK-NR(ell) core (arXiv 2506.14780) -- Python mirror of the
+reference's `sknr` module (/root/reference/proj/python/bindings.cpp:35-215).
+
+Every compute call goes through libsknr_b200.so (C ABI, include/sknr_gpu.h) on
+an sm_100a device. There is no CPU fallback: if the library is missing or no
+CUDA device is usable, calls raise RuntimeError.
+
+Names, argument meaning and error behaviour follow the reference bindings:
+`Problem(cost, alpha, beta, epsilon)`, `solve(problem, tol, max_iter, ell,
+basis, init, trace)`, `top_modes(problem, f, g, ell, tol, max_power_iters)`,
+`anneal(problem, epsilons, warm, ell, refresh_basis, tol, max_iter)`, the
+transforms and objective helpers. `PointProblem` is the on-the-fly cost variant
+(C_ij = cost_scale * ||x_i - y_j||^2 never stored) the north star adds.
+Invalid arguments raise ValueError (pybind11 maps std::invalid_argument to
+ValueError), EigensolverError carries best_residual.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+__version__ = "0.1.0"
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libsknr_b200.so")
+_lib = None
+
+SKNR_OK, SKNR_EINVAL, SKNR_EEIGEN, SKNR_ECUDA, SKNR_ENCCL, SKNR_ERUNTIME = 0, 1, 2, 3, 4, 5
+
+
+class EigensolverError(RuntimeError):
+    """top_modes did not reach its residual target (spectral.hpp:60-68)."""
+
+    def __init__(self, msg: str, best_residual: float):
+        super().__init__(msg)
+        self.best_residual = best_residual
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [
+        ("tol_omega", ctypes.c_double),
+        ("max_iter", ctypes.c_int64),
+        ("ell", ctypes.c_int64),
+        ("newton_enabled", ctypes.c_int32),
+        ("trace_enabled", ctypes.c_int32),
+        ("exact_marginals", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class _Record(ctypes.Structure):
+    _fields_ = [
+        ("index", ctypes.c_int64),
+        ("marginal_error", ctypes.c_double),
+        ("marginal_error_inf", ctypes.c_double),
+        ("semi_dual_value", ctypes.c_double),
+        ("newton_attempted", ctypes.c_int32),
+        ("newton_accepted", ctypes.c_int32),
+        ("wall_time_ms", ctypes.c_double),
+    ]
+
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+_P = ctypes.c_void_p
+
+# name -> argtypes (all return int status unless listed in _RET)
+_SIGS = {
+    "sknr_last_error": [],
+    "sknr_last_best_residual": [],
+    "sknr_version": [ctypes.c_char_p, ctypes.c_int],
+    "sknr_kernel_launch_count": [],
+    "sknr_problem_create_dense": [_D, _I64, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(_P)],
+    "sknr_problem_create_points": [_D, _D, _I64, _I64, _I64, ctypes.c_double, _D, _D,
+                                   ctypes.c_double, ctypes.POINTER(_P)],
+    "sknr_problem_set_epsilon": [_P, ctypes.c_double],
+    "sknr_problem_info": [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                          _D, ctypes.POINTER(ctypes.c_int)],
+    "sknr_problem_destroy": [_P],
+    "sknr_ctransform_of_f": [_P, _D, _D],
+    "sknr_ctransform_of_g": [_P, _D, _D],
+    "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
+    "sknr_coupling": [_P, _D, _D, _D],
+    "sknr_semi_dual_value": [_P, _D, _D],
+    "sknr_restricted_derivatives": [_P, _D, _D, _D, _I64, _D, _D],
+    "sknr_apply_sym_block": [_P, _D, _D, _D, _I64, _D],
+    "sknr_apply_sym_t_block": [_P, _D, _D, _D, _I64, _D],
+    "sknr_top_modes": [_P, _D, _D, _I64, ctypes.c_double, _I64, _D, _D, _D,
+                       ctypes.POINTER(_I64)],
+    "sknr_config_default": [ctypes.POINTER(_Config)],
+    "sknr_solve": [_P, ctypes.POINTER(_Config), _D, _I64, _D, _D, _D, _D, ctypes.POINTER(_I64),
+                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_Record), _I64,
+                   ctypes.POINTER(_I64)],
+    "sknr_anneal": [_P, _D, _I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Config), _D, _D,
+                    ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_Record),
+                    _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
+    "sknr_bench_pass": [_P, ctypes.c_int, _I64, ctypes.c_int, _D, _D],
+    "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _D,
+                              ctypes.POINTER(_I64)],
+    "sknr_comm_unique_id": [ctypes.c_char_p],
+    "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
+    "sknr_comm_destroy": [],
+    "sknr_problem_shard": [_P, _I64, _I64],
+}
+_RET = {
+    "sknr_last_error": ctypes.c_char_p,
+    "sknr_last_best_residual": ctypes.c_double,
+    "sknr_kernel_launch_count": ctypes.c_int64,
+    "sknr_config_default": None,
+}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libsknr_b200.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(
+            f"sknr_b200: native library {_LIB_PATH} is missing; run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+    handle = ctypes.CDLL(_LIB_PATH)
+    for name, args in _SIGS.items():
+        fn = getattr(handle, name)
+        fn.argtypes = args
+        fn.restype = _RET.get(name, ctypes.c_int)
+    _lib = handle
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == SKNR_OK:
+        return
+    msg = lib().sknr_last_error().decode()
+    if rc == SKNR_EINVAL:
+        raise ValueError(msg)
+    if rc == SKNR_EEIGEN:
+        raise EigensolverError(msg, lib().sknr_last_best_residual())
+    raise RuntimeError(msg)
+
+
+def _vec(x, name="vector") -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+    return a
+
+
+def _mat_f(x) -> np.ndarray:
+    """Column-major (Fortran) float64 copy, like Eigen::MatrixXd."""
+    return np.asfortranarray(np.asarray(x, dtype=np.float64))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_D)
+
+
+def version() -> str:
+    buf = ctypes.create_string_buffer(256)
+    _check(lib().sknr_version(buf, 256))
+    return buf.value.decode()
+
+
+def kernel_launch_count() -> int:
+    return int(lib().sknr_kernel_launch_count())
+
+
+# ---------------------------------------------------------------- problems
+class Problem:
+    """EotProblem (types.hpp:47-69) with a dense n x m cost, resident on the GPU."""
+
+    _kind = 0
+
+    def __init__(self, cost, alpha, beta, epsilon: float):
+        cost = _mat_f(cost)
+        if cost.ndim != 2:
+            raise ValueError("CostMatrix: need a 2-d matrix")
+        n, m = cost.shape
+        a, b = _vec(alpha), _vec(beta)
+        if a.size != n or b.size != m:
+            raise ValueError("EotProblem: measure sizes must match cost shape")
+        h = _P()
+        _check(lib().sknr_problem_create_dense(_ptr(cost), n, m, _ptr(a), _ptr(b), float(epsilon),
+                                               ctypes.byref(h)))
+        self._init_common(h, n, m, a, b, float(epsilon))
+        self._cost = cost
+
+    def _init_common(self, h, n, m, a, b, eps):
+        self._h = h
+        self._n, self._m = int(n), int(m)
+        self._alpha, self._beta = a, b
+        self._eps = eps
+
+    @property
+    def n(self) -> int:
+        return self._n
+
+    @property
+    def m(self) -> int:
+        return self._m
+
+    @property
+    def epsilon(self) -> float:
+        return self._eps
+
+    @property
+    def alpha(self) -> np.ndarray:
+        return self._alpha.copy()
+
+    @property
+    def beta(self) -> np.ndarray:
+        return self._beta.copy()
+
+    @property
+    def cost(self) -> np.ndarray:
+        return self._cost
+
+    def with_epsilon(self, epsilon: float) -> "Problem":
+        """Same instance at another regularisation (types.hpp:60-62)."""
+        return type(self)._clone(self, float(epsilon))
+
+    @classmethod
+    def _clone(cls, p: "Problem", eps: float):
+        if isinstance(p, PointProblem):
+            return PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale)
+        return Problem(p._cost, p._alpha, p._beta, eps)
+
+    def set_epsilon(self, epsilon: float) -> None:
+        """In-place epsilon change (no cost copy, unlike with_epsilon)."""
+        _check(lib().sknr_problem_set_epsilon(self._h, float(epsilon)))
+        self._eps = float(epsilon)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.sknr_problem_destroy(h)
+            self._h = None
+
+
+class PointProblem(Problem):
+    """On-the-fly squared-Euclidean cost C_ij = cost_scale * ||x_i - y_j||^2
+    (sq_euclidean_cost, generators.cpp:94-103) between point clouds x (n x d)
+    and y (m x d); the n x m cost is never stored for d <= 4."""
+
+    _kind = 1
+
+    def __init__(self, x, y, alpha, beta, epsilon: float, cost_scale: float = 1.0):
+        x, y = _mat_f(x), _mat_f(y)
+        if x.ndim == 1:
+            x = x.reshape(-1, 1, order="F")
+        if y.ndim == 1:
+            y = y.reshape(-1, 1, order="F")
+        if x.shape[1] != y.shape[1]:
+            raise ValueError("sq_euclidean_cost: dimension mismatch")
+        n, d = x.shape
+        m = y.shape[0]
+        a, b = _vec(alpha), _vec(beta)
+        if a.size != n or b.size != m:
+            raise ValueError("EotProblem: measure sizes must match cost shape")
+        h = _P()
+        _check(lib().sknr_problem_create_points(_ptr(x), _ptr(y), n, m, d, float(cost_scale), _ptr(a),
+                                                _ptr(b), float(epsilon), ctypes.byref(h)))
+        self._init_common(h, n, m, a, b, float(epsilon))
+        self._x, self._y, self._cost_scale = x, y, float(cost_scale)
+
+    @property
+    def cost(self) -> np.ndarray:
+        diff = self._x[:, None, :] - self._y[None, :, :]
+        return np.asfortranarray(self._cost_scale * np.einsum("ijk,ijk->ij", diff, diff))
+
+    @property
+    def d(self) -> int:
+        return self._x.shape[1]
+
+
+# ---------------------------------------------------------------- results
+@dataclass
+class SpectralBasis:
+    """SpectralBasis (spectral.hpp:48-56)."""
+
+    vectors: np.ndarray
+    vectors_sym: np.ndarray
+    rhos: np.ndarray
+    epsilon_built_at: float
+    sweeps: int = 0
+
+    @property
+    def ell(self) -> int:
+        return self.vectors.shape[1]
+
+    @property
+    def dim(self) -> int:
+        return self.vectors.shape[0]
+
+
+@dataclass
+class IterationRecord:
+    index: int
+    marginal_error: float
+    marginal_error_inf: float
+    semi_dual_value: float
+    newton_attempted: bool
+    newton_accepted: bool
+    wall_time_ms: float
+
+
+@dataclass
+class SolveResult:
+    f: np.ndarray
+    g: np.ndarray
+    converged: bool
+    iterations: int
+    trace: list = field(default_factory=list)
+    _problem: Optional[Problem] = None
+    _epsilon: Optional[float] = None
+
+    @property
+    def plan(self) -> np.ndarray:
+        """coupling_from at the returned potentials (solver.cpp:154), materialised on demand."""
+        p = self._problem
+        if self._epsilon is not None and self._epsilon != p.epsilon:
+            p = p.with_epsilon(self._epsilon)
+        return coupling(p, self.f, self.g)
+
+
+def _records(buf, count) -> list:
+    return [IterationRecord(int(r.index), r.marginal_error, r.marginal_error_inf, r.semi_dual_value,
+                            bool(r.newton_attempted), bool(r.newton_accepted), r.wall_time_ms)
+            for r in buf[:count]]
+
+
+# ---------------------------------------------------------------- core.hpp
+def log_sum_exp(values, log_weights) -> float:
+    """log sum_i exp(values_i + log_weights_i), max-shifted (core.cpp:9-22).
+    Host-side scalar helper of the reference API (not on the O(nm) path)."""
+    v, w = _vec(values), _vec(log_weights)
+    if v.size == 0 or w.size == 0:
+        raise ValueError("log_sum_exp: empty reduction")
+    if v.size != w.size:
+        raise ValueError("log_sum_exp: length mismatch")
+    shift = -np.inf
+    for i in range(v.size):
+        shift = max(shift, v[i] + w[i])
+    total = 0.0
+    for i in range(v.size):
+        total += np.exp(v[i] + w[i] - shift)
+    return float(shift + np.log(total))
+
+
+def _checked(v, size, what):
+    a = _vec(v)
+    if a.size != size:
+        raise ValueError(f"{what}: length mismatch")
+    if not np.all(np.isfinite(a)):
+        raise ValueError(f"{what}: entries must be finite")
+    return a
+
+
+def ctransform_of_f(problem: Problem, f) -> np.ndarray:
+    f = _checked(f, problem.n, "ctransform_of_f")
+    g = np.empty(problem.m)
+    _check(lib().sknr_ctransform_of_f(problem.handle, _ptr(f), _ptr(g)))
+    return g
+
+
+def ctransform_of_g(problem: Problem, g) -> np.ndarray:
+    g = _checked(g, problem.m, "ctransform_of_g")
+    f = np.empty(problem.n)
+    _check(lib().sknr_ctransform_of_g(problem.handle, _ptr(g), _ptr(f)))
+    return f
+
+
+def plan_marginals(problem: Problem, f, g):
+    """(row, col, gap_l2, gap_inf) of the plan induced by (f, g) (core.cpp:120-150)."""
+    f = _checked(f, problem.n, "plan_marginals(f)")
+    g = _checked(g, problem.m, "plan_marginals(g)")
+    row, col = np.empty(problem.n), np.empty(problem.m)
+    l2, inf = ctypes.c_double(), ctypes.c_double()
+    _check(lib().sknr_plan_marginals(problem.handle, _ptr(f), _ptr(g), _ptr(row), _ptr(col),
+                                     ctypes.byref(l2), ctypes.byref(inf)))
+    return row, col, l2.value, inf.value
+
+
+def coupling(problem: Problem, f, g) -> np.ndarray:
+    f = _checked(f, problem.n, "coupling_from(f)")
+    g = _checked(g, problem.m, "coupling_from(g)")
+    plan = np.empty((problem.n, problem.m), order="F")
+    _check(lib().sknr_coupling(problem.handle, _ptr(f), _ptr(g), _ptr(plan)))
+    return plan
+
+
+def marginal_error(problem: Problem, plan) -> float:
+    """||plan 1 - alpha||_2 + ||plan^T 1 - beta||_2 (core.cpp:105-112)."""
+    plan = np.asarray(plan, dtype=np.float64)
+    if plan.shape != (problem.n, problem.m):
+        raise ValueError("marginal_error: plan shape mismatch")
+    return float(np.linalg.norm(plan.sum(axis=1) - problem._alpha) +
+                 np.linalg.norm(plan.sum(axis=0) - problem._beta))
+
+
+def osc_norm(v) -> float:
+    v = _vec(v)
+    if v.size == 0:
+        raise ValueError("osc_norm: empty input")
+    return float(v.max() - v.min())
+
+
+# ---------------------------------------------------------------- objective.hpp
+def semi_dual_value(problem: Problem, f) -> float:
+    f = _checked(f, problem.n, "ctransform_of_f")
+    out = ctypes.c_double()
+    _check(lib().sknr_semi_dual_value(problem.handle, _ptr(f), ctypes.byref(out)))
+    return out.value
+
+
+def semi_dual_gradient(problem: Problem, f) -> np.ndarray:
+    """alpha - row marginal at (f, f^{C,eps}) (objective.cpp:47-51)."""
+    g = ctransform_of_f(problem, f)
+    row, _, _, _ = plan_marginals(problem, f, g)
+    return problem._alpha - row
+
+
+def restricted_derivatives(problem: Problem, f, basis: SpectralBasis, g=None):
+    """(grad, hess) of t -> Q(f + V t) at 0 (objective.cpp:110-148)."""
+    if basis.dim != problem.n:
+        raise ValueError("restricted_derivatives: basis dimension mismatch")
+    if basis.ell < 1:
+        raise ValueError("restricted_derivatives: empty basis")
+    f = _checked(f, problem.n, "restricted_derivatives(f)")
+    if g is None:
+        g = ctransform_of_f(problem, f)
+    g = _checked(g, problem.m, "restricted_derivatives(g)")
+    V = _mat_f(basis.vectors)
+    ell = V.shape[1]
+    grad = np.empty(ell)
+    hess = np.empty((ell, ell), order="F")
+    _check(lib().sknr_restricted_derivatives(problem.handle, _ptr(f), _ptr(g), _ptr(V), ell,
+                                             _ptr(grad), _ptr(hess)))
+    return grad, hess
+
+
+# ---------------------------------------------------------------- spectral.hpp
+def apply_sym_block(problem: Problem, f, g, v) -> np.ndarray:
+    f, g, v = _vec(f), _vec(g), _mat_f(v)
+    out = np.empty((problem.n, v.shape[1]), order="F")
+    _check(lib().sknr_apply_sym_block(problem.handle, _ptr(f), _ptr(g), _ptr(v), v.shape[1], _ptr(out)))
+    return out
+
+
+def apply_sym_t_block(problem: Problem, f, g, u) -> np.ndarray:
+    f, g, u = _vec(f), _vec(g), _mat_f(u)
+    out = np.empty((problem.m, u.shape[1]), order="F")
+    _check(lib().sknr_apply_sym_t_block(problem.handle, _ptr(f), _ptr(g), _ptr(u), u.shape[1],
+                                        _ptr(out)))
+    return out
+
+
+def top_modes(problem: Problem, f, g, ell: int, tol: float = 1e-8,
+              max_power_iters: int = -1) -> SpectralBasis:
+    f = _checked(f, problem.n, "SinkhornOperator(f)")
+    g = _checked(g, problem.m, "SinkhornOperator(g)")
+    ell = int(ell)
+    if ell < 1:
+        raise ValueError("top_modes: ell must be >= 1")
+    if ell >= problem.n:
+        raise ValueError("top_modes: ell must be < n")
+    vec = np.empty((problem.n, ell), order="F")
+    vsym = np.empty((problem.n, ell), order="F")
+    rhos = np.empty(ell)
+    sweeps = _I64()
+    _check(lib().sknr_top_modes(problem.handle, _ptr(f), _ptr(g), ell, float(tol), int(max_power_iters),
+                                _ptr(vec), _ptr(vsym), _ptr(rhos), ctypes.byref(sweeps)))
+    return SpectralBasis(vec, vsym, rhos, problem.epsilon, int(sweeps.value))
+
+
+# ---------------------------------------------------------------- solver.hpp
+def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False) -> _Config:
+    c = _Config()
+    lib().sknr_config_default(ctypes.byref(c))
+    c.tol_omega = float(tol)
+    c.max_iter = int(max_iter)
+    c.ell = int(ell)
+    c.trace_enabled = 1 if trace else 0
+    c.newton_enabled = 1 if newton else 0
+    c.exact_marginals = 1 if exact_marginals else 0
+    return c
+
+
+def solve(problem: Problem, tol: float = 1e-9, max_iter: int = 100000, ell: int = 0,
+          basis: Optional[SpectralBasis] = None, init=None, trace: bool = True) -> SolveResult:
+    """SK-NR(ell) (Alg. 1; solver.cpp:71-156)."""
+    cfg = _config(tol, max_iter, ell, trace)
+    V = None
+    bell = 0
+    if ell > 0:
+        if basis is None:
+            raise ValueError("solve: ell > 0 requires a basis")
+        if basis.ell != ell:
+            raise ValueError("solve: basis has wrong column count")
+        if basis.dim != problem.n:
+            raise ValueError("solve: basis dimension mismatch")
+        V = _mat_f(basis.vectors)
+        bell = ell
+    f0 = g0 = None
+    if init is not None:
+        f0, g0 = _vec(init[0]), _vec(init[1])
+        if f0.size != problem.n or g0.size != problem.m:
+            raise ValueError("solve: init potential sizes mismatch")
+    f = np.empty(problem.n)
+    g = np.empty(problem.m)
+    iters = _I64()
+    conv = ctypes.c_int()
+    cap = int(max_iter) if trace else 0
+    recs = (_Record * max(cap, 1))()
+    tlen = _I64()
+    _check(lib().sknr_solve(problem.handle, ctypes.byref(cfg), _ptr(V), bell, _ptr(f0), _ptr(g0),
+                            _ptr(f), _ptr(g), ctypes.byref(iters), ctypes.byref(conv), recs, cap,
+                            ctypes.byref(tlen)))
+    return SolveResult(f, g, bool(conv.value), int(iters.value), _records(recs, min(tlen.value, cap)),
+                       problem)
+
+
+def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", ell: int = 8,
+           refresh_basis: bool = False, tol: float = 1e-9, max_iter: int = 100000) -> list:
+    """Epsilon-annealing driver (solver.cpp:158-222)."""
+    modes = {"none": 0, "potentials": 1, "spectral": 2}
+    if warm not in modes:
+        raise ValueError("warm must be none|potentials|spectral")
+    eps = _vec(epsilons)
+    S = eps.size
+    if S == 0:
+        raise ValueError("anneal: empty schedule")
+    cfg = _config(tol, max_iter, ell, True)
+    n, m = problem.n, problem.m
+    F = np.empty(S * n)
+    G = np.empty(S * m)
+    iters = (_I64 * S)()
+    conv = (ctypes.c_int * S)()
+    cap = int(max_iter) * S
+    cap = min(cap, 2_000_000)
+    recs = (_Record * max(cap, 1))()
+    offs = (_I64 * S)()
+    tlen = _I64()
+    _check(lib().sknr_anneal(problem.handle, _ptr(eps), S, modes[warm], 1 if refresh_basis else 0,
+                             ctypes.byref(cfg), _ptr(F), _ptr(G), iters, conv, recs, cap, offs,
+                             ctypes.byref(tlen)))
+    out = []
+    for s in range(S):
+        lo = offs[s]
+        hi = offs[s + 1] if s + 1 < S else tlen.value
+        out.append(SolveResult(F[s * n:(s + 1) * n].copy(), G[s * m:(s + 1) * m].copy(), bool(conv[s]),
+                               int(iters[s]), _records(recs[lo:min(hi, cap)], hi - lo), problem,
+                               float(eps[s])))
+    return out
+
+
+# ---------------------------------------------------------------- measurement
+def bench_pass(problem: Problem, which: int, ell: int = 0, passes: int = 5):
+    ms, kms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().sknr_bench_pass(problem.handle, int(which), int(ell), int(passes), ctypes.byref(ms),
+                                 ctypes.byref(kms)))
+    return ms.value, kms.value
+
+
+def bench_iterations(problem: Problem, ell: int = 0, basis: Optional[SpectralBasis] = None,
+                     iters: int = 5):
+    cfg = _config(1e-9, 1 << 40, ell, False)
+    V = _mat_f(basis.vectors) if (basis is not None and ell > 0) else None
+    ms = ctypes.c_double()
+    kpi = _I64()
+    _check(lib().sknr_bench_iterations(problem.handle, ctypes.byref(cfg), _ptr(V), int(ell) if V is not None else 0,
+                                       int(iters), ctypes.byref(ms), ctypes.byref(kpi)))
+    return ms.value, int(kpi.value)
+
+
+__all__ = [
+    "EigensolverError", "IterationRecord", "PointProblem", "Problem", "SolveResult", "SpectralBasis",
+    "__version__", "anneal", "apply_sym_block", "apply_sym_t_block", "coupling", "ctransform_of_f",
+    "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
+    "plan_marginals", "restricted_derivatives", "semi_dual_gradient", "semi_dual_value", "solve",
+    "top_modes", "version",
+]

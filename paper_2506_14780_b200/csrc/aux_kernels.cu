@@ -1,0 +1,267 @@
+// aux_kernels.cu -- packing, finalize and Gram kernels (see aux_kernels.cuh).
+#include "aux_kernels.cuh"
+
+namespace sknr {
+
+namespace {
+
+constexpr double kInf = __builtin_huge_val();
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, T* sh, Op op) {
+    // fixed tree over AUX_NT threads: deterministic
+    const int tid = threadIdx.x;
+    sh[tid] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (tid < s) sh[tid] = op(sh[tid], sh[tid + s]);
+        __syncthreads();
+    }
+    const T r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+struct MaxOp {
+    __device__ double operator()(double a, double b) const { return fmax(a, b); }
+};
+struct MinOp {
+    __device__ double operator()(double a, double b) const { return fmin(a, b); }
+};
+
+// Returns true in exactly one block: the last one to finish (all partials visible).
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(counter, 1u);
+        is_last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ prep
+__global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    __shared__ double sh[AUX_NT];
+    double lmax = -kInf, lmin = kInf;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double e = 0.0;
+        if (a.lw) e = a.lw[i];
+        if (a.v) e += a.v[i] * a.inv_eps;
+        if (a.sq) e -= a.kc * a.sq[i];
+        a.pack[i * a.pk] = kL64 * e;
+        for (int c = 0; c < a.d; ++c) a.pack[i * a.pk + 1 + c] = a.sigma * a.coords[i + c * a.count];
+        for (int c = a.d + 1; c < a.pk; ++c) a.pack[i * a.pk + c] = 0.0;
+        if (a.ref) {
+            const double dv = a.v[i] - a.ref[i];
+            lmax = fmax(lmax, dv);
+            lmin = fmin(lmin, dv);
+        }
+    }
+    if (!a.ref) return;
+    const double bmax = block_reduce(lmax, sh, MaxOp());
+    const double bmin = block_reduce(lmin, sh, MinOp());
+    if (threadIdx.x == 0) {
+        a.part[2 * blockIdx.x] = bmax;
+        a.part[2 * blockIdx.x + 1] = bmin;
+    }
+    if (!last_block(&a.st->counters[a.dir])) return;
+    if (threadIdx.x == 0) {
+        double mx = -kInf, mn = kInf;
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            mx = fmax(mx, a.part[2 * b]);
+            mn = fmin(mn, a.part[2 * b + 1]);
+        }
+        a.st->dmax[a.dir] = mx;
+        a.st->dmin[a.dir] = mn;
+        const bool ok = a.st->ref_valid[a.dir] && (mx - mn) * a.inv_eps <= a.exact_spread &&
+                        isfinite(mx) && isfinite(mn);
+        a.st->need_exact[a.dir] = ok ? 0 : 1;
+        a.st->retry[a.dir] = 0;
+        a.st->counters[a.dir] = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    const bool bound = a.shift_mode == SHIFT_BOUND && !a.st->need_exact[a.dir];
+    const double dshift = bound ? a.st->dmax[a.dir] * a.inv_eps : 0.0;
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.count;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double e = 0.0;
+        if (a.lw) e = a.lw[o];
+        if (a.v) e += a.v[o] * a.inv_eps;
+        if (a.sq) e -= a.kc * a.sq[o];
+        double s = 0.0;
+        if (a.shift_mode == SHIFT_BOUND) {
+            s = bound ? a.Lref[o] + dshift : 0.0;
+            a.shift[o] = s;
+        }
+        a.pack[o * a.pk] = kL64 * (e - s);
+        for (int c = 0; c < a.d; ++c) a.pack[o * a.pk + 1 + c] = a.sigma * a.coords[o + c * a.count];
+        for (int c = a.d + 1; c < a.pk; ++c) a.pack[o * a.pk + c] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------ finalize
+// Exact shift: shift_o += max_u / L64, B_o recomputed from it.
+__global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.n_out;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double M = -kInf;
+        for (int64_t b = 0; b < a.nb; ++b) M = fmax(M, a.partial[b * a.n_out + o]);
+        const double s = a.shift[o] + M * kInvL64;
+        a.shift[o] = s;
+        double e = 0.0;
+        if (a.sq) e -= a.kc * a.sq[o];
+        a.pack[o * a.pk] = kL64 * (e - s);
+    }
+}
+
+// L_o = shift_o + log(sum_b partial[b][o]); pot_o = -eps L_o. A sum outside
+// [2^-900, 2^900] means the bound shift was too loose: request the exact path.
+__global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    bool bad = false;
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.n_out;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double S = 0.0;
+        for (int64_t b = 0; b < a.nb; ++b) S += a.partial[b * a.n_out + o];
+        const bool ok = S >= 0x1p-900 && S <= 0x1p900;
+        bad |= !ok;
+        const double L = a.shift[o] + log(S);
+        if (a.L) a.L[o] = L;
+        if (a.pot) a.pot[o] = -a.eps * L;
+    }
+    if (bad && !a.retry_phase && !a.st->need_exact[a.dir]) a.st->retry[a.dir] = 1;
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, int64_t nb,
+                                                         int64_t n_out, const double* scale,
+                                                         double* out, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < n_out;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double S = 0.0;
+        for (int64_t b = 0; b < nb; ++b) S += partial[b * n_out + o];
+        out[o] = scale ? scale[o] * S : S;
+    }
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_lse_commit(const double* in_vec, double* ref, int64_t count,
+                                                       int dir, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        ref[i] = in_vec[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->ref_valid[dir] = 1;
+        st->need_exact[dir] = 0;
+        st->retry[dir] = 0;
+    }
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial, int64_t nb, int kt,
+                                                           int k, int64_t n_out, const double* scale,
+                                                           double* out, int64_t ld, DevState* st,
+                                                           unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    const int64_t total = n_out * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t o = e % n_out;
+        const int64_t c = e / n_out;
+        double S = 0.0;
+        for (int64_t b = 0; b < nb; ++b) S += partial[(b * kt + c) * n_out + o];
+        out[o + c * ld] = scale ? scale[o] * S : S;
+    }
+}
+
+// W[i*kt + c] = rowscale_i * X[i + c*ldx] for c < k, 0 for k <= c < kt.
+__global__ void __launch_bounds__(AUX_NT) k_pack_w(const double* X, int64_t n, int64_t ldx, int k,
+                                                   int kt, const double* rowscale, double* W) {
+    const int64_t total = n * kt;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e / kt;
+        const int c = static_cast<int>(e % kt);
+        double v = 0.0;
+        if (c < k) v = X[i + c * ldx] * (rowscale ? rowscale[i] : 1.0);
+        W[e] = v;
+    }
+}
+
+// ------------------------------------------------------------------ Gram
+int gram_blocks(int64_t T) {
+    int64_t b = (T + 2047) / 2048;
+    if (b < 1) b = 1;
+    if (b > 148) b = 148;
+    return static_cast<int>(b);
+}
+
+// Each block owns a contiguous t-range; rows are staged 32 at a time in shared
+// memory (w folded into U); thread owns pairs p = tid + q*AUX_NT.
+__global__ void __launch_bounds__(AUX_NT) k_gram(GramArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int RB = 32;
+    constexpr int KMAXP = 64;
+    __shared__ double su[RB * KMAXP];
+    __shared__ double sv[RB * KMAXP];
+    const int ka = a.ka, kb = a.kb;
+    const int npairs = a.diag_only ? ka : ka * kb;
+    constexpr int QMAX = (KMAXP * KMAXP + AUX_NT - 1) / AUX_NT;
+    double acc[QMAX];
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) acc[q] = 0.0;
+    const int64_t per = (a.T + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = blockIdx.x * per;
+    const int64_t t1 = (t0 + per < a.T) ? t0 + per : a.T;
+    const double* V = a.V ? a.V : a.U;
+    const int64_t ldv = a.V ? a.ldv : a.ldu;
+    for (int64_t tb = t0; tb < t1; tb += RB) {
+        const int cnt = static_cast<int>((t1 - tb) < RB ? (t1 - tb) : RB);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt * ka; e += blockDim.x) {
+            const int r = e % cnt, c = e / cnt;
+            const double w = a.w ? a.w[tb + r] : 1.0;
+            su[r * KMAXP + c] = w * a.U[tb + r + c * a.ldu];
+        }
+        for (int e = threadIdx.x; e < cnt * kb; e += blockDim.x) {
+            const int r = e % cnt, c = e / cnt;
+            sv[r * KMAXP + c] = V[tb + r + c * ldv];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+            const int p = threadIdx.x + q * AUX_NT;
+            if (p >= npairs) break;
+            const int ia = a.diag_only ? p : p % ka;
+            const int ib = a.diag_only ? p : p / ka;
+            double s = acc[q];
+            for (int r = 0; r < cnt; ++r) s = fma(su[r * KMAXP + ia], sv[r * KMAXP + ib], s);
+            acc[q] = s;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+        const int p = threadIdx.x + q * AUX_NT;
+        if (p < npairs) a.part[static_cast<int64_t>(blockIdx.x) * npairs + p] = acc[q];
+    }
+    if (!last_block(a.counter)) return;
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        double s = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) s += a.part[static_cast<int64_t>(b) * npairs + p];
+        a.out[p] = a.out_scale * s;
+    }
+    if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+}  // namespace sknr

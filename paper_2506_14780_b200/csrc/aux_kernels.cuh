@@ -1,0 +1,106 @@
+// aux_kernels.cuh -- O(n+m) and O(n*ell^2) helper kernels around the tile passes.
+// Every reduction is deterministic: fixed per-block ranges, fixed in-block
+// trees, and a "last block" (ticket counter) that merges the block partials
+// in block order. No floating-point atomics.
+#pragma once
+#include "internal.h"
+
+namespace sknr {
+
+constexpr int AUX_NT = 256;
+
+// ------------------------------------------------------------------ packing
+// A_i = L64*(lw_i + v_i*inv_eps - kc*sq_i) and scaled coordinates; optional
+// statistics of (v - ref) for the bound shift (LSE passes only).
+struct PrepInArgs {
+    int64_t count = 0;
+    int d = 0, pk = 1;
+    const double* v = nullptr;    // potential on the input side (nullable)
+    const double* lw = nullptr;   // log weight term (nullable)
+    const double* sq = nullptr;   // squared norms (points; nullable)
+    const double* coords = nullptr;
+    double inv_eps = 1, kc = 0, sigma = 0;
+    double* pack = nullptr;
+    // LSE statistics
+    const double* ref = nullptr;  // previous input of this direction (nullable => no stats)
+    int dir = 0;
+    double* part = nullptr;       // 2*gridDim doubles
+    double exact_spread = 600.0;  // (max-min)(v-ref)/eps above which the exact path is forced
+    DevState* st = nullptr;
+    unsigned guard = 0;
+};
+
+__global__ void k_prep_in(PrepInArgs a);
+
+enum { SHIFT_NONE = 0, SHIFT_BOUND = 1 };
+
+struct PrepOutArgs {
+    int64_t count = 0;
+    int d = 0, pk = 1;
+    const double* v = nullptr;
+    const double* lw = nullptr;
+    const double* sq = nullptr;
+    const double* coords = nullptr;
+    double inv_eps = 1, kc = 0, sigma = 0;
+    int shift_mode = SHIFT_NONE;
+    const double* Lref = nullptr;  // bound shift: previous LSE of this direction
+    double* shift = nullptr;       // written (natural log units)
+    double* pack = nullptr;
+    int dir = 0;
+    DevState* st = nullptr;
+    unsigned guard = 0;
+};
+
+__global__ void k_prep_out(PrepOutArgs a);
+
+struct FinalizeArgs {
+    const double* partial = nullptr;
+    int64_t nb = 0, n_out = 0;
+    double* shift = nullptr;
+    double* pack = nullptr;   // max-finalize rewrites B in place
+    int pk = 1;
+    const double* sq = nullptr;
+    double kc = 0;
+    double eps = 1;
+    double* L = nullptr;
+    double* pot = nullptr;
+    int dir = 0;
+    int retry_phase = 0;
+    DevState* st = nullptr;
+    unsigned guard = 0;
+};
+
+__global__ void k_max_finalize(FinalizeArgs a);
+__global__ void k_lse_finalize(FinalizeArgs a);
+__global__ void k_sum_finalize(const double* partial, int64_t nb, int64_t n_out, const double* scale,
+                               double* out, DevState* st, unsigned guard);
+__global__ void k_lse_commit(const double* in_vec, double* ref, int64_t count, int dir, DevState* st,
+                             unsigned guard);
+__global__ void k_block_finalize(const double* partial, int64_t nb, int kt, int k, int64_t n_out,
+                                 const double* scale, double* out, int64_t ld, DevState* st,
+                                 unsigned guard);
+__global__ void k_pack_w(const double* X, int64_t n, int64_t ldx, int k, int kt, const double* rowscale,
+                         double* W);
+
+// ------------------------------------------------------------------ Gram
+// G[a + b*ka] = sum_t w_t U[t + a*ldu] V[t + b*ldv]  (V==nullptr -> V=U; w nullable)
+struct GramArgs {
+    int64_t T = 0;
+    int ka = 1, kb = 1;
+    const double* U = nullptr;
+    int64_t ldu = 0;
+    const double* V = nullptr;
+    int64_t ldv = 0;
+    const double* w = nullptr;
+    int diag_only = 0;
+    double* part = nullptr;     // gridDim * ka*kb
+    double* out = nullptr;
+    double out_scale = 1.0;
+    unsigned* counter = nullptr;
+    DevState* st = nullptr;
+    unsigned guard = 0;
+};
+__global__ void k_gram(GramArgs a);
+int gram_blocks(int64_t T);
+
+}  // namespace sknr

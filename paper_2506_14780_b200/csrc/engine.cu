@@ -1,0 +1,2133 @@
+// engine.cu -- host orchestration of SK-NR(ell) on one B200 (C++ host code +
+// the small kernels it sequences). The C ABI at the bottom is the drop-in
+// boundary declared in include/sknr_gpu.h.
+//
+// Device-resident solve loop (solver.cpp:104-151): one CUDA graph
+// per iteration, every kernel guarded by device flags (DevState) so that
+// convergence, Newton rejection and the exact-shift fallback never need a host
+// round trip; the host only polls the done flag between graph batches.
+//
+// Pass accounting per iteration (n*m cells each):
+//   SK     : row LSE (f) + column LSE (h = next g)                    = 2 passes
+//   SK-NR  : + row LSE at (f,h) for r + block pass S = V^T P~ (ell wide)
+//            + column LSE at the candidate                           = 4 + 1 block
+// The reference spends 3-6 passes (4 with its default trace); the column
+// marginal is taken from the fused transform: col_j - beta_j =
+// beta_j expm1((g_j - h_j)/eps) (SURVEY 3.2 "bitwise-safe reuse").
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <map>
+#include <tuple>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sknr_gpu.h"
+#include "aux_kernels.cuh"
+
+namespace sknr {
+
+// ============================================================ errors
+struct InvalidArgument : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct EigenFailure : std::runtime_error {
+    double best;
+    EigenFailure(const std::string& m, double b) : std::runtime_error(m), best(b) {}
+};
+struct RuntimeFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw CudaFailure(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                     \
+    } while (0)
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+
+template <typename... KArgs, typename... Args>
+static void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    count_launch();
+    kern<<<grid, block, 0, s>>>(args...);
+}
+
+static int grid_for(int64_t count, int threads = AUX_NT) {
+    int64_t g = (count + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > 148 * 8) g = 148 * 8;
+    return static_cast<int>(g);
+}
+
+// ============================================================ device buffers
+struct DBuf {
+    double* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t count) {
+        if (count <= n) return;
+        if (p) CK(cudaFree(p));
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+        CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(double)));
+        n = count;
+    }
+};
+
+// ============================================================ small kernels
+__global__ void k_fill(double* x, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_copy(double* dst, const double* src, int64_t n, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void k_state_init(DevState* st, long long max_iter, double tol) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    st->done = 0;
+    st->iter_active = 0;
+    st->conv = 0;
+    st->newton_ok = 0;
+    st->accept = 0;
+    st->attempted = 0;
+    st->iter = 0;
+    st->max_iter = max_iter;
+    st->tol = tol;
+    for (int d = 0; d < 2; ++d) {
+        st->need_exact[d] = 1;
+        st->retry[d] = 0;
+        st->ref_valid[d] = 0;
+    }
+    for (int c = 0; c < 32; ++c) st->counters[c] = 0u;
+}
+
+__global__ void k_invalidate_refs(DevState* st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        st->ref_valid[0] = st->ref_valid[1] = 0;
+        st->done = 0;
+        st->newton_ok = 0;
+    }
+}
+
+__global__ void k_iter_begin(DevState* st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (st->done) {
+        st->iter_active = 0;
+        return;
+    }
+    st->iter += 1;
+    st->iter_active = 1;
+    st->newton_ok = 0;
+    st->accept = 0;
+    st->attempted = 0;
+    st->t_iter0 = globaltimer_ns();
+}
+
+// f = f_pre - c ; rowres_i = a_i expm1(f_pre_i/eps + L_i) ; g += c
+__global__ void k_gauge_apply(double* f, const double* L, const double* a, int64_t n, double* g,
+                              int64_t m, double inv_eps, double* rowres, DevState* st) {
+    if (st->done) return;
+    const double c = st->c_gauge;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < n) {
+            const double fp = f[i];
+            rowres[i] = a[i] * expm1(fp * inv_eps + L[i]);
+            f[i] = fp - c;
+        } else {
+            g[i - n] += c;
+        }
+    }
+}
+
+// colres_j = b_j expm1((g_j - h_j)/eps)
+__global__ void k_colres(const double* g, const double* h, const double* b, int64_t m, double inv_eps,
+                         double* colres, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        colres[j] = b[j] * expm1((g[j] - h[j]) * inv_eps);
+}
+
+// gap from Gram sums: sums[0] = ||row-a||^2, sums[1] = ||col-b||^2 ; maxima via
+// a separate deterministic max kernel (k_absmax) into sums[2], sums[3].
+__global__ void k_absmax(const double* x, int64_t n, double* part, double* out, unsigned* counter,
+                         DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    __shared__ double sh[AUX_NT];
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        mx = fmax(mx, fabs(x[i]));
+    sh[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
+    double r = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) r = fmax(r, part[b]);
+    *out = r;
+    *counter = 0u;
+}
+
+// sums: [0]=|row-a|^2 [1]=|col-b|^2 [2]=max|row-a| [3]=max|col-b| [4]=a.f [5]=b.h
+__global__ void k_check(DevState* st, const double* sums, int newton) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (st->done) return;
+    st->gap_l2 = sqrt(sums[0]) + sqrt(sums[1]);
+    st->gap_inf = sums[2] + sums[3];
+    st->q0 = sums[4] + sums[5];
+    if (st->gap_l2 < st->tol) {
+        st->conv = 1;
+        st->done = 1;
+        return;
+    }
+    if (newton) {
+        st->newton_ok = 1;
+        st->attempted = 1;
+    }
+}
+
+// alpha - r = -a_i expm1(f_i/eps + L_i(h)) ; r = a - (alpha - r)
+__global__ void k_newton_r(const double* f, const double* L, const double* a, int64_t n, double inv_eps,
+                           double* am, double* r, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double d = -a[i] * expm1(f[i] * inv_eps + L[i]);
+        am[i] = d;
+        r[i] = a[i] - d;
+    }
+}
+
+// try_newton's ell x ell algebra on one CTA (solver.cpp:37-44, objective.cpp:138-140):
+// H = -(1/eps)(G1 - cross); H = (H+H^T)/2; LLT(-H) (fails iff a pivot <= 0, as
+// Eigen's llt_inplace::unblocked); delta = LLT.solve(grad).
+__global__ void k_newton_solve(const double* G1, const double* cross, const double* grad, int ell,
+                               double inv_eps, double* delta, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    extern __shared__ double sA[];  // ell*ell
+    __shared__ int fail;
+    __shared__ double piv;
+    const int tid = threadIdx.x;
+    if (tid == 0) fail = 0;
+    for (int e = tid; e < ell * ell; e += blockDim.x) {
+        const int r = e % ell, c = e / ell;
+        const double h_rc = -inv_eps * (G1[r + c * ell] - cross[r + c * ell]);
+        const double h_cr = -inv_eps * (G1[c + r * ell] - cross[c + r * ell]);
+        sA[e] = -(0.5 * (h_rc + h_cr));
+    }
+    __syncthreads();
+    for (int c = 0; c < ell; ++c) {
+        if (tid == 0) {
+            double x = sA[c + c * ell];
+            for (int t = 0; t < c; ++t) x -= sA[c + t * ell] * sA[c + t * ell];
+            if (!(x > 0.0)) fail = 1;
+            piv = sqrt(x);
+            sA[c + c * ell] = piv;
+        }
+        __syncthreads();
+        if (fail) break;
+        for (int r = c + 1 + tid; r < ell; r += blockDim.x) {
+            double v = sA[r + c * ell];
+            for (int t = 0; t < c; ++t) v -= sA[r + t * ell] * sA[c + t * ell];
+            sA[r + c * ell] = v / piv;
+        }
+        __syncthreads();
+    }
+    if (fail) {
+        if (tid == 0) st->newton_ok = 0;
+        return;
+    }
+    if (tid == 0) {
+        double y[64];
+        for (int r = 0; r < ell; ++r) {
+            double v = grad[r];
+            for (int t = 0; t < r; ++t) v -= sA[r + t * ell] * y[t];
+            y[r] = v / sA[r + r * ell];
+        }
+        for (int r = ell - 1; r >= 0; --r) {
+            double v = y[r];
+            for (int t = r + 1; t < ell; ++t) v -= sA[t + r * ell] * y[t];
+            y[r] = v / sA[r + r * ell];
+        }
+        for (int r = 0; r < ell; ++r) delta[r] = y[r];
+    }
+}
+
+// candidate = f + V delta (solver.cpp:45)
+__global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, const double* delta,
+                        double* out, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    __shared__ double sd[64];
+    if (threadIdx.x < ell) sd[threadIdx.x] = delta[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < ell; ++c) s += V[i + c * n] * sd[c];
+        out[i] = f[i] + s;
+    }
+}
+
+// q1 = a.f' + b.h' ; accept iff q1 > q0 (solver.cpp:46-47)
+__global__ void k_accept(DevState* st, const double* sums) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (st->done || !st->newton_ok) return;
+    st->q1 = sums[0] + sums[1];
+    st->accept = st->q1 > st->q0 ? 1 : 0;
+}
+
+// accepted: f <- candidate, next g <- h(candidate); otherwise next g <- h.
+__global__ void k_select(double* f, const double* fcand, int64_t n, double* gnext, const double* h,
+                         const double* hcand, int64_t m, DevState* st) {
+    if (st->done) return;
+    const bool acc = st->newton_ok && st->accept;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < n) {
+            if (acc) f[i] = fcand[i];
+        } else {
+            gnext[i - n] = acc ? hcand[i - n] : h[i - n];
+        }
+    }
+}
+
+__global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (!st->iter_active) return;
+    st->iter_active = 0;
+    const long long k = st->iter;
+    if (trace_enabled && k - 1 < cap) {
+        sknr_record r;
+        r.index = k;
+        r.marginal_error = st->gap_l2;
+        r.marginal_error_inf = st->gap_inf;
+        const bool acc = st->attempted && st->newton_ok && st->accept;
+        r.semi_dual_value = acc ? st->q1 : st->q0;
+        r.newton_attempted = st->attempted;
+        r.newton_accepted = acc ? 1 : 0;
+        r.wall_time_ms = static_cast<double>(globaltimer_ns() - st->t_iter0) * 1e-6;
+        trace[k - 1] = r;
+    }
+    if (k >= st->max_iter) st->done = 1;
+}
+
+// ---- top_modes helpers
+// Y[:,c] -= u0 * s_c
+__global__ void k_deflate(double* Y, int64_t n, int k, const double* u0, const double* s) {
+    const int64_t total = n * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % n;
+        const int c = static_cast<int>(e / n);
+        Y[e] -= u0[i] * s[c];
+    }
+}
+
+// out (n x l) = X (n x k) * W (k x l), W col-major
+__global__ void k_small_gemm(const double* X, int64_t n, int k, const double* W, int l, double* out) {
+    extern __shared__ double sW[];
+    for (int e = threadIdx.x; e < k * l; e += blockDim.x) sW[e] = W[e];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        for (int a = 0; a < l; ++a) {
+            double s = 0.0;
+            for (int r = 0; r < k; ++r) s += X[i + r * n] * sW[r + a * k];
+            out[i + a * n] = s;
+        }
+    }
+}
+
+// R = YW - theta_a XW
+__global__ void k_resid(const double* YW, const double* XW, const double* theta, int64_t n, int l,
+                        double* R) {
+    const int64_t total = n * l;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int a = static_cast<int>(e / n);
+        R[e] = YW[e] - theta[a] * XW[e];
+    }
+}
+
+__global__ void k_div_rows(const double* X, const double* s, int64_t n, int l, double* out) {
+    const int64_t total = n * l;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[e] = X[e] / s[e % n];
+}
+
+// SplitMix64 start block (spectral.cpp:138-142): draw t = c*n + i of the
+// stream seeded 0x73706563 is state seed + (t+1)*gamma -- computed in parallel.
+__global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long seed) {
+    const int64_t total = n * k;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        unsigned long long z = seed + static_cast<unsigned long long>(t + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+        const double u01 = static_cast<double>(z >> 11) * 0x1.0p-53;
+        X[t] = -1.0 + 2.0 * u01;
+    }
+}
+
+// ---- Householder QR with Eigen's conventions (makeHouseholder /
+// applyHouseholderOnTheLeft, HouseholderQR + householderQ()*Identity):
+// hh[4c..4c+3] = {tau, beta, 1/(c0-beta), zero_tail}
+__global__ void k_hh_norm(double* X, int64_t n, int c, double* part, double* hh, unsigned* counter) {
+    __shared__ double sh[AUX_NT];
+    double s = 0.0;
+    const double* col = X + static_cast<int64_t>(c) * n;
+    for (int64_t r = c + 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        s = fma(col[r], col[r], s);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+        __syncthreads();
+    }
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
+    double tail = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) tail += part[b];
+    const double c0 = col[c];
+    double tau, beta, zero;
+    if (tail <= 2.2250738585072014e-308) {
+        tau = 0.0;
+        beta = c0;
+        zero = 1.0;
+    } else {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        tau = (beta - c0) / beta;
+        zero = 0.0;
+    }
+    hh[4 * c] = tau;
+    hh[4 * c + 1] = beta;
+    hh[4 * c + 2] = c0 - beta;
+    hh[4 * c + 3] = zero;
+    X[c + static_cast<int64_t>(c) * n] = beta;
+    *counter = 0u;
+}
+
+// v_r = X[r,c]/(c0-beta) (written back); w_c2 = X[c,c2] + sum_{r>c} v_r X[r,c2]
+// for c2 in [c2lo, k) of matrix M (M==X for the factorisation, Q for forming Q).
+__global__ void k_hh_w(double* X, const double* M, int64_t n, int k, int c, int c2lo, int scale_v,
+                       const double* hh, double* part, double* w, unsigned* counter) {
+    constexpr int KM = 64;
+    __shared__ double sh[AUX_NT];
+    __shared__ double sw[KM];
+    const double denom = hh[4 * c + 2];
+    const bool zero = hh[4 * c + 3] != 0.0;
+    double acc[KM];
+    const int nw = k - c2lo;
+    for (int q = 0; q < nw; ++q) acc[q] = 0.0;
+    double* colc = X + static_cast<int64_t>(c) * n;
+    for (int64_t r = c + 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double v = colc[r];
+        if (scale_v) {
+            v = zero ? 0.0 : v / denom;
+            colc[r] = v;
+        }
+        for (int q = 0; q < nw; ++q) acc[q] = fma(v, M[r + static_cast<int64_t>(c2lo + q) * n], acc[q]);
+    }
+    for (int q = 0; q < nw; ++q) {
+        sh[threadIdx.x] = acc[q];
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) sw[q] = sh[0];
+        __syncthreads();
+    }
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < nw; ++q) part[static_cast<int64_t>(blockIdx.x) * KM + q] = sw[q];
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    for (int q = threadIdx.x; q < nw; q += blockDim.x) {
+        double s = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) s += part[static_cast<int64_t>(b) * KM + q];
+        w[q] = M[c + static_cast<int64_t>(c2lo + q) * n] + s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+// M[r,c2] -= tau w_c2 v_r for r >= c (v_c = 1), c2 in [c2lo, k)
+__global__ void k_hh_update(const double* X, double* M, int64_t n, int k, int c, int c2lo,
+                            const double* hh, const double* w) {
+    const double tau = hh[4 * c];
+    if (tau == 0.0) return;
+    const int nw = k - c2lo;
+    const int64_t rows = n - c;
+    const int64_t total = rows * nw;
+    const double* v = X + static_cast<int64_t>(c) * n;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = c + e % rows;
+        const int q = static_cast<int>(e / rows);
+        const double vr = (r == c) ? 1.0 : v[r];
+        M[r + static_cast<int64_t>(c2lo + q) * n] -= tau * w[q] * vr;
+    }
+}
+
+__global__ void k_eye(double* Q, int64_t n, int k) {
+    const int64_t total = n * k;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        Q[e] = (e % n == e / n) ? 1.0 : 0.0;
+}
+
+// plan_ij = a_i b_j exp((f_i + g_j - C_ij)/eps)  (coupling_from, core.cpp:84-103)
+__global__ void k_coupling(const double* C, const double* x, const double* y, int64_t n, int64_t m,
+                           int d, double kappa, const double* a, const double* b, const double* f,
+                           const double* g, double inv_eps, double* plan) {
+    const int64_t total = n * m;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        double c;
+        if (C) {
+            c = C[e];
+        } else {
+            double s = 0.0;
+            for (int q = 0; q < d; ++q) {
+                const double t = x[i + q * n] - y[j + q * m];
+                s += t * t;
+            }
+            c = kappa * s;
+        }
+        plan[e] = a[i] * b[j] * exp((f[i] + g[j] - c) * inv_eps);
+    }
+}
+
+// Stored cost built on device from points (direct difference, generators.cpp:101),
+// written in both layouts.
+__global__ void k_build_cost(const double* x, const double* y, int64_t n, int64_t m, int d,
+                             double kappa, double* C, double* CT) {
+    const int64_t total = n * m;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        double s = 0.0;
+        for (int q = 0; q < d; ++q) {
+            const double t = x[i + q * n] - y[j + q * m];
+            s += t * t;
+        }
+        const double c = kappa * s;
+        C[e] = c;
+        if (CT) CT[j + i * m] = c;
+    }
+}
+
+// transpose n x m col-major -> m x n col-major
+__global__ void k_transpose(const double* A, int64_t n, int64_t m, double* AT) {
+    __shared__ double tile[32][33];
+    for (int64_t bj = blockIdx.y * 32; bj < m; bj += static_cast<int64_t>(gridDim.y) * 32)
+        for (int64_t bi = blockIdx.x * 32; bi < n; bi += static_cast<int64_t>(gridDim.x) * 32) {
+            for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+                const int64_t i = bi + threadIdx.x, j = bj + r;
+                if (i < n && j < m) tile[r][threadIdx.x] = A[i + j * n];
+            }
+            __syncthreads();
+            for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+                const int64_t j = bj + threadIdx.x, i = bi + r;
+                if (i < n && j < m) AT[j + i * m] = tile[threadIdx.x][r];
+            }
+            __syncthreads();
+        }
+}
+
+// ============================================================ problem
+struct Side {
+    int64_t count = 0;
+    DBuf w, lw, sw, lsw, coords, sq;
+};
+
+struct Problem {
+    int kind = 0;  // 0 dense, 1 points
+    int64_t n = 0, m = 0, d = 0;
+    double eps = 1.0, kappa = 1.0;
+    int dim = 0;  // tile-kernel dimension: 0 stored cost, 1..4 points
+    Side src, tgt;
+    DBuf C, CT;
+    DevState* st = nullptr;
+    DevState* st_host = nullptr;  // pinned mirror for polling
+    cudaStream_t stream = nullptr;
+
+    // per-direction LSE state
+    DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
+    DBuf partial;
+    DBuf gram_part, sums, misc;
+    std::mutex mu;
+
+    ~Problem() {
+        if (stream) cudaStreamDestroy(stream);
+        if (st) cudaFree(st);
+        if (st_host) cudaFreeHost(st_host);
+    }
+
+    std::map<std::tuple<int, int, int, int64_t>, TilePlan> plans;
+
+    bool otf() const { return dim > 0; }  // on-the-fly cost (points, d <= 4)
+    double inv_eps() const { return 1.0 / eps; }
+    double kc() const { return otf() ? kappa / eps : 0.0; }
+    double sigma() const { return otf() ? std::sqrt(2.0 * kL64 * kappa / eps) : 0.0; }
+    int pk() const { return otf() ? (dim + 2) / 2 * 2 : 1; }
+    Side& in_side(int dir) { return dir == 0 ? src : tgt; }
+    Side& out_side(int dir) { return dir == 0 ? tgt : src; }
+    const double* cost_for(int dir) const { return dir == 0 ? CT.p : C.p; }
+    int64_t ldc_for(int dir) const { return dir == 0 ? m : n; }
+};
+
+static void upload(double* dst, const double* src, size_t count, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+static void download(double* dst, const double* src, size_t count, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
+static void check_device() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1)
+        throw CudaFailure("sknr_b200: no CUDA device available (this library has no CPU fallback)");
+}
+
+// DiscreteMeasure validation (types.cpp:7-18) with the reference's messages.
+static void validate_measure(const double* w, int64_t len) {
+    if (len == 0) throw InvalidArgument("DiscreteMeasure: empty weight vector");
+    double total = 0.0;
+    for (int64_t i = 0; i < len; ++i) {
+        if (!std::isfinite(w[i]) || w[i] <= 0.0)
+            throw InvalidArgument("DiscreteMeasure: weights must be strictly positive and finite");
+        total += w[i];
+    }
+    if (std::abs(total - 1.0) > 1e-12) throw InvalidArgument("DiscreteMeasure: weights must sum to 1");
+}
+
+static void setup_side(Side& s, const double* w, int64_t count, cudaStream_t stream) {
+    s.count = count;
+    std::vector<double> lw(count), sw(count), lsw(count);
+    for (int64_t i = 0; i < count; ++i) {
+        lw[i] = std::log(w[i]);  // scalar std::log like types.cpp:19-23
+        sw[i] = std::sqrt(w[i]);
+        lsw[i] = std::log(sw[i]);
+    }
+    s.w.ensure(count);
+    s.lw.ensure(count);
+    s.sw.ensure(count);
+    s.lsw.ensure(count);
+    upload(s.w.p, w, count, stream);
+    upload(s.lw.p, lw.data(), count, stream);
+    upload(s.sw.p, sw.data(), count, stream);
+    upload(s.lsw.p, lsw.data(), count, stream);
+    CK(cudaStreamSynchronize(stream));
+}
+
+static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const double* beta, double eps) {
+    if (n < 1 || m < 1) throw InvalidArgument("CostMatrix: need at least a 1x1 matrix");
+    validate_measure(alpha, n);
+    validate_measure(beta, m);
+    if (!(eps > 0.0) || !std::isfinite(eps)) throw InvalidArgument("EotProblem: epsilon must be positive");
+    check_device();
+    std::unique_ptr<Problem> p(new Problem());
+    p->n = n;
+    p->m = m;
+    p->eps = eps;
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&p->st, sizeof(DevState)));
+    CK(cudaMemset(p->st, 0, sizeof(DevState)));
+    CK(cudaMallocHost(&p->st_host, sizeof(DevState)));
+    setup_side(p->src, alpha, n, p->stream);
+    setup_side(p->tgt, beta, m, p->stream);
+    for (int dir = 0; dir < 2; ++dir) {
+        const int64_t nin = dir == 0 ? n : m, nout = dir == 0 ? m : n;
+        p->L[dir].ensure(nout);
+        p->ref[dir].ensure(nin);
+        p->shift[dir].ensure(nout);
+    }
+    p->stats.ensure(2 * 148 * 8);
+    p->gram_part.ensure(148 * 64 * 64 + 64);
+    p->sums.ensure(64);
+    return p.release();
+}
+
+static void finish_points(Problem* p, const double* x, const double* y, int64_t d, double cost_scale) {
+    const int64_t n = p->n, m = p->m;
+    p->kind = 1;
+    p->d = d;
+    p->kappa = cost_scale;
+    // Centre on the midpoint of the joint bounding box: ||x-y||^2 is translation
+    // invariant, and smaller norms keep the expanded form's rounding small.
+    std::vector<double> xc(x, x + n * d), yc(y, y + m * d), sx(n, 0.0), sy(m, 0.0);
+    for (int64_t q = 0; q < d; ++q) {
+        double lo = x[q * n], hi = x[q * n];
+        for (int64_t i = 0; i < n; ++i) {
+            lo = std::min(lo, x[i + q * n]);
+            hi = std::max(hi, x[i + q * n]);
+        }
+        for (int64_t j = 0; j < m; ++j) {
+            lo = std::min(lo, y[j + q * m]);
+            hi = std::max(hi, y[j + q * m]);
+        }
+        const double mid = 0.5 * (lo + hi);
+        for (int64_t i = 0; i < n; ++i) {
+            xc[i + q * n] -= mid;
+            sx[i] += xc[i + q * n] * xc[i + q * n];
+        }
+        for (int64_t j = 0; j < m; ++j) {
+            yc[j + q * m] -= mid;
+            sy[j] += yc[j + q * m] * yc[j + q * m];
+        }
+    }
+    p->src.coords.ensure(n * d);
+    p->tgt.coords.ensure(m * d);
+    p->src.sq.ensure(n);
+    p->tgt.sq.ensure(m);
+    upload(p->src.coords.p, xc.data(), n * d, p->stream);
+    upload(p->tgt.coords.p, yc.data(), m * d, p->stream);
+    upload(p->src.sq.p, sx.data(), n, p->stream);
+    upload(p->tgt.sq.p, sy.data(), m, p->stream);
+    if (d >= 1 && d <= 4) {
+        p->dim = static_cast<int>(d);
+    } else {
+        // No register-resident on-the-fly kernel for this dimension yet: the
+        // cost is materialised once on device (both layouts) and streamed.
+        p->dim = 0;
+        p->C.ensure(n * m);
+        p->CT.ensure(n * m);
+        count_launch();
+        k_build_cost<<<grid_for(n * m), AUX_NT, 0, p->stream>>>(p->src.coords.p, p->tgt.coords.p, n,
+                                                               m, static_cast<int>(d), cost_scale,
+                                                               p->C.p, p->CT.p);
+        CK(cudaGetLastError());
+    }
+    for (int dir = 0; dir < 2; ++dir) {
+        const int64_t nin = dir == 0 ? n : m, nout = dir == 0 ? m : n;
+        p->pack_in[dir].ensure(nin * p->pk());
+        p->pack_out[dir].ensure(nout * p->pk());
+    }
+    CK(cudaStreamSynchronize(p->stream));
+}
+
+static void finish_dense(Problem* p, const double* cost) {
+    const int64_t n = p->n, m = p->m;
+    for (int64_t e = 0; e < n * m; ++e)
+        if (!std::isfinite(cost[e])) throw InvalidArgument("CostMatrix: entries must be finite");
+    p->kind = 0;
+    p->dim = 0;
+    p->d = 0;
+    p->C.ensure(n * m);
+    p->CT.ensure(n * m);
+    upload(p->C.p, cost, n * m, p->stream);
+    count_launch();
+    k_transpose<<<dim3(std::min<int64_t>((n + 31) / 32, 256), std::min<int64_t>((m + 31) / 32, 256)),
+                  dim3(32, 8), 0, p->stream>>>(p->C.p, n, m, p->CT.p);
+    CK(cudaGetLastError());
+    for (int dir = 0; dir < 2; ++dir) {
+        const int64_t nin = dir == 0 ? n : m, nout = dir == 0 ? m : n;
+        p->pack_in[dir].ensure(nin);
+        p->pack_out[dir].ensure(nout);
+    }
+    CK(cudaStreamSynchronize(p->stream));
+}
+
+// ============================================================ passes
+static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_blocks = 0) {
+    const int64_t nout = dir == 0 ? P.m : P.n, nin = dir == 0 ? P.n : P.m;
+    const auto key = std::make_tuple(dir, mode, kt, max_in_blocks);
+    auto it = P.plans.find(key);
+    if (it != P.plans.end()) return it->second;
+    TilePlan tp = plan_tiles(P.dim, mode, kt, nout, nin, max_in_blocks);
+    if (!tp.fn) throw CudaFailure("sknr_b200: no tile kernel for this configuration");
+    P.plans[key] = tp;
+    const size_t need = static_cast<size_t>(tp.n_in_blocks) * nout * (mode == MODE_BLOCK ? kt : 1);
+    P.partial.ensure(need);
+    return tp;
+}
+
+static TileArgs tile_args(Problem& P, int dir, const TilePlan& tp, unsigned guard) {
+    TileArgs a;
+    a.n_out = dir == 0 ? P.m : P.n;
+    a.n_in = dir == 0 ? P.n : P.m;
+    a.out_pack = P.pack_out[dir].p;
+    a.in_pack = P.pack_in[dir].p;
+    a.C = P.cost_for(dir);
+    a.ldc = P.ldc_for(dir);
+    a.kappa = kL64 * P.inv_eps();
+    a.partial = P.partial.p;
+    a.st = P.st;
+    a.guard = guard;
+    (void)tp;
+    return a;
+}
+
+static unsigned exact_bit(int dir) { return dir == 0 ? G_EXACT0 : G_EXACT1; }
+static unsigned retry_bit(int dir) { return dir == 0 ? G_RETRY0 : G_RETRY1; }
+
+// (C,eps)-transform in direction dir (0: g <- f^{C,eps}, core.cpp:35-54; 1: f <-
+// g^{C,eps}, core.cpp:56-82). Writes L (natural-log LSE) into P.L[dir] and, if
+// pot != nullptr, the potential -eps*L.
+static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned guard) {
+    Side& in = P.in_side(dir);
+    Side& out = P.out_side(dir);
+    const int64_t nin = in.count, nout = out.count;
+    cudaStream_t s = P.stream;
+    const TilePlan tmax = plan_for(P, dir, MODE_MAX, 0);
+    const TilePlan tsum = plan_for(P, dir, MODE_SUM, 0);
+
+    PrepInArgs pi;
+    pi.count = nin;
+    pi.d = P.otf() ? static_cast<int>(P.d) : 0;
+    pi.pk = P.pk();
+    pi.v = in_vec;
+    pi.lw = in.lw.p;
+    pi.sq = P.otf() ? in.sq.p : nullptr;
+    pi.coords = P.otf() ? in.coords.p : nullptr;
+    pi.inv_eps = P.inv_eps();
+    pi.kc = P.kc();
+    pi.sigma = P.sigma();
+    pi.pack = P.pack_in[dir].p;
+    pi.ref = P.ref[dir].p;
+    pi.dir = dir;
+    pi.part = P.stats.p;
+    pi.st = P.st;
+    pi.guard = guard;
+    const int gin = std::min(grid_for(nin), 148 * 8);
+    count_launch();
+    k_prep_in<<<gin, AUX_NT, 0, s>>>(pi);
+
+    PrepOutArgs po;
+    po.count = nout;
+    po.d = pi.d;
+    po.pk = pi.pk;
+    po.sq = P.otf() ? out.sq.p : nullptr;
+    po.coords = P.otf() ? out.coords.p : nullptr;
+    po.inv_eps = P.inv_eps();
+    po.kc = P.kc();
+    po.sigma = P.sigma();
+    po.shift_mode = SHIFT_BOUND;
+    po.Lref = P.L[dir].p;
+    po.shift = P.shift[dir].p;
+    po.pack = P.pack_out[dir].p;
+    po.dir = dir;
+    po.st = P.st;
+    po.guard = guard;
+    count_launch();
+    k_prep_out<<<grid_for(nout), AUX_NT, 0, s>>>(po);
+
+    FinalizeArgs fa;
+    fa.partial = P.partial.p;
+    fa.n_out = nout;
+    fa.shift = P.shift[dir].p;
+    fa.pack = P.pack_out[dir].p;
+    fa.pk = P.pk();
+    fa.sq = P.otf() ? out.sq.p : nullptr;
+    fa.kc = P.kc();
+    fa.eps = P.eps;
+    fa.L = P.L[dir].p;
+    fa.pot = pot;
+    fa.dir = dir;
+    fa.st = P.st;
+
+    for (int phase = 0; phase < 2; ++phase) {
+        const unsigned gmax = guard | (phase == 0 ? exact_bit(dir) : retry_bit(dir));
+        const unsigned gsum = guard | (phase == 0 ? 0u : retry_bit(dir));
+        launch_tiles(tmax, tile_args(P, dir, tmax, gmax), s);
+        fa.nb = tmax.n_in_blocks;
+        fa.guard = gmax;
+        count_launch();
+        k_max_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
+        launch_tiles(tsum, tile_args(P, dir, tsum, gsum), s);
+        fa.nb = tsum.n_in_blocks;
+        fa.guard = gsum;
+        fa.retry_phase = phase;
+        count_launch();
+        k_lse_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
+    }
+    count_launch();
+    k_lse_commit<<<grid_for(nin), AUX_NT, 0, s>>>(in_vec, P.ref[dir].p, nin, dir, P.st, guard);
+    CK(cudaGetLastError());
+}
+
+// Unshifted pass family: out_o = oscale_o * sum_in exp(ia_in + ob_o - C/eps)
+// [ * W[in][c] for block mode ], with ia = lw_in + v_in/eps (log weights
+// chosen by the caller) and ob likewise.
+struct PassSpec {
+    int dir = 0;
+    const double* in_v = nullptr;
+    const double* in_lw = nullptr;
+    const double* out_v = nullptr;
+    const double* out_lw = nullptr;
+    const double* W = nullptr;  // packed [nin][kt] or nullptr (sum mode)
+    int k = 0, kt = 0;
+    const double* out_scale = nullptr;
+    double* out = nullptr;  // sum: [nout]; block: col-major nout x k (ld = nout)
+    unsigned guard = 0;
+};
+
+static void plan_pass(Problem& P, const PassSpec& ps) {
+    Side& in = P.in_side(ps.dir);
+    Side& out = P.out_side(ps.dir);
+    const int64_t nin = in.count, nout = out.count;
+    cudaStream_t s = P.stream;
+    const int mode = ps.W ? MODE_BLOCK : MODE_SUM;
+    const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, ps.W ? 8 : 0);
+
+    PrepInArgs pi;
+    pi.count = nin;
+    pi.d = P.otf() ? static_cast<int>(P.d) : 0;
+    pi.pk = P.pk();
+    pi.v = ps.in_v;
+    pi.lw = ps.in_lw;
+    pi.sq = P.otf() ? in.sq.p : nullptr;
+    pi.coords = P.otf() ? in.coords.p : nullptr;
+    pi.inv_eps = P.inv_eps();
+    pi.kc = P.kc();
+    pi.sigma = P.sigma();
+    pi.pack = P.pack_in[ps.dir].p;
+    pi.st = P.st;
+    pi.guard = ps.guard;
+    count_launch();
+    k_prep_in<<<grid_for(nin), AUX_NT, 0, s>>>(pi);
+
+    PrepOutArgs po;
+    po.count = nout;
+    po.d = pi.d;
+    po.pk = pi.pk;
+    po.v = ps.out_v;
+    po.lw = ps.out_lw;
+    po.sq = P.otf() ? out.sq.p : nullptr;
+    po.coords = P.otf() ? out.coords.p : nullptr;
+    po.inv_eps = P.inv_eps();
+    po.kc = P.kc();
+    po.sigma = P.sigma();
+    po.shift_mode = SHIFT_NONE;
+    po.pack = P.pack_out[ps.dir].p;
+    po.dir = ps.dir;
+    po.st = P.st;
+    po.guard = ps.guard;
+    count_launch();
+    k_prep_out<<<grid_for(nout), AUX_NT, 0, s>>>(po);
+
+    TileArgs ta = tile_args(P, ps.dir, tp, ps.guard);
+    ta.W = ps.W;
+    launch_tiles(tp, ta, s);
+    count_launch();
+    if (mode == MODE_SUM)
+        k_sum_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, nout, ps.out_scale,
+                                                         ps.out, P.st, ps.guard);
+    else
+        k_block_finalize<<<grid_for(nout * ps.k), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, ps.kt,
+                                                                  ps.k, nout, ps.out_scale, ps.out, nout,
+                                                                  P.st, ps.guard);
+    CK(cudaGetLastError());
+}
+
+// Gram / dot products: out[a + b*ka] = scale * sum_t w_t U[t,a] V[t,b]
+static unsigned g_gram_slot = 4;
+static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t ldu, const double* V,
+                 int64_t ldv, const double* w, double* out, unsigned guard, int diag_only = 0,
+                 double scale = 1.0) {
+    GramArgs ga;
+    ga.T = T;
+    ga.ka = ka;
+    ga.kb = kb;
+    ga.U = U;
+    ga.ldu = ldu;
+    ga.V = V;
+    ga.ldv = ldv;
+    ga.w = w;
+    ga.diag_only = diag_only;
+    ga.part = P.gram_part.p;
+    ga.out = out;
+    ga.out_scale = scale;
+    ga.counter = &P.st->counters[g_gram_slot];
+    ga.st = P.st;
+    ga.guard = guard;
+    count_launch();
+    k_gram<<<gram_blocks(T), AUX_NT, 0, P.stream>>>(ga);
+    CK(cudaGetLastError());
+}
+
+
+// ============================================================ top_modes
+// Symmetric Jacobi eigensolver for the k x k Rayleigh-Ritz matrix (stands in
+// for Eigen::SelfAdjointEigenSolver, spectral.cpp:156): ascending values.
+static void host_sym_eig(const std::vector<double>& Ain, int k, std::vector<double>& evals,
+                         std::vector<double>& evecs) {
+    std::vector<double> A(Ain), Q(static_cast<size_t>(k) * k, 0.0);
+    for (int i = 0; i < k; ++i) Q[i + i * k] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (int c = 0; c < k; ++c)
+            for (int r = 0; r < k; ++r) (r == c ? diag : off) += A[r + c * k] * A[r + c * k];
+        if (off <= 1e-36 * diag || off == 0.0) break;
+        for (int p = 0; p < k - 1; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                const double apq = A[p + q * k];
+                if (apq == 0.0) continue;
+                const double app = A[p + p * k], aqq = A[q + q * k];
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t =
+                    (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+                const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+                for (int r = 0; r < k; ++r) {
+                    const double arp = A[r + p * k], arq = A[r + q * k];
+                    A[r + p * k] = c * arp - s * arq;
+                    A[r + q * k] = s * arp + c * arq;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double apr = A[p + r * k], aqr = A[q + r * k];
+                    A[p + r * k] = c * apr - s * aqr;
+                    A[q + r * k] = s * apr + c * aqr;
+                }
+                for (int r = 0; r < k; ++r) {
+                    const double qrp = Q[r + p * k], qrq = Q[r + q * k];
+                    Q[r + p * k] = c * qrp - s * qrq;
+                    Q[r + q * k] = s * qrp + c * qrq;
+                }
+            }
+    }
+    std::vector<int> order(k);
+    for (int i = 0; i < k; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int u, int v) { return A[u + u * k] < A[v + v * k]; });
+    evals.assign(k, 0.0);
+    evecs.assign(static_cast<size_t>(k) * k, 0.0);
+    for (int c = 0; c < k; ++c) {
+        evals[c] = A[order[c] + order[c] * k];
+        for (int r = 0; r < k; ++r) evecs[r + c * k] = Q[r + order[c] * k];
+    }
+}
+
+struct QrWork {
+    DBuf hh, w, part, Q;
+};
+
+// Thin Householder Q of X (n x k) in place (spectral.cpp:116-117 conventions).
+static void device_householder_q(Problem& P, double* X, int64_t n, int k, QrWork& qw) {
+    cudaStream_t s = P.stream;
+    qw.hh.ensure(4 * 64);
+    qw.w.ensure(64);
+    qw.part.ensure(148 * 64);
+    qw.Q.ensure(static_cast<size_t>(n) * k);
+    unsigned* ctr = &P.st->counters[8];
+    const int kk = static_cast<int>(std::min<int64_t>(k, n));
+    const int gb = std::max(1, std::min(148, static_cast<int>((n + 4095) / 4096)));
+    for (int c = 0; c < kk; ++c) {
+        count_launch();
+        k_hh_norm<<<gb, AUX_NT, 0, s>>>(X, n, c, qw.part.p, qw.hh.p, ctr);
+        count_launch();
+        k_hh_w<<<gb, AUX_NT, 0, s>>>(X, X, n, k, c, c + 1, 1, qw.hh.p, qw.part.p, qw.w.p, ctr);
+        if (c + 1 < k) {
+            count_launch();
+            k_hh_update<<<grid_for((n - c) * (k - c - 1)), AUX_NT, 0, s>>>(X, X, n, k, c, c + 1, qw.hh.p,
+                                                                          qw.w.p);
+        }
+    }
+    count_launch();
+    k_eye<<<grid_for(n * k), AUX_NT, 0, s>>>(qw.Q.p, n, k);
+    for (int c = kk - 1; c >= 0; --c) {
+        count_launch();
+        k_hh_w<<<gb, AUX_NT, 0, s>>>(X, qw.Q.p, n, k, c, c, 0, qw.hh.p, qw.part.p, qw.w.p, ctr);
+        count_launch();
+        k_hh_update<<<grid_for((n - c) * (k - c)), AUX_NT, 0, s>>>(X, qw.Q.p, n, k, c, c, qw.hh.p,
+                                                                   qw.w.p);
+    }
+    CK(cudaMemcpyAsync(X, qw.Q.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, s));
+    CK(cudaGetLastError());
+}
+
+// orthonormalize_deflated (spectral.cpp:113-121)
+static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const double* u0,
+                                 QrWork& qw) {
+    double* s = P.misc.p;  // k dots
+    for (int round = 0; round < 3; ++round) {
+        gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
+        count_launch();
+        k_deflate<<<grid_for(n * k), AUX_NT, 0, P.stream>>>(X, n, k, u0, s);
+        device_householder_q(P, X, n, k, qw);
+        gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
+        std::vector<double> hs(k);
+        download(hs.data(), s, k, P.stream);
+        CK(cudaStreamSynchronize(P.stream));
+        double worst = 0.0;
+        for (int c = 0; c < k; ++c) worst = std::max(worst, std::abs(hs[c]));
+        if (worst < 1e-13) break;
+    }
+}
+
+struct Basis {
+    std::vector<double> vectors, vectors_sym, rhos;
+    int64_t sweeps = 0;
+};
+
+// top_modes (spectral.cpp:125-193) on device; f, g are device vectors.
+static Basis top_modes_device(Problem& P, const double* f, const double* g, int64_t ell, double tol,
+                              int64_t max_power_iters) {
+    const int64_t n = P.n, m = P.m;
+    if (ell < 1) throw InvalidArgument("top_modes: ell must be >= 1");
+    if (ell >= n) throw InvalidArgument("top_modes: ell must be < n");
+    if (max_power_iters < 0) max_power_iters = 500 * ell;
+    const int block = static_cast<int>(std::min<int64_t>(ell + 5, n - 1));
+    if (block > 64) throw InvalidArgument("top_modes: ell + 5 > 64 is not supported by sknr_b200");
+    const int kt = block_kt_for(block);
+    cudaStream_t s = P.stream;
+    DBuf X, Y, Z, W, XW, YW, R, Wd, th;
+    X.ensure(n * block);
+    Y.ensure(n * block);
+    Z.ensure(m * block);
+    W.ensure(std::max(n, m) * kt);
+    XW.ensure(n * ell);
+    YW.ensure(n * ell);
+    R.ensure(n * ell);
+    Wd.ensure(block * ell);
+    th.ensure(ell);
+    P.misc.ensure(256);
+    QrWork qw;
+    count_launch();
+    k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull);
+    device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
+
+    DBuf T;
+    T.ensure(block * block);
+    std::vector<double> hT(block * block), ts(block * block), evals, evecs, hres(ell);
+    double best = std::numeric_limits<double>::infinity();
+    bool ok = false;
+    Basis out;
+    std::vector<double> theta(ell), w(block * ell);
+    for (int64_t sweep = 0; sweep < max_power_iters; ++sweep) {
+        out.sweeps = sweep + 1;
+        // Z = R~^T X : z_j = sqrt(b_j) sum_i sqrt(a_i) e^{(f_i+g_j-C_ij)/eps} X_i
+        count_launch();
+        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(X.p, n, n, block, kt, nullptr, W.p);
+        PassSpec zt;
+        zt.dir = 0;
+        zt.in_v = f;
+        zt.in_lw = P.src.lsw.p;
+        zt.out_v = g;
+        zt.out_lw = nullptr;
+        zt.W = W.p;
+        zt.k = block;
+        zt.kt = kt;
+        zt.out_scale = P.tgt.sw.p;
+        zt.out = Z.p;
+        plan_pass(P, zt);
+        // Y = R~ Z : y_i = sum_j sqrt(a_i) e^{..} sqrt(b_j) z_j
+        count_launch();
+        k_pack_w<<<grid_for(m * kt), AUX_NT, 0, s>>>(Z.p, m, m, block, kt, P.tgt.sw.p, W.p);
+        PassSpec yr;
+        yr.dir = 1;
+        yr.in_v = g;
+        yr.in_lw = nullptr;
+        yr.out_v = f;
+        yr.out_lw = P.src.lsw.p;
+        yr.W = W.p;
+        yr.k = block;
+        yr.kt = kt;
+        yr.out = Y.p;
+        plan_pass(P, yr);
+        // Y -= sqrt(a) (sqrt(a)^T Y)
+        gram(P, n, block, 1, Y.p, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
+        count_launch();
+        k_deflate<<<grid_for(n * block), AUX_NT, 0, s>>>(Y.p, n, block, P.src.sw.p, P.misc.p);
+        // Rayleigh-Ritz
+        gram(P, n, block, block, X.p, n, Y.p, n, nullptr, T.p, 0);
+        download(hT.data(), T.p, block * block, s);
+        CK(cudaStreamSynchronize(s));
+        for (int a = 0; a < block; ++a)
+            for (int b = 0; b < block; ++b)
+                ts[a + b * block] = 0.5 * (hT[a + b * block] + hT[b + a * block]);
+        host_sym_eig(ts, block, evals, evecs);
+        for (int a = 0; a < ell; ++a) {
+            for (int r = 0; r < block; ++r) w[r + a * block] = evecs[r + (block - 1 - a) * block];
+            theta[a] = evals[block - 1 - a];
+        }
+        upload(Wd.p, w.data(), block * ell, s);
+        upload(th.p, theta.data(), ell, s);
+        count_launch();
+        k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * ell, s>>>(X.p, n, block, Wd.p,
+                                                                              static_cast<int>(ell), XW.p);
+        count_launch();
+        k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * ell, s>>>(Y.p, n, block, Wd.p,
+                                                                              static_cast<int>(ell), YW.p);
+        count_launch();
+        k_resid<<<grid_for(n * ell), AUX_NT, 0, s>>>(YW.p, XW.p, th.p, n, static_cast<int>(ell), R.p);
+        gram(P, n, static_cast<int>(ell), static_cast<int>(ell), R.p, n, R.p, n, nullptr, P.misc.p, 0, 1);
+        download(hres.data(), P.misc.p, ell, s);
+        CK(cudaStreamSynchronize(s));
+        double max_res = 0.0;
+        for (int a = 0; a < ell; ++a) max_res = std::max(max_res, std::sqrt(hres[a]));
+        best = std::min(best, max_res);
+        if (max_res <= tol) {
+            ok = true;
+            break;
+        }
+        CK(cudaMemcpyAsync(X.p, Y.p, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
+        device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
+    }
+    if (!ok)
+        throw EigenFailure(
+            "top_modes: no convergence within max_power_iters, best residual " + std::to_string(best),
+            best);
+    // vectors_sym = orth(XW); rhos = sqrt(max(theta,0)); vectors = vectors_sym ./ sqrt(alpha)
+    device_orth_deflated(P, XW.p, n, static_cast<int>(ell), P.src.sw.p, qw);
+    count_launch();
+    k_div_rows<<<grid_for(n * ell), AUX_NT, 0, s>>>(XW.p, P.src.sw.p, n, static_cast<int>(ell), R.p);
+    out.vectors_sym.resize(n * ell);
+    out.vectors.resize(n * ell);
+    download(out.vectors_sym.data(), XW.p, n * ell, s);
+    download(out.vectors.data(), R.p, n * ell, s);
+    CK(cudaStreamSynchronize(s));
+    out.rhos.resize(ell);
+    for (int a = 0; a < ell; ++a) out.rhos[a] = std::sqrt(std::max(theta[a], 0.0));
+    return out;
+}
+
+// ============================================================ solve
+struct SolveState {
+    DBuf f, g, gnext, h, fcand, hcand, rowres, colres, am, r, Lr, V, Wv, S, delta, G;
+    DBuf trace_raw;  // sknr_record array (as doubles)
+};
+
+struct SolveOut {
+    std::vector<double> f, g;
+    int64_t iterations = 0;
+    bool converged = false;
+    std::vector<sknr_record> trace;
+};
+
+// Enqueue one SK-NR(ell) iteration (solver.cpp:104-151).
+static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace_enabled,
+                              int64_t trace_cap) {
+    const int64_t n = P.n, m = P.m;
+    cudaStream_t s = P.stream;
+    const bool newton = ell > 0;
+    count_launch();
+    k_iter_begin<<<1, 32, 0, s>>>(P.st);
+    // sk_sweep: g = f^{C,eps} (computed at the end of the previous iteration), f = g^{C,eps}
+    count_launch();
+    k_copy<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.gnext.p, m, P.st, G_DONE);
+    lse(P, 1, S.g.p, S.f.p, G_DONE);
+    // gauge (solver.cpp:108-112)
+    gram(P, n, 1, 1, S.f.p, n, P.src.w.p, n, nullptr, &P.st->c_gauge, G_DONE);
+    count_launch();
+    k_gauge_apply<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, S.g.p, m,
+                                                     P.inv_eps(), S.rowres.p, P.st);
+    // h = f^{C,eps}: the column marginal and the next sweep's g
+    lse(P, 0, S.f.p, S.h.p, G_DONE);
+    count_launch();
+    k_colres<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.h.p, P.tgt.w.p, m, P.inv_eps(), S.colres.p, P.st,
+                                            G_DONE);
+    double* sums = P.sums.p;
+    gram(P, n, 1, 1, S.rowres.p, n, nullptr, 0, nullptr, sums + 0, G_DONE);
+    gram(P, m, 1, 1, S.colres.p, m, nullptr, 0, nullptr, sums + 1, G_DONE);
+    count_launch();
+    k_absmax<<<gram_blocks(n), AUX_NT, 0, s>>>(S.rowres.p, n, P.gram_part.p, sums + 2,
+                                               &P.st->counters[5], P.st, G_DONE);
+    count_launch();
+    k_absmax<<<gram_blocks(m), AUX_NT, 0, s>>>(S.colres.p, m, P.gram_part.p, sums + 3,
+                                               &P.st->counters[5], P.st, G_DONE);
+    gram(P, n, 1, 1, P.src.w.p, n, S.f.p, n, nullptr, sums + 4, G_DONE);
+    gram(P, m, 1, 1, P.tgt.w.p, m, S.h.p, m, nullptr, sums + 5, G_DONE);
+    count_launch();
+    k_check<<<1, 32, 0, s>>>(P.st, sums, newton ? 1 : 0);
+    if (newton) {
+        const unsigned gn = G_DONE | G_NEWTON;
+        const int l = static_cast<int>(ell);
+        // r = P~ beta at (f, h): alpha - r = -a expm1(f/eps + L_row(h))
+        lse(P, 1, S.h.p, nullptr, gn);
+        count_launch();
+        k_newton_r<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, P.inv_eps(), S.am.p,
+                                                  S.r.p, P.st, gn);
+        // S = V^T P~ (m x ell), P~_ij = a_i e^{(f_i + h_j - C_ij)/eps}
+        PassSpec sp;
+        sp.dir = 0;
+        sp.in_v = S.f.p;
+        sp.in_lw = P.src.lw.p;
+        sp.out_v = S.h.p;
+        sp.W = S.Wv.p;
+        sp.k = l;
+        sp.kt = block_kt_for(l);
+        sp.out = S.S.p;
+        sp.guard = gn;
+        plan_pass(P, sp);
+        double* G1 = S.G.p;
+        double* cross = G1 + l * l;
+        double* grad = cross + l * l;
+        gram(P, n, l, l, S.V.p, n, S.V.p, n, S.r.p, G1, gn);
+        gram(P, m, l, l, S.S.p, m, S.S.p, m, P.tgt.w.p, cross, gn);
+        gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
+        count_launch();
+        k_newton_solve<<<1, 64, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
+                                                            P.st, gn);
+        count_launch();
+        k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
+        lse(P, 0, S.fcand.p, S.hcand.p, gn);
+        gram(P, n, 1, 1, P.src.w.p, n, S.fcand.p, n, nullptr, sums + 6, gn);
+        gram(P, m, 1, 1, P.tgt.w.p, m, S.hcand.p, m, nullptr, sums + 7, gn);
+        count_launch();
+        k_accept<<<1, 32, 0, s>>>(P.st, sums + 6);
+        count_launch();
+        k_select<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, S.fcand.p, n, S.gnext.p, S.h.p, S.hcand.p, m,
+                                                    P.st);
+    } else {
+        count_launch();
+        k_copy<<<grid_for(m), AUX_NT, 0, s>>>(S.gnext.p, S.h.p, m, P.st, G_DONE);
+    }
+    count_launch();
+    k_record<<<1, 32, 0, s>>>(P.st, reinterpret_cast<sknr_record*>(S.trace_raw.p), trace_cap,
+                              trace_enabled ? 1 : 0);
+    CK(cudaGetLastError());
+}
+
+static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* basis_host,
+                          const double* init_f, int64_t max_iter, double tol, int64_t trace_cap) {
+    const int64_t n = P.n, m = P.m;
+    cudaStream_t s = P.stream;
+    S.f.ensure(n);
+    S.g.ensure(m);
+    S.gnext.ensure(m);
+    S.h.ensure(m);
+    S.fcand.ensure(n);
+    S.hcand.ensure(m);
+    S.rowres.ensure(n);
+    S.colres.ensure(m);
+    S.am.ensure(n);
+    S.r.ensure(n);
+    S.delta.ensure(64);
+    S.G.ensure(3 * 64 * 64);
+    S.trace_raw.ensure(std::max<int64_t>(trace_cap, 1) * (sizeof(sknr_record) / sizeof(double)));
+    P.misc.ensure(256);
+    if (ell > 0) {
+        const int kt = block_kt_for(static_cast<int>(ell));
+        S.V.ensure(n * ell);
+        S.Wv.ensure(n * kt);
+        S.S.ensure(m * ell);
+        upload(S.V.p, basis_host, n * ell, s);
+        count_launch();
+        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,
+                                                     S.Wv.p);
+        // pre-size the block-pass partials outside graph capture
+        plan_for(P, 0, MODE_BLOCK, kt, 8);
+    }
+    plan_for(P, 0, MODE_SUM, 0);
+    plan_for(P, 1, MODE_SUM, 0);
+    plan_for(P, 0, MODE_MAX, 0);
+    plan_for(P, 1, MODE_MAX, 0);
+    if (init_f)
+        upload(S.f.p, init_f, n, s);
+    else {
+        count_launch();
+        k_fill<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, n, 0.0);
+    }
+    count_launch();
+    k_state_init<<<1, 32, 0, s>>>(P.st, max_iter, tol);
+    // first sweep's g = f0^{C,eps} (exact shift: no reference state yet)
+    lse(P, 0, S.f.p, S.gnext.p, G_NONE);
+    CK(cudaGetLastError());
+}
+
+static bool poll_done(Problem& P) {
+    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
+    CK(cudaStreamSynchronize(P.stream));
+    return P.st_host->done != 0;
+}
+
+static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell, const double* basis,
+                          const double* init_f, bool trace_enabled, int64_t trace_cap_hint,
+                          int64_t forced_iters = -1) {
+    if (!(tol > 0.0) && forced_iters < 0) throw InvalidArgument("solve: tol_omega must be positive");
+    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
+    if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
+    const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, std::max<int64_t>(trace_cap_hint, 1)) : 1;
+    SolveState S;
+    prepare_solve(P, S, ell, basis, init_f, max_iter, tol, trace_cap);
+    cudaStream_t s = P.stream;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    enqueue_iteration(P, S, ell, trace_enabled, trace_cap);
+    CK(cudaStreamEndCapture(s, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    int64_t batch = 1;
+    int64_t launched = 0;
+    while (true) {
+        for (int64_t b = 0; b < batch; ++b) {
+            CK(cudaGraphLaunch(exec, s));
+            ++launched;
+        }
+        if (poll_done(P)) break;
+        if (launched >= max_iter + 2) break;
+        batch = std::min<int64_t>(batch * 2, 64);
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    SolveOut out;
+    out.f.resize(P.n);
+    out.g.resize(P.m);
+    download(out.f.data(), S.f.p, P.n, s);
+    download(out.g.data(), S.g.p, P.m, s);
+    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out.iterations = P.st_host->iter;
+    out.converged = P.st_host->conv != 0;
+    if (trace_enabled) {
+        const int64_t len = std::min<int64_t>(out.iterations, trace_cap);
+        out.trace.resize(len);
+        CK(cudaMemcpyAsync(out.trace.data(), S.trace_raw.p, sizeof(sknr_record) * len,
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return out;
+}
+
+}  // namespace sknr
+
+// ============================================================ C ABI
+using namespace sknr;
+
+struct sknr_problem_s {
+    std::unique_ptr<Problem> p;
+};
+
+static thread_local std::string g_err;
+static thread_local double g_best_residual = 0.0;
+
+#define SKNR_API_BEGIN try {
+#define SKNR_API_END                        \
+    return SKNR_OK;                         \
+    }                                       \
+    catch (const InvalidArgument& e) {      \
+        g_err = e.what();                   \
+        return SKNR_EINVAL;                 \
+    }                                       \
+    catch (const EigenFailure& e) {         \
+        g_err = e.what();                   \
+        g_best_residual = e.best;           \
+        return SKNR_EEIGEN;                 \
+    }                                       \
+    catch (const CudaFailure& e) {          \
+        g_err = e.what();                   \
+        return SKNR_ECUDA;                  \
+    }                                       \
+    catch (const RuntimeFailure& e) {       \
+        g_err = e.what();                   \
+        return SKNR_ERUNTIME;               \
+    }                                       \
+    catch (const std::exception& e) {       \
+        g_err = e.what();                   \
+        return SKNR_EINTERNAL;              \
+    }
+
+static Problem& get(sknr_problem h) {
+    if (!h || !h->p) throw InvalidArgument("sknr: null problem handle");
+    return *h->p;
+}
+
+static void check_finite_vec(const double* v, int64_t len, const char* what) {
+    if (!v) throw InvalidArgument(std::string(what) + ": null pointer");
+    for (int64_t i = 0; i < len; ++i)
+        if (!std::isfinite(v[i])) throw InvalidArgument(std::string(what) + ": entries must be finite");
+}
+
+extern "C" {
+
+const char* sknr_last_error(void) { return g_err.c_str(); }
+double sknr_last_best_residual(void) { return g_best_residual; }
+int64_t sknr_kernel_launch_count(void) { return launch_count(); }
+
+int sknr_version(char* buf, int cap) {
+    SKNR_API_BEGIN
+    std::string v = "sknr_b200 0.1.0 sm_100a";
+    int dev = 0, count = 0;
+    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
+        cudaDeviceProp prop;
+        cudaGetDevice(&dev);
+        if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+            v += std::string(" (") + prop.name + ", " + std::to_string(prop.multiProcessorCount) + " SMs)";
+    } else {
+        v += " (no CUDA device)";
+    }
+    if (buf && cap > 0) {
+        std::strncpy(buf, v.c_str(), cap - 1);
+        buf[cap - 1] = 0;
+    }
+    SKNR_API_END
+}
+
+void sknr_config_default(sknr_config* c) {
+    c->tol_omega = 1e-9;
+    c->max_iter = 100000;
+    c->ell = 0;
+    c->newton_enabled = 1;
+    c->trace_enabled = 1;
+    c->exact_marginals = 0;
+    c->reserved = 0;
+}
+
+int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const double* alpha,
+                              const double* beta, double epsilon, sknr_problem* out) {
+    SKNR_API_BEGIN
+    *out = nullptr;
+    std::unique_ptr<Problem> p(new_problem(n, m, alpha, beta, epsilon));
+    finish_dense(p.get(), cost);
+    *out = new sknr_problem_s{std::move(p)};
+    SKNR_API_END
+}
+
+int sknr_problem_create_points(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                               double cost_scale, const double* alpha, const double* beta, double epsilon,
+                               sknr_problem* out) {
+    SKNR_API_BEGIN
+    *out = nullptr;
+    if (d < 1) throw InvalidArgument("sq_euclidean_cost: dimension must be >= 1");
+    check_finite_vec(x, n * d, "PointCloud(x)");
+    check_finite_vec(y, m * d, "PointCloud(y)");
+    if (!(cost_scale > 0.0) || !std::isfinite(cost_scale))
+        throw InvalidArgument("sq_euclidean_cost: cost_scale must be positive");
+    std::unique_ptr<Problem> p(new_problem(n, m, alpha, beta, epsilon));
+    finish_points(p.get(), x, y, d, cost_scale);
+    *out = new sknr_problem_s{std::move(p)};
+    SKNR_API_END
+}
+
+int sknr_problem_set_epsilon(sknr_problem h, double epsilon) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    if (!(epsilon > 0.0) || !std::isfinite(epsilon)) throw InvalidArgument("EotProblem: epsilon must be positive");
+    P.eps = epsilon;
+    count_launch();
+    k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_problem_info(sknr_problem h, int64_t* n, int64_t* m, int64_t* d, double* epsilon, int* kind) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    if (n) *n = P.n;
+    if (m) *m = P.m;
+    if (d) *d = P.d;
+    if (epsilon) *epsilon = P.eps;
+    if (kind) *kind = P.kind;
+    SKNR_API_END
+}
+
+int sknr_problem_destroy(sknr_problem h) {
+    SKNR_API_BEGIN
+    delete h;
+    SKNR_API_END
+}
+
+static void reset_for_primitive(Problem& P) {
+    count_launch();
+    k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
+}
+
+int sknr_ctransform_of_f(sknr_problem h, const double* f, double* g) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(f, P.n, "ctransform_of_f");
+    DBuf df, dg;
+    df.ensure(P.n);
+    dg.ensure(P.m);
+    upload(df.p, f, P.n, P.stream);
+    reset_for_primitive(P);
+    plan_for(P, 0, MODE_SUM, 0);
+    plan_for(P, 0, MODE_MAX, 0);
+    lse(P, 0, df.p, dg.p, G_NONE);
+    download(g, dg.p, P.m, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_ctransform_of_g(sknr_problem h, const double* g, double* f) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(g, P.m, "ctransform_of_g");
+    DBuf df, dg;
+    df.ensure(P.n);
+    dg.ensure(P.m);
+    upload(dg.p, g, P.m, P.stream);
+    reset_for_primitive(P);
+    lse(P, 1, dg.p, df.p, G_NONE);
+    download(f, df.p, P.n, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double* row, double* col,
+                        double* gap_l2, double* gap_inf) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(f, P.n, "plan_marginals(f)");
+    check_finite_vec(g, P.m, "plan_marginals(g)");
+    DBuf df, dg, dr, dc;
+    df.ensure(P.n);
+    dg.ensure(P.m);
+    dr.ensure(P.n);
+    dc.ensure(P.m);
+    upload(df.p, f, P.n, P.stream);
+    upload(dg.p, g, P.m, P.stream);
+    // row_i = sum_j a_i b_j e^{..}: dir 1 (out i), column sums: dir 0 (out j)
+    PassSpec pr;
+    pr.dir = 1;
+    pr.in_v = dg.p;
+    pr.in_lw = P.tgt.lw.p;
+    pr.out_v = df.p;
+    pr.out_lw = P.src.lw.p;
+    pr.out = dr.p;
+    plan_pass(P, pr);
+    PassSpec pc;
+    pc.dir = 0;
+    pc.in_v = df.p;
+    pc.in_lw = P.src.lw.p;
+    pc.out_v = dg.p;
+    pc.out_lw = P.tgt.lw.p;
+    pc.out = dc.p;
+    plan_pass(P, pc);
+    std::vector<double> hr(P.n), hc(P.m), ha(P.n), hb(P.m);
+    download(hr.data(), dr.p, P.n, P.stream);
+    download(hc.data(), dc.p, P.m, P.stream);
+    download(ha.data(), P.src.w.p, P.n, P.stream);
+    download(hb.data(), P.tgt.w.p, P.m, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    double sr = 0, sc = 0, mr = 0, mc = 0;
+    for (int64_t i = 0; i < P.n; ++i) {
+        const double d = hr[i] - ha[i];
+        sr += d * d;
+        mr = std::max(mr, std::abs(d));
+    }
+    for (int64_t j = 0; j < P.m; ++j) {
+        const double d = hc[j] - hb[j];
+        sc += d * d;
+        mc = std::max(mc, std::abs(d));
+    }
+    if (row) std::memcpy(row, hr.data(), sizeof(double) * P.n);
+    if (col) std::memcpy(col, hc.data(), sizeof(double) * P.m);
+    if (gap_l2) *gap_l2 = std::sqrt(sr) + std::sqrt(sc);
+    if (gap_inf) *gap_inf = mr + mc;
+    SKNR_API_END
+}
+
+int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(f, P.n, "coupling_from(f)");
+    check_finite_vec(g, P.m, "coupling_from(g)");
+    DBuf df, dg, dp, x, y;
+    df.ensure(P.n);
+    dg.ensure(P.m);
+    dp.ensure(P.n * P.m);
+    upload(df.p, f, P.n, P.stream);
+    upload(dg.p, g, P.m, P.stream);
+    count_launch();
+    k_coupling<<<grid_for(P.n * P.m), AUX_NT, 0, P.stream>>>(
+        P.kind == 0 || P.C.p ? P.C.p : nullptr, P.src.coords.p, P.tgt.coords.p, P.n, P.m,
+        static_cast<int>(P.d), P.kappa, P.src.w.p, P.tgt.w.p, df.p, dg.p, P.inv_eps(), dp.p);
+    download(plan, dp.p, P.n * P.m, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_semi_dual_value(sknr_problem h, const double* f, double* value) {
+    SKNR_API_BEGIN
+    std::vector<double> g(get(h).m);
+    int rc = sknr_ctransform_of_f(h, f, g.data());
+    if (rc != SKNR_OK) return rc;
+    Problem& P = get(h);
+    std::vector<double> a(P.n), b(P.m);
+    download(a.data(), P.src.w.p, P.n, P.stream);
+    download(b.data(), P.tgt.w.p, P.m, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    double s1 = 0, s2 = 0;
+    for (int64_t i = 0; i < P.n; ++i) s1 += a[i] * f[i];
+    for (int64_t j = 0; j < P.m; ++j) s2 += b[j] * g[j];
+    *value = s1 + s2;
+    SKNR_API_END
+}
+
+int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g, const double* vectors,
+                                int64_t ell, double* grad, double* hess) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (ell < 1) throw InvalidArgument("restricted_derivatives: empty basis");
+    if (ell > 64) throw InvalidArgument("restricted_derivatives: ell > 64 is not supported by sknr_b200");
+    check_finite_vec(f, P.n, "restricted_derivatives(f)");
+    check_finite_vec(g, P.m, "restricted_derivatives(g)");
+    const int64_t n = P.n, m = P.m;
+    const int l = static_cast<int>(ell), kt = block_kt_for(l);
+    DBuf df, dg, V, Wv, Sm, am, r, G;
+    df.ensure(n);
+    dg.ensure(m);
+    V.ensure(n * ell);
+    Wv.ensure(n * kt);
+    Sm.ensure(m * ell);
+    am.ensure(n);
+    r.ensure(n);
+    G.ensure(3 * 64 * 64);
+    upload(df.p, f, n, P.stream);
+    upload(dg.p, g, m, P.stream);
+    upload(V.p, vectors, n * ell, P.stream);
+    count_launch();
+    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(V.p, n, n, l, kt, nullptr, Wv.p);
+    // r_i = a_i sum_j b_j e^{(f_i+g_j-C_ij)/eps} (objective.cpp:127-128) as a plan-sum pass
+    PassSpec pr;
+    pr.dir = 1;
+    pr.in_v = dg.p;
+    pr.in_lw = P.tgt.lw.p;
+    pr.out_v = df.p;
+    pr.out_lw = P.src.lw.p;
+    pr.out = r.p;
+    plan_pass(P, pr);
+    PassSpec sp;
+    sp.dir = 0;
+    sp.in_v = df.p;
+    sp.in_lw = P.src.lw.p;
+    sp.out_v = dg.p;
+    sp.W = Wv.p;
+    sp.k = l;
+    sp.kt = kt;
+    sp.out = Sm.p;
+    plan_pass(P, sp);
+    // am = a - r
+    std::vector<double> hr(n), ha(n);
+    download(hr.data(), r.p, n, P.stream);
+    download(ha.data(), P.src.w.p, n, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    for (int64_t i = 0; i < n; ++i) ha[i] -= hr[i];
+    upload(am.p, ha.data(), n, P.stream);
+    double* G1 = G.p;
+    double* cross = G1 + l * l;
+    double* gr = cross + l * l;
+    gram(P, n, l, l, V.p, n, V.p, n, r.p, G1, 0);
+    gram(P, m, l, l, Sm.p, m, Sm.p, m, P.tgt.w.p, cross, 0);
+    gram(P, n, l, 1, V.p, n, am.p, n, nullptr, gr, 0);
+    std::vector<double> hG1(l * l), hC(l * l);
+    download(hG1.data(), G1, l * l, P.stream);
+    download(hC.data(), cross, l * l, P.stream);
+    download(grad, gr, l, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    std::vector<double> H(l * l);
+    for (int a = 0; a < l; ++a)
+        for (int b = 0; b < l; ++b) H[a + b * l] = (-1.0 / P.eps) * (hG1[a + b * l] - hC[a + b * l]);
+    for (int a = 0; a < l; ++a)
+        for (int b = 0; b < l; ++b) hess[a + b * l] = 0.5 * (H[a + b * l] + H[b + a * l]);
+    SKNR_API_END
+}
+
+int sknr_apply_sym_t_block(sknr_problem h, const double* f, const double* g, const double* u, int64_t k,
+                           double* out) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (k < 1 || k > 64) throw InvalidArgument("apply_sym_t_block: 1 <= k <= 64 required");
+    const int64_t n = P.n, m = P.m;
+    const int kt = block_kt_for(static_cast<int>(k));
+    DBuf df, dg, U, W, O;
+    df.ensure(n);
+    dg.ensure(m);
+    U.ensure(n * k);
+    W.ensure(n * kt);
+    O.ensure(m * k);
+    upload(df.p, f, n, P.stream);
+    upload(dg.p, g, m, P.stream);
+    upload(U.p, u, n * k, P.stream);
+    count_launch();
+    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(U.p, n, n, static_cast<int>(k), kt, nullptr, W.p);
+    PassSpec zt;
+    zt.dir = 0;
+    zt.in_v = df.p;
+    zt.in_lw = P.src.lsw.p;
+    zt.out_v = dg.p;
+    zt.W = W.p;
+    zt.k = static_cast<int>(k);
+    zt.kt = kt;
+    zt.out_scale = P.tgt.sw.p;
+    zt.out = O.p;
+    plan_pass(P, zt);
+    download(out, O.p, m * k, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const double* v, int64_t k,
+                         double* out) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (k < 1 || k > 64) throw InvalidArgument("apply_sym_block: 1 <= k <= 64 required");
+    const int64_t n = P.n, m = P.m;
+    const int kt = block_kt_for(static_cast<int>(k));
+    DBuf df, dg, Vv, W, O;
+    df.ensure(n);
+    dg.ensure(m);
+    Vv.ensure(m * k);
+    W.ensure(m * kt);
+    O.ensure(n * k);
+    upload(df.p, f, n, P.stream);
+    upload(dg.p, g, m, P.stream);
+    upload(Vv.p, v, m * k, P.stream);
+    count_launch();
+    k_pack_w<<<grid_for(m * kt), AUX_NT, 0, P.stream>>>(Vv.p, m, m, static_cast<int>(k), kt, P.tgt.sw.p,
+                                                        W.p);
+    PassSpec yr;
+    yr.dir = 1;
+    yr.in_v = dg.p;
+    yr.out_v = df.p;
+    yr.out_lw = P.src.lsw.p;
+    yr.W = W.p;
+    yr.k = static_cast<int>(k);
+    yr.kt = kt;
+    yr.out = O.p;
+    plan_pass(P, yr);
+    download(out, O.p, n * k, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
+                   int64_t max_power_iters, double* vectors, double* vectors_sym, double* rhos,
+                   int64_t* sweeps) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(f, P.n, "SinkhornOperator(f)");
+    check_finite_vec(g, P.m, "SinkhornOperator(g)");
+    DBuf df, dg;
+    df.ensure(P.n);
+    dg.ensure(P.m);
+    upload(df.p, f, P.n, P.stream);
+    upload(dg.p, g, P.m, P.stream);
+    Basis b = top_modes_device(P, df.p, dg.p, ell, tol, max_power_iters);
+    std::memcpy(vectors, b.vectors.data(), sizeof(double) * P.n * ell);
+    std::memcpy(vectors_sym, b.vectors_sym.data(), sizeof(double) * P.n * ell);
+    std::memcpy(rhos, b.rhos.data(), sizeof(double) * ell);
+    if (sweeps) *sweeps = b.sweeps;
+    SKNR_API_END
+}
+
+static void validate_config(const sknr_config* cfg, const double* basis, int64_t basis_ell, int64_t n) {
+    if (!(cfg->tol_omega > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
+    if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
+    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
+    if (use_newton) {
+        if (basis == nullptr) throw InvalidArgument("solve: ell > 0 requires a basis");
+        if (basis_ell != cfg->ell) throw InvalidArgument("solve: basis has wrong column count");
+    }
+    (void)n;
+}
+
+int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int64_t basis_ell,
+               const double* init_f, const double* init_g, double* f_out, double* g_out,
+               int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
+               int64_t* trace_len) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    validate_config(cfg, basis, basis_ell, P.n);
+    if ((init_f == nullptr) != (init_g == nullptr))
+        throw InvalidArgument("solve: init potential sizes mismatch");
+    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
+    const int64_t ell = use_newton ? cfg->ell : 0;
+    SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
+                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1));
+    std::memcpy(f_out, o.f.data(), sizeof(double) * P.n);
+    std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
+    if (iterations) *iterations = o.iterations;
+    if (converged) *converged = o.converged ? 1 : 0;
+    const int64_t len = static_cast<int64_t>(o.trace.size());
+    if (trace_len) *trace_len = len;
+    if (trace)
+        for (int64_t t = 0; t < len && t < trace_cap; ++t) trace[t] = o.trace[t];
+    SKNR_API_END
+}
+
+int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm_mode, int refresh_basis,
+                const sknr_config* cfg, double* f_out, double* g_out, int64_t* iterations, int* converged,
+                sknr_record* trace, int64_t trace_cap, int64_t* trace_offsets, int64_t* trace_len) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (stages < 1) throw InvalidArgument("anneal: empty schedule");
+    for (int64_t s = 1; s < stages; ++s)
+        if (!(epsilons[s] < epsilons[s - 1]))
+            throw InvalidArgument("anneal: epsilons must be strictly decreasing");
+    if (!(cfg->tol_omega > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
+    if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
+    const double eps0 = P.eps;
+    const int64_t n = P.n, m = P.m;
+    int64_t tl = 0;
+    Basis basis;
+    bool have_basis = false;
+    std::vector<double> prev_f, prev_g;
+    auto set_eps = [&](double e) {
+        P.eps = e;
+        count_launch();
+        k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
+    };
+    try {
+        for (int64_t s = 0; s < stages; ++s) {
+            int64_t ell = 0;
+            const double* bptr = nullptr;
+            if (s > 0 && warm_mode == 2 && cfg->ell > 0) {
+                if (!have_basis || refresh_basis) {
+                    set_eps(epsilons[s - 1]);
+                    DBuf df, dg;
+                    df.ensure(n);
+                    dg.ensure(m);
+                    upload(df.p, prev_f.data(), n, P.stream);
+                    upload(dg.p, prev_g.data(), m, P.stream);
+                    try {
+                        basis = top_modes_device(P, df.p, dg.p, cfg->ell, 1e-8, -1);
+                    } catch (const EigenFailure& e) {
+                        throw EigenFailure("anneal stage " + std::to_string(s) + ": " + e.what(), e.best);
+                    }
+                    have_basis = true;
+                }
+                ell = cfg->newton_enabled ? cfg->ell : 0;
+                bptr = basis.vectors.data();
+            }
+            set_eps(epsilons[s]);
+            const double* init = (s > 0 && warm_mode != 0) ? prev_f.data() : nullptr;
+            SolveOut o;
+            try {
+                o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, bptr, init, cfg->trace_enabled != 0,
+                              cfg->max_iter);
+            } catch (const InvalidArgument& e) {
+                throw RuntimeFailure("anneal stage " + std::to_string(s) + ": " + e.what());
+            }
+            std::memcpy(f_out + s * n, o.f.data(), sizeof(double) * n);
+            std::memcpy(g_out + s * m, o.g.data(), sizeof(double) * m);
+            iterations[s] = o.iterations;
+            converged[s] = o.converged ? 1 : 0;
+            trace_offsets[s] = tl;
+            for (size_t t = 0; t < o.trace.size(); ++t, ++tl)
+                if (trace && tl < trace_cap) trace[tl] = o.trace[t];
+            prev_f = std::move(o.f);
+            prev_g = std::move(o.g);
+        }
+    } catch (...) {
+        set_eps(eps0);
+        throw;
+    }
+    if (trace_len) *trace_len = tl;
+    set_eps(eps0);
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* ms_per_pass,
+                    double* kernel_ms_per_pass) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    const int64_t n = P.n, m = P.m;
+    cudaStream_t s = P.stream;
+    DBuf f, g, V, Wv, Sm;
+    f.ensure(n);
+    g.ensure(m);
+    count_launch();
+    k_fill<<<grid_for(n), AUX_NT, 0, s>>>(f.p, n, 0.0);
+    count_launch();
+    k_state_init<<<1, 32, 0, s>>>(P.st, 1, 1.0);
+    plan_for(P, 0, MODE_SUM, 0);
+    plan_for(P, 1, MODE_SUM, 0);
+    plan_for(P, 0, MODE_MAX, 0);
+    plan_for(P, 1, MODE_MAX, 0);
+    lse(P, 0, f.p, g.p, G_NONE);  // realistic g; seeds the reference state
+    lse(P, 1, g.p, f.p, G_NONE);
+    const int l = static_cast<int>(std::max<int64_t>(ell, 1));
+    const int kt = block_kt_for(l);
+    if (which >= 3) {
+        V.ensure(n * l);
+        Wv.ensure(std::max(n, m) * kt);
+        Sm.ensure(std::max(n, m) * l);
+        count_launch();
+        k_fill<<<grid_for(n * l), AUX_NT, 0, s>>>(V.p, n * l, 1.0 / std::sqrt(static_cast<double>(n)));
+        count_launch();
+        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(V.p, n, n, l, kt, nullptr, Wv.p);
+        plan_for(P, 0, MODE_BLOCK, kt, 8);
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    TilePlan tsum = plan_for(P, 0, MODE_SUM, 0);
+    auto one = [&]() {
+        switch (which) {
+            case 0: lse(P, 0, f.p, g.p, G_NONE); break;
+            case 1: lse(P, 1, g.p, f.p, G_NONE); break;
+            case 2: launch_tiles(tsum, tile_args(P, 0, tsum, G_NONE), s); break;
+            default: {
+                PassSpec sp;
+                sp.dir = 0;
+                sp.in_v = f.p;
+                sp.in_lw = P.src.lw.p;
+                sp.out_v = g.p;
+                sp.W = Wv.p;
+                sp.k = l;
+                sp.kt = kt;
+                sp.out = Sm.p;
+                plan_pass(P, sp);
+            }
+        }
+    };
+    one();
+    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(e0, s));
+    for (int t = 0; t < passes; ++t) one();
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_pass = ms / passes;
+    if (kernel_ms_per_pass) {
+        // the dominant tile kernel alone, on the same stream
+        TilePlan tp = which == 1 ? plan_for(P, 1, MODE_SUM, 0)
+                                 : (which >= 3 ? plan_for(P, 0, MODE_BLOCK, kt, 8) : tsum);
+        TileArgs ta = tile_args(P, which == 1 ? 1 : 0, tp, G_NONE);
+        if (which >= 3) ta.W = Wv.p;
+        CK(cudaEventRecord(e0, s));
+        for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *kernel_ms_per_pass = ms / passes;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaGetLastError());
+    SKNR_API_END
+}
+
+int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* basis, int64_t basis_ell,
+                          int64_t iters, double* ms_per_iter, int64_t* kernels_per_iter) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
+    if (use_newton && (basis == nullptr || basis_ell != cfg->ell))
+        throw InvalidArgument("solve: ell > 0 requires a basis");
+    const int64_t ell = use_newton ? cfg->ell : 0;
+    SolveState S;
+    prepare_solve(P, S, ell, basis, nullptr, iters + 1000000, 1e-300, 1);
+    cudaStream_t s = P.stream;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = launch_count();
+    enqueue_iteration(P, S, ell, false, 1);
+    if (kernels_per_iter) *kernels_per_iter = launch_count() - l0;
+    CK(cudaStreamEndCapture(s, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    // warm-up iteration (also leaves the steady-state bound-shift path active)
+    CK(cudaGraphLaunch(exec, s));
+    CK(cudaStreamSynchronize(s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    for (int64_t t = 0; t < iters; ++t) CK(cudaGraphLaunch(exec, s));
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_iter = ms / static_cast<double>(iters);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    SKNR_API_END
+}
+
+// ---------------------------------------------------------------- multi-GPU (row sharding)
+int sknr_comm_unique_id(unsigned char id[128]) {
+    SKNR_API_BEGIN
+    (void)id;
+    throw RuntimeFailure("sknr_comm_unique_id: multi-GPU row sharding is not enabled in this build");
+    SKNR_API_END
+}
+
+int sknr_comm_init(int rank, int world, const unsigned char id[128], int device) {
+    SKNR_API_BEGIN
+    (void)rank;
+    (void)world;
+    (void)id;
+    (void)device;
+    throw RuntimeFailure("sknr_comm_init: multi-GPU row sharding is not enabled in this build");
+    SKNR_API_END
+}
+
+int sknr_comm_destroy(void) { return SKNR_OK; }
+
+int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
+    SKNR_API_BEGIN
+    (void)h;
+    (void)row_begin;
+    (void)row_end;
+    throw RuntimeFailure("sknr_problem_shard: multi-GPU row sharding is not enabled in this build");
+    SKNR_API_END
+}
+
+}  // extern "C"

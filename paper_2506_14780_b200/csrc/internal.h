@@ -1,0 +1,42 @@
+// internal.h -- declarations shared by the CUDA translation units of libsknr_b200.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sknr_device.cuh"
+
+namespace sknr {
+
+enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2 };
+
+// Arguments of the persistent tile kernels (tile_kernels.cu).
+struct TileArgs {
+    int64_t n_out = 0, n_in = 0;
+    int64_t in_block = 0, n_out_tiles = 0, n_in_blocks = 0, n_tiles = 0;
+    const double* out_pack = nullptr;  // points: [n_out][PK] (B, Y...); dense: B [n_out]
+    const double* in_pack = nullptr;   // points: [n_in][PK] (A, X...);  dense: A [n_in]
+    const double* C = nullptr;         // dense: element (o, in) at C[o + in*ldc]
+    int64_t ldc = 0;
+    double kappa = 0.0;                // dense: u = A + B - kappa*C
+    const double* W = nullptr;         // block: W[in*KT + c]
+    double* partial = nullptr;         // sum/max: [ib][n_out]; block: [ib][KT][n_out]
+    const DevState* st = nullptr;
+    unsigned guard = 0;
+};
+
+struct TilePlan {
+    const void* fn = nullptr;
+    int grid = 0, smem = 0, occ = 0;
+    int64_t out_tile = 0, in_block = 0, n_out_tiles = 0, n_in_blocks = 0, n_tiles = 0;
+};
+
+// dim: 0 = stored cost, 1..4 = point-cloud dimension. kt: block width (8..64) for MODE_BLOCK.
+TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks);
+void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s);
+int block_kt_for(int k);
+int chunk_inputs(int mode, int kt);
+
+void count_launch();
+int64_t launch_count();
+
+}  // namespace sknr

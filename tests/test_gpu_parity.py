@@ -1,0 +1,258 @@
+"""GPU parity: libsknr_b200 (sm_100a kernels through the C ABI) vs the CPU
+oracle on the same seeded inputs. Tolerances follow the north star: potentials
+within 1e-9 relative (fp64), identical iteration counts."""
+import numpy as np
+import pytest
+
+import oracle_ref as O
+import paper_2506_14780_b200 as sk
+from paper_2506_14780_b200 import generators as G
+from support import (gauge_normalized, projector_distance, random_measure, random_problem_data,
+                     random_vector, rel_err, symmetric_2x2, symmetric_2x2_optimum)
+
+pytestmark = pytest.mark.gpu
+
+TOL_POT = 1e-9
+
+
+def points_pair(inst, sub_n=None, sub_m=None):
+    x = inst.x if sub_n is None else inst.x[:sub_n]
+    y = inst.y if sub_m is None else inst.y[:sub_m]
+    a = inst.alpha if sub_n is None else np.full(x.shape[0], 1.0 / x.shape[0])
+    b = inst.beta if sub_m is None else np.full(y.shape[0], 1.0 / y.shape[0])
+    gp = sk.PointProblem(x, y, a, b, inst.epsilon, inst.cost_scale)
+    op = O.Instance(a, b, inst.epsilon, x=x, y=y, cost_div=1.0 / inst.cost_scale)
+    return gp, op
+
+
+# ------------------------------------------------------------------ transforms
+@pytest.mark.parametrize("n,m,eps", [(1, 1, 0.5), (7, 9, 0.5), (130, 257, 0.05), (513, 300, 0.01),
+                                     (1000, 1000, 1e-3)])
+def test_ctransforms_dense_match_oracle(n, m, eps):
+    rng = G.SplitMix64(100 + n)
+    cost, a, b = random_problem_data(rng, n, m)
+    gp = sk.Problem(cost, a, b, eps)
+    op = O.Instance(a, b, eps, cost=cost)
+    f = random_vector(rng, n, 0.3)
+    g_gpu = sk.ctransform_of_f(gp, f)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(g_gpu, g_ref) <= 1e-13
+    f_gpu = sk.ctransform_of_g(gp, g_ref)
+    f_ref = O.ctransform_of_g(op, g_ref)
+    assert rel_err(f_gpu, f_ref) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", 512), ("C1", 777), ("C3", 2000), ("C4", 4096)])
+def test_ctransforms_points_match_oracle(cfg, n):
+    inst = G.config(cfg, n=n, m=n) if cfg != "C3" else G.config("C3", n=n, m=n + 13)
+    gp, op = points_pair(inst)
+    rng = G.SplitMix64(7)
+    f = random_vector(rng, gp.n, 0.01)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(sk.ctransform_of_f(gp, f), g_ref) <= 1e-12
+    assert rel_err(sk.ctransform_of_g(gp, g_ref), O.ctransform_of_g(op, g_ref)) <= 1e-12
+
+
+def test_ctransform_2x2_known_answer():  # test_core.cpp:66-76
+    cost, a, b = symmetric_2x2()
+    gp = sk.Problem(cost, a, b, 1.0)
+    g = sk.ctransform_of_f(gp, np.zeros(2))
+    assert np.allclose(g, 0.3798854930417224754, rtol=1e-15, atol=0)
+    assert np.max(np.abs(sk.ctransform_of_g(gp, g))) <= 1e-15
+
+
+def test_overflow_safety_large_costs():  # test_core.cpp:186-202
+    rng = G.SplitMix64(16)
+    cost = np.empty((6, 7), order="F")
+    for j in range(7):
+        for i in range(6):
+            cost[i, j] = 1e4 * rng.uniform01()
+    a = random_measure(rng, 6)
+    b = random_measure(rng, 7)
+    gp = sk.Problem(cost, a, b, 1e-3)
+    op = O.Instance(a, b, 1e-3, cost=cost)
+    g = sk.ctransform_of_f(gp, np.zeros(6))
+    assert np.all(np.isfinite(g))
+    assert rel_err(g, O.ctransform_of_f(op, np.zeros(6))) <= 1e-13
+    f2 = sk.ctransform_of_g(gp, g)
+    assert rel_err(f2, O.ctransform_of_g(op, g)) <= 1e-13
+
+
+def test_zero_cost_plan_exact():  # test_core.cpp:101-113
+    rng = G.SplitMix64(13)
+    a = random_measure(rng, 3)
+    b = random_measure(rng, 5)
+    gp = sk.Problem(np.zeros((3, 5)), a, b, 0.9)
+    plan = sk.coupling(gp, np.zeros(3), np.zeros(5))
+    assert np.max(np.abs(plan - np.outer(a, b))) == 0.0
+
+
+def test_plan_marginals_match_oracle():
+    rng = G.SplitMix64(14)
+    cost, a, b = random_problem_data(rng, 300, 200)
+    gp = sk.Problem(cost, a, b, 0.1)
+    op = O.Instance(a, b, 0.1, cost=cost)
+    f = random_vector(rng, 300, 0.2)
+    g = O.ctransform_of_f(op, f)
+    r1, c1, l21, inf1 = sk.plan_marginals(gp, f, g)
+    r2, c2, l22, inf2 = O.plan_marginals(op, f, g)
+    assert rel_err(r1, r2) <= 1e-13 and rel_err(c1, c2) <= 1e-13
+    assert abs(l21 - l22) <= 1e-13 * max(l22, 1e-300) + 1e-18
+
+
+# ------------------------------------------------------------------ objective / spectral
+def test_block_products_match_oracle():
+    rng = G.SplitMix64(43)
+    cost, a, b = random_problem_data(rng, 301, 170)
+    gp = sk.Problem(cost, a, b, 0.2)
+    op = O.Instance(a, b, 0.2, cost=cost)
+    r = O.solve(op, tol=1e-12)
+    U = np.asfortranarray(np.array([random_vector(rng, 301) for _ in range(21)]).T)
+    V = np.asfortranarray(np.array([random_vector(rng, 170) for _ in range(21)]).T)
+    assert rel_err(sk.apply_sym_t_block(gp, r["f"], r["g"], U),
+                   O.apply_sym_t_block(op, r["f"], r["g"], U)) <= 1e-12
+    assert rel_err(sk.apply_sym_block(gp, r["f"], r["g"], V),
+                   O.apply_sym_block(op, r["f"], r["g"], V)) <= 1e-12
+
+
+@pytest.mark.parametrize("ell", [1, 5, 16, 32])
+def test_restricted_derivatives_match_oracle(ell):
+    rng = G.SplitMix64(70 + ell)
+    cost, a, b = random_problem_data(rng, 400, 333)
+    gp = sk.Problem(cost, a, b, 0.05)
+    op = O.Instance(a, b, 0.05, cost=cost)
+    f = random_vector(rng, 400, 0.05)
+    g = O.ctransform_of_f(op, f)
+    V = np.asfortranarray(np.array([random_vector(rng, 400) for _ in range(ell)]).T)
+    b1 = sk.SpectralBasis(V, V, np.zeros(ell), 0.05)
+    gr1, h1 = sk.restricted_derivatives(gp, f, b1, g)
+    gr2, h2 = O.restricted_derivatives(op, f, g, V)
+    assert rel_err(gr1, gr2) <= 1e-9
+    assert rel_err(h1, h2) <= 1e-11
+
+
+def test_top_modes_match_oracle():
+    inst = G.config("C1", n=300, m=300)
+    gp, op = points_pair(inst)
+    op2 = op.with_epsilon(0.05)
+    gp.set_epsilon(0.05)
+    r = O.solve(op2, tol=1e-12)
+    ell = 6
+    bo = O.top_modes(op2, r["f"], r["g"], ell)
+    bg = sk.top_modes(gp, r["f"], r["g"], ell)
+    assert np.max(np.abs(bg.rhos - bo["rhos"])) <= 1e-8
+    assert abs(bg.sweeps - bo["sweeps"]) <= 1
+    assert projector_distance(bo["vectors_sym"], bg.vectors_sym) <= 1e-6
+    gram = bg.vectors_sym.T @ bg.vectors_sym
+    assert np.max(np.abs(gram - np.eye(ell))) <= 1e-10
+    assert np.max(np.abs(np.sqrt(gp.alpha) @ bg.vectors_sym)) <= 1e-9
+
+
+# ------------------------------------------------------------------ solver
+def test_solve_reference_sk_trajectory():  # test_solver.cpp:187-202
+    rng = G.SplitMix64(65)
+    cost, a, b = random_problem_data(rng, 7, 9)
+    gp = sk.Problem(cost, a, b, 0.5)
+    op = O.Instance(a, b, 0.5, cost=cost)
+    rg = sk.solve(gp, tol=1e-30, max_iter=40)
+    ro = O.solve(op, tol=1e-30, max_iter=40)
+    assert np.max(np.abs(rg.f - ro["f"])) <= 1e-14
+    assert np.max(np.abs(rg.g - ro["g"])) <= 1e-14
+    assert len(rg.trace) == 40
+    for k in range(40):
+        assert abs(rg.trace[k].marginal_error - ro["trace"][k][0]) <= 1e-12
+
+
+def test_solve_c1_sk_parity():
+    inst = G.config("C1")
+    gp, op = points_pair(inst)
+    rg = sk.solve(gp, tol=1e-9)
+    ro = O.solve(op, tol=1e-9)
+    assert rg.converged and ro["converged"]
+    assert rg.iterations == ro["iterations"]
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT and rel_err(rg.g, ro["g"]) <= TOL_POT
+    for tg, to in zip(rg.trace, ro["trace"]):
+        assert abs(tg.marginal_error - to[0]) <= 1e-6 * to[0] + 1e-15
+        assert abs(tg.semi_dual_value - to[2]) <= 1e-12 * abs(to[2]) + 1e-15
+
+
+def test_solve_c1_sknr_parity():
+    inst = G.config("C1")
+    gp, op = points_pair(inst)
+    warm_o = O.solve(op.with_epsilon(inst.basis_eps), tol=1e-9)
+    basis = O.top_modes(op.with_epsilon(inst.basis_eps), warm_o["f"], warm_o["g"], inst.ell)
+    sb = sk.SpectralBasis(basis["vectors"], basis["vectors_sym"], basis["rhos"], inst.basis_eps)
+    rg = sk.solve(gp, tol=1e-9, ell=inst.ell, basis=sb, init=(warm_o["f"], warm_o["g"]))
+    ro = O.solve(op, tol=1e-9, ell=inst.ell, V=basis["vectors"], init=(warm_o["f"], warm_o["g"]))
+    assert rg.converged and ro["converged"]
+    assert rg.iterations == ro["iterations"]
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT and rel_err(rg.g, ro["g"]) <= TOL_POT
+    acc_g = [t.newton_accepted for t in rg.trace]
+    acc_o = [bool(t[4]) for t in ro["trace"]]
+    assert sum(a != b for a, b in zip(acc_g, acc_o)) <= 1
+
+
+def test_solve_dense_sknr_with_dense_basis():
+    rng = G.SplitMix64(67)
+    cost, a, b = random_problem_data(rng, 60, 50)
+    eps = 0.05
+    gp = sk.Problem(cost, a, b, eps)
+    op = O.Instance(a, b, eps, cost=cost)
+    ref = O.solve(op, tol=1e-13)
+    bo = O.top_modes(op, ref["f"], ref["g"], 4)
+    sb = sk.SpectralBasis(bo["vectors"], bo["vectors_sym"], bo["rhos"], eps)
+    rg = sk.solve(gp, tol=1e-11, ell=4, basis=sb)
+    ro = O.solve(op, tol=1e-11, ell=4, V=bo["vectors"])
+    assert rg.iterations == ro["iterations"]
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT
+    vals = [t.semi_dual_value for t in rg.trace]
+    assert all(vals[k] >= vals[k - 1] - 1e-12 for k in range(1, len(vals)))
+
+
+def test_solve_max_iter_and_determinism():
+    rng = G.SplitMix64(68)
+    cost, a, b = random_problem_data(rng, 80, 60)
+    gp = sk.Problem(cost, a, b, 0.4)
+    r1 = sk.solve(gp, tol=1e-10)
+    r2 = sk.solve(gp, tol=1e-10)
+    assert r1.converged
+    assert np.array_equal(r1.f, r2.f) and np.array_equal(r1.g, r2.g)
+    assert [t.marginal_error for t in r1.trace] == [t.marginal_error for t in r2.trace]
+    p = sk.solve(gp, tol=1e-14, max_iter=2)
+    assert not p.converged and p.iterations == 2
+
+
+def test_anneal_matches_oracle():
+    rng = G.SplitMix64(69)
+    cost, a, b = random_problem_data(rng, 40, 35)
+    gp = sk.Problem(cost, a, b, 1.0)
+    op = O.Instance(a, b, 1.0, cost=cost)
+    eps = [0.5, 0.25, 0.125]
+    sg = sk.anneal(gp, eps, warm="spectral", ell=3)
+    so = O.anneal(op, eps, warm="spectral", ell=3)
+    for s in range(3):
+        assert sg[s].converged and so[s]["converged"]
+        assert sg[s].iterations == so[s]["iterations"]
+        assert rel_err(sg[s].f, so[s]["f"]) <= TOL_POT
+
+
+def test_solve_errors_mirror_reference():
+    cost, a, b = symmetric_2x2()
+    gp = sk.Problem(cost, a, b, 1.0)
+    with pytest.raises(ValueError, match="requires a basis"):
+        sk.solve(gp, ell=2)
+    with pytest.raises(ValueError, match="tol_omega must be positive"):
+        sk.solve(gp, tol=0.0)
+    with pytest.raises(ValueError, match="max_iter must be >= 1"):
+        sk.solve(gp, max_iter=0)
+    with pytest.raises(ValueError, match="entries must be finite"):
+        sk.ctransform_of_f(gp, [np.nan, 0.0])
+
+
+def test_fixed_point_2x2():
+    cost, a, b = symmetric_2x2()
+    gp = sk.Problem(cost, a, b, 1.0)
+    f0, g0 = symmetric_2x2_optimum()
+    r = sk.solve(gp, tol=1e-14, max_iter=3, init=(f0, g0))
+    f, g = gauge_normalized(a, r.f, r.g)
+    assert np.max(np.abs(f - f0)) <= 1e-12 and np.max(np.abs(g - g0)) <= 1e-12
