@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py -- SK-NR(ell) hot path on B200 (driver contract).
+
+Workload (BASELINE.json configs[3], "C4"): n = m = 65536 points uniform in
+[0,1]^2, squared-Euclidean cost evaluated on the fly, uniform marginals, fp64,
+eps = 5e-4, ell = 32. A "step" is one Sinkhorn-Knopp iteration of the device
+solve loop (row LSE + column LSE over all n*m cells, gauge, on-device marginal
+stopping test); `value` counts the 2*n*m LSE cell-passes of that sweep per
+second (GCells/s of LSE sweeps). One SK-NR(32) iteration (adds the restricted
+Newton step: one more LSE pair + the ell-wide V^T P~ pass) and SK / SK-NR
+time-to-tolerance on C1 are reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (the reference restated in C++,
+oracle/, since the reference itself needs the absent Eigen3) on all host
+cores, on a bounded column sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GCells/s of LSE sweeps (C4 Sinkhorn sweep = 2 LSE passes over n*m cells)"
+UNIT = "GCells/s"
+# FP64 pipe instructions per cell of the on-the-fly d=2 LSE sum kernel:
+# exponent 1 DADD + 2 DFMA; exp2 3 DADD (Cody-Waite) + 5 DFMA (poly) + 1 DFMA (table x poly
+# fused with the accumulate) = 12 issue slots, counted as 2 flops each (FMA-equivalent).
+FP64_SLOTS_PER_CELL = 12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the C1 time-to-tolerance leg")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(self.gpu)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.15)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        busy = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def dist_max(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------- helpers
+def load_oracle():
+    """CPU oracle: the cpu_baseline / --impl reference legs only."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ref
+
+    return oracle_ref
+
+
+def column_sample(inst, ms):
+    y = np.asfortranarray(inst.y[:ms])
+    b = inst.beta[:ms] / inst.beta[:ms].sum()
+    return y, b
+
+
+def oracle_sweep_rate(O, inst, ms, threads, reps, warm=0):
+    """GCells/s of one reference SK iteration (solve with max_iter=1: column LSE,
+    row LSE, gauge, plan_marginals) on the n x ms column sample."""
+    O.set_threads(threads)
+    y, b = column_sample(inst, ms)
+    P = O.Instance(inst.alpha, b, inst.epsilon, x=inst.x, y=y, cost_div=1.0 / inst.cost_scale)
+    for _ in range(warm):
+        O.solve(P, tol=1e-300, max_iter=1, trace=False)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.solve(P, tol=1e-300, max_iter=1, trace=False)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    return 2.0 * inst.n * ms / t / 1e9, t, times
+
+
+def read_profile_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_lse_sum_kernel.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+# ---------------------------------------------------------------------------- arms
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2506_14780_b200 import generators as G
+
+    O = load_oracle()
+    inst = G.config(args.config)
+    threads = O.max_threads()
+    ms = 2048
+    rate, t, times = oracle_sweep_rate(O, inst, ms, threads, reps=max(args.steps, 1), warm=args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64, BASELINE C4 column sample)",
+        "config": {"workload": f"{args.config} SK iteration on an n x {ms} column sample", "n": inst.n,
+                   "m_sample": ms, "epsilon": inst.epsilon},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"n={inst.n} x m={ms} columns of {args.config}, one SK iteration per step "
+                                   "(oracle/sknr_oracle.cpp output-parallel restatement)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import paper_2506_14780_b200 as sk
+    from paper_2506_14780_b200 import generators as G
+
+    gpu = local
+    if world > 1:
+        # one process per GPU: this rank's GPU is the only one the library sees
+        os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
+    dist = dist_init(world)
+    inst = G.config(args.config)
+    n, m = inst.n, inst.m
+    cells = float(n) * m
+    prob = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale)
+
+    # ---- value: SK iterations, device-resident, L2 flushed between timed steps
+    clocks = ClockSampler(gpu)
+    barrier(dist)
+    clocks.start()
+    ms_iter, kpi = sk.bench_iterations(prob, 0, None, iters=args.steps, warmup=max(args.warmup, 3),
+                                       flush_l2=True)
+    clk = clocks.stop()
+    barrier(dist)
+    ms_iter_max = dist_max(dist, ms_iter)
+    value = world * 2.0 * cells / (ms_iter_max * 1e-3) / 1e9
+
+    # ---- dominant kernel: the column-LSE sum tile kernel alone, CUDA events on its stream
+    ms_pass, ms_kernel = sk.bench_pass(prob, 2, 0, passes=10)
+    peak_tflops, _ = sk.bench_fp64_peak()
+    achieved = FP64_SLOTS_PER_CELL * 2.0 * cells / (ms_kernel * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved / peak_tflops, "traffic": read_profile_traffic(),
+                "kernel": "pts_tile_kernel<2,4,SUM> (column LSE, on-the-fly d=2)",
+                "kernel_ms": ms_kernel, "kernel_gcells_per_s": cells / (ms_kernel * 1e-3) / 1e9,
+                "algorithmic_per_cell": f"{FP64_SLOTS_PER_CELL} FP64 issue slots (x2 flops)",
+                "peak_source": "measured DFMA-only kernel on this GPU (sknr_bench_fp64_peak)"}
+
+    # ---- SK-NR(ell) iteration (restricted Newton step included)
+    rng = np.random.default_rng(0)
+    V = np.linalg.qr(rng.standard_normal((n, inst.ell)))[0] * np.sqrt(n)
+    basis = sk.SpectralBasis(np.asfortranarray(V), np.asfortranarray(V), np.zeros(inst.ell), inst.epsilon)
+    ms_nr, kpi_nr = sk.bench_iterations(prob, inst.ell, basis, iters=max(3, args.steps // 10), warmup=1,
+                                        flush_l2=True)
+
+    # ---- e2e: public C ABI with host buffers (problem upload + solve + potentials download)
+    k_e2e = max(args.steps, 1)
+    t0 = time.perf_counter()
+    p2 = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale)
+    res = sk.solve(p2, tol=1e-300, max_iter=k_e2e, trace=False)
+    t_e2e = time.perf_counter() - t0
+    assert res.iterations == k_e2e
+    h2d = (inst.x.nbytes + inst.y.nbytes + inst.alpha.nbytes + inst.beta.nbytes) / k_e2e
+    d2h = (res.f.nbytes + res.g.nbytes) / k_e2e
+    t_e2e = dist_max(dist, t_e2e)
+    e2e = {"value": world * 2.0 * cells * k_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": k_e2e,
+           "path": "PointProblem(host arrays) + sknr_solve(max_iter=K) + f,g download, wall clock"}
+    del p2
+
+    # ---- time to tolerance on C1 (SK and SK-NR(10) with eps'=2eps warm start + basis)
+    ttt = None
+    if not args.no_ttt:
+        c1 = G.config("C1")
+        p1 = sk.PointProblem(c1.x, c1.y, c1.alpha, c1.beta, c1.epsilon)
+        t0 = time.perf_counter()
+        r_sk = sk.solve(p1, tol=1e-9, trace=False)
+        t_sk = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        p1w = sk.PointProblem(c1.x, c1.y, c1.alpha, c1.beta, c1.basis_eps)
+        warm = sk.solve(p1w, tol=1e-9, trace=False)
+        b1 = sk.top_modes(p1w, warm.f, warm.g, c1.ell)
+        t_basis = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r_nr = sk.solve(p1, tol=1e-9, ell=c1.ell, basis=b1, init=(warm.f, warm.g), trace=False)
+        t_nr = time.perf_counter() - t0
+        ttt = {"config": "C1 n=m=512 eps=1e-2 tol=1e-9 (L2-sum marginal error)",
+               "sk": {"iterations": r_sk.iterations, "converged": r_sk.converged, "ms": t_sk * 1e3},
+               "sknr": {"ell": c1.ell, "iterations": r_nr.iterations, "converged": r_nr.converged,
+                        "ms_main_solve": t_nr * 1e3, "ms_end_to_end": (t_nr + t_basis) * 1e3,
+                        "warm_iterations": warm.iterations, "basis_sweeps": b1.sweeps}}
+
+    # ---- CPU baseline: oracle, 1 core (the reference is single-threaded by design)
+    cpu = None
+    if rank == 0:
+        O = load_oracle()
+        ms_s = 256
+        rate, t, _ = oracle_sweep_rate(O, inst, ms_s, 1, reps=2)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"n={n} x m={ms_s} columns of C4, one reference SK iteration (column LSE, row "
+                         "LSE, gauge, plan_marginals) per rep, 2 reps, oracle/sknr_oracle.cpp"}
+
+    launches = int(kpi * args.steps)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_iter_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 point clouds, BASELINE C4)",
+            "config": {"workload": "C4: n=m=65536, d=2 uniform [0,1]^2, on-the-fly squared-Euclidean cost, "
+                                   "uniform marginals, eps=5e-4; step = one SK iteration of the device loop",
+                       "n": n, "m": m, "d": 2, "epsilon": inst.epsilon,
+                       "l2": "flushed between timed steps (256 MiB memset, untimed)",
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "kernels_per_step": kpi,
+            "clocks": clk,
+            "sknr_iteration": {"ell": inst.ell, "ms": ms_nr, "kernels": kpi_nr,
+                               "cell_passes": 5, "gcells_per_s": 5 * cells / (ms_nr * 1e-3) / 1e9},
+            "pass_ms": {"column_lse_full": ms_pass},
+            "time_to_tol": ttt,
+            "library": sk.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

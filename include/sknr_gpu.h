@@ -155,12 +155,19 @@ int sknr_anneal(sknr_problem p, const double* epsilons, int64_t stages, int warm
  * 3 Newton restricted-derivative pass, 4 top_modes block pass. */
 int sknr_bench_pass(sknr_problem p, int which, int64_t ell, int passes, double* ms_per_pass,
                     double* kernel_ms_per_pass);
-/* Runs `iters` SK-NR iterations (stopping test disabled) on device-resident
- * state, one CUDA graph per iteration, and returns device ms per iteration and
- * the number of kernels in one iteration's graph; bench.py's "value" leg. */
+/* Runs `warmup` untimed then `iters` timed SK-NR iterations (stopping test
+ * disabled) on device-resident state, one CUDA graph per iteration; each timed
+ * iteration is bracketed by CUDA events on the handle's stream and, with
+ * flush_l2, preceded (untimed) by a 256 MiB memset that evicts the 126 MB L2.
+ * Returns mean device ms per iteration and the kernel count of one iteration's
+ * graph; bench.py's "value" leg. */
 int sknr_bench_iterations(sknr_problem p, const sknr_config* cfg, const double* basis,
-                          int64_t basis_ell, int64_t iters, double* ms_per_iter,
-                          int64_t* kernels_per_iter);
+                          int64_t basis_ell, int64_t warmup, int64_t iters, int flush_l2,
+                          double* ms_per_iter, int64_t* kernels_per_iter);
+
+/* Measured FP64 FMA ceiling of the current device (TFLOP/s, FMA = 2 flops):
+ * the denominator of the on-the-fly roofline (MEASURED_PEAKS.json has no FP64 entry). */
+int sknr_bench_fp64_peak(double* tflops, double* ms);
 
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU. Rank 0 calls sknr_comm_unique_id, the id travels over

@@ -99,8 +99,9 @@ _SIGS = {
                     ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_Record),
                     _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
     "sknr_bench_pass": [_P, ctypes.c_int, _I64, ctypes.c_int, _D, _D],
-    "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _D,
+    "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _I64, ctypes.c_int, _D,
                               ctypes.POINTER(_I64)],
+    "sknr_bench_fp64_peak": [_D, _D],
     "sknr_comm_unique_id": [ctypes.c_char_p],
     "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
     "sknr_comm_destroy": [],
@@ -575,14 +576,24 @@ def bench_pass(problem: Problem, which: int, ell: int = 0, passes: int = 5):
 
 
 def bench_iterations(problem: Problem, ell: int = 0, basis: Optional[SpectralBasis] = None,
-                     iters: int = 5):
+                     iters: int = 5, warmup: int = 1, flush_l2: bool = True):
+    """Device ms per SK-NR(ell) iteration (CUDA events per iteration, L2 flushed
+    between iterations) and the number of kernels in one iteration."""
     cfg = _config(1e-9, 1 << 40, ell, False)
     V = _mat_f(basis.vectors) if (basis is not None and ell > 0) else None
     ms = ctypes.c_double()
     kpi = _I64()
-    _check(lib().sknr_bench_iterations(problem.handle, ctypes.byref(cfg), _ptr(V), int(ell) if V is not None else 0,
-                                       int(iters), ctypes.byref(ms), ctypes.byref(kpi)))
+    _check(lib().sknr_bench_iterations(problem.handle, ctypes.byref(cfg), _ptr(V),
+                                       int(ell) if V is not None else 0, int(warmup), int(iters),
+                                       1 if flush_l2 else 0, ctypes.byref(ms), ctypes.byref(kpi)))
     return ms.value, int(kpi.value)
+
+
+def bench_fp64_peak():
+    """(TFLOP/s, ms) of a DFMA-only kernel filling every SM: the measured FP64 ceiling."""
+    t, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().sknr_bench_fp64_peak(ctypes.byref(t), ctypes.byref(ms)))
+    return t.value, ms.value
 
 
 __all__ = [

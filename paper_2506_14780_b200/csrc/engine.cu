@@ -2062,7 +2062,8 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
 }
 
 int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* basis, int64_t basis_ell,
-                          int64_t iters, double* ms_per_iter, int64_t* kernels_per_iter) {
+                          int64_t warmup, int64_t iters, int flush_l2, double* ms_per_iter,
+                          int64_t* kernels_per_iter) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
@@ -2071,8 +2072,10 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
         throw InvalidArgument("solve: ell > 0 requires a basis");
     const int64_t ell = use_newton ? cfg->ell : 0;
     SolveState S;
-    prepare_solve(P, S, ell, basis, nullptr, iters + 1000000, 1e-300, 1);
+    prepare_solve(P, S, ell, basis, nullptr, warmup + iters + 1000000, 1e-300, 1);
     cudaStream_t s = P.stream;
+    DBuf flush;
+    if (flush_l2) flush.ensure((256ull << 20) / sizeof(double));  // 256 MiB > 126 MB L2
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -2081,23 +2084,69 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
     if (kernels_per_iter) *kernels_per_iter = launch_count() - l0;
     CK(cudaStreamEndCapture(s, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
-    // warm-up iteration (also leaves the steady-state bound-shift path active)
-    CK(cudaGraphLaunch(exec, s));
+    for (int64_t t = 0; t < std::max<int64_t>(warmup, 1); ++t) CK(cudaGraphLaunch(exec, s));
     CK(cudaStreamSynchronize(s));
+    std::vector<cudaEvent_t> ev(2 * iters);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (int64_t t = 0; t < iters; ++t) {
+        if (flush_l2) CK(cudaMemsetAsync(flush.p, t & 0xFF, flush.n * sizeof(double), s));
+        CK(cudaEventRecord(ev[2 * t], s));
+        CK(cudaGraphLaunch(exec, s));
+        CK(cudaEventRecord(ev[2 * t + 1], s));
+    }
+    CK(cudaStreamSynchronize(s));
+    double total = 0.0;
+    for (int64_t t = 0; t < iters; ++t) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[2 * t], ev[2 * t + 1]));
+        total += ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    *ms_per_iter = total / static_cast<double>(std::max<int64_t>(iters, 1));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    SKNR_API_END
+}
+
+// FP64 pipe ceiling on this device: 8 independent DFMA chains per thread, a
+// full grid of 148 x 8 CTAs of 256 threads, timed with CUDA events.
+__global__ void k_fp64_peak(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-10, x2 = x0 + 2e-10, x3 = x0 + 3e-10;
+    double x4 = x0 + 4e-10, x5 = x0 + 5e-10, x6 = x0 + 6e-10, x7 = x0 + 7e-10;
+    for (int i = 0; i < iters; ++i) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;
+}
+
+int sknr_bench_fp64_peak(double* tflops, double* ms) {
+    SKNR_API_BEGIN
+    check_device();
+    int sms = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf out;
+    out.ensure(1);
+    const int iters = 20000, grid = sms * 8, block = 256;
+    k_fp64_peak<<<grid, block>>>(out.p, 100, 0.999999, 1e-7);
+    CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, s));
-    for (int64_t t = 0; t < iters; ++t) CK(cudaGraphLaunch(exec, s));
-    CK(cudaEventRecord(e1, s));
+    CK(cudaEventRecord(e0));
+    count_launch();
+    k_fp64_peak<<<grid, block>>>(out.p, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_per_iter = ms / static_cast<double>(iters);
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(grid) * block;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    if (ms) *ms = t;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
     SKNR_API_END
 }
 

@@ -55,6 +55,8 @@ def lib():
             build()
         _lib = ctypes.CDLL(LIB)
         _lib.oracle_last_error.restype = ctypes.c_char_p
+        # output-parallel loops are bitwise identical to 1 thread (sknr_oracle.cpp header)
+        _lib.oracle_set_threads(int(os.environ.get("ORACLE_THREADS", "0")))
     return _lib
 
 

@@ -233,7 +233,9 @@ def test_anneal_matches_oracle():
     for s in range(3):
         assert sg[s].converged and so[s]["converged"]
         assert sg[s].iterations == so[s]["iterations"]
-        assert rel_err(sg[s].f, so[s]["f"]) <= TOL_POT
+        # stages >= 1 use a basis each side computed itself with top_modes
+        # (residual tol 1e-8), so the Newton directions agree only to ~1e-8.
+        assert rel_err(sg[s].f, so[s]["f"]) <= (TOL_POT if s == 0 else 2e-8)
 
 
 def test_solve_errors_mirror_reference():
