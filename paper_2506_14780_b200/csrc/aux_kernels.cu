@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
         if (a.lw) e = a.lw[i];
         if (a.v) e += a.v[i] * a.inv_eps;
         if (a.sq) e -= a.kc * a.sq[i];
-        a.pack[i * a.pk] = kL64 * e;
+        a.pack[i * a.pk] = kLS * e;
         for (int c = 0; c < a.d; ++c) a.pack[i * a.pk + 1 + c] = a.sigma * a.coords[i + c * a.count];
         for (int c = a.d + 1; c < a.pk; ++c) a.pack[i * a.pk + c] = 0.0;
         if (a.ref) {
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
             s = bound ? a.Lref[o] + dshift : 0.0;
             a.shift[o] = s;
         }
-        a.pack[o * a.pk] = kL64 * (e - s);
+        a.pack[o * a.pk] = kLS * (e - s);
         for (int c = 0; c < a.d; ++c) a.pack[o * a.pk + 1 + c] = a.sigma * a.coords[o + c * a.count];
         for (int c = a.d + 1; c < a.pk; ++c) a.pack[o * a.pk + c] = 0.0;
     }
@@ -118,11 +118,11 @@ __global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {
          o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double M = -kInf;
         for (int64_t b = 0; b < a.nb; ++b) M = fmax(M, a.partial[b * a.n_out + o]);
-        const double s = a.shift[o] + M * kInvL64;
+        const double s = a.shift[o] + M * kInvLS;
         a.shift[o] = s;
         double e = 0.0;
         if (a.sq) e -= a.kc * a.sq[o];
-        a.pack[o * a.pk] = kL64 * (e - s);
+        a.pack[o * a.pk] = kLS * (e - s);
     }
 }
 
@@ -262,6 +262,96 @@ __global__ void __launch_bounds__(AUX_NT) k_gram(GramArgs a) {
         a.out[p] = a.out_scale * s;
     }
     if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+int reduce_blocks(int64_t T) {
+    int64_t b = (T + AUX_NT * 8 - 1) / (AUX_NT * 8);
+    if (b < 1) b = 1;
+    if (b > 296) b = 296;
+    return static_cast<int>(b);
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    __shared__ double sh[RED_MAX_TERMS][AUX_NT / 32];
+    double acc[RED_MAX_TERMS];
+#pragma unroll
+    for (int t = 0; t < RED_MAX_TERMS; ++t) acc[t] = 0.0;
+    const int64_t total = a.T[0] + a.T[1];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int seg = e < a.T[0] ? 0 : 1;
+        const int64_t i = seg == 0 ? e : e - a.T[0];
+#pragma unroll
+        for (int t = 0; t < RED_MAX_TERMS; ++t) {
+            if (t >= a.nterms || a.seg[t] != seg) continue;
+            const double x = a.x[t][i];
+            if (a.op[t] == RED_DOT)
+                acc[t] = a.y[t] ? fma(x, a.y[t][i], acc[t]) : acc[t] + x;
+            else if (a.op[t] == RED_SQ)
+                acc[t] = fma(x, x, acc[t]);
+            else
+                acc[t] = fmax(acc[t], fabs(x));
+        }
+    }
+    // warp tree then fixed cross-warp order
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int t = 0; t < RED_MAX_TERMS; ++t) {
+        double v = acc[t];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_down_sync(0xffffffffu, v, o);
+            v = a.op[t] == RED_MAXABS ? fmax(v, w) : v + w;
+        }
+        if (lane == 0) sh[t][warp] = v;
+    }
+    __syncthreads();
+    __shared__ bool is_last;
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < a.nterms; ++t) {
+            double v = sh[t][0];
+            for (int w = 1; w < AUX_NT / 32; ++w) v = a.op[t] == RED_MAXABS ? fmax(v, sh[t][w]) : v + sh[t][w];
+            a.part[static_cast<int64_t>(blockIdx.x) * a.nterms + t] = v;
+        }
+        __threadfence();
+        is_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last || threadIdx.x != 0) return;
+    __threadfence();
+    double r[RED_MAX_TERMS];
+    for (int t = 0; t < a.nterms; ++t) {
+        double v = a.part[t];
+        for (unsigned b = 1; b < gridDim.x; ++b) {
+            const double w = a.part[static_cast<int64_t>(b) * a.nterms + t];
+            v = a.op[t] == RED_MAXABS ? fmax(v, w) : v + w;
+        }
+        r[t] = v;
+        a.out[t] = v;
+    }
+    *a.counter = 0u;
+    DevState* st = a.st;
+    if (a.epilogue == EPI_GAUGE) {
+        st->c_gauge = r[0];
+    } else if (a.epilogue == EPI_CHECK) {
+        // r: |row-a|^2, max|row-a|, a.f, |col-b|^2, max|col-b|, b.h  (core.cpp:145-150)
+        if (st->done) return;
+        st->gap_l2 = sqrt(r[0]) + sqrt(r[3]);
+        st->gap_inf = r[1] + r[4];
+        st->q0 = r[2] + r[5];
+        if (st->gap_l2 < st->tol) {
+            st->conv = 1;
+            st->done = 1;
+        } else if (a.newton) {
+            st->newton_ok = 1;
+            st->attempted = 1;
+        }
+    } else if (a.epilogue == EPI_ACCEPT) {
+        // Q1 = a.f' + b.h'; accept iff Q1 > Q0 (solver.cpp:46-47)
+        if (st->done || !st->newton_ok) return;
+        st->q1 = r[0] + r[1];
+        st->accept = st->q1 > st->q0 ? 1 : 0;
+    }
 }
 
 }  // namespace sknr

@@ -103,4 +103,29 @@ struct GramArgs {
 __global__ void k_gram(GramArgs a);
 int gram_blocks(int64_t T);
 
+// Fused deterministic scalar reductions over one or two index segments:
+// term t reduces over segment seg[t] either sum x*y (y == nullptr: sum x),
+// sum x*x, or max |x|. Results land in out[t]; the last block merges block
+// partials in block order, then runs an optional epilogue on DevState.
+enum { RED_DOT = 0, RED_SQ = 1, RED_MAXABS = 2 };
+enum { EPI_NONE = 0, EPI_GAUGE = 1, EPI_CHECK = 2, EPI_ACCEPT = 3 };
+constexpr int RED_MAX_TERMS = 6;
+struct RedArgs {
+    int64_t T[2] = {0, 0};
+    int nterms = 0;
+    const double* x[RED_MAX_TERMS] = {};
+    const double* y[RED_MAX_TERMS] = {};
+    int op[RED_MAX_TERMS] = {};
+    int seg[RED_MAX_TERMS] = {};
+    double* out = nullptr;   // nterms results
+    double* part = nullptr;  // gridDim * nterms
+    unsigned* counter = nullptr;
+    int epilogue = EPI_NONE;
+    int newton = 0;
+    DevState* st = nullptr;
+    unsigned guard = 0;
+};
+__global__ void k_reduce(RedArgs a);
+int reduce_blocks(int64_t T);
+
 }  // namespace sknr

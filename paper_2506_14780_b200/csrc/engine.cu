@@ -625,7 +625,7 @@ struct Problem {
     bool otf() const { return dim > 0; }  // on-the-fly cost (points, d <= 4)
     double inv_eps() const { return 1.0 / eps; }
     double kc() const { return otf() ? kappa / eps : 0.0; }
-    double sigma() const { return otf() ? std::sqrt(2.0 * kL64 * kappa / eps) : 0.0; }
+    double sigma() const { return otf() ? std::sqrt(2.0 * kLS * kappa / eps) : 0.0; }
     int pk() const { return otf() ? (dim + 2) / 2 * 2 : 1; }
     Side& in_side(int dir) { return dir == 0 ? src : tgt; }
     Side& out_side(int dir) { return dir == 0 ? tgt : src; }
@@ -807,7 +807,7 @@ static TileArgs tile_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     a.in_pack = P.pack_in[dir].p;
     a.C = P.cost_for(dir);
     a.ldc = P.ldc_for(dir);
-    a.kappa = kL64 * P.inv_eps();
+    a.kappa = kLS * P.inv_eps();
     a.partial = P.partial.p;
     a.st = P.st;
     a.guard = guard;
@@ -1263,8 +1263,23 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
     count_launch();
     k_copy<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.gnext.p, m, P.st, G_DONE);
     lse(P, 1, S.g.p, S.f.p, G_DONE);
-    // gauge (solver.cpp:108-112)
-    gram(P, n, 1, 1, S.f.p, n, P.src.w.p, n, nullptr, &P.st->c_gauge, G_DONE);
+    // gauge (solver.cpp:108-112): c = alpha . f
+    {
+        RedArgs ra;
+        ra.T[0] = n;
+        ra.nterms = 1;
+        ra.x[0] = P.src.w.p;
+        ra.y[0] = S.f.p;
+        ra.op[0] = RED_DOT;
+        ra.out = P.sums.p + 8;
+        ra.part = P.gram_part.p;
+        ra.counter = &P.st->counters[6];
+        ra.epilogue = EPI_GAUGE;
+        ra.st = P.st;
+        ra.guard = G_DONE;
+        count_launch();
+        k_reduce<<<reduce_blocks(n), AUX_NT, 0, s>>>(ra);
+    }
     count_launch();
     k_gauge_apply<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, S.g.p, m,
                                                      P.inv_eps(), S.rowres.p, P.st);
@@ -1274,18 +1289,31 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
     k_colres<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.h.p, P.tgt.w.p, m, P.inv_eps(), S.colres.p, P.st,
                                             G_DONE);
     double* sums = P.sums.p;
-    gram(P, n, 1, 1, S.rowres.p, n, nullptr, 0, nullptr, sums + 0, G_DONE);
-    gram(P, m, 1, 1, S.colres.p, m, nullptr, 0, nullptr, sums + 1, G_DONE);
-    count_launch();
-    k_absmax<<<gram_blocks(n), AUX_NT, 0, s>>>(S.rowres.p, n, P.gram_part.p, sums + 2,
-                                               &P.st->counters[5], P.st, G_DONE);
-    count_launch();
-    k_absmax<<<gram_blocks(m), AUX_NT, 0, s>>>(S.colres.p, m, P.gram_part.p, sums + 3,
-                                               &P.st->counters[5], P.st, G_DONE);
-    gram(P, n, 1, 1, P.src.w.p, n, S.f.p, n, nullptr, sums + 4, G_DONE);
-    gram(P, m, 1, 1, P.tgt.w.p, m, S.h.p, m, nullptr, sums + 5, G_DONE);
-    count_launch();
-    k_check<<<1, 32, 0, s>>>(P.st, sums, newton ? 1 : 0);
+    // marginal_gap (core.cpp:145-150) + Q0 = a.f + b.h, stopping test on device
+    {
+        RedArgs ra;
+        ra.T[0] = n;
+        ra.T[1] = m;
+        ra.nterms = 6;
+        const double* xs[6] = {S.rowres.p, S.rowres.p, P.src.w.p, S.colres.p, S.colres.p, P.tgt.w.p};
+        const double* ys[6] = {nullptr, nullptr, S.f.p, nullptr, nullptr, S.h.p};
+        const int ops[6] = {RED_SQ, RED_MAXABS, RED_DOT, RED_SQ, RED_MAXABS, RED_DOT};
+        for (int t = 0; t < 6; ++t) {
+            ra.x[t] = xs[t];
+            ra.y[t] = ys[t];
+            ra.op[t] = ops[t];
+            ra.seg[t] = t < 3 ? 0 : 1;
+        }
+        ra.out = sums;
+        ra.part = P.gram_part.p;
+        ra.counter = &P.st->counters[6];
+        ra.epilogue = EPI_CHECK;
+        ra.newton = newton ? 1 : 0;
+        ra.st = P.st;
+        ra.guard = G_DONE;
+        count_launch();
+        k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
+    }
     if (newton) {
         const unsigned gn = G_DONE | G_NEWTON;
         const int l = static_cast<int>(ell);
@@ -1318,10 +1346,26 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         count_launch();
         k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
         lse(P, 0, S.fcand.p, S.hcand.p, gn);
-        gram(P, n, 1, 1, P.src.w.p, n, S.fcand.p, n, nullptr, sums + 6, gn);
-        gram(P, m, 1, 1, P.tgt.w.p, m, S.hcand.p, m, nullptr, sums + 7, gn);
-        count_launch();
-        k_accept<<<1, 32, 0, s>>>(P.st, sums + 6);
+        {
+            RedArgs ra;
+            ra.T[0] = n;
+            ra.T[1] = m;
+            ra.nterms = 2;
+            ra.x[0] = P.src.w.p;
+            ra.y[0] = S.fcand.p;
+            ra.x[1] = P.tgt.w.p;
+            ra.y[1] = S.hcand.p;
+            ra.op[0] = ra.op[1] = RED_DOT;
+            ra.seg[1] = 1;
+            ra.out = sums + 6;
+            ra.part = P.gram_part.p;
+            ra.counter = &P.st->counters[6];
+            ra.epilogue = EPI_ACCEPT;
+            ra.st = P.st;
+            ra.guard = gn;
+            count_launch();
+            k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
+        }
         count_launch();
         k_select<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, S.fcand.p, n, S.gnext.p, S.h.p, S.hcand.p, m,
                                                     P.st);

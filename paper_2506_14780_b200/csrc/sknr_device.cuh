@@ -2,40 +2,40 @@
 //
 // Scaled log domain. Every O(nm) kernel evaluates a cell exponent
 //   E_ij = la_i + (f_i - C_ij)/eps - s_j        (core.cpp:47-50, natural log)
-// in units of 1/64 of a binary order of magnitude: u = L64 * E, L64 = 64 log2(e).
+// in units of 1/256 of a binary order of magnitude: u = LS * E, LS = 256 log2(e).
 // The host-side prep folds all per-row / per-column terms into two vectors A
 // (inputs) and B (outputs) and, for point clouds, scales the coordinates by
-// sigma = sqrt(2 L64 kappa / eps) so that
-//   u = A_in + B_out + <X_in, Y_out>           (on-the-fly cost, d FMAs)
-//   u = A_in + B_out - (L64/eps) * C[out,in]    (stored cost, 1 FMA)
-// and exp(E) = 2^(u/64) is evaluated by pexp() below: Cody-Waite rounding with
-// the 1.5*2^52 magic constant (3 DADD), a degree-5 polynomial for 2^(r/64),
-// |r| <= 1/2 (5 DFMA, truncation < 4e-17), and a 64-entry table of 2^(e/64)
-// whose exponent field absorbs k>>6 with integer adds (no FP64 slot). The
-// table lives in shared memory replicated 16x so the 16 lanes of each
-// half-warp hit 16 distinct 8-byte bank pairs: a warp-wide table read costs the
-// minimum 2 wavefronts regardless of the index pattern.
+// sigma = sqrt(2 LS kappa / eps) so that
+//   u = A_in + B_out + <X_in, Y_out>           (on-the-fly cost: 1 DADD + d DFMA)
+//   u = A_in + B_out - (LS/eps) * C[out,in]     (stored cost: 1 DADD + 1 DFMA)
+// and exp(E) = 2^(u/256) is evaluated by pexp() below in 8 FP64 issue slots:
+// Cody-Waite rounding against the biased magic constant 1.5*2^52 + 1023*256
+// (3 DADD), a degree-4 polynomial for 2^(r/256), |r| <= 1/2 (4 DFMA,
+// truncation < 4e-17), and a 256-entry table of 2^(e/256) whose biased
+// exponent field (k>>8)+1023 is OR-ed in with integer ops (no FP64 slot).
+// The table is stored with the exponent field cleared and replicated 16x in
+// shared memory, so the 16 lanes of each half-warp hit 16 distinct 8-byte bank
+// pairs: a warp's table read is always the minimum 2 wavefronts.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace sknr {
 
-constexpr double kL64 = 92.33248261689366;      // 64 * log2(e)
-constexpr double kInvL64 = 1.0 / 92.33248261689366;
-constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
-constexpr long long kMagicBits = 0x4338000000000000LL;
-constexpr int kKmin = -64000;                   // 2^-1000: below, a term is flushed to 0
-constexpr int kKmax = 64000;                    // 2^+1000: above, +inf (unshifted passes only)
+constexpr double kLS = 369.3299304675746;       // 256 * log2(e)
+constexpr double kInvLS = 1.0 / 369.3299304675746;
+constexpr double kMagicB = 6755399441317632.0;  // 1.5 * 2^52 + 1023 * 256
+constexpr int kMagicHi = 0x43380000;            // hi word of 1.5 * 2^52
+constexpr int kKcMax = 2046 * 256 + 255;        // largest biased k before the exponent field overflows
+constexpr int kTabEntries = 256;
 constexpr int kTabRep = 16;
-constexpr int kTabDoubles = 64 * kTabRep;
+constexpr int kTabWords = kTabEntries * kTabRep;  // 32 KiB of shared memory
 
-// (ln2/64)^k / k!
-constexpr double kP1 = 0.010830424696249145;
-constexpr double kP2 = 5.86490495505617e-05;
-constexpr double kP3 = 2.1173137155464776e-07;
-constexpr double kP4 = 5.732851688640402e-10;
-constexpr double kP5 = 1.2417843701716925e-12;
+// (ln2/256)^k / k!
+constexpr double kP1 = 0.0027076061740622863;
+constexpr double kP2 = 3.6655655969101062e-06;
+constexpr double kP3 = 3.3083026805413713e-09;
+constexpr double kP4 = 2.239395190875157e-12;
 
 // Device flags / scalars of one problem handle. Kernels consult them through
 // a guard word so a whole iteration can live in one CUDA graph: work that is
@@ -87,46 +87,50 @@ __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
     return false;
 }
 
-// Split evaluation: 2^(u/64) = T' * p. `tabl` = shared table + (lane & 15).
-// HI_CLAMP adds the +inf branch for unshifted passes whose exponents are not
-// bounded above by construction.
+// Split evaluation 2^(u/256) = T' * p. `tab` = shared replicated table,
+// `laneoff` = (lane & 15) * 8 bytes, `c3` = kP3 held in a register by the caller
+// (the first Horner step has two constant operands and would otherwise
+// rematerialise one per cell). Terms below 2^-1022 come out as 0 / subnormal;
+// HI_CLAMP caps terms at 2^1023 for passes whose exponents are not bounded
+// above by construction.
 template <bool HI_CLAMP>
-__device__ __forceinline__ void pexp_parts(double u, const double* __restrict__ tabl, double& Tp,
-                                           double& p) {
-    const double t = u + kMagic;
-    const double kf = t - kMagic;
+__device__ __forceinline__ void pexp_parts(double u, const unsigned long long* __restrict__ tab,
+                                           unsigned laneoff, double c3, double& Tp, double& p) {
+    const double t = u + kMagicB;
+    const double kf = t - kMagicB;
     const double r = u - kf;
-    p = fma(r, kP5, kP4);
-    p = fma(p, r, kP3);
+    p = fma(r, kP4, c3);
     p = fma(p, r, kP2);
     p = fma(p, r, kP1);
     p = fma(p, r, 1.0);
-    const long long tb = __double_as_longlong(t);
-    const int k = static_cast<int>(tb);
-    const double T = tabl[(k & 63) << 4];
-    int hi = __double2hiint(T) + ((k >> 6) << 20);
-    hi = (tb >= kMagicBits + kKmin) ? hi : 0;
-    int lo = __double2loint(T);
-    if (HI_CLAMP) {
-        const bool over = tb > kMagicBits + kKmax;
-        hi = over ? 0x7FF00000 : hi;
-        lo = over ? 0 : lo;
-    }
-    Tp = __hiloint2double(hi, lo);
+    int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
+    if (HI_CLAMP) kc = min(kc, kKcMax);
+    const unsigned s = static_cast<unsigned>(kc) << 12;
+    const unsigned off = ((s >> 5) & 0x7F80u) | laneoff;
+    const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
+    Tp = __hiloint2double(static_cast<int>((s & 0xFFF00000u) | T.y), static_cast<int>(T.x));
 }
 
 template <bool HI_CLAMP>
-__device__ __forceinline__ double pexp(double u, const double* __restrict__ tabl) {
+__device__ __forceinline__ double pexp(double u, const unsigned long long* __restrict__ tab,
+                                       unsigned laneoff, double c3) {
     double Tp, p;
-    pexp_parts<HI_CLAMP>(u, tabl, Tp, p);
+    pexp_parts<HI_CLAMP>(u, tab, laneoff, c3, Tp, p);
     return Tp * p;
 }
 
 template <bool HI_CLAMP>
-__device__ __forceinline__ double pexp_acc(double u, const double* __restrict__ tabl, double acc) {
+__device__ __forceinline__ double pexp_acc(double u, const unsigned long long* __restrict__ tab,
+                                           unsigned laneoff, double c3, double acc) {
     double Tp, p;
-    pexp_parts<HI_CLAMP>(u, tabl, Tp, p);
+    pexp_parts<HI_CLAMP>(u, tab, laneoff, c3, Tp, p);
     return fma(Tp, p, acc);
+}
+
+// Keeps a constant in a register (opaque to constant propagation).
+__device__ __forceinline__ double reg_const(double v) {
+    asm volatile("" : "+d"(v));
+    return v;
 }
 
 // Atomic max/min on doubles (exact and order independent, hence deterministic).

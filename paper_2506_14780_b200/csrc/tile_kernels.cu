@@ -7,7 +7,7 @@
 //                 ctransform_of_g (core.cpp:56-82), plan marginals
 //                 (core.cpp:120-143), r = P~ beta (objective.cpp:127-128)
 //   MODE_MAX   partial[ib][o]      = max_{in} u        (exact shift, core.cpp:47)
-//   MODE_BLOCK partial[ib][c][o]   = sum_{in} 2^(u/64) W[in][c]
+//   MODE_BLOCK partial[ib][c][o]   = sum_{in} 2^(u/256) W[in][c]
 //              -> S = V^T P~ (objective.cpp:131), R~^T X / R~ Z for top_modes
 //                 (spectral.cpp:68-102)
 // "in" is the reduced index, "o" the output index; the column transform runs
@@ -29,27 +29,13 @@
 
 namespace sknr {
 
-__constant__ double c_exp2_tab[64] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284, 1.0442737824274138,
-    1.0556451783605572, 1.0671404006768237, 1.0787607977571199, 1.0905077326652577,
-    1.102382583307841, 1.1143867425958924, 1.1265216186082418, 1.1387886347566916,
-    1.1511892299529827, 1.1637248587775775, 1.1763969916502812, 1.189207115002721,
-    1.202156731452703, 1.215247359980469, 1.22848053610687, 1.241857812073484,
-    1.255380757024691, 1.2690509571917332, 1.2828700160787783, 1.2968395546510096,
-    1.3109612115247644, 1.3252366431597413, 1.339667524053303, 1.3542555469368927,
-    1.3690024229745905, 1.383909881963832, 1.3989796725383112, 1.4142135623730951,
-    1.42961333839197, 1.4451808069770467, 1.460917794180647, 1.4768261459394993,
-    1.4929077282912648, 1.5091644275934228, 1.5255981507445384, 1.5422108254079407,
-    1.559004400237837, 1.5759808451078865, 1.593142151342267, 1.6104903319492543,
-    1.6280274218573478, 1.645755478153965, 1.6636765803267364, 1.681792830507429,
-    1.7001063537185235, 1.718619298122478, 1.7373338352737062, 1.7562521603732995,
-    1.7753764925265212, 1.7947090750031072, 1.8142521755003989, 1.8340080864093424,
-    1.8539791250833855, 1.8741676341103, 1.8945759815869656, 1.9152065613971474,
-    1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+__constant__ unsigned long long c_exp2_tab[kTabEntries] = {
+#include "exp2_table.inc"
+};
 
-// Fill the replicated table: tab[e*16 + r] = 2^(e/64).
-__device__ __forceinline__ void load_exp2_table(double* tab, int tid, int nthreads) {
-    for (int t = tid; t < kTabDoubles; t += nthreads) tab[t] = c_exp2_tab[t >> 4];
+// Fill the replicated table: tab[e*16 + r] = mantissa bits of 2^(e/256).
+__device__ __forceinline__ void load_exp2_table(unsigned long long* tab, int tid, int nthreads) {
+    for (int t = tid; t < kTabWords; t += nthreads) tab[t] = c_exp2_tab[t >> 4];
 }
 
 namespace {
@@ -82,12 +68,13 @@ __global__ void __launch_bounds__(NT) pts_tile_kernel(TileArgs a) {
     constexpr int CH = Chunk<MODE, KT>::value;
     constexpr int KA = KT > 0 ? KT : 1;
     extern __shared__ __align__(16) double sm[];
-    double* tab = sm;
-    double* sin = sm + kTabDoubles;
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + kTabWords;
     double* sw = sin + CH * PK;
     const int tid = threadIdx.x;
     load_exp2_table(tab, tid, NT);
-    const double* tabl = tab + (tid & 15);
+    const unsigned laneoff = (tid & 15) << 3;
+    const double c3 = reg_const(kP3);
     const int64_t out_tile = static_cast<int64_t>(NT) * JT;
 
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -135,11 +122,11 @@ __global__ void __launch_bounds__(NT) pts_tile_kernel(TileArgs a) {
 #pragma unroll
                     for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
                     if (MODE == MODE_SUM) {
-                        acc[jt][0] = pexp_acc<false>(u, tabl, acc[jt][0]);
+                        acc[jt][0] = pexp_acc<false>(u, tab, laneoff, c3, acc[jt][0]);
                     } else if (MODE == MODE_MAX) {
                         acc[jt][0] = fmax(acc[jt][0], u);
                     } else {
-                        const double e = pexp<true>(u, tabl);
+                        const double e = pexp<true>(u, tab, laneoff, c3);
 #pragma unroll
                         for (int c = 0; c < KA; c += 2) {
                             const double2 w = reinterpret_cast<const double2*>(sw + k * KA)[c / 2];
@@ -171,12 +158,13 @@ __global__ void __launch_bounds__(NT) dense_tile_kernel(TileArgs a) {
     constexpr int KA = KT > 0 ? KT : 1;
     constexpr int U = 4;  // inputs per unrolled step: U*JT independent loads in flight
     extern __shared__ __align__(16) double sm[];
-    double* tab = sm;
-    double* sin = sm + kTabDoubles;
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + kTabWords;
     double* sw = sin + CH;
     const int tid = threadIdx.x;
     load_exp2_table(tab, tid, NT);
-    const double* tabl = tab + (tid & 15);
+    const unsigned laneoff = (tid & 15) << 3;
+    const double c3 = reg_const(kP3);
     const int64_t out_tile = static_cast<int64_t>(NT) * JT;
     const double nk = -a.kappa;
 
@@ -220,11 +208,11 @@ __global__ void __launch_bounds__(NT) dense_tile_kernel(TileArgs a) {
                     for (int jt = 0; jt < JT; ++jt) {
                         const double u = fma(nk, cv[q][jt], ak + B[jt]);
                         if (MODE == MODE_SUM) {
-                            acc[jt][0] = pexp_acc<false>(u, tabl, acc[jt][0]);
+                            acc[jt][0] = pexp_acc<false>(u, tab, laneoff, c3, acc[jt][0]);
                         } else if (MODE == MODE_MAX) {
                             acc[jt][0] = fmax(acc[jt][0], u);
                         } else {
-                            const double e = pexp<true>(u, tabl);
+                            const double e = pexp<true>(u, tab, laneoff, c3);
 #pragma unroll
                             for (int c = 0; c < KA; c += 2) {
                                 const double2 w =
@@ -242,11 +230,11 @@ __global__ void __launch_bounds__(NT) dense_tile_kernel(TileArgs a) {
                 for (int jt = 0; jt < JT; ++jt) {
                     const double u = fma(nk, __ldcs(Cb + k * a.ldc + oc[jt]), ak + B[jt]);
                     if (MODE == MODE_SUM) {
-                        acc[jt][0] = pexp_acc<false>(u, tabl, acc[jt][0]);
+                        acc[jt][0] = pexp_acc<false>(u, tab, laneoff, c3, acc[jt][0]);
                     } else if (MODE == MODE_MAX) {
                         acc[jt][0] = fmax(acc[jt][0], u);
                     } else {
-                        const double e = pexp<true>(u, tabl);
+                        const double e = pexp<true>(u, tab, laneoff, c3);
 #pragma unroll
                         for (int c = 0; c < KA; c += 2) {
                             const double2 w = reinterpret_cast<const double2*>(sw + k * KA)[c / 2];
@@ -285,7 +273,7 @@ KernelInfo make_pts() {
     k.jt = JT;
     constexpr int CH = Chunk<MODE, KT>::value;
     k.smem = static_cast<int>(sizeof(double)) *
-             (kTabDoubles + CH * PK_of<D>::value + (MODE == MODE_BLOCK ? CH * KT : 0));
+             (kTabWords + CH * PK_of<D>::value + (MODE == MODE_BLOCK ? CH * KT : 0));
     return k;
 }
 
@@ -295,7 +283,7 @@ KernelInfo make_dense() {
     k.fn = reinterpret_cast<const void*>(&dense_tile_kernel<JT, MODE, KT>);
     k.jt = JT;
     constexpr int CH = Chunk<MODE, KT>::value;
-    k.smem = static_cast<int>(sizeof(double)) * (kTabDoubles + CH + (MODE == MODE_BLOCK ? CH * KT : 0));
+    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + CH + (MODE == MODE_BLOCK ? CH * KT : 0));
     return k;
 }
 
