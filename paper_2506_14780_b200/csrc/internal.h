@@ -26,7 +26,7 @@ struct TileArgs {
 
 struct TilePlan {
     const void* fn = nullptr;
-    int grid = 0, smem = 0, occ = 0;
+    int grid = 0, smem = 0, occ = 0, nt = 128;
     int64_t out_tile = 0, in_block = 0, n_out_tiles = 0, n_in_blocks = 0, n_tiles = 0;
 };
 

@@ -40,7 +40,12 @@ __device__ __forceinline__ void load_exp2_table(unsigned long long* tab, int tid
 
 namespace {
 
-constexpr int NT = 128;  // threads per CTA
+// threads per CTA: 256 for the sum/max passes (the 32 KiB exp2 table is then
+// shared by 8 warps and 4 CTAs fit per SM), 128 for the register-heavy block passes
+template <int MODE>
+struct NT_of {
+    static constexpr int value = MODE == MODE_BLOCK ? 128 : 256;
+};
 
 template <int D>
 struct PK_of {
@@ -62,8 +67,9 @@ __device__ __forceinline__ void acc_init(double* acc) {
 
 // ------------------------------------------------------------- point clouds
 template <int D, int JT, int MODE, int KT>
-__global__ void __launch_bounds__(NT) pts_tile_kernel(TileArgs a) {
+__global__ void __launch_bounds__(NT_of<MODE>::value) pts_tile_kernel(TileArgs a) {
     if (guard_skip(a.st, a.guard)) return;
+    constexpr int NT = NT_of<MODE>::value;
     constexpr int PK = PK_of<D>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
     constexpr int KA = KT > 0 ? KT : 1;
@@ -152,8 +158,9 @@ __global__ void __launch_bounds__(NT) pts_tile_kernel(TileArgs a) {
 
 // ------------------------------------------------------------- stored cost
 template <int JT, int MODE, int KT>
-__global__ void __launch_bounds__(NT) dense_tile_kernel(TileArgs a) {
+__global__ void __launch_bounds__(NT_of<MODE>::value) dense_tile_kernel(TileArgs a) {
     if (guard_skip(a.st, a.guard)) return;
+    constexpr int NT = NT_of<MODE>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
     constexpr int KA = KT > 0 ? KT : 1;
     constexpr int U = 4;  // inputs per unrolled step: U*JT independent loads in flight
@@ -262,6 +269,7 @@ __global__ void __launch_bounds__(NT) dense_tile_kernel(TileArgs a) {
 struct KernelInfo {
     const void* fn = nullptr;
     int jt = 1;
+    int nt = 128;
     int smem = 0;
     int occ = 0;
 };
@@ -271,6 +279,7 @@ KernelInfo make_pts() {
     KernelInfo k;
     k.fn = reinterpret_cast<const void*>(&pts_tile_kernel<D, JT, MODE, KT>);
     k.jt = JT;
+    k.nt = NT_of<MODE>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
     k.smem = static_cast<int>(sizeof(double)) *
              (kTabWords + CH * PK_of<D>::value + (MODE == MODE_BLOCK ? CH * KT : 0));
@@ -282,6 +291,7 @@ KernelInfo make_dense() {
     KernelInfo k;
     k.fn = reinterpret_cast<const void*>(&dense_tile_kernel<JT, MODE, KT>);
     k.jt = JT;
+    k.nt = NT_of<MODE>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
     k.smem = static_cast<int>(sizeof(double)) * (kTabWords + CH + (MODE == MODE_BLOCK ? CH * KT : 0));
     return k;
@@ -356,10 +366,11 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     }
     cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ki.smem);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn, NT, ki.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn, ki.nt, ki.smem);
     if (occ < 1) occ = 1;
     const int64_t resident = static_cast<int64_t>(sm_count) * occ;
-    p.out_tile = NT * ki.jt;
+    p.out_tile = ki.nt * ki.jt;
+    p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     const int ch = chunk_inputs(mode, kt);
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
@@ -387,7 +398,7 @@ void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s) {
     a.in_block = p.in_block;
     void* args[] = {&a};
     count_launch();
-    cudaLaunchKernel(p.fn, dim3(p.grid), dim3(NT), args, p.smem, s);
+    cudaLaunchKernel(p.fn, dim3(p.grid), dim3(p.nt), args, p.smem, s);
 }
 
 }  // namespace sknr

@@ -192,9 +192,13 @@ def test_solve_c1_sknr_parity():
     # sides; a flipped decision moves f by one Newton step of the size of the
     # remaining error (~tol-level), which bounds agreement at ~1e-8 relative.
     assert rel_err(rg.f, ro["f"]) <= TOL_POT_NEWTON and rel_err(rg.g, ro["g"]) <= TOL_POT_NEWTON
-    acc_g = [t.newton_accepted for t in rg.trace]
-    acc_o = [bool(t[4]) for t in ro["trace"]]
-    assert sum(a != b for a, b in zip(acc_g, acc_o)) <= 2
+    # accept/reject may differ only in the tail where the whole iteration's
+    # gain in Q (sweep + Newton) is <= 1e-10 |Q|: there the Newton gain alone is
+    # below the ~1e-16 absolute rounding of Q (tools/diag_sknr.py trace)
+    qo = [t[2] for t in ro["trace"]]
+    for k, (tg, to) in enumerate(zip(rg.trace, ro["trace"])):
+        if tg.newton_accepted != bool(to[4]):
+            assert k > 0 and abs(qo[k] - qo[k - 1]) <= 1e-10 * abs(qo[k])
 
 
 def test_solve_dense_sknr_with_dense_basis():
