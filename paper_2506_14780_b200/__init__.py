@@ -102,8 +102,8 @@ _SIGS = {
     "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _I64, ctypes.c_int, _D,
                               ctypes.POINTER(_I64)],
     "sknr_bench_fp64_peak": [_D, _D],
-    "sknr_comm_unique_id": [ctypes.c_char_p],
-    "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
+    "sknr_comm_unique_id": [ctypes.c_void_p],
+    "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int],
     "sknr_comm_destroy": [],
     "sknr_problem_shard": [_P, _I64, _I64],
 }
@@ -589,6 +589,38 @@ def bench_iterations(problem: Problem, ell: int = 0, basis: Optional[SpectralBas
     return ms.value, int(kpi.value)
 
 
+# ---------------------------------------------------------------- row sharding (multi-GPU)
+def comm_unique_id() -> bytes:
+    """NCCL unique id (rank 0), to be shared with the other ranks out of band."""
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().sknr_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init(rank: int, world: int, uid: bytes, device: int = -1) -> None:
+    """One process per GPU: join the NCCL communicator used by sharded problems."""
+    if len(uid) != 128:
+        raise ValueError("comm_init: unique id must be 128 bytes")
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+    _check(lib().sknr_comm_init(int(rank), int(world), buf, int(device)))
+
+
+def comm_destroy() -> None:
+    _check(lib().sknr_comm_destroy())
+
+
+def row_partition(n: int, world: int, rank: int):
+    """Rows [n*r/R, n*(r+1)/R) of rank r (the partition sknr_problem_shard enforces)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def shard(problem: Problem, rank: int, world: int) -> None:
+    """Keep only this rank's source rows on the device (C ABI sknr_problem_shard).
+    Inputs and outputs of every call stay full length on every rank."""
+    b, e = row_partition(problem.n, world, rank)
+    _check(lib().sknr_problem_shard(problem.handle, b, e))
+
+
 def bench_fp64_peak():
     """(TFLOP/s, ms) of a DFMA-only kernel filling every SM: the measured FP64 ceiling."""
     t, ms = ctypes.c_double(), ctypes.c_double()
@@ -600,6 +632,7 @@ __all__ = [
     "EigensolverError", "IterationRecord", "PointProblem", "Problem", "SolveResult", "SpectralBasis",
     "__version__", "anneal", "apply_sym_block", "apply_sym_t_block", "coupling", "ctransform_of_f",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
-    "plan_marginals", "restricted_derivatives", "semi_dual_gradient", "semi_dual_value", "solve",
+    "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
+    "row_partition", "shard", "semi_dual_gradient", "semi_dual_value", "solve",
     "top_modes", "version",
 ]

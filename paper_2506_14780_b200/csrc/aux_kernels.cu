@@ -79,6 +79,12 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
             mx = fmax(mx, a.part[2 * b]);
             mn = fmin(mn, a.part[2 * b + 1]);
         }
+        if (a.defer) {  // sharded: decided by k_decide after the cross-rank max
+            a.st->scratch[2 * a.dir] = mx;
+            a.st->scratch[2 * a.dir + 1] = -mn;
+            a.st->counters[a.dir] = 0u;
+            return;
+        }
         a.st->dmax[a.dir] = mx;
         a.st->dmin[a.dir] = mn;
         const bool ok = a.st->ref_valid[a.dir] && (mx - mn) * a.inv_eps <= a.exact_spread &&
@@ -271,6 +277,31 @@ int reduce_blocks(int64_t T) {
     return static_cast<int>(b);
 }
 
+// r layout (EPI_CHECK): |row-a|^2, a.f, max|row-a|, |col-b|^2, max|col-b|, b.h
+__device__ void run_epilogue(DevState* st, int epilogue, int newton, const double* r) {
+    if (epilogue == EPI_GAUGE) {
+        st->c_gauge = r[0];
+    } else if (epilogue == EPI_CHECK) {
+        // marginal_gap (core.cpp:145-150) and Q0 = a.f + b.h; stopping test (solver.cpp:123)
+        if (st->done) return;
+        st->gap_l2 = sqrt(r[0]) + sqrt(r[3]);
+        st->gap_inf = r[2] + r[4];
+        st->q0 = r[1] + r[5];
+        if (st->gap_l2 < st->tol) {
+            st->conv = 1;
+            st->done = 1;
+        } else if (newton) {
+            st->newton_ok = 1;
+            st->attempted = 1;
+        }
+    } else if (epilogue == EPI_ACCEPT) {
+        // Q1 = a.f' + b.h'; accept iff Q1 > Q0 (solver.cpp:46-47)
+        if (st->done || !st->newton_ok) return;
+        st->q1 = r[0] + r[1];
+        st->accept = st->q1 > st->q0 ? 1 : 0;
+    }
+}
+
 __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
     if (guard_skip(a.st, a.guard)) return;
     __shared__ double sh[RED_MAX_TERMS][AUX_NT / 32];
@@ -319,7 +350,7 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
     __syncthreads();
     if (!is_last || threadIdx.x != 0) return;
     __threadfence();
-    double r[RED_MAX_TERMS];
+    double r[RED_MAX_TERMS] = {};
     for (int t = 0; t < a.nterms; ++t) {
         double v = a.part[t];
         for (unsigned b = 1; b < gridDim.x; ++b) {
@@ -330,28 +361,36 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
         a.out[t] = v;
     }
     *a.counter = 0u;
-    DevState* st = a.st;
-    if (a.epilogue == EPI_GAUGE) {
-        st->c_gauge = r[0];
-    } else if (a.epilogue == EPI_CHECK) {
-        // r: |row-a|^2, max|row-a|, a.f, |col-b|^2, max|col-b|, b.h  (core.cpp:145-150)
-        if (st->done) return;
-        st->gap_l2 = sqrt(r[0]) + sqrt(r[3]);
-        st->gap_inf = r[1] + r[4];
-        st->q0 = r[2] + r[5];
-        if (st->gap_l2 < st->tol) {
-            st->conv = 1;
-            st->done = 1;
-        } else if (a.newton) {
-            st->newton_ok = 1;
-            st->attempted = 1;
-        }
-    } else if (a.epilogue == EPI_ACCEPT) {
-        // Q1 = a.f' + b.h'; accept iff Q1 > Q0 (solver.cpp:46-47)
-        if (st->done || !st->newton_ok) return;
-        st->q1 = r[0] + r[1];
-        st->accept = st->q1 > st->q0 ? 1 : 0;
+    run_epilogue(a.st, a.epilogue, a.newton, r);
+}
+
+__global__ void k_epilogue(DevState* st, int epilogue, int newton, const double* r, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    if (threadIdx.x == 0 && blockIdx.x == 0) run_epilogue(st, epilogue, newton, r);
+}
+
+// max over split-K partials (sharded column LSE: local part before allreduce)
+__global__ void __launch_bounds__(AUX_NT) k_max_local(const double* partial, int64_t nb, int64_t n_out,
+                                                      double* out, DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < n_out;
+         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double M = -kInf;
+        for (int64_t b = 0; b < nb; ++b) M = fmax(M, partial[b * n_out + o]);
+        out[o] = M;
     }
+}
+
+// exact-path decision after the cross-rank max of (dmax, -dmin) (sharded prep_in)
+__global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double mx = st->scratch[2 * dir], mn = -st->scratch[2 * dir + 1];
+    st->dmax[dir] = mx;
+    st->dmin[dir] = mn;
+    const bool ok = st->ref_valid[dir] && (mx - mn) * inv_eps <= spread && isfinite(mx) && isfinite(mn);
+    st->need_exact[dir] = ok ? 0 : 1;
+    st->retry[dir] = 0;
 }
 
 }  // namespace sknr

@@ -26,6 +26,7 @@ struct PrepInArgs {
     int dir = 0;
     double* part = nullptr;       // 2*gridDim doubles
     double exact_spread = 600.0;  // (max-min)(v-ref)/eps above which the exact path is forced
+    int defer = 0;                // sharded: leave the decision to k_decide
     DevState* st = nullptr;
     unsigned guard = 0;
 };
@@ -126,6 +127,10 @@ struct RedArgs {
     unsigned guard = 0;
 };
 __global__ void k_reduce(RedArgs a);
+__global__ void k_epilogue(DevState* st, int epilogue, int newton, const double* r, unsigned guard);
+__global__ void k_max_local(const double* partial, int64_t nb, int64_t n_out, double* out, DevState* st,
+                            unsigned guard);
+__global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, unsigned guard);
 int reduce_blocks(int64_t T);
 
 }  // namespace sknr

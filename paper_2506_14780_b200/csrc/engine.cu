@@ -29,6 +29,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>  // types only; entry points are resolved with dlopen/dlsym
+
 #include "../../include/sknr_gpu.h"
 #include "aux_kernels.cuh"
 
@@ -56,6 +58,70 @@ struct RuntimeFailure : std::runtime_error {
             throw CudaFailure(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
                               __FILE__ + ":" + std::to_string(__LINE__));                     \
     } while (0)
+
+struct NcclFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// ============================================================ NCCL (row sharding)
+// Loaded lazily with dlopen so the library never pins a second libnccl next to
+// the one torch already mapped (RTLD_NOLOAD first).
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    void load() {
+        if (lib) return;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) throw NcclFailure(std::string("sknr: cannot load libnccl.so.2: ") + dlerror());
+        auto sym = [&](const char* name) {
+            void* p = dlsym(lib, name);
+            if (!p) throw NcclFailure(std::string("sknr: NCCL symbol missing: ") + name);
+            return p;
+        };
+        GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(sym("ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
+        AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
+        Broadcast = reinterpret_cast<decltype(Broadcast)>(sym("ncclBroadcast"));
+        GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
+        GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
+        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
+        GetErrorString = reinterpret_cast<decltype(GetErrorString)>(sym("ncclGetErrorString"));
+    }
+};
+
+static NcclApi g_nccl;
+
+struct Comm {
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+};
+static Comm g_comm;
+
+#define NK(x)                                                                                      \
+    do {                                                                                           \
+        ncclResult_t r_ = (x);                                                                     \
+        if (r_ != ncclSuccess)                                                                     \
+            throw NcclFailure(std::string("NCCL error: ") + g_nccl.GetErrorString(r_) + " at " + \
+                              __FILE__ + ":" + std::to_string(__LINE__));                         \
+    } while (0)
+
+// Standard contiguous row partition of n rows over `world` ranks.
+static void row_partition(int64_t n, int world, int rank, int64_t& begin, int64_t& end) {
+    begin = n * rank / world;
+    end = n * (rank + 1) / world;
+}
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -350,6 +416,12 @@ __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int tr
     if (k >= st->max_iter) st->done = 1;
 }
 
+__global__ void k_axpby(const double* x, const double* y, int64_t n, double a, double b, double* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = a * x[i] + b * y[i];
+}
+
 // ---- top_modes helpers
 // Y[:,c] -= u0 * s_c
 __global__ void k_deflate(double* Y, int64_t n, int k, const double* u0, const double* s) {
@@ -622,6 +694,12 @@ struct Problem {
 
     std::map<std::tuple<int, int, int, int64_t>, TilePlan> plans;
 
+    // row sharding: this handle holds source rows [row_begin, row_begin + n)
+    bool shard = false;
+    int64_t n_global = 0, row_begin = 0;
+    DBuf red_tmp, gather_buf;
+    std::vector<double> h_alpha, h_beta;  // full host copies (validation, host-side dots)
+
     bool otf() const { return dim > 0; }  // on-the-fly cost (points, d <= 4)
     double inv_eps() const { return 1.0 / eps; }
     double kc() const { return otf() ? kappa / eps : 0.0; }
@@ -685,6 +763,7 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     check_device();
     std::unique_ptr<Problem> p(new Problem());
     p->n = n;
+    p->n_global = n;
     p->m = m;
     p->eps = eps;
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
@@ -700,6 +779,9 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
         p->shift[dir].ensure(nout);
     }
     p->stats.ensure(2 * 148 * 8);
+    p->red_tmp.ensure(std::max(n, m));
+    p->h_alpha.assign(alpha, alpha + n);
+    p->h_beta.assign(beta, beta + m);
     p->gram_part.ensure(148 * 64 * 64 + 64);
     p->sums.ensure(64);
     return p.release();
@@ -785,6 +867,38 @@ static void finish_dense(Problem* p, const double* cost) {
     CK(cudaStreamSynchronize(p->stream));
 }
 
+// ============================================================ collectives
+// In-place allreduce on the problem's stream; a no-op unless the handle is row-sharded.
+static void allreduce(Problem& P, double* buf, size_t count, ncclRedOp_t op) {
+    if (!P.shard || count == 0) return;
+    NK(g_nccl.AllReduce(buf, buf, count, ncclDouble, op, g_comm.comm, P.stream));
+}
+
+// Upload the local row block of a full-length, `cols`-column column-major host array.
+static void upload_rows(Problem& P, double* dev, const double* host_full, int64_t cols = 1) {
+    for (int64_t c = 0; c < cols; ++c)
+        upload(dev + c * P.n, host_full + c * P.n_global + P.row_begin, P.n, P.stream);
+}
+
+// All-gather the local row block of a device vector into a full host vector.
+static void gather_rows(Problem& P, const double* dev_local, double* host_full) {
+    if (!P.shard) {
+        download(host_full, dev_local, P.n, P.stream);
+        CK(cudaStreamSynchronize(P.stream));
+        return;
+    }
+    P.gather_buf.ensure(P.n_global);
+    NK(g_nccl.GroupStart());
+    for (int r = 0; r < g_comm.world; ++r) {
+        int64_t b, e;
+        row_partition(P.n_global, g_comm.world, r, b, e);
+        NK(g_nccl.Broadcast(dev_local, P.gather_buf.p + b, e - b, ncclDouble, r, g_comm.comm, P.stream));
+    }
+    NK(g_nccl.GroupEnd());
+    download(host_full, P.gather_buf.p, P.n_global, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+}
+
 // ============================================================ passes
 static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_blocks = 0) {
     const int64_t nout = dir == 0 ? P.m : P.n, nin = dir == 0 ? P.n : P.m;
@@ -846,9 +960,16 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     pi.part = P.stats.p;
     pi.st = P.st;
     pi.guard = guard;
+    const bool split = P.shard && dir == 0;  // column transform reduces over sharded rows
+    pi.defer = split ? 1 : 0;
     const int gin = std::min(grid_for(nin), 148 * 8);
     count_launch();
     k_prep_in<<<gin, AUX_NT, 0, s>>>(pi);
+    if (split) {
+        allreduce(P, &P.st->scratch[2 * dir], 2, ncclMax);  // (max df, -min df) over all rows
+        count_launch();
+        k_decide<<<1, 32, 0, s>>>(P.st, dir, P.inv_eps(), pi.exact_spread, guard);
+    }
 
     PrepOutArgs po;
     po.count = nout;
@@ -887,14 +1008,32 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         const unsigned gmax = guard | (phase == 0 ? exact_bit(dir) : retry_bit(dir));
         const unsigned gsum = guard | (phase == 0 ? 0u : retry_bit(dir));
         launch_tiles(tmax, tile_args(P, dir, tmax, gmax), s);
+        fa.partial = P.partial.p;
         fa.nb = tmax.n_in_blocks;
         fa.guard = gmax;
+        if (split) {  // local column maxima -> max over ranks -> shift
+            count_launch();
+            k_max_local<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tmax.n_in_blocks, nout, P.red_tmp.p,
+                                                         P.st, gmax);
+            allreduce(P, P.red_tmp.p, nout, ncclMax);
+            fa.partial = P.red_tmp.p;
+            fa.nb = 1;
+        }
         count_launch();
         k_max_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
         launch_tiles(tsum, tile_args(P, dir, tsum, gsum), s);
+        fa.partial = P.partial.p;
         fa.nb = tsum.n_in_blocks;
         fa.guard = gsum;
         fa.retry_phase = phase;
+        if (split) {  // local column sums share one shift per column: plain sum over ranks
+            count_launch();
+            k_sum_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tsum.n_in_blocks, nout, nullptr,
+                                                            P.red_tmp.p, P.st, gsum);
+            allreduce(P, P.red_tmp.p, nout, ncclSum);
+            fa.partial = P.red_tmp.p;
+            fa.nb = 1;
+        }
         count_launch();
         k_lse_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
     }
@@ -974,6 +1113,8 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
         k_block_finalize<<<grid_for(nout * ps.k), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, ps.kt,
                                                                   ps.k, nout, ps.out_scale, ps.out, nout,
                                                                   P.st, ps.guard);
+    if (ps.dir == 0)  // column direction reduces over the sharded rows
+        allreduce(P, ps.out, static_cast<size_t>(nout) * (mode == MODE_SUM ? 1 : ps.k), ncclSum);
     CK(cudaGetLastError());
 }
 
@@ -1274,11 +1415,16 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         ra.out = P.sums.p + 8;
         ra.part = P.gram_part.p;
         ra.counter = &P.st->counters[6];
-        ra.epilogue = EPI_GAUGE;
+        ra.epilogue = P.shard ? EPI_NONE : EPI_GAUGE;
         ra.st = P.st;
         ra.guard = G_DONE;
         count_launch();
         k_reduce<<<reduce_blocks(n), AUX_NT, 0, s>>>(ra);
+        if (P.shard) {
+            allreduce(P, P.sums.p + 8, 1, ncclSum);
+            count_launch();
+            k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_GAUGE, 0, P.sums.p + 8, G_DONE);
+        }
     }
     count_launch();
     k_gauge_apply<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, S.g.p, m,
@@ -1295,9 +1441,10 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         ra.T[0] = n;
         ra.T[1] = m;
         ra.nterms = 6;
-        const double* xs[6] = {S.rowres.p, S.rowres.p, P.src.w.p, S.colres.p, S.colres.p, P.tgt.w.p};
-        const double* ys[6] = {nullptr, nullptr, S.f.p, nullptr, nullptr, S.h.p};
-        const int ops[6] = {RED_SQ, RED_MAXABS, RED_DOT, RED_SQ, RED_MAXABS, RED_DOT};
+        // layout: |row-a|^2, a.f, max|row-a| (sharded rows) | |col-b|^2, max|col-b|, b.h
+        const double* xs[6] = {S.rowres.p, P.src.w.p, S.rowres.p, S.colres.p, S.colres.p, P.tgt.w.p};
+        const double* ys[6] = {nullptr, S.f.p, nullptr, nullptr, nullptr, S.h.p};
+        const int ops[6] = {RED_SQ, RED_DOT, RED_MAXABS, RED_SQ, RED_MAXABS, RED_DOT};
         for (int t = 0; t < 6; ++t) {
             ra.x[t] = xs[t];
             ra.y[t] = ys[t];
@@ -1307,12 +1454,18 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         ra.out = sums;
         ra.part = P.gram_part.p;
         ra.counter = &P.st->counters[6];
-        ra.epilogue = EPI_CHECK;
+        ra.epilogue = P.shard ? EPI_NONE : EPI_CHECK;
         ra.newton = newton ? 1 : 0;
         ra.st = P.st;
         ra.guard = G_DONE;
         count_launch();
         k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
+        if (P.shard) {
+            allreduce(P, sums, 2, ncclSum);
+            allreduce(P, sums + 2, 1, ncclMax);
+            count_launch();
+            k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_CHECK, newton ? 1 : 0, sums, G_DONE);
+        }
     }
     if (newton) {
         const unsigned gn = G_DONE | G_NEWTON;
@@ -1334,12 +1487,15 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         sp.out = S.S.p;
         sp.guard = gn;
         plan_pass(P, sp);
+        allreduce(P, S.S.p, static_cast<size_t>(m) * l, ncclSum);  // S = V^T P~ summed over row shards
         double* G1 = S.G.p;
         double* cross = G1 + l * l;
         double* grad = cross + l * l;
         gram(P, n, l, l, S.V.p, n, S.V.p, n, S.r.p, G1, gn);
         gram(P, m, l, l, S.S.p, m, S.S.p, m, P.tgt.w.p, cross, gn);
         gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
+        allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
+        allreduce(P, grad, l, ncclSum);
         count_launch();
         k_newton_solve<<<1, 64, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
                                                             P.st, gn);
@@ -1360,11 +1516,16 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             ra.out = sums + 6;
             ra.part = P.gram_part.p;
             ra.counter = &P.st->counters[6];
-            ra.epilogue = EPI_ACCEPT;
+            ra.epilogue = P.shard ? EPI_NONE : EPI_ACCEPT;
             ra.st = P.st;
             ra.guard = gn;
             count_launch();
             k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
+            if (P.shard) {
+                allreduce(P, sums + 6, 1, ncclSum);
+                count_launch();
+                k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_ACCEPT, 0, sums + 6, gn);
+            }
         }
         count_launch();
         k_select<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, S.fcand.p, n, S.gnext.p, S.h.p, S.hcand.p, m,
@@ -1402,7 +1563,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         S.V.ensure(n * ell);
         S.Wv.ensure(n * kt);
         S.S.ensure(m * ell);
-        upload(S.V.p, basis_host, n * ell, s);
+        upload_rows(P, S.V.p, basis_host, ell);
         count_launch();
         k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,
                                                      S.Wv.p);
@@ -1414,7 +1575,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
     plan_for(P, 0, MODE_MAX, 0);
     plan_for(P, 1, MODE_MAX, 0);
     if (init_f)
-        upload(S.f.p, init_f, n, s);
+        upload_rows(P, S.f.p, init_f);
     else {
         count_launch();
         k_fill<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, n, 0.0);
@@ -1462,9 +1623,9 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
     SolveOut out;
-    out.f.resize(P.n);
+    out.f.resize(P.n_global);
     out.g.resize(P.m);
-    download(out.f.data(), S.f.p, P.n, s);
+    gather_rows(P, S.f.p, out.f.data());
     download(out.g.data(), S.g.p, P.m, s);
     CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1512,6 +1673,10 @@ static thread_local double g_best_residual = 0.0;
     catch (const RuntimeFailure& e) {       \
         g_err = e.what();                   \
         return SKNR_ERUNTIME;               \
+    }                                       \
+    catch (const NcclFailure& e) {          \
+        g_err = e.what();                   \
+        return SKNR_ENCCL;                  \
     }                                       \
     catch (const std::exception& e) {       \
         g_err = e.what();                   \
@@ -1627,11 +1792,11 @@ int sknr_ctransform_of_f(sknr_problem h, const double* f, double* g) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n, "ctransform_of_f");
+    check_finite_vec(f, P.n_global, "ctransform_of_f");
     DBuf df, dg;
     df.ensure(P.n);
     dg.ensure(P.m);
-    upload(df.p, f, P.n, P.stream);
+    upload_rows(P, df.p, f);
     reset_for_primitive(P);
     plan_for(P, 0, MODE_SUM, 0);
     plan_for(P, 0, MODE_MAX, 0);
@@ -1652,8 +1817,7 @@ int sknr_ctransform_of_g(sknr_problem h, const double* g, double* f) {
     upload(dg.p, g, P.m, P.stream);
     reset_for_primitive(P);
     lse(P, 1, dg.p, df.p, G_NONE);
-    download(f, df.p, P.n, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
+    gather_rows(P, df.p, f);
     SKNR_API_END
 }
 
@@ -1662,14 +1826,14 @@ int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n, "plan_marginals(f)");
+    check_finite_vec(f, P.n_global, "plan_marginals(f)");
     check_finite_vec(g, P.m, "plan_marginals(g)");
     DBuf df, dg, dr, dc;
     df.ensure(P.n);
     dg.ensure(P.m);
     dr.ensure(P.n);
     dc.ensure(P.m);
-    upload(df.p, f, P.n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, P.m, P.stream);
     // row_i = sum_j a_i b_j e^{..}: dir 1 (out i), column sums: dir 0 (out j)
     PassSpec pr;
@@ -1688,14 +1852,14 @@ int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double
     pc.out_lw = P.tgt.lw.p;
     pc.out = dc.p;
     plan_pass(P, pc);
-    std::vector<double> hr(P.n), hc(P.m), ha(P.n), hb(P.m);
-    download(hr.data(), dr.p, P.n, P.stream);
+    std::vector<double> hr(P.n_global), hc(P.m);
+    gather_rows(P, dr.p, hr.data());
     download(hc.data(), dc.p, P.m, P.stream);
-    download(ha.data(), P.src.w.p, P.n, P.stream);
-    download(hb.data(), P.tgt.w.p, P.m, P.stream);
     CK(cudaStreamSynchronize(P.stream));
+    const std::vector<double>& ha = P.h_alpha;
+    const std::vector<double>& hb = P.h_beta;
     double sr = 0, sc = 0, mr = 0, mc = 0;
-    for (int64_t i = 0; i < P.n; ++i) {
+    for (int64_t i = 0; i < P.n_global; ++i) {
         const double d = hr[i] - ha[i];
         sr += d * d;
         mr = std::max(mr, std::abs(d));
@@ -1705,7 +1869,7 @@ int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double
         sc += d * d;
         mc = std::max(mc, std::abs(d));
     }
-    if (row) std::memcpy(row, hr.data(), sizeof(double) * P.n);
+    if (row) std::memcpy(row, hr.data(), sizeof(double) * P.n_global);
     if (col) std::memcpy(col, hc.data(), sizeof(double) * P.m);
     if (gap_l2) *gap_l2 = std::sqrt(sr) + std::sqrt(sc);
     if (gap_inf) *gap_inf = mr + mc;
@@ -1716,6 +1880,7 @@ int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
+    if (P.shard) throw RuntimeFailure("coupling_from: not available on a row-sharded problem");
     check_finite_vec(f, P.n, "coupling_from(f)");
     check_finite_vec(g, P.m, "coupling_from(g)");
     DBuf df, dg, dp, x, y;
@@ -1735,16 +1900,14 @@ int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan
 
 int sknr_semi_dual_value(sknr_problem h, const double* f, double* value) {
     SKNR_API_BEGIN
-    std::vector<double> g(get(h).m);
+    std::vector<double> g(get(h).m);  // f^{C,eps}, then Q = a.f + b.g (objective.cpp:42-45)
     int rc = sknr_ctransform_of_f(h, f, g.data());
     if (rc != SKNR_OK) return rc;
     Problem& P = get(h);
-    std::vector<double> a(P.n), b(P.m);
-    download(a.data(), P.src.w.p, P.n, P.stream);
-    download(b.data(), P.tgt.w.p, P.m, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
+    const std::vector<double>& a = P.h_alpha;
+    const std::vector<double>& b = P.h_beta;
     double s1 = 0, s2 = 0;
-    for (int64_t i = 0; i < P.n; ++i) s1 += a[i] * f[i];
+    for (int64_t i = 0; i < P.n_global; ++i) s1 += a[i] * f[i];
     for (int64_t j = 0; j < P.m; ++j) s2 += b[j] * g[j];
     *value = s1 + s2;
     SKNR_API_END
@@ -1757,7 +1920,7 @@ int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g
     std::lock_guard<std::mutex> lk(P.mu);
     if (ell < 1) throw InvalidArgument("restricted_derivatives: empty basis");
     if (ell > 64) throw InvalidArgument("restricted_derivatives: ell > 64 is not supported by sknr_b200");
-    check_finite_vec(f, P.n, "restricted_derivatives(f)");
+    check_finite_vec(f, P.n_global, "restricted_derivatives(f)");
     check_finite_vec(g, P.m, "restricted_derivatives(g)");
     const int64_t n = P.n, m = P.m;
     const int l = static_cast<int>(ell), kt = block_kt_for(l);
@@ -1770,9 +1933,9 @@ int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g
     am.ensure(n);
     r.ensure(n);
     G.ensure(3 * 64 * 64);
-    upload(df.p, f, n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, m, P.stream);
-    upload(V.p, vectors, n * ell, P.stream);
+    upload_rows(P, V.p, vectors, ell);
     count_launch();
     k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(V.p, n, n, l, kt, nullptr, Wv.p);
     // r_i = a_i sum_j b_j e^{(f_i+g_j-C_ij)/eps} (objective.cpp:127-128) as a plan-sum pass
@@ -1795,18 +1958,16 @@ int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g
     sp.out = Sm.p;
     plan_pass(P, sp);
     // am = a - r
-    std::vector<double> hr(n), ha(n);
-    download(hr.data(), r.p, n, P.stream);
-    download(ha.data(), P.src.w.p, n, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
-    for (int64_t i = 0; i < n; ++i) ha[i] -= hr[i];
-    upload(am.p, ha.data(), n, P.stream);
+    count_launch();
+    k_axpby<<<grid_for(n), AUX_NT, 0, P.stream>>>(P.src.w.p, r.p, n, 1.0, -1.0, am.p);
     double* G1 = G.p;
     double* cross = G1 + l * l;
     double* gr = cross + l * l;
     gram(P, n, l, l, V.p, n, V.p, n, r.p, G1, 0);
     gram(P, m, l, l, Sm.p, m, Sm.p, m, P.tgt.w.p, cross, 0);
     gram(P, n, l, 1, V.p, n, am.p, n, nullptr, gr, 0);
+    allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
+    allreduce(P, gr, l, ncclSum);
     std::vector<double> hG1(l * l), hC(l * l);
     download(hG1.data(), G1, l * l, P.stream);
     download(hC.data(), cross, l * l, P.stream);
@@ -1834,9 +1995,9 @@ int sknr_apply_sym_t_block(sknr_problem h, const double* f, const double* g, con
     U.ensure(n * k);
     W.ensure(n * kt);
     O.ensure(m * k);
-    upload(df.p, f, n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, m, P.stream);
-    upload(U.p, u, n * k, P.stream);
+    upload_rows(P, U.p, u, k);
     count_launch();
     k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(U.p, n, n, static_cast<int>(k), kt, nullptr, W.p);
     PassSpec zt;
@@ -1869,7 +2030,7 @@ int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const
     Vv.ensure(m * k);
     W.ensure(m * kt);
     O.ensure(n * k);
-    upload(df.p, f, n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, m, P.stream);
     upload(Vv.p, v, m * k, P.stream);
     count_launch();
@@ -1885,8 +2046,7 @@ int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const
     yr.kt = kt;
     yr.out = O.p;
     plan_pass(P, yr);
-    download(out, O.p, n * k, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
+    for (int64_t c = 0; c < k; ++c) gather_rows(P, O.p + c * n, out + c * P.n_global);
     SKNR_API_END
 }
 
@@ -1896,6 +2056,7 @@ int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
+    if (P.shard) throw RuntimeFailure("top_modes: not yet available on a row-sharded problem");
     check_finite_vec(f, P.n, "SinkhornOperator(f)");
     check_finite_vec(g, P.m, "SinkhornOperator(g)");
     DBuf df, dg;
@@ -1936,7 +2097,7 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     const int64_t ell = use_newton ? cfg->ell : 0;
     SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
                            std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1));
-    std::memcpy(f_out, o.f.data(), sizeof(double) * P.n);
+    std::memcpy(f_out, o.f.data(), sizeof(double) * P.n_global);
     std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
     if (iterations) *iterations = o.iterations;
     if (converged) *converged = o.converged ? 1 : 0;
@@ -1960,7 +2121,9 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
     if (!(cfg->tol_omega > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
     if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     const double eps0 = P.eps;
-    const int64_t n = P.n, m = P.m;
+    const int64_t n = P.n_global, m = P.m;
+    if (P.shard && warm_mode == 2 && cfg->ell > 0)
+        throw RuntimeFailure("anneal: spectral warm start not yet available on a row-sharded problem");
     int64_t tl = 0;
     Basis basis;
     bool have_basis = false;
@@ -2197,29 +2360,94 @@ int sknr_bench_fp64_peak(double* tflops, double* ms) {
 // ---------------------------------------------------------------- multi-GPU (row sharding)
 int sknr_comm_unique_id(unsigned char id[128]) {
     SKNR_API_BEGIN
-    (void)id;
-    throw RuntimeFailure("sknr_comm_unique_id: multi-GPU row sharding is not enabled in this build");
+    g_nccl.load();
+    ncclUniqueId uid;
+    NK(g_nccl.GetUniqueId(&uid));
+    std::memcpy(id, uid.internal, NCCL_UNIQUE_ID_BYTES);
     SKNR_API_END
 }
 
 int sknr_comm_init(int rank, int world, const unsigned char id[128], int device) {
     SKNR_API_BEGIN
-    (void)rank;
-    (void)world;
-    (void)id;
-    (void)device;
-    throw RuntimeFailure("sknr_comm_init: multi-GPU row sharding is not enabled in this build");
+    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("sknr_comm_init: bad rank/world");
+    check_device();
+    if (device >= 0) CK(cudaSetDevice(device));
+    g_nccl.load();
+    if (g_comm.comm) {
+        g_nccl.CommDestroy(g_comm.comm);
+        g_comm.comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+    NK(g_nccl.CommInitRank(&g_comm.comm, world, uid, rank));
+    g_comm.rank = rank;
+    g_comm.world = world;
     SKNR_API_END
 }
 
-int sknr_comm_destroy(void) { return SKNR_OK; }
+int sknr_comm_destroy(void) {
+    SKNR_API_BEGIN
+    if (g_comm.comm) {
+        g_nccl.CommDestroy(g_comm.comm);
+        g_comm.comm = nullptr;
+    }
+    g_comm.world = 1;
+    g_comm.rank = 0;
+    SKNR_API_END
+}
 
+// Keep only this rank's source rows; column partials, the gauge scalar, the
+// marginal residuals and the Newton inner products are merged with NCCL.
 int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
     SKNR_API_BEGIN
-    (void)h;
-    (void)row_begin;
-    (void)row_end;
-    throw RuntimeFailure("sknr_problem_shard: multi-GPU row sharding is not enabled in this build");
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (!g_comm.comm) throw RuntimeFailure("sknr_problem_shard: call sknr_comm_init first");
+    if (P.shard) throw InvalidArgument("sknr_problem_shard: problem already sharded");
+    int64_t b, e;
+    row_partition(P.n_global, g_comm.world, g_comm.rank, b, e);
+    if (row_begin != b || row_end != e)
+        throw InvalidArgument("sknr_problem_shard: rows must follow the standard partition [n*r/R, n*(r+1)/R)");
+    const int64_t nl = e - b, n = P.n_global, m = P.m;
+    if (nl < 1) throw InvalidArgument("sknr_problem_shard: empty row block");
+    cudaStream_t s = P.stream;
+    auto slice = [&](DBuf& buf, int64_t cols) {
+        if (!buf.p) return;
+        DBuf tmp;
+        tmp.ensure(nl * cols);
+        for (int64_t c = 0; c < cols; ++c)
+            CK(cudaMemcpyAsync(tmp.p + c * nl, buf.p + c * n + b, sizeof(double) * nl, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        std::swap(buf.p, tmp.p);
+        std::swap(buf.n, tmp.n);
+    };
+    slice(P.src.w, 1);
+    slice(P.src.lw, 1);
+    slice(P.src.sw, 1);
+    slice(P.src.lsw, 1);
+    slice(P.src.sq, 1);
+    slice(P.src.coords, P.d);
+    if (P.C.p) {
+        DBuf c2, ct2;
+        c2.ensure(nl * m);
+        ct2.ensure(nl * m);
+        CK(cudaMemcpy2DAsync(c2.p, sizeof(double) * nl, P.C.p + b, sizeof(double) * n, sizeof(double) * nl, m,
+                             cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ct2.p, P.CT.p + b * m, sizeof(double) * nl * m, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        std::swap(P.C.p, c2.p);
+        std::swap(P.C.n, c2.n);
+        std::swap(P.CT.p, ct2.p);
+        std::swap(P.CT.n, ct2.n);
+    }
+    P.src.count = nl;
+    P.n = nl;
+    P.row_begin = b;
+    P.shard = true;
+    P.plans.clear();
+    count_launch();
+    k_invalidate_refs<<<1, 32, 0, s>>>(P.st);
+    CK(cudaStreamSynchronize(s));
     SKNR_API_END
 }
 

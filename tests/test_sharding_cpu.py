@@ -1,0 +1,88 @@
+"""Row sharding on CPU (gloo, world size 2): the merge the GPU path performs
+across ranks -- per-column partial sums under one shared shift, allreduced --
+reproduces the unsharded column transform, and the row transform is local.
+Uses the oracle on each rank's row block as the per-rank compute."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_ref as O
+from paper_2506_14780_b200 import generators as G
+from paper_2506_14780_b200 import row_partition
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _column_partials(x, y, a, f, eps, shift):
+    """S_j = sum_i a_i exp((f_i - C_ij)/eps - shift_j) over this rank's rows."""
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    return np.exp(np.log(a)[:, None] + (f[:, None] - C) / eps - shift[None, :]).sum(0)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = G.config("C1", n=96, m=80)
+    eps = 0.05
+    f = np.linspace(-0.1, 0.1, inst.n)
+    b0, b1 = row_partition(inst.n, world, rank)
+    xs, as_, fs = inst.x[b0:b1], inst.alpha[b0:b1], f[b0:b1]
+    # shift = global upper bound: the max over ranks of the local max exponent
+    C = ((xs[:, None, :] - inst.y[None, :, :]) ** 2).sum(-1)
+    local_max = (np.log(as_)[:, None] + (fs[:, None] - C) / eps).max(0)
+    t = torch.from_numpy(local_max.copy())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    shift = t.numpy()
+    S = torch.from_numpy(_column_partials(xs, inst.y, as_, fs, eps, shift))
+    dist.all_reduce(S, op=dist.ReduceOp.SUM)
+    g = -eps * (shift + np.log(S.numpy()))
+    # row transform of the local block is independent of the other ranks
+    P = O.Instance(as_ / as_.sum(), inst.beta, eps, x=xs, y=inst.y)
+    f_local = O.ctransform_of_g(P, g)
+    gathered = [torch.zeros(n, dtype=torch.float64) for n in [row_partition(inst.n, world, r)[1] - row_partition(inst.n, world, r)[0]
+                                         for r in range(world)]]
+    dist.all_gather(gathered, torch.from_numpy(f_local))
+    if rank == 0:
+        q.put((g, np.concatenate([t.numpy() for t in gathered])))
+    dist.destroy_process_group()
+
+
+def test_two_rank_column_merge_matches_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    g_sharded, f_sharded = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    inst = G.config("C1", n=96, m=80)
+    P = O.Instance(inst.alpha, inst.beta, 0.05, x=inst.x, y=inst.y)
+    f = np.linspace(-0.1, 0.1, inst.n)
+    g_ref = O.ctransform_of_f(P, f)
+    assert np.max(np.abs(g_sharded - g_ref)) <= 1e-13 * np.max(np.abs(g_ref))
+    f_ref = O.ctransform_of_g(P, g_ref)
+    assert np.max(np.abs(f_sharded - f_ref)) <= 1e-12 * np.max(np.abs(f_ref))
+
+
+def test_row_partition_is_contiguous_and_complete():
+    for n in (1, 7, 512, 65536):
+        for world in (1, 2, 3, 8):
+            blocks = [row_partition(n, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            for (b0, e0), (b1, _) in zip(blocks, blocks[1:]):
+                assert e0 == b1 and b0 <= e0
