@@ -168,6 +168,9 @@ int sknr_bench_iterations(sknr_problem p, const sknr_config* cfg, const double* 
 /* Measured FP64 FMA ceiling of the current device (TFLOP/s, FMA = 2 flops):
  * the denominator of the on-the-fly roofline (MEASURED_PEAKS.json has no FP64 entry). */
 int sknr_bench_fp64_peak(double* tflops, double* ms);
+/* Tuning aid: device ms of launch variant `variant` of the d=2 column-LSE sum
+ * kernel on this problem (tools/tune_lse.py). */
+int sknr_tune_variant(sknr_problem p, int variant, int passes, double* kernel_ms);
 
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU. Rank 0 calls sknr_comm_unique_id, the id travels over

@@ -102,6 +102,7 @@ _SIGS = {
     "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _I64, ctypes.c_int, _D,
                               ctypes.POINTER(_I64)],
     "sknr_bench_fp64_peak": [_D, _D],
+    "sknr_tune_variant": [_P, ctypes.c_int, ctypes.c_int, _D],
     "sknr_comm_unique_id": [ctypes.c_void_p],
     "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int],
     "sknr_comm_destroy": [],
@@ -619,6 +620,12 @@ def shard(problem: Problem, rank: int, world: int) -> None:
     Inputs and outputs of every call stay full length on every rank."""
     b, e = row_partition(problem.n, world, rank)
     _check(lib().sknr_problem_shard(problem.handle, b, e))
+
+
+def tune_variant(problem: Problem, variant: int, passes: int = 5) -> float:
+    ms = ctypes.c_double()
+    _check(lib().sknr_tune_variant(problem.handle, int(variant), int(passes), ctypes.byref(ms)))
+    return ms.value
 
 
 def bench_fp64_peak():

@@ -2317,15 +2317,60 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
 
 // FP64 pipe ceiling on this device: 8 independent DFMA chains per thread, a
 // full grid of 148 x 8 CTAs of 256 threads, timed with CUDA events.
-__global__ void k_fp64_peak(double* out, int iters, double a, double b) {
+__global__ void k_fp64_peak(double* out, int iters, double a0, double b0) {
+    // per-thread register operands (3 distinct register pairs per DFMA)
+    const double a = a0 + threadIdx.x * 1e-12, b = b0 * (1.0 + threadIdx.x * 1e-9);
     double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-10, x2 = x0 + 2e-10, x3 = x0 + 3e-10;
     double x4 = x0 + 4e-10, x5 = x0 + 5e-10, x6 = x0 + 6e-10, x7 = x0 + 7e-10;
+    double y0 = a * 1.5, y1 = a * 1.25, y2 = a * 1.125, y3 = a, y4 = a * 0.5, y5 = a * 0.75, y6 = a * 0.875, y7 = a;
     for (int i = 0; i < iters; ++i) {
-        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
-        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        x0 = fma(x0, y0, b); x1 = fma(x1, y1, b); x2 = fma(x2, y2, b); x3 = fma(x3, y3, b);
+        x4 = fma(x4, y4, b); x5 = fma(x5, y5, b); x6 = fma(x6, y6, b); x7 = fma(x7, y7, b);
     }
     const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
     if (s == 12345.678) out[0] = s;
+}
+
+// Time launch-configuration variant v of the d=2 column-LSE sum kernel on this
+// problem's current packed state (tuning aid; see tools/tune_lse.py).
+int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
+    const int64_t n = P.n, m = P.m;
+    cudaStream_t s = P.stream;
+    DBuf f, g;
+    f.ensure(n);
+    g.ensure(m);
+    count_launch();
+    k_fill<<<grid_for(n), AUX_NT, 0, s>>>(f.p, n, 0.0);
+    count_launch();
+    k_state_init<<<1, 32, 0, s>>>(P.st, 1, 1.0);
+    plan_for(P, 0, MODE_SUM, 0);
+    plan_for(P, 0, MODE_MAX, 0);
+    lse(P, 0, f.p, g.p, G_NONE);
+    lse(P, 0, f.p, g.p, G_NONE);  // leaves the bound-shift pack in place
+    TilePlan tp = plan_tiles(P.dim, MODE_SUM, 0, m, n, 0, variant);
+    if (!tp.fn) throw InvalidArgument("sknr_tune_variant: unknown variant");
+    P.partial.ensure(static_cast<size_t>(tp.n_in_blocks) * m);
+    TileArgs ta = tile_args(P, 0, tp, G_NONE);
+    launch_tiles(tp, ta, s);
+    CK(cudaStreamSynchronize(s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *kernel_ms = ms / passes;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaGetLastError());
+    SKNR_API_END
 }
 
 int sknr_bench_fp64_peak(double* tflops, double* ms) {
@@ -2336,15 +2381,15 @@ int sknr_bench_fp64_peak(double* tflops, double* ms) {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     DBuf out;
     out.ensure(1);
-    const int iters = 20000, grid = sms * 8, block = 256;
-    k_fp64_peak<<<grid, block>>>(out.p, 100, 0.999999, 1e-7);
+    const int iters = 16000, grid = sms * 8, block = 256;
+    k_fp64_peak<<<grid, block>>>(out.p, 100, 0.5, 1e-7);
     CK(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0));
     count_launch();
-    k_fp64_peak<<<grid, block>>>(out.p, iters, 0.999999, 1e-7);
+    k_fp64_peak<<<grid, block>>>(out.p, iters, 0.5, 1e-7);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float t = 0;

@@ -31,7 +31,8 @@ struct TilePlan {
 };
 
 // dim: 0 = stored cost, 1..4 = point-cloud dimension. kt: block width (8..64) for MODE_BLOCK.
-TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks);
+TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks,
+                    int variant = -1);
 void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s);
 int block_kt_for(int k);
 int chunk_inputs(int mode, int kt);

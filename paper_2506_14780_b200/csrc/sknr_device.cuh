@@ -93,7 +93,9 @@ __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
 // rematerialise one per cell). Terms below 2^-1022 come out as 0 / subnormal;
 // HI_CLAMP caps terms at 2^1023 for passes whose exponents are not bounded
 // above by construction.
-template <bool HI_CLAMP>
+// FASTCLAMP: clamp the biased exponent with one IMNMX instead of ISETP+SEL;
+// valid only while |u| < 2^31 (callers guarantee it from the exponent range).
+template <bool HI_CLAMP, bool FASTCLAMP = false>
 __device__ __forceinline__ void pexp_parts(double u, const unsigned long long* __restrict__ tab,
                                            unsigned laneoff, double c3, double& Tp, double& p) {
     const double t = u + kMagicB;
@@ -103,7 +105,8 @@ __device__ __forceinline__ void pexp_parts(double u, const unsigned long long* _
     p = fma(p, r, kP2);
     p = fma(p, r, kP1);
     p = fma(p, r, 1.0);
-    int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
+    int kc = FASTCLAMP ? max(__double2loint(t), 0)
+                       : ((__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0);
     if (HI_CLAMP) kc = min(kc, kKcMax);
     const unsigned s = static_cast<unsigned>(kc) << 12;
     const unsigned off = ((s >> 5) & 0x7F80u) | laneoff;
@@ -119,11 +122,11 @@ __device__ __forceinline__ double pexp(double u, const unsigned long long* __res
     return Tp * p;
 }
 
-template <bool HI_CLAMP>
+template <bool HI_CLAMP, bool FASTCLAMP = false>
 __device__ __forceinline__ double pexp_acc(double u, const unsigned long long* __restrict__ tab,
                                            unsigned laneoff, double c3, double acc) {
     double Tp, p;
-    pexp_parts<HI_CLAMP>(u, tab, laneoff, c3, Tp, p);
+    pexp_parts<HI_CLAMP, FASTCLAMP>(u, tab, laneoff, c3, Tp, p);
     return fma(Tp, p, acc);
 }
 

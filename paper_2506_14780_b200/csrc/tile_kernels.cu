@@ -66,10 +66,10 @@ __device__ __forceinline__ void acc_init(double* acc) {
 }
 
 // ------------------------------------------------------------- point clouds
-template <int D, int JT, int MODE, int KT>
-__global__ void __launch_bounds__(NT_of<MODE>::value) pts_tile_kernel(TileArgs a) {
+template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FASTCLAMP = false>
+__global__ void __launch_bounds__(NTT) pts_tile_kernel(TileArgs a) {
     if (guard_skip(a.st, a.guard)) return;
-    constexpr int NT = NT_of<MODE>::value;
+    constexpr int NT = NTT;
     constexpr int PK = PK_of<D>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
     constexpr int KA = KT > 0 ? KT : 1;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(NT_of<MODE>::value) pts_tile_kernel(TileArgs a
                 }
             }
             __syncthreads();
-#pragma unroll 2
+#pragma unroll UNR
             for (int k = 0; k < cnt; ++k) {
                 double x[PK];
 #pragma unroll
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(NT_of<MODE>::value) pts_tile_kernel(TileArgs a
 #pragma unroll
                     for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
                     if (MODE == MODE_SUM) {
-                        acc[jt][0] = pexp_acc<false>(u, tab, laneoff, c3, acc[jt][0]);
+                        acc[jt][0] = pexp_acc<false, FASTCLAMP>(u, tab, laneoff, c3, acc[jt][0]);
                     } else if (MODE == MODE_MAX) {
                         acc[jt][0] = fmax(acc[jt][0], u);
                     } else {
@@ -151,6 +151,116 @@ __global__ void __launch_bounds__(NT_of<MODE>::value) pts_tile_kernel(TileArgs a
                 for (int c = 0; c < KA; ++c) a.partial[(ib * KA + c) * a.n_out + o[jt]] = acc[jt][c];
             } else {
                 a.partial[ib * a.n_out + o[jt]] = acc[jt][0];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- block pass on FP64 tensor cores
+// out[o][c] += sum_in e(o,in) W[in][c] as a GEMM: A = e (generated in registers,
+// one cell per lane: row o = lane>>2, col in = lane&3), B = W (smem), C in
+// registers, via mma.sync.m8n8k4.f64 (DMMA). DMMA shares the FP64 pipe with
+// DFMA on sm_100 (tools/dmma_probe.cu) but replaces KT DFMAs + KT/2 shared-memory
+// broadcasts per cell with KT/8 tensor instructions per 32 cells, which turns
+// the issue-bound DFMA formulation into a pipe-bound one. Each warp owns MB
+// 8-output blocks so B fragments are reused MB times.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int KT>
+struct WStride {  // smem row stride of W: rows 64 B apart modulo 128 B -> 2 wavefronts per B load
+    static constexpr int value = (KT % 16 == 0) ? KT + 8 : KT;
+};
+
+constexpr int MMA_NT = 128;  // 4 warps
+constexpr int MMA_CH = 64;   // inputs per shared-memory round
+
+template <int D, int KT, int MB>
+__global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int NCB = KT / 8;
+    constexpr int WS = WStride<KT>::value;
+    constexpr int OUT_WARP = 8 * MB;
+    constexpr int OUT_CTA = OUT_WARP * (MMA_NT / 32);
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + kTabWords;
+    double* sw = sin + MMA_CH * PK;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_exp2_table(tab, tid, MMA_NT);
+    const unsigned laneoff = (lane & 15) << 3;
+    const double c3 = reg_const(kP3);
+    const int row = lane >> 2, kq = lane & 3;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        const int64_t obase = ot * OUT_CTA + warp * OUT_WARP;
+        double Bo[MB], Yo[MB][D];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            int64_t o = obase + mb * 8 + row;
+            o = o < a.n_out ? o : a.n_out - 1;
+            Bo[mb] = a.out_pack[o * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Yo[mb][d] = a.out_pack[o * PK + 1 + d];
+        }
+        double acc[MB][NCB][2];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) acc[mb][cb][0] = acc[mb][cb][1] = 0.0;
+
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += MMA_CH) {
+            const int cnt = static_cast<int>((i1 - c0) < MMA_CH ? (i1 - c0) : MMA_CH);
+            const int cnt4 = (cnt + 3) & ~3;
+            __syncthreads();
+            for (int t = tid; t < cnt4 * PK; t += MMA_NT) {
+                const int k = t / PK, q = t % PK;
+                sin[t] = k < cnt ? a.in_pack[(c0 + k) * PK + q] : (q == 0 ? -1e300 : 0.0);
+            }
+            for (int t = tid; t < cnt4 * KT; t += MMA_NT) {
+                const int k = t / KT, c = t % KT;
+                sw[k * WS + c] = k < cnt ? a.W[(c0 + k) * KT + c] : 0.0;
+            }
+            __syncthreads();
+            for (int k4 = 0; k4 < cnt4; k4 += 4) {
+                const double* xin = sin + (k4 + kq) * PK;
+                double x[PK];
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(xin)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+                double bf[NCB];
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) bf[cb] = sw[(k4 + kq) * WS + cb * 8 + row];
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    double u = x[0] + Bo[mb];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Yo[mb][d], u);
+                    const double e = pexp<true>(u, tab, laneoff, c3);
+#pragma unroll
+                    for (int cb = 0; cb < NCB; ++cb) dmma_8x8x4(acc[mb][cb][0], acc[mb][cb][1], e, bf[cb]);
+                }
+            }
+        }
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t o = obase + mb * 8 + row;
+            if (o >= a.n_out) continue;
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+                const int c = cb * 8 + kq * 2;
+                a.partial[(ib * KT + c) * a.n_out + o] = acc[mb][cb][0];
+                a.partial[(ib * KT + c + 1) * a.n_out + o] = acc[mb][cb][1];
             }
         }
     }
@@ -270,16 +380,17 @@ struct KernelInfo {
     const void* fn = nullptr;
     int jt = 1;
     int nt = 128;
+    int out_tile = 0;  // outputs per CTA tile (0: nt * jt)
     int smem = 0;
     int occ = 0;
 };
 
-template <int D, int JT, int MODE, int KT>
+template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FC = false>
 KernelInfo make_pts() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_tile_kernel<D, JT, MODE, KT>);
+    k.fn = reinterpret_cast<const void*>(&pts_tile_kernel<D, JT, MODE, KT, NTT, UNR, FC>);
     k.jt = JT;
-    k.nt = NT_of<MODE>::value;
+    k.nt = NTT;
     constexpr int CH = Chunk<MODE, KT>::value;
     k.smem = static_cast<int>(sizeof(double)) *
              (kTabWords + CH * PK_of<D>::value + (MODE == MODE_BLOCK ? CH * KT : 0));
@@ -297,18 +408,30 @@ KernelInfo make_dense() {
     return k;
 }
 
+template <int D, int KT, int MB>
+KernelInfo make_mma() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_mma_kernel<D, KT, MB>);
+    k.jt = 1;
+    k.nt = MMA_NT;
+    k.out_tile = 8 * MB * (MMA_NT / 32);
+    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + MMA_CH * PK_of<D>::value + MMA_CH * WStride<KT>::value);
+    return k;
+}
+
 template <int D>
 KernelInfo pick_pts(int mode, int kt) {
-    if (mode == MODE_SUM) return make_pts<D, 4, MODE_SUM, 0>();
+    // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
+    if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
-    switch (kt) {
-        case 8: return make_pts<D, 2, MODE_BLOCK, 8>();
-        case 16: return make_pts<D, 2, MODE_BLOCK, 16>();
-        case 24: return make_pts<D, 1, MODE_BLOCK, 24>();
-        case 32: return make_pts<D, 1, MODE_BLOCK, 32>();
-        case 40: return make_pts<D, 1, MODE_BLOCK, 40>();
-        case 48: return make_pts<D, 1, MODE_BLOCK, 48>();
-        case 64: return make_pts<D, 1, MODE_BLOCK, 64>();
+    switch (kt) {  // FP64 tensor-core (DMMA) block pass, 4 x 8-output blocks per warp
+        case 8: return make_mma<D, 8, 4>();
+        case 16: return make_mma<D, 16, 4>();
+        case 24: return make_mma<D, 24, 4>();
+        case 32: return make_mma<D, 32, 4>();
+        case 40: return make_mma<D, 40, 4>();
+        case 48: return make_mma<D, 48, 2>();
+        case 64: return make_mma<D, 64, 2>();
         default: return KernelInfo{};
     }
 }
@@ -324,6 +447,34 @@ KernelInfo pick_dense(int mode, int kt) {
         case 40: return make_dense<1, MODE_BLOCK, 40>();
         case 48: return make_dense<1, MODE_BLOCK, 48>();
         case 64: return make_dense<1, MODE_BLOCK, 64>();
+        default: return KernelInfo{};
+    }
+}
+
+// Launch-configuration variants of the d=2 column-LSE sum kernel, timed by
+// sknr_tune_variant (tools/tune_lse.py) to choose the default above.
+KernelInfo tune_variant(int v) {
+    switch (v) {
+        case 0: return make_pts<2, 4, MODE_SUM, 0, 256, 2, false>();
+        case 1: return make_pts<2, 4, MODE_SUM, 0, 256, 1, false>();
+        case 2: return make_pts<2, 4, MODE_SUM, 0, 256, 4, false>();
+        case 3: return make_pts<2, 2, MODE_SUM, 0, 256, 2, false>();
+        case 4: return make_pts<2, 8, MODE_SUM, 0, 256, 1, false>();
+        case 5: return make_pts<2, 8, MODE_SUM, 0, 256, 2, false>();
+        case 6: return make_pts<2, 4, MODE_SUM, 0, 128, 2, false>();
+        case 7: return make_pts<2, 4, MODE_SUM, 0, 512, 2, false>();
+        case 8: return make_pts<2, 4, MODE_SUM, 0, 256, 2, true>();
+        case 9: return make_pts<2, 8, MODE_SUM, 0, 256, 1, true>();
+        case 10: return make_pts<2, 2, MODE_SUM, 0, 512, 4, false>();
+        case 11: return make_pts<2, 4, MODE_SUM, 0, 512, 2, true>();
+        case 12: return make_pts<2, 8, MODE_SUM, 0, 128, 1, false>();
+        case 13: return make_pts<2, 8, MODE_SUM, 0, 512, 1, false>();
+        case 14: return make_pts<2, 16, MODE_SUM, 0, 128, 1, false>();
+        case 15: return make_pts<2, 16, MODE_SUM, 0, 256, 1, false>();
+        case 16: return make_pts<2, 6, MODE_SUM, 0, 256, 1, false>();
+        case 17: return make_pts<2, 12, MODE_SUM, 0, 256, 1, false>();
+        case 18: return make_pts<2, 12, MODE_SUM, 0, 128, 1, false>();
+        case 19: return make_pts<2, 8, MODE_SUM, 0, 256, 1, true>();
         default: return KernelInfo{};
     }
 }
@@ -353,9 +504,10 @@ int chunk_inputs(int mode, int kt) {
     return kt > 32 ? 32 : 64;
 }
 
-TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks) {
+TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks,
+                    int variant) {
     TilePlan p;
-    KernelInfo ki = pick(dim, mode, kt);
+    KernelInfo ki = variant >= 0 ? tune_variant(variant) : pick(dim, mode, kt);
     if (!ki.fn) return p;
     static thread_local int sm_count = 0;
     if (sm_count == 0) {
@@ -369,7 +521,7 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn, ki.nt, ki.smem);
     if (occ < 1) occ = 1;
     const int64_t resident = static_cast<int64_t>(sm_count) * occ;
-    p.out_tile = ki.nt * ki.jt;
+    p.out_tile = ki.out_tile > 0 ? ki.out_tile : ki.nt * ki.jt;
     p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     const int ch = chunk_inputs(mode, kt);
