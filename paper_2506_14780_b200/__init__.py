@@ -103,6 +103,7 @@ _SIGS = {
                               ctypes.POINTER(_I64)],
     "sknr_bench_fp64_peak": [_D, _D],
     "sknr_tune_variant": [_P, ctypes.c_int, ctypes.c_int, _D],
+    "sknr_debug_counters": [_P, ctypes.POINTER(_I64)],
     "sknr_comm_unique_id": [ctypes.c_void_p],
     "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int],
     "sknr_comm_destroy": [],
@@ -620,6 +621,12 @@ def shard(problem: Problem, rank: int, world: int) -> None:
     Inputs and outputs of every call stay full length on every rank."""
     b, e = row_partition(problem.n, world, rank)
     _check(lib().sknr_problem_shard(problem.handle, b, e))
+
+
+def debug_counters(problem: Problem) -> dict:
+    out = (_I64 * 4)()
+    _check(lib().sknr_debug_counters(problem.handle, out))
+    return {"exact_col": out[0], "exact_row": out[1], "retry_col": out[2], "retry_row": out[3]}
 
 
 def tune_variant(problem: Problem, variant: int, passes: int = 5) -> float:

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
                         isfinite(mx) && isfinite(mn);
         a.st->need_exact[a.dir] = ok ? 0 : 1;
         a.st->retry[a.dir] = 0;
+        if (!ok) a.st->n_exact[a.dir] += 1;
         a.st->counters[a.dir] = 0u;
     }
 }
@@ -147,7 +148,10 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
         if (a.L) a.L[o] = L;
         if (a.pot) a.pot[o] = -a.eps * L;
     }
-    if (bad && !a.retry_phase && !a.st->need_exact[a.dir]) a.st->retry[a.dir] = 1;
+    if (bad && !a.retry_phase && !a.st->need_exact[a.dir]) {
+        a.st->retry[a.dir] = 1;
+        atomicAdd(&a.st->n_retry[a.dir], 1ull);
+    }
 }
 
 __global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, int64_t nb,
@@ -391,6 +395,7 @@ __global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, u
     const bool ok = st->ref_valid[dir] && (mx - mn) * inv_eps <= spread && isfinite(mx) && isfinite(mn);
     st->need_exact[dir] = ok ? 0 : 1;
     st->retry[dir] = 0;
+    if (!ok) st->n_exact[dir] += 1;
 }
 
 }  // namespace sknr

@@ -150,6 +150,9 @@ struct DBuf {
     ~DBuf() {
         if (p) cudaFree(p);
     }
+    // Grows (never inside stream capture). The zero fill is complete before
+    // returning: the problem streams are non-blocking, so an asynchronous
+    // default-stream memset could otherwise land after later work on them.
     void ensure(size_t count) {
         if (count <= n) return;
         if (p) CK(cudaFree(p));
@@ -157,6 +160,7 @@ struct DBuf {
         n = 0;
         CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
         CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(double)));
+        CK(cudaDeviceSynchronize());
         n = count;
     }
 };
@@ -1196,8 +1200,62 @@ static void host_sym_eig(const std::vector<double>& Ain, int k, std::vector<doub
 }
 
 struct QrWork {
-    DBuf hh, w, part, Q;
+    DBuf hh, w, part, Q, backup, flag;
+    bool force_householder = false;
 };
+
+// Cholesky G + shift*I = L L^T (shift = coef * trace(G)), then Rinv = L^{-T}
+// (upper). One CTA; k <= 64. *fail = 1 if a pivot is not positive.
+__global__ void k_chol_inv(const double* G, int k, double coef, double* Rinv, int* fail) {
+    extern __shared__ double sL[];  // k*k
+    __shared__ double piv;
+    __shared__ int bad;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        bad = 0;
+        double tr = 0.0;
+        for (int c = 0; c < k; ++c) tr += G[c + c * k];
+        piv = coef * tr;
+    }
+    __syncthreads();
+    const double shift = piv;
+    for (int e = tid; e < k * k; e += blockDim.x) {
+        const int r = e % k, c = e / k;
+        sL[e] = G[e] + (r == c ? shift : 0.0);
+    }
+    __syncthreads();
+    for (int c = 0; c < k; ++c) {
+        if (tid == 0) {
+            double x = sL[c + c * k];
+            for (int t = 0; t < c; ++t) x -= sL[c + t * k] * sL[c + t * k];
+            if (!(x > 0.0)) bad = 1;
+            piv = sqrt(x);
+            sL[c + c * k] = piv;
+        }
+        __syncthreads();
+        if (bad) break;
+        for (int r = c + 1 + tid; r < k; r += blockDim.x) {
+            double v = sL[r + c * k];
+            for (int t = 0; t < c; ++t) v -= sL[r + t * k] * sL[c + t * k];
+            sL[r + c * k] = v / piv;
+        }
+        __syncthreads();
+    }
+    if (bad) {
+        if (tid == 0) *fail = 1;
+        return;
+    }
+    // column j of L^{-1} by forward substitution; Rinv = (L^{-1})^T
+    for (int j = tid; j < k; j += blockDim.x) {
+        double x[64];
+        for (int r = 0; r < k; ++r) {
+            double v = (r == j) ? 1.0 : 0.0;
+            for (int t = j; t < r; ++t) v -= sL[r + t * k] * x[t];
+            x[r] = r < j ? 0.0 : v / sL[r + r * k];
+        }
+        for (int r = 0; r < k; ++r) Rinv[j + r * k] = x[r];  // Rinv(j, r) = Linv(r, j)
+    }
+}
 
 // Thin Householder Q of X (n x k) in place (spectral.cpp:116-117 conventions).
 static void device_householder_q(Problem& P, double* X, int64_t n, int k, QrWork& qw) {
@@ -1233,19 +1291,60 @@ static void device_householder_q(Problem& P, double* X, int64_t n, int k, QrWork
     CK(cudaGetLastError());
 }
 
-// orthonormalize_deflated (spectral.cpp:113-121)
+// CholeskyQR step: X <- X R^{-1} with R^T R = X^T X (+ shift I). The shifted
+// first pass makes the factorisation succeed for cond(X) up to ~1/u (shifted
+// CholeskyQR3); a failed Cholesky sets *fail and the caller falls back to
+// Householder.
+static void device_cholqr_step(Problem& P, double* X, int64_t n, int k, bool shifted, QrWork& qw,
+                               int* fail) {
+    qw.Q.ensure(static_cast<size_t>(n) * k);
+    qw.w.ensure(64 * 64 * 2);
+    double* G = qw.w.p;
+    double* Rinv = qw.w.p + 64 * 64;
+    gram(P, n, k, k, X, n, X, n, nullptr, G, 0);
+    const double shift_coef = shifted ? 11.0 * (static_cast<double>(n) * k + k * (k + 1.0)) * 0x1p-53 : 0.0;
+    count_launch();
+    k_chol_inv<<<1, 64, sizeof(double) * k * k, P.stream>>>(G, k, shift_coef, Rinv, fail);
+    count_launch();
+    k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * k * k, P.stream>>>(X, n, k, Rinv, k, qw.Q.p);
+    CK(cudaMemcpyAsync(X, qw.Q.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
+}
+
+// orthonormalize_deflated (spectral.cpp:113-121): same deflation rounds and
+// stopping test; the QR is shifted CholeskyQR3 (same column space as the
+// reference's Householder Q; columns may differ in sign, which neither the
+// Rayleigh-Ritz step nor the Newton step sees) with a device Householder
+// fallback (Eigen's reflector convention) when the Gram is numerically singular.
 static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const double* u0,
                                  QrWork& qw) {
     double* s = P.misc.p;  // k dots
+    qw.flag.ensure(1);
+    int* fail = reinterpret_cast<int*>(qw.flag.p);
     for (int round = 0; round < 3; ++round) {
         gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
         count_launch();
         k_deflate<<<grid_for(n * k), AUX_NT, 0, P.stream>>>(X, n, k, u0, s);
-        device_householder_q(P, X, n, k, qw);
+        bool use_householder = qw.force_householder;
+        if (!use_householder) {
+            CK(cudaMemcpyAsync(qw.backup.p, X, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
+            CK(cudaMemsetAsync(fail, 0, sizeof(int), P.stream));
+            device_cholqr_step(P, X, n, k, true, qw, fail);
+            device_cholqr_step(P, X, n, k, false, qw, fail);
+            device_cholqr_step(P, X, n, k, false, qw, fail);
+        }
         gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
-        std::vector<double> hs(k);
+        std::vector<double> hs(k + 1);
         download(hs.data(), s, k, P.stream);
+        int hfail = 0;
+        if (!use_householder) CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
         CK(cudaStreamSynchronize(P.stream));
+        if (hfail) {  // restore the deflated block and redo this round with Householder
+            CK(cudaMemcpyAsync(X, qw.backup.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
+            device_householder_q(P, X, n, k, qw);
+            gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
+            download(hs.data(), s, k, P.stream);
+            CK(cudaStreamSynchronize(P.stream));
+        }
         double worst = 0.0;
         for (int c = 0; c < k; ++c) worst = std::max(worst, std::abs(hs[c]));
         if (worst < 1e-13) break;
@@ -1280,6 +1379,7 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
     th.ensure(ell);
     P.misc.ensure(256);
     QrWork qw;
+    qw.backup.ensure(static_cast<size_t>(n) * block);
     count_launch();
     k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull);
     device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
@@ -2370,6 +2470,19 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     CK(cudaGetLastError());
+    SKNR_API_END
+}
+
+// Diagnostics: [exact col, exact row, retry col, retry row] counters since creation.
+int sknr_debug_counters(sknr_problem h, int64_t* out) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
+    CK(cudaStreamSynchronize(P.stream));
+    out[0] = static_cast<int64_t>(P.st_host->n_exact[0]);
+    out[1] = static_cast<int64_t>(P.st_host->n_exact[1]);
+    out[2] = static_cast<int64_t>(P.st_host->n_retry[0]);
+    out[3] = static_cast<int64_t>(P.st_host->n_retry[1]);
     SKNR_API_END
 }
 

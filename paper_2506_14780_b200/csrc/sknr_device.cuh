@@ -60,6 +60,8 @@ struct DevState {
     double dmax[2], dmin[2];     // max/min of (in - ref_in) per direction
     double scratch[16];
     unsigned int counters[32];   // last-block tickets of fused reductions
+    unsigned long long n_exact[2];  // diagnostics: exact-shift passes per direction
+    unsigned long long n_retry[2];  // diagnostics: bound-shift validation failures
 };
 
 enum Guard : unsigned {
