@@ -773,6 +773,7 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&p->st, sizeof(DevState)));
     CK(cudaMemset(p->st, 0, sizeof(DevState)));
+    CK(cudaDeviceSynchronize());
     CK(cudaMallocHost(&p->st_host, sizeof(DevState)));
     setup_side(p->src, alpha, n, p->stream);
     setup_side(p->tgt, beta, m, p->stream);
