@@ -210,10 +210,10 @@ __global__ void __launch_bounds__(AUX_NT) k_pack_w(const double* X, int64_t n, i
 }
 
 // ------------------------------------------------------------------ Gram
-int gram_blocks(int64_t T) {
-    int64_t b = (T + 2047) / 2048;
+int gram_blocks(int64_t T) {  // >= 64 rows per block, up to two CTAs per SM
+    int64_t b = (T + 63) / 64;
     if (b < 1) b = 1;
-    if (b > 148) b = 148;
+    if (b > 296) b = 296;
     return static_cast<int>(b);
 }
 

@@ -787,7 +787,7 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     p->red_tmp.ensure(std::max(n, m));
     p->h_alpha.assign(alpha, alpha + n);
     p->h_beta.assign(beta, beta + m);
-    p->gram_part.ensure(148 * 64 * 64 + 64);
+    p->gram_part.ensure(296 * 64 * 64 + 64);
     p->sums.ensure(64);
     return p.release();
 }
@@ -1151,53 +1151,129 @@ static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t
 
 
 // ============================================================ top_modes
-// Symmetric Jacobi eigensolver for the k x k Rayleigh-Ritz matrix (stands in
-// for Eigen::SelfAdjointEigenSolver, spectral.cpp:156): ascending values.
-static void host_sym_eig(const std::vector<double>& Ain, int k, std::vector<double>& evals,
-                         std::vector<double>& evecs) {
-    std::vector<double> A(Ain), Q(static_cast<size_t>(k) * k, 0.0);
-    for (int i = 0; i < k; ++i) Q[i + i * k] = 1.0;
-    for (int sweep = 0; sweep < 100; ++sweep) {
-        double off = 0.0, diag = 0.0;
-        for (int c = 0; c < k; ++c)
-            for (int r = 0; r < k; ++r) (r == c ? diag : off) += A[r + c * k] * A[r + c * k];
-        if (off <= 1e-36 * diag || off == 0.0) break;
-        for (int p = 0; p < k - 1; ++p)
-            for (int q = p + 1; q < k; ++q) {
-                const double apq = A[p + q * k];
-                if (apq == 0.0) continue;
-                const double app = A[p + p * k], aqq = A[q + q * k];
-                const double theta = (aqq - app) / (2.0 * apq);
-                const double t =
-                    (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
-                const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
-                for (int r = 0; r < k; ++r) {
-                    const double arp = A[r + p * k], arq = A[r + q * k];
-                    A[r + p * k] = c * arp - s * arq;
-                    A[r + q * k] = s * arp + c * arq;
+// Symmetric eigen-decomposition (stands in for Eigen::SelfAdjointEigenSolver,
+// spectral.cpp:156): Householder tridiagonalisation followed by implicit QL
+// with Wilkinson-type shifts (the classic tred2/tql2 pair), ascending
+// eigenvalues, orthonormal eigenvectors in columns. O(k^3) for the k x k
+// Rayleigh-Ritz matrix.
+static bool symeig_tql(const double* Ain, int k, double* evals, double* evecs) {
+    std::vector<double> a(static_cast<size_t>(k) * k), d(k), e(k);
+    auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(i) * k + j]; };
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) A(i, j) = Ain[i + j * k];
+    for (int i = k - 1; i > 0; --i) {
+        const int l = i - 1;
+        double h = 0.0, scale = 0.0;
+        if (l > 0) {
+            for (int q = 0; q <= l; ++q) scale += std::abs(A(i, q));
+            if (scale == 0.0) {
+                e[i] = A(i, l);
+            } else {
+                for (int q = 0; q <= l; ++q) {
+                    A(i, q) /= scale;
+                    h += A(i, q) * A(i, q);
                 }
-                for (int r = 0; r < k; ++r) {
-                    const double apr = A[p + r * k], aqr = A[q + r * k];
-                    A[p + r * k] = c * apr - s * aqr;
-                    A[q + r * k] = s * apr + c * aqr;
+                double f = A(i, l);
+                double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
+                e[i] = scale * g;
+                h -= f * g;
+                A(i, l) = f - g;
+                f = 0.0;
+                for (int j = 0; j <= l; ++j) {
+                    A(j, i) = A(i, j) / h;
+                    g = 0.0;
+                    for (int q = 0; q <= j; ++q) g += A(j, q) * A(i, q);
+                    for (int q = j + 1; q <= l; ++q) g += A(q, j) * A(i, q);
+                    e[j] = g / h;
+                    f += e[j] * A(i, j);
                 }
-                for (int r = 0; r < k; ++r) {
-                    const double qrp = Q[r + p * k], qrq = Q[r + q * k];
-                    Q[r + p * k] = c * qrp - s * qrq;
-                    Q[r + q * k] = s * qrp + c * qrq;
+                const double hh = f / (h + h);
+                for (int j = 0; j <= l; ++j) {
+                    f = A(i, j);
+                    e[j] = g = e[j] - hh * f;
+                    for (int q = 0; q <= j; ++q) A(j, q) -= (f * e[q] + g * A(i, q));
                 }
             }
+        } else {
+            e[i] = A(i, l);
+        }
+        d[i] = h;
+    }
+    d[0] = 0.0;
+    e[0] = 0.0;
+    for (int i = 0; i < k; ++i) {
+        const int l = i - 1;
+        if (d[i] != 0.0) {
+            for (int j = 0; j <= l; ++j) {
+                double g = 0.0;
+                for (int q = 0; q <= l; ++q) g += A(i, q) * A(q, j);
+                for (int q = 0; q <= l; ++q) A(q, j) -= g * A(q, i);
+            }
+        }
+        d[i] = A(i, i);
+        A(i, i) = 1.0;
+        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
+    }
+    for (int i = 1; i < k; ++i) e[i - 1] = e[i];
+    e[k - 1] = 0.0;
+    for (int l = 0; l < k; ++l) {
+        int iter = 0, m;
+        do {
+            for (m = l; m < k - 1; ++m) {
+                const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
+                if (std::abs(e[m]) <= 0x1p-53 * dd) break;
+            }
+            if (m != l) {
+                if (iter++ == 100) return false;
+                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                double r = std::hypot(g, 1.0);
+                g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
+                double s = 1.0, c = 1.0, p = 0.0;
+                int i;
+                for (i = m - 1; i >= l; --i) {
+                    double f = s * e[i];
+                    const double b = c * e[i];
+                    e[i + 1] = (r = std::hypot(f, g));
+                    if (r == 0.0) {
+                        d[i + 1] -= p;
+                        e[m] = 0.0;
+                        break;
+                    }
+                    s = f / r;
+                    c = g / r;
+                    g = d[i + 1] - p;
+                    r = (d[i] - g) * s + 2.0 * c * b;
+                    d[i + 1] = g + (p = s * r);
+                    g = c * r - b;
+                    for (int q = 0; q < k; ++q) {
+                        f = A(q, i + 1);
+                        A(q, i + 1) = s * A(q, i) + c * f;
+                        A(q, i) = c * A(q, i) - s * f;
+                    }
+                }
+                if (r == 0.0 && i >= l) continue;
+                d[l] -= p;
+                e[l] = g;
+                e[m] = 0.0;
+            }
+        } while (m != l);
     }
     std::vector<int> order(k);
     for (int i = 0; i < k; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int u, int v) { return A[u + u * k] < A[v + v * k]; });
+    std::stable_sort(order.begin(), order.end(), [&](int u, int v) { return d[u] < d[v]; });
+    for (int c = 0; c < k; ++c) {
+        evals[c] = d[order[c]];
+        for (int r = 0; r < k; ++r) evecs[r + c * k] = A(r, order[c]);
+    }
+    return true;
+}
+
+static void host_sym_eig(const std::vector<double>& A, int k, std::vector<double>& evals,
+                         std::vector<double>& evecs) {
     evals.assign(k, 0.0);
     evecs.assign(static_cast<size_t>(k) * k, 0.0);
-    for (int c = 0; c < k; ++c) {
-        evals[c] = A[order[c] + order[c] * k];
-        for (int r = 0; r < k; ++r) evecs[r + c * k] = Q[r + order[c] * k];
-    }
+    if (!symeig_tql(A.data(), k, evals.data(), evecs.data()))
+        throw EigenFailure("top_modes: dense Ritz solve failed", std::numeric_limits<double>::infinity());
 }
 
 struct QrWork {
