@@ -36,8 +36,8 @@ METRIC = "GCells/s of LSE sweeps (C4 Sinkhorn sweep = 2 LSE passes over n*m cell
 UNIT = "GCells/s"
 # FP64 pipe instructions per cell of the on-the-fly d=2 LSE sum kernel:
 # exponent 1 DADD + 2 DFMA; exp2 3 DADD (Cody-Waite) + 5 DFMA (poly) + 1 DFMA (table x poly
-# fused with the accumulate) = 12 issue slots, counted as 2 flops each (FMA-equivalent).
-FP64_SLOTS_PER_CELL = 12
+# fused with the accumulate) = 11 issue slots, counted as 2 flops each (FMA-equivalent).
+FP64_SLOTS_PER_CELL = 11
 
 
 def parse():
@@ -190,7 +190,7 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64, BASELINE C4 column sample)",
         "config": {"workload": f"{args.config} SK iteration on an n x {ms} column sample", "n": inst.n,
                    "m_sample": ms, "epsilon": inst.epsilon},
@@ -214,7 +214,25 @@ def run_ours(args, world, rank, local):
     inst = G.config(args.config)
     n, m = inst.n, inst.m
     cells = float(n) * m
-    prob = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale)
+    if world > 1:
+        # row sharding: NCCL communicator over NVLink, id shared via gloo
+        import torch
+
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.tensor(list(sk.comm_unique_id()), dtype=torch.uint8)
+        dist.broadcast(uid, src=0)
+        sk.comm_init(rank, world, bytes(uid.tolist()), 0)
+
+    def make_problem():
+        p = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale)
+        if world > 1:
+            sk.shard(p, rank, world)
+        return p
+
+    prob = make_problem()
+    rb, re_ = sk.row_partition(n, world, rank)
+    cells_local = float(re_ - rb) * m
 
     # ---- value: SK iterations, device-resident, L2 flushed between timed steps
     clocks = ClockSampler(gpu)
@@ -225,16 +243,16 @@ def run_ours(args, world, rank, local):
     clk = clocks.stop()
     barrier(dist)
     ms_iter_max = dist_max(dist, ms_iter)
-    value = world * 2.0 * cells / (ms_iter_max * 1e-3) / 1e9
+    value = 2.0 * cells / (ms_iter_max * 1e-3) / 1e9  # whole job: all rows of C4 per step
 
     # ---- dominant kernel: the column-LSE sum tile kernel alone, CUDA events on its stream
     ms_pass, ms_kernel = sk.bench_pass(prob, 2, 0, passes=10)
     peak_tflops, _ = sk.bench_fp64_peak()
-    achieved = FP64_SLOTS_PER_CELL * 2.0 * cells / (ms_kernel * 1e-3) / 1e12
+    achieved = FP64_SLOTS_PER_CELL * 2.0 * cells_local / (ms_kernel * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / peak_tflops, "traffic": read_profile_traffic(),
-                "kernel": "pts_tile_kernel<2,4,SUM> (column LSE, on-the-fly d=2)",
-                "kernel_ms": ms_kernel, "kernel_gcells_per_s": cells / (ms_kernel * 1e-3) / 1e9,
+                "kernel": "pts_tile_kernel<2,8,SUM> (column LSE, on-the-fly d=2)",
+                "kernel_ms": ms_kernel, "kernel_gcells_per_s": cells_local / (ms_kernel * 1e-3) / 1e9,
                 "algorithmic_per_cell": f"{FP64_SLOTS_PER_CELL} FP64 issue slots (x2 flops)",
                 "peak_source": "measured DFMA-only kernel on this GPU (sknr_bench_fp64_peak)"}
 
@@ -247,22 +265,23 @@ def run_ours(args, world, rank, local):
 
     # ---- e2e: public C ABI with host buffers (problem upload + solve + potentials download)
     k_e2e = max(args.steps, 1)
+    barrier(dist)
     t0 = time.perf_counter()
-    p2 = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale)
+    p2 = make_problem()
     res = sk.solve(p2, tol=1e-300, max_iter=k_e2e, trace=False)
     t_e2e = time.perf_counter() - t0
     assert res.iterations == k_e2e
     h2d = (inst.x.nbytes + inst.y.nbytes + inst.alpha.nbytes + inst.beta.nbytes) / k_e2e
     d2h = (res.f.nbytes + res.g.nbytes) / k_e2e
     t_e2e = dist_max(dist, t_e2e)
-    e2e = {"value": world * 2.0 * cells * k_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+    e2e = {"value": 2.0 * cells * k_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": k_e2e,
            "path": "PointProblem(host arrays) + sknr_solve(max_iter=K) + f,g download, wall clock"}
     del p2
 
     # ---- time to tolerance on C1 (SK and SK-NR(10) with eps'=2eps warm start + basis)
     ttt = None
-    if not args.no_ttt:
+    if not args.no_ttt and rank == 0:
         c1 = G.config("C1")
         p1 = sk.PointProblem(c1.x, c1.y, c1.alpha, c1.beta, c1.epsilon)
         t0 = time.perf_counter()
@@ -297,13 +316,13 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_iter_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SplitMix64 point clouds, BASELINE C4)",
             "config": {"workload": "C4: n=m=65536, d=2 uniform [0,1]^2, on-the-fly squared-Euclidean cost, "
                                    "uniform marginals, eps=5e-4; step = one SK iteration of the device loop",
                        "n": n, "m": m, "d": 2, "epsilon": inst.epsilon,
                        "l2": "flushed between timed steps (256 MiB memset, untimed)",
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
+                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "single GPU"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -317,6 +336,8 @@ def run_ours(args, world, rank, local):
             "library": sk.version(),
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        sk.comm_destroy()
     if dist is not None:
         dist.destroy_process_group()
 

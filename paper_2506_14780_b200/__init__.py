@@ -502,9 +502,12 @@ def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False) -> _C
 
 
 def solve(problem: Problem, tol: float = 1e-9, max_iter: int = 100000, ell: int = 0,
-          basis: Optional[SpectralBasis] = None, init=None, trace: bool = True) -> SolveResult:
-    """SK-NR(ell) (Alg. 1; solver.cpp:71-156)."""
-    cfg = _config(tol, max_iter, ell, trace)
+          basis: Optional[SpectralBasis] = None, init=None, trace: bool = True,
+          exact_marginals: bool = False) -> SolveResult:
+    """SK-NR(ell) (Alg. 1; solver.cpp:71-156). exact_marginals=True evaluates the
+    stopping test from explicit plan row/column sums (core.cpp:120-143) instead
+    of the fused transform (2 extra passes per iteration)."""
+    cfg = _config(tol, max_iter, ell, trace, exact_marginals=exact_marginals)
     V = None
     bell = 0
     if ell > 0:

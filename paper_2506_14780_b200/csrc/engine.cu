@@ -1571,7 +1571,7 @@ struct SolveOut {
 
 // Enqueue one SK-NR(ell) iteration (solver.cpp:104-151).
 static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace_enabled,
-                              int64_t trace_cap) {
+                              int64_t trace_cap, bool exact_marginals = false) {
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     const bool newton = ell > 0;
@@ -1608,9 +1608,36 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
                                                      P.inv_eps(), S.rowres.p, P.st);
     // h = f^{C,eps}: the column marginal and the next sweep's g
     lse(P, 0, S.f.p, S.h.p, G_DONE);
-    count_launch();
-    k_colres<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.h.p, P.tgt.w.p, m, P.inv_eps(), S.colres.p, P.st,
-                                            G_DONE);
+    if (exact_marginals) {
+        // reference-faithful plan_marginals (core.cpp:120-143): explicit row and
+        // column sums of a_i b_j exp((f_i + g_j - C_ij)/eps) at the gauged (f, g)
+        PassSpec pr;
+        pr.dir = 1;
+        pr.in_v = S.g.p;
+        pr.in_lw = P.tgt.lw.p;
+        pr.out_v = S.f.p;
+        pr.out_lw = P.src.lw.p;
+        pr.out = S.rowres.p;
+        pr.guard = G_DONE;
+        plan_pass(P, pr);
+        PassSpec pc;
+        pc.dir = 0;
+        pc.in_v = S.f.p;
+        pc.in_lw = P.src.lw.p;
+        pc.out_v = S.g.p;
+        pc.out_lw = P.tgt.lw.p;
+        pc.out = S.colres.p;
+        pc.guard = G_DONE;
+        plan_pass(P, pc);
+        count_launch();
+        k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(S.rowres.p, P.src.w.p, n, 1.0, -1.0, S.rowres.p);
+        count_launch();
+        k_axpby<<<grid_for(m), AUX_NT, 0, s>>>(S.colres.p, P.tgt.w.p, m, 1.0, -1.0, S.colres.p);
+    } else {
+        count_launch();
+        k_colres<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.h.p, P.tgt.w.p, m, P.inv_eps(), S.colres.p, P.st,
+                                                G_DONE);
+    }
     double* sums = P.sums.p;
     // marginal_gap (core.cpp:145-150) + Q0 = a.f + b.h, stopping test on device
     {
@@ -1772,7 +1799,7 @@ static bool poll_done(Problem& P) {
 
 static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell, const double* basis,
                           const double* init_f, bool trace_enabled, int64_t trace_cap_hint,
-                          int64_t forced_iters = -1) {
+                          int64_t forced_iters = -1, bool exact_marginals = false) {
     if (!(tol > 0.0) && forced_iters < 0) throw InvalidArgument("solve: tol_omega must be positive");
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
@@ -1783,7 +1810,7 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    enqueue_iteration(P, S, ell, trace_enabled, trace_cap);
+    enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
     CK(cudaStreamEndCapture(s, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
     int64_t batch = 1;
@@ -2273,7 +2300,8 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
     const int64_t ell = use_newton ? cfg->ell : 0;
     SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
-                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1));
+                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1), -1,
+                           cfg->exact_marginals != 0);
     std::memcpy(f_out, o.f.data(), sizeof(double) * P.n_global);
     std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
     if (iterations) *iterations = o.iterations;
@@ -2337,7 +2365,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
             SolveOut o;
             try {
                 o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, bptr, init, cfg->trace_enabled != 0,
-                              cfg->max_iter);
+                              cfg->max_iter, -1, cfg->exact_marginals != 0);
             } catch (const InvalidArgument& e) {
                 throw RuntimeFailure("anneal stage " + std::to_string(s) + ": " + e.what());
             }

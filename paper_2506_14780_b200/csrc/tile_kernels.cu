@@ -171,8 +171,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 template <int KT>
-struct WStride {  // smem row stride of W: rows 64 B apart modulo 128 B -> 2 wavefronts per B load
-    static constexpr int value = (KT % 16 == 0) ? KT + 8 : KT;
+struct WStride {  // smem row stride of W, == 4 (mod 16) doubles: the 16 lanes of a half-warp
+                  // (rows lane>>2, k = lane&3) hit 16 distinct bank pairs for a B-fragment load
+    static constexpr int value = KT + ((4 - KT % 16) + 16) % 16;
 };
 
 constexpr int MMA_NT = 128;  // 4 warps

@@ -311,3 +311,18 @@ def test_sharded_code_path_single_rank_is_bitwise_identical():
         assert np.array_equal(sk.ctransform_of_g(shp, g), sk.ctransform_of_g(ref, g))
     finally:
         sk.comm_destroy()
+
+
+def test_exact_marginals_mode_matches_fused_and_oracle():
+    """exact_marginals evaluates the stopping rule from explicit plan sums like the
+    reference; the fused default must stop at the same iteration."""
+    inst = G.config("C1", n=256, m=256)
+    gp, op = points_pair(inst)
+    rf = sk.solve(gp, tol=1e-9)
+    re_ = sk.solve(gp, tol=1e-9, exact_marginals=True)
+    ro = O.solve(op, tol=1e-9)
+    assert rf.iterations == re_.iterations == ro["iterations"]
+    for a, b, c in zip(rf.trace, re_.trace, ro["trace"]):
+        # the gap is a difference of nearly equal sums: absolute rounding floor ~1e-15
+        assert abs(b.marginal_error - c[0]) <= 1e-9 * c[0] + 1e-15
+        assert abs(a.marginal_error - c[0]) <= 1e-6 * c[0] + 1e-15
