@@ -279,27 +279,34 @@ def run_ours(args, world, rank, local):
            "path": "PointProblem(host arrays) + sknr_solve(max_iter=K) + f,g download, wall clock"}
     del p2
 
-    # ---- time to tolerance on C1 (SK and SK-NR(10) with eps'=2eps warm start + basis)
+    # ---- time to tolerance: C1 (reference basis method) and C3 (Chebyshev-filtered basis)
     ttt = None
     if not args.no_ttt and rank == 0:
-        c1 = G.config("C1")
-        p1 = sk.PointProblem(c1.x, c1.y, c1.alpha, c1.beta, c1.epsilon)
-        t0 = time.perf_counter()
-        r_sk = sk.solve(p1, tol=1e-9, trace=False)
-        t_sk = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        p1w = sk.PointProblem(c1.x, c1.y, c1.alpha, c1.beta, c1.basis_eps)
-        warm = sk.solve(p1w, tol=1e-9, trace=False)
-        b1 = sk.top_modes(p1w, warm.f, warm.g, c1.ell)
-        t_basis = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        r_nr = sk.solve(p1, tol=1e-9, ell=c1.ell, basis=b1, init=(warm.f, warm.g), trace=False)
-        t_nr = time.perf_counter() - t0
-        ttt = {"config": "C1 n=m=512 eps=1e-2 tol=1e-9 (L2-sum marginal error)",
-               "sk": {"iterations": r_sk.iterations, "converged": r_sk.converged, "ms": t_sk * 1e3},
-               "sknr": {"ell": c1.ell, "iterations": r_nr.iterations, "converged": r_nr.converged,
-                        "ms_main_solve": t_nr * 1e3, "ms_end_to_end": (t_nr + t_basis) * 1e3,
-                        "warm_iterations": warm.iterations, "basis_sweeps": b1.sweeps}}
+        ttt = {}
+        for name, method in (("C1", "subspace"), ("C3", "chebyshev")):
+            c = G.config(name)
+            p1 = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale)
+            t0 = time.perf_counter()
+            r_sk = sk.solve(p1, tol=1e-9, trace=False)
+            t_sk = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            p1w = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps, c.cost_scale)
+            warm = sk.solve(p1w, tol=1e-9, trace=False)
+            t_warm = time.perf_counter() - t0
+            b1 = sk.top_modes(p1w, warm.f, warm.g, c.ell, method=method)
+            t_basis = time.perf_counter() - t0 - t_warm
+            t0 = time.perf_counter()
+            r_nr = sk.solve(p1, tol=1e-9, ell=c.ell, basis=b1, init=(warm.f, warm.g), trace=False)
+            t_nr = time.perf_counter() - t0
+            ttt[name] = {"n": c.n, "m": c.m, "d": c.x.shape[1], "epsilon": c.epsilon, "tol": 1e-9,
+                         "sk": {"iterations": r_sk.iterations, "converged": r_sk.converged, "ms": t_sk * 1e3},
+                         "sknr": {"ell": c.ell, "iterations": r_nr.iterations, "converged": r_nr.converged,
+                                  "ms_main_solve": t_nr * 1e3,
+                                  "ms_end_to_end": (t_warm + t_basis + t_nr) * 1e3,
+                                  "warm_eps": c.basis_eps, "warm_iterations": warm.iterations,
+                                  "warm_ms": t_warm * 1e3, "basis_method": method,
+                                  "basis_operator_applications": b1.sweeps, "basis_ms": t_basis * 1e3}}
+            del p1, p1w
 
     # ---- CPU baseline: oracle, 1 core (the reference is single-threaded by design)
     cpu = None

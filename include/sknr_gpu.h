@@ -106,6 +106,14 @@ int sknr_top_modes(sknr_problem p, const double* f, const double* g, int64_t ell
                    double* vectors_sym /* n x ell */, double* rhos /* ell */,
                    int64_t* sweeps /* may be NULL */);
 
+/* Opt-in accelerated variant (not in the reference): method 1 = Chebyshev-
+ * filtered subspace iteration of polynomial degree `degree` (same Rayleigh-Ritz,
+ * same residual test, same returned basis semantics); method 0 = top_modes.
+ * `sweeps` counts operator applications R~R~^T in both cases. */
+int sknr_top_modes_ex(sknr_problem p, const double* f, const double* g, int64_t ell, double tol,
+                      int64_t max_power_iters, int method, int degree, double* vectors,
+                      double* vectors_sym, double* rhos, int64_t* sweeps);
+
 /* ---------------------------------------------------------------- solver.hpp */
 typedef struct {
     double tol_omega;      /* 1e-9   (SolverConfig, solver.hpp:13-19) */

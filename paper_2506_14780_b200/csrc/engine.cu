@@ -1433,29 +1433,90 @@ struct Basis {
     int64_t sweeps = 0;
 };
 
-// top_modes (spectral.cpp:125-193) on device; f, g are device vectors.
-static Basis top_modes_device(Problem& P, const double* f, const double* g, int64_t ell, double tol,
-                              int64_t max_power_iters) {
+// Y = R~ R~^T X with the Perron direction sqrt(alpha) deflated (spectral.cpp:150-151):
+// two DMMA block passes (column then row direction) and a rank-one correction.
+struct OpWork {
+    DBuf Z, W;
+};
+
+static void apply_sym_sym(Problem& P, const double* f, const double* g, const double* X, double* Y,
+                          int block, int kt, OpWork& ow) {
     const int64_t n = P.n, m = P.m;
+    cudaStream_t s = P.stream;
+    ow.Z.ensure(m * block);
+    ow.W.ensure(std::max(n, m) * kt);
+    // Z = R~^T X : z_j = sqrt(b_j) sum_i sqrt(a_i) e^{(f_i+g_j-C_ij)/eps} X_i
+    count_launch();
+    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(X, n, n, block, kt, nullptr, ow.W.p);
+    PassSpec zt;
+    zt.dir = 0;
+    zt.in_v = f;
+    zt.in_lw = P.src.lsw.p;
+    zt.out_v = g;
+    zt.W = ow.W.p;
+    zt.k = block;
+    zt.kt = kt;
+    zt.out_scale = P.tgt.sw.p;
+    zt.out = ow.Z.p;
+    plan_pass(P, zt);
+    // Y = R~ Z : y_i = sum_j sqrt(a_i) e^{..} sqrt(b_j) z_j
+    count_launch();
+    k_pack_w<<<grid_for(m * kt), AUX_NT, 0, s>>>(ow.Z.p, m, m, block, kt, P.tgt.sw.p, ow.W.p);
+    PassSpec yr;
+    yr.dir = 1;
+    yr.in_v = g;
+    yr.out_v = f;
+    yr.out_lw = P.src.lsw.p;
+    yr.W = ow.W.p;
+    yr.k = block;
+    yr.kt = kt;
+    yr.out = Y;
+    plan_pass(P, yr);
+    // Y -= sqrt(a) (sqrt(a)^T Y)
+    gram(P, n, block, 1, Y, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
+    count_launch();
+    k_deflate<<<grid_for(n * block), AUX_NT, 0, s>>>(Y, n, block, P.src.sw.p, P.misc.p);
+}
+
+// Chebyshev three-term step: out = a * (AY - c * Y) - b * Yprev
+__global__ void k_cheb_step(const double* AY, const double* Y, const double* Yprev, int64_t count, double a,
+                            double c, double b, double* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = a * (AY[i] - c * Y[i]) - (Yprev ? b * Yprev[i] : 0.0);
+}
+
+// top_modes (spectral.cpp:125-193) on device; f, g are device vectors.
+// method 0: the reference's block subspace iteration (one operator application
+// per sweep; `sweeps` counts them). method 1 (opt-in, not in the reference):
+// Chebyshev-filtered subspace iteration -- each outer step applies a degree-q
+// Chebyshev polynomial of R~R~^T that damps the unwanted interval [0, theta_k]
+// (theta_k = smallest Ritz value of the block) before the same Rayleigh-Ritz
+// and the same residual test; `sweeps` then counts operator applications.
+static Basis top_modes_device(Problem& P, const double* f, const double* g, int64_t ell, double tol,
+                              int64_t max_power_iters, int method = 0, int degree = 8) {
+    const int64_t n = P.n;
     if (ell < 1) throw InvalidArgument("top_modes: ell must be >= 1");
     if (ell >= n) throw InvalidArgument("top_modes: ell must be < n");
     if (max_power_iters < 0) max_power_iters = 500 * ell;
     const int block = static_cast<int>(std::min<int64_t>(ell + 5, n - 1));
     if (block > 64) throw InvalidArgument("top_modes: ell + 5 > 64 is not supported by sknr_b200");
+    if (degree < 1) degree = 1;
     const int kt = block_kt_for(block);
     cudaStream_t s = P.stream;
-    DBuf X, Y, Z, W, XW, YW, R, Wd, th;
+    DBuf X, Y, Y2, XW, YW, R, Wd, th, Wfull;
     X.ensure(n * block);
     Y.ensure(n * block);
-    Z.ensure(m * block);
-    W.ensure(std::max(n, m) * kt);
+    Y2.ensure(n * block);
     XW.ensure(n * ell);
     YW.ensure(n * ell);
     R.ensure(n * ell);
     Wd.ensure(block * ell);
+    Wfull.ensure(block * block);
     th.ensure(ell);
     P.misc.ensure(256);
     QrWork qw;
+    OpWork ow;
     qw.backup.ensure(static_cast<size_t>(n) * block);
     count_launch();
     k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull);
@@ -1468,48 +1529,16 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
     bool ok = false;
     Basis out;
     std::vector<double> theta(ell), w(block * ell);
-    for (int64_t sweep = 0; sweep < max_power_iters; ++sweep) {
-        out.sweeps = sweep + 1;
-        // Z = R~^T X : z_j = sqrt(b_j) sum_i sqrt(a_i) e^{(f_i+g_j-C_ij)/eps} X_i
-        count_launch();
-        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(X.p, n, n, block, kt, nullptr, W.p);
-        PassSpec zt;
-        zt.dir = 0;
-        zt.in_v = f;
-        zt.in_lw = P.src.lsw.p;
-        zt.out_v = g;
-        zt.out_lw = nullptr;
-        zt.W = W.p;
-        zt.k = block;
-        zt.kt = kt;
-        zt.out_scale = P.tgt.sw.p;
-        zt.out = Z.p;
-        plan_pass(P, zt);
-        // Y = R~ Z : y_i = sum_j sqrt(a_i) e^{..} sqrt(b_j) z_j
-        count_launch();
-        k_pack_w<<<grid_for(m * kt), AUX_NT, 0, s>>>(Z.p, m, m, block, kt, P.tgt.sw.p, W.p);
-        PassSpec yr;
-        yr.dir = 1;
-        yr.in_v = g;
-        yr.in_lw = nullptr;
-        yr.out_v = f;
-        yr.out_lw = P.src.lsw.p;
-        yr.W = W.p;
-        yr.k = block;
-        yr.kt = kt;
-        yr.out = Y.p;
-        plan_pass(P, yr);
-        // Y -= sqrt(a) (sqrt(a)^T Y)
-        gram(P, n, block, 1, Y.p, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
-        count_launch();
-        k_deflate<<<grid_for(n * block), AUX_NT, 0, s>>>(Y.p, n, block, P.src.sw.p, P.misc.p);
-        // Rayleigh-Ritz
+    int64_t applications = 0;
+    while (applications < max_power_iters) {
+        apply_sym_sym(P, f, g, X.p, Y.p, block, kt, ow);  // Y = A X
+        ++applications;
+        // Rayleigh-Ritz on the current orthonormal block
         gram(P, n, block, block, X.p, n, Y.p, n, nullptr, T.p, 0);
         download(hT.data(), T.p, block * block, s);
         CK(cudaStreamSynchronize(s));
         for (int a = 0; a < block; ++a)
-            for (int b = 0; b < block; ++b)
-                ts[a + b * block] = 0.5 * (hT[a + b * block] + hT[b + a * block]);
+            for (int b = 0; b < block; ++b) ts[a + b * block] = 0.5 * (hT[a + b * block] + hT[b + a * block]);
         host_sym_eig(ts, block, evals, evecs);
         for (int a = 0; a < ell; ++a) {
             for (int r = 0; r < block; ++r) w[r + a * block] = evecs[r + (block - 1 - a) * block];
@@ -1535,9 +1564,42 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
             ok = true;
             break;
         }
-        CK(cudaMemcpyAsync(X.p, Y.p, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
+        const bool tiny_gap = evals[0] < 1e-3 * evals[block - 1];  // fast decay: plain steps suffice
+        if (method == 0 || tiny_gap || applications + degree > max_power_iters) {
+            CK(cudaMemcpyAsync(X.p, Y.p, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
+        } else {
+            // rotate to the full Ritz basis, then filter with T_q on [0, theta_min]
+            upload(Wfull.p, evecs.data(), block * block, s);
+            count_launch();
+            k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * block, s>>>(X.p, n, block, Wfull.p,
+                                                                                    block, Y2.p);
+            count_launch();
+            k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * block, s>>>(Y.p, n, block, Wfull.p,
+                                                                                    block, X.p);
+            // now Y2 = X W (basis), X = A X W (its image)
+            const double lo = 0.0, hi = std::max(evals[0], 0.0);
+            const double e = 0.5 * (hi - lo), c = 0.5 * (hi + lo);
+            double* Yprev = Y2.p;   // T_0 term
+            double* Ycur = Y.p;     // T_1 term
+            count_launch();
+            k_cheb_step<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, Y2.p, nullptr, n * block, 1.0 / e, c, 0.0,
+                                                               Ycur);
+            double* spare = X.p;
+            for (int q = 2; q <= degree; ++q) {
+                apply_sym_sym(P, f, g, Ycur, spare, block, kt, ow);  // spare = A Ycur
+                ++applications;
+                count_launch();
+                k_cheb_step<<<grid_for(n * block), AUX_NT, 0, s>>>(spare, Ycur, Yprev, n * block, 2.0 / e, c, 1.0,
+                                                                   spare);
+                std::swap(Yprev, Ycur);
+                std::swap(Ycur, spare);
+            }
+            if (Ycur != X.p)
+                CK(cudaMemcpyAsync(X.p, Ycur, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
+        }
         device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
     }
+    out.sweeps = applications;
     if (!ok)
         throw EigenFailure(
             "top_modes: no convergence within max_power_iters, best residual " + std::to_string(best),
@@ -2254,9 +2316,19 @@ int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const
     SKNR_API_END
 }
 
+int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
+                      int64_t max_power_iters, int method, int degree, double* vectors, double* vectors_sym,
+                      double* rhos, int64_t* sweeps);
+
 int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
                    int64_t max_power_iters, double* vectors, double* vectors_sym, double* rhos,
                    int64_t* sweeps) {
+    return sknr_top_modes_ex(h, f, g, ell, tol, max_power_iters, 0, 1, vectors, vectors_sym, rhos, sweeps);
+}
+
+int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
+                      int64_t max_power_iters, int method, int degree, double* vectors, double* vectors_sym,
+                      double* rhos, int64_t* sweeps) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
@@ -2268,7 +2340,8 @@ int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell
     dg.ensure(P.m);
     upload(df.p, f, P.n, P.stream);
     upload(dg.p, g, P.m, P.stream);
-    Basis b = top_modes_device(P, df.p, dg.p, ell, tol, max_power_iters);
+    if (method < 0 || method > 1) throw InvalidArgument("top_modes: method must be 0 (subspace) or 1 (chebyshev)");
+    Basis b = top_modes_device(P, df.p, dg.p, ell, tol, max_power_iters, method, degree);
     std::memcpy(vectors, b.vectors.data(), sizeof(double) * P.n * ell);
     std::memcpy(vectors_sym, b.vectors_sym.data(), sizeof(double) * P.n * ell);
     std::memcpy(rhos, b.rhos.data(), sizeof(double) * ell);

@@ -326,3 +326,17 @@ def test_exact_marginals_mode_matches_fused_and_oracle():
         # the gap is a difference of nearly equal sums: absolute rounding floor ~1e-15
         assert abs(b.marginal_error - c[0]) <= 1e-9 * c[0] + 1e-15
         assert abs(a.marginal_error - c[0]) <= 1e-6 * c[0] + 1e-15
+
+
+def test_chebyshev_top_modes_matches_subspace():
+    """Opt-in Chebyshev filtering returns the same basis (same residual test) with
+    fewer operator applications."""
+    inst = G.config("C1", n=400, m=400)
+    gp, op = points_pair(inst)
+    gp.set_epsilon(0.02)
+    r = O.solve(op.with_epsilon(0.02), tol=1e-12)
+    b0 = sk.top_modes(gp, r["f"], r["g"], 10)
+    b1 = sk.top_modes(gp, r["f"], r["g"], 10, method="chebyshev", degree=8)
+    assert np.max(np.abs(b0.rhos - b1.rhos)) <= 1e-8
+    assert projector_distance(b0.vectors_sym, b1.vectors_sym) <= 1e-6
+    assert b1.sweeps <= b0.sweeps
