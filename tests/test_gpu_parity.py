@@ -340,3 +340,62 @@ def test_chebyshev_top_modes_matches_subspace():
     assert np.max(np.abs(b0.rhos - b1.rhos)) <= 1e-8
     assert projector_distance(b0.vectors_sym, b1.vectors_sym) <= 1e-6
     assert b1.sweeps <= b0.sweeps
+
+
+@pytest.mark.parametrize("d,n,m", [(1, 300, 200), (4, 257, 301), (5, 120, 90), (2, 1, 7), (3, 9, 1)])
+def test_points_dimensions_and_ragged_shapes(d, n, m):
+    """d = 1..4 run the register-resident on-the-fly kernels; d = 5 materialises
+    the cost on device; n != m and single-point sides exercise tile edges."""
+    rng = np.random.default_rng(d * 1000 + n)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, d)))
+    y = np.asfortranarray(rng.normal(0, 0.7, (m, d)))
+    a = rng.uniform(0.5, 1.5, n)
+    a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m)
+    b /= b.sum()
+    gp = sk.PointProblem(x, y, a, b, 0.05)
+    op = O.Instance(a, b, 0.05, x=x, y=y)
+    f = rng.uniform(-0.1, 0.1, n)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(sk.ctransform_of_f(gp, f), g_ref) <= 1e-12
+    assert rel_err(sk.ctransform_of_g(gp, g_ref), O.ctransform_of_g(op, g_ref)) <= 1e-12
+    rg = sk.solve(gp, tol=1e-10, max_iter=5000)
+    ro = O.solve(op, tol=1e-10, max_iter=5000)
+    assert rg.iterations == ro["iterations"] and rg.converged == ro["converged"]
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT
+
+
+def test_cost_scale_matches_divided_cost():
+    """C2's max-normalised cost: PointProblem(cost_scale=1/cmax) vs the dense cost
+    built by division (generators.cpp:101 then / max)."""
+    inst = G.config("C2", n=300, m=300)
+    gp = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, 0.01, inst.cost_scale)
+    cost = G.sq_euclidean_cost(inst.x, inst.y, inst.cost_scale)
+    dp = sk.Problem(cost, inst.alpha, inst.beta, 0.01)
+    f = np.linspace(-0.05, 0.05, 300)
+    assert rel_err(sk.ctransform_of_f(gp, f), sk.ctransform_of_f(dp, f)) <= 1e-12
+
+
+def test_negative_and_shifted_costs():
+    """Costs may be negative (types.hpp:31-33); a constant shift of C shifts g."""
+    rng = G.SplitMix64(5)
+    cost, a, b = random_problem_data(rng, 40, 30)
+    p1 = sk.Problem(cost, a, b, 0.1)
+    p2 = sk.Problem(cost - 3.0, a, b, 0.1)
+    f = random_vector(rng, 40, 0.2)
+    g1 = sk.ctransform_of_f(p1, f)
+    g2 = sk.ctransform_of_f(p2, f)
+    assert np.max(np.abs((g2 + 3.0) - g1)) <= 1e-12
+
+
+def test_invalid_inputs_raise():
+    with pytest.raises(ValueError):
+        sk.Problem(np.zeros((0, 3)), [], [1 / 3] * 3, 1.0)
+    with pytest.raises(ValueError, match="entries must be finite"):
+        sk.Problem(np.array([[np.inf, 0.0], [0.0, 0.0]]), [0.5, 0.5], [0.5, 0.5], 1.0)
+    cost, a, b = symmetric_2x2()
+    gp = sk.Problem(cost, a, b, 1.0)
+    with pytest.raises(ValueError, match="length mismatch"):
+        sk.ctransform_of_f(gp, [0.0, 0.0, 0.0])
+    with pytest.raises(ValueError, match="ell must be < n"):
+        sk.top_modes(gp, [0.0, 0.0], [0.0, 0.0], 2)
