@@ -26,7 +26,7 @@ import numpy as np
 __version__ = "0.1.0"
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libsknr_b200.so")
+_LIB_PATH = os.environ.get("SKNR_B200_LIB", os.path.join(_HERE, "libsknr_b200.so"))
 _lib = None
 
 SKNR_OK, SKNR_EINVAL, SKNR_EEIGEN, SKNR_ECUDA, SKNR_ENCCL, SKNR_ERUNTIME = 0, 1, 2, 3, 4, 5

@@ -22,20 +22,40 @@
 
 namespace sknr {
 
+// Table resolution: SKNR_TB = 8 -> 256 entries x 16 replicas (32 KiB), degree-4
+// polynomial (11 FP64 slots per cell); SKNR_TB = 10 -> 1024 entries x 8 replicas
+// (64 KiB), degree-3 minimax polynomial (10 slots per cell).
+#ifndef SKNR_TB
+#define SKNR_TB 8
+#endif
+constexpr int kTB = SKNR_TB;
+#if SKNR_TB == 10
+constexpr double kLS = 1477.3197218702985;       // 1024 * log2(e)
+constexpr double kInvLS = 1.0 / 1477.3197218702985;
+constexpr double kMagicB = 6755399442103296.0;   // 1.5 * 2^52 + 1023 * 1024
+constexpr int kKcMax = 2046 * 1024 + 1023;
+constexpr int kTabRep = 8;
+// minimax-adjusted coefficients of 2^(r/1024), |r| <= 1/2 (max rel. error 1.4e-16)
+constexpr double kP1 = 0.0006769015435155716;
+constexpr double kP2 = 2.29097851993791e-07;
+constexpr double kP3 = 5.1692229383458926e-11;
+constexpr double kP4 = 0.0;
+#else
 constexpr double kLS = 369.3299304675746;       // 256 * log2(e)
 constexpr double kInvLS = 1.0 / 369.3299304675746;
 constexpr double kMagicB = 6755399441317632.0;  // 1.5 * 2^52 + 1023 * 256
-constexpr int kMagicHi = 0x43380000;            // hi word of 1.5 * 2^52
 constexpr int kKcMax = 2046 * 256 + 255;        // largest biased k before the exponent field overflows
-constexpr int kTabEntries = 256;
 constexpr int kTabRep = 16;
-constexpr int kTabWords = kTabEntries * kTabRep;  // 32 KiB of shared memory
-
 // (ln2/256)^k / k!
 constexpr double kP1 = 0.0027076061740622863;
 constexpr double kP2 = 3.6655655969101062e-06;
 constexpr double kP3 = 3.3083026805413713e-09;
 constexpr double kP4 = 2.239395190875157e-12;
+#endif
+constexpr int kMagicHi = 0x43380000;            // hi word of 1.5 * 2^52
+constexpr int kTabEntries = 1 << kTB;
+constexpr int kTabWords = kTabEntries * kTabRep;
+constexpr int kRepShift = (kTabRep == 16) ? 7 : 6;  // log2(kTabRep * 8 bytes)
 
 // Device flags / scalars of one problem handle. Kernels consult them through
 // a guard word so a whole iteration can live in one CUDA graph: work that is
@@ -103,17 +123,34 @@ __device__ __forceinline__ void pexp_parts(double u, const unsigned long long* _
     const double t = u + kMagicB;
     const double kf = t - kMagicB;
     const double r = u - kf;
+#if SKNR_TB == 10
+    p = fma(r, kP3, c3);  // c3 holds kP2 in a register
+    p = fma(p, r, kP1);
+    p = fma(p, r, 1.0);
+#else
     p = fma(r, kP4, c3);
     p = fma(p, r, kP2);
     p = fma(p, r, kP1);
     p = fma(p, r, 1.0);
+#endif
     int kc = FASTCLAMP ? max(__double2loint(t), 0)
                        : ((__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0);
     if (HI_CLAMP) kc = min(kc, kKcMax);
-    const unsigned s = static_cast<unsigned>(kc) << 12;
-    const unsigned off = ((s >> 5) & 0x7F80u) | laneoff;
+    const unsigned s = static_cast<unsigned>(kc) << (20 - kTB);
+    const unsigned off = ((s >> (20 - kTB - kRepShift)) & (((1u << kTB) - 1u) << kRepShift)) | laneoff;
     const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
     Tp = __hiloint2double(static_cast<int>((s & 0xFFF00000u) | T.y), static_cast<int>(T.x));
+}
+
+// register-resident first Horner constant for pexp_parts
+__device__ __forceinline__ double pexp_c3() {
+#if SKNR_TB == 10
+    double v = kP2;
+#else
+    double v = kP3;
+#endif
+    asm volatile("" : "+d"(v));
+    return v;
 }
 
 template <bool HI_CLAMP>

@@ -30,12 +30,16 @@
 namespace sknr {
 
 __constant__ unsigned long long c_exp2_tab[kTabEntries] = {
+#if SKNR_TB == 10
+#include "exp2_table1024.inc"
+#else
 #include "exp2_table.inc"
+#endif
 };
 
-// Fill the replicated table: tab[e*16 + r] = mantissa bits of 2^(e/256).
+// Fill the replicated table: tab[e*kTabRep + r] = mantissa bits of 2^(e/2^kTB).
 __device__ __forceinline__ void load_exp2_table(unsigned long long* tab, int tid, int nthreads) {
-    for (int t = tid; t < kTabWords; t += nthreads) tab[t] = c_exp2_tab[t >> 4];
+    for (int t = tid; t < kTabWords; t += nthreads) tab[t] = c_exp2_tab[t / kTabRep];
 }
 
 namespace {
@@ -79,8 +83,8 @@ __global__ void __launch_bounds__(NTT) pts_tile_kernel(TileArgs a) {
     double* sw = sin + CH * PK;
     const int tid = threadIdx.x;
     load_exp2_table(tab, tid, NT);
-    const unsigned laneoff = (tid & 15) << 3;
-    const double c3 = reg_const(kP3);
+    const unsigned laneoff = (tid & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
     const int64_t out_tile = static_cast<int64_t>(NT) * JT;
 
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -193,8 +197,8 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
     double* sw = sin + MMA_CH * PK;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     load_exp2_table(tab, tid, MMA_NT);
-    const unsigned laneoff = (lane & 15) << 3;
-    const double c3 = reg_const(kP3);
+    const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
     const int row = lane >> 2, kq = lane & 3;
 
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -281,8 +285,8 @@ __global__ void __launch_bounds__(NT_of<MODE>::value) dense_tile_kernel(TileArgs
     double* sw = sin + CH;
     const int tid = threadIdx.x;
     load_exp2_table(tab, tid, NT);
-    const unsigned laneoff = (tid & 15) << 3;
-    const double c3 = reg_const(kP3);
+    const unsigned laneoff = (tid & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
     const int64_t out_tile = static_cast<int64_t>(NT) * JT;
     const double nk = -a.kappa;
 
