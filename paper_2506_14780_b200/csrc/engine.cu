@@ -2615,7 +2615,8 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    if (P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
+    if (variant < 100 && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
+    if (variant >= 100 && P.dim != 0) throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     DBuf f, g;

@@ -29,3 +29,29 @@ out = {"config": "C2 n=m=4096, eps " + str(eps) + ", warm=spectral, ell=16, tol=
        "rel_f": rel}
 print(json.dumps(out), flush=True)
 json.dump(out, open(os.path.join(ROOT, "gpurun_out", "c2_anneal_parity_r01.json"), "w"), indent=1)
+
+# Second comparison: the same stage logic with the oracle's basis handed to the GPU
+# solve (isolates the top_modes rounding: ~1e-8 residual-level basis differences).
+prev = None
+basis_o = None
+shared = {"iterations_gpu": [], "iterations_oracle": [], "rel_f": [], "last_gap_gpu": [], "last_gap_oracle": []}
+for s, e in enumerate(eps):
+    gp.set_epsilon(e)
+    if s == 0:
+        rg = sk.solve(gp, tol=1e-9)
+        ro = O.solve(op.with_epsilon(e), tol=1e-9)
+    else:
+        if basis_o is None:
+            basis_o = O.top_modes(op.with_epsilon(eps[s - 1]), prev["f"], prev["g"], inst.ell)
+        sb = sk.SpectralBasis(basis_o["vectors"], basis_o["vectors_sym"], basis_o["rhos"], eps[s - 1])
+        rg = sk.solve(gp, tol=1e-9, ell=inst.ell, basis=sb, init=(prev["f"], prev["g"]))
+        ro = O.solve(op.with_epsilon(e), tol=1e-9, ell=inst.ell, V=basis_o["vectors"], init=(prev["f"], prev["g"]))
+    shared["iterations_gpu"].append(rg.iterations)
+    shared["iterations_oracle"].append(ro["iterations"])
+    shared["rel_f"].append(float(np.max(np.abs(rg.f - ro["f"])) / np.max(np.abs(ro["f"]))))
+    shared["last_gap_gpu"].append([t.marginal_error for t in rg.trace[-2:]])
+    shared["last_gap_oracle"].append([t[0] for t in ro["trace"][-2:]])
+    prev = ro
+out["shared_basis"] = shared
+print(json.dumps(shared), flush=True)
+json.dump(out, open(os.path.join(ROOT, "gpurun_out", "c2_anneal_parity_r01.json"), "w"), indent=1)
