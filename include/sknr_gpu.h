@@ -70,10 +70,17 @@ int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const do
 int sknr_problem_create_points(const double* x, const double* y, int64_t n, int64_t m,
                                int64_t d, double cost_scale, const double* alpha,
                                const double* beta, double epsilon, sknr_problem* out);
+/* cost_mode: 0 auto (d <= 4: cost evaluated in registers; d > 4: stored on
+ * device if 2 n m doubles fit, else on the fly), 1 stored, 2 on the fly (d > 4:
+ * the x.y contraction runs on FP64 tensor cores, mma.sync m8n8k4). */
+int sknr_problem_create_points_ex(const double* x, const double* y, int64_t n, int64_t m,
+                                  int64_t d, double cost_scale, const double* alpha,
+                                  const double* beta, double epsilon, int cost_mode,
+                                  sknr_problem* out);
 /* EotProblem::with_epsilon (types.hpp:60-62) without the dense-cost copy. */
 int sknr_problem_set_epsilon(sknr_problem p, double epsilon);
 int sknr_problem_info(sknr_problem p, int64_t* n, int64_t* m, int64_t* d, double* epsilon,
-                      int* kind /* 0 dense, 1 points */);
+                      int* kind /* 0 stored cost, 1 on the fly (registers), 2 on the fly (DMMA) */);
 int sknr_problem_destroy(sknr_problem p);
 
 /* ---------------------------------------------------------------- core.hpp

@@ -77,6 +77,8 @@ _SIGS = {
     "sknr_problem_create_dense": [_D, _I64, _I64, _D, _D, ctypes.c_double, ctypes.POINTER(_P)],
     "sknr_problem_create_points": [_D, _D, _I64, _I64, _I64, ctypes.c_double, _D, _D,
                                    ctypes.c_double, ctypes.POINTER(_P)],
+    "sknr_problem_create_points_ex": [_D, _D, _I64, _I64, _I64, ctypes.c_double, _D, _D,
+                                      ctypes.c_double, ctypes.c_int, ctypes.POINTER(_P)],
     "sknr_problem_set_epsilon": [_P, ctypes.c_double],
     "sknr_problem_info": [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                           _D, ctypes.POINTER(ctypes.c_int)],
@@ -235,7 +237,7 @@ class Problem:
     @classmethod
     def _clone(cls, p: "Problem", eps: float):
         if isinstance(p, PointProblem):
-            return PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale)
+            return PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale, p._cost_mode)
         return Problem(p._cost, p._alpha, p._beta, eps)
 
     def set_epsilon(self, epsilon: float) -> None:
@@ -261,7 +263,14 @@ class PointProblem(Problem):
 
     _kind = 1
 
-    def __init__(self, x, y, alpha, beta, epsilon: float, cost_scale: float = 1.0):
+    COST_MODES = {"auto": 0, "stored": 1, "onthefly": 2}
+
+    def __init__(self, x, y, alpha, beta, epsilon: float, cost_scale: float = 1.0, cost_mode: str = "auto"):
+        """cost_mode: "auto" (d <= 4 in registers; d > 4 stored when 2nm doubles fit in
+        HBM, else on the fly), "stored", "onthefly" (d > 4: x.y contraction on FP64
+        tensor cores)."""
+        if cost_mode not in self.COST_MODES:
+            raise ValueError("cost_mode must be auto|stored|onthefly")
         x, y = _mat_f(x), _mat_f(y)
         if x.ndim == 1:
             x = x.reshape(-1, 1, order="F")
@@ -275,10 +284,12 @@ class PointProblem(Problem):
         if a.size != n or b.size != m:
             raise ValueError("EotProblem: measure sizes must match cost shape")
         h = _P()
-        _check(lib().sknr_problem_create_points(_ptr(x), _ptr(y), n, m, d, float(cost_scale), _ptr(a),
-                                                _ptr(b), float(epsilon), ctypes.byref(h)))
+        _check(lib().sknr_problem_create_points_ex(_ptr(x), _ptr(y), n, m, d, float(cost_scale), _ptr(a),
+                                                   _ptr(b), float(epsilon), self.COST_MODES[cost_mode],
+                                                   ctypes.byref(h)))
         self._init_common(h, n, m, a, b, float(epsilon))
         self._x, self._y, self._cost_scale = x, y, float(cost_scale)
+        self._cost_mode = cost_mode
 
     @property
     def cost(self) -> np.ndarray:
@@ -288,6 +299,13 @@ class PointProblem(Problem):
     @property
     def d(self) -> int:
         return self._x.shape[1]
+
+    @property
+    def cost_path(self) -> str:
+        """Which kernel family evaluates the cost: registers / contraction / stored."""
+        kind = ctypes.c_int()
+        _check(lib().sknr_problem_info(self.handle, None, None, None, None, ctypes.byref(kind)))
+        return {0: "stored", 1: "registers", 2: "contraction"}[kind.value]
 
 
 # ---------------------------------------------------------------- results

@@ -704,11 +704,11 @@ struct Problem {
     DBuf red_tmp, gather_buf;
     std::vector<double> h_alpha, h_beta;  // full host copies (validation, host-side dots)
 
-    bool otf() const { return dim > 0; }  // on-the-fly cost (points, d <= 4)
+    bool otf() const { return dim != 0; }  // on-the-fly cost (dim > 0: registers, dim < 0: DMMA contraction)
     double inv_eps() const { return 1.0 / eps; }
     double kc() const { return otf() ? kappa / eps : 0.0; }
     double sigma() const { return otf() ? std::sqrt(2.0 * kLS * kappa / eps) : 0.0; }
-    int pk() const { return otf() ? (dim + 2) / 2 * 2 : 1; }
+    int pk() const { return dim > 0 ? (dim + 2) / 2 * 2 : (dim < 0 ? -dim + 2 : 1); }
     Side& in_side(int dir) { return dir == 0 ? src : tgt; }
     Side& out_side(int dir) { return dir == 0 ? tgt : src; }
     const double* cost_for(int dir) const { return dir == 0 ? CT.p : C.p; }
@@ -792,7 +792,8 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     return p.release();
 }
 
-static void finish_points(Problem* p, const double* x, const double* y, int64_t d, double cost_scale) {
+static void finish_points(Problem* p, const double* x, const double* y, int64_t d, double cost_scale,
+                          int cost_mode = 0) {
     const int64_t n = p->n, m = p->m;
     p->kind = 1;
     p->d = d;
@@ -828,8 +829,18 @@ static void finish_points(Problem* p, const double* x, const double* y, int64_t 
     upload(p->tgt.coords.p, yc.data(), m * d, p->stream);
     upload(p->src.sq.p, sx.data(), n, p->stream);
     upload(p->tgt.sq.p, sy.data(), m, p->stream);
-    if (d >= 1 && d <= 4) {
+    // cost_mode 0 auto: d <= 4 register kernels, larger d stored (fits: 2 n m 8 B < 1/2 free HBM)
+    // else DMMA contraction; 1 stored; 2 on the fly.
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const bool fits = 2.0 * static_cast<double>(n) * m * 8.0 < 0.5 * static_cast<double>(free_b);
+    int dk = 8;
+    while (dk < d) dk *= 2;
+    const bool contract_ok = d > 4 && dk <= 128;
+    if (cost_mode != 1 && d >= 1 && d <= 4) {
         p->dim = static_cast<int>(d);
+    } else if (contract_ok && (cost_mode == 2 || (cost_mode == 0 && !fits))) {
+        p->dim = -dk;  // coordinates zero-padded to dk in the packs
     } else {
         // No register-resident on-the-fly kernel for this dimension yet: the
         // cost is materialised once on device (both layouts) and streamed.
@@ -2005,10 +2016,21 @@ int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const do
     SKNR_API_END
 }
 
+int sknr_problem_create_points_ex(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                                  double cost_scale, const double* alpha, const double* beta, double epsilon,
+                                  int cost_mode, sknr_problem* out);
+
 int sknr_problem_create_points(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
                                double cost_scale, const double* alpha, const double* beta, double epsilon,
                                sknr_problem* out) {
+    return sknr_problem_create_points_ex(x, y, n, m, d, cost_scale, alpha, beta, epsilon, 0, out);
+}
+
+int sknr_problem_create_points_ex(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
+                                  double cost_scale, const double* alpha, const double* beta, double epsilon,
+                                  int cost_mode, sknr_problem* out) {
     SKNR_API_BEGIN
+    if (cost_mode < 0 || cost_mode > 2) throw InvalidArgument("sknr_problem_create_points: cost_mode must be 0, 1 or 2");
     *out = nullptr;
     if (d < 1) throw InvalidArgument("sq_euclidean_cost: dimension must be >= 1");
     check_finite_vec(x, n * d, "PointCloud(x)");
@@ -2016,7 +2038,7 @@ int sknr_problem_create_points(const double* x, const double* y, int64_t n, int6
     if (!(cost_scale > 0.0) || !std::isfinite(cost_scale))
         throw InvalidArgument("sq_euclidean_cost: cost_scale must be positive");
     std::unique_ptr<Problem> p(new_problem(n, m, alpha, beta, epsilon));
-    finish_points(p.get(), x, y, d, cost_scale);
+    finish_points(p.get(), x, y, d, cost_scale, cost_mode);
     *out = new sknr_problem_s{std::move(p)};
     SKNR_API_END
 }
@@ -2035,11 +2057,12 @@ int sknr_problem_set_epsilon(sknr_problem h, double epsilon) {
 int sknr_problem_info(sknr_problem h, int64_t* n, int64_t* m, int64_t* d, double* epsilon, int* kind) {
     SKNR_API_BEGIN
     Problem& P = get(h);
+    // kind: 0 stored cost (given or materialised), 1 on the fly (registers), 2 on the fly (DMMA contraction)
     if (n) *n = P.n;
     if (m) *m = P.m;
     if (d) *d = P.d;
     if (epsilon) *epsilon = P.eps;
-    if (kind) *kind = P.kind;
+    if (kind) *kind = P.dim > 0 ? 1 : (P.dim < 0 ? 2 : 0);
     SKNR_API_END
 }
 

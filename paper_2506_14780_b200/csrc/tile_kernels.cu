@@ -271,6 +271,235 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
     }
 }
 
+// Stored-cost block pass on DMMA: like pts_mma_kernel, with the A fragment's cell
+// e(o, in) computed from C[o + in*ldc] (one global load per lane per 4 inputs,
+// 8 consecutive outputs per 64 B segment), the next step's loads issued before
+// the current step's math.
+template <int KT, int MB>
+__global__ void __launch_bounds__(MMA_NT) dense_mma_kernel(TileArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int NCB = KT / 8;
+    constexpr int WS = WStride<KT>::value;
+    constexpr int OUT_WARP = 8 * MB;
+    constexpr int OUT_CTA = OUT_WARP * (MMA_NT / 32);
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + kTabWords;
+    double* sw = sin + MMA_CH;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_exp2_table(tab, tid, MMA_NT);
+    const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+    const int row = lane >> 2, kq = lane & 3;
+    const double nk = -a.kappa;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        const int64_t obase = ot * OUT_CTA + warp * OUT_WARP;
+        double Bo[MB];
+        int64_t oc[MB];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t o = obase + mb * 8 + row;
+            oc[mb] = o < a.n_out ? o : a.n_out - 1;
+            Bo[mb] = a.out_pack[oc[mb]];
+        }
+        double acc[MB][NCB][2];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) acc[mb][cb][0] = acc[mb][cb][1] = 0.0;
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += MMA_CH) {
+            const int cnt = static_cast<int>((i1 - c0) < MMA_CH ? (i1 - c0) : MMA_CH);
+            const int cnt4 = (cnt + 3) & ~3;
+            __syncthreads();
+            for (int t = tid; t < cnt4; t += MMA_NT) sin[t] = t < cnt ? a.in_pack[c0 + t] : -1e300;
+            for (int t = tid; t < cnt4 * KT; t += MMA_NT) {
+                const int k = t / KT, c = t % KT;
+                sw[k * WS + c] = k < cnt ? a.W[(c0 + k) * KT + c] : 0.0;
+            }
+            __syncthreads();
+            double cv[MB];
+            {
+                const int64_t in = c0 + (kq < cnt ? kq : cnt - 1);
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) cv[mb] = __ldcs(a.C + in * a.ldc + oc[mb]);
+            }
+            for (int k4 = 0; k4 < cnt4; k4 += 4) {
+                double nv[MB];
+                const int kn = k4 + 4 + kq;
+                const int64_t inn = c0 + (kn < cnt ? kn : cnt - 1);
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) nv[mb] = __ldcs(a.C + inn * a.ldc + oc[mb]);
+                const double ak = sin[k4 + kq];
+                double bf[NCB];
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) bf[cb] = sw[(k4 + kq) * WS + cb * 8 + row];
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    const double u = fma(nk, cv[mb], ak + Bo[mb]);
+                    const double e = pexp<true>(u, tab, laneoff, c3);
+#pragma unroll
+                    for (int cb = 0; cb < NCB; ++cb) dmma_8x8x4(acc[mb][cb][0], acc[mb][cb][1], e, bf[cb]);
+                    cv[mb] = nv[mb];
+                }
+            }
+        }
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t o = obase + mb * 8 + row;
+            if (o >= a.n_out) continue;
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+                const int c = cb * 8 + kq * 2;
+                a.partial[(ib * KT + c) * a.n_out + o] = acc[mb][cb][0];
+                a.partial[(ib * KT + c + 1) * a.n_out + o] = acc[mb][cb][1];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- on-the-fly, large d
+// u = A_in + B_out + <X_in, Y_out> with the d-contraction on FP64 tensor cores:
+// each warp forms 8x8 (output x input) blocks of u with DK/4 DMMAs (A = Y_out
+// fragment, registers; B = X_in fragment, shared memory), then evaluates the
+// exponentials from the accumulator fragment (2 cells per lane). MODE_BLOCK
+// re-shuffles the exponentials into A fragments of a second DMMA chain against
+// W (the ell-wide pass). Pack rows: (A, x_0 .. x_{d-1}, 0-padding), stride DK+2.
+template <int DK>
+struct XStride {  // smem stride of staged X rows: == 4 or 12 (mod 16) -> conflict-free B fragments
+    static constexpr int value = DK + 4;
+};
+
+constexpr int CT_NT = 128;
+constexpr int CT_CH = 64;
+
+template <int DK, int MODE, int KT, int MB>
+__global__ void __launch_bounds__(CT_NT) pts_contract_kernel(TileArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int PK = DK + 2;
+    constexpr int NK = DK / 4;
+    constexpr int XS = XStride<DK>::value;
+    constexpr int KA = KT > 0 ? KT : 8;
+    constexpr int NCB = KA / 8;
+    constexpr int WS = WStride<KA>::value;
+    constexpr int OUT_WARP = 8 * MB;
+    constexpr int OUT_CTA = OUT_WARP * (CT_NT / 32);
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sX = sm + kTabWords;
+    double* sA = sX + CT_CH * XS;
+    double* sw = sA + CT_CH;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_exp2_table(tab, tid, CT_NT);
+    const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+    const int row = lane >> 2, kq = lane & 3;
+    const double ninf = -__longlong_as_double(0x7FF0000000000000LL);
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        const int64_t obase = ot * OUT_CTA + warp * OUT_WARP;
+        double yf[MB][NK], Bo[MB];
+        double acc[MB];
+        double bacc[MB][NCB][2];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            int64_t o = obase + mb * 8 + row;
+            o = o < a.n_out ? o : a.n_out - 1;
+            const double* yo = a.out_pack + o * PK;
+            Bo[mb] = yo[0];
+#pragma unroll
+            for (int kk = 0; kk < NK; ++kk) yf[mb][kk] = yo[1 + kk * 4 + kq];
+            acc[mb] = (MODE == MODE_MAX) ? ninf : 0.0;
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) bacc[mb][cb][0] = bacc[mb][cb][1] = 0.0;
+        }
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += CT_CH) {
+            const int cnt = static_cast<int>((i1 - c0) < CT_CH ? (i1 - c0) : CT_CH);
+            const int cnt8 = (cnt + 7) & ~7;
+            __syncthreads();
+            for (int t = tid; t < cnt8 * DK; t += CT_NT) {
+                const int k = t / DK, q = t % DK;
+                sX[k * XS + q] = k < cnt ? a.in_pack[(c0 + k) * PK + 1 + q] : 0.0;
+            }
+            for (int t = tid; t < cnt8; t += CT_NT) sA[t] = t < cnt ? a.in_pack[(c0 + t) * PK] : -1e300;
+            if (MODE == MODE_BLOCK)
+                for (int t = tid; t < cnt8 * KA; t += CT_NT) {
+                    const int k = t / KA, c = t % KA;
+                    sw[k * WS + c] = k < cnt ? a.W[(c0 + k) * KA + c] : 0.0;
+                }
+            __syncthreads();
+            for (int j8 = 0; j8 < cnt8; j8 += 8) {
+                double xf[NK];
+#pragma unroll
+                for (int kk = 0; kk < NK; ++kk) xf[kk] = sX[(j8 + row) * XS + kk * 4 + kq];
+                const double a0 = sA[j8 + 2 * kq], a1 = sA[j8 + 2 * kq + 1];
+                double wf[2][NCB];
+                if (MODE == MODE_BLOCK) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int cb = 0; cb < NCB; ++cb) wf[h][cb] = sw[(j8 + 4 * h + kq) * WS + cb * 8 + row];
+                }
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < NK; ++kk) dmma_8x8x4(u0, u1, yf[mb][kk], xf[kk]);
+                    u0 += a0 + Bo[mb];
+                    u1 += a1 + Bo[mb];
+                    if (MODE == MODE_SUM) {
+                        acc[mb] = pexp_acc<false>(u0, tab, laneoff, c3, acc[mb]);
+                        acc[mb] = pexp_acc<false>(u1, tab, laneoff, c3, acc[mb]);
+                    } else if (MODE == MODE_MAX) {
+                        acc[mb] = fmax(acc[mb], fmax(u0, u1));
+                    } else {
+                        const double e0 = pexp<true>(u0, tab, laneoff, c3);
+                        const double e1 = pexp<true>(u1, tab, laneoff, c3);
+                        // A fragment of chunk h needs e(row, 4h + kq), held by lane
+                        // row*4 + 2h + kq/2 as element kq&1
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int src = (lane & ~3) + 2 * h + (kq >> 1);
+                            const double s0 = __shfl_sync(0xffffffffu, e0, src);
+                            const double s1 = __shfl_sync(0xffffffffu, e1, src);
+                            const double af = (kq & 1) ? s1 : s0;
+#pragma unroll
+                            for (int cb = 0; cb < NCB; ++cb)
+                                dmma_8x8x4(bacc[mb][cb][0], bacc[mb][cb][1], af, wf[h][cb]);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t o = obase + mb * 8 + row;
+            if (MODE == MODE_BLOCK) {
+                if (o >= a.n_out) continue;
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) {
+                    const int c = cb * 8 + kq * 2;
+                    a.partial[(ib * KA + c) * a.n_out + o] = bacc[mb][cb][0];
+                    a.partial[(ib * KA + c + 1) * a.n_out + o] = bacc[mb][cb][1];
+                }
+            } else {
+                double v = acc[mb];
+                const double w1 = __shfl_xor_sync(0xffffffffu, v, 1);
+                v = (MODE == MODE_MAX) ? fmax(v, w1) : v + w1;
+                const double w2 = __shfl_xor_sync(0xffffffffu, v, 2);
+                v = (MODE == MODE_MAX) ? fmax(v, w2) : v + w2;
+                if (kq == 0 && o < a.n_out) a.partial[ib * a.n_out + o] = v;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- stored cost
 template <int JT, int MODE, int KT>
 __global__ void __launch_bounds__(NT_of<MODE>::value) dense_tile_kernel(TileArgs a) {
@@ -498,6 +727,35 @@ KernelInfo make_mma() {
     return k;
 }
 
+template <int DK, int MODE, int KT, int MB>
+KernelInfo make_contract() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_contract_kernel<DK, MODE, KT, MB>);
+    k.jt = 1;
+    k.nt = CT_NT;
+    k.out_tile = 8 * MB * (CT_NT / 32);
+    constexpr int KA = KT > 0 ? KT : 8;
+    k.smem = static_cast<int>(sizeof(double)) *
+             (kTabWords + CT_CH * XStride<DK>::value + CT_CH + (MODE == MODE_BLOCK ? CT_CH * WStride<KA>::value : 0));
+    return k;
+}
+
+template <int DK>
+KernelInfo pick_contract(int mode, int kt) {
+    if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
+    if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
+    switch (kt) {
+        case 8: return make_contract<DK, MODE_BLOCK, 8, 1>();
+        case 16: return make_contract<DK, MODE_BLOCK, 16, 1>();
+        case 24: return make_contract<DK, MODE_BLOCK, 24, 1>();
+        case 32: return make_contract<DK, MODE_BLOCK, 32, 1>();
+        case 40: return make_contract<DK, MODE_BLOCK, 40, 1>();
+        case 48: return make_contract<DK, MODE_BLOCK, 48, 1>();
+        case 64: return make_contract<DK, MODE_BLOCK, 64, 1>();
+        default: return KernelInfo{};
+    }
+}
+
 template <int D>
 KernelInfo pick_pts(int mode, int kt) {
     // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
@@ -525,17 +783,28 @@ KernelInfo make_dense_v2() {
     return k;
 }
 
+template <int KT, int MB>
+KernelInfo make_dense_mma() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&dense_mma_kernel<KT, MB>);
+    k.jt = 1;
+    k.nt = MMA_NT;
+    k.out_tile = 8 * MB * (MMA_NT / 32);
+    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + MMA_CH + MMA_CH * WStride<KT>::value);
+    return k;
+}
+
 KernelInfo pick_dense(int mode, int kt) {
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
-    switch (kt) {
-        case 8: return make_dense<2, MODE_BLOCK, 8>();
-        case 16: return make_dense<1, MODE_BLOCK, 16>();
-        case 24: return make_dense<1, MODE_BLOCK, 24>();
-        case 32: return make_dense<1, MODE_BLOCK, 32>();
-        case 40: return make_dense<1, MODE_BLOCK, 40>();
-        case 48: return make_dense<1, MODE_BLOCK, 48>();
-        case 64: return make_dense<1, MODE_BLOCK, 64>();
+    switch (kt) {  // FP64 tensor-core (DMMA) block pass
+        case 8: return make_dense_mma<8, 4>();
+        case 16: return make_dense_mma<16, 4>();
+        case 24: return make_dense_mma<24, 4>();
+        case 32: return make_dense_mma<32, 4>();
+        case 40: return make_dense_mma<40, 4>();
+        case 48: return make_dense_mma<48, 2>();
+        case 64: return make_dense_mma<64, 2>();
         default: return KernelInfo{};
     }
 }
@@ -578,6 +847,16 @@ KernelInfo tune_variant(int v) {
 }
 
 KernelInfo pick(int dim, int mode, int kt, bool vec_ok) {
+    if (dim < 0) {  // -DK: tensor-core contraction, coordinates padded to DK (multiple of 8)
+        switch (-dim) {
+            case 8: return pick_contract<8>(mode, kt);
+            case 16: return pick_contract<16>(mode, kt);
+            case 32: return pick_contract<32>(mode, kt);
+            case 64: return pick_contract<64>(mode, kt);
+            case 128: return pick_contract<128>(mode, kt);
+            default: return KernelInfo{};
+        }
+    }
     switch (dim) {
         case 0:
             // 128-bit loads (4 outputs per thread): 806 GCells/s = 98 % of HBM on C5 (tools/tune_dense.py)

@@ -399,3 +399,36 @@ def test_invalid_inputs_raise():
         sk.ctransform_of_f(gp, [0.0, 0.0, 0.0])
     with pytest.raises(ValueError, match="ell must be < n"):
         sk.top_modes(gp, [0.0, 0.0], [0.0, 0.0], 2)
+
+
+@pytest.mark.parametrize("d,n,m", [(5, 150, 131), (16, 200, 96), (64, 257, 130)])
+def test_onthefly_contraction_kernels_match_oracle(d, n, m):
+    """cost_mode="onthefly" with d > 4: the x.y contraction runs on DMMA; sum, max
+    (exact shift) and block (Newton / top_modes) passes against the oracle."""
+    rng = np.random.default_rng(d)
+    x = np.asfortranarray(rng.normal(0, 0.125, (n, d)))
+    y = np.asfortranarray(rng.normal(0, 0.125, (m, d)))
+    a = rng.uniform(0.5, 1.5, n)
+    a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m)
+    b /= b.sum()
+    eps = 0.01
+    gp = sk.PointProblem(x, y, a, b, eps, cost_mode="onthefly")
+    assert gp.cost_path == "contraction"
+    sp = sk.PointProblem(x, y, a, b, eps, cost_mode="stored")
+    assert sp.cost_path == "stored"
+    op = O.Instance(a, b, eps, x=x, y=y)
+    f = rng.uniform(-0.05, 0.05, n)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(sk.ctransform_of_f(gp, f), g_ref) <= 1e-12
+    assert rel_err(sk.ctransform_of_g(gp, g_ref), O.ctransform_of_g(op, g_ref)) <= 1e-12
+    r = O.solve(op, tol=1e-11)
+    V = np.asfortranarray(rng.standard_normal((n, 6)))
+    bas = sk.SpectralBasis(V, V, np.zeros(6), eps)
+    gr1, h1 = sk.restricted_derivatives(gp, r["f"], bas, r["g"])
+    gr2, h2 = O.restricted_derivatives(op, r["f"], r["g"], V)
+    assert rel_err(h1, h2) <= 1e-11
+    rg = sk.solve(gp, tol=1e-10)
+    ro = O.solve(op, tol=1e-10)
+    assert rg.iterations == ro["iterations"]
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT

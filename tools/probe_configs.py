@@ -23,6 +23,16 @@ if what == "passes":
             print(f"  which={which} pass {ms:8.3f} ms kernel {kms:8.3f} ms {cells/kms/1e6:8.1f} GCells/s",
                   flush=True)
         del p
+elif what == "c5":
+    inst = G.config("C5")
+    cells = inst.n * inst.m
+    for mode in ("stored", "onthefly"):
+        p = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon, inst.cost_scale, cost_mode=mode)
+        for which in (0, 1, 3):
+            ms, kms = sk.bench_pass(p, which, inst.ell, passes=5)
+            print(f"C5 {mode:9s} ({p.cost_path}) which={which} pass {ms:8.3f} ms kernel {kms:8.3f} ms "
+                  f"{cells/kms/1e6:8.1f} GCells/s", flush=True)
+        del p
 elif what == "ttt":
     cfg = sys.argv[2]
     inst = G.config(cfg)
