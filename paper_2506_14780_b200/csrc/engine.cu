@@ -246,55 +246,6 @@ __global__ void k_colres(const double* g, const double* h, const double* b, int6
         colres[j] = b[j] * expm1((g[j] - h[j]) * inv_eps);
 }
 
-// gap from Gram sums: sums[0] = ||row-a||^2, sums[1] = ||col-b||^2 ; maxima via
-// a separate deterministic max kernel (k_absmax) into sums[2], sums[3].
-__global__ void k_absmax(const double* x, int64_t n, double* part, double* out, unsigned* counter,
-                         DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    __shared__ double sh[AUX_NT];
-    double mx = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        mx = fmax(mx, fabs(x[i]));
-    sh[threadIdx.x] = mx;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
-        __syncthreads();
-    }
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = sh[0];
-        __threadfence();
-        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!is_last || threadIdx.x != 0) return;
-    __threadfence();
-    double r = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) r = fmax(r, part[b]);
-    *out = r;
-    *counter = 0u;
-}
-
-// sums: [0]=|row-a|^2 [1]=|col-b|^2 [2]=max|row-a| [3]=max|col-b| [4]=a.f [5]=b.h
-__global__ void k_check(DevState* st, const double* sums, int newton) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (st->done) return;
-    st->gap_l2 = sqrt(sums[0]) + sqrt(sums[1]);
-    st->gap_inf = sums[2] + sums[3];
-    st->q0 = sums[4] + sums[5];
-    if (st->gap_l2 < st->tol) {
-        st->conv = 1;
-        st->done = 1;
-        return;
-    }
-    if (newton) {
-        st->newton_ok = 1;
-        st->attempted = 1;
-    }
-}
-
 // alpha - r = -a_i expm1(f_i/eps + L_i(h)) ; r = a - (alpha - r)
 __global__ void k_newton_r(const double* f, const double* L, const double* a, int64_t n, double inv_eps,
                            double* am, double* r, DevState* st, unsigned guard) {
@@ -375,14 +326,6 @@ __global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, co
         for (int c = 0; c < ell; ++c) s += V[i + c * n] * sd[c];
         out[i] = f[i] + s;
     }
-}
-
-// q1 = a.f' + b.h' ; accept iff q1 > q0 (solver.cpp:46-47)
-__global__ void k_accept(DevState* st, const double* sums) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (st->done || !st->newton_ok) return;
-    st->q1 = sums[0] + sums[1];
-    st->accept = st->q1 > st->q0 ? 1 : 0;
 }
 
 // accepted: f <- candidate, next g <- h(candidate); otherwise next g <- h.
@@ -473,16 +416,18 @@ __global__ void k_div_rows(const double* X, const double* s, int64_t n, int l, d
 
 // SplitMix64 start block (spectral.cpp:138-142): draw t = c*n + i of the
 // stream seeded 0x73706563 is state seed + (t+1)*gamma -- computed in parallel.
-__global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long seed) {
+__global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long seed, int64_t n_global,
+                                 int64_t row_begin) {
     const int64_t total = n * k;
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t t = (e / n) * n_global + row_begin + e % n;  // draw index of (row, column)
         unsigned long long z = seed + static_cast<unsigned long long>(t + 1) * 0x9E3779B97F4A7C15ull;
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z = z ^ (z >> 31);
         const double u01 = static_cast<double>(z >> 11) * 0x1.0p-53;
-        X[t] = -1.0 + 2.0 * u01;
+        X[e] = -1.0 + 2.0 * u01;
     }
 }
 
@@ -1161,6 +1106,13 @@ static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t
 }
 
 
+// gram() followed by the cross-rank sum when the rows are sharded.
+static void gram_all(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t ldu, const double* V,
+                     int64_t ldv, const double* w, double* out, unsigned guard, int diag_only = 0) {
+    gram(P, T, ka, kb, U, ldu, V, ldv, w, out, guard, diag_only);
+    allreduce(P, out, static_cast<size_t>(diag_only ? ka : ka * kb), ncclSum);
+}
+
 // ============================================================ top_modes
 // Symmetric eigen-decomposition (stands in for Eigen::SelfAdjointEigenSolver,
 // spectral.cpp:156): Householder tridiagonalisation followed by implicit QL
@@ -1389,7 +1341,7 @@ static void device_cholqr_step(Problem& P, double* X, int64_t n, int k, bool shi
     qw.w.ensure(64 * 64 * 2);
     double* G = qw.w.p;
     double* Rinv = qw.w.p + 64 * 64;
-    gram(P, n, k, k, X, n, X, n, nullptr, G, 0);
+    gram_all(P, n, k, k, X, n, X, n, nullptr, G, 0);
     const double shift_coef = shifted ? 11.0 * (static_cast<double>(n) * k + k * (k + 1.0)) * 0x1p-53 : 0.0;
     count_launch();
     k_chol_inv<<<1, 64, sizeof(double) * k * k, P.stream>>>(G, k, shift_coef, Rinv, fail);
@@ -1409,7 +1361,7 @@ static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const 
     qw.flag.ensure(1);
     int* fail = reinterpret_cast<int*>(qw.flag.p);
     for (int round = 0; round < 3; ++round) {
-        gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
+        gram_all(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
         count_launch();
         k_deflate<<<grid_for(n * k), AUX_NT, 0, P.stream>>>(X, n, k, u0, s);
         bool use_householder = qw.force_householder;
@@ -1420,13 +1372,16 @@ static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const 
             device_cholqr_step(P, X, n, k, false, qw, fail);
             device_cholqr_step(P, X, n, k, false, qw, fail);
         }
-        gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
+        gram_all(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
         std::vector<double> hs(k + 1);
         download(hs.data(), s, k, P.stream);
         int hfail = 0;
         if (!use_householder) CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
         CK(cudaStreamSynchronize(P.stream));
         if (hfail) {  // restore the deflated block and redo this round with Householder
+            if (P.shard)
+                throw EigenFailure("top_modes: CholeskyQR breakdown on a row-sharded problem (no sharded "
+                                   "Householder fallback)", std::numeric_limits<double>::infinity());
             CK(cudaMemcpyAsync(X, qw.backup.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
             device_householder_q(P, X, n, k, qw);
             gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
@@ -1484,7 +1439,7 @@ static void apply_sym_sym(Problem& P, const double* f, const double* g, const do
     yr.out = Y;
     plan_pass(P, yr);
     // Y -= sqrt(a) (sqrt(a)^T Y)
-    gram(P, n, block, 1, Y, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
+    gram_all(P, n, block, 1, Y, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
     count_launch();
     k_deflate<<<grid_for(n * block), AUX_NT, 0, s>>>(Y, n, block, P.src.sw.p, P.misc.p);
 }
@@ -1508,9 +1463,9 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
                               int64_t max_power_iters, int method = 0, int degree = 8) {
     const int64_t n = P.n;
     if (ell < 1) throw InvalidArgument("top_modes: ell must be >= 1");
-    if (ell >= n) throw InvalidArgument("top_modes: ell must be < n");
+    if (ell >= P.n_global) throw InvalidArgument("top_modes: ell must be < n");
     if (max_power_iters < 0) max_power_iters = 500 * ell;
-    const int block = static_cast<int>(std::min<int64_t>(ell + 5, n - 1));
+    const int block = static_cast<int>(std::min<int64_t>(ell + 5, P.n_global - 1));
     if (block > 64) throw InvalidArgument("top_modes: ell + 5 > 64 is not supported by sknr_b200");
     if (degree < 1) degree = 1;
     const int kt = block_kt_for(block);
@@ -1530,7 +1485,8 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
     OpWork ow;
     qw.backup.ensure(static_cast<size_t>(n) * block);
     count_launch();
-    k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull);
+    k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull, P.n_global,
+                                                            P.row_begin);
     device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
 
     DBuf T;
@@ -1545,7 +1501,7 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
         apply_sym_sym(P, f, g, X.p, Y.p, block, kt, ow);  // Y = A X
         ++applications;
         // Rayleigh-Ritz on the current orthonormal block
-        gram(P, n, block, block, X.p, n, Y.p, n, nullptr, T.p, 0);
+        gram_all(P, n, block, block, X.p, n, Y.p, n, nullptr, T.p, 0);
         download(hT.data(), T.p, block * block, s);
         CK(cudaStreamSynchronize(s));
         for (int a = 0; a < block; ++a)
@@ -1565,7 +1521,7 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
                                                                               static_cast<int>(ell), YW.p);
         count_launch();
         k_resid<<<grid_for(n * ell), AUX_NT, 0, s>>>(YW.p, XW.p, th.p, n, static_cast<int>(ell), R.p);
-        gram(P, n, static_cast<int>(ell), static_cast<int>(ell), R.p, n, R.p, n, nullptr, P.misc.p, 0, 1);
+        gram_all(P, n, static_cast<int>(ell), static_cast<int>(ell), R.p, n, R.p, n, nullptr, P.misc.p, 0, 1);
         download(hres.data(), P.misc.p, ell, s);
         CK(cudaStreamSynchronize(s));
         double max_res = 0.0;
@@ -1619,11 +1575,13 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
     device_orth_deflated(P, XW.p, n, static_cast<int>(ell), P.src.sw.p, qw);
     count_launch();
     k_div_rows<<<grid_for(n * ell), AUX_NT, 0, s>>>(XW.p, P.src.sw.p, n, static_cast<int>(ell), R.p);
-    out.vectors_sym.resize(n * ell);
-    out.vectors.resize(n * ell);
-    download(out.vectors_sym.data(), XW.p, n * ell, s);
-    download(out.vectors.data(), R.p, n * ell, s);
-    CK(cudaStreamSynchronize(s));
+    const int64_t ng = P.n_global;
+    out.vectors_sym.resize(ng * ell);
+    out.vectors.resize(ng * ell);
+    for (int64_t c = 0; c < ell; ++c) {
+        gather_rows(P, XW.p + c * n, out.vectors_sym.data() + c * ng);
+        gather_rows(P, R.p + c * n, out.vectors.data() + c * ng);
+    }
     out.rhos.resize(ell);
     for (int a = 0; a < ell; ++a) out.rhos[a] = std::sqrt(std::max(theta[a], 0.0));
     return out;
@@ -2355,18 +2313,17 @@ int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t 
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    if (P.shard) throw RuntimeFailure("top_modes: not yet available on a row-sharded problem");
-    check_finite_vec(f, P.n, "SinkhornOperator(f)");
+    check_finite_vec(f, P.n_global, "SinkhornOperator(f)");
     check_finite_vec(g, P.m, "SinkhornOperator(g)");
     DBuf df, dg;
     df.ensure(P.n);
     dg.ensure(P.m);
-    upload(df.p, f, P.n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, P.m, P.stream);
     if (method < 0 || method > 1) throw InvalidArgument("top_modes: method must be 0 (subspace) or 1 (chebyshev)");
     Basis b = top_modes_device(P, df.p, dg.p, ell, tol, max_power_iters, method, degree);
-    std::memcpy(vectors, b.vectors.data(), sizeof(double) * P.n * ell);
-    std::memcpy(vectors_sym, b.vectors_sym.data(), sizeof(double) * P.n * ell);
+    std::memcpy(vectors, b.vectors.data(), sizeof(double) * P.n_global * ell);
+    std::memcpy(vectors_sym, b.vectors_sym.data(), sizeof(double) * P.n_global * ell);
     std::memcpy(rhos, b.rhos.data(), sizeof(double) * ell);
     if (sweeps) *sweeps = b.sweeps;
     SKNR_API_END
@@ -2423,8 +2380,6 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
     if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     const double eps0 = P.eps;
     const int64_t n = P.n_global, m = P.m;
-    if (P.shard && warm_mode == 2 && cfg->ell > 0)
-        throw RuntimeFailure("anneal: spectral warm start not yet available on a row-sharded problem");
     int64_t tl = 0;
     Basis basis;
     bool have_basis = false;
@@ -2444,7 +2399,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
                     DBuf df, dg;
                     df.ensure(n);
                     dg.ensure(m);
-                    upload(df.p, prev_f.data(), n, P.stream);
+                    upload_rows(P, df.p, prev_f.data());
                     upload(dg.p, prev_g.data(), m, P.stream);
                     try {
                         basis = top_modes_device(P, df.p, dg.p, cfg->ell, 1e-8, -1);

@@ -309,6 +309,14 @@ def test_sharded_code_path_single_rank_is_bitwise_identical():
         g = sk.ctransform_of_f(ref, n1.f)
         assert np.array_equal(sk.ctransform_of_f(shp, n1.f), g)
         assert np.array_equal(sk.ctransform_of_g(shp, g), sk.ctransform_of_g(ref, g))
+        b1 = sk.top_modes(ref, r1.f, r1.g, 4)
+        b2 = sk.top_modes(shp, r1.f, r1.g, 4)
+        assert b1.sweeps == b2.sweeps
+        assert np.array_equal(b1.rhos, b2.rhos) and np.array_equal(b1.vectors, b2.vectors)
+        a1 = sk.anneal(ref, [0.08, 0.04, 0.02], warm="spectral", ell=3)
+        a2 = sk.anneal(shp, [0.08, 0.04, 0.02], warm="spectral", ell=3)
+        assert [s.iterations for s in a1] == [s.iterations for s in a2]
+        assert np.array_equal(a1[-1].f, a2[-1].f)
     finally:
         sk.comm_destroy()
 
