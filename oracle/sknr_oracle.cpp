@@ -234,11 +234,15 @@ void restricted_derivatives(const Problem& p, const Vec& f, const Vec& g, const 
     constexpr Index kChunk = 128;
     // S = V^T P~ (ell x m), computed column by column.
     Vec S(static_cast<size_t>(ell) * m, 0.0);
+    Vec Vr(static_cast<size_t>(n) * ell);  // row-major copy: contiguous per i (same arithmetic)
+    for (Index c = 0; c < ell; ++c)
+        for (Index i = 0; i < n; ++i) Vr[i * ell + c] = V[i + c * n];
     par_for(m, [&](Index j) {
         std::vector<double> s(ell, 0.0);
         for (Index i = 0; i < n; ++i) {
             const double w = p.a[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
-            for (Index c = 0; c < ell; ++c) s[c] += V[i + c * n] * w;
+            const double* vr = &Vr[i * ell];
+            for (Index c = 0; c < ell; ++c) s[c] += vr[c] * w;
         }
         for (Index c = 0; c < ell; ++c) S[c + j * ell] = s[c];
     });
@@ -524,12 +528,16 @@ Vec apply_sym_t_block(const Problem& p, const Vec& f, const Vec& g, const Vec& U
     const Index n = p.n, m = p.m;
     Vec sa(n), out(static_cast<size_t>(m) * k);
     for (Index i = 0; i < n; ++i) sa[i] = std::sqrt(p.a[i]);
+    Vec Ur(static_cast<size_t>(n) * k);  // row-major copy: contiguous per i (same arithmetic)
+    for (Index c = 0; c < k; ++c)
+        for (Index i = 0; i < n; ++i) Ur[i * k + c] = U[i + c * n];
     par_for(m, [&](Index j) {
         std::vector<double> acc(k, 0.0);
         const double sb = std::sqrt(p.b[j]);
         for (Index i = 0; i < n; ++i) {
             const double w = sa[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
-            for (Index c = 0; c < k; ++c) acc[c] += w * U[i + c * n];
+            const double* ur = &Ur[i * k];
+            for (Index c = 0; c < k; ++c) acc[c] += w * ur[c];
         }
         for (Index c = 0; c < k; ++c) out[j + c * m] = sb * acc[c];
     });
@@ -543,11 +551,15 @@ Vec apply_sym_block(const Problem& p, const Vec& f, const Vec& g, const Vec& V, 
     Vec sa(n), sb(m), out(static_cast<size_t>(n) * k);
     for (Index i = 0; i < n; ++i) sa[i] = std::sqrt(p.a[i]);
     for (Index j = 0; j < m; ++j) sb[j] = std::sqrt(p.b[j]);
+    Vec Vr(static_cast<size_t>(m) * k);  // row-major copy: contiguous per j (same arithmetic)
+    for (Index c = 0; c < k; ++c)
+        for (Index j = 0; j < m; ++j) Vr[j * k + c] = V[j + c * m];
     par_for(n, [&](Index i) {
         std::vector<double> acc(k, 0.0);
         for (Index j = 0; j < m; ++j) {
             const double w = sa[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
-            for (Index c = 0; c < k; ++c) acc[c] += w * (sb[j] * V[j + c * m]);
+            const double* vr = &Vr[j * k];
+            for (Index c = 0; c < k; ++c) acc[c] += w * (sb[j] * vr[c]);
         }
         for (Index c = 0; c < k; ++c) out[i + c * n] = acc[c];
     });

@@ -2593,11 +2593,14 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
+    const bool block = variant >= 200;
     if (variant < 100 && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
-    if (variant >= 100 && P.dim != 0) throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
+    if (variant >= 100 && variant < 200 && P.dim != 0)
+        throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
+    if (block && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
-    DBuf f, g;
+    DBuf f, g, V, Wv;
     f.ensure(n);
     g.ensure(m);
     count_launch();
@@ -2608,10 +2611,18 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     plan_for(P, 0, MODE_MAX, 0);
     lse(P, 0, f.p, g.p, G_NONE);
     lse(P, 0, f.p, g.p, G_NONE);  // leaves the bound-shift pack in place
-    TilePlan tp = plan_tiles(P.dim, MODE_SUM, 0, m, n, 0, variant);
+    const int kt = 32;
+    TilePlan tp = plan_tiles(P.dim, block ? MODE_BLOCK : MODE_SUM, block ? kt : 0, m, n, block ? 8 : 0, variant);
     if (!tp.fn) throw InvalidArgument("sknr_tune_variant: unknown variant");
-    P.partial.ensure(static_cast<size_t>(tp.n_in_blocks) * m);
+    P.partial.ensure(static_cast<size_t>(tp.n_in_blocks) * m * (block ? kt : 1));
     TileArgs ta = tile_args(P, 0, tp, G_NONE);
+    if (block) {
+        V.ensure(n * kt);
+        Wv.ensure(n * kt);
+        count_launch();
+        k_fill<<<grid_for(n * kt), AUX_NT, 0, s>>>(Wv.p, n * kt, 1.0 / std::sqrt(static_cast<double>(n)));
+        ta.W = Wv.p;
+    }
     launch_tiles(tp, ta, s);
     CK(cudaStreamSynchronize(s));
     cudaEvent_t e0, e1;

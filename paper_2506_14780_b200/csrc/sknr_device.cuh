@@ -109,6 +109,11 @@ __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
     return false;
 }
 
+// Polynomial coefficients and the magic constant as constant-bank operands:
+// DFMA/DADD read c[bank][offset] directly, so the loop carries no UMOV
+// re-materialisations of uniform registers. Defined in tile_kernels.cu.
+static __constant__ double c_pexp_k[6] = {kMagicB, kP1, kP2, kP3, kP4, 0.0};
+
 // Split evaluation 2^(u/256) = T' * p. `tab` = shared replicated table,
 // `laneoff` = (lane & 15) * 8 bytes, `c3` = kP3 held in a register by the caller
 // (the first Horner step has two constant operands and would otherwise
@@ -120,17 +125,17 @@ __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
 template <bool HI_CLAMP, bool FASTCLAMP = false>
 __device__ __forceinline__ void pexp_parts(double u, const unsigned long long* __restrict__ tab,
                                            unsigned laneoff, double c3, double& Tp, double& p) {
-    const double t = u + kMagicB;
-    const double kf = t - kMagicB;
+    const double t = u + c_pexp_k[0];
+    const double kf = t - c_pexp_k[0];
     const double r = u - kf;
 #if SKNR_TB == 10
-    p = fma(r, kP3, c3);  // c3 holds kP2 in a register
-    p = fma(p, r, kP1);
+    p = fma(r, c_pexp_k[3], c3);  // c3 holds kP2 in a register
+    p = fma(p, r, c_pexp_k[1]);
     p = fma(p, r, 1.0);
 #else
-    p = fma(r, kP4, c3);
-    p = fma(p, r, kP2);
-    p = fma(p, r, kP1);
+    p = fma(r, c_pexp_k[4], c3);
+    p = fma(p, r, c_pexp_k[2]);
+    p = fma(p, r, c_pexp_k[1]);
     p = fma(p, r, 1.0);
 #endif
     int kc = FASTCLAMP ? max(__double2loint(t), 0)

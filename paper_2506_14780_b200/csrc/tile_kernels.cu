@@ -842,6 +842,11 @@ KernelInfo tune_variant(int v) {
         case 105: return make_dense_v2<1, 4, 512, MODE_SUM>();
         case 106: return make_dense_v2<4, 2, 256, MODE_SUM>();
         case 107: return make_dense_v2<2, 4, 128, MODE_SUM>();
+        // DMMA block pass, d=2, KT=32 (MB = 8-output blocks per warp)
+        case 200: return make_mma<2, 32, 2>();
+        case 201: return make_mma<2, 32, 4>();
+        case 202: return make_mma<2, 32, 8>();
+        case 203: return make_mma<2, 32, 6>();
         default: return KernelInfo{};
     }
 }

@@ -11,6 +11,7 @@ inst = G.config("C4")
 p = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon)
 cells = inst.n * inst.m
 print("fp64 peak (TFLOP/s, ms):", sk.bench_fp64_peak())
-for v in range(20):
+variants = [int(a) for a in sys.argv[1:]] or list(range(20))
+for v in variants:
     ms = sk.tune_variant(p, v, passes=5)
     print(f"variant {v:2d}: {ms:7.3f} ms  {cells/ms/1e6:8.1f} GCells/s", flush=True)
