@@ -70,8 +70,9 @@ __device__ __forceinline__ void acc_init(double* acc) {
 }
 
 // ------------------------------------------------------------- point clouds
-template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FASTCLAMP = false>
-__global__ void __launch_bounds__(NTT) pts_tile_kernel(TileArgs a) {
+template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FASTCLAMP = false,
+          int MINB = 1>
+__global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
     if (guard_skip(a.st, a.guard)) return;
     constexpr int NT = NTT;
     constexpr int PK = PK_of<D>::value;
@@ -693,10 +694,11 @@ struct KernelInfo {
     int occ = 0;
 };
 
-template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FC = false>
+template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FC = false,
+          int MINB = 1>
 KernelInfo make_pts() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_tile_kernel<D, JT, MODE, KT, NTT, UNR, FC>);
+    k.fn = reinterpret_cast<const void*>(&pts_tile_kernel<D, JT, MODE, KT, NTT, UNR, FC, MINB>);
     k.jt = JT;
     k.nt = NTT;
     constexpr int CH = Chunk<MODE, KT>::value;
@@ -833,6 +835,10 @@ KernelInfo tune_variant(int v) {
         case 17: return make_pts<2, 12, MODE_SUM, 0, 256, 1, false>();
         case 18: return make_pts<2, 12, MODE_SUM, 0, 128, 1, false>();
         case 19: return make_pts<2, 8, MODE_SUM, 0, 256, 1, true>();
+        case 20: return make_pts<2, 8, MODE_SUM, 0, 256, 1, false, 3>();
+        case 21: return make_pts<2, 8, MODE_SUM, 0, 128, 1, false, 6>();
+        case 22: return make_pts<2, 6, MODE_SUM, 0, 256, 1, false, 3>();
+        case 23: return make_pts<2, 4, MODE_SUM, 0, 256, 2, false, 4>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();
@@ -896,6 +902,16 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     // the stored cost's leading dimension equals n_out in both directions
     KernelInfo ki = variant >= 0 ? tune_variant(variant) : pick(dim, mode, kt, n_out % 2 == 0);
     if (!ki.fn) return p;
+    // Small problems (e.g. C1 512^2, C2 4096^2): the 2048-output tiles of the
+    // register kernels leave most SMs idle; use 128-output tiles instead.
+    if (variant < 0 && dim > 0 && mode != MODE_BLOCK && n_out * n_in <= (int64_t(1) << 26)) {
+        switch (dim) {
+            case 1: ki = mode == MODE_SUM ? make_pts<1, 1, MODE_SUM, 0, 128, 2>() : make_pts<1, 1, MODE_MAX, 0, 128, 2>(); break;
+            case 2: ki = mode == MODE_SUM ? make_pts<2, 1, MODE_SUM, 0, 128, 2>() : make_pts<2, 1, MODE_MAX, 0, 128, 2>(); break;
+            case 3: ki = mode == MODE_SUM ? make_pts<3, 1, MODE_SUM, 0, 128, 2>() : make_pts<3, 1, MODE_MAX, 0, 128, 2>(); break;
+            default: ki = mode == MODE_SUM ? make_pts<4, 1, MODE_SUM, 0, 128, 2>() : make_pts<4, 1, MODE_MAX, 0, 128, 2>(); break;
+        }
+    }
     static thread_local int sm_count = 0;
     if (sm_count == 0) {
         int dev = 0;
@@ -911,7 +927,8 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.out_tile = ki.out_tile > 0 ? ki.out_tile : ki.nt * ki.jt;
     p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
-    const int ch = chunk_inputs(mode, kt);
+    // input-block granularity (the kernels stage up to their chunk size per round)
+    const int ch = mode == MODE_BLOCK ? chunk_inputs(mode, kt) : 32;
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
     // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small.
     int64_t want = (8 * resident + p.n_out_tiles - 1) / p.n_out_tiles;
