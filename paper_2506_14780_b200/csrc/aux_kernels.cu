@@ -154,6 +154,19 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
     }
 }
 
+// out[i] = sum over output tiles t (in order) of rsum[t][i]: the fused block pass's
+// transposed sums (r = P~ beta), deterministic.
+__global__ void __launch_bounds__(AUX_NT) k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n,
+                                                          double* out, const DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int64_t t = 0; t < n_tiles; ++t) s += rsum[t * n + i];
+        out[i] = s;
+    }
+}
+
 __global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, int64_t nb,
                                                          int64_t n_out, const double* scale,
                                                          double* out, DevState* st, unsigned guard) {

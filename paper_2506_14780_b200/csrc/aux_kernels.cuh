@@ -73,6 +73,8 @@ struct FinalizeArgs {
 
 __global__ void k_max_finalize(FinalizeArgs a);
 __global__ void k_lse_finalize(FinalizeArgs a);
+__global__ void k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n, double* out, const DevState* st,
+                                unsigned guard);
 __global__ void k_sum_finalize(const double* partial, int64_t nb, int64_t n_out, const double* scale,
                                double* out, DevState* st, unsigned guard);
 __global__ void k_lse_commit(const double* in_vec, double* ref, int64_t count, int dir, DevState* st,

@@ -631,7 +631,7 @@ struct Problem {
 
     // per-direction LSE state
     DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
-    DBuf partial;
+    DBuf partial, rsum;
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -869,8 +869,10 @@ static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_b
     TilePlan tp = plan_tiles(P.dim, mode, kt, nout, nin, max_in_blocks);
     if (!tp.fn) throw CudaFailure("sknr_b200: no tile kernel for this configuration");
     P.plans[key] = tp;
-    const size_t need = static_cast<size_t>(tp.n_in_blocks) * nout * (mode == MODE_BLOCK ? kt : 1);
+    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS;
+    const size_t need = static_cast<size_t>(tp.n_in_blocks) * nout * (blk ? kt : 1);
     P.partial.ensure(need);
+    if (mode == MODE_BLOCK_RS) P.rsum.ensure(static_cast<size_t>(tp.n_out_tiles) * nin);
     return tp;
 }
 
@@ -1016,15 +1018,21 @@ struct PassSpec {
     int k = 0, kt = 0;
     const double* out_scale = nullptr;
     double* out = nullptr;  // sum: [nout]; block: col-major nout x k (ld = nout)
+    double* rsum_out = nullptr;  // block, dir 0 only: r_i = sum_j e(j, i) b_j fused into the pass
     unsigned guard = 0;
 };
+
+// Whether the block pass can fuse r = P~ beta (register point kernels, d <= 4).
+static bool block_rs_fusable(const Problem& P) { return P.dim >= 1 && P.dim <= 4; }
 
 static void plan_pass(Problem& P, const PassSpec& ps) {
     Side& in = P.in_side(ps.dir);
     Side& out = P.out_side(ps.dir);
     const int64_t nin = in.count, nout = out.count;
     cudaStream_t s = P.stream;
-    const int mode = ps.W ? MODE_BLOCK : MODE_SUM;
+    const bool rs = ps.W && ps.rsum_out;
+    if (rs && (ps.dir != 0 || !block_rs_fusable(P))) throw InvalidArgument("sknr_b200: fused row sums unsupported here");
+    const int mode = ps.W ? (rs ? MODE_BLOCK_RS : MODE_BLOCK) : MODE_SUM;
     const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, ps.W ? 8 : 0);
 
     PrepInArgs pi;
@@ -1065,7 +1073,16 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
 
     TileArgs ta = tile_args(P, ps.dir, tp, ps.guard);
     ta.W = ps.W;
+    if (rs) {
+        ta.out_w = out.w.p;
+        ta.rsum = P.rsum.p;
+    }
     launch_tiles(tp, ta, s);
+    if (rs) {
+        count_launch();
+        k_rsum_finalize<<<grid_for(nin), AUX_NT, 0, s>>>(P.rsum.p, tp.n_out_tiles, nin, ps.rsum_out, P.st,
+                                                         ps.guard);
+    }
     count_launch();
     if (mode == MODE_SUM)
         k_sum_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, nout, ps.out_scale,
@@ -1705,12 +1722,16 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
     if (newton) {
         const unsigned gn = G_DONE | G_NEWTON;
         const int l = static_cast<int>(ell);
-        // r = P~ beta at (f, h): alpha - r = -a expm1(f/eps + L_row(h))
-        lse(P, 1, S.h.p, nullptr, gn);
-        count_launch();
-        k_newton_r<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, P.inv_eps(), S.am.p,
-                                                  S.r.p, P.st, gn);
-        // S = V^T P~ (m x ell), P~_ij = a_i e^{(f_i + h_j - C_ij)/eps}
+        const bool fuse_r = block_rs_fusable(P);
+        if (!fuse_r) {
+            // r = P~ beta at (f, h): alpha - r = -a expm1(f/eps + L_row(h))
+            lse(P, 1, S.h.p, nullptr, gn);
+            count_launch();
+            k_newton_r<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, P.inv_eps(), S.am.p,
+                                                      S.r.p, P.st, gn);
+        }
+        // S = V^T P~ (m x ell), P~_ij = a_i e^{(f_i + h_j - C_ij)/eps}; with fuse_r the
+        // same cells also give r = P~ beta (objective.cpp:127-128) in this pass
         PassSpec sp;
         sp.dir = 0;
         sp.in_v = S.f.p;
@@ -1720,8 +1741,13 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         sp.k = l;
         sp.kt = block_kt_for(l);
         sp.out = S.S.p;
+        sp.rsum_out = fuse_r ? S.r.p : nullptr;
         sp.guard = gn;
         plan_pass(P, sp);
+        if (fuse_r) {
+            count_launch();
+            k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(P.src.w.p, S.r.p, n, 1.0, -1.0, S.am.p);
+        }
         allreduce(P, S.S.p, static_cast<size_t>(m) * l, ncclSum);  // S = V^T P~ summed over row shards
         double* G1 = S.G.p;
         double* cross = G1 + l * l;
@@ -1803,7 +1829,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,
                                                      S.Wv.p);
         // pre-size the block-pass partials outside graph capture
-        plan_for(P, 0, MODE_BLOCK, kt, 8);
+        plan_for(P, 0, block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK, kt, 8);
     }
     plan_for(P, 0, MODE_SUM, 0);
     plan_for(P, 1, MODE_SUM, 0);
@@ -2185,15 +2211,19 @@ int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g
     upload_rows(P, V.p, vectors, ell);
     count_launch();
     k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(V.p, n, n, l, kt, nullptr, Wv.p);
-    // r_i = a_i sum_j b_j e^{(f_i+g_j-C_ij)/eps} (objective.cpp:127-128) as a plan-sum pass
-    PassSpec pr;
-    pr.dir = 1;
-    pr.in_v = dg.p;
-    pr.in_lw = P.tgt.lw.p;
-    pr.out_v = df.p;
-    pr.out_lw = P.src.lw.p;
-    pr.out = r.p;
-    plan_pass(P, pr);
+    // r_i = a_i sum_j b_j e^{(f_i+g_j-C_ij)/eps} (objective.cpp:127-128): fused into the
+    // block pass for point clouds, else a plan-sum pass
+    const bool fuse_r = block_rs_fusable(P);
+    if (!fuse_r) {
+        PassSpec pr;
+        pr.dir = 1;
+        pr.in_v = dg.p;
+        pr.in_lw = P.tgt.lw.p;
+        pr.out_v = df.p;
+        pr.out_lw = P.src.lw.p;
+        pr.out = r.p;
+        plan_pass(P, pr);
+    }
     PassSpec sp;
     sp.dir = 0;
     sp.in_v = df.p;
@@ -2203,6 +2233,7 @@ int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g
     sp.k = l;
     sp.kt = kt;
     sp.out = Sm.p;
+    sp.rsum_out = fuse_r ? r.p : nullptr;
     plan_pass(P, sp);
     // am = a - r
     count_launch();
@@ -2622,6 +2653,9 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
         count_launch();
         k_fill<<<grid_for(n * kt), AUX_NT, 0, s>>>(Wv.p, n * kt, 1.0 / std::sqrt(static_cast<double>(n)));
         ta.W = Wv.p;
+        P.rsum.ensure(static_cast<size_t>(tp.n_out_tiles) * n);  // for the fused-r variants
+        ta.out_w = P.tgt.w.p;
+        ta.rsum = P.rsum.p;
     }
     launch_tiles(tp, ta, s);
     CK(cudaStreamSynchronize(s));

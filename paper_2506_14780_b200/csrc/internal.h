@@ -7,7 +7,9 @@
 
 namespace sknr {
 
-enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2 };
+// MODE_BLOCK_RS: block pass that also emits the transposed weighted sums
+// rsum[out_tile][in] = sum_{o in tile} e(o, in) * out_w[o] (points d <= 4 only).
+enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3 };
 
 // Arguments of the persistent tile kernels (tile_kernels.cu).
 struct TileArgs {
@@ -20,6 +22,8 @@ struct TileArgs {
     double kappa = 0.0;                // dense: u = A + B - kappa*C
     const double* W = nullptr;         // block: W[in*KT + c]
     double* partial = nullptr;         // sum/max: [ib][n_out]; block: [ib][KT][n_out]
+    const double* out_w = nullptr;     // block_rs: weights of the outputs (n_out)
+    double* rsum = nullptr;            // block_rs: [n_out_tiles][n_in]
     const DevState* st = nullptr;
     unsigned guard = 0;
 };

@@ -184,8 +184,17 @@ struct WStride {  // smem row stride of W, == 4 (mod 16) doubles: the 16 lanes o
 constexpr int MMA_NT = 128;  // 4 warps
 constexpr int MMA_CH = 64;   // inputs per shared-memory round
 
-template <int D, int KT, int MB>
+// RS: also emit rsum[out_tile][in] = sum_o e(o, in) out_w[o] (the transposed,
+// output-weighted sums, e.g. r = P~ beta of restricted_derivatives). Each lane's
+// per-step partial over its MB outputs goes to the warp's staging rows in shared
+// memory; at the end of a chunk each warp sums its 8 rows (warp-synchronous), and
+// the 4 warp sums are combined after the next chunk's existing barrier. All sums
+// run in a fixed order, so the result is deterministic, and every (out_tile, in)
+// slot is written exactly once.
+// MCH: inputs staged per shared-memory round (32 with RS keeps 4 CTAs per SM).
+template <int D, int KT, int MB, bool RS = false, int MCH = MMA_CH>
 __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
+    constexpr int RS_LD = MCH + 4;  // staging row stride (conflict-free half-warp stores)
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = PK_of<D>::value;
     constexpr int NCB = KT / 8;
@@ -195,7 +204,9 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
     extern __shared__ __align__(16) double sm[];
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
     double* sin = sm + kTabWords;
-    double* sw = sin + MMA_CH * PK;
+    double* sw = sin + MCH * PK;
+    double* srs = sw + MCH * WS;                    // RS: staging [warp*8 + row][RS_LD]
+    double* srw = srs + (MMA_NT / 32) * 8 * RS_LD;  // RS: warp sums [warp][MCH]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     load_exp2_table(tab, tid, MMA_NT);
     const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
@@ -205,10 +216,11 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
         const int64_t obase = ot * OUT_CTA + warp * OUT_WARP;
-        double Bo[MB], Yo[MB][D];
+        double Bo[MB], Yo[MB][D], Bw[MB];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
             int64_t o = obase + mb * 8 + row;
+            if (RS) Bw[mb] = o < a.n_out ? a.out_w[o] : 0.0;
             o = o < a.n_out ? o : a.n_out - 1;
             Bo[mb] = a.out_pack[o * PK];
 #pragma unroll
@@ -222,10 +234,17 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
 
         const int64_t i0 = ib * a.in_block;
         const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
-        for (int64_t c0 = i0; c0 < i1; c0 += MMA_CH) {
-            const int cnt = static_cast<int>((i1 - c0) < MMA_CH ? (i1 - c0) : MMA_CH);
+        int pend = 0;       // RS: inputs of the previous chunk whose warp sums await combining
+        int64_t pbase = 0;  // RS: first input of that chunk
+        auto rs_combine = [&]() {
+            for (int k = tid; k < pend; k += MMA_NT)
+                a.rsum[ot * a.n_in + pbase + k] = (srw[k] + srw[MCH + k]) + (srw[2 * MCH + k] + srw[3 * MCH + k]);
+        };
+        for (int64_t c0 = i0; c0 < i1; c0 += MCH) {
+            const int cnt = static_cast<int>((i1 - c0) < MCH ? (i1 - c0) : MCH);
             const int cnt4 = (cnt + 3) & ~3;
             __syncthreads();
+            if (RS) rs_combine();
             for (int t = tid; t < cnt4 * PK; t += MMA_NT) {
                 const int k = t / PK, q = t % PK;
                 sin[t] = k < cnt ? a.in_pack[(c0 + k) * PK + q] : (q == 0 ? -1e300 : 0.0);
@@ -247,6 +266,7 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
                 double bf[NCB];
 #pragma unroll
                 for (int cb = 0; cb < NCB; ++cb) bf[cb] = sw[(k4 + kq) * WS + cb * 8 + row];
+                double rt = 0.0;
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb) {
                     double u = x[0] + Bo[mb];
@@ -255,8 +275,29 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
                     const double e = pexp<true>(u, tab, laneoff, c3);
 #pragma unroll
                     for (int cb = 0; cb < NCB; ++cb) dmma_8x8x4(acc[mb][cb][0], acc[mb][cb][1], e, bf[cb]);
+                    if (RS) rt = mb == 0 ? e * Bw[0] : fma(e, Bw[mb], rt);
                 }
+                if (RS) srs[(warp * 8 + row) * RS_LD + k4 + kq] = rt;
             }
+            if (RS) {
+                __syncwarp();
+                const double* st8 = srs + warp * 8 * RS_LD;
+#pragma unroll
+                for (int h = 0; h < MCH / 32; ++h) {
+                    const int k = lane + 32 * h;
+                    const double s01 = st8[k] + st8[RS_LD + k], s23 = st8[2 * RS_LD + k] + st8[3 * RS_LD + k];
+                    const double s45 = st8[4 * RS_LD + k] + st8[5 * RS_LD + k];
+                    const double s67 = st8[6 * RS_LD + k] + st8[7 * RS_LD + k];
+                    srw[warp * MCH + k] = (s01 + s23) + (s45 + s67);
+                }
+                __syncwarp();
+                pend = cnt;
+                pbase = c0;
+            }
+        }
+        if (RS) {
+            __syncthreads();
+            rs_combine();
         }
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
@@ -718,14 +759,16 @@ KernelInfo make_dense() {
     return k;
 }
 
-template <int D, int KT, int MB>
+template <int D, int KT, int MB, bool RS = false, int MCH = MMA_CH>
 KernelInfo make_mma() {
+    static_assert(MCH % 32 == 0 && MCH <= MMA_CH, "chunk must be a multiple of 32");
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_mma_kernel<D, KT, MB>);
+    k.fn = reinterpret_cast<const void*>(&pts_mma_kernel<D, KT, MB, RS, MCH>);
     k.jt = 1;
     k.nt = MMA_NT;
     k.out_tile = 8 * MB * (MMA_NT / 32);
-    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + MMA_CH * PK_of<D>::value + MMA_CH * WStride<KT>::value);
+    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + MCH * PK_of<D>::value + MCH * WStride<KT>::value +
+                                                 (RS ? (MMA_NT / 32) * (8 * (MCH + 4) + MCH) : 0));
     return k;
 }
 
@@ -744,6 +787,7 @@ KernelInfo make_contract() {
 
 template <int DK>
 KernelInfo pick_contract(int mode, int kt) {
+    if (mode == MODE_BLOCK_RS) return KernelInfo{};  // not fused for the contraction kernels
     if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
     if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
     switch (kt) {
@@ -763,6 +807,18 @@ KernelInfo pick_pts(int mode, int kt) {
     // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
+    if (mode == MODE_BLOCK_RS) {  // 32-input rounds: 4 CTAs/SM fit (C4 ell=32: 13.9 ms vs 14.1 ms at 64)
+        switch (kt) {
+            case 8: return make_mma<D, 8, 4, true, 32>();
+            case 16: return make_mma<D, 16, 4, true, 32>();
+            case 24: return make_mma<D, 24, 4, true, 32>();
+            case 32: return make_mma<D, 32, 4, true, 32>();
+            case 40: return make_mma<D, 40, 4, true, 32>();
+            case 48: return make_mma<D, 48, 2, true, 32>();
+            case 64: return make_mma<D, 64, 2, true, 32>();
+            default: return KernelInfo{};
+        }
+    }
     switch (kt) {  // FP64 tensor-core (DMMA) block pass, 4 x 8-output blocks per warp
         case 8: return make_mma<D, 8, 4>();
         case 16: return make_mma<D, 16, 4>();
@@ -797,6 +853,7 @@ KernelInfo make_dense_mma() {
 }
 
 KernelInfo pick_dense(int mode, int kt) {
+    if (mode == MODE_BLOCK_RS) return KernelInfo{};  // not fused for stored costs
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
     switch (kt) {  // FP64 tensor-core (DMMA) block pass
@@ -853,6 +910,10 @@ KernelInfo tune_variant(int v) {
         case 201: return make_mma<2, 32, 4>();
         case 202: return make_mma<2, 32, 8>();
         case 203: return make_mma<2, 32, 6>();
+        case 204: return make_mma<2, 32, 4, true>();
+        case 205: return make_mma<2, 32, 2, true>();
+        case 206: return make_mma<2, 32, 4, true, 32>();
+        case 207: return make_mma<2, 32, 4, false, 32>();
         default: return KernelInfo{};
     }
 }
@@ -904,7 +965,8 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     if (!ki.fn) return p;
     // Small problems (e.g. C1 512^2, C2 4096^2): the 2048-output tiles of the
     // register kernels leave most SMs idle; use 128-output tiles instead.
-    if (variant < 0 && dim > 0 && mode != MODE_BLOCK && n_out * n_in <= (int64_t(1) << 26)) {
+    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS;
+    if (variant < 0 && dim > 0 && !blk && n_out * n_in <= (int64_t(1) << 26)) {
         switch (dim) {
             case 1: ki = mode == MODE_SUM ? make_pts<1, 1, MODE_SUM, 0, 128, 2>() : make_pts<1, 1, MODE_MAX, 0, 128, 2>(); break;
             case 2: ki = mode == MODE_SUM ? make_pts<2, 1, MODE_SUM, 0, 128, 2>() : make_pts<2, 1, MODE_MAX, 0, 128, 2>(); break;
@@ -928,7 +990,7 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     // input-block granularity (the kernels stage up to their chunk size per round)
-    const int ch = mode == MODE_BLOCK ? chunk_inputs(mode, kt) : 32;
+    const int ch = blk ? chunk_inputs(MODE_BLOCK, kt) : 32;
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
     // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small.
     int64_t want = (8 * resident + p.n_out_tiles - 1) / p.n_out_tiles;

@@ -132,6 +132,30 @@ def test_restricted_derivatives_match_oracle(ell):
     assert rel_err(h1, h2) <= 1e-11
 
 
+@pytest.mark.parametrize("d,n,m,ell", [(2, 401, 333, 5), (1, 77, 1000, 16), (3, 1000, 77, 32),
+                                        (4, 257, 129, 40), (2, 64, 64, 64), (2, 3000, 2500, 24)])
+def test_restricted_derivatives_points_fused_r(d, n, m, ell):
+    """Point clouds with d <= 4 fuse r = P~ beta into the DMMA block pass
+    (32-input rounds, per-warp staging); ragged n, m exercise partial rounds and
+    output tiles."""
+    rng = np.random.default_rng(d * 7919 + n + ell)
+    x = np.asfortranarray(rng.uniform(0, 1, (n, d)))
+    y = np.asfortranarray(rng.uniform(0, 1, (m, d)))
+    a = rng.uniform(0.5, 1.5, n)
+    a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m)
+    b /= b.sum()
+    gp = sk.PointProblem(x, y, a, b, 0.02)
+    op = O.Instance(a, b, 0.02, x=x, y=y)
+    f = rng.uniform(-0.05, 0.05, n)
+    g = O.ctransform_of_f(op, f)
+    V = np.asfortranarray(rng.standard_normal((n, ell)))
+    gr1, h1 = sk.restricted_derivatives(gp, f, sk.SpectralBasis(V, V, np.zeros(ell), 0.02), g)
+    gr2, h2 = O.restricted_derivatives(op, f, g, V)
+    assert rel_err(gr1, gr2) <= 1e-9
+    assert rel_err(h1, h2) <= 1e-11
+
+
 def test_top_modes_match_oracle():
     inst = G.config("C1", n=300, m=300)
     gp, op = points_pair(inst)
