@@ -92,6 +92,11 @@ int sknr_plan_marginals(sknr_problem p, const double* f, const double* g, double
                         double* col, double* gap_l2, double* gap_inf);
 /* coupling_from (core.cpp:84-103): n x m col-major into a host buffer. */
 int sknr_coupling(sknr_problem p, const double* f, const double* g, double* plan);
+/* Rows [row_begin, row_end) of the same plan, col-major with leading dimension
+ * row_end - row_begin: lets a caller stream an n x m coupling (e.g. the CLI's
+ * coupling.csv, main.cpp:149-154) without holding it whole. */
+int sknr_coupling_rows(sknr_problem p, const double* f, const double* g, int64_t row_begin, int64_t row_end,
+                       double* plan_rows);
 
 /* ---------------------------------------------------------------- objective.hpp */
 int sknr_semi_dual_value(sknr_problem p, const double* f, double* value);
@@ -99,11 +104,20 @@ int sknr_semi_dual_value(sknr_problem p, const double* f, double* value);
 int sknr_restricted_derivatives(sknr_problem p, const double* f, const double* g,
                                 const double* vectors /* n x ell */, int64_t ell,
                                 double* grad /* ell */, double* hess /* ell x ell */);
+/* dual_value (objective.cpp:10-40): a.f + b.g - eps*expm1(log sum_ij a_i b_j e^{(f_i+g_j-C_ij)/eps}). */
+int sknr_dual_value(sknr_problem p, const double* f, const double* g, double* value);
+/* semi_dual_hessian_quadform (objective.cpp:53-77): u^T H(f) u. */
+int sknr_semi_dual_hessian_quadform(sknr_problem p, const double* f, const double* u, double* value);
 
 /* ---------------------------------------------------------------- spectral.hpp
  * SinkhornOperator::apply_sym_block / apply_sym_t_block (spectral.cpp:68-102)
  * and top_modes (spectral.cpp:125-193). Returns SKNR_EEIGEN with
  * sknr_last_best_residual() when the residual target is not met. */
+/* SinkhornOperator::apply_R / apply_Rt (spectral.cpp:29-62):
+ * (R g1)_i = sum_j e^{(f_i+g_j-C_ij)/eps} b_j g1_j ; (R^T f1)_j = sum_i e^{..} a_i f1_i.
+ * apply_K(f1, g1) = (apply_R(g1), apply_Rt(f1)) (spectral.cpp:64-66). */
+int sknr_apply_R(sknr_problem p, const double* f, const double* g, const double* g1, double* out /* n */);
+int sknr_apply_Rt(sknr_problem p, const double* f, const double* g, const double* f1, double* out /* m */);
 int sknr_apply_sym_block(sknr_problem p, const double* f, const double* g,
                          const double* v /* m x k */, int64_t k, double* out /* n x k */);
 int sknr_apply_sym_t_block(sknr_problem p, const double* f, const double* g,
@@ -112,6 +126,14 @@ int sknr_top_modes(sknr_problem p, const double* f, const double* g, int64_t ell
                    int64_t max_power_iters /* -1: 500*ell */, double* vectors /* n x ell */,
                    double* vectors_sym /* n x ell */, double* rhos /* ell */,
                    int64_t* sweeps /* may be NULL */);
+
+/* spectrum_report (spectral.cpp:195-228): rhos, (1-rho)/eps, (1+rho)/eps; with
+ * include_vectors, vectors_f (n x k) and vectors_g (m x k). Needs 1 <= k <= min(n,m)-1. */
+int sknr_spectrum_report(sknr_problem p, const double* f, const double* g, int64_t k, int include_vectors,
+                         double tol, int64_t max_power_iters, double* rhos, double* hess_low,
+                         double* hess_high, double* vectors_f, double* vectors_g);
+/* projector_distance (spectral.cpp:230-242) between two n x k symmetrized bases. */
+int sknr_projector_distance(int64_t n, int64_t k, const double* a_sym, const double* b_sym, double* out);
 
 /* Opt-in accelerated variant (not in the reference): method 1 = Chebyshev-
  * filtered subspace iteration of polynomial degree `degree` (same Rayleigh-Ritz,
@@ -153,6 +175,11 @@ int sknr_solve(sknr_problem p, const sknr_config* cfg, const double* basis, int6
                const double* init_f, const double* init_g, double* f_out, double* g_out,
                int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
                int64_t* trace_len);
+
+/* newton_step (solver.cpp:59-69, try_newton :30-56): one restricted Newton step
+ * from f with basis vectors (n x ell). f_out = accepted ? f + V delta : f. */
+int sknr_newton_step(sknr_problem p, const double* f, const double* vectors, int64_t ell, double* f_out,
+                     int* accepted, int* factorization_failed);
 
 /* anneal (solver.cpp:158-222). warm_mode 0 none, 1 potentials, 2 spectral.
  * Per stage s: f_out[s*n ..], g_out[s*m ..], iterations[s], converged[s];

@@ -730,6 +730,53 @@ struct SolveOut {
     std::vector<Record> trace;
 };
 
+// dual_value (objective.cpp:10-40): one global max shift over all cells, then
+// one global sum, both j-outer / i-inner like the reference loops.
+double dual_value(const Problem& p, const Vec& f, const Vec& g) {
+    check_finite(f.data(), p.n, "dual_value");
+    check_finite(g.data(), p.m, "dual_value");
+    const double inv_eps = 1.0 / p.eps;
+    // per-column partials in parallel, combined in column order (the reference's
+    // running max is order independent; its running sum is j-major, i-minor)
+    Vec colmax(p.m);
+    par_for(p.m, [&](Index j) {
+        const double base = p.lb[j] + g[j] * inv_eps;
+        double s = -std::numeric_limits<double>::infinity();
+        for (Index i = 0; i < p.n; ++i) s = std::max(s, p.la[i] + base + (f[i] - p.C(i, j)) * inv_eps);
+        colmax[j] = s;
+    });
+    double shift = -std::numeric_limits<double>::infinity();
+    for (Index j = 0; j < p.m; ++j) shift = std::max(shift, colmax[j]);
+    double total = 0.0;
+    for (Index j = 0; j < p.m; ++j) {
+        const double base = p.lb[j] + g[j] * inv_eps;
+        for (Index i = 0; i < p.n; ++i) total += std::exp(p.la[i] + base + (f[i] - p.C(i, j)) * inv_eps - shift);
+    }
+    const double log_mass = shift + std::log(total);
+    return dot(p.a, f) + dot(p.b, g) - p.eps * std::expm1(log_mass);
+}
+
+// semi_dual_hessian_quadform (objective.cpp:53-77)
+double semi_dual_hessian_quadform(const Problem& p, const Vec& f, const Vec& u) {
+    if (static_cast<Index>(u.size()) != p.n)
+        throw std::invalid_argument("semi_dual_hessian_quadform: length mismatch");
+    const Vec g = ctransform_of_f(p, f);
+    const double inv_eps = 1.0 / p.eps;
+    Vec term(p.m);
+    par_for(p.m, [&](Index j) {
+        double m1 = 0.0, m2 = 0.0;
+        for (Index i = 0; i < p.n; ++i) {
+            const double w = p.a[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
+            m1 += w * u[i];
+            m2 += w * u[i] * u[i];
+        }
+        term[j] = p.b[j] * (m2 - m1 * m1);
+    });
+    double acc = 0.0;
+    for (Index j = 0; j < p.m; ++j) acc += term[j];
+    return -acc * inv_eps;
+}
+
 // try_newton (solver.cpp:30-56)
 static bool try_newton(const Problem& p, Vec& f, const Vec& h, double value_at_f,
                        const double* V, Index ell, double& value_out, Vec* g_cand) {
@@ -933,6 +980,44 @@ int oracle_restricted_derivatives(const oracle_problem* q, const double* f, cons
         restricted_derivatives(p, ff, gg, V, ell, gr, he);
         std::memcpy(grad, gr.data(), sizeof(double) * ell);
         std::memcpy(hess, he.data(), sizeof(double) * ell * ell);
+    })
+}
+
+int oracle_dual_value(const oracle_problem* q, const double* f, const double* g, double* out) {
+    ORACLE_TRY({
+        Problem p = build(q);
+        Vec ff(f, f + p.n), gg(g, g + p.m);
+        *out = dual_value(p, ff, gg);
+    })
+}
+
+int oracle_semi_dual_hessian_quadform(const oracle_problem* q, const double* f, const double* u, double* out) {
+    ORACLE_TRY({
+        Problem p = build(q);
+        Vec ff(f, f + p.n), uu(u, u + p.n);
+        *out = semi_dual_hessian_quadform(p, ff, uu);
+    })
+}
+
+// newton_step (solver.cpp:59-69)
+int oracle_newton_step(const oracle_problem* q, const double* f, const double* V, long ell, double* f_out,
+                       int* accepted, int* factorization_failed) {
+    ORACLE_TRY({
+        Problem p = build(q);
+        if (ell < 1) throw std::invalid_argument("newton_step: empty basis");
+        Vec ff(f, f + p.n);
+        const Vec g = ctransform_of_f(p, ff);
+        const double value = dot(p.a, ff) + dot(p.b, g);
+        // factorization failure leaves f unchanged and is reported separately
+        Vec grad, hess;
+        restricted_derivatives(p, ff, g, V, ell, grad, hess);
+        Vec L(hess.size());
+        for (size_t t2 = 0; t2 < hess.size(); ++t2) L[t2] = -hess[t2];
+        *factorization_failed = cholesky(L, ell) ? 0 : 1;
+        double vout = value;
+        *accepted = 0;
+        if (!*factorization_failed) *accepted = try_newton(p, ff, g, value, V, ell, vout, nullptr) ? 1 : 0;
+        std::memcpy(f_out, ff.data(), sizeof(double) * p.n);
     })
 }
 

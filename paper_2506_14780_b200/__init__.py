@@ -87,6 +87,14 @@ _SIGS = {
     "sknr_ctransform_of_g": [_P, _D, _D],
     "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
     "sknr_coupling": [_P, _D, _D, _D],
+    "sknr_coupling_rows": [_P, _D, _D, _I64, _I64, _D],
+    "sknr_apply_R": [_P, _D, _D, _D, _D],
+    "sknr_apply_Rt": [_P, _D, _D, _D, _D],
+    "sknr_dual_value": [_P, _D, _D, _D],
+    "sknr_semi_dual_hessian_quadform": [_P, _D, _D, _D],
+    "sknr_newton_step": [_P, _D, _D, _I64, _D, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
+    "sknr_spectrum_report": [_P, _D, _D, _I64, ctypes.c_int, ctypes.c_double, _I64, _D, _D, _D, _D, _D],
+    "sknr_projector_distance": [_I64, _I64, _D, _D, _D],
     "sknr_semi_dual_value": [_P, _D, _D],
     "sknr_restricted_derivatives": [_P, _D, _D, _D, _I64, _D, _D],
     "sknr_apply_sym_block": [_P, _D, _D, _D, _I64, _D],
@@ -424,6 +432,43 @@ def coupling(problem: Problem, f, g) -> np.ndarray:
     return plan
 
 
+def coupling_rows(problem: Problem, f, g, row_begin: int, row_end: int) -> np.ndarray:
+    """Rows [row_begin, row_end) of coupling_from's plan (for streaming an n x m plan)."""
+    f = _checked(f, problem.n, "coupling_from(f)")
+    g = _checked(g, problem.m, "coupling_from(g)")
+    rows = int(row_end) - int(row_begin)
+    if rows < 0:
+        raise ValueError("coupling_rows: row range out of bounds")
+    block = np.empty((rows, problem.m), order="F")
+    _check(lib().sknr_coupling_rows(problem.handle, _ptr(f), _ptr(g), int(row_begin), int(row_end),
+                                    _ptr(block)))
+    return block
+
+
+def marginal_gap(problem: Problem, row, col):
+    """(l2, inf) = (||row - alpha||_2 + ||col - beta||_2, ||.||_inf + ||.||_inf) (core.cpp:145-150)."""
+    row, col = _vec(row), _vec(col)
+    if row.size != problem.n or col.size != problem.m:
+        raise ValueError("marginal_gap: length mismatch")
+    dr, dc = row - problem._alpha, col - problem._beta
+    return (float(np.linalg.norm(dr) + np.linalg.norm(dc)),
+            float(np.max(np.abs(dr)) + np.max(np.abs(dc))))
+
+
+def gauge_normalized(problem: Problem, f, g):
+    """(f - c, g + c) with c = alpha . f (core.cpp:152-157)."""
+    f, g = _vec(f), _vec(g)
+    c = float(problem._alpha @ f)
+    return f - c, g + c
+
+
+def gauge_distance(problem: Problem, a, b) -> float:
+    """max |.| between gauge-normalised potential pairs a=(f,g), b=(f,g) (core.cpp:159-165)."""
+    fa, ga = gauge_normalized(problem, *a)
+    fb, gb = gauge_normalized(problem, *b)
+    return float(max(np.max(np.abs(fa - fb)), np.max(np.abs(ga - gb))))
+
+
 def marginal_error(problem: Problem, plan) -> float:
     """||plan 1 - alpha||_2 + ||plan^T 1 - beta||_2 (core.cpp:105-112)."""
     plan = np.asarray(plan, dtype=np.float64)
@@ -445,6 +490,26 @@ def semi_dual_value(problem: Problem, f) -> float:
     f = _checked(f, problem.n, "ctransform_of_f")
     out = ctypes.c_double()
     _check(lib().sknr_semi_dual_value(problem.handle, _ptr(f), ctypes.byref(out)))
+    return out.value
+
+
+def dual_value(problem: Problem, f, g) -> float:
+    """a.f + b.g - eps*expm1(log sum_ij a_i b_j e^{(f_i+g_j-C_ij)/eps}) (objective.cpp:10-40)."""
+    f = _checked(f, problem.n, "dual_value")
+    g = _checked(g, problem.m, "dual_value")
+    out = ctypes.c_double()
+    _check(lib().sknr_dual_value(problem.handle, _ptr(f), _ptr(g), ctypes.byref(out)))
+    return out.value
+
+
+def semi_dual_hessian_quadform(problem: Problem, f, u) -> float:
+    """u^T H(f) u of the semi-dual (objective.cpp:53-77)."""
+    f = _checked(f, problem.n, "ctransform_of_f")
+    u = _vec(u)
+    if u.size != problem.n:
+        raise ValueError("semi_dual_hessian_quadform: length mismatch")
+    out = ctypes.c_double()
+    _check(lib().sknr_semi_dual_hessian_quadform(problem.handle, _ptr(f), _ptr(u), ctypes.byref(out)))
     return out.value
 
 
@@ -475,6 +540,35 @@ def restricted_derivatives(problem: Problem, f, basis: SpectralBasis, g=None):
 
 
 # ---------------------------------------------------------------- spectral.hpp
+def apply_R(problem: Problem, f, g, g1) -> np.ndarray:
+    """(R g1)_i = sum_j e^{(f_i+g_j-C_ij)/eps} b_j g1_j (spectral.cpp:29-43)."""
+    f = _checked(f, problem.n, "SinkhornOperator(f)")
+    g = _checked(g, problem.m, "SinkhornOperator(g)")
+    g1 = _vec(g1)
+    if g1.size != problem.m:
+        raise ValueError("apply_R: length mismatch")
+    out = np.empty(problem.n)
+    _check(lib().sknr_apply_R(problem.handle, _ptr(f), _ptr(g), _ptr(g1), _ptr(out)))
+    return out
+
+
+def apply_Rt(problem: Problem, f, g, f1) -> np.ndarray:
+    """(R^T f1)_j = sum_i e^{(f_i+g_j-C_ij)/eps} a_i f1_i (spectral.cpp:45-62)."""
+    f = _checked(f, problem.n, "SinkhornOperator(f)")
+    g = _checked(g, problem.m, "SinkhornOperator(g)")
+    f1 = _vec(f1)
+    if f1.size != problem.n:
+        raise ValueError("apply_Rt: length mismatch")
+    out = np.empty(problem.m)
+    _check(lib().sknr_apply_Rt(problem.handle, _ptr(f), _ptr(g), _ptr(f1), _ptr(out)))
+    return out
+
+
+def apply_K(problem: Problem, f, g, f1, g1):
+    """(apply_R(g1), apply_Rt(f1)) (spectral.cpp:64-66)."""
+    return apply_R(problem, f, g, g1), apply_Rt(problem, f, g, f1)
+
+
 def apply_sym_block(problem: Problem, f, g, v) -> np.ndarray:
     f, g, v = _vec(f), _vec(g), _mat_f(v)
     out = np.empty((problem.n, v.shape[1]), order="F")
@@ -516,7 +610,71 @@ def top_modes(problem: Problem, f, g, ell: int, tol: float = 1e-8,
     return SpectralBasis(vec, vsym, rhos, problem.epsilon, int(sweeps.value))
 
 
+def spectrum(problem: Problem, f, g, k: int, vectors: bool = False, tol: float = 1e-8,
+             max_power_iters: int = -1) -> dict:
+    """spectrum_report (spectral.cpp:195-228) as the reference binding's dict
+    (bindings.cpp:118-136): epsilon, rho, eigenvalues_of_K (+rho, -rho),
+    hessian_eigs_low/high = (1 -+ rho)/eps and, with vectors, vectors_f (n x k)
+    and vectors_g (m x k)."""
+    f = _checked(f, problem.n, "SinkhornOperator(f)")
+    g = _checked(g, problem.m, "SinkhornOperator(g)")
+    k = int(k)
+    if k < 1 or k > min(problem.n, problem.m) - 1:
+        raise ValueError("spectrum_report: need 1 <= k <= min(n,m)-1")
+    rho, lo, hi = np.empty(k), np.empty(k), np.empty(k)
+    vf = np.empty((problem.n, k), order="F") if vectors else None
+    vg = np.empty((problem.m, k), order="F") if vectors else None
+    _check(lib().sknr_spectrum_report(problem.handle, _ptr(f), _ptr(g), k, 1 if vectors else 0, float(tol),
+                                      int(max_power_iters), _ptr(rho), _ptr(lo), _ptr(hi), _ptr(vf), _ptr(vg)))
+    out = {"epsilon": problem.epsilon, "rho": rho, "eigenvalues_of_K": [(float(r), float(-r)) for r in rho],
+           "hessian_eigs_low": lo, "hessian_eigs_high": hi}
+    if vectors:
+        out["vectors_f"] = vf
+        out["vectors_g"] = vg
+    return out
+
+
+def projector_distance(basis_a: SpectralBasis, basis_b: SpectralBasis) -> float:
+    """||P_A - P_B||_2 = ||(I - A A^T) B||_2 in symmetrised coordinates (spectral.cpp:230-242)."""
+    a, b = _mat_f(basis_a.vectors_sym), _mat_f(basis_b.vectors_sym)
+    if a.shape != b.shape:
+        raise ValueError("projector_distance: dimension mismatch")
+    out = ctypes.c_double()
+    _check(lib().sknr_projector_distance(a.shape[0], a.shape[1], _ptr(a), _ptr(b), ctypes.byref(out)))
+    return out.value
+
+
 # ---------------------------------------------------------------- solver.hpp
+@dataclass
+class NewtonOutcome:
+    """NewtonOutcome (solver.hpp:50-57)."""
+
+    f: np.ndarray
+    accepted: bool
+    factorization_failed: bool
+
+
+def sk_sweep(problem: Problem, f, g=None):
+    """One Sinkhorn sweep, g-then-f (solver.cpp:12-17): returns (f', g')."""
+    g1 = ctransform_of_f(problem, f)
+    return ctransform_of_g(problem, g1), g1
+
+
+def newton_step(problem: Problem, f, basis: SpectralBasis) -> NewtonOutcome:
+    """One restricted Newton step from f (solver.cpp:59-69)."""
+    if basis.ell < 1:
+        raise ValueError("newton_step: empty basis")
+    f = _checked(f, problem.n, "ctransform_of_f")
+    V = _mat_f(basis.vectors)
+    if V.shape[0] != problem.n:
+        raise ValueError("restricted_derivatives: basis dimension mismatch")
+    fo = np.empty(problem.n)
+    acc, fail = ctypes.c_int(), ctypes.c_int()
+    _check(lib().sknr_newton_step(problem.handle, _ptr(f), _ptr(V), V.shape[1], _ptr(fo), ctypes.byref(acc),
+                                  ctypes.byref(fail)))
+    return NewtonOutcome(fo, bool(acc.value), bool(fail.value))
+
+
 def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False) -> _Config:
     c = _Config()
     lib().sknr_config_default(ctypes.byref(c))
@@ -674,8 +832,11 @@ def bench_fp64_peak():
 
 
 __all__ = [
-    "EigensolverError", "IterationRecord", "PointProblem", "Problem", "SolveResult", "SpectralBasis",
-    "__version__", "anneal", "apply_sym_block", "apply_sym_t_block", "coupling", "ctransform_of_f",
+    "EigensolverError", "IterationRecord", "NewtonOutcome", "PointProblem", "Problem", "SolveResult",
+    "SpectralBasis", "__version__", "anneal", "apply_K", "apply_R", "apply_Rt", "apply_sym_block",
+    "apply_sym_t_block", "coupling", "coupling_rows", "ctransform_of_f", "dual_value", "gauge_distance",
+    "gauge_normalized", "marginal_gap", "newton_step", "projector_distance", "semi_dual_hessian_quadform",
+    "sk_sweep", "spectrum",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
     "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
     "row_partition", "shard", "semi_dual_gradient", "semi_dual_value", "solve",

@@ -552,17 +552,19 @@ __global__ void k_eye(double* Q, int64_t n, int k) {
         Q[e] = (e % n == e / n) ? 1.0 : 0.0;
 }
 
-// plan_ij = a_i b_j exp((f_i + g_j - C_ij)/eps)  (coupling_from, core.cpp:84-103)
+// plan_ij = a_i b_j exp((f_i + g_j - C_ij)/eps)  (coupling_from, core.cpp:84-103) for the
+// rows [r0, r0 + rows), col-major with leading dimension rows; f is indexed globally.
 __global__ void k_coupling(const double* C, const double* x, const double* y, int64_t n, int64_t m,
-                           int d, double kappa, const double* a, const double* b, const double* f,
-                           const double* g, double inv_eps, double* plan) {
-    const int64_t total = n * m;
+                           int64_t r0, int64_t rows, int d, double kappa, const double* a,
+                           const double* b, const double* f, const double* g, double inv_eps,
+                           double* plan) {
+    const int64_t total = rows * m;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % n, j = e / n;
+        const int64_t i = r0 + e % rows, j = e / rows;
         double c;
         if (C) {
-            c = C[e];
+            c = C[i + j * n];
         } else {
             double s = 0.0;
             for (int q = 0; q < d; ++q) {
@@ -2149,26 +2151,51 @@ int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double
     SKNR_API_END
 }
 
-int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan) {
+int sknr_coupling_rows(sknr_problem h, const double* f, const double* g, int64_t row_begin, int64_t row_end,
+                       double* plan_rows) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
     if (P.shard) throw RuntimeFailure("coupling_from: not available on a row-sharded problem");
+    if (row_begin < 0 || row_end > P.n || row_begin > row_end)
+        throw InvalidArgument("coupling_rows: row range out of bounds");
     check_finite_vec(f, P.n, "coupling_from(f)");
     check_finite_vec(g, P.m, "coupling_from(g)");
-    DBuf df, dg, dp, x, y;
+    const int64_t rows = row_end - row_begin;
+    if (rows == 0) return SKNR_OK;
+    // host-side block size bounded to 1 GiB of device scratch per launch
+    const int64_t m = P.m;
+    const int64_t cap_rows = std::max<int64_t>(1, (int64_t(1) << 27) / std::max<int64_t>(m, 1));
+    DBuf df, dg, dp;
     df.ensure(P.n);
-    dg.ensure(P.m);
-    dp.ensure(P.n * P.m);
+    dg.ensure(m);
     upload(df.p, f, P.n, P.stream);
-    upload(dg.p, g, P.m, P.stream);
-    count_launch();
-    k_coupling<<<grid_for(P.n * P.m), AUX_NT, 0, P.stream>>>(
-        P.kind == 0 || P.C.p ? P.C.p : nullptr, P.src.coords.p, P.tgt.coords.p, P.n, P.m,
-        static_cast<int>(P.d), P.kappa, P.src.w.p, P.tgt.w.p, df.p, dg.p, P.inv_eps(), dp.p);
-    download(plan, dp.p, P.n * P.m, P.stream);
+    upload(dg.p, g, m, P.stream);
+    const bool whole = rows <= cap_rows;
+    dp.ensure((whole ? rows : cap_rows) * m);
+    std::vector<double> tmp;
+    for (int64_t r = row_begin; r < row_end; r += cap_rows) {
+        const int64_t cnt = std::min(cap_rows, row_end - r);
+        count_launch();
+        k_coupling<<<grid_for(cnt * m), AUX_NT, 0, P.stream>>>(
+            P.kind == 0 || P.C.p ? P.C.p : nullptr, P.src.coords.p, P.tgt.coords.p, P.n, m, r, cnt,
+            static_cast<int>(P.d), P.kappa, P.src.w.p, P.tgt.w.p, df.p, dg.p, P.inv_eps(), dp.p);
+        if (whole) {
+            download(plan_rows, dp.p, cnt * m, P.stream);
+        } else {  // scatter the cnt-row block into the rows-leading-dimension output
+            tmp.resize(cnt * m);
+            download(tmp.data(), dp.p, cnt * m, P.stream);
+            CK(cudaStreamSynchronize(P.stream));
+            for (int64_t j = 0; j < m; ++j)
+                std::memcpy(plan_rows + (r - row_begin) + j * rows, tmp.data() + j * cnt, sizeof(double) * cnt);
+        }
+    }
     CK(cudaStreamSynchronize(P.stream));
     SKNR_API_END
+}
+
+int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan) {
+    return sknr_coupling_rows(h, f, g, 0, h && h->p ? h->p->n : 0, plan);
 }
 
 int sknr_semi_dual_value(sknr_problem h, const double* f, double* value) {
@@ -2331,6 +2358,281 @@ int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const
 int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
                       int64_t max_power_iters, int method, int degree, double* vectors, double* vectors_sym,
                       double* rhos, int64_t* sweeps);
+
+// ---- SinkhornOperator::apply_R / apply_Rt (spectral.cpp:29-62): one k=1 block pass each.
+// dir 1: (R g1)_i = sum_j e^{(f_i+g_j-C_ij)/eps} (b_j g1_j); dir 0: (Rt f1)_j = sum_i e^{..} (a_i f1_i)
+static void apply_R_dir(sknr_problem h, int dir, const double* f, const double* g, const double* v, double* out,
+                        const char* what) {
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    check_finite_vec(f, P.n_global, "SinkhornOperator(f)");
+    check_finite_vec(g, P.m, "SinkhornOperator(g)");
+    const int64_t n = P.n, m = P.m;
+    const int64_t nv = dir == 0 ? n : m, nout = dir == 0 ? m : n;
+    if (!v) throw InvalidArgument(std::string(what) + ": null pointer");
+    const int kt = block_kt_for(1);
+    DBuf df, dg, dv, W, O;
+    df.ensure(n);
+    dg.ensure(m);
+    dv.ensure(nv);
+    W.ensure(nv * kt);
+    O.ensure(nout);
+    upload_rows(P, df.p, f);
+    upload(dg.p, g, m, P.stream);
+    if (dir == 0)
+        upload_rows(P, dv.p, v);
+    else
+        upload(dv.p, v, m, P.stream);
+    count_launch();
+    k_pack_w<<<grid_for(nv * kt), AUX_NT, 0, P.stream>>>(dv.p, nv, nv, 1, kt, dir == 0 ? P.src.w.p : P.tgt.w.p,
+                                                         W.p);
+    PassSpec ps;
+    ps.dir = dir;
+    ps.in_v = dir == 0 ? df.p : dg.p;
+    ps.out_v = dir == 0 ? dg.p : df.p;
+    ps.W = W.p;
+    ps.k = 1;
+    ps.kt = kt;
+    ps.out = O.p;
+    plan_pass(P, ps);
+    if (dir == 0)
+        download(out, O.p, m, P.stream);
+    else
+        gather_rows(P, O.p, out);
+    CK(cudaStreamSynchronize(P.stream));
+}
+
+int sknr_apply_R(sknr_problem h, const double* f, const double* g, const double* g1, double* out) {
+    SKNR_API_BEGIN
+    apply_R_dir(h, 1, f, g, g1, out, "apply_R");
+    SKNR_API_END
+}
+
+int sknr_apply_Rt(sknr_problem h, const double* f, const double* g, const double* f1, double* out) {
+    SKNR_API_BEGIN
+    apply_R_dir(h, 0, f, g, f1, out, "apply_Rt");
+    SKNR_API_END
+}
+
+// ---- dual_value (objective.cpp:10-40): a.f + b.g - eps expm1(log sum_ij a_i b_j e^{(f_i+g_j-C_ij)/eps}).
+// The double sum is taken as sum_i a_i e^{(f_i - f~_i)/eps} with f~ = g^{C,eps} (one row-LSE pass),
+// max-shifted on the host.
+int sknr_dual_value(sknr_problem h, const double* f, const double* g, double* value) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    const int64_t n = P.n_global, m = P.m;
+    if (!f || !g || !value) throw InvalidArgument("dual_value: null pointer");
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(f[i])) throw InvalidArgument("dual_value: potentials must be finite");
+    for (int64_t j = 0; j < m; ++j)
+        if (!std::isfinite(g[j])) throw InvalidArgument("dual_value: potentials must be finite");
+    std::vector<double> ft(n);
+    const int rc = sknr_ctransform_of_g(h, g, ft.data());
+    if (rc != SKNR_OK) return rc;
+    const double inv_eps = 1.0 / P.eps;
+    double shift = -std::numeric_limits<double>::infinity();
+    std::vector<double> t(n);
+    for (int64_t i = 0; i < n; ++i) {
+        t[i] = std::log(P.h_alpha[i]) + (f[i] - ft[i]) * inv_eps;
+        shift = std::max(shift, t[i]);
+    }
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) total += std::exp(t[i] - shift);
+    const double log_mass = shift + std::log(total);
+    double af = 0.0, bg = 0.0;
+    for (int64_t i = 0; i < n; ++i) af += P.h_alpha[i] * f[i];
+    for (int64_t j = 0; j < m; ++j) bg += P.h_beta[j] * g[j];
+    *value = af + bg - P.eps * std::expm1(log_mass);
+    SKNR_API_END
+}
+
+// ---- semi_dual_hessian_quadform (objective.cpp:53-77): -(1/eps) sum_j b_j (m2_j - m1_j^2) with
+// m1_j = sum_i P~_ij u_i, m2_j = sum_i P~_ij u_i^2 at g = f^{C,eps}: one k=2 block pass.
+int sknr_semi_dual_hessian_quadform(sknr_problem h, const double* f, const double* u, double* value) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    const int64_t n = P.n_global, m = P.m;
+    if (!u || !value) throw InvalidArgument("semi_dual_hessian_quadform: null pointer");
+    std::vector<double> g(m);
+    int rc = sknr_ctransform_of_f(h, f, g.data());
+    if (rc != SKNR_OK) return rc;
+    std::vector<double> U(2 * n);
+    for (int64_t i = 0; i < n; ++i) {
+        U[i] = u[i];
+        U[n + i] = u[i] * u[i];
+    }
+    std::vector<double> M(2 * m);
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        const int kt = block_kt_for(2);
+        DBuf df, dg, dU, W, O;
+        df.ensure(P.n);
+        dg.ensure(m);
+        dU.ensure(2 * P.n);
+        W.ensure(P.n * kt);
+        O.ensure(2 * m);
+        upload_rows(P, df.p, f);
+        upload(dg.p, g.data(), m, P.stream);
+        upload_rows(P, dU.p, U.data(), 2);
+        count_launch();
+        k_pack_w<<<grid_for(P.n * kt), AUX_NT, 0, P.stream>>>(dU.p, P.n, P.n, 2, kt, nullptr, W.p);
+        PassSpec ps;
+        ps.dir = 0;
+        ps.in_v = df.p;
+        ps.in_lw = P.src.lw.p;
+        ps.out_v = dg.p;
+        ps.W = W.p;
+        ps.k = 2;
+        ps.kt = kt;
+        ps.out = O.p;
+        plan_pass(P, ps);
+        download(M.data(), O.p, 2 * m, P.stream);
+        CK(cudaStreamSynchronize(P.stream));
+    }
+    double acc = 0.0;
+    for (int64_t j = 0; j < m; ++j) acc += P.h_beta[j] * (M[m + j] - M[j] * M[j]);
+    *value = -acc / P.eps;
+    SKNR_API_END
+}
+
+// Eigen::LLT<Matrix>(A) convention (llt_inplace::unblocked): fails iff a pivot is <= 0 or NaN.
+static bool host_llt_solve(std::vector<double> A, int l, const double* b, double* x) {
+    for (int k = 0; k < l; ++k) {
+        double piv = A[k + k * l];
+        for (int j = 0; j < k; ++j) piv -= A[k + j * l] * A[k + j * l];
+        if (!(piv > 0.0)) return false;
+        const double d = std::sqrt(piv);
+        A[k + k * l] = d;
+        for (int i = k + 1; i < l; ++i) {
+            double s = A[i + k * l];
+            for (int j = 0; j < k; ++j) s -= A[i + j * l] * A[k + j * l];
+            A[i + k * l] = s / d;
+        }
+    }
+    std::vector<double> y(l);
+    for (int i = 0; i < l; ++i) {
+        double s = b[i];
+        for (int j = 0; j < i; ++j) s -= A[i + j * l] * y[j];
+        y[i] = s / A[i + i * l];
+    }
+    for (int i = l - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int j = i + 1; j < l; ++j) s -= A[j + i * l] * x[j];
+        x[i] = s / A[i + i * l];
+    }
+    return true;
+}
+
+// ---- newton_step (solver.cpp:59-69 with try_newton :30-56): g = f^{C,eps}, Q0 = a.f + b.g,
+// restricted derivatives, LLT(-H) (reject on failure), delta, f' = f + V delta, accept iff Q(f') > Q0.
+int sknr_newton_step(sknr_problem h, const double* f, const double* vectors, int64_t ell, double* f_out,
+                     int* accepted, int* factorization_failed) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    if (ell < 1) throw InvalidArgument("newton_step: empty basis");
+    if (!vectors || !f_out || !accepted || !factorization_failed)
+        throw InvalidArgument("newton_step: null pointer");
+    const int64_t n = P.n_global, m = P.m;
+    const int l = static_cast<int>(ell);
+    std::vector<double> g(m), grad(l), hess(static_cast<size_t>(l) * l);
+    int rc = sknr_ctransform_of_f(h, f, g.data());
+    if (rc != SKNR_OK) return rc;
+    double af = 0.0, bg = 0.0;
+    for (int64_t i = 0; i < n; ++i) af += P.h_alpha[i] * f[i];
+    for (int64_t j = 0; j < m; ++j) bg += P.h_beta[j] * g[j];
+    const double value = af + bg;
+    rc = sknr_restricted_derivatives(h, f, g.data(), vectors, ell, grad.data(), hess.data());
+    if (rc != SKNR_OK) return rc;
+    std::vector<double> negH(hess.size()), delta(l);
+    for (size_t e = 0; e < hess.size(); ++e) negH[e] = -hess[e];
+    *accepted = 0;
+    *factorization_failed = 0;
+    std::memcpy(f_out, f, sizeof(double) * n);
+    if (!host_llt_solve(negH, l, grad.data(), delta.data())) {
+        *factorization_failed = 1;
+        return SKNR_OK;
+    }
+    std::vector<double> cand(n);
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int c = 0; c < l; ++c) s += vectors[i + c * n] * delta[c];
+        cand[i] = f[i] + s;
+    }
+    double q1 = 0.0;
+    rc = sknr_semi_dual_value(h, cand.data(), &q1);
+    if (rc != SKNR_OK) return rc;
+    if (q1 > value) {
+        std::memcpy(f_out, cand.data(), sizeof(double) * n);
+        *accepted = 1;
+    }
+    SKNR_API_END
+}
+
+// ---- projector_distance (spectral.cpp:230-242): ||(I - A A^T) B||_2 for n x k column blocks,
+// via the largest eigenvalue of R^T R, R = B - A (A^T B); clamped to [0, 1]. Host arithmetic
+// (O(n k^2), a diagnostic off the solve path).
+int sknr_projector_distance(int64_t n, int64_t k, const double* a_sym, const double* b_sym, double* out) {
+    SKNR_API_BEGIN
+    if (n < 1 || k < 1 || !a_sym || !b_sym || !out) throw InvalidArgument("projector_distance: dimension mismatch");
+    std::vector<double> AtB(static_cast<size_t>(k) * k, 0.0), R(static_cast<size_t>(n) * k);
+    for (int64_t c = 0; c < k; ++c)
+        for (int64_t a = 0; a < k; ++a) {
+            double s = 0.0;
+            for (int64_t i = 0; i < n; ++i) s += a_sym[i + a * n] * b_sym[i + c * n];
+            AtB[a + c * k] = s;
+        }
+    for (int64_t c = 0; c < k; ++c)
+        for (int64_t i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int64_t a = 0; a < k; ++a) s += a_sym[i + a * n] * AtB[a + c * k];
+            R[i + c * n] = b_sym[i + c * n] - s;
+        }
+    std::vector<double> G(static_cast<size_t>(k) * k);
+    for (int64_t c = 0; c < k; ++c)
+        for (int64_t a = 0; a <= c; ++a) {
+            double s = 0.0;
+            for (int64_t i = 0; i < n; ++i) s += R[i + a * n] * R[i + c * n];
+            G[a + c * k] = G[c + a * k] = s;
+        }
+    std::vector<double> ev, evec;
+    host_sym_eig(G, static_cast<int>(k), ev, evec);
+    double lmax = 0.0;
+    for (double e : ev) lmax = std::max(lmax, e);
+    *out = std::clamp(std::sqrt(std::max(lmax, 0.0)), 0.0, 1.0);
+    SKNR_API_END
+}
+
+// ---- spectrum_report (spectral.cpp:195-228): top_modes at the anchor, Hessian eigenvalue pairs
+// (1 -+ rho)/eps, optional right vectors v = R~^T u / rho in potential coordinates.
+int sknr_spectrum_report(sknr_problem h, const double* f, const double* g, int64_t k, int include_vectors,
+                         double tol, int64_t max_power_iters, double* rhos, double* hess_low, double* hess_high,
+                         double* vectors_f, double* vectors_g) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    const int64_t n = P.n_global, m = P.m;
+    if (k < 1 || k > std::min(n, m) - 1) throw InvalidArgument("spectrum_report: need 1 <= k <= min(n,m)-1");
+    if (!rhos || !hess_low || !hess_high) throw InvalidArgument("spectrum_report: null pointer");
+    std::vector<double> vec(static_cast<size_t>(n) * k), vsym(static_cast<size_t>(n) * k);
+    int64_t sweeps = 0;
+    int rc = sknr_top_modes(h, f, g, k, tol, max_power_iters, vec.data(), vsym.data(), rhos, &sweeps);
+    if (rc != SKNR_OK) return rc;
+    for (int64_t a = 0; a < k; ++a) {
+        hess_low[a] = (1.0 - rhos[a]) / P.eps;
+        hess_high[a] = (1.0 + rhos[a]) / P.eps;
+    }
+    if (include_vectors) {
+        if (!vectors_f || !vectors_g) throw InvalidArgument("spectrum_report: null pointer");
+        std::memcpy(vectors_f, vec.data(), sizeof(double) * n * k);
+        std::vector<double> vs(static_cast<size_t>(m) * k);
+        rc = sknr_apply_sym_t_block(h, f, g, vsym.data(), k, vs.data());
+        if (rc != SKNR_OK) return rc;
+        for (int64_t a = 0; a < k; ++a)
+            for (int64_t j = 0; j < m; ++j)
+                vectors_g[j + a * m] = rhos[a] > 1e-12 ? (vs[j + a * m] / rhos[a]) / std::sqrt(P.h_beta[j]) : 0.0;
+    }
+    SKNR_API_END
+}
+
 
 int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
                    int64_t max_power_iters, double* vectors, double* vectors_sym, double* rhos,

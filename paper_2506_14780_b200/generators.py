@@ -205,3 +205,102 @@ def sq_euclidean_cost(x: np.ndarray, y: np.ndarray, cost_scale: float = 1.0) -> 
     if cost_scale != 1.0:
         c = c / (1.0 / cost_scale)
     return np.asfortranarray(c)
+
+
+# ---------------------------------------------------------------- named 2-d families
+# harness generators (generators.cpp:19-92) and make_instance (experiments.cpp:83-106),
+# used by the CLI's --synthetic flag. Points come back n x 2 column-major with
+# uniform weights, drawn in the reference's order from the scalar stream.
+def gaussian_cloud(count: int, mean, cov, seed: int):
+    """mean + L z with L = chol(cov), z = (normal, normal) per point (generators.cpp:19-36)."""
+    if count < 1:
+        raise ValueError("gaussian_cloud: count must be positive")
+    cov = np.asarray(cov, dtype=np.float64).reshape(2, 2)
+    mean = np.asarray(mean, dtype=np.float64).reshape(2)
+    if np.max(np.abs(cov - cov.T)) > 1e-12:
+        raise ValueError("gaussian_cloud: covariance must be symmetric")
+    # Eigen LLT of a 2 x 2 (lower factor)
+    if not cov[0, 0] > 0.0:
+        raise ValueError("gaussian_cloud: covariance must be positive definite")
+    l00 = math.sqrt(cov[0, 0])
+    l10 = cov[1, 0] / l00
+    piv = cov[1, 1] - l10 * l10
+    if not piv > 0.0:
+        raise ValueError("gaussian_cloud: covariance must be positive definite")
+    l11 = math.sqrt(piv)
+    rng = SplitMix64(seed)
+    pts = np.empty((count, 2))
+    for i in range(count):
+        z0 = rng.normal()
+        z1 = rng.normal()
+        pts[i, 0] = mean[0] + l00 * z0
+        pts[i, 1] = mean[1] + (l10 * z0 + l11 * z1)
+    return np.asfortranarray(pts), _uniform_weights(count)
+
+
+def two_moons(count_per_moon: int, noise: float, seed: int):
+    """Upper and lower half-moons (generators.cpp:38-59)."""
+    if count_per_moon < 1:
+        raise ValueError("two_moons: count must be positive")
+    if noise < 0.0:
+        raise ValueError("two_moons: noise must be nonnegative")
+    rng = SplitMix64(seed)
+    upper = np.empty((count_per_moon, 2))
+    lower = np.empty((count_per_moon, 2))
+    for i in range(count_per_moon):
+        th = rng.uniform(0.0, math.pi)
+        upper[i, 0] = math.cos(th) + noise * rng.normal()
+        upper[i, 1] = math.sin(th) + noise * rng.normal()
+    for i in range(count_per_moon):
+        th = rng.uniform(0.0, math.pi)
+        lower[i, 0] = 1.0 - math.cos(th) + noise * rng.normal()
+        lower[i, 1] = 0.5 - math.sin(th) + noise * rng.normal()
+    w = _uniform_weights(count_per_moon)
+    return (np.asfortranarray(upper), w), (np.asfortranarray(lower), w.copy())
+
+
+def annulus_and_square(count_annulus: int, count_square: int, r_in: float, r_out: float, side: float,
+                       seed: int):
+    """Rejection-sampled annulus and a uniform square from one stream (generators.cpp:61-92)."""
+    if count_annulus < 1 or count_square < 1:
+        raise ValueError("annulus_and_square: counts must be positive")
+    if not (0.0 <= r_in < r_out):
+        raise ValueError("annulus_and_square: need 0 <= r_in < r_out")
+    if not side > 0.0:
+        raise ValueError("annulus_and_square: side must be positive")
+    rng = SplitMix64(seed)
+    ann = np.empty((count_annulus, 2))
+    for i in range(count_annulus):
+        while True:
+            x = rng.uniform(-r_out, r_out)
+            y = rng.uniform(-r_out, r_out)
+            q = x * x + y * y
+            if not (q > r_out * r_out or q < r_in * r_in):
+                break
+        ann[i] = (x, y)
+    half = side / 2.0
+    sq = np.empty((count_square, 2))
+    for i in range(count_square):
+        sq[i, 0] = rng.uniform(-half, half)
+        sq[i, 1] = rng.uniform(-half, half)
+    return ((np.asfortranarray(ann), _uniform_weights(count_annulus)),
+            (np.asfortranarray(sq), _uniform_weights(count_square)))
+
+
+def make_instance(family: str, n: int, m: int, seed: int = 1, noise: float = 0.05, r_in: float = 0.5,
+                  r_out: float = 1.0, side: float = 2.0):
+    """(x, alpha, y, beta) of a named family (experiments.cpp:83-106): gauss2d | two_moons |
+    annulus_square; target stream seeded seed ^ 0xD1B54A32D192ED03."""
+    tseed = (seed ^ TARGET_XOR) & _M64
+    if family == "gauss2d":
+        xs, a = gaussian_cloud(n, (0.0, 0.0), np.eye(2), seed)
+        yt, b = gaussian_cloud(m, (4.0, 4.0), [[1.0, -0.8], [-0.8, 1.0]], tseed)
+        return xs, a, yt, b
+    if family == "two_moons":
+        (xs, a), _ = two_moons(n, noise, seed)
+        _, (yt, b) = two_moons(m, noise, tseed)
+        return xs, a, yt, b
+    if family == "annulus_square":
+        (xs, a), (yt, b) = annulus_and_square(n, m, r_in, r_out, side, seed)
+        return xs, a, yt, b
+    raise ValueError(f"make_instance: unknown family '{family}'")

@@ -192,6 +192,44 @@ def apply_sym_t_block(P: Instance, f, g, U):
     return out
 
 
+def apply_R(P: Instance, f, g, g1):
+    f, g, g1 = (np.ascontiguousarray(v, dtype=np.float64) for v in (f, g, g1))
+    out = np.empty(P.n)
+    _check(lib().oracle_apply_R(ctypes.byref(P.s), _p(f), _p(g), _p(g1), _p(out)))
+    return out
+
+
+def apply_Rt(P: Instance, f, g, f1):
+    f, g, f1 = (np.ascontiguousarray(v, dtype=np.float64) for v in (f, g, f1))
+    out = np.empty(P.m)
+    _check(lib().oracle_apply_Rt(ctypes.byref(P.s), _p(f), _p(g), _p(f1), _p(out)))
+    return out
+
+
+def dual_value(P: Instance, f, g):
+    f, g = (np.ascontiguousarray(v, dtype=np.float64) for v in (f, g))
+    out = ctypes.c_double()
+    _check(lib().oracle_dual_value(ctypes.byref(P.s), _p(f), _p(g), ctypes.byref(out)))
+    return out.value
+
+
+def semi_dual_hessian_quadform(P: Instance, f, u):
+    f, u = (np.ascontiguousarray(v, dtype=np.float64) for v in (f, u))
+    out = ctypes.c_double()
+    _check(lib().oracle_semi_dual_hessian_quadform(ctypes.byref(P.s), _p(f), _p(u), ctypes.byref(out)))
+    return out.value
+
+
+def newton_step(P: Instance, f, V):
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    V = np.asfortranarray(V, dtype=np.float64)
+    fo = np.empty(P.n)
+    acc, fail = ctypes.c_int(), ctypes.c_int()
+    _check(lib().oracle_newton_step(ctypes.byref(P.s), _p(f), _p(V), ctypes.c_long(V.shape[1]), _p(fo),
+                                    ctypes.byref(acc), ctypes.byref(fail)))
+    return fo, bool(acc.value), bool(fail.value)
+
+
 def top_modes(P: Instance, f, g, ell, tol=1e-8, max_power_iters=-1):
     f = np.ascontiguousarray(f, dtype=np.float64)
     g = np.ascontiguousarray(g, dtype=np.float64)

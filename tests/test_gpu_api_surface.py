@@ -1,0 +1,253 @@
+"""GPU checks of the rest of the reference API surface (SinkhornOperator apply_R /
+apply_Rt, dual_value, semi_dual_hessian_quadform, newton_step, sk_sweep,
+spectrum_report, projector_distance, streamed coupling, harness oracle_solve /
+full_semi_dual_hessian, and the CLI) against the CPU oracle and the reference's
+own closed-form tests."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_ref as O
+import paper_2506_14780_b200 as sk
+from paper_2506_14780_b200 import cli
+from paper_2506_14780_b200 import generators as G
+from paper_2506_14780_b200 import harness as H
+from paper_2506_14780_b200 import io as sio
+from support import (projector_distance, random_problem_data, random_vector, rel_err, symmetric_2x2,
+                     symmetric_2x2_optimum)
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_pair(seed, n, m, eps):
+    rng = G.SplitMix64(seed)
+    cost, a, b = random_problem_data(rng, n, m)
+    return sk.Problem(cost, a, b, eps), O.Instance(a, b, eps, cost=cost), rng
+
+
+def points_pair(seed, n, m, d, eps):
+    r = np.random.default_rng(seed)
+    x = np.asfortranarray(r.uniform(0, 1, (n, d)))
+    y = np.asfortranarray(r.uniform(0, 1, (m, d)))
+    a = r.uniform(0.5, 1.5, n)
+    a /= a.sum()
+    b = r.uniform(0.5, 1.5, m)
+    b /= b.sum()
+    return sk.PointProblem(x, y, a, b, eps), O.Instance(a, b, eps, x=x, y=y), r
+
+
+@pytest.mark.parametrize("kind", ["dense", "points"])
+def test_apply_R_and_Rt_match_oracle(kind):  # spectral.cpp:29-66
+    if kind == "dense":
+        gp, op, rng = dense_pair(11, 150, 97, 0.1)
+        f = random_vector(rng, 150, 0.1)
+        g1 = random_vector(rng, 97)
+        f1 = random_vector(rng, 150)
+    else:
+        gp, op, r = points_pair(12, 300, 211, 3, 0.02)
+        f = r.uniform(-0.05, 0.05, 300)
+        g1 = r.standard_normal(211)
+        f1 = r.standard_normal(300)
+    g = O.ctransform_of_f(op, f)
+    assert rel_err(sk.apply_R(gp, f, g, g1), O.apply_R(op, f, g, g1)) <= 1e-12
+    assert rel_err(sk.apply_Rt(gp, f, g, f1), O.apply_Rt(op, f, g, f1)) <= 1e-12
+    rk, rtk = sk.apply_K(gp, f, g, f1, g1)
+    assert rel_err(rk, O.apply_R(op, f, g, g1)) <= 1e-12 and rel_err(rtk, O.apply_Rt(op, f, g, f1)) <= 1e-12
+    with pytest.raises(ValueError, match="length mismatch"):
+        sk.apply_R(gp, f, g, f1)
+
+
+@pytest.mark.parametrize("kind", ["dense", "points"])
+def test_dual_value_matches_oracle(kind):  # objective.cpp:10-40
+    gp, op, _ = dense_pair(21, 64, 80, 0.2) if kind == "dense" else points_pair(22, 200, 150, 2, 0.05)
+    r = sk.solve(gp, tol=1e-12)
+    for f, g in [(r.f, r.g), (r.f + 0.01, r.g - 0.02)]:
+        v_gpu = sk.dual_value(gp, f, g)
+        v_ref = O.dual_value(op, f, g)
+        assert abs(v_gpu - v_ref) <= 1e-12 * max(1.0, abs(v_ref))
+    # at the optimum the dual equals the semi-dual (total mass 1)
+    assert abs(sk.dual_value(gp, r.f, r.g) - sk.semi_dual_value(gp, r.f)) <= 1e-9
+    with pytest.raises(ValueError, match="finite"):
+        sk.dual_value(gp, np.full(gp.n, np.nan), r.g)
+
+
+def test_hessian_quadform_matches_oracle_and_dense_hessian():  # test_objective.cpp:190-205
+    rng = G.SplitMix64(29)
+    cost, a, b = random_problem_data(rng, 7, 9, 1.0)
+    gp = sk.Problem(cost, a, b, 0.6)
+    op = O.Instance(a, b, 0.6, cost=cost)
+    f = random_vector(rng, 7, 0.5)
+    hess = H.full_semi_dual_hessian(gp, f)
+    assert np.max(np.abs(hess @ np.ones(7))) <= 1e-12
+    for _ in range(20):
+        u = random_vector(rng, 7)
+        direct = sk.semi_dual_hessian_quadform(gp, f, u)
+        assert abs(direct - O.semi_dual_hessian_quadform(op, f, u)) <= 1e-12 * abs(direct)
+        assert abs(u @ hess @ u - direct) <= 1e-12 * abs(direct)
+    with pytest.raises(ValueError, match="dense Hessian too large"):
+        H.full_semi_dual_hessian(gp, f, 5)
+
+
+def test_2x2_hessian_spectrum_closed_form():  # test_objective.cpp:207-223, support.hpp:87-101
+    eps = 0.7
+    cost, a, b = symmetric_2x2()
+    gp = sk.Problem(cost, a, b, eps)
+    f, g = symmetric_2x2_optimum(eps)
+    hess = H.full_semi_dual_hessian(gp, f)
+    hs = np.diag(1 / np.sqrt(a)) @ hess @ np.diag(1 / np.sqrt(a))
+    ev = np.linalg.eigvalsh(hs)
+    rho = np.tanh(1.0 / (2 * eps))
+    assert abs(ev[0] - (-(1 - rho ** 2) / eps)) <= 1e-9 * abs(ev[0])
+    assert abs(ev[1]) <= 1e-9
+    rep = sk.spectrum(gp, f, g, 1, vectors=True)
+    assert abs(rep["rho"][0] - rho) <= 1e-10
+    assert abs(rep["hessian_eigs_low"][0] - (1 - rho) / eps) <= 1e-9
+    assert abs(rep["hessian_eigs_high"][0] - (1 + rho) / eps) <= 1e-9
+    assert rep["eigenvalues_of_K"][0] == (rep["rho"][0], -rep["rho"][0])
+    # restricted Hessian in the exact eigenbasis (test_objective.cpp:181-188)
+    basis = sk.top_modes(gp, f, g, 1)
+    _, hr = sk.restricted_derivatives(gp, f, basis, g)
+    assert abs(hr[0, 0] - (-(1 - basis.rhos[0] ** 2) / eps)) <= 1e-8 * abs(hr[0, 0])
+    with pytest.raises(ValueError, match="need 1 <= k"):
+        sk.spectrum(gp, f, g, 2)
+
+
+def test_spectrum_vectors_match_oracle():  # spectral.cpp:195-228
+    gp, op, _ = dense_pair(41, 120, 90, 0.2)
+    r = O.solve(op, tol=1e-12)
+    k = 5
+    rep = sk.spectrum(gp, r["f"], r["g"], k, vectors=True)
+    ob = O.top_modes(op, r["f"], r["g"], k)
+    assert rel_err(rep["rho"], ob["rhos"]) <= 1e-8
+    assert projector_distance(np.sqrt(op.alpha)[:, None] * rep["vectors_f"], ob["vectors_sym"]) <= 1e-6
+    vs = O.apply_sym_t_block(op, r["f"], r["g"], ob["vectors_sym"])
+    vg_ref = vs / ob["rhos"][None, :] / np.sqrt(op.beta)[:, None]
+    for c in range(k):  # eigenvector signs are arbitrary
+        s = np.sign(rep["vectors_g"][:, c] @ vg_ref[:, c])
+        assert rel_err(s * rep["vectors_g"][:, c], vg_ref[:, c]) <= 1e-6
+
+
+def test_projector_distance():  # spectral.cpp:230-242
+    r = np.random.default_rng(5)
+    A = np.linalg.qr(r.standard_normal((200, 6)))[0]
+    B = np.linalg.qr(A + 1e-3 * r.standard_normal((200, 6)))[0]
+    ba = sk.SpectralBasis(A, A, np.zeros(6), 0.1)
+    bb = sk.SpectralBasis(B, B, np.zeros(6), 0.1)
+    assert abs(sk.projector_distance(ba, bb) - projector_distance(A, B)) <= 1e-12
+    assert sk.projector_distance(ba, ba) <= 1e-7
+    C = np.linalg.qr(r.standard_normal((200, 5)))[0]
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        sk.projector_distance(ba, sk.SpectralBasis(C, C, np.zeros(5), 0.1))
+
+
+def test_newton_step_and_sk_sweep_match_oracle():  # solver.cpp:12-17, :59-69
+    gp, op, r = points_pair(51, 400, 300, 2, 0.01)
+    f0 = O.solve(op, tol=1e-4)["f"]
+    V = np.asfortranarray(np.linalg.qr(r.standard_normal((400, 6)))[0])
+    out = sk.newton_step(gp, f0, sk.SpectralBasis(V, V, np.zeros(6), 0.01))
+    fo, acc, fail = O.newton_step(op, f0, V)
+    assert out.accepted == acc and out.factorization_failed == fail
+    assert rel_err(out.f, fo) <= 1e-9
+    f1, g1 = sk.sk_sweep(gp, f0)
+    g_ref = O.ctransform_of_f(op, f0)
+    assert rel_err(g1, g_ref) <= 1e-12 and rel_err(f1, O.ctransform_of_g(op, g_ref)) <= 1e-12
+    with pytest.raises(ValueError, match="empty basis"):
+        sk.newton_step(gp, f0, sk.SpectralBasis(np.zeros((400, 0)), np.zeros((400, 0)), np.zeros(0), 0.01))
+
+
+def test_coupling_rows_and_streamed_csv(tmp_path):  # core.cpp:84-112, main.cpp:149-154
+    gp, op, rng = dense_pair(61, 37, 23, 0.3)
+    r = sk.solve(gp, tol=1e-11)
+    plan = sk.coupling(gp, r.f, r.g)
+    assert rel_err(plan, O.coupling(op, r.f, r.g)) <= 1e-13
+    assert np.array_equal(sk.coupling_rows(gp, r.f, r.g, 5, 19), plan[5:19])
+    path = str(tmp_path / "coupling.csv")
+    err = sio.write_coupling_csv(path, gp, r.f, r.g, block_bytes=8 * 23 * 4)
+    back = sio.read_csv_matrix(path)
+    assert np.array_equal(back, plan)  # %.17g round-trips bitwise
+    assert abs(err - sk.marginal_error(gp, plan)) <= 1e-15
+    with pytest.raises(ValueError, match="row range"):
+        sk.coupling_rows(gp, r.f, r.g, 10, 40)
+
+
+def test_oracle_solve_ground_truth():  # oracle.cpp:21-90
+    gp, op, _ = dense_pair(71, 40, 50, 0.05)
+    sol = H.oracle_solve(gp, 1e-12)
+    assert sol.residual <= 1e-11 and sol["residual"] == sol.residual
+    ref = O.solve(op, tol=1e-13)
+    c = float(op.alpha @ ref["f"])
+    assert rel_err(sol.f, ref["f"] - c) <= 1e-9
+    assert abs(float(op.alpha @ sol.f)) <= 1e-15
+
+
+def test_cli_solve_spectrum_anneal(tmp_path, capsys):  # main.cpp:120-218
+    r = np.random.default_rng(3)
+    src = tmp_path / "src.csv"
+    tgt = tmp_path / "tgt.csv"
+    xs = r.uniform(0, 1, (60, 2))
+    yt = r.uniform(0, 1, (70, 2))
+    w = r.uniform(0.5, 1.5, 70)
+    np.savetxt(src, xs, delimiter=",", fmt="%.17g")
+    with open(tgt, "w") as fh:
+        fh.write("x,y,weight\n")
+        for p, wi in zip(yt, w):
+            fh.write(f"{p[0]!r},{p[1]!r},{wi!r}\n")
+    out = tmp_path / "solve"
+    rc = cli.main(["solve", "--points", str(src), str(tgt), "--epsilon", "0.05", "--ell", "4",
+                   "--basis-from", "0.1", "--out", str(out)])
+    text = capsys.readouterr()
+    assert rc == 0, text
+    assert "weights renormalized" in text.err
+    assert text.out.startswith("converged=true iters=")
+    for name in ("potentials.csv", "coupling.csv", "trace.csv"):
+        assert os.path.exists(out / name)
+    pots = open(out / "potentials.csv").read().splitlines()
+    assert pots[0] == "which,index,value" and len(pots) == 1 + 60 + 70
+    # same result through the library
+    gp = sk.PointProblem(xs, yt, np.full(60, 1 / 60), w / w.sum(), 0.05)
+    f_cli = np.array([float(line.split(",")[2]) for line in pots[1:61]])
+    warm = sk.solve(gp.with_epsilon(0.1))
+    basis = sk.top_modes(gp.with_epsilon(0.1), warm.f, warm.g, 4)
+    res = sk.solve(gp, ell=4, basis=basis, init=(warm.f, warm.g))
+    assert np.array_equal(f_cli, res.f)
+    rc = cli.main(["spectrum", "--synthetic", "gauss2d", "--n", "30", "--m", "40", "--epsilons", "0.5,0.25",
+                   "--k", "3", "--vectors", "--out", str(tmp_path / "spec")])
+    assert rc == 0
+    assert os.path.exists(tmp_path / "spec" / "spectrum_001.json")
+    rc = cli.main(["anneal", "--synthetic", "two_moons", "--n", "40", "--m", "40", "--schedule", "0.2,0.1,0.05",
+                   "--warm", "spectral", "--ell", "3", "--out", str(tmp_path / "ann")])
+    assert rc == 0
+    assert open(tmp_path / "ann" / "anneal_trace.csv").readline().startswith("stage,epsilon,iter,")
+    rc = cli.main(["solve", "--synthetic", "gauss2d", "--epsilon", "0.01", "--max-iter", "3",
+                   "--out", str(tmp_path / "capped")])
+    assert rc == 2
+
+
+def test_cli_zero_cost_exact_outer_product(tmp_path):  # test_cli.cpp:74-90
+    (tmp_path / "zero3x3.csv").write_text("0,0,0\n0,0,0\n0,0,0\n")
+    rc = cli.main(["solve", "--cost", str(tmp_path / "zero3x3.csv"), "--epsilon", "0.5", "--out",
+                   str(tmp_path / "out")])
+    assert rc == 0
+    plan = sio.read_csv_matrix(str(tmp_path / "out" / "coupling.csv"))
+    w = 1.0 / 3.0
+    assert np.all(plan == w * w)
+
+
+def test_cli_spectrum_round_trip_and_single_stage_anneal(tmp_path, capsys):  # test_cli.cpp:159-203
+    import json
+    rc = cli.main(["spectrum", "--synthetic", "gauss2d", "--n", "30", "--m", "40", "--epsilons", "0.5",
+                   "--k", "4", "--out", str(tmp_path / "s")])
+    assert rc == 0
+    line = capsys.readouterr().out.strip()
+    rep = json.load(open(tmp_path / "s" / "spectrum_000.json"))
+    assert len(rep["rho"]) == 4 and rep["k"] == 4
+    assert line.endswith("file=spectrum_000.json")
+    assert float(line.split("rho_1=")[1].split()[0]) == rep["rho"][0]  # bitwise through %.17g
+    rc = cli.main(["anneal", "--synthetic", "gauss2d", "--n", "30", "--m", "40", "--schedule", "0.2",
+                   "--out", str(tmp_path / "a")])
+    assert rc == 0
+    x, a, y, b = G.make_instance("gauss2d", 30, 40)
+    ref = sk.solve(sk.PointProblem(x, y, a, b, 0.2))
+    rows = open(tmp_path / "a" / "stage_00_potentials.csv").read().splitlines()[1:31]
+    assert np.array_equal([float(r.split(",")[2]) for r in rows], ref.f)
