@@ -15,6 +15,8 @@
 //    the reference always builds the n x m plan at the end of solve.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -207,10 +209,82 @@ inline PlanMarginals plan_marginals(const EotProblem& p, const Potentials& pots)
     return out;
 }
 
+inline MarginalGap marginal_gap(const EotProblem& p, const PlanMarginals& m) {  // core.cpp:145-150
+    double r2 = 0, c2 = 0, ri = 0, ci = 0;
+    for (Index i = 0; i < p.n(); ++i) {
+        const double d = m.row[i] - p.alpha().weights()[i];
+        r2 += d * d;
+        ri = std::max(ri, std::abs(d));
+    }
+    for (Index j = 0; j < p.m(); ++j) {
+        const double d = m.col[j] - p.beta().weights()[j];
+        c2 += d * d;
+        ci = std::max(ci, std::abs(d));
+    }
+    return MarginalGap{std::sqrt(r2) + std::sqrt(c2), ri + ci};
+}
+inline double marginal_error(const EotProblem& p, const Coupling& c) {  // core.cpp:105-112
+    if (c.plan.rows() != p.n() || c.plan.cols() != p.m())
+        throw std::invalid_argument("marginal_error: plan shape mismatch");
+    PlanMarginals m{Vector(p.n()), Vector(p.m())};
+    for (Index j = 0; j < p.m(); ++j) {
+        double s = 0;
+        for (Index i = 0; i < p.n(); ++i) {
+            m.row[i] += c.plan(i, j);
+            s += c.plan(i, j);
+        }
+        m.col[j] = s;
+    }
+    return marginal_gap(p, m).l2;
+}
+inline double osc_norm(const Vector& v) {  // core.cpp:114-118
+    if (v.size() == 0) throw std::invalid_argument("osc_norm: empty input");
+    double lo = v[0], hi = v[0];
+    for (Index i = 1; i < v.size(); ++i) {
+        lo = std::min(lo, v[i]);
+        hi = std::max(hi, v[i]);
+    }
+    return hi - lo;
+}
+inline Potentials gauge_normalized(const EotProblem& p, Potentials pots) {  // core.cpp:152-157
+    double c = 0;
+    for (Index i = 0; i < p.n(); ++i) c += p.alpha().weights()[i] * pots.f[i];
+    for (Index i = 0; i < p.n(); ++i) pots.f[i] -= c;
+    for (Index j = 0; j < p.m(); ++j) pots.g[j] += c;
+    return pots;
+}
+inline double gauge_distance(const EotProblem& p, const Potentials& a, const Potentials& b) {
+    const Potentials na = gauge_normalized(p, a), nb = gauge_normalized(p, b);
+    double d = 0;
+    for (Index i = 0; i < p.n(); ++i) d = std::max(d, std::abs(na.f[i] - nb.f[i]));
+    for (Index j = 0; j < p.m(); ++j) d = std::max(d, std::abs(na.g[j] - nb.g[j]));
+    return d;
+}
+
 // ---- objective.hpp
 inline double semi_dual_value(const EotProblem& p, const Vector& f) {
     double v = 0;
     detail::check(sknr_semi_dual_value(p.handle(), f.data(), &v));
+    return v;
+}
+inline double dual_value(const EotProblem& p, const Potentials& pots) {
+    if (pots.f.size() != p.n() || pots.g.size() != p.m())
+        throw std::invalid_argument("dual_value: potential sizes mismatch");
+    double v = 0;
+    detail::check(sknr_dual_value(p.handle(), pots.f.data(), pots.g.data(), &v));
+    return v;
+}
+inline Vector semi_dual_gradient(const EotProblem& p, const Vector& f) {  // objective.cpp:47-51
+    const Vector g = ctransform_of_f(p, f);
+    const PlanMarginals m = plan_marginals(p, Potentials{f, g});
+    Vector out(p.n());
+    for (Index i = 0; i < p.n(); ++i) out[i] = p.alpha().weights()[i] - m.row[i];
+    return out;
+}
+inline double semi_dual_hessian_quadform(const EotProblem& p, const Vector& f, const Vector& u) {
+    if (u.size() != p.n()) throw std::invalid_argument("semi_dual_hessian_quadform: length mismatch");
+    double v = 0;
+    detail::check(sknr_semi_dual_hessian_quadform(p.handle(), f.data(), u.data(), &v));
     return v;
 }
 struct RestrictedDerivatives {
@@ -242,7 +316,120 @@ inline SpectralBasis top_modes(const EotProblem& p, const Potentials& anchor, In
     return b;
 }
 
+// SinkhornOperator (spectral.hpp:14-42): matrix-free view of K_eps at (f, g); keeps a
+// pointer to the problem, which must outlive it (as in the reference).
+class SinkhornOperator {
+public:
+    SinkhornOperator(const EotProblem& problem, const Potentials& pots)
+        : problem_(&problem), f_(pots.f), g_(pots.g) {
+        if (f_.size() != problem.n() || g_.size() != problem.m())
+            throw std::invalid_argument("SinkhornOperator: potential sizes mismatch");
+    }
+    Index rows() const { return problem_->n(); }
+    Index cols() const { return problem_->m(); }
+    const Vector& f() const { return f_; }
+    const Vector& g() const { return g_; }
+    const EotProblem& problem() const { return *problem_; }
+    Vector apply_R(const Vector& g1) const {
+        if (g1.size() != cols()) throw std::invalid_argument("apply_R: length mismatch");
+        Vector out(rows());
+        detail::check(sknr_apply_R(problem_->handle(), f_.data(), g_.data(), g1.data(), out.data()));
+        return out;
+    }
+    Vector apply_Rt(const Vector& f1) const {
+        if (f1.size() != rows()) throw std::invalid_argument("apply_Rt: length mismatch");
+        Vector out(cols());
+        detail::check(sknr_apply_Rt(problem_->handle(), f_.data(), g_.data(), f1.data(), out.data()));
+        return out;
+    }
+    std::pair<Vector, Vector> apply_K(const Vector& f1, const Vector& g1) const {
+        return {apply_R(g1), apply_Rt(f1)};
+    }
+    Matrix apply_sym_block(const Matrix& v) const {
+        if (v.rows() != cols()) throw std::invalid_argument("apply_sym_block: row count mismatch");
+        Matrix out(rows(), v.cols());
+        detail::check(sknr_apply_sym_block(problem_->handle(), f_.data(), g_.data(), v.data(), v.cols(),
+                                           out.data()));
+        return out;
+    }
+    Matrix apply_sym_t_block(const Matrix& u) const {
+        if (u.rows() != rows()) throw std::invalid_argument("apply_sym_t_block: row count mismatch");
+        Matrix out(cols(), u.cols());
+        detail::check(sknr_apply_sym_t_block(problem_->handle(), f_.data(), g_.data(), u.data(), u.cols(),
+                                             out.data()));
+        return out;
+    }
+
+private:
+    const EotProblem* problem_;
+    Vector f_, g_;
+};
+inline SinkhornOperator build_operator(const EotProblem& p, const Potentials& pots) {
+    return SinkhornOperator(p, pots);
+}
+inline SpectralBasis top_modes(const SinkhornOperator& op, Index ell, double tol = 1e-8,
+                               Index max_power_iters = -1) {
+    return top_modes(op.problem(), Potentials{op.f(), op.g()}, ell, tol, max_power_iters);
+}
+
+struct SpectrumReport {  // spectral.hpp:79-92
+    double epsilon = 0.0;
+    Vector rhos;
+    std::vector<std::pair<double, double>> eigenvalues_of_K;
+    Vector hessian_eigs_low, hessian_eigs_high;
+    Matrix vectors_f, vectors_g;
+};
+inline SpectrumReport spectrum_report(const EotProblem& p, const Potentials& pots, Index k,
+                                      bool include_vectors = false, double tol = 1e-8,
+                                      Index max_power_iters = -1) {
+    SpectrumReport r;
+    r.epsilon = p.epsilon();
+    r.rhos = Vector(k > 0 ? k : 0);
+    r.hessian_eigs_low = Vector(k > 0 ? k : 0);
+    r.hessian_eigs_high = Vector(k > 0 ? k : 0);
+    if (include_vectors) {
+        r.vectors_f = Matrix(p.n(), k);
+        r.vectors_g = Matrix(p.m(), k);
+    }
+    detail::check(sknr_spectrum_report(p.handle(), pots.f.data(), pots.g.data(), k, include_vectors ? 1 : 0, tol,
+                                       max_power_iters, r.rhos.data(), r.hessian_eigs_low.data(),
+                                       r.hessian_eigs_high.data(), include_vectors ? r.vectors_f.data() : nullptr,
+                                       include_vectors ? r.vectors_g.data() : nullptr));
+    for (Index a = 0; a < k; ++a) r.eigenvalues_of_K.emplace_back(r.rhos[a], -r.rhos[a]);
+    return r;
+}
+inline double projector_distance(const SpectralBasis& a, const SpectralBasis& b) {
+    if (a.vectors_sym.rows() != b.vectors_sym.rows() || a.vectors_sym.cols() != b.vectors_sym.cols())
+        throw std::invalid_argument("projector_distance: dimension mismatch");
+    double d = 0;
+    detail::check(sknr_projector_distance(a.vectors_sym.rows(), a.vectors_sym.cols(), a.vectors_sym.data(),
+                                          b.vectors_sym.data(), &d));
+    return d;
+}
+
 // ---- solver.hpp
+inline Potentials sk_sweep(const EotProblem& p, const Potentials& pots) {  // solver.cpp:12-17
+    Potentials out;
+    out.g = ctransform_of_f(p, pots.f);
+    out.f = ctransform_of_g(p, out.g);
+    return out;
+}
+struct NewtonOutcome {  // solver.hpp:50-57
+    Vector f;
+    bool accepted = false;
+    bool factorization_failed = false;
+};
+inline NewtonOutcome newton_step(const EotProblem& p, const Vector& f, const SpectralBasis& basis) {
+    if (basis.ell() < 1) throw std::invalid_argument("newton_step: empty basis");
+    if (basis.dim() != p.n()) throw std::invalid_argument("restricted_derivatives: basis dimension mismatch");
+    NewtonOutcome o{Vector(p.n())};
+    int acc = 0, fail = 0;
+    detail::check(sknr_newton_step(p.handle(), f.data(), basis.vectors.data(), basis.ell(), o.f.data(), &acc, &fail));
+    o.accepted = acc != 0;
+    o.factorization_failed = fail != 0;
+    return o;
+}
+
 inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
                          const SpectralBasis* basis = nullptr, const Potentials* init = nullptr) {
     sknr_config c;

@@ -192,7 +192,7 @@ def test_cli_solve_spectrum_anneal(tmp_path, capsys):  # main.cpp:120-218
     with open(tgt, "w") as fh:
         fh.write("x,y,weight\n")
         for p, wi in zip(yt, w):
-            fh.write(f"{p[0]!r},{p[1]!r},{wi!r}\n")
+            fh.write(f"{float(p[0])!r},{float(p[1])!r},{float(wi)!r}\n")
     out = tmp_path / "solve"
     rc = cli.main(["solve", "--points", str(src), str(tgt), "--epsilon", "0.05", "--ell", "4",
                    "--basis-from", "0.1", "--out", str(out)])

@@ -303,7 +303,7 @@ def test_cpp_facade_demo_runs():
         pytest.skip("facade demo not built")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "converged=1" in out.stdout
+    assert "converged=1" in out.stdout and "rho1=" in out.stdout
 
 
 def test_sharded_code_path_single_rank_is_bitwise_identical():
