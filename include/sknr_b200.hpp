@@ -464,6 +464,49 @@ inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
     return r;
 }
 
+// Batched solve (not in the reference): independent problems advanced together on the
+// device; results equal solve() one by one (no trace). bases/inits: empty or one per problem.
+inline std::vector<SolveResult> solve_batch(const std::vector<const EotProblem*>& problems,
+                                            const SolverConfig& config,
+                                            const std::vector<const SpectralBasis*>& bases = {},
+                                            const std::vector<const Potentials*>& inits = {}) {
+    const size_t B = problems.size();
+    sknr_config c;
+    sknr_config_default(&c);
+    c.tol_omega = config.tol_omega;
+    c.max_iter = config.max_iter;
+    c.ell = config.ell;
+    c.newton_enabled = config.newton_enabled ? 1 : 0;
+    c.trace_enabled = 0;
+    std::vector<sknr_problem> h(B);
+    std::vector<const double*> bp(B, nullptr), fi(B, nullptr), gi(B, nullptr);
+    std::vector<double*> fo(B), go(B);
+    std::vector<int64_t> iters(B);
+    std::vector<int> conv(B);
+    std::vector<SolveResult> r(B);
+    for (size_t b = 0; b < B; ++b) {
+        h[b] = problems[b]->handle();
+        if (!bases.empty()) bp[b] = bases[b] ? bases[b]->vectors.data() : nullptr;
+        if (!inits.empty()) {
+            fi[b] = inits[b]->f.data();
+            gi[b] = inits[b]->g.data();
+        }
+        r[b].potentials.f = Vector(problems[b]->n());
+        r[b].potentials.g = Vector(problems[b]->m());
+        fo[b] = r[b].potentials.f.data();
+        go[b] = r[b].potentials.g.data();
+    }
+    detail::check(sknr_solve_batch(h.data(), static_cast<int64_t>(B), &c, bases.empty() ? nullptr : bp.data(),
+                                   config.ell, inits.empty() ? nullptr : fi.data(),
+                                   inits.empty() ? nullptr : gi.data(), fo.data(), go.data(), iters.data(),
+                                   conv.data()));
+    for (size_t b = 0; b < B; ++b) {
+        r[b].iterations = iters[b];
+        r[b].converged = conv[b] != 0;
+    }
+    return r;
+}
+
 inline std::vector<SolveResult> anneal(const EotProblem& p, const AnnealSchedule& schedule,
                                        const SolverConfig& config) {
     const Index S = static_cast<Index>(schedule.epsilons.size());

@@ -176,6 +176,18 @@ int sknr_solve(sknr_problem p, const sknr_config* cfg, const double* basis, int6
                int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
                int64_t* trace_len);
 
+/* Batched solve (not in the reference): `count` independent
+ * problems (any sizes / cost kinds, distinct unsharded handles) solved with the
+ * same config in one device loop -- one CUDA graph per iteration with one
+ * concurrent branch per problem. Per-problem arrays: bases[b] (n_b x ell, or
+ * bases NULL when ell = 0), init_f[b]/init_g[b] (both arrays NULL or both set),
+ * f_out[b], g_out[b]; iterations[count], converged[count]. Results equal the
+ * one-by-one sknr_solve bit for bit. No trace. */
+int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_config* cfg,
+                     const double* const* bases, int64_t basis_ell, const double* const* init_f,
+                     const double* const* init_g, double* const* f_out, double* const* g_out,
+                     int64_t* iterations, int* converged);
+
 /* newton_step (solver.cpp:59-69, try_newton :30-56): one restricted Newton step
  * from f with basis vectors (n x ell). f_out = accepted ? f + V delta : f. */
 int sknr_newton_step(sknr_problem p, const double* f, const double* vectors, int64_t ell, double* f_out,

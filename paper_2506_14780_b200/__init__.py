@@ -88,6 +88,9 @@ _SIGS = {
     "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
     "sknr_coupling": [_P, _D, _D, _D],
     "sknr_coupling_rows": [_P, _D, _D, _I64, _I64, _D],
+    "sknr_solve_batch": [ctypes.POINTER(_P), _I64, ctypes.POINTER(_Config), ctypes.POINTER(_D), _I64,
+                         ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D),
+                         ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int)],
     "sknr_apply_R": [_P, _D, _D, _D, _D],
     "sknr_apply_Rt": [_P, _D, _D, _D, _D],
     "sknr_dual_value": [_P, _D, _D, _D],
@@ -724,6 +727,59 @@ def solve(problem: Problem, tol: float = 1e-9, max_iter: int = 100000, ell: int 
                        problem)
 
 
+def solve_batch(problems: Sequence[Problem], tol: float = 1e-9, max_iter: int = 100000, ell: int = 0,
+                bases: Optional[Sequence[SpectralBasis]] = None, inits=None,
+                exact_marginals: bool = False) -> list:
+    """Solve independent problems together (one CUDA graph per iteration, one
+    concurrent branch per problem; not in the reference API). Each result equals
+    solve(problems[b], ...) bit for bit; traces are not recorded."""
+    B = len(problems)
+    if B < 1:
+        raise ValueError("solve_batch: empty batch")
+    cfg = _config(tol, max_iter, ell, False, exact_marginals=exact_marginals)
+    handles = (_P * B)(*[p.handle for p in problems])
+    keep = []
+
+    def arr(vals):
+        out = (_D * B)()
+        for b, v in enumerate(vals):
+            out[b] = _ptr(v)
+        return out
+
+    bptr = None
+    if ell > 0:
+        if bases is None or len(bases) != B:
+            raise ValueError("solve: ell > 0 requires a basis")
+        Vs = []
+        for p, bs in zip(problems, bases):
+            V = _mat_f(bs.vectors)
+            if V.shape[0] != p.n:
+                raise ValueError("solve: basis dimension mismatch")
+            if V.shape[1] != ell:
+                raise ValueError("solve: basis has wrong column count")
+            Vs.append(V)
+        keep.append(Vs)
+        bptr = arr(Vs)
+    fptr = gptr = None
+    if inits is not None:
+        fs, gs = [], []
+        for p, (f0, g0) in zip(problems, inits):
+            f0, g0 = _vec(f0), _vec(g0)
+            if f0.size != p.n or g0.size != p.m:
+                raise ValueError("solve: init potential sizes mismatch")
+            fs.append(f0)
+            gs.append(g0)
+        keep.append((fs, gs))
+        fptr, gptr = arr(fs), arr(gs)
+    fo = [np.empty(p.n) for p in problems]
+    go = [np.empty(p.m) for p in problems]
+    iters = (_I64 * B)()
+    conv = (ctypes.c_int * B)()
+    _check(lib().sknr_solve_batch(handles, B, ctypes.byref(cfg), bptr, int(ell), fptr, gptr, arr(fo), arr(go),
+                                  iters, conv))
+    return [SolveResult(fo[b], go[b], bool(conv[b]), int(iters[b]), [], problems[b]) for b in range(B)]
+
+
 def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", ell: int = 8,
            refresh_basis: bool = False, tol: float = 1e-9, max_iter: int = 100000) -> list:
     """Epsilon-annealing driver (solver.cpp:158-222)."""
@@ -836,7 +892,7 @@ __all__ = [
     "SpectralBasis", "__version__", "anneal", "apply_K", "apply_R", "apply_Rt", "apply_sym_block",
     "apply_sym_t_block", "coupling", "coupling_rows", "ctransform_of_f", "dual_value", "gauge_distance",
     "gauge_normalized", "marginal_gap", "newton_step", "projector_distance", "semi_dual_hessian_quadform",
-    "sk_sweep", "spectrum",
+    "sk_sweep", "solve_batch", "spectrum",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
     "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
     "row_partition", "shard", "semi_dual_gradient", "semi_dual_value", "solve",

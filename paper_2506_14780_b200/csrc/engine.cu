@@ -1904,6 +1904,92 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     return out;
 }
 
+// Batched solve: B independent problems advance together,
+// one CUDA graph per iteration whose B branches (one per problem stream, forked
+// from and joined to an origin stream) run concurrently on the GPU. Problems may
+// differ in size and cost kind; each keeps its own device state, so a finished
+// problem's branch turns into guarded no-op kernels until the slowest converges.
+// Every branch issues exactly the kernels of run_solve, so per-problem results
+// are bitwise identical to solving the problems one by one.
+struct BatchItem {
+    Problem* P = nullptr;
+    const double* basis = nullptr;
+    const double* init_f = nullptr;
+};
+
+static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, double tol, int64_t max_iter,
+                                             int64_t ell, bool exact_marginals) {
+    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
+    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
+    if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
+    const size_t B = items.size();
+    std::vector<SolveState> S(B);
+    for (size_t b = 0; b < B; ++b) {
+        prepare_solve(*items[b].P, S[b], ell, items[b].basis, items[b].init_f, max_iter, tol, 1);
+        CK(cudaStreamSynchronize(items[b].P->stream));
+    }
+    cudaStream_t s0 = nullptr;
+    CK(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev(B + 1, nullptr);
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<SolveOut> out(B);
+    try {
+        CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+        CK(cudaEventRecord(ev[B], s0));
+        for (size_t b = 0; b < B; ++b) {
+            Problem& P = *items[b].P;
+            CK(cudaStreamWaitEvent(P.stream, ev[B], 0));
+            enqueue_iteration(P, S[b], ell, false, 1, exact_marginals);
+            CK(cudaEventRecord(ev[b], P.stream));
+            CK(cudaStreamWaitEvent(s0, ev[b], 0));
+        }
+        CK(cudaStreamEndCapture(s0, &graph));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        int64_t batch = 1, launched = 0;
+        while (true) {
+            for (int64_t k = 0; k < batch; ++k) {
+                CK(cudaGraphLaunch(exec, s0));
+                ++launched;
+            }
+            for (size_t b = 0; b < B; ++b)
+                CK(cudaMemcpyAsync(items[b].P->st_host, items[b].P->st, sizeof(DevState), cudaMemcpyDeviceToHost,
+                                   s0));
+            CK(cudaStreamSynchronize(s0));
+            bool all = true;
+            for (size_t b = 0; b < B; ++b) all = all && items[b].P->st_host->done != 0;
+            if (all || launched >= max_iter + 2) break;
+            batch = std::min<int64_t>(batch * 2, 64);
+        }
+        for (size_t b = 0; b < B; ++b) {
+            Problem& P = *items[b].P;
+            out[b].f.resize(P.n_global);
+            out[b].g.resize(P.m);
+            download(out[b].f.data(), S[b].f.p, P.n, P.stream);
+            download(out[b].g.data(), S[b].g.p, P.m, P.stream);
+            CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
+        }
+        for (size_t b = 0; b < B; ++b) {
+            Problem& P = *items[b].P;
+            CK(cudaStreamSynchronize(P.stream));
+            out[b].iterations = P.st_host->iter;
+            out[b].converged = P.st_host->conv != 0;
+        }
+    } catch (...) {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (auto& e : ev) cudaEventDestroy(e);
+        cudaStreamDestroy(s0);
+        throw;
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(s0);
+    return out;
+}
+
 }  // namespace sknr
 
 // ============================================================ C ABI
@@ -2696,6 +2782,41 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     if (trace_len) *trace_len = len;
     if (trace)
         for (int64_t t = 0; t < len && t < trace_cap; ++t) trace[t] = o.trace[t];
+    SKNR_API_END
+}
+
+int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_config* cfg,
+                     const double* const* bases, int64_t basis_ell, const double* const* init_f,
+                     const double* const* init_g, double* const* f_out, double* const* g_out, int64_t* iterations,
+                     int* converged) {
+    SKNR_API_BEGIN
+    if (count < 1 || !problems || !cfg || !f_out || !g_out) throw InvalidArgument("solve_batch: empty batch");
+    if ((init_f == nullptr) != (init_g == nullptr)) throw InvalidArgument("solve: init potential sizes mismatch");
+    std::vector<BatchItem> items(static_cast<size_t>(count));
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (int64_t b = 0; b < count; ++b) {
+        Problem& P = get(problems[b]);
+        for (int64_t c = 0; c < b; ++c)
+            if (problems[c] == problems[b]) throw InvalidArgument("solve_batch: duplicate problem handle");
+        if (P.shard) throw InvalidArgument("solve_batch: row-sharded problems are not supported");
+        validate_config(cfg, bases ? bases[b] : nullptr, basis_ell, P.n);
+        if (init_f && ((init_f[b] == nullptr) != (init_g[b] == nullptr)))
+            throw InvalidArgument("solve: init potential sizes mismatch");
+        if (!f_out[b] || !g_out[b]) throw InvalidArgument("solve_batch: null output");
+        items[b].P = &P;
+        items[b].basis = bases ? bases[b] : nullptr;
+        items[b].init_f = init_f ? init_f[b] : nullptr;
+        locks.emplace_back(P.mu);
+    }
+    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
+    std::vector<SolveOut> o = run_solve_batch(items, cfg->tol_omega, cfg->max_iter, use_newton ? cfg->ell : 0,
+                                              cfg->exact_marginals != 0);
+    for (int64_t b = 0; b < count; ++b) {
+        std::memcpy(f_out[b], o[b].f.data(), sizeof(double) * items[b].P->n_global);
+        std::memcpy(g_out[b], o[b].g.data(), sizeof(double) * items[b].P->m);
+        if (iterations) iterations[b] = o[b].iterations;
+        if (converged) converged[b] = o[b].converged ? 1 : 0;
+    }
     SKNR_API_END
 }
 

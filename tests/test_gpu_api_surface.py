@@ -251,3 +251,27 @@ def test_cli_spectrum_round_trip_and_single_stage_anneal(tmp_path, capsys):  # t
     ref = sk.solve(sk.PointProblem(x, y, a, b, 0.2))
     rows = open(tmp_path / "a" / "stage_00_potentials.csv").read().splitlines()[1:31]
     assert np.array_equal([float(r.split(",")[2]) for r in rows], ref.f)
+
+
+def test_solve_batch_is_bitwise_identical_to_single_solves():
+    probs, bases, inits = [], [], []
+    for s in range(6):
+        if s % 3 == 2:
+            gp, _, _ = dense_pair(100 + s, 90 + 7 * s, 70 + 5 * s, 0.05)
+        else:
+            gp, _, _ = points_pair(100 + s, 200 + 31 * s, 150 + 17 * s, 1 + s % 4, 0.02)
+        probs.append(gp)
+        warm = sk.solve(gp.with_epsilon(0.04))
+        bases.append(sk.top_modes(gp.with_epsilon(0.04), warm.f, warm.g, 5))
+        inits.append((warm.f, warm.g))
+    for ell in (0, 5):
+        kw = dict(tol=1e-10, ell=ell, bases=bases if ell else None, inits=inits)
+        res = sk.solve_batch(probs, **kw)
+        for p, r, b, i in zip(probs, res, bases, inits):
+            one = sk.solve(p, tol=1e-10, ell=ell, basis=b if ell else None, init=i)
+            assert r.converged and r.iterations == one.iterations
+            assert np.array_equal(r.f, one.f) and np.array_equal(r.g, one.g)
+    with pytest.raises(ValueError, match="duplicate problem handle"):
+        sk.solve_batch([probs[0], probs[0]])
+    with pytest.raises(ValueError, match="requires a basis"):
+        sk.solve_batch(probs, ell=5)
