@@ -620,6 +620,8 @@ struct Side {
     DBuf w, lw, sw, lsw, coords, sq;
 };
 
+struct SolveState;
+
 struct Problem {
     int kind = 0;  // 0 dense, 1 points
     int64_t n = 0, m = 0, d = 0;
@@ -634,6 +636,7 @@ struct Problem {
     // per-direction LSE state
     DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
     DBuf partial, rsum;
+    std::shared_ptr<SolveState> solve_cache;  // per-solve device buffers, reused across solves
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -1863,7 +1866,8 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
     const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, std::max<int64_t>(trace_cap_hint, 1)) : 1;
-    SolveState S;
+    if (!P.solve_cache) P.solve_cache = std::make_shared<SolveState>();
+    SolveState& S = *P.solve_cache;
     prepare_solve(P, S, ell, basis, init_f, max_iter, tol, trace_cap);
     cudaStream_t s = P.stream;
     cudaGraph_t graph = nullptr;
@@ -1923,9 +1927,15 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
     const size_t B = items.size();
-    std::vector<SolveState> S(B);
+    std::vector<SolveState*> Sp(B);
     for (size_t b = 0; b < B; ++b) {
-        prepare_solve(*items[b].P, S[b], ell, items[b].basis, items[b].init_f, max_iter, tol, 1);
+        Problem& P = *items[b].P;
+        if (!P.solve_cache) P.solve_cache = std::make_shared<SolveState>();
+        Sp[b] = P.solve_cache.get();
+    }
+    auto S = [&](size_t b) -> SolveState& { return *Sp[b]; };
+    for (size_t b = 0; b < B; ++b) {
+        prepare_solve(*items[b].P, S(b), ell, items[b].basis, items[b].init_f, max_iter, tol, 1);
         CK(cudaStreamSynchronize(items[b].P->stream));
     }
     cudaStream_t s0 = nullptr;
@@ -1941,7 +1951,7 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
         for (size_t b = 0; b < B; ++b) {
             Problem& P = *items[b].P;
             CK(cudaStreamWaitEvent(P.stream, ev[B], 0));
-            enqueue_iteration(P, S[b], ell, false, 1, exact_marginals);
+            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals);
             CK(cudaEventRecord(ev[b], P.stream));
             CK(cudaStreamWaitEvent(s0, ev[b], 0));
         }
@@ -1966,8 +1976,8 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
             Problem& P = *items[b].P;
             out[b].f.resize(P.n_global);
             out[b].g.resize(P.m);
-            download(out[b].f.data(), S[b].f.p, P.n, P.stream);
-            download(out[b].g.data(), S[b].g.p, P.m, P.stream);
+            download(out[b].f.data(), S(b).f.p, P.n, P.stream);
+            download(out[b].g.data(), S(b).g.p, P.m, P.stream);
             CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
         }
         for (size_t b = 0; b < B; ++b) {
