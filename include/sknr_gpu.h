@@ -82,6 +82,13 @@ int sknr_problem_set_epsilon(sknr_problem p, double epsilon);
 int sknr_problem_info(sknr_problem p, int64_t* n, int64_t* m, int64_t* d, double* epsilon,
                       int* kind /* 0 stored cost, 1 on the fly (registers), 2 on the fly (DMMA) */);
 int sknr_problem_destroy(sknr_problem p);
+/* Opt-in culling of negligible terms in the column/row LSE passes (not in the
+ * reference): both clouds are visited in Morton order and a (64-input group,
+ * 256-output group) pair is skipped when a rigorous bound puts every one of its
+ * terms below e^-threshold of the output's total (threshold >= 40, typically 60;
+ * 0 turns culling off). Point clouds with d <= 4, unsharded. The sums change by
+ * less than n e^-threshold relative (< 1e-21 at 60). */
+int sknr_problem_set_culling(sknr_problem p, double threshold);
 
 /* ---------------------------------------------------------------- core.hpp
  * core.hpp:16-43 / core.cpp:35-150 on host buffers (upload, device kernels,

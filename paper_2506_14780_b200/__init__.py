@@ -83,6 +83,7 @@ _SIGS = {
     "sknr_problem_info": [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                           _D, ctypes.POINTER(ctypes.c_int)],
     "sknr_problem_destroy": [_P],
+    "sknr_problem_set_culling": [_P, ctypes.c_double],
     "sknr_ctransform_of_f": [_P, _D, _D],
     "sknr_ctransform_of_g": [_P, _D, _D],
     "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
@@ -248,7 +249,10 @@ class Problem:
     @classmethod
     def _clone(cls, p: "Problem", eps: float):
         if isinstance(p, PointProblem):
-            return PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale, p._cost_mode)
+            q = PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale, p._cost_mode)
+            if getattr(p, "_cull", 0.0) > 0.0:
+                q.set_culling(p._cull)
+            return q
         return Problem(p._cost, p._alpha, p._beta, eps)
 
     def set_epsilon(self, epsilon: float) -> None:
@@ -301,6 +305,12 @@ class PointProblem(Problem):
         self._init_common(h, n, m, a, b, float(epsilon))
         self._x, self._y, self._cost_scale = x, y, float(cost_scale)
         self._cost_mode = cost_mode
+
+    def set_culling(self, threshold: float = 60.0) -> None:
+        """Opt-in: skip LSE terms provably below e^-threshold of their output's total
+        (Morton-ordered group bounds; 0 disables). Not in the reference API."""
+        _check(lib().sknr_problem_set_culling(self.handle, float(threshold)))
+        self._cull = float(threshold)
 
     @property
     def cost(self) -> np.ndarray:

@@ -117,6 +117,42 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
     }
 }
 
+// ------------------------------------------------------------------ culling bounds
+__global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk, const double* sq, double lskc,
+                                                      const int* perm, int64_t count, int gs, int gb,
+                                                      double* out_small, double* out_big, const DevState* st,
+                                                      unsigned guard, unsigned* zero_counter) {
+    if (guard_skip(st, guard)) return;
+    if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
+    __shared__ double vals[2048];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * gb;
+    for (int t = threadIdx.x; t < gb; t += blockDim.x) {
+        const int64_t p = base + t;
+        double v = -kInf;
+        if (p < count) {
+            const int64_t i = perm[p];
+            v = pack[i * pk] + lskc * sq[i];
+        }
+        vals[t] = v;
+    }
+    __syncthreads();
+    const int nsmall = gb / gs;
+    __shared__ double smax[64];
+    for (int g = threadIdx.x; g < nsmall; g += blockDim.x) {
+        double m = -kInf;
+        for (int t = 0; t < gs; ++t) m = fmax(m, vals[g * gs + t]);
+        smax[g] = m;
+        const int64_t gidx = base / gs + g;
+        if (gidx * gs < count) out_small[gidx] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = -kInf;
+        for (int g = 0; g < nsmall; ++g) m = fmax(m, smax[g]);
+        out_big[blockIdx.x] = m;
+    }
+}
+
 // ------------------------------------------------------------------ finalize
 // Exact shift: shift_o += max_u / L64, B_o recomputed from it.
 __global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {

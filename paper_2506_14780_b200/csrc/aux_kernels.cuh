@@ -71,6 +71,13 @@ struct FinalizeArgs {
     unsigned guard = 0;
 };
 
+// Culling bounds (MODE_SUM_CULL): over permuted positions, the maximum of
+// pack[i*pk] + lskc*sq[i] (i = perm[p]) per group of gs and per group of gb
+// (gb a multiple of gs, <= 2048). One block per big group.
+__global__ void k_group_max(const double* pack, int pk, const double* sq, double lskc, const int* perm,
+                            int64_t count, int gs, int gb, double* out_small, double* out_big, const DevState* st,
+                            unsigned guard, unsigned* zero_counter);
+
 __global__ void k_max_finalize(FinalizeArgs a);
 __global__ void k_lse_finalize(FinalizeArgs a);
 __global__ void k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n, double* out, const DevState* st,

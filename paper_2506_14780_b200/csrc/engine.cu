@@ -165,6 +165,25 @@ struct DBuf {
     }
 };
 
+struct IBuf {  // int32 device buffer (permutations)
+    int* p = nullptr;
+    size_t n = 0;
+    IBuf() = default;
+    IBuf(const IBuf&) = delete;
+    IBuf& operator=(const IBuf&) = delete;
+    ~IBuf() {
+        if (p) cudaFree(p);
+    }
+    void assign(const std::vector<int>& h) {
+        if (p) CK(cudaFree(p));
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, std::max<size_t>(h.size(), 1) * sizeof(int)));
+        CK(cudaMemcpy(p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+        n = h.size();
+    }
+};
+
 // ============================================================ small kernels
 __global__ void k_fill(double* x, int64_t n, double v) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -618,6 +637,10 @@ __global__ void k_transpose(const double* A, int64_t n, int64_t m, double* AT) {
 struct Side {
     int64_t count = 0;
     DBuf w, lw, sw, lsw, coords, sq;
+    // culling (opt-in): Morton order and bounding boxes of groups of 64 / 256 / 2048
+    // consecutive permuted points, [group][2d] = lo..., hi...
+    IBuf perm;
+    DBuf box64, box256, box2048;
 };
 
 struct SolveState;
@@ -637,6 +660,10 @@ struct Problem {
     DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
     DBuf partial, rsum;
     std::shared_ptr<SolveState> solve_cache;  // per-solve device buffers, reused across solves
+    // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
+    double cull_t = 0.0;
+    bool cull_ready = false;
+    DBuf f_gi[2], f_gc[2], s_go[2], s_gt[2];
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -897,6 +924,44 @@ static TileArgs tile_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     return a;
 }
 
+// Culled column/row LSE (opt-in): register point kernels, unsharded, large enough
+// for whole cull tiles.
+static bool cull_active(const Problem& P, int dir) {
+    if (!(P.cull_t > 0.0) || !P.cull_ready || P.shard || P.dim < 1 || P.dim > 4) return false;
+    const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
+    return nout >= CULL_GT && nin >= CULL_GC;
+}
+
+static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guard, int retry_phase) {
+    TileArgs a = tile_args(P, dir, tp, guard);
+    Side& in = P.in_side(dir);
+    Side& out = P.out_side(dir);
+    a.perm_in = in.perm.p;
+    a.perm_out = out.perm.p;
+    a.box_gi = in.box64.p;
+    a.box_gc = in.box256.p;
+    a.box_go = out.box256.p;
+    a.box_gt = out.box2048.p;
+    a.f_gi = P.f_gi[dir].p;
+    a.f_gc = P.f_gc[dir].p;
+    a.s_go = P.s_go[dir].p;
+    a.s_gt = P.s_gt[dir].p;
+    a.lskc = kLS * P.kc();
+    a.cull_t = P.cull_t;
+    a.inv_eps = P.inv_eps();
+    a.dir = dir;
+    a.retry_phase = retry_phase;
+    return a;
+}
+
+static void cull_group_max(Problem& P, const Side& side, const double* pack, double* small, double* big, int gs,
+                           int gb, unsigned guard, unsigned* zero_counter = nullptr) {
+    count_launch();
+    k_group_max<<<static_cast<int>((side.count + gb - 1) / gb), AUX_NT, 0, P.stream>>>(
+        pack, P.pk(), side.sq.p, kLS * P.kc(), side.perm.p, side.count, gs, gb, small, big, P.st, guard,
+        zero_counter);
+}
+
 static unsigned exact_bit(int dir) { return dir == 0 ? G_EXACT0 : G_EXACT1; }
 static unsigned retry_bit(int dir) { return dir == 0 ? G_RETRY0 : G_RETRY1; }
 
@@ -909,7 +974,8 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     const int64_t nin = in.count, nout = out.count;
     cudaStream_t s = P.stream;
     const TilePlan tmax = plan_for(P, dir, MODE_MAX, 0);
-    const TilePlan tsum = plan_for(P, dir, MODE_SUM, 0);
+    const bool cull = cull_active(P, dir);
+    const TilePlan tsum = plan_for(P, dir, cull ? MODE_SUM_CULL : MODE_SUM, 0);
 
     PrepInArgs pi;
     pi.count = nin;
@@ -957,6 +1023,8 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     po.guard = guard;
     count_launch();
     k_prep_out<<<grid_for(nout), AUX_NT, 0, s>>>(po);
+    if (cull)  // input-group maxima of F (the inputs do not change between phases)
+        cull_group_max(P, in, P.pack_in[dir].p, P.f_gi[dir].p, P.f_gc[dir].p, CULL_GI, CULL_GC, guard);
 
     FinalizeArgs fa;
     fa.partial = P.partial.p;
@@ -989,7 +1057,15 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         }
         count_launch();
         k_max_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
-        launch_tiles(tsum, tile_args(P, dir, tsum, gsum), s);
+        if (cull) {  // output-group maxima of S with this phase's shift
+            unsigned* sched = &P.st->counters[10 + dir];
+            cull_group_max(P, out, P.pack_out[dir].p, P.s_go[dir].p, P.s_gt[dir].p, CULL_GO, CULL_GT, gsum, sched);
+            TileArgs ca = cull_args(P, dir, tsum, gsum, phase);
+            ca.sched = sched;
+            launch_tiles(tsum, ca, s);
+        } else {
+            launch_tiles(tsum, tile_args(P, dir, tsum, gsum), s);
+        }
         fa.partial = P.partial.p;
         fa.nb = tsum.n_in_blocks;
         fa.guard = gsum;
@@ -1840,6 +1916,8 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
     plan_for(P, 1, MODE_SUM, 0);
     plan_for(P, 0, MODE_MAX, 0);
     plan_for(P, 1, MODE_MAX, 0);
+    for (int dir = 0; dir < 2; ++dir)
+        if (cull_active(P, dir)) plan_for(P, dir, MODE_SUM_CULL, 0);
     if (init_f)
         upload_rows(P, S.f.p, init_f);
     else {
@@ -2145,6 +2223,106 @@ int sknr_problem_info(sknr_problem h, int64_t* n, int64_t* m, int64_t* d, double
     if (d) *d = P.d;
     if (epsilon) *epsilon = P.eps;
     if (kind) *kind = P.dim > 0 ? 1 : (P.dim < 0 ? 2 : 0);
+    SKNR_API_END
+}
+
+// Morton order of a point set (centred coordinates, col-major count x d) in the
+// bounding box of both clouds; ties keep index order.
+static std::vector<int> morton_perm(const std::vector<double>& c, int64_t count, int d, const double* lo,
+                                    const double* hi) {
+    const int bits = std::min(21, 63 / d);
+    const double scale = static_cast<double>((1ull << bits) - 1);
+    std::vector<std::pair<uint64_t, int>> key(static_cast<size_t>(count));
+    for (int64_t i = 0; i < count; ++i) {
+        uint64_t q[4] = {0, 0, 0, 0};
+        for (int k = 0; k < d; ++k) {
+            const double span = hi[k] > lo[k] ? hi[k] - lo[k] : 1.0;
+            double v = (c[i + k * count] - lo[k]) / span * scale;
+            v = std::min(std::max(v, 0.0), scale);
+            q[k] = static_cast<uint64_t>(v);
+        }
+        uint64_t code = 0;
+        for (int b = bits - 1; b >= 0; --b)
+            for (int k = 0; k < d; ++k) code = (code << 1) | ((q[k] >> b) & 1ull);
+        key[static_cast<size_t>(i)] = {code, static_cast<int>(i)};
+    }
+    std::sort(key.begin(), key.end());
+    std::vector<int> perm(static_cast<size_t>(count));
+    for (int64_t i = 0; i < count; ++i) perm[static_cast<size_t>(i)] = key[static_cast<size_t>(i)].second;
+    return perm;
+}
+
+static void group_boxes(const std::vector<double>& c, int64_t count, int d, const std::vector<int>& perm, int g,
+                        DBuf& out) {
+    const int64_t ng = (count + g - 1) / g;
+    std::vector<double> box(static_cast<size_t>(ng) * 2 * d);
+    for (int64_t q = 0; q < ng; ++q)
+        for (int k = 0; k < d; ++k) {
+            double lo = std::numeric_limits<double>::infinity(), hi = -lo;
+            for (int64_t p = q * g; p < std::min(count, (q + 1) * g); ++p) {
+                const double v = c[perm[static_cast<size_t>(p)] + k * count];
+                lo = std::min(lo, v);
+                hi = std::max(hi, v);
+            }
+            box[q * 2 * d + k] = lo;
+            box[q * 2 * d + d + k] = hi;
+        }
+    out.ensure(box.size());
+    CK(cudaMemcpy(out.p, box.data(), box.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+static void prepare_culling(Problem& P) {
+    if (P.cull_ready) return;
+    const int d = static_cast<int>(P.d);
+    std::vector<double> xc(static_cast<size_t>(P.n * d)), yc(static_cast<size_t>(P.m * d));
+    CK(cudaMemcpy(xc.data(), P.src.coords.p, xc.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(yc.data(), P.tgt.coords.p, yc.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    double lo[4], hi[4];
+    for (int k = 0; k < d; ++k) {
+        lo[k] = std::numeric_limits<double>::infinity();
+        hi[k] = -lo[k];
+        for (int64_t i = 0; i < P.n; ++i) {
+            lo[k] = std::min(lo[k], xc[i + k * P.n]);
+            hi[k] = std::max(hi[k], xc[i + k * P.n]);
+        }
+        for (int64_t j = 0; j < P.m; ++j) {
+            lo[k] = std::min(lo[k], yc[j + k * P.m]);
+            hi[k] = std::max(hi[k], yc[j + k * P.m]);
+        }
+    }
+    const std::vector<int> px = morton_perm(xc, P.n, d, lo, hi), py = morton_perm(yc, P.m, d, lo, hi);
+    P.src.perm.assign(px);
+    P.tgt.perm.assign(py);
+    group_boxes(xc, P.n, d, px, 64, P.src.box64);
+    group_boxes(xc, P.n, d, px, 256, P.src.box256);
+    group_boxes(xc, P.n, d, px, 2048, P.src.box2048);
+    group_boxes(yc, P.m, d, py, 64, P.tgt.box64);
+    group_boxes(yc, P.m, d, py, 256, P.tgt.box256);
+    group_boxes(yc, P.m, d, py, 2048, P.tgt.box2048);
+    for (int dir = 0; dir < 2; ++dir) {
+        const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
+        P.f_gi[dir].ensure((nin + CULL_GI - 1) / CULL_GI);
+        P.f_gc[dir].ensure((nin + CULL_GC - 1) / CULL_GC);
+        P.s_go[dir].ensure((nout + CULL_GO - 1) / CULL_GO);
+        P.s_gt[dir].ensure((nout + CULL_GT - 1) / CULL_GT);
+    }
+    P.cull_ready = true;
+}
+
+int sknr_problem_set_culling(sknr_problem h, double threshold) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (!(threshold >= 0.0) || !std::isfinite(threshold))
+        throw InvalidArgument("set_culling: threshold must be finite and >= 0");
+    if (threshold > 0.0) {
+        if (threshold < 40.0) throw InvalidArgument("set_culling: threshold below 40 would perturb the sums");
+        if (P.dim < 1 || P.dim > 4)
+            throw InvalidArgument("set_culling: needs a point-cloud problem with d <= 4");
+        if (P.shard) throw InvalidArgument("set_culling: not available on a row-sharded problem");
+        prepare_culling(P);
+    }
+    P.cull_t = threshold;
     SKNR_API_END
 }
 

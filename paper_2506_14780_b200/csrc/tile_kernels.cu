@@ -161,6 +161,111 @@ __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
     }
 }
 
+// ------------------------------------------------------------- culled sum pass (opt-in)
+// Both point clouds are visited in Morton order (perm_in / perm_out), so a warp's
+// 256 outputs and a 64-input group each cover a small box. For every term
+//   u_io = F_i + S_o - LS kc |x_i - y_o|^2 <= max_I F + max_O S - LS kc dist2(box_I, box_O) =: U,
+// and the output's LSE satisfies L_o >= s_o - slack (slack = 0 after an exact max
+// pass, (max df - min df)/eps for the bound shift). A group pair with
+// U < -LS (T + slack) therefore only holds terms below e^-T of the output's total
+// (n e^-60 < 1e-21 relative for T = 60): it is skipped. The test runs per CTA for
+// a 256-input chunk (skipping the shared-memory staging too) and per warp for each
+// 64-input group. Kept terms are accumulated exactly as in pts_tile_kernel.
+template <int D>
+__device__ __forceinline__ double box_dist2(const double* __restrict__ a, const double* __restrict__ b) {
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const double g = fmax(fmax(a[d] - b[D + d], b[d] - a[D + d]), 0.0);
+        s = fma(g, g, s);
+    }
+    return s;
+}
+
+template <int D, int JT, int NTT>
+__global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int PK = PK_of<D>::value;
+    static_assert(32 * JT == CULL_GO, "one warp owns one output group");
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* sin = sm + kTabWords + warp * CULL_GI * PK;  // warp-private input staging
+    load_exp2_table(tab, tid, NTT);
+    __syncthreads();
+    const unsigned laneoff = (tid & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+    const bool exact = a.retry_phase || a.st->need_exact[a.dir];
+    const double slack = exact ? 0.0 : (a.st->dmax[a.dir] - a.st->dmin[a.dir]) * a.inv_eps;
+    const double thr = -kLS * (a.cull_t + slack);
+
+    // Work unit = (256-output group, input block), taken from a global queue by each
+    // warp independently: culled units cost only their bound tests, and no warp
+    // waits on another (the CTA only shares the exp2 table).
+    while (true) {
+        unsigned unit = 0;
+        if (lane == 0) unit = atomicAdd(a.sched, 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= a.n_tiles) break;
+        const int64_t og = unit % a.n_out_tiles, ib = unit / a.n_out_tiles;
+        const int64_t wpos = og * CULL_GO;
+        double B[JT], Y[JT][D], acc[JT];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            const int64_t pos = wpos + jt * 32 + lane;
+            const int64_t oc = a.perm_out[pos < a.n_out ? pos : a.n_out - 1];
+            B[jt] = a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Y[jt][d] = a.out_pack[oc * PK + 1 + d];
+            acc[jt] = 0.0;
+        }
+        double wbox[2 * D];
+#pragma unroll
+        for (int q = 0; q < 2 * D; ++q) wbox[q] = a.box_go[og * 2 * D + q];
+        const double s_w = a.s_go[og];
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+#pragma unroll 1
+        for (int64_t g0 = i0; g0 < i1; g0 += CULL_GI) {
+            const int64_t gi = g0 / CULL_GI;
+            const double uw = a.f_gi[gi] + s_w - a.lskc * box_dist2<D>(a.box_gi + gi * 2 * D, wbox);
+            if (uw < thr) continue;  // warp-uniform
+            const int cnt = static_cast<int>((i1 - g0) < CULL_GI ? (i1 - g0) : CULL_GI);
+            __syncwarp();
+            for (int t = lane; t < cnt; t += 32) {
+                const double2* src = reinterpret_cast<const double2*>(a.in_pack +
+                                                                      static_cast<int64_t>(a.perm_in[g0 + t]) * PK);
+                double2* dst = reinterpret_cast<double2*>(sin + t * PK);
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) dst[q] = src[q];
+            }
+            __syncwarp();
+#pragma unroll 1
+            for (int k = 0; k < cnt; ++k) {
+                double x[PK];
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(sin + k * PK)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    double u = x[0] + B[jt];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
+                    acc[jt] = pexp_acc<false, false>(u, tab, laneoff, c3, acc[jt]);
+                }
+            }
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            const int64_t pos = wpos + jt * 32 + lane;
+            if (pos < a.n_out) a.partial[ib * a.n_out + a.perm_out[pos]] = acc[jt];
+        }
+    }
+}
+
 // ------------------------------------------------------------- block pass on FP64 tensor cores
 // out[o][c] += sum_in e(o,in) W[in][c] as a GEMM: A = e (generated in registers,
 // one cell per lane: row o = lane>>2, col in = lane&3), B = W (smem), C in
@@ -748,6 +853,17 @@ KernelInfo make_pts() {
     return k;
 }
 
+template <int D>
+KernelInfo make_cull() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_cull_kernel<D, 8, 256>);
+    k.jt = 8;
+    k.nt = 256;
+    k.out_tile = CULL_GO;  // work units are per warp
+    k.smem = static_cast<int>(sizeof(double)) * (kTabWords + 8 * CULL_GI * PK_of<D>::value);
+    return k;
+}
+
 template <int JT, int MODE, int KT>
 KernelInfo make_dense() {
     KernelInfo k;
@@ -787,7 +903,7 @@ KernelInfo make_contract() {
 
 template <int DK>
 KernelInfo pick_contract(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS) return KernelInfo{};  // not fused for the contraction kernels
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL) return KernelInfo{};  // register kernels only
     if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
     if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
     switch (kt) {
@@ -807,6 +923,7 @@ KernelInfo pick_pts(int mode, int kt) {
     // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
+    if (mode == MODE_SUM_CULL) return make_cull<D>();
     if (mode == MODE_BLOCK_RS) {  // 32-input rounds: 4 CTAs/SM fit (C4 ell=32: 13.9 ms vs 14.1 ms at 64)
         switch (kt) {
             case 8: return make_mma<D, 8, 4, true, 32>();
@@ -853,7 +970,7 @@ KernelInfo make_dense_mma() {
 }
 
 KernelInfo pick_dense(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS) return KernelInfo{};  // not fused for stored costs
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL) return KernelInfo{};  // point clouds only
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
     switch (kt) {  // FP64 tensor-core (DMMA) block pass
@@ -966,7 +1083,7 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     // Small problems (e.g. C1 512^2, C2 4096^2): the 2048-output tiles of the
     // register kernels leave most SMs idle; use 128-output tiles instead.
     const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS;
-    if (variant < 0 && dim > 0 && !blk && n_out * n_in <= (int64_t(1) << 26)) {
+    if (variant < 0 && dim > 0 && !blk && mode != MODE_SUM_CULL && n_out * n_in <= (int64_t(1) << 26)) {
         switch (dim) {
             case 1: ki = mode == MODE_SUM ? make_pts<1, 1, MODE_SUM, 0, 128, 2>() : make_pts<1, 1, MODE_MAX, 0, 128, 2>(); break;
             case 2: ki = mode == MODE_SUM ? make_pts<2, 1, MODE_SUM, 0, 128, 2>() : make_pts<2, 1, MODE_MAX, 0, 128, 2>(); break;
@@ -990,10 +1107,12 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     // input-block granularity (the kernels stage up to their chunk size per round)
-    const int ch = blk ? chunk_inputs(MODE_BLOCK, kt) : 32;
+    const int ch = blk ? chunk_inputs(MODE_BLOCK, kt) : (mode == MODE_SUM_CULL ? CULL_GI : 32);
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
-    // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small.
-    int64_t want = (8 * resident + p.n_out_tiles - 1) / p.n_out_tiles;
+    // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small
+    // (culled pass: >= 8 work units per resident warp, taken from a queue).
+    const int64_t units = mode == MODE_SUM_CULL ? 8 * resident * (ki.nt / 32) : 8 * resident;
+    int64_t want = (units + p.n_out_tiles - 1) / p.n_out_tiles;
     if (want < 1) want = 1;
     if (want > max_blocks_by_chunk) want = max_blocks_by_chunk;
     if (max_in_blocks > 0 && want > max_in_blocks) want = max_in_blocks;

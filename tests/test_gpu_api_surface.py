@@ -275,3 +275,45 @@ def test_solve_batch_is_bitwise_identical_to_single_solves():
         sk.solve_batch([probs[0], probs[0]])
     with pytest.raises(ValueError, match="requires a basis"):
         sk.solve_batch(probs, ell=5)
+
+
+@pytest.mark.parametrize("d,n,m", [(1, 5000, 9000), (2, 9000, 5000), (3, 4100, 6000), (4, 2100, 4500)])
+def test_culled_transforms_match_oracle(d, n, m):
+    """Opt-in culling (sknr_problem_set_culling): Morton-ordered group bounds skip terms
+    below e^-60 of each output's total; ragged sizes exercise partial groups."""
+    r = np.random.default_rng(d * 31 + n)
+    x = np.asfortranarray(r.uniform(0, 1, (n, d)))
+    y = np.asfortranarray(r.uniform(0, 1, (m, d)))
+    a = np.full(n, 1.0 / n)
+    b = np.full(m, 1.0 / m)
+    eps = 2e-3
+    gp = sk.PointProblem(x, y, a, b, eps)
+    gp.set_culling(60.0)
+    op = O.Instance(a, b, eps, x=x, y=y)
+    f = 0.01 * r.standard_normal(n)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(sk.ctransform_of_f(gp, f), g_ref) <= 1e-12
+    assert rel_err(sk.ctransform_of_g(gp, g_ref), O.ctransform_of_g(op, g_ref)) <= 1e-12
+    # solver path (bound shift + culling) against the dense path
+    gd = sk.PointProblem(x, y, a, b, eps)
+    rc = sk.solve(gp, tol=1e-9, max_iter=400, trace=False)
+    rd = sk.solve(gd, tol=1e-9, max_iter=400, trace=False)
+    assert rc.iterations == rd.iterations and rc.converged == rd.converged
+    assert rel_err(rc.f, rd.f) <= 1e-12 and rel_err(rc.g, rd.g) <= 1e-12
+
+
+def test_culling_errors_and_off_switch():
+    gp, _, _ = dense_pair(5, 40, 30, 0.1)
+    with pytest.raises(ValueError, match="point-cloud problem"):
+        lib_set = sk.lib().sknr_problem_set_culling
+        sk._check(lib_set(gp.handle, 60.0))
+    pp, _, _ = points_pair(6, 3000, 2500, 2, 0.01)
+    with pytest.raises(ValueError, match="threshold below 40"):
+        pp.set_culling(10.0)
+    f = np.zeros(3000)
+    g0 = sk.ctransform_of_f(pp, f)
+    pp.set_culling(60.0)
+    g1 = sk.ctransform_of_f(pp, f)
+    pp.set_culling(0.0)
+    assert np.array_equal(sk.ctransform_of_f(pp, f), g0)
+    assert rel_err(g1, g0) <= 1e-13
