@@ -233,8 +233,9 @@ int sknr_bench_fp64_peak(double* tflops, double* ms);
  * kernel on this problem (tools/tune_lse.py). */
 int sknr_tune_variant(sknr_problem p, int variant, int passes, double* kernel_ms);
 /* Diagnostics: out[0..3] = exact-shift passes (column, row), bound-shift
- * validation failures that triggered the exact retry (column, row). */
-int sknr_debug_counters(sknr_problem p, int64_t* out);
+ * validation failures that triggered the exact retry (column, row); out[4..5] =
+ * culling group tests and kept groups (sknr_problem_set_culling). */
+int sknr_debug_counters(sknr_problem p, int64_t* out /* 6 */);
 
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU. Rank 0 calls sknr_comm_unique_id, the id travels over

@@ -879,9 +879,10 @@ def shard(problem: Problem, rank: int, world: int) -> None:
 
 
 def debug_counters(problem: Problem) -> dict:
-    out = (_I64 * 4)()
+    out = (_I64 * 6)()
     _check(lib().sknr_debug_counters(problem.handle, out))
-    return {"exact_col": out[0], "exact_row": out[1], "retry_col": out[2], "retry_row": out[3]}
+    return {"exact_col": out[0], "exact_row": out[1], "retry_col": out[2], "retry_row": out[3],
+            "cull_tested": out[4], "cull_kept": out[5]}
 
 
 def tune_variant(problem: Problem, variant: int, passes: int = 5) -> float:

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
 __global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk, const double* sq, double lskc,
                                                       const int* perm, int64_t count, int gs, int gb,
                                                       double* out_small, double* out_big, const DevState* st,
-                                                      unsigned guard, unsigned* zero_counter) {
+                                                      unsigned guard, unsigned* zero_counter, const double* sub) {
     if (guard_skip(st, guard)) return;
     if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
     __shared__ double vals[2048];
@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk
         if (p < count) {
             const int64_t i = perm[p];
             v = pack[i * pk] + lskc * sq[i];
+            if (sub) v -= kLS * sub[i];
         }
         vals[t] = v;
     }

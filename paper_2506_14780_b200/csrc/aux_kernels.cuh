@@ -76,7 +76,7 @@ struct FinalizeArgs {
 // (gb a multiple of gs, <= 2048). One block per big group.
 __global__ void k_group_max(const double* pack, int pk, const double* sq, double lskc, const int* perm,
                             int64_t count, int gs, int gb, double* out_small, double* out_big, const DevState* st,
-                            unsigned guard, unsigned* zero_counter);
+                            unsigned guard, unsigned* zero_counter, const double* sub = nullptr);
 
 __global__ void k_max_finalize(FinalizeArgs a);
 __global__ void k_lse_finalize(FinalizeArgs a);

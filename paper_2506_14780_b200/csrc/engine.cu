@@ -640,7 +640,7 @@ struct Side {
     // culling (opt-in): Morton order and bounding boxes of groups of 64 / 256 / 2048
     // consecutive permuted points, [group][2d] = lo..., hi...
     IBuf perm;
-    DBuf box64, box256, box2048;
+    DBuf box32, box64, box256, box2048;
 };
 
 struct SolveState;
@@ -663,7 +663,7 @@ struct Problem {
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
     bool cull_ready = false;
-    DBuf f_gi[2], f_gc[2], s_go[2], s_gt[2];
+    DBuf f_gi[2], f_gc[2], s_go[2], s_gt[2], f_g32[2], s_g32[2], s_g256[2];
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -901,7 +901,7 @@ static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_b
     TilePlan tp = plan_tiles(P.dim, mode, kt, nout, nin, max_in_blocks);
     if (!tp.fn) throw CudaFailure("sknr_b200: no tile kernel for this configuration");
     P.plans[key] = tp;
-    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS;
+    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS || mode == MODE_BLOCK_CULL;
     const size_t need = static_cast<size_t>(tp.n_in_blocks) * nout * (blk ? kt : 1);
     P.partial.ensure(need);
     if (mode == MODE_BLOCK_RS) P.rsum.ensure(static_cast<size_t>(tp.n_out_tiles) * nin);
@@ -955,11 +955,18 @@ static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
 }
 
 static void cull_group_max(Problem& P, const Side& side, const double* pack, double* small, double* big, int gs,
-                           int gb, unsigned guard, unsigned* zero_counter = nullptr) {
+                           int gb, unsigned guard, unsigned* zero_counter = nullptr, const double* sub = nullptr) {
     count_launch();
     k_group_max<<<static_cast<int>((side.count + gb - 1) / gb), AUX_NT, 0, P.stream>>>(
         pack, P.pk(), side.sq.p, kLS * P.kc(), side.perm.p, side.count, gs, gb, small, big, P.st, guard,
-        zero_counter);
+        zero_counter, sub);
+}
+
+// Culled block pass (opt-in): same conditions as the culled LSE, sizes above one work unit.
+static bool cull_block_active(const Problem& P, int dir) {
+    if (!(P.cull_t > 0.0) || !P.cull_ready || P.shard || P.dim < 1 || P.dim > 4) return false;
+    const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
+    return nout >= 1024 && nin >= 1024;
 }
 
 static unsigned exact_bit(int dir) { return dir == 0 ? G_EXACT0 : G_EXACT1; }
@@ -1100,6 +1107,8 @@ struct PassSpec {
     const double* out_scale = nullptr;
     double* out = nullptr;  // sum: [nout]; block: col-major nout x k (ld = nout)
     double* rsum_out = nullptr;  // block, dir 0 only: r_i = sum_j e(j, i) b_j fused into the pass
+    bool cull = false;                 // block pass may skip negligible terms (culling enabled)
+    const double* cull_logtot = nullptr;  // per-output log of sum_in e (nullptr: 0, i.e. sums are 1)
     unsigned guard = 0;
 };
 
@@ -1113,7 +1122,8 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     cudaStream_t s = P.stream;
     const bool rs = ps.W && ps.rsum_out;
     if (rs && (ps.dir != 0 || !block_rs_fusable(P))) throw InvalidArgument("sknr_b200: fused row sums unsupported here");
-    const int mode = ps.W ? (rs ? MODE_BLOCK_RS : MODE_BLOCK) : MODE_SUM;
+    const bool bcull = ps.W && !rs && ps.cull && cull_block_active(P, ps.dir);
+    const int mode = ps.W ? (rs ? MODE_BLOCK_RS : (bcull ? MODE_BLOCK_CULL : MODE_BLOCK)) : MODE_SUM;
     const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, ps.W ? 8 : 0);
 
     PrepInArgs pi;
@@ -1153,6 +1163,21 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     k_prep_out<<<grid_for(nout), AUX_NT, 0, s>>>(po);
 
     TileArgs ta = tile_args(P, ps.dir, tp, ps.guard);
+    if (bcull) {
+        unsigned* sched = &P.st->counters[12];
+        cull_group_max(P, in, P.pack_in[ps.dir].p, P.f_g32[ps.dir].p, P.f_gc[ps.dir].p, 32, 256, ps.guard);
+        cull_group_max(P, out, P.pack_out[ps.dir].p, P.s_g32[ps.dir].p, P.s_g256[ps.dir].p, 32, 256, ps.guard, sched,
+                       ps.cull_logtot);
+        ta.perm_in = in.perm.p;
+        ta.perm_out = out.perm.p;
+        ta.box_gi = in.box32.p;
+        ta.box_go = out.box32.p;
+        ta.f_gi = P.f_g32[ps.dir].p;
+        ta.s_go = P.s_g32[ps.dir].p;
+        ta.lskc = kLS * P.kc();
+        ta.cull_t = P.cull_t;
+        ta.sched = sched;
+    }
     ta.W = ps.W;
     if (rs) {
         ta.out_w = out.w.p;
@@ -1501,7 +1526,40 @@ struct Basis {
 // two DMMA block passes (column then row direction) and a rank-one correction.
 struct OpWork {
     DBuf Z, W;
+    // culling of the operator passes (opt-in): per-output lower bounds of log(sum of
+    // terms) for the two directions, from the anchor's own transforms
+    bool cull = false;
+    DBuf sub0, sub1, tmp;
 };
+
+// sub = (v - vt)/eps (+ lw): log-total lower bound of an operator pass's outputs
+__global__ void k_cull_sub(const double* v, const double* vt, const double* lw, double inv_eps, int64_t count,
+                           double* sub) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        sub[i] = (v[i] - vt[i]) * inv_eps + (lw ? lw[i] : 0.0);
+}
+
+static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned guard);
+
+// Operator passes of R~ R~^T at the anchor (f, g): column pass terms sqrt(a_i) e^{(f_i+g_j-C_ij)/eps}
+// sum to >= e^{(g_j - g~_j)/eps} (g~ = f^{C,eps}), row pass terms to >= sqrt(a_i) e^{(f_i - f~_i)/eps}
+// (f~ = g^{C,eps}); these lower bounds normalise the culling test (pts_mma_cull_kernel).
+static void prepare_op_culling(Problem& P, const double* f, const double* g, OpWork& ow) {
+    ow.cull = cull_block_active(P, 0) && cull_block_active(P, 1) && cull_active(P, 0) && cull_active(P, 1);
+    if (!ow.cull) return;
+    const int64_t n = P.n, m = P.m;
+    ow.sub0.ensure(m);
+    ow.sub1.ensure(n);
+    ow.tmp.ensure(std::max(n, m));
+    cudaStream_t s = P.stream;
+    lse(P, 0, f, ow.tmp.p, G_NONE);  // g~
+    count_launch();
+    k_cull_sub<<<grid_for(m), AUX_NT, 0, s>>>(g, ow.tmp.p, nullptr, P.inv_eps(), m, ow.sub0.p);
+    lse(P, 1, g, ow.tmp.p, G_NONE);  // f~
+    count_launch();
+    k_cull_sub<<<grid_for(n), AUX_NT, 0, s>>>(f, ow.tmp.p, P.src.lsw.p, P.inv_eps(), n, ow.sub1.p);
+}
 
 static void apply_sym_sym(Problem& P, const double* f, const double* g, const double* X, double* Y,
                           int block, int kt, OpWork& ow) {
@@ -1522,6 +1580,8 @@ static void apply_sym_sym(Problem& P, const double* f, const double* g, const do
     zt.kt = kt;
     zt.out_scale = P.tgt.sw.p;
     zt.out = ow.Z.p;
+    zt.cull = ow.cull;
+    zt.cull_logtot = ow.sub0.p;
     plan_pass(P, zt);
     // Y = R~ Z : y_i = sum_j sqrt(a_i) e^{..} sqrt(b_j) z_j
     count_launch();
@@ -1535,6 +1595,8 @@ static void apply_sym_sym(Problem& P, const double* f, const double* g, const do
     yr.k = block;
     yr.kt = kt;
     yr.out = Y;
+    yr.cull = ow.cull;
+    yr.cull_logtot = ow.sub1.p;
     plan_pass(P, yr);
     // Y -= sqrt(a) (sqrt(a)^T Y)
     gram_all(P, n, block, 1, Y, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
@@ -1581,6 +1643,7 @@ static Basis top_modes_device(Problem& P, const double* f, const double* g, int6
     P.misc.ensure(256);
     QrWork qw;
     OpWork ow;
+    prepare_op_culling(P, f, g, ow);
     qw.backup.ensure(static_cast<size_t>(n) * block);
     count_launch();
     k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull, P.n_global,
@@ -1803,7 +1866,8 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
     if (newton) {
         const unsigned gn = G_DONE | G_NEWTON;
         const int l = static_cast<int>(ell);
-        const bool fuse_r = block_rs_fusable(P);
+        const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
+        const bool fuse_r = block_rs_fusable(P) && !cull_nr;
         if (!fuse_r) {
             // r = P~ beta at (f, h): alpha - r = -a expm1(f/eps + L_row(h))
             lse(P, 1, S.h.p, nullptr, gn);
@@ -1823,6 +1887,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         sp.kt = block_kt_for(l);
         sp.out = S.S.p;
         sp.rsum_out = fuse_r ? S.r.p : nullptr;
+        sp.cull = cull_nr;  // P~ columns sum to 1 at h = f^{C,eps}: no normalisation needed
         sp.guard = gn;
         plan_pass(P, sp);
         if (fuse_r) {
@@ -1910,7 +1975,8 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,
                                                      S.Wv.p);
         // pre-size the block-pass partials outside graph capture
-        plan_for(P, 0, block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK, kt, 8);
+        const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
+        plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
     }
     plan_for(P, 0, MODE_SUM, 0);
     plan_for(P, 1, MODE_SUM, 0);
@@ -2293,6 +2359,8 @@ static void prepare_culling(Problem& P) {
     const std::vector<int> px = morton_perm(xc, P.n, d, lo, hi), py = morton_perm(yc, P.m, d, lo, hi);
     P.src.perm.assign(px);
     P.tgt.perm.assign(py);
+    group_boxes(xc, P.n, d, px, 32, P.src.box32);
+    group_boxes(yc, P.m, d, py, 32, P.tgt.box32);
     group_boxes(xc, P.n, d, px, 64, P.src.box64);
     group_boxes(xc, P.n, d, px, 256, P.src.box256);
     group_boxes(xc, P.n, d, px, 2048, P.src.box2048);
@@ -2305,6 +2373,9 @@ static void prepare_culling(Problem& P) {
         P.f_gc[dir].ensure((nin + CULL_GC - 1) / CULL_GC);
         P.s_go[dir].ensure((nout + CULL_GO - 1) / CULL_GO);
         P.s_gt[dir].ensure((nout + CULL_GT - 1) / CULL_GT);
+        P.f_g32[dir].ensure((nin + 31) / 32);
+        P.s_g32[dir].ensure((nout + 31) / 32);
+        P.s_g256[dir].ensure((nout + 255) / 256);
     }
     P.cull_ready = true;
 }
@@ -3296,6 +3367,8 @@ int sknr_debug_counters(sknr_problem h, int64_t* out) {
     out[1] = static_cast<int64_t>(P.st_host->n_exact[1]);
     out[2] = static_cast<int64_t>(P.st_host->n_retry[0]);
     out[3] = static_cast<int64_t>(P.st_host->n_retry[1]);
+    out[4] = static_cast<int64_t>(P.st_host->n_cull_tested);
+    out[5] = static_cast<int64_t>(P.st_host->n_cull_kept);
     SKNR_API_END
 }
 

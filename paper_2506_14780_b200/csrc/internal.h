@@ -12,7 +12,7 @@ namespace sknr {
 // MODE_SUM_CULL: sum pass over spatially sorted point clouds that skips (output
 // group, input group) pairs whose every term is provably below e^-T of the
 // output's total (points d <= 4, opt-in; see pts_cull_kernel).
-enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4 };
+enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4, MODE_BLOCK_CULL = 5 };
 
 // Group sizes of the culling bounds (permuted positions): inputs are tested in
 // groups of CULL_GI (per warp) and CULL_GC (per CTA chunk), outputs in groups of

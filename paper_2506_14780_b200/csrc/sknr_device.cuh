@@ -82,6 +82,7 @@ struct DevState {
     unsigned int counters[32];   // last-block tickets of fused reductions
     unsigned long long n_exact[2];  // diagnostics: exact-shift passes per direction
     unsigned long long n_retry[2];  // diagnostics: bound-shift validation failures
+    unsigned long long n_cull_tested, n_cull_kept;  // diagnostics: culling group tests / kept groups
 };
 
 enum Guard : unsigned {

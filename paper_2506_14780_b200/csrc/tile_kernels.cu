@@ -225,11 +225,24 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
         const double s_w = a.s_go[og];
         const int64_t i0 = ib * a.in_block;
         const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        unsigned tested = 0, kept = 0;
 #pragma unroll 1
-        for (int64_t g0 = i0; g0 < i1; g0 += CULL_GI) {
-            const int64_t gi = g0 / CULL_GI;
-            const double uw = a.f_gi[gi] + s_w - a.lskc * box_dist2<D>(a.box_gi + gi * 2 * D, wbox);
-            if (uw < thr) continue;  // warp-uniform
+        for (int64_t r0 = i0; r0 < i1; r0 += 32 * CULL_GI) {
+            const int64_t gl = r0 / CULL_GI + lane;
+            bool keep = false;
+            if (gl * CULL_GI < i1)
+                keep = !(a.f_gi[gl] + s_w - a.lskc * box_dist2<D>(a.box_gi + gl * 2 * D, wbox) < thr);
+            unsigned mask = __ballot_sync(0xffffffffu, keep);
+            {
+                const int64_t ng = (i1 - r0 + CULL_GI - 1) / CULL_GI;
+                tested += static_cast<unsigned>(ng < 32 ? ng : 32);
+            }
+            kept += __popc(mask);
+#pragma unroll 1
+        while (mask) {
+            const int bit = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int64_t g0 = r0 + static_cast<int64_t>(bit) * CULL_GI;
             const int cnt = static_cast<int>((i1 - g0) < CULL_GI ? (i1 - g0) : CULL_GI);
             __syncwarp();
             for (int t = lane; t < cnt; t += 32) {
@@ -258,10 +271,16 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
                 }
             }
         }
+        }
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
             const int64_t pos = wpos + jt * 32 + lane;
             if (pos < a.n_out) a.partial[ib * a.n_out + a.perm_out[pos]] = acc[jt];
+        }
+        if (lane == 0) {
+            DevState* st = const_cast<DevState*>(a.st);
+            atomicAdd(&st->n_cull_tested, static_cast<unsigned long long>(tested));
+            atomicAdd(&st->n_cull_kept, static_cast<unsigned long long>(kept));
         }
     }
 }
@@ -414,6 +433,162 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
                 a.partial[(ib * KT + c) * a.n_out + o] = acc[mb][cb][0];
                 a.partial[(ib * KT + c + 1) * a.n_out + o] = acc[mb][cb][1];
             }
+        }
+    }
+}
+
+// Culled block pass (opt-in, see pts_cull_kernel): work unit = (32 Morton-ordered
+// outputs, input block), taken from a queue by each warp; inputs are tested in
+// groups of 32 against the unit's box with the output-normalised bound
+// S'_o = S_o - LS log(total_o) supplied by the caller (0 when every output's terms
+// sum to 1, e.g. P~ at h = f^{C,eps}); kept groups are staged warp-privately
+// (inputs and their W rows gathered through perm_in) and multiplied on DMMA as
+// in pts_mma_kernel.
+constexpr int CULL_GB = 32;  // block-pass group size (inputs and outputs)
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <int D, int KT, int MB>
+__global__ void __launch_bounds__(MMA_NT, 3) pts_mma_cull_kernel(TileArgs a) {
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int NCB = KT / 8;
+    constexpr int WS = WStride<KT>::value;
+    static_assert(8 * MB == CULL_GB, "one warp owns one 32-output group");
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* sin = sm + kTabWords + warp * (CULL_GB * PK + CULL_GB * WS);
+    double* sw = sin + CULL_GB * PK;
+    load_exp2_table(tab, tid, MMA_NT);
+    __syncthreads();
+    const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+    const int row = lane >> 2, kq = lane & 3;
+    const double thr = -kLS * a.cull_t;
+
+    while (true) {
+        unsigned unit = 0;
+        if (lane == 0) unit = atomicAdd(a.sched, 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= a.n_tiles) break;
+        const int64_t og = unit % a.n_out_tiles, ib = unit / a.n_out_tiles;
+        const int64_t obase = og * CULL_GB;
+        double Bo[MB], Yo[MB][D];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t pos = obase + mb * 8 + row;
+            const int64_t oc = a.perm_out[pos < a.n_out ? pos : a.n_out - 1];
+            Bo[mb] = a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Yo[mb][d] = a.out_pack[oc * PK + 1 + d];
+        }
+        double acc[MB][NCB][2];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) acc[mb][cb][0] = acc[mb][cb][1] = 0.0;
+        double wbox[2 * D];
+#pragma unroll
+        for (int q = 0; q < 2 * D; ++q) wbox[q] = a.box_go[og * 2 * D + q];
+        const double s_w = a.s_go[og];
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        unsigned tested = 0, kept = 0;
+        // the group tests of 32 consecutive groups run in parallel (one per lane);
+        // the kept ones are then processed in order
+#pragma unroll 1
+        for (int64_t r0 = i0; r0 < i1; r0 += 32 * CULL_GB) {
+            const int64_t gl = r0 / CULL_GB + lane;
+            bool keep = false;
+            if (gl * CULL_GB < i1)
+                keep = !(a.f_gi[gl] + s_w - a.lskc * box_dist2<D>(a.box_gi + gl * 2 * D, wbox) < thr);
+            unsigned mask = __ballot_sync(0xffffffffu, keep);
+            {
+                const int64_t ng = (i1 - r0 + CULL_GB - 1) / CULL_GB;
+                tested += static_cast<unsigned>(ng < 32 ? ng : 32);
+            }
+            kept += __popc(mask);
+#pragma unroll 1
+        while (mask) {
+            const int bit = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int64_t g0 = r0 + static_cast<int64_t>(bit) * CULL_GB;
+            const int cnt = static_cast<int>((i1 - g0) < CULL_GB ? (i1 - g0) : CULL_GB);
+            const int cnt4 = (cnt + 3) & ~3;
+            __syncwarp();
+            {
+                // asynchronous gather (cp.async, 16 B per request, all in flight at once):
+                // the group's inputs and their W rows; padded inputs get A = -inf, W = 0
+                const int ii = lane < cnt ? a.perm_in[g0 + lane] : 0;
+                if (lane < cnt) {
+#pragma unroll
+                    for (int q = 0; q < PK / 2; ++q)
+                        cp_async16(sin + lane * PK + 2 * q, a.in_pack + static_cast<int64_t>(ii) * PK + 2 * q);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PK; ++q) sin[lane * PK + q] = q == 0 ? -1e300 : 0.0;
+                }
+                constexpr int HC = KT / 2;  // 16-byte chunks per W row
+#pragma unroll 4
+                for (int c = lane; c < CULL_GB * HC; c += 32) {
+                    const int k = c / HC, q = c - k * HC;
+                    const int ik = __shfl_sync(0xffffffffu, ii, k);
+                    if (k < cnt)
+                        cp_async16(sw + k * WS + 2 * q, a.W + static_cast<int64_t>(ik) * KT + 2 * q);
+                    else
+                        *reinterpret_cast<double2*>(sw + k * WS + 2 * q) = make_double2(0.0, 0.0);
+                }
+                cp_async_wait_all();
+            }
+            __syncwarp();
+#pragma unroll 1
+            for (int k4 = 0; k4 < cnt4; k4 += 4) {
+                const double* xin = sin + (k4 + kq) * PK;
+                double x[PK];
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(xin)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+                double bf[NCB];
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) bf[cb] = sw[(k4 + kq) * WS + cb * 8 + row];
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    double u = x[0] + Bo[mb];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Yo[mb][d], u);
+                    const double e = pexp<true>(u, tab, laneoff, c3);
+#pragma unroll
+                    for (int cb = 0; cb < NCB; ++cb) dmma_8x8x4(acc[mb][cb][0], acc[mb][cb][1], e, bf[cb]);
+                }
+            }
+        }
+        }
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int64_t pos = obase + mb * 8 + row;
+            if (pos >= a.n_out) continue;
+            const int64_t o = a.perm_out[pos];
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+                const int c = cb * 8 + kq * 2;
+                a.partial[(ib * KT + c) * a.n_out + o] = acc[mb][cb][0];
+                a.partial[(ib * KT + c + 1) * a.n_out + o] = acc[mb][cb][1];
+            }
+        }
+        if (lane == 0) {
+            DevState* st = const_cast<DevState*>(a.st);
+            atomicAdd(&st->n_cull_tested, static_cast<unsigned long long>(tested));
+            atomicAdd(&st->n_cull_kept, static_cast<unsigned long long>(kept));
         }
     }
 }
@@ -888,6 +1063,18 @@ KernelInfo make_mma() {
     return k;
 }
 
+template <int D, int KT>
+KernelInfo make_mma_cull() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_mma_cull_kernel<D, KT, 4>);
+    k.jt = 1;
+    k.nt = MMA_NT;
+    k.out_tile = CULL_GB;
+    k.smem = static_cast<int>(sizeof(double)) *
+             (kTabWords + (MMA_NT / 32) * (CULL_GB * PK_of<D>::value + CULL_GB * WStride<KT>::value));
+    return k;
+}
+
 template <int DK, int MODE, int KT, int MB>
 KernelInfo make_contract() {
     KernelInfo k;
@@ -903,7 +1090,7 @@ KernelInfo make_contract() {
 
 template <int DK>
 KernelInfo pick_contract(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL) return KernelInfo{};  // register kernels only
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL) return KernelInfo{};
     if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
     if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
     switch (kt) {
@@ -924,6 +1111,18 @@ KernelInfo pick_pts(int mode, int kt) {
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
     if (mode == MODE_SUM_CULL) return make_cull<D>();
+    if (mode == MODE_BLOCK_CULL) {
+        switch (kt) {
+            case 8: return make_mma_cull<D, 8>();
+            case 16: return make_mma_cull<D, 16>();
+            case 24: return make_mma_cull<D, 24>();
+            case 32: return make_mma_cull<D, 32>();
+            case 40: return make_mma_cull<D, 40>();
+            case 48: return make_mma_cull<D, 48>();
+            case 64: return make_mma_cull<D, 64>();
+            default: return KernelInfo{};
+        }
+    }
     if (mode == MODE_BLOCK_RS) {  // 32-input rounds: 4 CTAs/SM fit (C4 ell=32: 13.9 ms vs 14.1 ms at 64)
         switch (kt) {
             case 8: return make_mma<D, 8, 4, true, 32>();
@@ -970,7 +1169,7 @@ KernelInfo make_dense_mma() {
 }
 
 KernelInfo pick_dense(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL) return KernelInfo{};  // point clouds only
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL) return KernelInfo{};
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
     switch (kt) {  // FP64 tensor-core (DMMA) block pass
@@ -1082,8 +1281,9 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     if (!ki.fn) return p;
     // Small problems (e.g. C1 512^2, C2 4096^2): the 2048-output tiles of the
     // register kernels leave most SMs idle; use 128-output tiles instead.
-    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS;
-    if (variant < 0 && dim > 0 && !blk && mode != MODE_SUM_CULL && n_out * n_in <= (int64_t(1) << 26)) {
+    const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS || mode == MODE_BLOCK_CULL;
+    const bool culled = mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL;
+    if (variant < 0 && dim > 0 && !blk && !culled && n_out * n_in <= (int64_t(1) << 26)) {
         switch (dim) {
             case 1: ki = mode == MODE_SUM ? make_pts<1, 1, MODE_SUM, 0, 128, 2>() : make_pts<1, 1, MODE_MAX, 0, 128, 2>(); break;
             case 2: ki = mode == MODE_SUM ? make_pts<2, 1, MODE_SUM, 0, 128, 2>() : make_pts<2, 1, MODE_MAX, 0, 128, 2>(); break;
@@ -1107,11 +1307,12 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.nt = ki.nt;
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     // input-block granularity (the kernels stage up to their chunk size per round)
-    const int ch = blk ? chunk_inputs(MODE_BLOCK, kt) : (mode == MODE_SUM_CULL ? CULL_GI : 32);
+    const int ch = mode == MODE_BLOCK_CULL ? CULL_GB
+                                          : (blk ? chunk_inputs(MODE_BLOCK, kt) : (mode == MODE_SUM_CULL ? CULL_GI : 32));
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
     // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small
     // (culled pass: >= 8 work units per resident warp, taken from a queue).
-    const int64_t units = mode == MODE_SUM_CULL ? 8 * resident * (ki.nt / 32) : 8 * resident;
+    const int64_t units = culled ? 8 * resident * (ki.nt / 32) : 8 * resident;
     int64_t want = (units + p.n_out_tiles - 1) / p.n_out_tiles;
     if (want < 1) want = 1;
     if (want > max_blocks_by_chunk) want = max_blocks_by_chunk;

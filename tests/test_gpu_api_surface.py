@@ -317,3 +317,28 @@ def test_culling_errors_and_off_switch():
     pp.set_culling(0.0)
     assert np.array_equal(sk.ctransform_of_f(pp, f), g0)
     assert rel_err(g1, g0) <= 1e-13
+
+
+def test_culled_sknr_and_top_modes_match_dense():
+    """Culled Newton derivative pass (DMMA, r from a culled row LSE) and culled
+    top_modes operator passes (normalised by the anchor's own transforms)."""
+    r = np.random.default_rng(11)
+    n = m = 8192
+    x = np.asfortranarray(r.uniform(0, 1, (n, 2)))
+    y = np.asfortranarray(r.uniform(0, 1, (m, 2)))
+    a = np.full(n, 1.0 / n)
+    b = np.full(m, 1.0 / m)
+    eps, ell = 2e-3, 12
+    pd = sk.PointProblem(x, y, a, b, eps)
+    pc = sk.PointProblem(x, y, a, b, eps)
+    pc.set_culling(60.0)
+    wd = sk.solve(pd.with_epsilon(2 * eps), tol=1e-9, trace=False)
+    bd = sk.top_modes(pd.with_epsilon(2 * eps), wd.f, wd.g, ell)
+    bc = sk.top_modes(pc.with_epsilon(2 * eps), wd.f, wd.g, ell)
+    assert rel_err(bc.rhos, bd.rhos) <= 1e-9
+    assert sk.projector_distance(bc, bd) <= 1e-6
+    rd = sk.solve(pd, tol=1e-9, ell=ell, basis=bd, init=(wd.f, wd.g))
+    rc = sk.solve(pc, tol=1e-9, ell=ell, basis=bd, init=(wd.f, wd.g))
+    assert rd.converged and rc.converged
+    assert abs(rc.iterations - rd.iterations) <= 1
+    assert rel_err(rc.f, rd.f) <= 2e-8  # accept decisions at the rounding level (TOL_POT_NEWTON)
