@@ -119,39 +119,27 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
 
 // ------------------------------------------------------------------ culling bounds
 __global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk, const double* sq, double lskc,
-                                                      const int* perm, int64_t count, int gs, int gb,
-                                                      double* out_small, double* out_big, const DevState* st,
-                                                      unsigned guard, unsigned* zero_counter, const double* sub) {
+                                                      const int* perm, int64_t count, int gs, double* out,
+                                                      const DevState* st, unsigned guard, unsigned* zero_counter,
+                                                      const double* sub) {
     if (guard_skip(st, guard)) return;
     if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
-    __shared__ double vals[2048];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * gb;
-    for (int t = threadIdx.x; t < gb; t += blockDim.x) {
-        const int64_t p = base + t;
-        double v = -kInf;
-        if (p < count) {
-            const int64_t i = perm[p];
-            v = pack[i * pk] + lskc * sq[i];
-            if (sub) v -= kLS * sub[i];
-        }
-        vals[t] = v;
+    __shared__ double vals[AUX_NT];
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * AUX_NT + threadIdx.x;
+    double v = -kInf;
+    if (p < count) {
+        const int64_t i = perm[p];
+        v = pack[i * pk] + lskc * sq[i];
+        if (sub) v -= kLS * sub[i];
     }
+    vals[threadIdx.x] = v;
     __syncthreads();
-    const int nsmall = gb / gs;
-    __shared__ double smax[64];
-    for (int g = threadIdx.x; g < nsmall; g += blockDim.x) {
-        double m = -kInf;
-        for (int t = 0; t < gs; ++t) m = fmax(m, vals[g * gs + t]);
-        smax[g] = m;
-        const int64_t gidx = base / gs + g;
-        if (gidx * gs < count) out_small[gidx] = m;
+    // tree max within each group of gs consecutive positions (gs a power of two <= AUX_NT)
+    for (int s = gs / 2; s > 0; s >>= 1) {
+        if ((threadIdx.x % gs) < s) vals[threadIdx.x] = fmax(vals[threadIdx.x], vals[threadIdx.x + s]);
+        __syncthreads();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = -kInf;
-        for (int g = 0; g < nsmall; ++g) m = fmax(m, smax[g]);
-        out_big[blockIdx.x] = m;
-    }
+    if (threadIdx.x % gs == 0 && p < count) out[p / gs] = vals[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ finalize

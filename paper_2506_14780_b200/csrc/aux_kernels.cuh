@@ -71,12 +71,12 @@ struct FinalizeArgs {
     unsigned guard = 0;
 };
 
-// Culling bounds (MODE_SUM_CULL): over permuted positions, the maximum of
-// pack[i*pk] + lskc*sq[i] (i = perm[p]) per group of gs and per group of gb
-// (gb a multiple of gs, <= 2048). One block per big group.
+// Culling bounds: over permuted positions, the maximum of pack[i*pk] + lskc*sq[i]
+// (- LS sub[i] when given), i = perm[p], per group of gs (gs divides AUX_NT).
+// Optionally zeroes a work-queue counter for the pass that follows.
 __global__ void k_group_max(const double* pack, int pk, const double* sq, double lskc, const int* perm,
-                            int64_t count, int gs, int gb, double* out_small, double* out_big, const DevState* st,
-                            unsigned guard, unsigned* zero_counter, const double* sub = nullptr);
+                            int64_t count, int gs, double* out, const DevState* st, unsigned guard,
+                            unsigned* zero_counter, const double* sub = nullptr);
 
 __global__ void k_max_finalize(FinalizeArgs a);
 __global__ void k_lse_finalize(FinalizeArgs a);

@@ -640,7 +640,7 @@ struct Side {
     // culling (opt-in): Morton order and bounding boxes of groups of 64 / 256 / 2048
     // consecutive permuted points, [group][2d] = lo..., hi...
     IBuf perm;
-    DBuf box32, box64, box256, box2048;
+    DBuf box32, box64, box256;
 };
 
 struct SolveState;
@@ -663,7 +663,7 @@ struct Problem {
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
     bool cull_ready = false;
-    DBuf f_gi[2], f_gc[2], s_go[2], s_gt[2], f_g32[2], s_g32[2], s_g256[2];
+    DBuf f_gi[2], s_go[2], f_g32[2], s_g32[2];
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -929,7 +929,7 @@ static TileArgs tile_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
 static bool cull_active(const Problem& P, int dir) {
     if (!(P.cull_t > 0.0) || !P.cull_ready || P.shard || P.dim < 1 || P.dim > 4) return false;
     const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
-    return nout >= CULL_GT && nin >= CULL_GC;
+    return nout >= 8 * CULL_GO && nin >= 4 * CULL_GI;
 }
 
 static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guard, int retry_phase) {
@@ -939,13 +939,9 @@ static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     a.perm_in = in.perm.p;
     a.perm_out = out.perm.p;
     a.box_gi = in.box64.p;
-    a.box_gc = in.box256.p;
     a.box_go = out.box256.p;
-    a.box_gt = out.box2048.p;
     a.f_gi = P.f_gi[dir].p;
-    a.f_gc = P.f_gc[dir].p;
     a.s_go = P.s_go[dir].p;
-    a.s_gt = P.s_gt[dir].p;
     a.lskc = kLS * P.kc();
     a.cull_t = P.cull_t;
     a.inv_eps = P.inv_eps();
@@ -954,12 +950,12 @@ static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     return a;
 }
 
-static void cull_group_max(Problem& P, const Side& side, const double* pack, double* small, double* big, int gs,
-                           int gb, unsigned guard, unsigned* zero_counter = nullptr, const double* sub = nullptr) {
+// Per-group maxima (groups of gs permuted positions) of the culling bound terms.
+static void cull_group_max(Problem& P, const Side& side, const double* pack, double* out, int gs, unsigned guard,
+                           unsigned* zero_counter = nullptr, const double* sub = nullptr) {
     count_launch();
-    k_group_max<<<static_cast<int>((side.count + gb - 1) / gb), AUX_NT, 0, P.stream>>>(
-        pack, P.pk(), side.sq.p, kLS * P.kc(), side.perm.p, side.count, gs, gb, small, big, P.st, guard,
-        zero_counter, sub);
+    k_group_max<<<static_cast<int>((side.count + AUX_NT - 1) / AUX_NT), AUX_NT, 0, P.stream>>>(
+        pack, P.pk(), side.sq.p, kLS * P.kc(), side.perm.p, side.count, gs, out, P.st, guard, zero_counter, sub);
 }
 
 // Culled block pass (opt-in): same conditions as the culled LSE, sizes above one work unit.
@@ -1031,7 +1027,7 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     count_launch();
     k_prep_out<<<grid_for(nout), AUX_NT, 0, s>>>(po);
     if (cull)  // input-group maxima of F (the inputs do not change between phases)
-        cull_group_max(P, in, P.pack_in[dir].p, P.f_gi[dir].p, P.f_gc[dir].p, CULL_GI, CULL_GC, guard);
+        cull_group_max(P, in, P.pack_in[dir].p, P.f_gi[dir].p, CULL_GI, guard);
 
     FinalizeArgs fa;
     fa.partial = P.partial.p;
@@ -1066,7 +1062,7 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         k_max_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
         if (cull) {  // output-group maxima of S with this phase's shift
             unsigned* sched = &P.st->counters[10 + dir];
-            cull_group_max(P, out, P.pack_out[dir].p, P.s_go[dir].p, P.s_gt[dir].p, CULL_GO, CULL_GT, gsum, sched);
+            cull_group_max(P, out, P.pack_out[dir].p, P.s_go[dir].p, CULL_GO, gsum, sched);
             TileArgs ca = cull_args(P, dir, tsum, gsum, phase);
             ca.sched = sched;
             launch_tiles(tsum, ca, s);
@@ -1165,8 +1161,8 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     TileArgs ta = tile_args(P, ps.dir, tp, ps.guard);
     if (bcull) {
         unsigned* sched = &P.st->counters[12];
-        cull_group_max(P, in, P.pack_in[ps.dir].p, P.f_g32[ps.dir].p, P.f_gc[ps.dir].p, 32, 256, ps.guard);
-        cull_group_max(P, out, P.pack_out[ps.dir].p, P.s_g32[ps.dir].p, P.s_g256[ps.dir].p, 32, 256, ps.guard, sched,
+        cull_group_max(P, in, P.pack_in[ps.dir].p, P.f_g32[ps.dir].p, 32, ps.guard);
+        cull_group_max(P, out, P.pack_out[ps.dir].p, P.s_g32[ps.dir].p, 32, ps.guard, sched,
                        ps.cull_logtot);
         ta.perm_in = in.perm.p;
         ta.perm_out = out.perm.p;
@@ -2363,19 +2359,14 @@ static void prepare_culling(Problem& P) {
     group_boxes(yc, P.m, d, py, 32, P.tgt.box32);
     group_boxes(xc, P.n, d, px, 64, P.src.box64);
     group_boxes(xc, P.n, d, px, 256, P.src.box256);
-    group_boxes(xc, P.n, d, px, 2048, P.src.box2048);
     group_boxes(yc, P.m, d, py, 64, P.tgt.box64);
     group_boxes(yc, P.m, d, py, 256, P.tgt.box256);
-    group_boxes(yc, P.m, d, py, 2048, P.tgt.box2048);
     for (int dir = 0; dir < 2; ++dir) {
         const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
         P.f_gi[dir].ensure((nin + CULL_GI - 1) / CULL_GI);
-        P.f_gc[dir].ensure((nin + CULL_GC - 1) / CULL_GC);
         P.s_go[dir].ensure((nout + CULL_GO - 1) / CULL_GO);
-        P.s_gt[dir].ensure((nout + CULL_GT - 1) / CULL_GT);
         P.f_g32[dir].ensure((nin + 31) / 32);
         P.s_g32[dir].ensure((nout + 31) / 32);
-        P.s_g256[dir].ensure((nout + 255) / 256);
     }
     P.cull_ready = true;
 }

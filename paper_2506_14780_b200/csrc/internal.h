@@ -14,10 +14,10 @@ namespace sknr {
 // output's total (points d <= 4, opt-in; see pts_cull_kernel).
 enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4, MODE_BLOCK_CULL = 5 };
 
-// Group sizes of the culling bounds (permuted positions): inputs are tested in
-// groups of CULL_GI (per warp) and CULL_GC (per CTA chunk), outputs in groups of
-// CULL_GO (one warp's 32 x 8 outputs) and CULL_GT (one CTA tile).
-constexpr int CULL_GI = 64, CULL_GC = 256, CULL_GO = 256, CULL_GT = 2048;
+// Group sizes of the culling bounds (permuted positions): the sum pass tests input
+// groups of CULL_GI against output groups of CULL_GO (one warp's 32 x 8 outputs);
+// the block pass uses 32 x 32 (CULL_GB in tile_kernels.cu).
+constexpr int CULL_GI = 64, CULL_GO = 256;
 
 // Arguments of the persistent tile kernels (tile_kernels.cu).
 struct TileArgs {
@@ -37,14 +37,10 @@ struct TileArgs {
     // MODE_SUM_CULL
     const int* perm_in = nullptr;      // permuted position -> input index
     const int* perm_out = nullptr;     // permuted position -> output index
-    const double* box_gi = nullptr;    // [n_in/CULL_GI][2D] lo..., hi... (centred coordinates)
-    const double* box_gc = nullptr;    // [n_in/CULL_GC][2D]
-    const double* box_go = nullptr;    // [n_out/CULL_GO][2D]
-    const double* box_gt = nullptr;    // [n_out/CULL_GT][2D]
+    const double* box_gi = nullptr;    // [input group][2D] lo..., hi... (centred coordinates)
+    const double* box_go = nullptr;    // [output group][2D]
     const double* f_gi = nullptr;      // group max of F_in = A_in + LS kc |x_in|^2
-    const double* f_gc = nullptr;
-    const double* s_go = nullptr;      // group max of S_out = B_out + LS kc |y_out|^2
-    const double* s_gt = nullptr;
+    const double* s_go = nullptr;      // group max of S_out = B_out + LS kc |y_out|^2 (- LS log-total)
     double lskc = 0.0;                 // LS * kappa / eps
     double cull_t = 60.0;              // skip terms below e^-T of the output's total
     double inv_eps = 1.0;

@@ -168,9 +168,9 @@ __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
 // and the output's LSE satisfies L_o >= s_o - slack (slack = 0 after an exact max
 // pass, (max df - min df)/eps for the bound shift). A group pair with
 // U < -LS (T + slack) therefore only holds terms below e^-T of the output's total
-// (n e^-60 < 1e-21 relative for T = 60): it is skipped. The test runs per CTA for
-// a 256-input chunk (skipping the shared-memory staging too) and per warp for each
-// 64-input group. Kept terms are accumulated exactly as in pts_tile_kernel.
+// (n e^-60 < 1e-21 relative for T = 60): it is skipped. Each warp tests 32 groups
+// at once (one per lane, ballot), stages only the kept groups and accumulates
+// their terms exactly as in pts_tile_kernel.
 template <int D>
 __device__ __forceinline__ double box_dist2(const double* __restrict__ a, const double* __restrict__ b) {
     double s = 0.0;
