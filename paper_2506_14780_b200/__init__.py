@@ -898,12 +898,32 @@ def bench_fp64_peak():
     return t.value, ms.value
 
 
+# ---------------------------------------------------------------- harness (bindings.cpp:180-215)
+def oracle_solve(problem: Problem, target_residual: float = 1e-13):
+    """Ground-truth desk-scale solve (oracle.cpp:21-90); see harness.oracle_solve."""
+    from .harness import oracle_solve as _os
+    return _os(problem, target_residual)
+
+
+def gaussian_cloud(count: int, mean, cov, seed: int):
+    """(points n x 2, uniform weights) drawn as generators.cpp:19-36."""
+    from .generators import gaussian_cloud as _gc
+    return _gc(count, mean, cov, seed)
+
+
+def sq_euclidean_cost(source, target) -> np.ndarray:
+    """Dense ||x_i - y_j||^2 (generators.cpp:94-103); the solver itself never stores it
+    for point clouds (PointProblem)."""
+    from .generators import sq_euclidean_cost as _sq
+    return _sq(np.asarray(source, dtype=np.float64), np.asarray(target, dtype=np.float64))
+
+
 __all__ = [
     "EigensolverError", "IterationRecord", "NewtonOutcome", "PointProblem", "Problem", "SolveResult",
     "SpectralBasis", "__version__", "anneal", "apply_K", "apply_R", "apply_Rt", "apply_sym_block",
     "apply_sym_t_block", "coupling", "coupling_rows", "ctransform_of_f", "dual_value", "gauge_distance",
     "gauge_normalized", "marginal_gap", "newton_step", "projector_distance", "semi_dual_hessian_quadform",
-    "sk_sweep", "solve_batch", "spectrum",
+    "sk_sweep", "solve_batch", "spectrum", "oracle_solve", "gaussian_cloud", "sq_euclidean_cost",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
     "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
     "row_partition", "shard", "semi_dual_gradient", "semi_dual_value", "solve",
