@@ -257,6 +257,31 @@ def run_ours(args, world, rank, local):
                 "algorithmic_per_cell": f"{FP64_SLOTS_PER_CELL} FP64 issue slots (x2 flops)",
                 "peak_source": "measured DFMA-only kernel on this GPU (sknr_bench_fp64_peak)"}
 
+    # ---- row LSE separately (K1 vs K2)
+    ms_row_pass, ms_row_kernel = sk.bench_pass(prob, 1, 0, passes=5)
+
+    # ---- stored-cost roofline (HBM): C5 (32768 x 16384, d = 64) with the cost built once on device,
+    # column LSE streaming 8 B per cell with 128-bit loads
+    stored = None
+    if rank == 0 and not args.no_ttt:
+        c5 = G.config("C5")
+        p5 = sk.PointProblem(c5.x, c5.y, c5.alpha, c5.beta, c5.epsilon, cost_mode="stored")
+        ms5, k5 = sk.bench_pass(p5, 2, 0, passes=10)
+        cells5 = float(c5.n) * c5.m
+        hbm_peak = 6552.0
+        try:
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as fh:
+                hbm_peak = float(json.load(fh)["hbm_gbs"])
+        except (OSError, KeyError, ValueError):
+            pass
+        gbs = 8.0 * cells5 / (k5 * 1e-3) / 1e9
+        stored = {"workload": "C5 stored cost: n=32768, m=16384, d=64, column LSE sum kernel (dense_v2)",
+                  "kernel_ms": k5, "gcells_per_s": cells5 / (k5 * 1e-3) / 1e9, "bound": "hbm",
+                  "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                  "algorithmic_per_cell": "8 B (the fp64 cost element, read once)",
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        del p5
+
     # ---- SK-NR(ell) iteration (restricted Newton step included)
     rng = np.random.default_rng(0)
     V = np.linalg.qr(rng.standard_normal((n, inst.ell)))[0] * np.sqrt(n)
@@ -377,7 +402,9 @@ def run_ours(args, world, rank, local):
             "sknr_iteration": {"ell": inst.ell, "ms": ms_nr, "kernels": kpi_nr,
                                "cell_passes": 4, "gcells_per_s": 4 * cells / (ms_nr * 1e-3) / 1e9,
                                "note": "2 sweep LSEs + fused V^T P~ / P~ beta pass + candidate column LSE"},
-            "pass_ms": {"column_lse_full": ms_pass},
+            "pass_ms": {"column_lse_full": ms_pass, "row_lse_full": ms_row_pass,
+                        "row_lse_kernel_gcells_per_s": cells_local / (ms_row_kernel * 1e-3) / 1e9},
+            "roofline_stored": stored,
             "time_to_tol": ttt,
             "batch_c1": batch,
             "library": sk.version(),
