@@ -279,7 +279,8 @@ def run_ours(args, world, rank, local):
                   "kernel_ms": k5, "gcells_per_s": cells5 / (k5 * 1e-3) / 1e9, "bound": "hbm",
                   "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                   "algorithmic_per_cell": "8 B (the fp64 cost element, read once)",
-                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured; a STREAM copy, so a read-only "
+                                 "stream can land slightly above 1.0)"}
         del p5
 
     # ---- SK-NR(ell) iteration (restricted Newton step included)
