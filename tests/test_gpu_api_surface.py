@@ -342,3 +342,26 @@ def test_culled_sknr_and_top_modes_match_dense():
     assert rd.converged and rc.converged
     assert abs(rc.iterations - rd.iterations) <= 1
     assert rel_err(rc.f, rd.f) <= 2e-8  # accept decisions at the rounding level (TOL_POT_NEWTON)
+
+
+def test_culled_anneal_and_batch_match_dense():
+    """Culling inside anneal (epsilon changes between stages, bounds recomputed per pass)
+    and inside solve_batch (per-problem work queues)."""
+    inst = G.config("C2", n=4096, m=4096)
+    mk = lambda: sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilons[0], inst.cost_scale)
+    pd, pc = mk(), mk()
+    pc.set_culling(60.0)
+    eps = list(inst.epsilons[:5])
+    sd = sk.anneal(pd, eps, warm="potentials", ell=0)
+    sc = sk.anneal(pc, eps, warm="potentials", ell=0)
+    for a, c in zip(sd, sc):
+        assert a.iterations == c.iterations and a.converged and c.converged
+        assert rel_err(c.f, a.f) <= 1e-12
+    probs = [mk() for _ in range(3)]
+    for p in probs:
+        p.set_epsilon(inst.epsilons[3])
+        p.set_culling(60.0)
+    rb = sk.solve_batch(probs, tol=1e-9)
+    ref = sk.solve(pd.with_epsilon(inst.epsilons[3]), tol=1e-9)
+    for r in rb:
+        assert r.iterations == ref.iterations and rel_err(r.f, ref.f) <= 1e-12
