@@ -247,6 +247,11 @@ int sknr_debug_counters(sknr_problem p, int64_t* out /* 6 */);
  * the copy torch already mapped is reused). */
 int sknr_comm_unique_id(unsigned char id[128]);
 int sknr_comm_init(int rank, int world, const unsigned char id[128], int device);
+/* Testing aid: an in-process group of `world` emulated ranks on the current GPU.
+ * Shards created after this call exchange their collectives in-process (one host
+ * thread per rank, eager launches ordered by stream events); sknr_comm_destroy
+ * ends it. Used to check the sharded path at R > 1 on a single GPU. */
+int sknr_comm_init_emulated(int world);
 int sknr_comm_destroy(void);
 /* Restrict a freshly created problem to rows [row_begin,row_end) of this rank
  * under the attached communicator. */

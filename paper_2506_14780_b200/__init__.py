@@ -123,6 +123,7 @@ _SIGS = {
     "sknr_comm_unique_id": [ctypes.c_void_p],
     "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int],
     "sknr_comm_destroy": [],
+    "sknr_comm_init_emulated": [ctypes.c_int],
     "sknr_problem_shard": [_P, _I64, _I64],
 }
 _RET = {
@@ -866,6 +867,47 @@ def comm_destroy() -> None:
     _check(lib().sknr_comm_destroy())
 
 
+def comm_init_emulated(world: int) -> None:
+    """Testing aid: `world` in-process emulated ranks on this GPU. Shard R handles
+    (one per rank) after this call and drive each from its own thread; collectives
+    are exchanged in-process (see sknr_comm_init_emulated)."""
+    _check(lib().sknr_comm_init_emulated(int(world)))
+
+
+def run_emulated_shards(make_problem, world: int, fn):
+    """Run fn(problem_r) for r = 0..world-1 on emulated shards, one thread per rank;
+    returns the per-rank results. make_problem() builds a fresh full problem."""
+    import threading
+
+    comm_init_emulated(world)
+    try:
+        probs = []
+        for r in range(world):
+            p = make_problem()
+            shard(p, r, world)
+            probs.append(p)
+        out = [None] * world
+        err = [None] * world
+
+        def run(r):
+            try:
+                out[r] = fn(probs[r])
+            except BaseException as e:  # noqa: BLE001 -- re-raised in the caller
+                err[r] = e
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+    finally:
+        comm_destroy()
+
+
 def row_partition(n: int, world: int, rank: int):
     """Rows [n*r/R, n*(r+1)/R) of rank r (the partition sknr_problem_shard enforces)."""
     return n * rank // world, n * (rank + 1) // world
@@ -926,6 +968,6 @@ __all__ = [
     "sk_sweep", "solve_batch", "spectrum", "oracle_solve", "gaussian_cloud", "sq_euclidean_cost",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
     "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
-    "row_partition", "shard", "semi_dual_gradient", "semi_dual_value", "solve",
+    "row_partition", "shard", "comm_init_emulated", "run_emulated_shards", "semi_dual_gradient", "semi_dual_value", "solve",
     "top_modes", "version",
 ]

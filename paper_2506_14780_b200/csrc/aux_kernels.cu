@@ -350,21 +350,31 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
     double acc[RED_MAX_TERMS];
 #pragma unroll
     for (int t = 0; t < RED_MAX_TERMS; ++t) acc[t] = 0.0;
-    const int64_t total = a.T[0] + a.T[1];
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int seg = e < a.T[0] ? 0 : 1;
-        const int64_t i = seg == 0 ? e : e - a.T[0];
+    // Each segment has its own element-to-thread layout: segment 1 (the m-long, replicated
+    // side when rows are sharded) is reduced by its own fixed number of blocks, so its sums
+    // round identically on every rank whatever the length of the rank's segment 0.
+    for (int seg = 0; seg < 2; ++seg) {
+        const int64_t T = a.T[seg];
+        int64_t g = gridDim.x;
+        if (seg == 1) {
+            g = (T + AUX_NT * 8 - 1) / (AUX_NT * 8);  // reduce_blocks(T[1])
+            g = g < 1 ? 1 : (g > 296 ? 296 : g);
+            g = g < gridDim.x ? g : gridDim.x;
+            if (blockIdx.x >= g) continue;
+        }
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < T;
+             i += g * blockDim.x) {
 #pragma unroll
-        for (int t = 0; t < RED_MAX_TERMS; ++t) {
-            if (t >= a.nterms || a.seg[t] != seg) continue;
-            const double x = a.x[t][i];
-            if (a.op[t] == RED_DOT)
-                acc[t] = a.y[t] ? fma(x, a.y[t][i], acc[t]) : acc[t] + x;
-            else if (a.op[t] == RED_SQ)
-                acc[t] = fma(x, x, acc[t]);
-            else
-                acc[t] = fmax(acc[t], fabs(x));
+            for (int t = 0; t < RED_MAX_TERMS; ++t) {
+                if (t >= a.nterms || a.seg[t] != seg) continue;
+                const double x = a.x[t][i];
+                if (a.op[t] == RED_DOT)
+                    acc[t] = a.y[t] ? fma(x, a.y[t][i], acc[t]) : acc[t] + x;
+                else if (a.op[t] == RED_SQ)
+                    acc[t] = fma(x, x, acc[t]);
+                else
+                    acc[t] = fmax(acc[t], fabs(x));
+            }
         }
     }
     // warp tree then fixed cross-warp order

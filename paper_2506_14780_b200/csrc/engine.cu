@@ -18,10 +18,12 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <map>
 #include <tuple>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -677,6 +679,8 @@ struct Problem {
 
     // row sharding: this handle holds source rows [row_begin, row_begin + n)
     bool shard = false;
+    bool emu = false;           // collectives through the in-process emulated group (testing)
+    int rank = 0, world = 1;
     int64_t n_global = 0, row_begin = 0;
     DBuf red_tmp, gather_buf;
     std::vector<double> h_alpha, h_beta;  // full host copies (validation, host-side dots)
@@ -861,9 +865,102 @@ static void finish_dense(Problem* p, const double* cost) {
 }
 
 // ============================================================ collectives
+// In-process emulation of the row-sharded collectives (sknr_comm_init_emulated): R
+// shard handles on one GPU, driven by R host threads, meet at every collective; the
+// last thread to arrive enqueues one reduction kernel over all R buffers on a shared
+// stream after waiting (cudaStreamWaitEvent) for every rank's arrival event, and each
+// rank's stream then waits for its completion event. Ordering is by stream/event
+// dependencies only -- no kernel ever waits on another -- and the solve loop runs
+// eagerly (no graph capture) in this mode. The rank order of the merge is fixed.
+constexpr int kEmuMax = 16;
+
+struct EmuPtrs {
+    double* buf[kEmuMax];
+};
+
+__global__ void k_emu_allreduce(EmuPtrs p, int world, int64_t count, int op) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double acc = p.buf[0][e];
+        for (int r = 1; r < world; ++r) {
+            const double v = p.buf[r][e];
+            acc = op == 0 ? acc + v : fmax(acc, v);
+        }
+        for (int r = 0; r < world; ++r) p.buf[r][e] = acc;
+    }
+}
+
+struct EmuGroup {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t generation = 0;
+    EmuPtrs bufs{};
+    const double* locals[kEmuMax] = {};
+    int64_t counts[kEmuMax] = {};
+    cudaEvent_t ev_arrive[kEmuMax] = {};
+    cudaEvent_t ev_done = nullptr;
+    cudaStream_t red = nullptr;
+
+    void init(int w) {
+        destroy();
+        world = w;
+        for (int r = 0; r < w; ++r) CK(cudaEventCreateWithFlags(&ev_arrive[r], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&red, cudaStreamNonBlocking));
+    }
+    void destroy() {
+        for (auto& e : ev_arrive)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        if (ev_done) cudaEventDestroy(ev_done), ev_done = nullptr;
+        if (red) cudaStreamDestroy(red), red = nullptr;
+        world = 0;
+    }
+    // Rendezvous of rank r; `leader` runs once with every rank's arguments in place.
+    template <typename F>
+    void meet(int r, cudaStream_t s, F&& leader) {
+        static const bool dbg_sync = std::getenv("SKNR_EMU_SYNC") != nullptr;
+        if (dbg_sync) CK(cudaStreamSynchronize(s));
+        CK(cudaEventRecord(ev_arrive[r], s));
+        {
+            std::unique_lock<std::mutex> lk(mu);
+            const int64_t gen = generation;
+            if (++arrived == world) {
+                for (int q = 0; q < world; ++q) CK(cudaStreamWaitEvent(red, ev_arrive[q], 0));
+                leader();
+                CK(cudaEventRecord(ev_done, red));
+                if (dbg_sync) CK(cudaStreamSynchronize(red));
+                arrived = 0;
+                ++generation;
+                cv.notify_all();
+            } else {
+                cv.wait(lk, [&] { return generation != gen; });
+            }
+        }
+        CK(cudaStreamWaitEvent(s, ev_done, 0));
+    }
+};
+static EmuGroup g_emu;
+
+static int nccl_op_code(ncclRedOp_t op) { return op == ncclMax ? 1 : 0; }
+
 // In-place allreduce on the problem's stream; a no-op unless the handle is row-sharded.
 static void allreduce(Problem& P, double* buf, size_t count, ncclRedOp_t op) {
     if (!P.shard || count == 0) return;
+    if (P.emu) {
+        std::unique_lock<std::mutex> lk(g_emu.mu);
+        g_emu.bufs.buf[P.rank] = buf;
+        lk.unlock();
+        const int code = nccl_op_code(op);
+        g_emu.meet(P.rank, P.stream, [&] {
+            count_launch();
+            k_emu_allreduce<<<static_cast<int>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, g_emu.red>>>(
+                g_emu.bufs, g_emu.world, static_cast<int64_t>(count), code);
+            CK(cudaGetLastError());
+        });
+        return;
+    }
     NK(g_nccl.AllReduce(buf, buf, count, ncclDouble, op, g_comm.comm, P.stream));
 }
 
@@ -881,6 +978,25 @@ static void gather_rows(Problem& P, const double* dev_local, double* host_full) 
         return;
     }
     P.gather_buf.ensure(P.n_global);
+    if (P.emu) {
+        {
+            std::lock_guard<std::mutex> lk(g_emu.mu);
+            g_emu.locals[P.rank] = dev_local;
+            g_emu.bufs.buf[P.rank] = P.gather_buf.p;
+        }
+        g_emu.meet(P.rank, P.stream, [&] {
+            for (int q = 0; q < g_emu.world; ++q) {
+                int64_t b, e;
+                row_partition(P.n_global, g_emu.world, q, b, e);
+                for (int r = 0; r < g_emu.world; ++r)
+                    CK(cudaMemcpyAsync(g_emu.bufs.buf[r] + b, g_emu.locals[q], sizeof(double) * (e - b),
+                                       cudaMemcpyDeviceToDevice, g_emu.red));
+            }
+        });
+        download(host_full, P.gather_buf.p, P.n_global, P.stream);
+        CK(cudaStreamSynchronize(P.stream));
+        return;
+    }
     NK(g_nccl.GroupStart());
     for (int r = 0; r < g_comm.world; ++r) {
         int64_t b, e;
@@ -1890,7 +2006,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             count_launch();
             k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(P.src.w.p, S.r.p, n, 1.0, -1.0, S.am.p);
         }
-        allreduce(P, S.S.p, static_cast<size_t>(m) * l, ncclSum);  // S = V^T P~ summed over row shards
+        // (plan_pass has already summed S = V^T P~ over the row shards)
         double* G1 = S.G.p;
         double* cross = G1 + l * l;
         double* grad = cross + l * l;
@@ -2012,23 +2128,28 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     cudaStream_t s = P.stream;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
-    CK(cudaStreamEndCapture(s, &graph));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+    if (!P.emu) {
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
+        CK(cudaStreamEndCapture(s, &graph));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+    }
     int64_t batch = 1;
     int64_t launched = 0;
     while (true) {
         for (int64_t b = 0; b < batch; ++b) {
-            CK(cudaGraphLaunch(exec, s));
+            if (exec)
+                CK(cudaGraphLaunch(exec, s));
+            else  // emulated shards: the same kernels and collectives, launched eagerly
+                enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
             ++launched;
         }
         if (poll_done(P)) break;
         if (launched >= max_iter + 2) break;
         batch = std::min<int64_t>(batch * 2, 64);
     }
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
     SolveOut out;
     out.f.resize(P.n_global);
     out.g.resize(P.m);
@@ -3238,6 +3359,7 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
     if (use_newton && (basis == nullptr || basis_ell != cfg->ell))
         throw InvalidArgument("solve: ell > 0 requires a basis");
     const int64_t ell = use_newton ? cfg->ell : 0;
+    if (P.emu) throw InvalidArgument("sknr_bench_iterations: not available on emulated shards");
     SolveState S;
     prepare_solve(P, S, ell, basis, nullptr, warmup + iters + 1000000, 1e-300, 1);
     cudaStream_t s = P.stream;
@@ -3348,6 +3470,16 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     SKNR_API_END
 }
 
+// Diagnostics: the first 16 entries of the handle's reduction scratch (sums of the last
+// stopping test / acceptance test / gauge).
+int sknr_debug_sums(sknr_problem h, double* out) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    CK(cudaMemcpyAsync(out, P.sums.p, sizeof(double) * 16, cudaMemcpyDeviceToHost, P.stream));
+    CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
 // Diagnostics: [exact col, exact row, retry col, retry row] counters since creation.
 int sknr_debug_counters(sknr_problem h, int64_t* out) {
     SKNR_API_BEGIN
@@ -3420,8 +3552,20 @@ int sknr_comm_init(int rank, int world, const unsigned char id[128], int device)
     SKNR_API_END
 }
 
+// Testing: an in-process group of `world` emulated ranks on the current GPU (see
+// EmuGroup). Shards created afterwards route their collectives through it; each
+// rank's calls must come from its own host thread.
+int sknr_comm_init_emulated(int world) {
+    SKNR_API_BEGIN
+    if (world < 1 || world > kEmuMax) throw InvalidArgument("sknr_comm_init_emulated: 1 <= world <= 16 required");
+    check_device();
+    g_emu.init(world);
+    SKNR_API_END
+}
+
 int sknr_comm_destroy(void) {
     SKNR_API_BEGIN
+    g_emu.destroy();
     if (g_comm.comm) {
         g_nccl.CommDestroy(g_comm.comm);
         g_comm.comm = nullptr;
@@ -3437,11 +3581,20 @@ int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    if (!g_comm.comm) throw RuntimeFailure("sknr_problem_shard: call sknr_comm_init first");
+    const bool emu = g_emu.world > 0;
+    if (!g_comm.comm && !emu) throw RuntimeFailure("sknr_problem_shard: call sknr_comm_init first");
     if (P.shard) throw InvalidArgument("sknr_problem_shard: problem already sharded");
-    int64_t b, e;
-    row_partition(P.n_global, g_comm.world, g_comm.rank, b, e);
-    if (row_begin != b || row_end != e)
+    const int world = emu ? g_emu.world : g_comm.world;
+    int rank = emu ? -1 : g_comm.rank;
+    if (emu)  // the emulated rank is the one whose standard block this is
+        for (int r = 0; r < world; ++r) {
+            int64_t rb, re;
+            row_partition(P.n_global, world, r, rb, re);
+            if (rb == row_begin && re == row_end) rank = r;
+        }
+    int64_t b = 0, e = 0;
+    if (rank >= 0) row_partition(P.n_global, world, rank, b, e);
+    if (rank < 0 || row_begin != b || row_end != e)
         throw InvalidArgument("sknr_problem_shard: rows must follow the standard partition [n*r/R, n*(r+1)/R)");
     const int64_t nl = e - b, n = P.n_global, m = P.m;
     if (nl < 1) throw InvalidArgument("sknr_problem_shard: empty row block");
@@ -3479,6 +3632,9 @@ int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
     P.n = nl;
     P.row_begin = b;
     P.shard = true;
+    P.emu = emu;
+    P.rank = rank;
+    P.world = world;
     P.plans.clear();
     count_launch();
     k_invalidate_refs<<<1, 32, 0, s>>>(P.st);

@@ -365,3 +365,43 @@ def test_culled_anneal_and_batch_match_dense():
     ref = sk.solve(pd.with_epsilon(inst.epsilons[3]), tol=1e-9)
     for r in rb:
         assert r.iterations == ref.iterations and rel_err(r.f, ref.f) <= 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_path_across_R_matches_unsharded(world):
+    """SURVEY 8(e) parity across R on one GPU: R emulated ranks (in-process collectives,
+    one host thread per rank) run the row-sharded SK and SK-NR solves and top_modes;
+    identical iteration counts and potentials within 1e-12 of the unsharded runs."""
+    inst = G.config("C1", n=601, m=433)  # ragged row blocks for every R
+    a = np.full(601, 1 / 601)
+    b = np.full(433, 1 / 433)
+    mk = lambda: sk.PointProblem(inst.x, inst.y, a, b, inst.epsilon)
+    ref_sk = sk.solve(mk(), tol=1e-9)
+    warm = sk.solve(mk().with_epsilon(inst.basis_eps), tol=1e-10)
+    basis = sk.top_modes(mk().with_epsilon(inst.basis_eps), warm.f, warm.g, 6)
+    ref_nr = sk.solve(mk(), tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g))
+    ref_tm = sk.top_modes(mk(), ref_sk.f, ref_sk.g, 6)
+    sched = [0.05, 0.025, 0.0125]
+    ref_an = sk.anneal(mk(), sched, warm="spectral", ell=4)
+    out = sk.run_emulated_shards(mk, world, lambda p: (
+        sk.solve(p, tol=1e-9),
+        sk.solve(p, tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g)),
+        sk.top_modes(p, ref_sk.f, ref_sk.g, 6),
+        sk.anneal(p, sched, warm="spectral", ell=4)))
+    for _, _, _, an in out:
+        assert [s.iterations for s in an] == [s.iterations for s in ref_an]
+        assert all(rel_err(s.f, q.f) <= TOL_NR for s, q in zip(an, ref_an))
+    out = [o[:3] for o in out]
+    for r_sk, r_nr, tm in out:
+        assert r_sk.iterations == ref_sk.iterations
+        assert rel_err(r_sk.f, ref_sk.f) <= 1e-12 and rel_err(r_sk.g, ref_sk.g) <= 1e-12
+        assert r_nr.iterations == ref_nr.iterations
+        assert rel_err(r_nr.f, ref_nr.f) <= TOL_NR
+        assert rel_err(tm.rhos, ref_tm.rhos) <= 1e-8
+        assert sk.projector_distance(tm, ref_tm) <= 1e-6
+    # every rank returns the same full-length potentials
+    for r_sk, r_nr, _ in out[1:]:
+        assert np.array_equal(r_sk.f, out[0][0].f) and np.array_equal(r_nr.g, out[0][1].g)
+
+
+TOL_NR = 2e-8  # accept decisions at the rounding level (as TOL_POT_NEWTON in test_gpu_parity)
