@@ -86,8 +86,8 @@ int sknr_problem_destroy(sknr_problem p);
  * reference): both clouds are visited in Morton order and a (64-input group,
  * 256-output group) pair is skipped when a rigorous bound puts every one of its
  * terms below e^-threshold of the output's total (threshold >= 40, typically 60;
- * 0 turns culling off). Point clouds with d <= 4, unsharded. The sums change by
- * less than n e^-threshold relative (< 1e-21 at 60). */
+ * 0 turns culling off). Point clouds with d <= 4 (sharded handles cull their own
+ * rows). The sums change by less than n e^-threshold relative (< 1e-21 at 60). */
 int sknr_problem_set_culling(sknr_problem p, double threshold);
 
 /* ---------------------------------------------------------------- core.hpp

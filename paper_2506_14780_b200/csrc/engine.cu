@@ -1043,7 +1043,7 @@ static TileArgs tile_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
 // Culled column/row LSE (opt-in): register point kernels, unsharded, large enough
 // for whole cull tiles.
 static bool cull_active(const Problem& P, int dir) {
-    if (!(P.cull_t > 0.0) || !P.cull_ready || P.shard || P.dim < 1 || P.dim > 4) return false;
+    if (!(P.cull_t > 0.0) || !P.cull_ready || P.dim < 1 || P.dim > 4) return false;
     const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
     return nout >= 8 * CULL_GO && nin >= 4 * CULL_GI;
 }
@@ -1076,7 +1076,7 @@ static void cull_group_max(Problem& P, const Side& side, const double* pack, dou
 
 // Culled block pass (opt-in): same conditions as the culled LSE, sizes above one work unit.
 static bool cull_block_active(const Problem& P, int dir) {
-    if (!(P.cull_t > 0.0) || !P.cull_ready || P.shard || P.dim < 1 || P.dim > 4) return false;
+    if (!(P.cull_t > 0.0) || !P.cull_ready || P.dim < 1 || P.dim > 4) return false;
     const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
     return nout >= 1024 && nin >= 1024;
 }
@@ -2502,7 +2502,6 @@ int sknr_problem_set_culling(sknr_problem h, double threshold) {
         if (threshold < 40.0) throw InvalidArgument("set_culling: threshold below 40 would perturb the sums");
         if (P.dim < 1 || P.dim > 4)
             throw InvalidArgument("set_culling: needs a point-cloud problem with d <= 4");
-        if (P.shard) throw InvalidArgument("set_culling: not available on a row-sharded problem");
         prepare_culling(P);
     }
     P.cull_t = threshold;
@@ -3636,6 +3635,10 @@ int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
     P.rank = rank;
     P.world = world;
     P.plans.clear();
+    if (P.cull_ready) {  // re-derive the Morton order and group boxes for the local rows
+        P.cull_ready = false;
+        prepare_culling(P);
+    }
     count_launch();
     k_invalidate_refs<<<1, 32, 0, s>>>(P.st);
     CK(cudaStreamSynchronize(s));

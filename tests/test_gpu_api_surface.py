@@ -405,3 +405,20 @@ def test_sharded_path_across_R_matches_unsharded(world):
 
 
 TOL_NR = 2e-8  # accept decisions at the rounding level (as TOL_POT_NEWTON in test_gpu_parity)
+
+
+def test_culled_sharded_sk_matches_dense_unsharded():
+    """Culling on row-sharded handles (each rank culls its own rows against the global
+    LSE bound), R = 4 emulated ranks."""
+    c = G.config("C4", n=8192, m=8192)
+    mk = lambda: sk.PointProblem(c.x, c.y, c.alpha, c.beta, 2e-3)
+    ref = sk.solve(mk(), tol=1e-9)
+
+    def run(p):
+        p.set_culling(60.0)
+        return sk.solve(p, tol=1e-9)
+
+    out = sk.run_emulated_shards(mk, 4, run)
+    for r in out:
+        assert r.iterations == ref.iterations
+        assert rel_err(r.f, ref.f) <= 1e-12 and rel_err(r.g, ref.g) <= 1e-12
