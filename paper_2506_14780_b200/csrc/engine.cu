@@ -364,9 +364,15 @@ __global__ void k_select(double* f, const double* fcand, int64_t n, double* gnex
     }
 }
 
-__global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled) {
+// End of an iteration: trace record, max_iter stop and -- when the solve runs as a
+// device-side WHILE loop (conditional graph node) -- the loop condition.
+__global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled,
+                         cudaGraphConditionalHandle loop) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (!st->iter_active) return;
+    if (!st->iter_active) {
+        if (loop) cudaGraphSetConditional(loop, 0);
+        return;
+    }
     st->iter_active = 0;
     const long long k = st->iter;
     if (trace_enabled && k - 1 < cap) {
@@ -382,6 +388,7 @@ __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int tr
         trace[k - 1] = r;
     }
     if (k >= st->max_iter) st->done = 1;
+    if (loop) cudaGraphSetConditional(loop, st->done ? 0 : 1);
 }
 
 __global__ void k_axpby(const double* x, const double* y, int64_t n, double a, double b, double* out) {
@@ -1875,7 +1882,8 @@ struct SolveOut {
 
 // Enqueue one SK-NR(ell) iteration (solver.cpp:104-151).
 static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace_enabled,
-                              int64_t trace_cap, bool exact_marginals = false) {
+                              int64_t trace_cap, bool exact_marginals = false,
+                              cudaGraphConditionalHandle loop = 0) {
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     const bool newton = ell > 0;
@@ -2055,7 +2063,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
     }
     count_launch();
     k_record<<<1, 32, 0, s>>>(P.st, reinterpret_cast<sknr_record*>(S.trace_raw.p), trace_cap,
-                              trace_enabled ? 1 : 0);
+                              trace_enabled ? 1 : 0, loop);
     CK(cudaGetLastError());
 }
 
@@ -2128,7 +2136,27 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     cudaStream_t s = P.stream;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    if (!P.emu) {
+    if (!P.shard) {
+        // the whole solve as one graph: a WHILE node whose body is one iteration;
+        // k_record clears the loop condition once the stopping test (or max_iter) hits
+        CK(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle loop = 0;
+        CK(cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = loop;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, loop);
+        CK(cudaStreamEndCapture(s, &body));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        CK(cudaGraphLaunch(exec, s));
+        CK(cudaStreamSynchronize(s));
+    } else if (!P.emu) {
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
         CK(cudaStreamEndCapture(s, &graph));
@@ -2136,7 +2164,7 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     }
     int64_t batch = 1;
     int64_t launched = 0;
-    while (true) {
+    while (P.shard) {  // sharded (NCCL in the graph) and emulated shards: host-polled batches
         for (int64_t b = 0; b < batch; ++b) {
             if (exec)
                 CK(cudaGraphLaunch(exec, s));
@@ -2169,13 +2197,12 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     return out;
 }
 
-// Batched solve: B independent problems advance together,
-// one CUDA graph per iteration whose B branches (one per problem stream, forked
-// from and joined to an origin stream) run concurrently on the GPU. Problems may
-// differ in size and cost kind; each keeps its own device state, so a finished
-// problem's branch turns into guarded no-op kernels until the slowest converges.
-// Every branch issues exactly the kernels of run_solve, so per-problem results
-// are bitwise identical to solving the problems one by one.
+// Batched solve: B independent problems in one CUDA graph,
+// each as its own device-side WHILE loop (conditional node) over its iteration
+// body, so the loops run concurrently and each stops at its own stopping test.
+// Problems may differ in size and cost kind; every body issues exactly the
+// kernels of run_solve, so per-problem results are bitwise identical to solving
+// the problems one by one.
 struct BatchItem {
     Problem* P = nullptr;
     const double* basis = nullptr;
@@ -2201,38 +2228,33 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
     }
     cudaStream_t s0 = nullptr;
     CK(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev(B + 1, nullptr);
-    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::vector<SolveOut> out(B);
     try {
-        CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
-        CK(cudaEventRecord(ev[B], s0));
+        // one graph, one independent device-side WHILE loop per problem (conditional
+        // nodes without dependencies between them): each problem iterates until its own
+        // stopping test, none waits for the others
+        CK(cudaGraphCreate(&graph, 0));
         for (size_t b = 0; b < B; ++b) {
             Problem& P = *items[b].P;
-            CK(cudaStreamWaitEvent(P.stream, ev[B], 0));
-            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals);
-            CK(cudaEventRecord(ev[b], P.stream));
-            CK(cudaStreamWaitEvent(s0, ev[b], 0));
+            cudaGraphConditionalHandle loop = 0;
+            CK(cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = loop;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            CK(cudaStreamBeginCaptureToGraph(P.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals, loop);
+            CK(cudaStreamEndCapture(P.stream, &body));
         }
-        CK(cudaStreamEndCapture(s0, &graph));
         CK(cudaGraphInstantiate(&exec, graph, 0));
-        int64_t batch = 1, launched = 0;
-        while (true) {
-            for (int64_t k = 0; k < batch; ++k) {
-                CK(cudaGraphLaunch(exec, s0));
-                ++launched;
-            }
-            for (size_t b = 0; b < B; ++b)
-                CK(cudaMemcpyAsync(items[b].P->st_host, items[b].P->st, sizeof(DevState), cudaMemcpyDeviceToHost,
-                                   s0));
-            CK(cudaStreamSynchronize(s0));
-            bool all = true;
-            for (size_t b = 0; b < B; ++b) all = all && items[b].P->st_host->done != 0;
-            if (all || launched >= max_iter + 2) break;
-            batch = std::min<int64_t>(batch * 2, 64);
-        }
+        CK(cudaGraphLaunch(exec, s0));
+        CK(cudaStreamSynchronize(s0));
         for (size_t b = 0; b < B; ++b) {
             Problem& P = *items[b].P;
             out[b].f.resize(P.n_global);
@@ -2250,13 +2272,11 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
     } catch (...) {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
-        for (auto& e : ev) cudaEventDestroy(e);
         cudaStreamDestroy(s0);
         throw;
     }
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
-    for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(s0);
     return out;
 }
