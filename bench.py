@@ -291,11 +291,11 @@ def run_ours(args, world, rank, local):
                                         flush_l2=True)
 
     # ---- e2e: public C ABI with host buffers (problem upload + solve + potentials download)
-    # Three complete runs (each: new problem from host arrays, K iterations, download);
-    # the median is reported, all three are listed (host-side allocation/clock jitter).
+    # Five complete runs (each: new problem from host arrays, K iterations, download);
+    # the median is reported, all five are listed (host-side allocation jitter).
     k_e2e = max(args.steps, 1)
     runs = []
-    for _ in range(3):
+    for _ in range(5):
         barrier(dist)
         t0 = time.perf_counter()
         p2 = make_problem()
@@ -308,7 +308,7 @@ def run_ours(args, world, rank, local):
     h2d = (inst.x.nbytes + inst.y.nbytes + inst.alpha.nbytes + inst.beta.nbytes) / k_e2e
     d2h = (res.f.nbytes + res.g.nbytes) / k_e2e
     e2e = {"value": 2.0 * cells * k_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "steps": k_e2e, "runs_s": runs, "statistic": "median of 3 runs",
+           "d2h_bytes_per_step": d2h, "steps": k_e2e, "runs_s": runs, "statistic": "median of 5 runs",
            "path": "PointProblem(host arrays) + sknr_solve(max_iter=K) + f,g download, wall clock"}
 
     # ---- time to tolerance: C1 (reference basis method) and C3 (Chebyshev-filtered basis)
