@@ -142,10 +142,11 @@ int sknr_spectrum_report(sknr_problem p, const double* f, const double* g, int64
 /* projector_distance (spectral.cpp:230-242) between two n x k symmetrized bases. */
 int sknr_projector_distance(int64_t n, int64_t k, const double* a_sym, const double* b_sym, double* out);
 
-/* Opt-in accelerated variant (not in the reference): method 1 = Chebyshev-
- * filtered subspace iteration of polynomial degree `degree` (same Rayleigh-Ritz,
- * same residual test, same returned basis semantics); method 0 = top_modes.
- * `sweeps` counts operator applications R~R~^T in both cases. */
+/* Opt-in accelerated variants (not in the reference): method 1 = Chebyshev-
+ * filtered subspace iteration of polynomial degree `degree`; method 2 = restarted
+ * block Lanczos with `degree` blocks per cycle (full reorthogonalisation). Same
+ * residual test and returned basis semantics as method 0 (= top_modes). `sweeps`
+ * counts operator applications R~R~^T. */
 int sknr_top_modes_ex(sknr_problem p, const double* f, const double* g, int64_t ell, double tol,
                       int64_t max_power_iters, int method, int degree, double* vectors,
                       double* vectors_sym, double* rhos, int64_t* sweeps);

@@ -603,7 +603,9 @@ def top_modes(problem: Problem, f, g, ell: int, tol: float = 1e-8,
     """top_modes (spectral.cpp:125-193). method="subspace" is the reference's block
     subspace iteration; method="chebyshev" (opt-in, not in the reference) filters
     each step with a degree-`degree` Chebyshev polynomial -- same Rayleigh-Ritz,
-    same residual criterion, far fewer operator applications on clustered spectra."""
+    same residual criterion, far fewer operator applications on clustered spectra;
+    method="lanczos" (opt-in) runs restarted block Lanczos with `degree` blocks per
+    cycle and the same explicit residual test."""
     f = _checked(f, problem.n, "SinkhornOperator(f)")
     g = _checked(g, problem.m, "SinkhornOperator(g)")
     ell = int(ell)
@@ -615,9 +617,9 @@ def top_modes(problem: Problem, f, g, ell: int, tol: float = 1e-8,
     vsym = np.empty((problem.n, ell), order="F")
     rhos = np.empty(ell)
     sweeps = _I64()
-    methods = {"subspace": 0, "chebyshev": 1}
+    methods = {"subspace": 0, "chebyshev": 1, "lanczos": 2}
     if method not in methods:
-        raise ValueError("top_modes: method must be subspace|chebyshev")
+        raise ValueError("top_modes: method must be subspace|chebyshev|lanczos")
     _check(lib().sknr_top_modes_ex(problem.handle, _ptr(f), _ptr(g), ell, float(tol), int(max_power_iters),
                                    methods[method], int(degree), _ptr(vec), _ptr(vsym), _ptr(rhos),
                                    ctypes.byref(sweeps)))

@@ -360,6 +360,19 @@ def test_exact_marginals_mode_matches_fused_and_oracle():
         assert abs(a.marginal_error - c[0]) <= 1e-6 * c[0] + 1e-15
 
 
+def test_lanczos_top_modes_matches_subspace():
+    """Opt-in restarted block Lanczos: same Ritz values and subspace as the
+    reference's block subspace iteration, far fewer operator applications."""
+    inst = G.config("C1")
+    gp = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.basis_eps)
+    w = sk.solve(gp, tol=1e-10)
+    b0 = sk.top_modes(gp, w.f, w.g, inst.ell)
+    b2 = sk.top_modes(gp, w.f, w.g, inst.ell, method="lanczos", degree=12)
+    assert rel_err(b2.rhos, b0.rhos) <= 1e-9
+    assert sk.projector_distance(b2, b0) <= 1e-6
+    assert b2.sweeps < b0.sweeps
+
+
 def test_chebyshev_top_modes_matches_subspace():
     """Opt-in Chebyshev filtering returns the same basis (same residual test) with
     fewer operator applications."""
