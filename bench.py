@@ -345,6 +345,18 @@ def run_ours(args, world, rank, local):
                              "basis_operator_applications": b1.sweeps, "basis_ms": t_basis * 1e3}}
 
         ttt = {"C1": ttt_case("C1", "subspace"), "C3": ttt_case("C3", "chebyshev")}
+        # C2 (BASELINE configs[1]): the reference's anneal driver, eps 0.1 -> 0.001 halving,
+        # spectral warm start, ell = 16, refresh_basis = false (solver.hpp:44)
+        c2 = G.config("C2")
+        p2c = sk.PointProblem(c2.x, c2.y, c2.alpha, c2.beta, c2.epsilons[0], c2.cost_scale)
+        t0 = time.perf_counter()
+        stages = sk.anneal(p2c, list(c2.epsilons), warm="spectral", ell=c2.ell)
+        t_an = time.perf_counter() - t0
+        ttt["C2_anneal"] = {"n": c2.n, "m": c2.m, "epsilons": list(c2.epsilons), "ell": c2.ell, "tol": 1e-9,
+                            "warm": "spectral", "ms_total": t_an * 1e3,
+                            "iterations": [s.iterations for s in stages],
+                            "converged": all(s.converged for s in stages)}
+        del p2c
         if not args.no_c4_ttt:
             ttt["C4"] = ttt_case("C4", "chebyshev", degree=16)
             ttt["C4_culled"] = ttt_case("C4", "chebyshev", cull=60.0, degree=16)
