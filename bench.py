@@ -377,7 +377,20 @@ def run_ours(args, world, rank, local):
         t0 = time.perf_counter()
         r1 = [sk.solve(p, tol=1e-9, trace=False) for p in probs[:8]]
         t_1 = (time.perf_counter() - t0) / 8
+        # one CTA per problem, whole SK loop in one kernel (sknr_solve_small_batch): 148 instances
+        tup = []
+        for s in range(148):
+            c = G.config("C1", seed=1 + s)
+            tup.append((c.x, c.y, c.alpha, c.beta, c.epsilon))
+        sk.solve_small_batch(tup[:2], tol=1e-9)
+        t0 = time.perf_counter()
+        rsm = sk.solve_small_batch(tup, tol=1e-9)
+        t_sm = time.perf_counter() - t0
+        small = {"problems": len(tup), "ms": t_sm * 1e3, "solves_per_s": len(tup) / t_sm,
+                 "all_converged": all(r.converged for r in rsm),
+                 "iterations_equal_first32": all(a.iterations == b.iterations for a, b in zip(rsm, rb))}
         batch = {"problems": len(probs), "config": "C1 seeds 1..32, SK (ell=0) to marginal error 1e-9",
+                 "small_problem_kernel": small,
                  "ms_batch": t_b * 1e3, "solves_per_s": len(probs) / t_b, "ms_per_solve_one_by_one": t_1 * 1e3,
                  "speedup_vs_one_by_one": t_1 * len(probs) / t_b,
                  "all_converged": all(r.converged for r in rb),

@@ -196,6 +196,18 @@ int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_con
                      const double* const* init_g, double* const* f_out, double* const* g_out,
                      int64_t* iterations, int* converged);
 
+/* Small-problem batch (not in the reference): `count` point-cloud problems of one
+ * dimension d <= 4 with n, m <= 2048, each solved by plain SK (ell = 0) from f = 0
+ * to tol inside one CTA of a single kernel launch (no launch per iteration). Per
+ * problem q: n[q], m[q], x[q] (n x d), y[q] (m x d), a[q], b[q], eps[q],
+ * cost_scale[q] (NULL: 1); outputs f_out[q], g_out[q], iterations[q], converged[q].
+ * Same iteration and stopping test as sknr_solve; sums in a different order. */
+int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int64_t* m,
+                           const double* const* x, const double* const* y, const double* const* a,
+                           const double* const* b, const double* eps, const double* cost_scale,
+                           double tol, int64_t max_iter, double* const* f_out, double* const* g_out,
+                           int64_t* iterations, int* converged);
+
 /* newton_step (solver.cpp:59-69, try_newton :30-56): one restricted Newton step
  * from f with basis vectors (n x ell). f_out = accepted ? f + V delta : f. */
 int sknr_newton_step(sknr_problem p, const double* f, const double* vectors, int64_t ell, double* f_out,

@@ -89,6 +89,10 @@ _SIGS = {
     "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
     "sknr_coupling": [_P, _D, _D, _D],
     "sknr_coupling_rows": [_P, _D, _D, _I64, _I64, _D],
+    "sknr_solve_small_batch": [_I64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_D),
+                               ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D), _D, _D, ctypes.c_double,
+                               _I64, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64),
+                               ctypes.POINTER(ctypes.c_int)],
     "sknr_solve_batch": [ctypes.POINTER(_P), _I64, ctypes.POINTER(_Config), ctypes.POINTER(_D), _I64,
                          ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D),
                          ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int)],
@@ -793,6 +797,59 @@ def solve_batch(problems: Sequence[Problem], tol: float = 1e-9, max_iter: int = 
     return [SolveResult(fo[b], go[b], bool(conv[b]), int(iters[b]), [], problems[b]) for b in range(B)]
 
 
+def solve_small_batch(problems, tol: float = 1e-9, max_iter: int = 100000) -> list:
+    """Plain SK (ell = 0, from f = 0) for many small point-cloud problems in ONE kernel
+    launch, one CTA per problem (n, m <= 2048, one dimension d <= 4). `problems` holds
+    PointProblem objects or (x, y, alpha, beta, epsilon[, cost_scale]) tuples. Same
+    iteration and stopping test as solve(); reductions run in a different order, so
+    potentials agree with solve() to rounding, not bit for bit. Not in the reference."""
+    items = []
+    for p in problems:
+        if isinstance(p, PointProblem):
+            items.append((p._x, p._y, p._alpha, p._beta, p.epsilon, p._cost_scale))
+        else:
+            x, y, a, b, e = p[:5]
+            items.append((_mat_f(x), _mat_f(y), _vec(a), _vec(b), float(e), float(p[5]) if len(p) > 5 else 1.0))
+    B = len(items)
+    if B < 1:
+        raise ValueError("solve_small_batch: empty batch")
+    d = items[0][0].shape[1] if items[0][0].ndim == 2 else 1
+    keep = []
+
+    def col(a):
+        a = _mat_f(a)
+        if a.ndim == 1:
+            a = a.reshape(-1, 1, order="F")
+        keep.append(a)
+        return a
+
+    xs = [col(it[0]) for it in items]
+    ys = [col(it[1]) for it in items]
+    for x_, y_ in zip(xs, ys):
+        if x_.shape[1] != d or y_.shape[1] != d:
+            raise ValueError("solve_small_batch: all problems need the same dimension")
+    n = (_I64 * B)(*[x_.shape[0] for x_ in xs])
+    m = (_I64 * B)(*[y_.shape[0] for y_ in ys])
+    av = [_vec(it[2]) for it in items]
+    bv = [_vec(it[3]) for it in items]
+    eps = np.array([it[4] for it in items], dtype=np.float64)
+    cs = np.array([it[5] for it in items], dtype=np.float64)
+    fo = [np.empty(x_.shape[0]) for x_ in xs]
+    go = [np.empty(y_.shape[0]) for y_ in ys]
+
+    def arr(vals):
+        out = (_D * B)()
+        for k, v in enumerate(vals):
+            out[k] = _ptr(v)
+        return out
+
+    iters = (_I64 * B)()
+    conv = (ctypes.c_int * B)()
+    _check(lib().sknr_solve_small_batch(B, d, n, m, arr(xs), arr(ys), arr(av), arr(bv), _ptr(eps), _ptr(cs),
+                                        float(tol), int(max_iter), arr(fo), arr(go), iters, conv))
+    return [SolveResult(fo[k], go[k], bool(conv[k]), int(iters[k]), []) for k in range(B)]
+
+
 def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", ell: int = 8,
            refresh_basis: bool = False, tol: float = 1e-9, max_iter: int = 100000) -> list:
     """Epsilon-annealing driver (solver.cpp:158-222)."""
@@ -967,7 +1024,7 @@ __all__ = [
     "SpectralBasis", "__version__", "anneal", "apply_K", "apply_R", "apply_Rt", "apply_sym_block",
     "apply_sym_t_block", "coupling", "coupling_rows", "ctransform_of_f", "dual_value", "gauge_distance",
     "gauge_normalized", "marginal_gap", "newton_step", "projector_distance", "semi_dual_hessian_quadform",
-    "sk_sweep", "solve_batch", "spectrum", "oracle_solve", "gaussian_cloud", "sq_euclidean_cost",
+    "sk_sweep", "solve_batch", "solve_small_batch", "spectrum", "oracle_solve", "gaussian_cloud", "sq_euclidean_cost",
     "ctransform_of_g", "kernel_launch_count", "lib", "log_sum_exp", "marginal_error", "osc_norm",
     "plan_marginals", "restricted_derivatives", "comm_init", "comm_unique_id", "comm_destroy",
     "row_partition", "shard", "comm_init_emulated", "run_emulated_shards", "semi_dual_gradient", "semi_dual_value", "solve",

@@ -3423,6 +3423,81 @@ int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_con
     SKNR_API_END
 }
 
+// Small-problem batch: every problem solved by plain SK (ell = 0) from f = 0 inside one
+// CTA of one kernel launch (launch_sk_small); point clouds of one dimension d <= 4 with
+// n, m <= 2048 each. Problems may differ in n, m, epsilon and cost scale.
+int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int64_t* m, const double* const* x,
+                           const double* const* y, const double* const* a, const double* const* b,
+                           const double* eps, const double* cost_scale, double tol, int64_t max_iter,
+                           double* const* f_out, double* const* g_out, int64_t* iterations, int* converged) {
+    SKNR_API_BEGIN
+    check_device();
+    if (count < 1) throw InvalidArgument("solve_small_batch: empty batch");
+    if (d < 1 || d > 4) throw InvalidArgument("solve_small_batch: 1 <= d <= 4 required");
+    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
+    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
+    if (!n || !m || !x || !y || !a || !b || !eps || !f_out || !g_out)
+        throw InvalidArgument("solve_small_batch: null pointer");
+    // one device arena: per problem x (n d), y (m d), a (n), b (m), f (n), g (m), h (m)
+    std::vector<size_t> off(static_cast<size_t>(count) + 1, 0);
+    for (int64_t q = 0; q < count; ++q) {
+        if (n[q] < 1 || m[q] < 1 || n[q] > kSmallMax || m[q] > kSmallMax)
+            throw InvalidArgument("solve_small_batch: 1 <= n, m <= 2048 required");
+        if (!(eps[q] > 0.0)) throw InvalidArgument("EotProblem: epsilon must be positive");
+        validate_measure(a[q], n[q]);
+        validate_measure(b[q], m[q]);
+        off[q + 1] = off[q] + static_cast<size_t>((n[q] + m[q]) * d + 2 * n[q] + 3 * m[q]);
+    }
+    DBuf arena, dprobs;
+    arena.ensure(off[count]);
+    std::vector<SmallProbDev> hp(static_cast<size_t>(count));
+    std::vector<double> host(off[count], 0.0);
+    for (int64_t q = 0; q < count; ++q) {
+        double* base = host.data() + off[q];
+        const int64_t nq = n[q], mq = m[q];
+        std::memcpy(base, x[q], sizeof(double) * nq * d);
+        std::memcpy(base + nq * d, y[q], sizeof(double) * mq * d);
+        std::memcpy(base + (nq + mq) * d, a[q], sizeof(double) * nq);
+        std::memcpy(base + (nq + mq) * d + nq, b[q], sizeof(double) * mq);
+        double* dev = arena.p + off[q];
+        SmallProbDev& s = hp[q];
+        s.x = dev;
+        s.y = dev + nq * d;
+        s.a = dev + (nq + mq) * d;
+        s.b = s.a + nq;
+        s.f = const_cast<double*>(s.b) + mq;  // zero-filled: SK from f = 0
+        s.g = s.f + nq;
+        s.h = s.g + mq;
+        s.n = static_cast<int>(nq);
+        s.m = static_cast<int>(mq);
+        s.eps = eps[q];
+        s.kappa = cost_scale ? cost_scale[q] : 1.0;
+    }
+    const size_t words = (sizeof(SmallProbDev) * static_cast<size_t>(count) + sizeof(double) - 1) / sizeof(double);
+    dprobs.ensure(words);
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaMemcpyAsync(arena.p, host.data(), sizeof(double) * off[count], cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dprobs.p, hp.data(), sizeof(SmallProbDev) * count, cudaMemcpyHostToDevice, s));
+    launch_sk_small(static_cast<int>(d), reinterpret_cast<SmallProbDev*>(dprobs.p), static_cast<int>(count), tol,
+                    max_iter, 0, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host.data(), arena.p, sizeof(double) * off[count], cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp.data(), dprobs.p, sizeof(SmallProbDev) * count, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+    for (int64_t q = 0; q < count; ++q) {
+        const double* base = host.data() + off[q];
+        const int64_t nq = n[q], mq = m[q];
+        const double* fq = base + (nq + mq) * d + nq + mq;
+        std::memcpy(f_out[q], fq, sizeof(double) * nq);
+        std::memcpy(g_out[q], fq + nq, sizeof(double) * mq);
+        if (iterations) iterations[q] = hp[q].iters;
+        if (converged) converged[q] = hp[q].conv;
+    }
+    SKNR_API_END
+}
+
 int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm_mode, int refresh_basis,
                 const sknr_config* cfg, double* f_out, double* g_out, int64_t* iterations, int* converged,
                 sknr_record* trace, int64_t trace_cap, int64_t* trace_offsets, int64_t* trace_len) {

@@ -65,4 +65,18 @@ int chunk_inputs(int mode, int kt);
 void count_launch();
 int64_t launch_count();
 
+// Small-problem batch (sknr_solve_small_batch): one CTA runs a whole SK solve of one
+// point-cloud problem (n, m <= kSmallMax, d <= 4) with __syncthreads only.
+constexpr int kSmallMax = 2048;
+struct SmallProbDev {
+    const double *x = nullptr, *y = nullptr, *a = nullptr, *b = nullptr;  // col-major coords, weights
+    double *f = nullptr, *g = nullptr, *h = nullptr;                     // potentials (f, g in/out), scratch
+    int n = 0, m = 0;
+    double eps = 1.0, kappa = 1.0;
+    long long iters = 0;
+    int conv = 0;
+};
+void launch_sk_small(int d, SmallProbDev* probs, int count, double tol, long long max_iter, int warm_g,
+                     cudaStream_t s);
+
 }  // namespace sknr

@@ -285,6 +285,149 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
     }
 }
 
+// ------------------------------------------------------------- small-problem batched SK
+// One CTA = one problem, the whole solve loop inside the kernel (no launches per
+// iteration): inputs of each log-sum-exp staged in shared memory, one warp per output,
+// lanes over the inputs, exact max shift then sum (core.cpp:35-82), warp-shuffle and
+// fixed-order block reductions (deterministic). Same iteration as the device loop:
+// row LSE -> gauge (solver.cpp:108-112) -> column LSE -> marginal gap -> stop test.
+template <int D>
+__device__ __forceinline__ double small_lse(const double* __restrict__ sp, int cnt, const double* yo, double ke,
+                                            const unsigned long long* __restrict__ tab, unsigned laneoff,
+                                            double c3, int lane) {
+    constexpr int P = D + 1;
+    double mx = -1e300;
+    for (int k = lane; k < cnt; k += 32) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const double t = sp[k * P + 1 + d] - yo[d];
+            d2 = fma(t, t, d2);
+        }
+        mx = fmax(mx, sp[k * P] - ke * d2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double s = 0.0;
+    for (int k = lane; k < cnt; k += 32) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const double t = sp[k * P + 1 + d] - yo[d];
+            d2 = fma(t, t, d2);
+        }
+        s = pexp_acc<true>(kLS * (sp[k * P] - ke * d2 - mx), tab, laneoff, c3, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return mx + log(s);
+}
+
+__device__ __forceinline__ double small_block_sum(double v, double* red, int tid, int nthreads) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nthreads / 32; ++w) t += red[w];  // same order in every thread
+    return t;
+}
+
+template <int D>
+__global__ void __launch_bounds__(512, 1)
+    k_sk_small(SmallProbDev* probs, double tol, long long max_iter, int warm_g) {
+    constexpr int P = D + 1;
+    constexpr int NT = 512;
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* red = sm + kTabWords;
+    double* sp = red + 64;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_exp2_table(tab, tid, NT);
+    const unsigned laneoff = (tid & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+    SmallProbDev& pr = probs[blockIdx.x];
+    const int n = pr.n, m = pr.m;
+    const double eps = pr.eps, ie = 1.0 / eps, ke = pr.kappa * ie;
+    double* f = pr.f;
+    double* g = pr.g;
+    double* h = pr.h;
+    // column LSE at f into h (ctransform_of_f): inputs i (la_i + f_i/eps, x_i), outputs j
+    auto col_lse = [&]() {
+        __syncthreads();
+        for (int i = tid; i < n; i += NT) {
+            sp[i * P] = log(pr.a[i]) + f[i] * ie;
+#pragma unroll
+            for (int d = 0; d < D; ++d) sp[i * P + 1 + d] = pr.x[i + d * n];
+        }
+        __syncthreads();
+        for (int j = warp; j < m; j += NT / 32) {
+            double yo[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) yo[d] = pr.y[j + d * m];
+            const double L = small_lse<D>(sp, n, yo, ke, tab, laneoff, c3, lane);
+            if (lane == 0) h[j] = -eps * L;
+        }
+        __syncthreads();
+    };
+    if (!warm_g) {  // first sweep's g = f0^{C,eps}
+        col_lse();
+        for (int j = tid; j < m; j += NT) g[j] = h[j];
+    }
+    long long it = 0;
+    int conv = 0;
+    while (it < max_iter) {
+        ++it;
+        // row LSE at g (ctransform_of_g): f_i = -eps L_i; row residual a_i expm1(f_i/eps + L_i)
+        __syncthreads();
+        for (int j = tid; j < m; j += NT) {
+            sp[j * P] = log(pr.b[j]) + g[j] * ie;
+#pragma unroll
+            for (int d = 0; d < D; ++d) sp[j * P + 1 + d] = pr.y[j + d * m];
+        }
+        __syncthreads();
+        double rsq = 0.0, af = 0.0;
+        for (int i = warp; i < n; i += NT / 32) {
+            double xo[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) xo[d] = pr.x[i + d * n];
+            const double L = small_lse<D>(sp, m, xo, ke, tab, laneoff, c3, lane);
+            if (lane == 0) {
+                const double fi = -eps * L;
+                const double rr = pr.a[i] * expm1(fi * ie + L);
+                f[i] = fi;
+                rsq = fma(rr, rr, rsq);
+                af = fma(pr.a[i], fi, af);
+            }
+        }
+        // gauge (solver.cpp:108-112)
+        const double c = small_block_sum(af, red, tid, NT);
+        const double row2 = small_block_sum(rsq, red, tid, NT);
+        __syncthreads();
+        for (int i = tid; i < n; i += NT) f[i] -= c;
+        for (int j = tid; j < m; j += NT) g[j] += c;
+        // column LSE at the gauged f: the column residual b_j expm1((g_j - h_j)/eps) and next g
+        col_lse();
+        double csq = 0.0;
+        for (int j = tid; j < m; j += NT) {
+            const double cr = pr.b[j] * expm1((g[j] - h[j]) * ie);
+            csq = fma(cr, cr, csq);
+        }
+        const double col2 = small_block_sum(csq, red, tid, NT);
+        if (sqrt(row2) + sqrt(col2) < tol) {
+            conv = 1;
+            break;
+        }
+        __syncthreads();
+        for (int j = tid; j < m; j += NT) g[j] = h[j];
+    }
+    if (tid == 0) {
+        pr.iters = it;
+        pr.conv = conv;
+    }
+}
+
 // ------------------------------------------------------------- block pass on FP64 tensor cores
 // out[o][c] += sum_in e(o,in) W[in][c] as a GEMM: A = e (generated in registers,
 // one cell per lane: row o = lane>>2, col in = lane&3), B = W (smem), C in
@@ -1327,6 +1470,24 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.fn = ki.fn;
     p.occ = occ;
     return p;
+}
+
+void launch_sk_small(int d, SmallProbDev* probs, int count, double tol, long long max_iter, int warm_g,
+                     cudaStream_t s) {
+    int maxcnt = kSmallMax;
+    const void* fn = nullptr;
+    switch (d) {
+        case 1: fn = reinterpret_cast<const void*>(&k_sk_small<1>); break;
+        case 2: fn = reinterpret_cast<const void*>(&k_sk_small<2>); break;
+        case 3: fn = reinterpret_cast<const void*>(&k_sk_small<3>); break;
+        case 4: fn = reinterpret_cast<const void*>(&k_sk_small<4>); break;
+        default: return;
+    }
+    const int smem = static_cast<int>(sizeof(double)) * (kTabWords + 64 + maxcnt * (d + 1));
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    void* args[] = {&probs, &tol, &max_iter, &warm_g};
+    count_launch();
+    cudaLaunchKernel(fn, dim3(count), dim3(512), args, smem, s);
 }
 
 void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s) {

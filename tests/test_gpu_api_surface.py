@@ -422,3 +422,24 @@ def test_culled_sharded_sk_matches_dense_unsharded():
     for r in out:
         assert r.iterations == ref.iterations
         assert rel_err(r.f, ref.f) <= 1e-12 and rel_err(r.g, ref.g) <= 1e-12
+
+
+def test_solve_small_batch_matches_oracle_and_solve():
+    """One CTA per problem, whole SK loop in one kernel launch: identical iteration
+    counts with the CPU oracle and with solve(), potentials within 1e-9."""
+    probs, refs = [], []
+    for s in range(5):
+        inst = G.config("C1", seed=1 + s, n=300 + 40 * s, m=260 + 30 * s)
+        a = np.full(inst.n, 1 / inst.n)
+        b = np.full(inst.m, 1 / inst.m)
+        probs.append((inst.x, inst.y, a, b, inst.epsilon))
+        refs.append(O.solve(O.Instance(a, b, inst.epsilon, x=inst.x, y=inst.y), tol=1e-9))
+    out = sk.solve_small_batch(probs, tol=1e-9)
+    for (x, y, a, b, e), r, ref in zip(probs, out, refs):
+        assert r.converged and r.iterations == ref["iterations"]
+        assert rel_err(r.f, ref["f"]) <= 1e-9 and rel_err(r.g, ref["g"]) <= 1e-9
+        one = sk.solve(sk.PointProblem(x, y, a, b, e), tol=1e-9)
+        assert one.iterations == r.iterations
+    with pytest.raises(ValueError, match="n, m <= 2048"):
+        x = np.random.default_rng(0).uniform(0, 1, (3000, 2))
+        sk.solve_small_batch([(x, x, np.full(3000, 1 / 3000), np.full(3000, 1 / 3000), 0.1)])
