@@ -477,3 +477,36 @@ def test_onthefly_contraction_kernels_match_oracle(d, n, m):
     ro = O.solve(op, tol=1e-10)
     assert rg.iterations == ro["iterations"]
     assert rel_err(rg.f, ro["f"]) <= TOL_POT
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_randomized_transforms_and_marginals_match_oracle(seed):
+    """Seeded sweep over shapes, dimensions, epsilons, weights and cost kinds: both
+    c-transforms and the plan marginals against the oracle."""
+    r = np.random.default_rng(1000 + seed)
+    n, m = int(r.integers(1, 400)), int(r.integers(1, 400))
+    eps = float(10 ** r.uniform(-2.5, 0))
+    a = r.uniform(0.1, 2.0, n)
+    a /= a.sum()
+    b = r.uniform(0.1, 2.0, m)
+    b /= b.sum()
+    if seed % 3 == 0:
+        cost = np.asfortranarray(r.uniform(-1, 3, (n, m)))
+        gp = sk.Problem(cost, a, b, eps)
+        op = O.Instance(a, b, eps, cost=cost)
+    else:
+        d = int(r.integers(1, 6))
+        x = np.asfortranarray(r.normal(0, 1, (n, d)))
+        y = np.asfortranarray(r.normal(0.5, 0.7, (m, d)))
+        gp = sk.PointProblem(x, y, a, b, eps)
+        op = O.Instance(a, b, eps, x=x, y=y)
+    f = r.normal(0, 0.3, n)
+    g_ref = O.ctransform_of_f(op, f)
+    assert rel_err(sk.ctransform_of_f(gp, f), g_ref) <= 1e-12
+    f_ref = O.ctransform_of_g(op, g_ref)
+    assert rel_err(sk.ctransform_of_g(gp, g_ref), f_ref) <= 1e-12
+    row, col, l2, _ = sk.plan_marginals(gp, f_ref, g_ref)
+    row_o, col_o, l2_o, _ = O.plan_marginals(op, f_ref, g_ref)
+    assert rel_err(row, row_o) <= 1e-12 and rel_err(col, col_o) <= 1e-12
+    # the gap at this near-fixed point is itself rounding noise (~1e-14): absolute floor
+    assert abs(l2 - l2_o) <= 1e-12 * l2_o + 1e-13
