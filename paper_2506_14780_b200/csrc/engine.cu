@@ -665,7 +665,7 @@ struct Side {
     // culling (opt-in): Morton order and bounding boxes of groups of 64 / 256 / 2048
     // consecutive permuted points, [group][2d] = lo..., hi...
     IBuf perm;
-    DBuf box32, box64, box256;
+    DBuf box32, box64, box128;
 };
 
 struct SolveState;
@@ -1078,7 +1078,7 @@ static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     a.perm_in = in.perm.p;
     a.perm_out = out.perm.p;
     a.box_gi = in.box64.p;
-    a.box_go = out.box256.p;
+    a.box_go = out.box128.p;
     a.f_gi = P.f_gi[dir].p;
     a.s_go = P.s_go[dir].p;
     a.lskc = kLS * P.kc();
@@ -2711,9 +2711,9 @@ static void prepare_culling(Problem& P) {
     group_boxes(xc, P.n, d, px, 32, P.src.box32);
     group_boxes(yc, P.m, d, py, 32, P.tgt.box32);
     group_boxes(xc, P.n, d, px, 64, P.src.box64);
-    group_boxes(xc, P.n, d, px, 256, P.src.box256);
+    group_boxes(xc, P.n, d, px, 128, P.src.box128);
     group_boxes(yc, P.m, d, py, 64, P.tgt.box64);
-    group_boxes(yc, P.m, d, py, 256, P.tgt.box256);
+    group_boxes(yc, P.m, d, py, 128, P.tgt.box128);
     for (int dir = 0; dir < 2; ++dir) {
         const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
         P.f_gi[dir].ensure((nin + CULL_GI - 1) / CULL_GI);

@@ -1174,8 +1174,8 @@ KernelInfo make_pts() {
 template <int D>
 KernelInfo make_cull() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_cull_kernel<D, 8, 256>);
-    k.jt = 8;
+    k.fn = reinterpret_cast<const void*>(&pts_cull_kernel<D, 4, 256>);
+    k.jt = 4;
     k.nt = 256;
     k.out_tile = CULL_GO;  // work units are per warp
     k.smem = static_cast<int>(sizeof(double)) * (kTabWords + 8 * CULL_GI * PK_of<D>::value);
