@@ -1077,7 +1077,7 @@ static TileArgs cull_args(Problem& P, int dir, const TilePlan& tp, unsigned guar
     Side& out = P.out_side(dir);
     a.perm_in = in.perm.p;
     a.perm_out = out.perm.p;
-    a.box_gi = in.box64.p;
+    a.box_gi = in.box32.p;
     a.box_go = out.box128.p;
     a.f_gi = P.f_gi[dir].p;
     a.s_go = P.s_go[dir].p;

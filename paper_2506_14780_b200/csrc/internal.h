@@ -17,7 +17,7 @@ enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_C
 // Group sizes of the culling bounds (permuted positions): the sum pass tests input
 // groups of CULL_GI against output groups of CULL_GO (one warp's 32 x 4 outputs);
 // the block pass uses 32 x 32 (CULL_GB in tile_kernels.cu).
-constexpr int CULL_GI = 64, CULL_GO = 128;
+constexpr int CULL_GI = 32, CULL_GO = 128;
 
 // Arguments of the persistent tile kernels (tile_kernels.cu).
 struct TileArgs {
