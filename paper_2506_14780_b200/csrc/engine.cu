@@ -665,7 +665,7 @@ struct Side {
     // culling (opt-in): Morton order and bounding boxes of groups of 64 / 256 / 2048
     // consecutive permuted points, [group][2d] = lo..., hi...
     IBuf perm;
-    DBuf box32, box64, box128;
+    DBuf box16, box32, box64, box128;
 };
 
 struct SolveState;
@@ -688,7 +688,7 @@ struct Problem {
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
     bool cull_ready = false;
-    DBuf f_gi[2], s_go[2], f_g32[2], s_g32[2];
+    DBuf f_gi[2], s_go[2], f_g32[2], s_g16[2];
     DBuf gram_part, sums, misc;
     std::mutex mu;
 
@@ -1301,14 +1301,14 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     if (bcull) {
         unsigned* sched = &P.st->counters[12];
         cull_group_max(P, in, P.pack_in[ps.dir].p, P.f_g32[ps.dir].p, 32, ps.guard);
-        cull_group_max(P, out, P.pack_out[ps.dir].p, P.s_g32[ps.dir].p, 32, ps.guard, sched,
+        cull_group_max(P, out, P.pack_out[ps.dir].p, P.s_g16[ps.dir].p, 16, ps.guard, sched,
                        ps.cull_logtot);
         ta.perm_in = in.perm.p;
         ta.perm_out = out.perm.p;
         ta.box_gi = in.box32.p;
-        ta.box_go = out.box32.p;
+        ta.box_go = out.box16.p;
         ta.f_gi = P.f_g32[ps.dir].p;
-        ta.s_go = P.s_g32[ps.dir].p;
+        ta.s_go = P.s_g16[ps.dir].p;
         ta.lskc = kLS * P.kc();
         ta.cull_t = P.cull_t;
         ta.sched = sched;
@@ -2708,6 +2708,8 @@ static void prepare_culling(Problem& P) {
     const std::vector<int> px = morton_perm(xc, P.n, d, lo, hi), py = morton_perm(yc, P.m, d, lo, hi);
     P.src.perm.assign(px);
     P.tgt.perm.assign(py);
+    group_boxes(xc, P.n, d, px, 16, P.src.box16);
+    group_boxes(yc, P.m, d, py, 16, P.tgt.box16);
     group_boxes(xc, P.n, d, px, 32, P.src.box32);
     group_boxes(yc, P.m, d, py, 32, P.tgt.box32);
     group_boxes(xc, P.n, d, px, 64, P.src.box64);
@@ -2719,7 +2721,7 @@ static void prepare_culling(Problem& P) {
         P.f_gi[dir].ensure((nin + CULL_GI - 1) / CULL_GI);
         P.s_go[dir].ensure((nout + CULL_GO - 1) / CULL_GO);
         P.f_g32[dir].ensure((nin + 31) / 32);
-        P.s_g32[dir].ensure((nout + 31) / 32);
+        P.s_g16[dir].ensure((nout + 15) / 16);
     }
     P.cull_ready = true;
 }

@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
 // sum to 1, e.g. P~ at h = f^{C,eps}); kept groups are staged warp-privately
 // (inputs and their W rows gathered through perm_in) and multiplied on DMMA as
 // in pts_mma_kernel.
-constexpr int CULL_GB = 32;  // block-pass group size (inputs and outputs)
+constexpr int CULL_GB = 32;  // block-pass input group size
+constexpr int CULL_GBO = 16;  // block-pass output group (one warp, MB = 2)
 
 __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_src) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(MMA_NT, 3) pts_mma_cull_kernel(TileArgs a) {
     constexpr int PK = PK_of<D>::value;
     constexpr int NCB = KT / 8;
     constexpr int WS = WStride<KT>::value;
-    static_assert(8 * MB == CULL_GB, "one warp owns one 32-output group");
+    static_assert(8 * MB == CULL_GBO, "one warp owns one output group");
     extern __shared__ __align__(16) double sm[];
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(MMA_NT, 3) pts_mma_cull_kernel(TileArgs a) {
         unit = __shfl_sync(0xffffffffu, unit, 0);
         if (unit >= a.n_tiles) break;
         const int64_t og = unit % a.n_out_tiles, ib = unit / a.n_out_tiles;
-        const int64_t obase = og * CULL_GB;
+        const int64_t obase = og * CULL_GBO;
         double Bo[MB], Yo[MB][D];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
@@ -1209,10 +1210,10 @@ KernelInfo make_mma() {
 template <int D, int KT>
 KernelInfo make_mma_cull() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_mma_cull_kernel<D, KT, 4>);
+    k.fn = reinterpret_cast<const void*>(&pts_mma_cull_kernel<D, KT, 2>);
     k.jt = 1;
     k.nt = MMA_NT;
-    k.out_tile = CULL_GB;
+    k.out_tile = CULL_GBO;
     k.smem = static_cast<int>(sizeof(double)) *
              (kTabWords + (MMA_NT / 32) * (CULL_GB * PK_of<D>::value + CULL_GB * WStride<KT>::value));
     return k;
