@@ -1338,7 +1338,7 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
 }
 
 // Gram / dot products: out[a + b*ka] = scale * sum_t w_t U[t,a] V[t,b]
-static unsigned g_gram_slot = 4;
+constexpr unsigned kGramSlot = 4;  // DevState ticket counter used by k_gram
 static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t ldu, const double* V,
                  int64_t ldv, const double* w, double* out, unsigned guard, int diag_only = 0,
                  double scale = 1.0) {
@@ -1355,7 +1355,7 @@ static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t
     ga.part = P.gram_part.p;
     ga.out = out;
     ga.out_scale = scale;
-    ga.counter = &P.st->counters[g_gram_slot];
+    ga.counter = &P.st->counters[kGramSlot];
     ga.st = P.st;
     ga.guard = guard;
     count_launch();
@@ -2337,8 +2337,8 @@ static bool poll_done(Problem& P) {
 
 static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell, const double* basis,
                           const double* init_f, bool trace_enabled, int64_t trace_cap_hint,
-                          int64_t forced_iters = -1, bool exact_marginals = false) {
-    if (!(tol > 0.0) && forced_iters < 0) throw InvalidArgument("solve: tol_omega must be positive");
+                          bool exact_marginals = false) {
+    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
     const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, std::max<int64_t>(trace_cap_hint, 1)) : 1;
@@ -3377,7 +3377,7 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
     const int64_t ell = use_newton ? cfg->ell : 0;
     SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
-                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1), -1,
+                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1),
                            cfg->exact_marginals != 0);
     std::memcpy(f_out, o.f.data(), sizeof(double) * P.n_global);
     std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
@@ -3550,7 +3550,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
             SolveOut o;
             try {
                 o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, bptr, init, cfg->trace_enabled != 0,
-                              cfg->max_iter, -1, cfg->exact_marginals != 0);
+                              cfg->max_iter, cfg->exact_marginals != 0);
             } catch (const InvalidArgument& e) {
                 throw RuntimeFailure("anneal stage " + std::to_string(s) + ": " + e.what());
             }

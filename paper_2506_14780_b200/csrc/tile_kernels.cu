@@ -1356,6 +1356,9 @@ KernelInfo tune_variant(int v) {
         case 21: return make_pts<2, 8, MODE_SUM, 0, 128, 1, false, 6>();
         case 22: return make_pts<2, 6, MODE_SUM, 0, 256, 1, false, 3>();
         case 23: return make_pts<2, 4, MODE_SUM, 0, 256, 2, false, 4>();
+        case 24: return make_pts<2, 8, MODE_SUM, 0, 256, 1, false, 2>();
+        case 25: return make_pts<2, 8, MODE_SUM, 0, 128, 1, false, 4>();
+        case 26: return make_pts<2, 6, MODE_SUM, 0, 256, 1, false, 2>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();
