@@ -143,26 +143,52 @@ static int grid_for(int64_t count, int threads = AUX_NT) {
 }
 
 // ============================================================ device buffers
+// Device allocations come from the device's stream-ordered memory pool (release
+// threshold raised once, so memory freed by a destroyed problem is reused by the next
+// one without going back to the driver) on a dedicated allocation stream.
+static cudaStream_t alloc_stream() {
+    static std::mutex mu;
+    static int dev_init = -1;
+    static cudaStream_t s = nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev_init != dev) {
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        dev_init = dev;
+    }
+    return s;
+}
+
 struct DBuf {
     double* p = nullptr;
     size_t n = 0;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() {
-        if (p) cudaFree(p);
-    }
-    // Grows (never inside stream capture). The zero fill is complete before
-    // returning: the problem streams are non-blocking, so an asynchronous
-    // default-stream memset could otherwise land after later work on them.
-    void ensure(size_t count) {
-        if (count <= n) return;
-        if (p) CK(cudaFree(p));
+    ~DBuf() { release(); }
+    // Returns the memory to the pool once no stream can still use it.
+    void release() {
+        if (!p) return;
+        if (cudaDeviceSynchronize() == cudaSuccess) cudaFreeAsync(p, alloc_stream());
         p = nullptr;
         n = 0;
-        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
-        CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(double)));
-        CK(cudaDeviceSynchronize());
+    }
+    // Grows (never inside stream capture). The zero fill is complete before
+    // returning: the problem streams are non-blocking, so the allocation stream's
+    // work must be finished before they touch the buffer.
+    void ensure(size_t count) {
+        if (count <= n) return;
+        release();
+        const size_t bytes = std::max<size_t>(count, 1) * sizeof(double);
+        cudaStream_t s = alloc_stream();
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s));
+        CK(cudaMemsetAsync(p, 0, bytes, s));
+        CK(cudaStreamSynchronize(s));
         n = count;
     }
 };
