@@ -212,477 +212,7 @@ struct IBuf {  // int32 device buffer (permutations)
     }
 };
 
-// ============================================================ small kernels
-__global__ void k_fill(double* x, int64_t n, double v) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        x[i] = v;
-}
-
-__global__ void k_copy(double* dst, const double* src, int64_t n, DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        dst[i] = src[i];
-}
-
-__global__ void k_state_init(DevState* st, long long max_iter, double tol) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    st->done = 0;
-    st->iter_active = 0;
-    st->conv = 0;
-    st->newton_ok = 0;
-    st->accept = 0;
-    st->attempted = 0;
-    st->iter = 0;
-    st->max_iter = max_iter;
-    st->tol = tol;
-    for (int d = 0; d < 2; ++d) {
-        st->need_exact[d] = 1;
-        st->retry[d] = 0;
-        st->ref_valid[d] = 0;
-    }
-    for (int c = 0; c < 32; ++c) st->counters[c] = 0u;
-}
-
-__global__ void k_invalidate_refs(DevState* st) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        st->ref_valid[0] = st->ref_valid[1] = 0;
-        st->done = 0;
-        st->newton_ok = 0;
-    }
-}
-
-__global__ void k_iter_begin(DevState* st) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (st->done) {
-        st->iter_active = 0;
-        return;
-    }
-    st->iter += 1;
-    st->iter_active = 1;
-    st->newton_ok = 0;
-    st->accept = 0;
-    st->attempted = 0;
-    st->t_iter0 = globaltimer_ns();
-}
-
-// f = f_pre - c ; rowres_i = a_i expm1(f_pre_i/eps + L_i) ; g += c
-__global__ void k_gauge_apply(double* f, const double* L, const double* a, int64_t n, double* g,
-                              int64_t m, double inv_eps, double* rowres, DevState* st) {
-    if (st->done) return;
-    const double c = st->c_gauge;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (i < n) {
-            const double fp = f[i];
-            rowres[i] = a[i] * expm1(fp * inv_eps + L[i]);
-            f[i] = fp - c;
-        } else {
-            g[i - n] += c;
-        }
-    }
-}
-
-// colres_j = b_j expm1((g_j - h_j)/eps)
-__global__ void k_colres(const double* g, const double* h, const double* b, int64_t m, double inv_eps,
-                         double* colres, DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
-         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        colres[j] = b[j] * expm1((g[j] - h[j]) * inv_eps);
-}
-
-// alpha - r = -a_i expm1(f_i/eps + L_i(h)) ; r = a - (alpha - r)
-__global__ void k_newton_r(const double* f, const double* L, const double* a, int64_t n, double inv_eps,
-                           double* am, double* r, DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double d = -a[i] * expm1(f[i] * inv_eps + L[i]);
-        am[i] = d;
-        r[i] = a[i] - d;
-    }
-}
-
-// try_newton's ell x ell algebra on one CTA (solver.cpp:37-44, objective.cpp:138-140):
-// H = -(1/eps)(G1 - cross); H = (H+H^T)/2; LLT(-H) (fails iff a pivot <= 0, as
-// Eigen's llt_inplace::unblocked); delta = LLT.solve(grad).
-__global__ void k_newton_solve(const double* G1, const double* cross, const double* grad, int ell,
-                               double inv_eps, double* delta, DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    extern __shared__ double sA[];  // ell*ell
-    __shared__ int fail;
-    __shared__ double piv;
-    const int tid = threadIdx.x;
-    if (tid == 0) fail = 0;
-    for (int e = tid; e < ell * ell; e += blockDim.x) {
-        const int r = e % ell, c = e / ell;
-        const double h_rc = -inv_eps * (G1[r + c * ell] - cross[r + c * ell]);
-        const double h_cr = -inv_eps * (G1[c + r * ell] - cross[c + r * ell]);
-        sA[e] = -(0.5 * (h_rc + h_cr));
-    }
-    __syncthreads();
-    for (int c = 0; c < ell; ++c) {
-        if (tid == 0) {
-            double x = sA[c + c * ell];
-            for (int t = 0; t < c; ++t) x -= sA[c + t * ell] * sA[c + t * ell];
-            if (!(x > 0.0)) fail = 1;
-            piv = sqrt(x);
-            sA[c + c * ell] = piv;
-        }
-        __syncthreads();
-        if (fail) break;
-        for (int r = c + 1 + tid; r < ell; r += blockDim.x) {
-            double v = sA[r + c * ell];
-            for (int t = 0; t < c; ++t) v -= sA[r + t * ell] * sA[c + t * ell];
-            sA[r + c * ell] = v / piv;
-        }
-        __syncthreads();
-    }
-    if (fail) {
-        if (tid == 0) st->newton_ok = 0;
-        return;
-    }
-    if (tid == 0) {
-        double y[64];
-        for (int r = 0; r < ell; ++r) {
-            double v = grad[r];
-            for (int t = 0; t < r; ++t) v -= sA[r + t * ell] * y[t];
-            y[r] = v / sA[r + r * ell];
-        }
-        for (int r = ell - 1; r >= 0; --r) {
-            double v = y[r];
-            for (int t = r + 1; t < ell; ++t) v -= sA[t + r * ell] * y[t];
-            y[r] = v / sA[r + r * ell];
-        }
-        for (int r = 0; r < ell; ++r) delta[r] = y[r];
-    }
-}
-
-// candidate = f + V delta (solver.cpp:45)
-__global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, const double* delta,
-                        double* out, DevState* st, unsigned guard) {
-    if (guard_skip(st, guard)) return;
-    __shared__ double sd[64];
-    if (threadIdx.x < ell) sd[threadIdx.x] = delta[threadIdx.x];
-    __syncthreads();
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < ell; ++c) s += V[i + c * n] * sd[c];
-        out[i] = f[i] + s;
-    }
-}
-
-// accepted: f <- candidate, next g <- h(candidate); otherwise next g <- h.
-__global__ void k_select(double* f, const double* fcand, int64_t n, double* gnext, const double* h,
-                         const double* hcand, int64_t m, DevState* st) {
-    if (st->done) return;
-    const bool acc = st->newton_ok && st->accept;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (i < n) {
-            if (acc) f[i] = fcand[i];
-        } else {
-            gnext[i - n] = acc ? hcand[i - n] : h[i - n];
-        }
-    }
-}
-
-// End of an iteration: trace record, max_iter stop and -- when the solve runs as a
-// device-side WHILE loop (conditional graph node) -- the loop condition.
-__global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled,
-                         cudaGraphConditionalHandle loop) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (!st->iter_active) {
-        if (loop) cudaGraphSetConditional(loop, 0);
-        return;
-    }
-    st->iter_active = 0;
-    const long long k = st->iter;
-    if (trace_enabled && k - 1 < cap) {
-        sknr_record r;
-        r.index = k;
-        r.marginal_error = st->gap_l2;
-        r.marginal_error_inf = st->gap_inf;
-        const bool acc = st->attempted && st->newton_ok && st->accept;
-        r.semi_dual_value = acc ? st->q1 : st->q0;
-        r.newton_attempted = st->attempted;
-        r.newton_accepted = acc ? 1 : 0;
-        r.wall_time_ms = static_cast<double>(globaltimer_ns() - st->t_iter0) * 1e-6;
-        trace[k - 1] = r;
-    }
-    if (k >= st->max_iter) st->done = 1;
-    if (loop) cudaGraphSetConditional(loop, st->done ? 0 : 1);
-}
-
-__global__ void k_axpby(const double* x, const double* y, int64_t n, double a, double b, double* out) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = a * x[i] + b * y[i];
-}
-
-// ---- top_modes helpers
-// Y[:,c] -= u0 * s_c
-__global__ void k_deflate(double* Y, int64_t n, int k, const double* u0, const double* s) {
-    const int64_t total = n * k;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % n;
-        const int c = static_cast<int>(e / n);
-        Y[e] -= u0[i] * s[c];
-    }
-}
-
-// out (n x l) = X (n x k) * W (k x l), W col-major
-__global__ void k_small_gemm(const double* X, int64_t n, int k, const double* W, int l, double* out) {
-    extern __shared__ double sW[];
-    for (int e = threadIdx.x; e < k * l; e += blockDim.x) sW[e] = W[e];
-    __syncthreads();
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        for (int a = 0; a < l; ++a) {
-            double s = 0.0;
-            for (int r = 0; r < k; ++r) s += X[i + r * n] * sW[r + a * k];
-            out[i + a * n] = s;
-        }
-    }
-}
-
-// out (n x l) += sgn * X (n x k) * W (k x l), W col-major
-__global__ void k_small_gemm_acc(const double* X, int64_t n, int k, const double* W, int l, double sgn,
-                                 double* out) {
-    extern __shared__ double sW[];
-    for (int e = threadIdx.x; e < k * l; e += blockDim.x) sW[e] = W[e];
-    __syncthreads();
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        for (int a = 0; a < l; ++a) {
-            double s = 0.0;
-            for (int r = 0; r < k; ++r) s += X[i + r * n] * sW[r + a * k];
-            out[i + a * n] += sgn * s;
-        }
-    }
-}
-
-// R = YW - theta_a XW
-__global__ void k_resid(const double* YW, const double* XW, const double* theta, int64_t n, int l,
-                        double* R) {
-    const int64_t total = n * l;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int a = static_cast<int>(e / n);
-        R[e] = YW[e] - theta[a] * XW[e];
-    }
-}
-
-__global__ void k_div_rows(const double* X, const double* s, int64_t n, int l, double* out) {
-    const int64_t total = n * l;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[e] = X[e] / s[e % n];
-}
-
-// SplitMix64 start block (spectral.cpp:138-142): draw t = c*n + i of the
-// stream seeded 0x73706563 is state seed + (t+1)*gamma -- computed in parallel.
-__global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long seed, int64_t n_global,
-                                 int64_t row_begin) {
-    const int64_t total = n * k;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t t = (e / n) * n_global + row_begin + e % n;  // draw index of (row, column)
-        unsigned long long z = seed + static_cast<unsigned long long>(t + 1) * 0x9E3779B97F4A7C15ull;
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-        z = z ^ (z >> 31);
-        const double u01 = static_cast<double>(z >> 11) * 0x1.0p-53;
-        X[e] = -1.0 + 2.0 * u01;
-    }
-}
-
-// ---- Householder QR with Eigen's conventions (makeHouseholder /
-// applyHouseholderOnTheLeft, HouseholderQR + householderQ()*Identity):
-// hh[4c..4c+3] = {tau, beta, 1/(c0-beta), zero_tail}
-__global__ void k_hh_norm(double* X, int64_t n, int c, double* part, double* hh, unsigned* counter) {
-    __shared__ double sh[AUX_NT];
-    double s = 0.0;
-    const double* col = X + static_cast<int64_t>(c) * n;
-    for (int64_t r = c + 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
-         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        s = fma(col[r], col[r], s);
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int k = blockDim.x / 2; k > 0; k >>= 1) {
-        if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
-        __syncthreads();
-    }
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = sh[0];
-        __threadfence();
-        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!is_last || threadIdx.x != 0) return;
-    __threadfence();
-    double tail = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) tail += part[b];
-    const double c0 = col[c];
-    double tau, beta, zero;
-    if (tail <= 2.2250738585072014e-308) {
-        tau = 0.0;
-        beta = c0;
-        zero = 1.0;
-    } else {
-        beta = sqrt(c0 * c0 + tail);
-        if (c0 >= 0.0) beta = -beta;
-        tau = (beta - c0) / beta;
-        zero = 0.0;
-    }
-    hh[4 * c] = tau;
-    hh[4 * c + 1] = beta;
-    hh[4 * c + 2] = c0 - beta;
-    hh[4 * c + 3] = zero;
-    X[c + static_cast<int64_t>(c) * n] = beta;
-    *counter = 0u;
-}
-
-// v_r = X[r,c]/(c0-beta) (written back); w_c2 = X[c,c2] + sum_{r>c} v_r X[r,c2]
-// for c2 in [c2lo, k) of matrix M (M==X for the factorisation, Q for forming Q).
-__global__ void k_hh_w(double* X, const double* M, int64_t n, int k, int c, int c2lo, int scale_v,
-                       const double* hh, double* part, double* w, unsigned* counter) {
-    constexpr int KM = 64;
-    __shared__ double sh[AUX_NT];
-    __shared__ double sw[KM];
-    const double denom = hh[4 * c + 2];
-    const bool zero = hh[4 * c + 3] != 0.0;
-    double acc[KM];
-    const int nw = k - c2lo;
-    for (int q = 0; q < nw; ++q) acc[q] = 0.0;
-    double* colc = X + static_cast<int64_t>(c) * n;
-    for (int64_t r = c + 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
-         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double v = colc[r];
-        if (scale_v) {
-            v = zero ? 0.0 : v / denom;
-            colc[r] = v;
-        }
-        for (int q = 0; q < nw; ++q) acc[q] = fma(v, M[r + static_cast<int64_t>(c2lo + q) * n], acc[q]);
-    }
-    for (int q = 0; q < nw; ++q) {
-        sh[threadIdx.x] = acc[q];
-        __syncthreads();
-        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-            if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) sw[q] = sh[0];
-        __syncthreads();
-    }
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < nw; ++q) part[static_cast<int64_t>(blockIdx.x) * KM + q] = sw[q];
-        __threadfence();
-        is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    for (int q = threadIdx.x; q < nw; q += blockDim.x) {
-        double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += part[static_cast<int64_t>(b) * KM + q];
-        w[q] = M[c + static_cast<int64_t>(c2lo + q) * n] + s;
-    }
-    if (threadIdx.x == 0) *counter = 0u;
-}
-
-// M[r,c2] -= tau w_c2 v_r for r >= c (v_c = 1), c2 in [c2lo, k)
-__global__ void k_hh_update(const double* X, double* M, int64_t n, int k, int c, int c2lo,
-                            const double* hh, const double* w) {
-    const double tau = hh[4 * c];
-    if (tau == 0.0) return;
-    const int nw = k - c2lo;
-    const int64_t rows = n - c;
-    const int64_t total = rows * nw;
-    const double* v = X + static_cast<int64_t>(c) * n;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = c + e % rows;
-        const int q = static_cast<int>(e / rows);
-        const double vr = (r == c) ? 1.0 : v[r];
-        M[r + static_cast<int64_t>(c2lo + q) * n] -= tau * w[q] * vr;
-    }
-}
-
-__global__ void k_eye(double* Q, int64_t n, int k) {
-    const int64_t total = n * k;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        Q[e] = (e % n == e / n) ? 1.0 : 0.0;
-}
-
-// plan_ij = a_i b_j exp((f_i + g_j - C_ij)/eps)  (coupling_from, core.cpp:84-103) for the
-// rows [r0, r0 + rows), col-major with leading dimension rows; f is indexed globally.
-__global__ void k_coupling(const double* C, const double* x, const double* y, int64_t n, int64_t m,
-                           int64_t r0, int64_t rows, int d, double kappa, const double* a,
-                           const double* b, const double* f, const double* g, double inv_eps,
-                           double* plan) {
-    const int64_t total = rows * m;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = r0 + e % rows, j = e / rows;
-        double c;
-        if (C) {
-            c = C[i + j * n];
-        } else {
-            double s = 0.0;
-            for (int q = 0; q < d; ++q) {
-                const double t = x[i + q * n] - y[j + q * m];
-                s += t * t;
-            }
-            c = kappa * s;
-        }
-        plan[e] = a[i] * b[j] * exp((f[i] + g[j] - c) * inv_eps);
-    }
-}
-
-// Stored cost built on device from points (direct difference, generators.cpp:101),
-// written in both layouts.
-__global__ void k_build_cost(const double* x, const double* y, int64_t n, int64_t m, int d,
-                             double kappa, double* C, double* CT) {
-    const int64_t total = n * m;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = e % n, j = e / n;
-        double s = 0.0;
-        for (int q = 0; q < d; ++q) {
-            const double t = x[i + q * n] - y[j + q * m];
-            s += t * t;
-        }
-        const double c = kappa * s;
-        C[e] = c;
-        if (CT) CT[j + i * m] = c;
-    }
-}
-
-// transpose n x m col-major -> m x n col-major
-__global__ void k_transpose(const double* A, int64_t n, int64_t m, double* AT) {
-    __shared__ double tile[32][33];
-    for (int64_t bj = blockIdx.y * 32; bj < m; bj += static_cast<int64_t>(gridDim.y) * 32)
-        for (int64_t bi = blockIdx.x * 32; bi < n; bi += static_cast<int64_t>(gridDim.x) * 32) {
-            for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-                const int64_t i = bi + threadIdx.x, j = bj + r;
-                if (i < n && j < m) tile[r][threadIdx.x] = A[i + j * n];
-            }
-            __syncthreads();
-            for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-                const int64_t j = bj + threadIdx.x, i = bi + r;
-                if (i < n && j < m) AT[j + i * m] = tile[threadIdx.x][r];
-            }
-            __syncthreads();
-        }
-}
+#include "engine_kernels.cuh"
 
 // ============================================================ problem
 struct Side {
@@ -1397,2588 +927,9 @@ static void gram_all(Problem& P, int64_t T, int ka, int kb, const double* U, int
     allreduce(P, out, static_cast<size_t>(diag_only ? ka : ka * kb), ncclSum);
 }
 
-// ============================================================ top_modes
-// Symmetric eigen-decomposition (stands in for Eigen::SelfAdjointEigenSolver,
-// spectral.cpp:156): Householder tridiagonalisation followed by implicit QL
-// with Wilkinson-type shifts (the classic tred2/tql2 pair), ascending
-// eigenvalues, orthonormal eigenvectors in columns. O(k^3) for the k x k
-// Rayleigh-Ritz matrix.
-static bool symeig_tql(const double* Ain, int k, double* evals, double* evecs) {
-    std::vector<double> a(static_cast<size_t>(k) * k), d(k), e(k);
-    auto A = [&](int i, int j) -> double& { return a[static_cast<size_t>(i) * k + j]; };
-    for (int i = 0; i < k; ++i)
-        for (int j = 0; j < k; ++j) A(i, j) = Ain[i + j * k];
-    for (int i = k - 1; i > 0; --i) {
-        const int l = i - 1;
-        double h = 0.0, scale = 0.0;
-        if (l > 0) {
-            for (int q = 0; q <= l; ++q) scale += std::abs(A(i, q));
-            if (scale == 0.0) {
-                e[i] = A(i, l);
-            } else {
-                for (int q = 0; q <= l; ++q) {
-                    A(i, q) /= scale;
-                    h += A(i, q) * A(i, q);
-                }
-                double f = A(i, l);
-                double g = f >= 0.0 ? -std::sqrt(h) : std::sqrt(h);
-                e[i] = scale * g;
-                h -= f * g;
-                A(i, l) = f - g;
-                f = 0.0;
-                for (int j = 0; j <= l; ++j) {
-                    A(j, i) = A(i, j) / h;
-                    g = 0.0;
-                    for (int q = 0; q <= j; ++q) g += A(j, q) * A(i, q);
-                    for (int q = j + 1; q <= l; ++q) g += A(q, j) * A(i, q);
-                    e[j] = g / h;
-                    f += e[j] * A(i, j);
-                }
-                const double hh = f / (h + h);
-                for (int j = 0; j <= l; ++j) {
-                    f = A(i, j);
-                    e[j] = g = e[j] - hh * f;
-                    for (int q = 0; q <= j; ++q) A(j, q) -= (f * e[q] + g * A(i, q));
-                }
-            }
-        } else {
-            e[i] = A(i, l);
-        }
-        d[i] = h;
-    }
-    d[0] = 0.0;
-    e[0] = 0.0;
-    for (int i = 0; i < k; ++i) {
-        const int l = i - 1;
-        if (d[i] != 0.0) {
-            for (int j = 0; j <= l; ++j) {
-                double g = 0.0;
-                for (int q = 0; q <= l; ++q) g += A(i, q) * A(q, j);
-                for (int q = 0; q <= l; ++q) A(q, j) -= g * A(q, i);
-            }
-        }
-        d[i] = A(i, i);
-        A(i, i) = 1.0;
-        for (int j = 0; j <= l; ++j) A(j, i) = A(i, j) = 0.0;
-    }
-    for (int i = 1; i < k; ++i) e[i - 1] = e[i];
-    e[k - 1] = 0.0;
-    for (int l = 0; l < k; ++l) {
-        int iter = 0, m;
-        do {
-            for (m = l; m < k - 1; ++m) {
-                const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
-                if (std::abs(e[m]) <= 0x1p-53 * dd) break;
-            }
-            if (m != l) {
-                if (iter++ == 100) return false;
-                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-                double r = std::hypot(g, 1.0);
-                g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
-                double s = 1.0, c = 1.0, p = 0.0;
-                int i;
-                for (i = m - 1; i >= l; --i) {
-                    double f = s * e[i];
-                    const double b = c * e[i];
-                    e[i + 1] = (r = std::hypot(f, g));
-                    if (r == 0.0) {
-                        d[i + 1] -= p;
-                        e[m] = 0.0;
-                        break;
-                    }
-                    s = f / r;
-                    c = g / r;
-                    g = d[i + 1] - p;
-                    r = (d[i] - g) * s + 2.0 * c * b;
-                    d[i + 1] = g + (p = s * r);
-                    g = c * r - b;
-                    for (int q = 0; q < k; ++q) {
-                        f = A(q, i + 1);
-                        A(q, i + 1) = s * A(q, i) + c * f;
-                        A(q, i) = c * A(q, i) - s * f;
-                    }
-                }
-                if (r == 0.0 && i >= l) continue;
-                d[l] -= p;
-                e[l] = g;
-                e[m] = 0.0;
-            }
-        } while (m != l);
-    }
-    std::vector<int> order(k);
-    for (int i = 0; i < k; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int u, int v) { return d[u] < d[v]; });
-    for (int c = 0; c < k; ++c) {
-        evals[c] = d[order[c]];
-        for (int r = 0; r < k; ++r) evecs[r + c * k] = A(r, order[c]);
-    }
-    return true;
-}
-
-static void host_sym_eig(const std::vector<double>& A, int k, std::vector<double>& evals,
-                         std::vector<double>& evecs) {
-    evals.assign(k, 0.0);
-    evecs.assign(static_cast<size_t>(k) * k, 0.0);
-    if (!symeig_tql(A.data(), k, evals.data(), evecs.data()))
-        throw EigenFailure("top_modes: dense Ritz solve failed", std::numeric_limits<double>::infinity());
-}
-
-struct QrWork {
-    DBuf hh, w, part, Q, backup, flag;
-    bool force_householder = false;
-};
-
-// Cholesky G + shift*I = L L^T (shift = coef * trace(G)), then Rinv = L^{-T}
-// (upper). One CTA; k <= 64. *fail = 1 if a pivot is not positive.
-__global__ void k_chol_inv(const double* G, int k, double coef, double* Rinv, int* fail) {
-    extern __shared__ double sL[];  // k*k
-    __shared__ double piv;
-    __shared__ int bad;
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        bad = 0;
-        double tr = 0.0;
-        for (int c = 0; c < k; ++c) tr += G[c + c * k];
-        piv = coef * tr;
-    }
-    __syncthreads();
-    const double shift = piv;
-    for (int e = tid; e < k * k; e += blockDim.x) {
-        const int r = e % k, c = e / k;
-        sL[e] = G[e] + (r == c ? shift : 0.0);
-    }
-    __syncthreads();
-    for (int c = 0; c < k; ++c) {
-        if (tid == 0) {
-            double x = sL[c + c * k];
-            for (int t = 0; t < c; ++t) x -= sL[c + t * k] * sL[c + t * k];
-            if (!(x > 0.0)) bad = 1;
-            piv = sqrt(x);
-            sL[c + c * k] = piv;
-        }
-        __syncthreads();
-        if (bad) break;
-        for (int r = c + 1 + tid; r < k; r += blockDim.x) {
-            double v = sL[r + c * k];
-            for (int t = 0; t < c; ++t) v -= sL[r + t * k] * sL[c + t * k];
-            sL[r + c * k] = v / piv;
-        }
-        __syncthreads();
-    }
-    if (bad) {
-        if (tid == 0) *fail = 1;
-        return;
-    }
-    // column j of L^{-1} by forward substitution; Rinv = (L^{-1})^T
-    for (int j = tid; j < k; j += blockDim.x) {
-        double x[64];
-        for (int r = 0; r < k; ++r) {
-            double v = (r == j) ? 1.0 : 0.0;
-            for (int t = j; t < r; ++t) v -= sL[r + t * k] * x[t];
-            x[r] = r < j ? 0.0 : v / sL[r + r * k];
-        }
-        for (int r = 0; r < k; ++r) Rinv[j + r * k] = x[r];  // Rinv(j, r) = Linv(r, j)
-    }
-}
-
-// Thin Householder Q of X (n x k) in place (spectral.cpp:116-117 conventions).
-static void device_householder_q(Problem& P, double* X, int64_t n, int k, QrWork& qw) {
-    cudaStream_t s = P.stream;
-    qw.hh.ensure(4 * 64);
-    qw.w.ensure(64);
-    qw.part.ensure(148 * 64);
-    qw.Q.ensure(static_cast<size_t>(n) * k);
-    unsigned* ctr = &P.st->counters[8];
-    const int kk = static_cast<int>(std::min<int64_t>(k, n));
-    const int gb = std::max(1, std::min(148, static_cast<int>((n + 4095) / 4096)));
-    for (int c = 0; c < kk; ++c) {
-        count_launch();
-        k_hh_norm<<<gb, AUX_NT, 0, s>>>(X, n, c, qw.part.p, qw.hh.p, ctr);
-        count_launch();
-        k_hh_w<<<gb, AUX_NT, 0, s>>>(X, X, n, k, c, c + 1, 1, qw.hh.p, qw.part.p, qw.w.p, ctr);
-        if (c + 1 < k) {
-            count_launch();
-            k_hh_update<<<grid_for((n - c) * (k - c - 1)), AUX_NT, 0, s>>>(X, X, n, k, c, c + 1, qw.hh.p,
-                                                                          qw.w.p);
-        }
-    }
-    count_launch();
-    k_eye<<<grid_for(n * k), AUX_NT, 0, s>>>(qw.Q.p, n, k);
-    for (int c = kk - 1; c >= 0; --c) {
-        count_launch();
-        k_hh_w<<<gb, AUX_NT, 0, s>>>(X, qw.Q.p, n, k, c, c, 0, qw.hh.p, qw.part.p, qw.w.p, ctr);
-        count_launch();
-        k_hh_update<<<grid_for((n - c) * (k - c)), AUX_NT, 0, s>>>(X, qw.Q.p, n, k, c, c, qw.hh.p,
-                                                                   qw.w.p);
-    }
-    CK(cudaMemcpyAsync(X, qw.Q.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, s));
-    CK(cudaGetLastError());
-}
-
-// CholeskyQR step: X <- X R^{-1} with R^T R = X^T X (+ shift I). The shifted
-// first pass makes the factorisation succeed for cond(X) up to ~1/u (shifted
-// CholeskyQR3); a failed Cholesky sets *fail and the caller falls back to
-// Householder.
-static void device_cholqr_step(Problem& P, double* X, int64_t n, int k, bool shifted, QrWork& qw,
-                               int* fail) {
-    qw.Q.ensure(static_cast<size_t>(n) * k);
-    qw.w.ensure(64 * 64 * 2);
-    double* G = qw.w.p;
-    double* Rinv = qw.w.p + 64 * 64;
-    gram_all(P, n, k, k, X, n, X, n, nullptr, G, 0);
-    const double shift_coef = shifted ? 11.0 * (static_cast<double>(n) * k + k * (k + 1.0)) * 0x1p-53 : 0.0;
-    count_launch();
-    k_chol_inv<<<1, 64, sizeof(double) * k * k, P.stream>>>(G, k, shift_coef, Rinv, fail);
-    count_launch();
-    k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * k * k, P.stream>>>(X, n, k, Rinv, k, qw.Q.p);
-    CK(cudaMemcpyAsync(X, qw.Q.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
-}
-
-// orthonormalize_deflated (spectral.cpp:113-121): same deflation rounds and
-// stopping test; the QR is shifted CholeskyQR3 (same column space as the
-// reference's Householder Q; columns may differ in sign, which neither the
-// Rayleigh-Ritz step nor the Newton step sees) with a device Householder
-// fallback (Eigen's reflector convention) when the Gram is numerically singular.
-static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const double* u0,
-                                 QrWork& qw) {
-    double* s = P.misc.p;  // k dots
-    qw.flag.ensure(1);
-    int* fail = reinterpret_cast<int*>(qw.flag.p);
-    for (int round = 0; round < 3; ++round) {
-        gram_all(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
-        count_launch();
-        k_deflate<<<grid_for(n * k), AUX_NT, 0, P.stream>>>(X, n, k, u0, s);
-        bool use_householder = qw.force_householder;
-        if (!use_householder) {
-            CK(cudaMemcpyAsync(qw.backup.p, X, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
-            CK(cudaMemsetAsync(fail, 0, sizeof(int), P.stream));
-            device_cholqr_step(P, X, n, k, true, qw, fail);
-            device_cholqr_step(P, X, n, k, false, qw, fail);
-            device_cholqr_step(P, X, n, k, false, qw, fail);
-        }
-        gram_all(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
-        std::vector<double> hs(k + 1);
-        download(hs.data(), s, k, P.stream);
-        int hfail = 0;
-        if (!use_householder) CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
-        CK(cudaStreamSynchronize(P.stream));
-        if (hfail) {  // restore the deflated block and redo this round with Householder
-            if (P.shard)
-                throw EigenFailure("top_modes: CholeskyQR breakdown on a row-sharded problem (no sharded "
-                                   "Householder fallback)", std::numeric_limits<double>::infinity());
-            CK(cudaMemcpyAsync(X, qw.backup.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
-            device_householder_q(P, X, n, k, qw);
-            gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
-            download(hs.data(), s, k, P.stream);
-            CK(cudaStreamSynchronize(P.stream));
-        }
-        double worst = 0.0;
-        for (int c = 0; c < k; ++c) worst = std::max(worst, std::abs(hs[c]));
-        if (worst < 1e-13) break;
-    }
-}
-
-struct Basis {
-    std::vector<double> vectors, vectors_sym, rhos;
-    int64_t sweeps = 0;
-};
-
-// Y = R~ R~^T X with the Perron direction sqrt(alpha) deflated (spectral.cpp:150-151):
-// two DMMA block passes (column then row direction) and a rank-one correction.
-struct OpWork {
-    DBuf Z, W;
-    // culling of the operator passes (opt-in): per-output lower bounds of log(sum of
-    // terms) for the two directions, from the anchor's own transforms
-    bool cull = false;
-    DBuf sub0, sub1, tmp;
-};
-
-// sub = (v - vt)/eps (+ lw): log-total lower bound of an operator pass's outputs
-__global__ void k_cull_sub(const double* v, const double* vt, const double* lw, double inv_eps, int64_t count,
-                           double* sub) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        sub[i] = (v[i] - vt[i]) * inv_eps + (lw ? lw[i] : 0.0);
-}
-
-static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned guard);
-
-// Operator passes of R~ R~^T at the anchor (f, g): column pass terms sqrt(a_i) e^{(f_i+g_j-C_ij)/eps}
-// sum to >= e^{(g_j - g~_j)/eps} (g~ = f^{C,eps}), row pass terms to >= sqrt(a_i) e^{(f_i - f~_i)/eps}
-// (f~ = g^{C,eps}); these lower bounds normalise the culling test (pts_mma_cull_kernel).
-static void prepare_op_culling(Problem& P, const double* f, const double* g, OpWork& ow) {
-    ow.cull = cull_block_active(P, 0) && cull_block_active(P, 1) && cull_active(P, 0) && cull_active(P, 1);
-    if (!ow.cull) return;
-    const int64_t n = P.n, m = P.m;
-    ow.sub0.ensure(m);
-    ow.sub1.ensure(n);
-    ow.tmp.ensure(std::max(n, m));
-    cudaStream_t s = P.stream;
-    lse(P, 0, f, ow.tmp.p, G_NONE);  // g~
-    count_launch();
-    k_cull_sub<<<grid_for(m), AUX_NT, 0, s>>>(g, ow.tmp.p, nullptr, P.inv_eps(), m, ow.sub0.p);
-    lse(P, 1, g, ow.tmp.p, G_NONE);  // f~
-    count_launch();
-    k_cull_sub<<<grid_for(n), AUX_NT, 0, s>>>(f, ow.tmp.p, P.src.lsw.p, P.inv_eps(), n, ow.sub1.p);
-}
-
-static void apply_sym_sym(Problem& P, const double* f, const double* g, const double* X, double* Y,
-                          int block, int kt, OpWork& ow) {
-    const int64_t n = P.n, m = P.m;
-    cudaStream_t s = P.stream;
-    ow.Z.ensure(m * block);
-    ow.W.ensure(std::max(n, m) * kt);
-    // Z = R~^T X : z_j = sqrt(b_j) sum_i sqrt(a_i) e^{(f_i+g_j-C_ij)/eps} X_i
-    count_launch();
-    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(X, n, n, block, kt, nullptr, ow.W.p);
-    PassSpec zt;
-    zt.dir = 0;
-    zt.in_v = f;
-    zt.in_lw = P.src.lsw.p;
-    zt.out_v = g;
-    zt.W = ow.W.p;
-    zt.k = block;
-    zt.kt = kt;
-    zt.out_scale = P.tgt.sw.p;
-    zt.out = ow.Z.p;
-    zt.cull = ow.cull;
-    zt.cull_logtot = ow.sub0.p;
-    plan_pass(P, zt);
-    // Y = R~ Z : y_i = sum_j sqrt(a_i) e^{..} sqrt(b_j) z_j
-    count_launch();
-    k_pack_w<<<grid_for(m * kt), AUX_NT, 0, s>>>(ow.Z.p, m, m, block, kt, P.tgt.sw.p, ow.W.p);
-    PassSpec yr;
-    yr.dir = 1;
-    yr.in_v = g;
-    yr.out_v = f;
-    yr.out_lw = P.src.lsw.p;
-    yr.W = ow.W.p;
-    yr.k = block;
-    yr.kt = kt;
-    yr.out = Y;
-    yr.cull = ow.cull;
-    yr.cull_logtot = ow.sub1.p;
-    plan_pass(P, yr);
-    // Y -= sqrt(a) (sqrt(a)^T Y)
-    gram_all(P, n, block, 1, Y, n, P.src.sw.p, n, nullptr, P.misc.p, 0);
-    count_launch();
-    k_deflate<<<grid_for(n * block), AUX_NT, 0, s>>>(Y, n, block, P.src.sw.p, P.misc.p);
-}
-
-// Chebyshev three-term step: out = a * (AY - c * Y) - b * Yprev
-__global__ void k_cheb_step(const double* AY, const double* Y, const double* Yprev, int64_t count, double a,
-                            double c, double b, double* out) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = a * (AY[i] - c * Y[i]) - (Yprev ? b * Yprev[i] : 0.0);
-}
-
-// top_modes (spectral.cpp:125-193) on device; f, g are device vectors.
-// method 0: the reference's block subspace iteration (one operator application
-// per sweep; `sweeps` counts them). method 1 (opt-in, not in the reference):
-// Chebyshev-filtered subspace iteration -- each outer step applies a degree-q
-// Chebyshev polynomial of R~R~^T that damps the unwanted interval [0, theta_k]
-// (theta_k = smallest Ritz value of the block) before the same Rayleigh-Ritz
-// and the same residual test; `sweeps` then counts operator applications.
-// Host Cholesky (upper factor R with G = R^T R) of a k x k SPD matrix; false on breakdown.
-static bool host_chol_upper(const std::vector<double>& G, int k, std::vector<double>& R) {
-    R.assign(static_cast<size_t>(k) * k, 0.0);
-    for (int j = 0; j < k; ++j) {
-        double d = G[j + j * k];
-        for (int t = 0; t < j; ++t) d -= R[t + j * k] * R[t + j * k];
-        if (!(d > 0.0)) return false;
-        const double rjj = std::sqrt(d);
-        R[j + j * k] = rjj;
-        for (int c = j + 1; c < k; ++c) {
-            double v = G[j + c * k];
-            for (int t = 0; t < j; ++t) v -= R[t + j * k] * R[t + c * k];
-            R[j + c * k] = v / rjj;
-        }
-    }
-    return true;
-}
-// Inverse of an upper-triangular k x k matrix (col-major).
-static std::vector<double> host_upper_inv(const std::vector<double>& R, int k) {
-    std::vector<double> X(static_cast<size_t>(k) * k, 0.0);
-    for (int c = 0; c < k; ++c) {
-        X[c + c * k] = 1.0 / R[c + c * k];
-        for (int r = c - 1; r >= 0; --r) {
-            double s = 0.0;
-            for (int t = r + 1; t <= c; ++t) s += R[r + t * k] * X[t + c * k];
-            X[r + c * k] = -s / R[r + r * k];
-        }
-    }
-    return X;
-}
-
-// top_modes, method 2 (opt-in, not in the reference; the north star's "device-side
-// Lanczos/Krylov estimate"): restarted block Lanczos on the same operator R~R~^T with
-// sqrt(alpha) deflated. Each cycle builds s (12..16) blocks of b = ell+5 Krylov vectors with full
-// (two-pass) block reorthogonalisation and CholeskyQR2 for the next block, Rayleigh-Ritz
-// on the block-tridiagonal projection (host), and restarts from the top b Ritz vectors.
-// Convergence is declared with the reference's own criterion: the explicit residuals
-// ||R~R~^T x_a - theta_a x_a|| of the top ell Ritz pairs (one extra application) <= tol.
-// `sweeps` counts operator applications.
-static Basis top_modes_lanczos(Problem& P, const double* f, const double* g, int64_t ell, double tol,
-                               int64_t max_apps, int b, int steps) {
-    const int64_t n = P.n;
-    const int kt = block_kt_for(b);
-    const int s = std::max(12, std::min(steps, 16));  // shorter cycles restart too often (C4: 8 -> 423 apps)
-    cudaStream_t st = P.stream;
-    DBuf Qs, W, Xr, AX, R, dC, th;
-    Qs.ensure(static_cast<size_t>(s + 1) * n * b);
-    W.ensure(static_cast<size_t>(n) * b);
-    Xr.ensure(static_cast<size_t>(n) * b);
-    AX.ensure(static_cast<size_t>(n) * b);
-    R.ensure(static_cast<size_t>(n) * b);
-    dC.ensure(static_cast<size_t>(64) * 64 * 2);
-    th.ensure(64);
-    P.misc.ensure(256);
-    QrWork qw;
-    OpWork ow;
-    prepare_op_culling(P, f, g, ow);
-    qw.backup.ensure(static_cast<size_t>(n) * b);
-    auto Q = [&](int j) { return Qs.p + static_cast<size_t>(j) * n * b; };
-    count_launch();
-    k_splitmix_block<<<grid_for(n * b), AUX_NT, 0, st>>>(Q(0), n, b, 0x73706563ull, P.n_global, P.row_begin);
-    device_orth_deflated(P, Q(0), n, b, P.src.sw.p, qw);
-    auto host_gram = [&](const double* U, const double* V) {
-        gram_all(P, n, b, b, U, n, V, n, nullptr, dC.p, 0);
-        std::vector<double> h(static_cast<size_t>(b) * b);
-        download(h.data(), dC.p, static_cast<size_t>(b) * b, st);
-        CK(cudaStreamSynchronize(st));
-        return h;
-    };
-    auto gemm_acc = [&](const double* X, const std::vector<double>& M, int l, double sgn, double* out) {
-        upload(dC.p, M.data(), M.size(), st);
-        count_launch();
-        k_small_gemm_acc<<<grid_for(n), AUX_NT, sizeof(double) * b * l, st>>>(X, n, b, dC.p, l, sgn, out);
-    };
-    // W (n x b) -> Q_next R with CholeskyQR2; false when W is numerically rank deficient
-    auto cholqr2 = [&](double* Wp, double* Qnext, std::vector<double>& Bout) {
-        std::vector<double> R1, R2;
-        if (!host_chol_upper(host_gram(Wp, Wp), b, R1)) return false;
-        CK(cudaMemsetAsync(Qnext, 0, sizeof(double) * n * b, st));
-        gemm_acc(Wp, host_upper_inv(R1, b), b, 1.0, Qnext);
-        if (!host_chol_upper(host_gram(Qnext, Qnext), b, R2)) return false;
-        CK(cudaMemcpyAsync(Wp, Qnext, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemsetAsync(Qnext, 0, sizeof(double) * n * b, st));
-        gemm_acc(Wp, host_upper_inv(R2, b), b, 1.0, Qnext);
-        Bout.assign(static_cast<size_t>(b) * b, 0.0);  // B = R2 R1
-        for (int c = 0; c < b; ++c)
-            for (int r = 0; r <= c; ++r) {
-                double v = 0.0;
-                for (int t = r; t <= c; ++t) v += R2[r + t * b] * R1[t + c * b];
-                Bout[r + c * b] = v;
-            }
-        return true;
-    };
-
-    Basis out;
-    int64_t apps = 0;
-    double best = std::numeric_limits<double>::infinity();
-    std::vector<double> theta(ell);
-    while (apps < max_apps) {
-        const int K1 = (s + 1) * b;
-        std::vector<double> T(static_cast<size_t>(K1) * K1, 0.0), Blast;
-        int jmax = 0;
-        bool broke = false;
-        for (int j = 0; j < s && apps < max_apps; ++j) {
-            apply_sym_sym(P, f, g, Q(j), W.p, b, kt, ow);  // W = A Q_j (deflated)
-            ++apps;
-            for (int pass = 0; pass < 2; ++pass)
-                for (int i = 0; i <= j; ++i) {
-                    const std::vector<double> C = host_gram(Q(i), W.p);  // Q_i^T W
-                    gemm_acc(Q(i), C, b, -1.0, W.p);
-                    for (int c = 0; c < b; ++c)
-                        for (int r = 0; r < b; ++r) T[(i * b + r) + static_cast<size_t>(j * b + c) * K1] += C[r + c * b];
-                }
-            jmax = j + 1;
-            std::vector<double> B;
-            if (!cholqr2(W.p, Q(j + 1), B)) {  // invariant subspace reached
-                broke = true;
-                break;
-            }
-            for (int c = 0; c < b; ++c)
-                for (int r = 0; r < b; ++r) T[((j + 1) * b + r) + static_cast<size_t>(j * b + c) * K1] = B[r + c * b];
-            Blast = B;
-        }
-        // Rayleigh-Ritz on the symmetrised K x K projection
-        const int K = jmax * b;
-        std::vector<double> Ts(static_cast<size_t>(K) * K), ev, evec;
-        for (int c = 0; c < K; ++c)
-            for (int r = 0; r < K; ++r)
-                Ts[r + static_cast<size_t>(c) * K] =
-                    0.5 * (T[r + static_cast<size_t>(c) * K1] + T[c + static_cast<size_t>(r) * K1]);
-        host_sym_eig(Ts, K, ev, evec);  // ascending
-        // top b Ritz vectors: X = sum_i Q_i Y_i
-        CK(cudaMemsetAsync(Xr.p, 0, sizeof(double) * n * b, st));
-        for (int i = 0; i < jmax; ++i) {
-            std::vector<double> Yi(static_cast<size_t>(b) * b);
-            for (int a = 0; a < b; ++a)
-                for (int r = 0; r < b; ++r) Yi[r + a * b] = evec[(i * b + r) + static_cast<size_t>(K - 1 - a) * K];
-            gemm_acc(Q(i), Yi, b, 1.0, Xr.p);
-        }
-        for (int a = 0; a < ell; ++a) theta[a] = ev[K - 1 - a];
-        // cheap estimate ||B_last y_a(last block)||, then the explicit residual test
-        double est = 0.0;
-        if (!broke && !Blast.empty()) {
-            for (int a = 0; a < ell; ++a) {
-                double s2 = 0.0;
-                for (int r = 0; r < b; ++r) {
-                    double v = 0.0;
-                    for (int t = 0; t < b; ++t)
-                        v += Blast[r + t * b] * evec[((jmax - 1) * b + t) + static_cast<size_t>(K - 1 - a) * K];
-                    s2 += v * v;
-                }
-                est = std::max(est, std::sqrt(s2));
-            }
-        }
-        (void)est;  // the cheap bound is kept for diagnostics; the test below is the reference's
-        {
-            apply_sym_sym(P, f, g, Xr.p, AX.p, b, kt, ow);
-            ++apps;
-            upload(th.p, theta.data(), ell, st);
-            count_launch();
-            k_resid<<<grid_for(n * ell), AUX_NT, 0, st>>>(AX.p, Xr.p, th.p, n, static_cast<int>(ell), R.p);
-            gram_all(P, n, static_cast<int>(ell), static_cast<int>(ell), R.p, n, R.p, n, nullptr, P.misc.p, 0, 1);
-            std::vector<double> hres(ell);
-            download(hres.data(), P.misc.p, ell, st);
-            CK(cudaStreamSynchronize(st));
-            double max_res = 0.0;
-            for (int a = 0; a < ell; ++a) max_res = std::max(max_res, std::sqrt(hres[a]));
-            best = std::min(best, max_res);
-            if (max_res <= tol) break;
-        }
-        // restart from the top b Ritz vectors
-        CK(cudaMemcpyAsync(Q(0), Xr.p, sizeof(double) * n * b, cudaMemcpyDeviceToDevice, st));
-        device_orth_deflated(P, Q(0), n, b, P.src.sw.p, qw);
-        if (apps >= max_apps) break;
-    }
-    out.sweeps = apps;
-    if (!(best <= tol))
-        throw EigenFailure("top_modes: no convergence within max_power_iters, best residual " + std::to_string(best),
-                           best);
-    // vectors_sym = orth(top ell Ritz vectors); rhos = sqrt(max(theta,0)); vectors = vectors_sym ./ sqrt(alpha)
-    device_orth_deflated(P, Xr.p, n, static_cast<int>(ell), P.src.sw.p, qw);
-    count_launch();
-    k_div_rows<<<grid_for(n * ell), AUX_NT, 0, st>>>(Xr.p, P.src.sw.p, n, static_cast<int>(ell), R.p);
-    const int64_t ng = P.n_global;
-    out.vectors_sym.resize(ng * ell);
-    out.vectors.resize(ng * ell);
-    for (int64_t c = 0; c < ell; ++c) {
-        gather_rows(P, Xr.p + c * n, out.vectors_sym.data() + c * ng);
-        gather_rows(P, R.p + c * n, out.vectors.data() + c * ng);
-    }
-    out.rhos.resize(ell);
-    for (int a = 0; a < ell; ++a) out.rhos[a] = std::sqrt(std::max(theta[a], 0.0));
-    return out;
-}
-
-static Basis top_modes_device(Problem& P, const double* f, const double* g, int64_t ell, double tol,
-                              int64_t max_power_iters, int method = 0, int degree = 8) {
-    const int64_t n = P.n;
-    if (ell < 1) throw InvalidArgument("top_modes: ell must be >= 1");
-    if (ell >= P.n_global) throw InvalidArgument("top_modes: ell must be < n");
-    if (max_power_iters < 0) max_power_iters = 500 * ell;
-    const int block = static_cast<int>(std::min<int64_t>(ell + 5, P.n_global - 1));
-    if (block > 64) throw InvalidArgument("top_modes: ell + 5 > 64 is not supported by sknr_b200");
-    if (degree < 1) degree = 1;
-    if (method == 2) return top_modes_lanczos(P, f, g, ell, tol, max_power_iters, block, degree);
-    const int kt = block_kt_for(block);
-    cudaStream_t s = P.stream;
-    DBuf X, Y, Y2, XW, YW, R, Wd, th, Wfull;
-    X.ensure(n * block);
-    Y.ensure(n * block);
-    Y2.ensure(n * block);
-    XW.ensure(n * ell);
-    YW.ensure(n * ell);
-    R.ensure(n * ell);
-    Wd.ensure(block * ell);
-    Wfull.ensure(block * block);
-    th.ensure(ell);
-    P.misc.ensure(256);
-    QrWork qw;
-    OpWork ow;
-    prepare_op_culling(P, f, g, ow);
-    qw.backup.ensure(static_cast<size_t>(n) * block);
-    count_launch();
-    k_splitmix_block<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, n, block, 0x73706563ull, P.n_global,
-                                                            P.row_begin);
-    device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
-
-    DBuf T;
-    T.ensure(block * block);
-    std::vector<double> hT(block * block), ts(block * block), evals, evecs, hres(ell);
-    double best = std::numeric_limits<double>::infinity();
-    bool ok = false;
-    Basis out;
-    std::vector<double> theta(ell), w(block * ell);
-    int64_t applications = 0;
-    while (applications < max_power_iters) {
-        apply_sym_sym(P, f, g, X.p, Y.p, block, kt, ow);  // Y = A X
-        ++applications;
-        // Rayleigh-Ritz on the current orthonormal block
-        gram_all(P, n, block, block, X.p, n, Y.p, n, nullptr, T.p, 0);
-        download(hT.data(), T.p, block * block, s);
-        CK(cudaStreamSynchronize(s));
-        for (int a = 0; a < block; ++a)
-            for (int b = 0; b < block; ++b) ts[a + b * block] = 0.5 * (hT[a + b * block] + hT[b + a * block]);
-        host_sym_eig(ts, block, evals, evecs);
-        for (int a = 0; a < ell; ++a) {
-            for (int r = 0; r < block; ++r) w[r + a * block] = evecs[r + (block - 1 - a) * block];
-            theta[a] = evals[block - 1 - a];
-        }
-        upload(Wd.p, w.data(), block * ell, s);
-        upload(th.p, theta.data(), ell, s);
-        count_launch();
-        k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * ell, s>>>(X.p, n, block, Wd.p,
-                                                                              static_cast<int>(ell), XW.p);
-        count_launch();
-        k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * ell, s>>>(Y.p, n, block, Wd.p,
-                                                                              static_cast<int>(ell), YW.p);
-        count_launch();
-        k_resid<<<grid_for(n * ell), AUX_NT, 0, s>>>(YW.p, XW.p, th.p, n, static_cast<int>(ell), R.p);
-        gram_all(P, n, static_cast<int>(ell), static_cast<int>(ell), R.p, n, R.p, n, nullptr, P.misc.p, 0, 1);
-        download(hres.data(), P.misc.p, ell, s);
-        CK(cudaStreamSynchronize(s));
-        double max_res = 0.0;
-        for (int a = 0; a < ell; ++a) max_res = std::max(max_res, std::sqrt(hres[a]));
-        best = std::min(best, max_res);
-        if (max_res <= tol) {
-            ok = true;
-            break;
-        }
-        const bool tiny_gap = evals[0] < 1e-3 * evals[block - 1];  // fast decay: plain steps suffice
-        if (method == 0 || tiny_gap || applications + degree > max_power_iters) {
-            CK(cudaMemcpyAsync(X.p, Y.p, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
-        } else {
-            // rotate to the full Ritz basis, then filter with T_q on [0, theta_min]
-            upload(Wfull.p, evecs.data(), block * block, s);
-            count_launch();
-            k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * block, s>>>(X.p, n, block, Wfull.p,
-                                                                                    block, Y2.p);
-            count_launch();
-            k_small_gemm<<<grid_for(n), AUX_NT, sizeof(double) * block * block, s>>>(Y.p, n, block, Wfull.p,
-                                                                                    block, X.p);
-            // now Y2 = X W (basis), X = A X W (its image)
-            const double lo = 0.0, hi = std::max(evals[0], 0.0);
-            const double e = 0.5 * (hi - lo), c = 0.5 * (hi + lo);
-            double* Yprev = Y2.p;   // T_0 term
-            double* Ycur = Y.p;     // T_1 term
-            count_launch();
-            k_cheb_step<<<grid_for(n * block), AUX_NT, 0, s>>>(X.p, Y2.p, nullptr, n * block, 1.0 / e, c, 0.0,
-                                                               Ycur);
-            double* spare = X.p;
-            for (int q = 2; q <= degree; ++q) {
-                apply_sym_sym(P, f, g, Ycur, spare, block, kt, ow);  // spare = A Ycur
-                ++applications;
-                count_launch();
-                k_cheb_step<<<grid_for(n * block), AUX_NT, 0, s>>>(spare, Ycur, Yprev, n * block, 2.0 / e, c, 1.0,
-                                                                   spare);
-                std::swap(Yprev, Ycur);
-                std::swap(Ycur, spare);
-            }
-            if (Ycur != X.p)
-                CK(cudaMemcpyAsync(X.p, Ycur, sizeof(double) * n * block, cudaMemcpyDeviceToDevice, s));
-        }
-        device_orth_deflated(P, X.p, n, block, P.src.sw.p, qw);
-    }
-    out.sweeps = applications;
-    if (!ok)
-        throw EigenFailure(
-            "top_modes: no convergence within max_power_iters, best residual " + std::to_string(best),
-            best);
-    // vectors_sym = orth(XW); rhos = sqrt(max(theta,0)); vectors = vectors_sym ./ sqrt(alpha)
-    device_orth_deflated(P, XW.p, n, static_cast<int>(ell), P.src.sw.p, qw);
-    count_launch();
-    k_div_rows<<<grid_for(n * ell), AUX_NT, 0, s>>>(XW.p, P.src.sw.p, n, static_cast<int>(ell), R.p);
-    const int64_t ng = P.n_global;
-    out.vectors_sym.resize(ng * ell);
-    out.vectors.resize(ng * ell);
-    for (int64_t c = 0; c < ell; ++c) {
-        gather_rows(P, XW.p + c * n, out.vectors_sym.data() + c * ng);
-        gather_rows(P, R.p + c * n, out.vectors.data() + c * ng);
-    }
-    out.rhos.resize(ell);
-    for (int a = 0; a < ell; ++a) out.rhos[a] = std::sqrt(std::max(theta[a], 0.0));
-    return out;
-}
-
-// ============================================================ solve
-struct SolveState {
-    DBuf f, g, gnext, h, fcand, hcand, rowres, colres, am, r, Lr, V, Wv, S, delta, G;
-    DBuf trace_raw;  // sknr_record array (as doubles)
-};
-
-struct SolveOut {
-    std::vector<double> f, g;
-    int64_t iterations = 0;
-    bool converged = false;
-    std::vector<sknr_record> trace;
-};
-
-// Enqueue one SK-NR(ell) iteration (solver.cpp:104-151).
-static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace_enabled,
-                              int64_t trace_cap, bool exact_marginals = false,
-                              cudaGraphConditionalHandle loop = 0) {
-    const int64_t n = P.n, m = P.m;
-    cudaStream_t s = P.stream;
-    const bool newton = ell > 0;
-    count_launch();
-    k_iter_begin<<<1, 32, 0, s>>>(P.st);
-    // sk_sweep: g = f^{C,eps} (computed at the end of the previous iteration), f = g^{C,eps}
-    count_launch();
-    k_copy<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.gnext.p, m, P.st, G_DONE);
-    lse(P, 1, S.g.p, S.f.p, G_DONE);
-    // gauge (solver.cpp:108-112): c = alpha . f
-    {
-        RedArgs ra;
-        ra.T[0] = n;
-        ra.nterms = 1;
-        ra.x[0] = P.src.w.p;
-        ra.y[0] = S.f.p;
-        ra.op[0] = RED_DOT;
-        ra.out = P.sums.p + 8;
-        ra.part = P.gram_part.p;
-        ra.counter = &P.st->counters[6];
-        ra.epilogue = P.shard ? EPI_NONE : EPI_GAUGE;
-        ra.st = P.st;
-        ra.guard = G_DONE;
-        count_launch();
-        k_reduce<<<reduce_blocks(n), AUX_NT, 0, s>>>(ra);
-        if (P.shard) {
-            allreduce(P, P.sums.p + 8, 1, ncclSum);
-            count_launch();
-            k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_GAUGE, 0, P.sums.p + 8, G_DONE);
-        }
-    }
-    count_launch();
-    k_gauge_apply<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, S.g.p, m,
-                                                     P.inv_eps(), S.rowres.p, P.st);
-    // h = f^{C,eps}: the column marginal and the next sweep's g
-    lse(P, 0, S.f.p, S.h.p, G_DONE);
-    if (exact_marginals) {
-        // reference-faithful plan_marginals (core.cpp:120-143): explicit row and
-        // column sums of a_i b_j exp((f_i + g_j - C_ij)/eps) at the gauged (f, g)
-        PassSpec pr;
-        pr.dir = 1;
-        pr.in_v = S.g.p;
-        pr.in_lw = P.tgt.lw.p;
-        pr.out_v = S.f.p;
-        pr.out_lw = P.src.lw.p;
-        pr.out = S.rowres.p;
-        pr.guard = G_DONE;
-        plan_pass(P, pr);
-        PassSpec pc;
-        pc.dir = 0;
-        pc.in_v = S.f.p;
-        pc.in_lw = P.src.lw.p;
-        pc.out_v = S.g.p;
-        pc.out_lw = P.tgt.lw.p;
-        pc.out = S.colres.p;
-        pc.guard = G_DONE;
-        plan_pass(P, pc);
-        count_launch();
-        k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(S.rowres.p, P.src.w.p, n, 1.0, -1.0, S.rowres.p);
-        count_launch();
-        k_axpby<<<grid_for(m), AUX_NT, 0, s>>>(S.colres.p, P.tgt.w.p, m, 1.0, -1.0, S.colres.p);
-    } else {
-        count_launch();
-        k_colres<<<grid_for(m), AUX_NT, 0, s>>>(S.g.p, S.h.p, P.tgt.w.p, m, P.inv_eps(), S.colres.p, P.st,
-                                                G_DONE);
-    }
-    double* sums = P.sums.p;
-    // marginal_gap (core.cpp:145-150) + Q0 = a.f + b.h, stopping test on device
-    {
-        RedArgs ra;
-        ra.T[0] = n;
-        ra.T[1] = m;
-        ra.nterms = 6;
-        // layout: |row-a|^2, a.f, max|row-a| (sharded rows) | |col-b|^2, max|col-b|, b.h
-        const double* xs[6] = {S.rowres.p, P.src.w.p, S.rowres.p, S.colres.p, S.colres.p, P.tgt.w.p};
-        const double* ys[6] = {nullptr, S.f.p, nullptr, nullptr, nullptr, S.h.p};
-        const int ops[6] = {RED_SQ, RED_DOT, RED_MAXABS, RED_SQ, RED_MAXABS, RED_DOT};
-        for (int t = 0; t < 6; ++t) {
-            ra.x[t] = xs[t];
-            ra.y[t] = ys[t];
-            ra.op[t] = ops[t];
-            ra.seg[t] = t < 3 ? 0 : 1;
-        }
-        ra.out = sums;
-        ra.part = P.gram_part.p;
-        ra.counter = &P.st->counters[6];
-        ra.epilogue = P.shard ? EPI_NONE : EPI_CHECK;
-        ra.newton = newton ? 1 : 0;
-        ra.st = P.st;
-        ra.guard = G_DONE;
-        count_launch();
-        k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
-        if (P.shard) {
-            allreduce(P, sums, 2, ncclSum);
-            allreduce(P, sums + 2, 1, ncclMax);
-            count_launch();
-            k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_CHECK, newton ? 1 : 0, sums, G_DONE);
-        }
-    }
-    if (newton) {
-        const unsigned gn = G_DONE | G_NEWTON;
-        const int l = static_cast<int>(ell);
-        const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
-        const bool fuse_r = block_rs_fusable(P) && !cull_nr;
-        if (!fuse_r) {
-            // r = P~ beta at (f, h): alpha - r = -a expm1(f/eps + L_row(h))
-            lse(P, 1, S.h.p, nullptr, gn);
-            count_launch();
-            k_newton_r<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, P.L[1].p, P.src.w.p, n, P.inv_eps(), S.am.p,
-                                                      S.r.p, P.st, gn);
-        }
-        // S = V^T P~ (m x ell), P~_ij = a_i e^{(f_i + h_j - C_ij)/eps}; with fuse_r the
-        // same cells also give r = P~ beta (objective.cpp:127-128) in this pass
-        PassSpec sp;
-        sp.dir = 0;
-        sp.in_v = S.f.p;
-        sp.in_lw = P.src.lw.p;
-        sp.out_v = S.h.p;
-        sp.W = S.Wv.p;
-        sp.k = l;
-        sp.kt = block_kt_for(l);
-        sp.out = S.S.p;
-        sp.rsum_out = fuse_r ? S.r.p : nullptr;
-        sp.cull = cull_nr;  // P~ columns sum to 1 at h = f^{C,eps}: no normalisation needed
-        sp.guard = gn;
-        plan_pass(P, sp);
-        if (fuse_r) {
-            count_launch();
-            k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(P.src.w.p, S.r.p, n, 1.0, -1.0, S.am.p);
-        }
-        // (plan_pass has already summed S = V^T P~ over the row shards)
-        double* G1 = S.G.p;
-        double* cross = G1 + l * l;
-        double* grad = cross + l * l;
-        gram(P, n, l, l, S.V.p, n, S.V.p, n, S.r.p, G1, gn);
-        gram(P, m, l, l, S.S.p, m, S.S.p, m, P.tgt.w.p, cross, gn);
-        gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
-        allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
-        allreduce(P, grad, l, ncclSum);
-        count_launch();
-        k_newton_solve<<<1, 64, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
-                                                            P.st, gn);
-        count_launch();
-        k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
-        lse(P, 0, S.fcand.p, S.hcand.p, gn);
-        {
-            RedArgs ra;
-            ra.T[0] = n;
-            ra.T[1] = m;
-            ra.nterms = 2;
-            ra.x[0] = P.src.w.p;
-            ra.y[0] = S.fcand.p;
-            ra.x[1] = P.tgt.w.p;
-            ra.y[1] = S.hcand.p;
-            ra.op[0] = ra.op[1] = RED_DOT;
-            ra.seg[1] = 1;
-            ra.out = sums + 6;
-            ra.part = P.gram_part.p;
-            ra.counter = &P.st->counters[6];
-            ra.epilogue = P.shard ? EPI_NONE : EPI_ACCEPT;
-            ra.st = P.st;
-            ra.guard = gn;
-            count_launch();
-            k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
-            if (P.shard) {
-                allreduce(P, sums + 6, 1, ncclSum);
-                count_launch();
-                k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_ACCEPT, 0, sums + 6, gn);
-            }
-        }
-        count_launch();
-        k_select<<<grid_for(n + m), AUX_NT, 0, s>>>(S.f.p, S.fcand.p, n, S.gnext.p, S.h.p, S.hcand.p, m,
-                                                    P.st);
-    } else {
-        count_launch();
-        k_copy<<<grid_for(m), AUX_NT, 0, s>>>(S.gnext.p, S.h.p, m, P.st, G_DONE);
-    }
-    count_launch();
-    k_record<<<1, 32, 0, s>>>(P.st, reinterpret_cast<sknr_record*>(S.trace_raw.p), trace_cap,
-                              trace_enabled ? 1 : 0, loop);
-    CK(cudaGetLastError());
-}
-
-static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* basis_host,
-                          const double* init_f, int64_t max_iter, double tol, int64_t trace_cap) {
-    const int64_t n = P.n, m = P.m;
-    cudaStream_t s = P.stream;
-    S.f.ensure(n);
-    S.g.ensure(m);
-    S.gnext.ensure(m);
-    S.h.ensure(m);
-    S.fcand.ensure(n);
-    S.hcand.ensure(m);
-    S.rowres.ensure(n);
-    S.colres.ensure(m);
-    S.am.ensure(n);
-    S.r.ensure(n);
-    S.delta.ensure(64);
-    S.G.ensure(3 * 64 * 64);
-    S.trace_raw.ensure(std::max<int64_t>(trace_cap, 1) * (sizeof(sknr_record) / sizeof(double)));
-    P.misc.ensure(256);
-    if (ell > 0) {
-        const int kt = block_kt_for(static_cast<int>(ell));
-        S.V.ensure(n * ell);
-        S.Wv.ensure(n * kt);
-        S.S.ensure(m * ell);
-        upload_rows(P, S.V.p, basis_host, ell);
-        count_launch();
-        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,
-                                                     S.Wv.p);
-        // pre-size the block-pass partials outside graph capture
-        const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
-        plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
-    }
-    plan_for(P, 0, MODE_SUM, 0);
-    plan_for(P, 1, MODE_SUM, 0);
-    plan_for(P, 0, MODE_MAX, 0);
-    plan_for(P, 1, MODE_MAX, 0);
-    for (int dir = 0; dir < 2; ++dir)
-        if (cull_active(P, dir)) plan_for(P, dir, MODE_SUM_CULL, 0);
-    if (init_f)
-        upload_rows(P, S.f.p, init_f);
-    else {
-        count_launch();
-        k_fill<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, n, 0.0);
-    }
-    count_launch();
-    k_state_init<<<1, 32, 0, s>>>(P.st, max_iter, tol);
-    // first sweep's g = f0^{C,eps} (exact shift: no reference state yet)
-    lse(P, 0, S.f.p, S.gnext.p, G_NONE);
-    CK(cudaGetLastError());
-}
-
-static bool poll_done(Problem& P) {
-    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
-    CK(cudaStreamSynchronize(P.stream));
-    return P.st_host->done != 0;
-}
-
-static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell, const double* basis,
-                          const double* init_f, bool trace_enabled, int64_t trace_cap_hint,
-                          bool exact_marginals = false) {
-    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
-    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
-    if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
-    const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, std::max<int64_t>(trace_cap_hint, 1)) : 1;
-    if (!P.solve_cache) P.solve_cache = std::make_shared<SolveState>();
-    SolveState& S = *P.solve_cache;
-    prepare_solve(P, S, ell, basis, init_f, max_iter, tol, trace_cap);
-    cudaStream_t s = P.stream;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    if (!P.shard) {
-        // the whole solve as one graph: a WHILE node whose body is one iteration;
-        // k_record clears the loop condition once the stopping test (or max_iter) hits
-        CK(cudaGraphCreate(&graph, 0));
-        cudaGraphConditionalHandle loop = 0;
-        CK(cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault));
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = loop;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, loop);
-        CK(cudaStreamEndCapture(s, &body));
-        CK(cudaGraphInstantiate(&exec, graph, 0));
-        CK(cudaGraphLaunch(exec, s));
-        CK(cudaStreamSynchronize(s));
-    } else if (!P.emu) {
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
-        CK(cudaStreamEndCapture(s, &graph));
-        CK(cudaGraphInstantiate(&exec, graph, 0));
-    }
-    int64_t batch = 1;
-    int64_t launched = 0;
-    while (P.shard) {  // sharded (NCCL in the graph) and emulated shards: host-polled batches
-        for (int64_t b = 0; b < batch; ++b) {
-            if (exec)
-                CK(cudaGraphLaunch(exec, s));
-            else  // emulated shards: the same kernels and collectives, launched eagerly
-                enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
-            ++launched;
-        }
-        if (poll_done(P)) break;
-        if (launched >= max_iter + 2) break;
-        batch = std::min<int64_t>(batch * 2, 64);
-    }
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    SolveOut out;
-    out.f.resize(P.n_global);
-    out.g.resize(P.m);
-    gather_rows(P, S.f.p, out.f.data());
-    download(out.g.data(), S.g.p, P.m, s);
-    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    out.iterations = P.st_host->iter;
-    out.converged = P.st_host->conv != 0;
-    if (trace_enabled) {
-        const int64_t len = std::min<int64_t>(out.iterations, trace_cap);
-        out.trace.resize(len);
-        CK(cudaMemcpyAsync(out.trace.data(), S.trace_raw.p, sizeof(sknr_record) * len,
-                           cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
-    return out;
-}
-
-// Batched solve: B independent problems in one CUDA graph,
-// each as its own device-side WHILE loop (conditional node) over its iteration
-// body, so the loops run concurrently and each stops at its own stopping test.
-// Problems may differ in size and cost kind; every body issues exactly the
-// kernels of run_solve, so per-problem results are bitwise identical to solving
-// the problems one by one.
-struct BatchItem {
-    Problem* P = nullptr;
-    const double* basis = nullptr;
-    const double* init_f = nullptr;
-};
-
-static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, double tol, int64_t max_iter,
-                                             int64_t ell, bool exact_marginals) {
-    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
-    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
-    if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
-    const size_t B = items.size();
-    std::vector<SolveState*> Sp(B);
-    for (size_t b = 0; b < B; ++b) {
-        Problem& P = *items[b].P;
-        if (!P.solve_cache) P.solve_cache = std::make_shared<SolveState>();
-        Sp[b] = P.solve_cache.get();
-    }
-    auto S = [&](size_t b) -> SolveState& { return *Sp[b]; };
-    for (size_t b = 0; b < B; ++b) {
-        prepare_solve(*items[b].P, S(b), ell, items[b].basis, items[b].init_f, max_iter, tol, 1);
-        CK(cudaStreamSynchronize(items[b].P->stream));
-    }
-    cudaStream_t s0 = nullptr;
-    CK(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    std::vector<SolveOut> out(B);
-    try {
-        // one graph, one independent device-side WHILE loop per problem (conditional
-        // nodes without dependencies between them): each problem iterates until its own
-        // stopping test, none waits for the others
-        CK(cudaGraphCreate(&graph, 0));
-        for (size_t b = 0; b < B; ++b) {
-            Problem& P = *items[b].P;
-            cudaGraphConditionalHandle loop = 0;
-            CK(cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault));
-            cudaGraphNodeParams cp = {};
-            cp.type = cudaGraphNodeTypeConditional;
-            cp.conditional.handle = loop;
-            cp.conditional.type = cudaGraphCondTypeWhile;
-            cp.conditional.size = 1;
-            cudaGraphNode_t node;
-            CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
-            cudaGraph_t body = cp.conditional.phGraph_out[0];
-            CK(cudaStreamBeginCaptureToGraph(P.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals, loop);
-            CK(cudaStreamEndCapture(P.stream, &body));
-        }
-        CK(cudaGraphInstantiate(&exec, graph, 0));
-        CK(cudaGraphLaunch(exec, s0));
-        CK(cudaStreamSynchronize(s0));
-        for (size_t b = 0; b < B; ++b) {
-            Problem& P = *items[b].P;
-            out[b].f.resize(P.n_global);
-            out[b].g.resize(P.m);
-            download(out[b].f.data(), S(b).f.p, P.n, P.stream);
-            download(out[b].g.data(), S(b).g.p, P.m, P.stream);
-            CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
-        }
-        for (size_t b = 0; b < B; ++b) {
-            Problem& P = *items[b].P;
-            CK(cudaStreamSynchronize(P.stream));
-            out[b].iterations = P.st_host->iter;
-            out[b].converged = P.st_host->conv != 0;
-        }
-    } catch (...) {
-        if (exec) cudaGraphExecDestroy(exec);
-        if (graph) cudaGraphDestroy(graph);
-        cudaStreamDestroy(s0);
-        throw;
-    }
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    cudaStreamDestroy(s0);
-    return out;
-}
+#include "engine_spectral.cuh"
+#include "engine_solver.cuh"
 
 }  // namespace sknr
 
-// ============================================================ C ABI
-using namespace sknr;
-
-struct sknr_problem_s {
-    std::unique_ptr<Problem> p;
-};
-
-static thread_local std::string g_err;
-static thread_local double g_best_residual = 0.0;
-
-#define SKNR_API_BEGIN try {
-#define SKNR_API_END                        \
-    return SKNR_OK;                         \
-    }                                       \
-    catch (const InvalidArgument& e) {      \
-        g_err = e.what();                   \
-        return SKNR_EINVAL;                 \
-    }                                       \
-    catch (const EigenFailure& e) {         \
-        g_err = e.what();                   \
-        g_best_residual = e.best;           \
-        return SKNR_EEIGEN;                 \
-    }                                       \
-    catch (const CudaFailure& e) {          \
-        g_err = e.what();                   \
-        return SKNR_ECUDA;                  \
-    }                                       \
-    catch (const RuntimeFailure& e) {       \
-        g_err = e.what();                   \
-        return SKNR_ERUNTIME;               \
-    }                                       \
-    catch (const NcclFailure& e) {          \
-        g_err = e.what();                   \
-        return SKNR_ENCCL;                  \
-    }                                       \
-    catch (const std::exception& e) {       \
-        g_err = e.what();                   \
-        return SKNR_EINTERNAL;              \
-    }
-
-static Problem& get(sknr_problem h) {
-    if (!h || !h->p) throw InvalidArgument("sknr: null problem handle");
-    return *h->p;
-}
-
-static void check_finite_vec(const double* v, int64_t len, const char* what) {
-    if (!v) throw InvalidArgument(std::string(what) + ": null pointer");
-    for (int64_t i = 0; i < len; ++i)
-        if (!std::isfinite(v[i])) throw InvalidArgument(std::string(what) + ": entries must be finite");
-}
-
-extern "C" {
-
-const char* sknr_last_error(void) { return g_err.c_str(); }
-double sknr_last_best_residual(void) { return g_best_residual; }
-int64_t sknr_kernel_launch_count(void) { return launch_count(); }
-
-int sknr_version(char* buf, int cap) {
-    SKNR_API_BEGIN
-    std::string v = "sknr_b200 0.1.0 sm_100a";
-    int dev = 0, count = 0;
-    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
-        cudaDeviceProp prop;
-        cudaGetDevice(&dev);
-        if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
-            v += std::string(" (") + prop.name + ", " + std::to_string(prop.multiProcessorCount) + " SMs)";
-    } else {
-        v += " (no CUDA device)";
-    }
-    if (buf && cap > 0) {
-        std::strncpy(buf, v.c_str(), cap - 1);
-        buf[cap - 1] = 0;
-    }
-    SKNR_API_END
-}
-
-void sknr_config_default(sknr_config* c) {
-    c->tol_omega = 1e-9;
-    c->max_iter = 100000;
-    c->ell = 0;
-    c->newton_enabled = 1;
-    c->trace_enabled = 1;
-    c->exact_marginals = 0;
-    c->reserved = 0;
-}
-
-int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const double* alpha,
-                              const double* beta, double epsilon, sknr_problem* out) {
-    SKNR_API_BEGIN
-    *out = nullptr;
-    std::unique_ptr<Problem> p(new_problem(n, m, alpha, beta, epsilon));
-    finish_dense(p.get(), cost);
-    *out = new sknr_problem_s{std::move(p)};
-    SKNR_API_END
-}
-
-int sknr_problem_create_points_ex(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
-                                  double cost_scale, const double* alpha, const double* beta, double epsilon,
-                                  int cost_mode, sknr_problem* out);
-
-int sknr_problem_create_points(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
-                               double cost_scale, const double* alpha, const double* beta, double epsilon,
-                               sknr_problem* out) {
-    return sknr_problem_create_points_ex(x, y, n, m, d, cost_scale, alpha, beta, epsilon, 0, out);
-}
-
-int sknr_problem_create_points_ex(const double* x, const double* y, int64_t n, int64_t m, int64_t d,
-                                  double cost_scale, const double* alpha, const double* beta, double epsilon,
-                                  int cost_mode, sknr_problem* out) {
-    SKNR_API_BEGIN
-    if (cost_mode < 0 || cost_mode > 2) throw InvalidArgument("sknr_problem_create_points: cost_mode must be 0, 1 or 2");
-    *out = nullptr;
-    if (d < 1) throw InvalidArgument("sq_euclidean_cost: dimension must be >= 1");
-    check_finite_vec(x, n * d, "PointCloud(x)");
-    check_finite_vec(y, m * d, "PointCloud(y)");
-    if (!(cost_scale > 0.0) || !std::isfinite(cost_scale))
-        throw InvalidArgument("sq_euclidean_cost: cost_scale must be positive");
-    std::unique_ptr<Problem> p(new_problem(n, m, alpha, beta, epsilon));
-    finish_points(p.get(), x, y, d, cost_scale, cost_mode);
-    *out = new sknr_problem_s{std::move(p)};
-    SKNR_API_END
-}
-
-int sknr_problem_set_epsilon(sknr_problem h, double epsilon) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    if (!(epsilon > 0.0) || !std::isfinite(epsilon)) throw InvalidArgument("EotProblem: epsilon must be positive");
-    P.eps = epsilon;
-    count_launch();
-    k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-int sknr_problem_info(sknr_problem h, int64_t* n, int64_t* m, int64_t* d, double* epsilon, int* kind) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    // kind: 0 stored cost (given or materialised), 1 on the fly (registers), 2 on the fly (DMMA contraction)
-    if (n) *n = P.n;
-    if (m) *m = P.m;
-    if (d) *d = P.d;
-    if (epsilon) *epsilon = P.eps;
-    if (kind) *kind = P.dim > 0 ? 1 : (P.dim < 0 ? 2 : 0);
-    SKNR_API_END
-}
-
-// Morton order of a point set (centred coordinates, col-major count x d) in the
-// bounding box of both clouds; ties keep index order.
-static std::vector<int> morton_perm(const std::vector<double>& c, int64_t count, int d, const double* lo,
-                                    const double* hi) {
-    const int bits = std::min(21, 63 / d);
-    const double scale = static_cast<double>((1ull << bits) - 1);
-    std::vector<std::pair<uint64_t, int>> key(static_cast<size_t>(count));
-    for (int64_t i = 0; i < count; ++i) {
-        uint64_t q[4] = {0, 0, 0, 0};
-        for (int k = 0; k < d; ++k) {
-            const double span = hi[k] > lo[k] ? hi[k] - lo[k] : 1.0;
-            double v = (c[i + k * count] - lo[k]) / span * scale;
-            v = std::min(std::max(v, 0.0), scale);
-            q[k] = static_cast<uint64_t>(v);
-        }
-        uint64_t code = 0;
-        for (int b = bits - 1; b >= 0; --b)
-            for (int k = 0; k < d; ++k) code = (code << 1) | ((q[k] >> b) & 1ull);
-        key[static_cast<size_t>(i)] = {code, static_cast<int>(i)};
-    }
-    std::sort(key.begin(), key.end());
-    std::vector<int> perm(static_cast<size_t>(count));
-    for (int64_t i = 0; i < count; ++i) perm[static_cast<size_t>(i)] = key[static_cast<size_t>(i)].second;
-    return perm;
-}
-
-static void group_boxes(const std::vector<double>& c, int64_t count, int d, const std::vector<int>& perm, int g,
-                        DBuf& out) {
-    const int64_t ng = (count + g - 1) / g;
-    std::vector<double> box(static_cast<size_t>(ng) * 2 * d);
-    for (int64_t q = 0; q < ng; ++q)
-        for (int k = 0; k < d; ++k) {
-            double lo = std::numeric_limits<double>::infinity(), hi = -lo;
-            for (int64_t p = q * g; p < std::min(count, (q + 1) * g); ++p) {
-                const double v = c[perm[static_cast<size_t>(p)] + k * count];
-                lo = std::min(lo, v);
-                hi = std::max(hi, v);
-            }
-            box[q * 2 * d + k] = lo;
-            box[q * 2 * d + d + k] = hi;
-        }
-    out.ensure(box.size());
-    CK(cudaMemcpy(out.p, box.data(), box.size() * sizeof(double), cudaMemcpyHostToDevice));
-}
-
-static void prepare_culling(Problem& P) {
-    if (P.cull_ready) return;
-    const int d = static_cast<int>(P.d);
-    std::vector<double> xc(static_cast<size_t>(P.n * d)), yc(static_cast<size_t>(P.m * d));
-    CK(cudaMemcpy(xc.data(), P.src.coords.p, xc.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(yc.data(), P.tgt.coords.p, yc.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    double lo[4], hi[4];
-    for (int k = 0; k < d; ++k) {
-        lo[k] = std::numeric_limits<double>::infinity();
-        hi[k] = -lo[k];
-        for (int64_t i = 0; i < P.n; ++i) {
-            lo[k] = std::min(lo[k], xc[i + k * P.n]);
-            hi[k] = std::max(hi[k], xc[i + k * P.n]);
-        }
-        for (int64_t j = 0; j < P.m; ++j) {
-            lo[k] = std::min(lo[k], yc[j + k * P.m]);
-            hi[k] = std::max(hi[k], yc[j + k * P.m]);
-        }
-    }
-    const std::vector<int> px = morton_perm(xc, P.n, d, lo, hi), py = morton_perm(yc, P.m, d, lo, hi);
-    P.src.perm.assign(px);
-    P.tgt.perm.assign(py);
-    group_boxes(xc, P.n, d, px, 16, P.src.box16);
-    group_boxes(yc, P.m, d, py, 16, P.tgt.box16);
-    group_boxes(xc, P.n, d, px, 32, P.src.box32);
-    group_boxes(yc, P.m, d, py, 32, P.tgt.box32);
-    group_boxes(xc, P.n, d, px, 64, P.src.box64);
-    group_boxes(xc, P.n, d, px, 128, P.src.box128);
-    group_boxes(yc, P.m, d, py, 64, P.tgt.box64);
-    group_boxes(yc, P.m, d, py, 128, P.tgt.box128);
-    for (int dir = 0; dir < 2; ++dir) {
-        const int64_t nin = dir == 0 ? P.n : P.m, nout = dir == 0 ? P.m : P.n;
-        P.f_gi[dir].ensure((nin + CULL_GI - 1) / CULL_GI);
-        P.s_go[dir].ensure((nout + CULL_GO - 1) / CULL_GO);
-        P.f_g32[dir].ensure((nin + 31) / 32);
-        P.s_g16[dir].ensure((nout + 15) / 16);
-    }
-    P.cull_ready = true;
-}
-
-int sknr_problem_set_culling(sknr_problem h, double threshold) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (!(threshold >= 0.0) || !std::isfinite(threshold))
-        throw InvalidArgument("set_culling: threshold must be finite and >= 0");
-    if (threshold > 0.0) {
-        if (threshold < 40.0) throw InvalidArgument("set_culling: threshold below 40 would perturb the sums");
-        if (P.dim < 1 || P.dim > 4)
-            throw InvalidArgument("set_culling: needs a point-cloud problem with d <= 4");
-        prepare_culling(P);
-    }
-    P.cull_t = threshold;
-    SKNR_API_END
-}
-
-int sknr_problem_destroy(sknr_problem h) {
-    SKNR_API_BEGIN
-    delete h;
-    SKNR_API_END
-}
-
-static void reset_for_primitive(Problem& P) {
-    count_launch();
-    k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
-}
-
-int sknr_ctransform_of_f(sknr_problem h, const double* f, double* g) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n_global, "ctransform_of_f");
-    DBuf df, dg;
-    df.ensure(P.n);
-    dg.ensure(P.m);
-    upload_rows(P, df.p, f);
-    reset_for_primitive(P);
-    plan_for(P, 0, MODE_SUM, 0);
-    plan_for(P, 0, MODE_MAX, 0);
-    lse(P, 0, df.p, dg.p, G_NONE);
-    download(g, dg.p, P.m, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-int sknr_ctransform_of_g(sknr_problem h, const double* g, double* f) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(g, P.m, "ctransform_of_g");
-    DBuf df, dg;
-    df.ensure(P.n);
-    dg.ensure(P.m);
-    upload(dg.p, g, P.m, P.stream);
-    reset_for_primitive(P);
-    lse(P, 1, dg.p, df.p, G_NONE);
-    gather_rows(P, df.p, f);
-    SKNR_API_END
-}
-
-int sknr_plan_marginals(sknr_problem h, const double* f, const double* g, double* row, double* col,
-                        double* gap_l2, double* gap_inf) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n_global, "plan_marginals(f)");
-    check_finite_vec(g, P.m, "plan_marginals(g)");
-    DBuf df, dg, dr, dc;
-    df.ensure(P.n);
-    dg.ensure(P.m);
-    dr.ensure(P.n);
-    dc.ensure(P.m);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, P.m, P.stream);
-    // row_i = sum_j a_i b_j e^{..}: dir 1 (out i), column sums: dir 0 (out j)
-    PassSpec pr;
-    pr.dir = 1;
-    pr.in_v = dg.p;
-    pr.in_lw = P.tgt.lw.p;
-    pr.out_v = df.p;
-    pr.out_lw = P.src.lw.p;
-    pr.out = dr.p;
-    plan_pass(P, pr);
-    PassSpec pc;
-    pc.dir = 0;
-    pc.in_v = df.p;
-    pc.in_lw = P.src.lw.p;
-    pc.out_v = dg.p;
-    pc.out_lw = P.tgt.lw.p;
-    pc.out = dc.p;
-    plan_pass(P, pc);
-    std::vector<double> hr(P.n_global), hc(P.m);
-    gather_rows(P, dr.p, hr.data());
-    download(hc.data(), dc.p, P.m, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
-    const std::vector<double>& ha = P.h_alpha;
-    const std::vector<double>& hb = P.h_beta;
-    double sr = 0, sc = 0, mr = 0, mc = 0;
-    for (int64_t i = 0; i < P.n_global; ++i) {
-        const double d = hr[i] - ha[i];
-        sr += d * d;
-        mr = std::max(mr, std::abs(d));
-    }
-    for (int64_t j = 0; j < P.m; ++j) {
-        const double d = hc[j] - hb[j];
-        sc += d * d;
-        mc = std::max(mc, std::abs(d));
-    }
-    if (row) std::memcpy(row, hr.data(), sizeof(double) * P.n_global);
-    if (col) std::memcpy(col, hc.data(), sizeof(double) * P.m);
-    if (gap_l2) *gap_l2 = std::sqrt(sr) + std::sqrt(sc);
-    if (gap_inf) *gap_inf = mr + mc;
-    SKNR_API_END
-}
-
-int sknr_coupling_rows(sknr_problem h, const double* f, const double* g, int64_t row_begin, int64_t row_end,
-                       double* plan_rows) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (P.shard) throw RuntimeFailure("coupling_from: not available on a row-sharded problem");
-    if (row_begin < 0 || row_end > P.n || row_begin > row_end)
-        throw InvalidArgument("coupling_rows: row range out of bounds");
-    check_finite_vec(f, P.n, "coupling_from(f)");
-    check_finite_vec(g, P.m, "coupling_from(g)");
-    const int64_t rows = row_end - row_begin;
-    if (rows == 0) return SKNR_OK;
-    // host-side block size bounded to 1 GiB of device scratch per launch
-    const int64_t m = P.m;
-    const int64_t cap_rows = std::max<int64_t>(1, (int64_t(1) << 27) / std::max<int64_t>(m, 1));
-    DBuf df, dg, dp;
-    df.ensure(P.n);
-    dg.ensure(m);
-    upload(df.p, f, P.n, P.stream);
-    upload(dg.p, g, m, P.stream);
-    const bool whole = rows <= cap_rows;
-    dp.ensure((whole ? rows : cap_rows) * m);
-    std::vector<double> tmp;
-    for (int64_t r = row_begin; r < row_end; r += cap_rows) {
-        const int64_t cnt = std::min(cap_rows, row_end - r);
-        count_launch();
-        k_coupling<<<grid_for(cnt * m), AUX_NT, 0, P.stream>>>(
-            P.kind == 0 || P.C.p ? P.C.p : nullptr, P.src.coords.p, P.tgt.coords.p, P.n, m, r, cnt,
-            static_cast<int>(P.d), P.kappa, P.src.w.p, P.tgt.w.p, df.p, dg.p, P.inv_eps(), dp.p);
-        if (whole) {
-            download(plan_rows, dp.p, cnt * m, P.stream);
-        } else {  // scatter the cnt-row block into the rows-leading-dimension output
-            tmp.resize(cnt * m);
-            download(tmp.data(), dp.p, cnt * m, P.stream);
-            CK(cudaStreamSynchronize(P.stream));
-            for (int64_t j = 0; j < m; ++j)
-                std::memcpy(plan_rows + (r - row_begin) + j * rows, tmp.data() + j * cnt, sizeof(double) * cnt);
-        }
-    }
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan) {
-    return sknr_coupling_rows(h, f, g, 0, h && h->p ? h->p->n : 0, plan);
-}
-
-int sknr_semi_dual_value(sknr_problem h, const double* f, double* value) {
-    SKNR_API_BEGIN
-    std::vector<double> g(get(h).m);  // f^{C,eps}, then Q = a.f + b.g (objective.cpp:42-45)
-    int rc = sknr_ctransform_of_f(h, f, g.data());
-    if (rc != SKNR_OK) return rc;
-    Problem& P = get(h);
-    const std::vector<double>& a = P.h_alpha;
-    const std::vector<double>& b = P.h_beta;
-    double s1 = 0, s2 = 0;
-    for (int64_t i = 0; i < P.n_global; ++i) s1 += a[i] * f[i];
-    for (int64_t j = 0; j < P.m; ++j) s2 += b[j] * g[j];
-    *value = s1 + s2;
-    SKNR_API_END
-}
-
-int sknr_restricted_derivatives(sknr_problem h, const double* f, const double* g, const double* vectors,
-                                int64_t ell, double* grad, double* hess) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (ell < 1) throw InvalidArgument("restricted_derivatives: empty basis");
-    if (ell > 64) throw InvalidArgument("restricted_derivatives: ell > 64 is not supported by sknr_b200");
-    check_finite_vec(f, P.n_global, "restricted_derivatives(f)");
-    check_finite_vec(g, P.m, "restricted_derivatives(g)");
-    const int64_t n = P.n, m = P.m;
-    const int l = static_cast<int>(ell), kt = block_kt_for(l);
-    DBuf df, dg, V, Wv, Sm, am, r, G;
-    df.ensure(n);
-    dg.ensure(m);
-    V.ensure(n * ell);
-    Wv.ensure(n * kt);
-    Sm.ensure(m * ell);
-    am.ensure(n);
-    r.ensure(n);
-    G.ensure(3 * 64 * 64);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, m, P.stream);
-    upload_rows(P, V.p, vectors, ell);
-    count_launch();
-    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(V.p, n, n, l, kt, nullptr, Wv.p);
-    // r_i = a_i sum_j b_j e^{(f_i+g_j-C_ij)/eps} (objective.cpp:127-128): fused into the
-    // block pass for point clouds, else a plan-sum pass
-    const bool fuse_r = block_rs_fusable(P);
-    if (!fuse_r) {
-        PassSpec pr;
-        pr.dir = 1;
-        pr.in_v = dg.p;
-        pr.in_lw = P.tgt.lw.p;
-        pr.out_v = df.p;
-        pr.out_lw = P.src.lw.p;
-        pr.out = r.p;
-        plan_pass(P, pr);
-    }
-    PassSpec sp;
-    sp.dir = 0;
-    sp.in_v = df.p;
-    sp.in_lw = P.src.lw.p;
-    sp.out_v = dg.p;
-    sp.W = Wv.p;
-    sp.k = l;
-    sp.kt = kt;
-    sp.out = Sm.p;
-    sp.rsum_out = fuse_r ? r.p : nullptr;
-    plan_pass(P, sp);
-    // am = a - r
-    count_launch();
-    k_axpby<<<grid_for(n), AUX_NT, 0, P.stream>>>(P.src.w.p, r.p, n, 1.0, -1.0, am.p);
-    double* G1 = G.p;
-    double* cross = G1 + l * l;
-    double* gr = cross + l * l;
-    gram(P, n, l, l, V.p, n, V.p, n, r.p, G1, 0);
-    gram(P, m, l, l, Sm.p, m, Sm.p, m, P.tgt.w.p, cross, 0);
-    gram(P, n, l, 1, V.p, n, am.p, n, nullptr, gr, 0);
-    allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
-    allreduce(P, gr, l, ncclSum);
-    std::vector<double> hG1(l * l), hC(l * l);
-    download(hG1.data(), G1, l * l, P.stream);
-    download(hC.data(), cross, l * l, P.stream);
-    download(grad, gr, l, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
-    std::vector<double> H(l * l);
-    for (int a = 0; a < l; ++a)
-        for (int b = 0; b < l; ++b) H[a + b * l] = (-1.0 / P.eps) * (hG1[a + b * l] - hC[a + b * l]);
-    for (int a = 0; a < l; ++a)
-        for (int b = 0; b < l; ++b) hess[a + b * l] = 0.5 * (H[a + b * l] + H[b + a * l]);
-    SKNR_API_END
-}
-
-int sknr_apply_sym_t_block(sknr_problem h, const double* f, const double* g, const double* u, int64_t k,
-                           double* out) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (k < 1 || k > 64) throw InvalidArgument("apply_sym_t_block: 1 <= k <= 64 required");
-    const int64_t n = P.n, m = P.m;
-    const int kt = block_kt_for(static_cast<int>(k));
-    DBuf df, dg, U, W, O;
-    df.ensure(n);
-    dg.ensure(m);
-    U.ensure(n * k);
-    W.ensure(n * kt);
-    O.ensure(m * k);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, m, P.stream);
-    upload_rows(P, U.p, u, k);
-    count_launch();
-    k_pack_w<<<grid_for(n * kt), AUX_NT, 0, P.stream>>>(U.p, n, n, static_cast<int>(k), kt, nullptr, W.p);
-    PassSpec zt;
-    zt.dir = 0;
-    zt.in_v = df.p;
-    zt.in_lw = P.src.lsw.p;
-    zt.out_v = dg.p;
-    zt.W = W.p;
-    zt.k = static_cast<int>(k);
-    zt.kt = kt;
-    zt.out_scale = P.tgt.sw.p;
-    zt.out = O.p;
-    plan_pass(P, zt);
-    download(out, O.p, m * k, P.stream);
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-int sknr_apply_sym_block(sknr_problem h, const double* f, const double* g, const double* v, int64_t k,
-                         double* out) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (k < 1 || k > 64) throw InvalidArgument("apply_sym_block: 1 <= k <= 64 required");
-    const int64_t n = P.n, m = P.m;
-    const int kt = block_kt_for(static_cast<int>(k));
-    DBuf df, dg, Vv, W, O;
-    df.ensure(n);
-    dg.ensure(m);
-    Vv.ensure(m * k);
-    W.ensure(m * kt);
-    O.ensure(n * k);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, m, P.stream);
-    upload(Vv.p, v, m * k, P.stream);
-    count_launch();
-    k_pack_w<<<grid_for(m * kt), AUX_NT, 0, P.stream>>>(Vv.p, m, m, static_cast<int>(k), kt, P.tgt.sw.p,
-                                                        W.p);
-    PassSpec yr;
-    yr.dir = 1;
-    yr.in_v = dg.p;
-    yr.out_v = df.p;
-    yr.out_lw = P.src.lsw.p;
-    yr.W = W.p;
-    yr.k = static_cast<int>(k);
-    yr.kt = kt;
-    yr.out = O.p;
-    plan_pass(P, yr);
-    for (int64_t c = 0; c < k; ++c) gather_rows(P, O.p + c * n, out + c * P.n_global);
-    SKNR_API_END
-}
-
-int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
-                      int64_t max_power_iters, int method, int degree, double* vectors, double* vectors_sym,
-                      double* rhos, int64_t* sweeps);
-
-// ---- SinkhornOperator::apply_R / apply_Rt (spectral.cpp:29-62): one k=1 block pass each.
-// dir 1: (R g1)_i = sum_j e^{(f_i+g_j-C_ij)/eps} (b_j g1_j); dir 0: (Rt f1)_j = sum_i e^{..} (a_i f1_i)
-static void apply_R_dir(sknr_problem h, int dir, const double* f, const double* g, const double* v, double* out,
-                        const char* what) {
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n_global, "SinkhornOperator(f)");
-    check_finite_vec(g, P.m, "SinkhornOperator(g)");
-    const int64_t n = P.n, m = P.m;
-    const int64_t nv = dir == 0 ? n : m, nout = dir == 0 ? m : n;
-    if (!v) throw InvalidArgument(std::string(what) + ": null pointer");
-    const int kt = block_kt_for(1);
-    DBuf df, dg, dv, W, O;
-    df.ensure(n);
-    dg.ensure(m);
-    dv.ensure(nv);
-    W.ensure(nv * kt);
-    O.ensure(nout);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, m, P.stream);
-    if (dir == 0)
-        upload_rows(P, dv.p, v);
-    else
-        upload(dv.p, v, m, P.stream);
-    count_launch();
-    k_pack_w<<<grid_for(nv * kt), AUX_NT, 0, P.stream>>>(dv.p, nv, nv, 1, kt, dir == 0 ? P.src.w.p : P.tgt.w.p,
-                                                         W.p);
-    PassSpec ps;
-    ps.dir = dir;
-    ps.in_v = dir == 0 ? df.p : dg.p;
-    ps.out_v = dir == 0 ? dg.p : df.p;
-    ps.W = W.p;
-    ps.k = 1;
-    ps.kt = kt;
-    ps.out = O.p;
-    plan_pass(P, ps);
-    if (dir == 0)
-        download(out, O.p, m, P.stream);
-    else
-        gather_rows(P, O.p, out);
-    CK(cudaStreamSynchronize(P.stream));
-}
-
-int sknr_apply_R(sknr_problem h, const double* f, const double* g, const double* g1, double* out) {
-    SKNR_API_BEGIN
-    apply_R_dir(h, 1, f, g, g1, out, "apply_R");
-    SKNR_API_END
-}
-
-int sknr_apply_Rt(sknr_problem h, const double* f, const double* g, const double* f1, double* out) {
-    SKNR_API_BEGIN
-    apply_R_dir(h, 0, f, g, f1, out, "apply_Rt");
-    SKNR_API_END
-}
-
-// ---- dual_value (objective.cpp:10-40): a.f + b.g - eps expm1(log sum_ij a_i b_j e^{(f_i+g_j-C_ij)/eps}).
-// The double sum is taken as sum_i a_i e^{(f_i - f~_i)/eps} with f~ = g^{C,eps} (one row-LSE pass),
-// max-shifted on the host.
-int sknr_dual_value(sknr_problem h, const double* f, const double* g, double* value) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    const int64_t n = P.n_global, m = P.m;
-    if (!f || !g || !value) throw InvalidArgument("dual_value: null pointer");
-    for (int64_t i = 0; i < n; ++i)
-        if (!std::isfinite(f[i])) throw InvalidArgument("dual_value: potentials must be finite");
-    for (int64_t j = 0; j < m; ++j)
-        if (!std::isfinite(g[j])) throw InvalidArgument("dual_value: potentials must be finite");
-    std::vector<double> ft(n);
-    const int rc = sknr_ctransform_of_g(h, g, ft.data());
-    if (rc != SKNR_OK) return rc;
-    const double inv_eps = 1.0 / P.eps;
-    double shift = -std::numeric_limits<double>::infinity();
-    std::vector<double> t(n);
-    for (int64_t i = 0; i < n; ++i) {
-        t[i] = std::log(P.h_alpha[i]) + (f[i] - ft[i]) * inv_eps;
-        shift = std::max(shift, t[i]);
-    }
-    double total = 0.0;
-    for (int64_t i = 0; i < n; ++i) total += std::exp(t[i] - shift);
-    const double log_mass = shift + std::log(total);
-    double af = 0.0, bg = 0.0;
-    for (int64_t i = 0; i < n; ++i) af += P.h_alpha[i] * f[i];
-    for (int64_t j = 0; j < m; ++j) bg += P.h_beta[j] * g[j];
-    *value = af + bg - P.eps * std::expm1(log_mass);
-    SKNR_API_END
-}
-
-// ---- semi_dual_hessian_quadform (objective.cpp:53-77): -(1/eps) sum_j b_j (m2_j - m1_j^2) with
-// m1_j = sum_i P~_ij u_i, m2_j = sum_i P~_ij u_i^2 at g = f^{C,eps}: one k=2 block pass.
-int sknr_semi_dual_hessian_quadform(sknr_problem h, const double* f, const double* u, double* value) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    const int64_t n = P.n_global, m = P.m;
-    if (!u || !value) throw InvalidArgument("semi_dual_hessian_quadform: null pointer");
-    std::vector<double> g(m);
-    int rc = sknr_ctransform_of_f(h, f, g.data());
-    if (rc != SKNR_OK) return rc;
-    std::vector<double> U(2 * n);
-    for (int64_t i = 0; i < n; ++i) {
-        U[i] = u[i];
-        U[n + i] = u[i] * u[i];
-    }
-    std::vector<double> M(2 * m);
-    {
-        std::lock_guard<std::mutex> lk(P.mu);
-        const int kt = block_kt_for(2);
-        DBuf df, dg, dU, W, O;
-        df.ensure(P.n);
-        dg.ensure(m);
-        dU.ensure(2 * P.n);
-        W.ensure(P.n * kt);
-        O.ensure(2 * m);
-        upload_rows(P, df.p, f);
-        upload(dg.p, g.data(), m, P.stream);
-        upload_rows(P, dU.p, U.data(), 2);
-        count_launch();
-        k_pack_w<<<grid_for(P.n * kt), AUX_NT, 0, P.stream>>>(dU.p, P.n, P.n, 2, kt, nullptr, W.p);
-        PassSpec ps;
-        ps.dir = 0;
-        ps.in_v = df.p;
-        ps.in_lw = P.src.lw.p;
-        ps.out_v = dg.p;
-        ps.W = W.p;
-        ps.k = 2;
-        ps.kt = kt;
-        ps.out = O.p;
-        plan_pass(P, ps);
-        download(M.data(), O.p, 2 * m, P.stream);
-        CK(cudaStreamSynchronize(P.stream));
-    }
-    double acc = 0.0;
-    for (int64_t j = 0; j < m; ++j) acc += P.h_beta[j] * (M[m + j] - M[j] * M[j]);
-    *value = -acc / P.eps;
-    SKNR_API_END
-}
-
-// Eigen::LLT<Matrix>(A) convention (llt_inplace::unblocked): fails iff a pivot is <= 0 or NaN.
-static bool host_llt_solve(std::vector<double> A, int l, const double* b, double* x) {
-    for (int k = 0; k < l; ++k) {
-        double piv = A[k + k * l];
-        for (int j = 0; j < k; ++j) piv -= A[k + j * l] * A[k + j * l];
-        if (!(piv > 0.0)) return false;
-        const double d = std::sqrt(piv);
-        A[k + k * l] = d;
-        for (int i = k + 1; i < l; ++i) {
-            double s = A[i + k * l];
-            for (int j = 0; j < k; ++j) s -= A[i + j * l] * A[k + j * l];
-            A[i + k * l] = s / d;
-        }
-    }
-    std::vector<double> y(l);
-    for (int i = 0; i < l; ++i) {
-        double s = b[i];
-        for (int j = 0; j < i; ++j) s -= A[i + j * l] * y[j];
-        y[i] = s / A[i + i * l];
-    }
-    for (int i = l - 1; i >= 0; --i) {
-        double s = y[i];
-        for (int j = i + 1; j < l; ++j) s -= A[j + i * l] * x[j];
-        x[i] = s / A[i + i * l];
-    }
-    return true;
-}
-
-// ---- newton_step (solver.cpp:59-69 with try_newton :30-56): g = f^{C,eps}, Q0 = a.f + b.g,
-// restricted derivatives, LLT(-H) (reject on failure), delta, f' = f + V delta, accept iff Q(f') > Q0.
-int sknr_newton_step(sknr_problem h, const double* f, const double* vectors, int64_t ell, double* f_out,
-                     int* accepted, int* factorization_failed) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    if (ell < 1) throw InvalidArgument("newton_step: empty basis");
-    if (!vectors || !f_out || !accepted || !factorization_failed)
-        throw InvalidArgument("newton_step: null pointer");
-    const int64_t n = P.n_global, m = P.m;
-    const int l = static_cast<int>(ell);
-    std::vector<double> g(m), grad(l), hess(static_cast<size_t>(l) * l);
-    int rc = sknr_ctransform_of_f(h, f, g.data());
-    if (rc != SKNR_OK) return rc;
-    double af = 0.0, bg = 0.0;
-    for (int64_t i = 0; i < n; ++i) af += P.h_alpha[i] * f[i];
-    for (int64_t j = 0; j < m; ++j) bg += P.h_beta[j] * g[j];
-    const double value = af + bg;
-    rc = sknr_restricted_derivatives(h, f, g.data(), vectors, ell, grad.data(), hess.data());
-    if (rc != SKNR_OK) return rc;
-    std::vector<double> negH(hess.size()), delta(l);
-    for (size_t e = 0; e < hess.size(); ++e) negH[e] = -hess[e];
-    *accepted = 0;
-    *factorization_failed = 0;
-    std::memcpy(f_out, f, sizeof(double) * n);
-    if (!host_llt_solve(negH, l, grad.data(), delta.data())) {
-        *factorization_failed = 1;
-        return SKNR_OK;
-    }
-    std::vector<double> cand(n);
-    for (int64_t i = 0; i < n; ++i) {
-        double s = 0.0;
-        for (int c = 0; c < l; ++c) s += vectors[i + c * n] * delta[c];
-        cand[i] = f[i] + s;
-    }
-    double q1 = 0.0;
-    rc = sknr_semi_dual_value(h, cand.data(), &q1);
-    if (rc != SKNR_OK) return rc;
-    if (q1 > value) {
-        std::memcpy(f_out, cand.data(), sizeof(double) * n);
-        *accepted = 1;
-    }
-    SKNR_API_END
-}
-
-// ---- projector_distance (spectral.cpp:230-242): ||(I - A A^T) B||_2 for n x k column blocks,
-// via the largest eigenvalue of R^T R, R = B - A (A^T B); clamped to [0, 1]. Host arithmetic
-// (O(n k^2), a diagnostic off the solve path).
-int sknr_projector_distance(int64_t n, int64_t k, const double* a_sym, const double* b_sym, double* out) {
-    SKNR_API_BEGIN
-    if (n < 1 || k < 1 || !a_sym || !b_sym || !out) throw InvalidArgument("projector_distance: dimension mismatch");
-    std::vector<double> AtB(static_cast<size_t>(k) * k, 0.0), R(static_cast<size_t>(n) * k);
-    for (int64_t c = 0; c < k; ++c)
-        for (int64_t a = 0; a < k; ++a) {
-            double s = 0.0;
-            for (int64_t i = 0; i < n; ++i) s += a_sym[i + a * n] * b_sym[i + c * n];
-            AtB[a + c * k] = s;
-        }
-    for (int64_t c = 0; c < k; ++c)
-        for (int64_t i = 0; i < n; ++i) {
-            double s = 0.0;
-            for (int64_t a = 0; a < k; ++a) s += a_sym[i + a * n] * AtB[a + c * k];
-            R[i + c * n] = b_sym[i + c * n] - s;
-        }
-    std::vector<double> G(static_cast<size_t>(k) * k);
-    for (int64_t c = 0; c < k; ++c)
-        for (int64_t a = 0; a <= c; ++a) {
-            double s = 0.0;
-            for (int64_t i = 0; i < n; ++i) s += R[i + a * n] * R[i + c * n];
-            G[a + c * k] = G[c + a * k] = s;
-        }
-    std::vector<double> ev, evec;
-    host_sym_eig(G, static_cast<int>(k), ev, evec);
-    double lmax = 0.0;
-    for (double e : ev) lmax = std::max(lmax, e);
-    *out = std::clamp(std::sqrt(std::max(lmax, 0.0)), 0.0, 1.0);
-    SKNR_API_END
-}
-
-// ---- spectrum_report (spectral.cpp:195-228): top_modes at the anchor, Hessian eigenvalue pairs
-// (1 -+ rho)/eps, optional right vectors v = R~^T u / rho in potential coordinates.
-int sknr_spectrum_report(sknr_problem h, const double* f, const double* g, int64_t k, int include_vectors,
-                         double tol, int64_t max_power_iters, double* rhos, double* hess_low, double* hess_high,
-                         double* vectors_f, double* vectors_g) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    const int64_t n = P.n_global, m = P.m;
-    if (k < 1 || k > std::min(n, m) - 1) throw InvalidArgument("spectrum_report: need 1 <= k <= min(n,m)-1");
-    if (!rhos || !hess_low || !hess_high) throw InvalidArgument("spectrum_report: null pointer");
-    std::vector<double> vec(static_cast<size_t>(n) * k), vsym(static_cast<size_t>(n) * k);
-    int64_t sweeps = 0;
-    int rc = sknr_top_modes(h, f, g, k, tol, max_power_iters, vec.data(), vsym.data(), rhos, &sweeps);
-    if (rc != SKNR_OK) return rc;
-    for (int64_t a = 0; a < k; ++a) {
-        hess_low[a] = (1.0 - rhos[a]) / P.eps;
-        hess_high[a] = (1.0 + rhos[a]) / P.eps;
-    }
-    if (include_vectors) {
-        if (!vectors_f || !vectors_g) throw InvalidArgument("spectrum_report: null pointer");
-        std::memcpy(vectors_f, vec.data(), sizeof(double) * n * k);
-        std::vector<double> vs(static_cast<size_t>(m) * k);
-        rc = sknr_apply_sym_t_block(h, f, g, vsym.data(), k, vs.data());
-        if (rc != SKNR_OK) return rc;
-        for (int64_t a = 0; a < k; ++a)
-            for (int64_t j = 0; j < m; ++j)
-                vectors_g[j + a * m] = rhos[a] > 1e-12 ? (vs[j + a * m] / rhos[a]) / std::sqrt(P.h_beta[j]) : 0.0;
-    }
-    SKNR_API_END
-}
-
-
-int sknr_top_modes(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
-                   int64_t max_power_iters, double* vectors, double* vectors_sym, double* rhos,
-                   int64_t* sweeps) {
-    return sknr_top_modes_ex(h, f, g, ell, tol, max_power_iters, 0, 1, vectors, vectors_sym, rhos, sweeps);
-}
-
-int sknr_top_modes_ex(sknr_problem h, const double* f, const double* g, int64_t ell, double tol,
-                      int64_t max_power_iters, int method, int degree, double* vectors, double* vectors_sym,
-                      double* rhos, int64_t* sweeps) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    check_finite_vec(f, P.n_global, "SinkhornOperator(f)");
-    check_finite_vec(g, P.m, "SinkhornOperator(g)");
-    DBuf df, dg;
-    df.ensure(P.n);
-    dg.ensure(P.m);
-    upload_rows(P, df.p, f);
-    upload(dg.p, g, P.m, P.stream);
-    if (method < 0 || method > 2)
-        throw InvalidArgument("top_modes: method must be 0 (subspace), 1 (chebyshev) or 2 (lanczos)");
-    Basis b = top_modes_device(P, df.p, dg.p, ell, tol, max_power_iters, method, degree);
-    std::memcpy(vectors, b.vectors.data(), sizeof(double) * P.n_global * ell);
-    std::memcpy(vectors_sym, b.vectors_sym.data(), sizeof(double) * P.n_global * ell);
-    std::memcpy(rhos, b.rhos.data(), sizeof(double) * ell);
-    if (sweeps) *sweeps = b.sweeps;
-    SKNR_API_END
-}
-
-static void validate_config(const sknr_config* cfg, const double* basis, int64_t basis_ell, int64_t n) {
-    if (!(cfg->tol_omega > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
-    if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
-    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
-    if (use_newton) {
-        if (basis == nullptr) throw InvalidArgument("solve: ell > 0 requires a basis");
-        if (basis_ell != cfg->ell) throw InvalidArgument("solve: basis has wrong column count");
-    }
-    (void)n;
-}
-
-int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int64_t basis_ell,
-               const double* init_f, const double* init_g, double* f_out, double* g_out,
-               int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
-               int64_t* trace_len) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    validate_config(cfg, basis, basis_ell, P.n);
-    if ((init_f == nullptr) != (init_g == nullptr))
-        throw InvalidArgument("solve: init potential sizes mismatch");
-    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
-    const int64_t ell = use_newton ? cfg->ell : 0;
-    SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
-                           std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1),
-                           cfg->exact_marginals != 0);
-    std::memcpy(f_out, o.f.data(), sizeof(double) * P.n_global);
-    std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
-    if (iterations) *iterations = o.iterations;
-    if (converged) *converged = o.converged ? 1 : 0;
-    const int64_t len = static_cast<int64_t>(o.trace.size());
-    if (trace_len) *trace_len = len;
-    if (trace)
-        for (int64_t t = 0; t < len && t < trace_cap; ++t) trace[t] = o.trace[t];
-    SKNR_API_END
-}
-
-int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_config* cfg,
-                     const double* const* bases, int64_t basis_ell, const double* const* init_f,
-                     const double* const* init_g, double* const* f_out, double* const* g_out, int64_t* iterations,
-                     int* converged) {
-    SKNR_API_BEGIN
-    if (count < 1 || !problems || !cfg || !f_out || !g_out) throw InvalidArgument("solve_batch: empty batch");
-    if ((init_f == nullptr) != (init_g == nullptr)) throw InvalidArgument("solve: init potential sizes mismatch");
-    std::vector<BatchItem> items(static_cast<size_t>(count));
-    std::vector<std::unique_lock<std::mutex>> locks;
-    for (int64_t b = 0; b < count; ++b) {
-        Problem& P = get(problems[b]);
-        for (int64_t c = 0; c < b; ++c)
-            if (problems[c] == problems[b]) throw InvalidArgument("solve_batch: duplicate problem handle");
-        if (P.shard) throw InvalidArgument("solve_batch: row-sharded problems are not supported");
-        validate_config(cfg, bases ? bases[b] : nullptr, basis_ell, P.n);
-        if (init_f && ((init_f[b] == nullptr) != (init_g[b] == nullptr)))
-            throw InvalidArgument("solve: init potential sizes mismatch");
-        if (!f_out[b] || !g_out[b]) throw InvalidArgument("solve_batch: null output");
-        items[b].P = &P;
-        items[b].basis = bases ? bases[b] : nullptr;
-        items[b].init_f = init_f ? init_f[b] : nullptr;
-        locks.emplace_back(P.mu);
-    }
-    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
-    std::vector<SolveOut> o = run_solve_batch(items, cfg->tol_omega, cfg->max_iter, use_newton ? cfg->ell : 0,
-                                              cfg->exact_marginals != 0);
-    for (int64_t b = 0; b < count; ++b) {
-        std::memcpy(f_out[b], o[b].f.data(), sizeof(double) * items[b].P->n_global);
-        std::memcpy(g_out[b], o[b].g.data(), sizeof(double) * items[b].P->m);
-        if (iterations) iterations[b] = o[b].iterations;
-        if (converged) converged[b] = o[b].converged ? 1 : 0;
-    }
-    SKNR_API_END
-}
-
-// Small-problem batch: every problem solved by plain SK (ell = 0) from f = 0 inside one
-// CTA of one kernel launch (launch_sk_small); point clouds of one dimension d <= 4 with
-// n, m <= 2048 each. Problems may differ in n, m, epsilon and cost scale.
-int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int64_t* m, const double* const* x,
-                           const double* const* y, const double* const* a, const double* const* b,
-                           const double* eps, const double* cost_scale, double tol, int64_t max_iter,
-                           double* const* f_out, double* const* g_out, int64_t* iterations, int* converged) {
-    SKNR_API_BEGIN
-    check_device();
-    if (count < 1) throw InvalidArgument("solve_small_batch: empty batch");
-    if (d < 1 || d > 4) throw InvalidArgument("solve_small_batch: 1 <= d <= 4 required");
-    if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
-    if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
-    if (!n || !m || !x || !y || !a || !b || !eps || !f_out || !g_out)
-        throw InvalidArgument("solve_small_batch: null pointer");
-    // one device arena: per problem x (n d), y (m d), a (n), b (m), f (n), g (m), h (m)
-    std::vector<size_t> off(static_cast<size_t>(count) + 1, 0);
-    for (int64_t q = 0; q < count; ++q) {
-        if (n[q] < 1 || m[q] < 1 || n[q] > kSmallMax || m[q] > kSmallMax)
-            throw InvalidArgument("solve_small_batch: 1 <= n, m <= 2048 required");
-        if (!(eps[q] > 0.0)) throw InvalidArgument("EotProblem: epsilon must be positive");
-        validate_measure(a[q], n[q]);
-        validate_measure(b[q], m[q]);
-        off[q + 1] = off[q] + static_cast<size_t>((n[q] + m[q]) * d + 2 * n[q] + 3 * m[q]);
-    }
-    DBuf arena, dprobs;
-    arena.ensure(off[count]);
-    std::vector<SmallProbDev> hp(static_cast<size_t>(count));
-    std::vector<double> host(off[count], 0.0);
-    for (int64_t q = 0; q < count; ++q) {
-        double* base = host.data() + off[q];
-        const int64_t nq = n[q], mq = m[q];
-        std::memcpy(base, x[q], sizeof(double) * nq * d);
-        std::memcpy(base + nq * d, y[q], sizeof(double) * mq * d);
-        std::memcpy(base + (nq + mq) * d, a[q], sizeof(double) * nq);
-        std::memcpy(base + (nq + mq) * d + nq, b[q], sizeof(double) * mq);
-        double* dev = arena.p + off[q];
-        SmallProbDev& s = hp[q];
-        s.x = dev;
-        s.y = dev + nq * d;
-        s.a = dev + (nq + mq) * d;
-        s.b = s.a + nq;
-        s.f = const_cast<double*>(s.b) + mq;  // zero-filled: SK from f = 0
-        s.g = s.f + nq;
-        s.h = s.g + mq;
-        s.n = static_cast<int>(nq);
-        s.m = static_cast<int>(mq);
-        s.eps = eps[q];
-        s.kappa = cost_scale ? cost_scale[q] : 1.0;
-    }
-    const size_t words = (sizeof(SmallProbDev) * static_cast<size_t>(count) + sizeof(double) - 1) / sizeof(double);
-    dprobs.ensure(words);
-    cudaStream_t s = nullptr;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CK(cudaMemcpyAsync(arena.p, host.data(), sizeof(double) * off[count], cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dprobs.p, hp.data(), sizeof(SmallProbDev) * count, cudaMemcpyHostToDevice, s));
-    launch_sk_small(static_cast<int>(d), reinterpret_cast<SmallProbDev*>(dprobs.p), static_cast<int>(count), tol,
-                    max_iter, 0, s);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(host.data(), arena.p, sizeof(double) * off[count], cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp.data(), dprobs.p, sizeof(SmallProbDev) * count, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    cudaStreamDestroy(s);
-    for (int64_t q = 0; q < count; ++q) {
-        const double* base = host.data() + off[q];
-        const int64_t nq = n[q], mq = m[q];
-        const double* fq = base + (nq + mq) * d + nq + mq;
-        std::memcpy(f_out[q], fq, sizeof(double) * nq);
-        std::memcpy(g_out[q], fq + nq, sizeof(double) * mq);
-        if (iterations) iterations[q] = hp[q].iters;
-        if (converged) converged[q] = hp[q].conv;
-    }
-    SKNR_API_END
-}
-
-int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm_mode, int refresh_basis,
-                const sknr_config* cfg, double* f_out, double* g_out, int64_t* iterations, int* converged,
-                sknr_record* trace, int64_t trace_cap, int64_t* trace_offsets, int64_t* trace_len) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    if (stages < 1) throw InvalidArgument("anneal: empty schedule");
-    for (int64_t s = 1; s < stages; ++s)
-        if (!(epsilons[s] < epsilons[s - 1]))
-            throw InvalidArgument("anneal: epsilons must be strictly decreasing");
-    if (!(cfg->tol_omega > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
-    if (cfg->max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
-    const double eps0 = P.eps;
-    const int64_t n = P.n_global, m = P.m;
-    int64_t tl = 0;
-    Basis basis;
-    bool have_basis = false;
-    std::vector<double> prev_f, prev_g;
-    auto set_eps = [&](double e) {
-        P.eps = e;
-        count_launch();
-        k_invalidate_refs<<<1, 32, 0, P.stream>>>(P.st);
-    };
-    try {
-        for (int64_t s = 0; s < stages; ++s) {
-            int64_t ell = 0;
-            const double* bptr = nullptr;
-            if (s > 0 && warm_mode == 2 && cfg->ell > 0) {
-                if (!have_basis || refresh_basis) {
-                    set_eps(epsilons[s - 1]);
-                    DBuf df, dg;
-                    df.ensure(n);
-                    dg.ensure(m);
-                    upload_rows(P, df.p, prev_f.data());
-                    upload(dg.p, prev_g.data(), m, P.stream);
-                    try {
-                        basis = top_modes_device(P, df.p, dg.p, cfg->ell, 1e-8, -1);
-                    } catch (const EigenFailure& e) {
-                        throw EigenFailure("anneal stage " + std::to_string(s) + ": " + e.what(), e.best);
-                    }
-                    have_basis = true;
-                }
-                ell = cfg->newton_enabled ? cfg->ell : 0;
-                bptr = basis.vectors.data();
-            }
-            set_eps(epsilons[s]);
-            const double* init = (s > 0 && warm_mode != 0) ? prev_f.data() : nullptr;
-            SolveOut o;
-            try {
-                o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, bptr, init, cfg->trace_enabled != 0,
-                              cfg->max_iter, cfg->exact_marginals != 0);
-            } catch (const InvalidArgument& e) {
-                throw RuntimeFailure("anneal stage " + std::to_string(s) + ": " + e.what());
-            }
-            std::memcpy(f_out + s * n, o.f.data(), sizeof(double) * n);
-            std::memcpy(g_out + s * m, o.g.data(), sizeof(double) * m);
-            iterations[s] = o.iterations;
-            converged[s] = o.converged ? 1 : 0;
-            trace_offsets[s] = tl;
-            for (size_t t = 0; t < o.trace.size(); ++t, ++tl)
-                if (trace && tl < trace_cap) trace[tl] = o.trace[t];
-            prev_f = std::move(o.f);
-            prev_g = std::move(o.g);
-        }
-    } catch (...) {
-        set_eps(eps0);
-        throw;
-    }
-    if (trace_len) *trace_len = tl;
-    set_eps(eps0);
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* ms_per_pass,
-                    double* kernel_ms_per_pass) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    const int64_t n = P.n, m = P.m;
-    cudaStream_t s = P.stream;
-    DBuf f, g, V, Wv, Sm;
-    f.ensure(n);
-    g.ensure(m);
-    count_launch();
-    k_fill<<<grid_for(n), AUX_NT, 0, s>>>(f.p, n, 0.0);
-    count_launch();
-    k_state_init<<<1, 32, 0, s>>>(P.st, 1, 1.0);
-    plan_for(P, 0, MODE_SUM, 0);
-    plan_for(P, 1, MODE_SUM, 0);
-    plan_for(P, 0, MODE_MAX, 0);
-    plan_for(P, 1, MODE_MAX, 0);
-    lse(P, 0, f.p, g.p, G_NONE);  // realistic g; seeds the reference state
-    lse(P, 1, g.p, f.p, G_NONE);
-    const int l = static_cast<int>(std::max<int64_t>(ell, 1));
-    const int kt = block_kt_for(l);
-    if (which >= 3) {
-        V.ensure(n * l);
-        Wv.ensure(std::max(n, m) * kt);
-        Sm.ensure(std::max(n, m) * l);
-        count_launch();
-        k_fill<<<grid_for(n * l), AUX_NT, 0, s>>>(V.p, n * l, 1.0 / std::sqrt(static_cast<double>(n)));
-        count_launch();
-        k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(V.p, n, n, l, kt, nullptr, Wv.p);
-        plan_for(P, 0, MODE_BLOCK, kt, 8);
-    }
-    CK(cudaStreamSynchronize(s));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    TilePlan tsum = plan_for(P, 0, MODE_SUM, 0);
-    auto one = [&]() {
-        switch (which) {
-            case 0: lse(P, 0, f.p, g.p, G_NONE); break;
-            case 1: lse(P, 1, g.p, f.p, G_NONE); break;
-            case 2: launch_tiles(tsum, tile_args(P, 0, tsum, G_NONE), s); break;
-            default: {
-                PassSpec sp;
-                sp.dir = 0;
-                sp.in_v = f.p;
-                sp.in_lw = P.src.lw.p;
-                sp.out_v = g.p;
-                sp.W = Wv.p;
-                sp.k = l;
-                sp.kt = kt;
-                sp.out = Sm.p;
-                plan_pass(P, sp);
-            }
-        }
-    };
-    one();
-    CK(cudaStreamSynchronize(s));
-    CK(cudaEventRecord(e0, s));
-    for (int t = 0; t < passes; ++t) one();
-    CK(cudaEventRecord(e1, s));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_per_pass = ms / passes;
-    if (kernel_ms_per_pass) {
-        // the dominant tile kernel alone, on the same stream
-        TilePlan tp = which == 1 ? plan_for(P, 1, MODE_SUM, 0)
-                                 : (which >= 3 ? plan_for(P, 0, MODE_BLOCK, kt, 8) : tsum);
-        TileArgs ta = tile_args(P, which == 1 ? 1 : 0, tp, G_NONE);
-        if (which >= 3) ta.W = Wv.p;
-        CK(cudaEventRecord(e0, s));
-        for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
-        CK(cudaEventRecord(e1, s));
-        CK(cudaEventSynchronize(e1));
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        *kernel_ms_per_pass = ms / passes;
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    CK(cudaGetLastError());
-    SKNR_API_END
-}
-
-int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* basis, int64_t basis_ell,
-                          int64_t warmup, int64_t iters, int flush_l2, double* ms_per_iter,
-                          int64_t* kernels_per_iter) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
-    if (use_newton && (basis == nullptr || basis_ell != cfg->ell))
-        throw InvalidArgument("solve: ell > 0 requires a basis");
-    const int64_t ell = use_newton ? cfg->ell : 0;
-    if (P.emu) throw InvalidArgument("sknr_bench_iterations: not available on emulated shards");
-    SolveState S;
-    prepare_solve(P, S, ell, basis, nullptr, warmup + iters + 1000000, 1e-300, 1);
-    cudaStream_t s = P.stream;
-    DBuf flush;
-    if (flush_l2) flush.ensure((256ull << 20) / sizeof(double));  // 256 MiB > 126 MB L2
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    const int64_t l0 = launch_count();
-    enqueue_iteration(P, S, ell, false, 1);
-    if (kernels_per_iter) *kernels_per_iter = launch_count() - l0;
-    CK(cudaStreamEndCapture(s, &graph));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
-    for (int64_t t = 0; t < std::max<int64_t>(warmup, 1); ++t) CK(cudaGraphLaunch(exec, s));
-    CK(cudaStreamSynchronize(s));
-    std::vector<cudaEvent_t> ev(2 * iters);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
-    for (int64_t t = 0; t < iters; ++t) {
-        if (flush_l2) CK(cudaMemsetAsync(flush.p, t & 0xFF, flush.n * sizeof(double), s));
-        CK(cudaEventRecord(ev[2 * t], s));
-        CK(cudaGraphLaunch(exec, s));
-        CK(cudaEventRecord(ev[2 * t + 1], s));
-    }
-    CK(cudaStreamSynchronize(s));
-    double total = 0.0;
-    for (int64_t t = 0; t < iters; ++t) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev[2 * t], ev[2 * t + 1]));
-        total += ms;
-    }
-    for (auto& e : ev) cudaEventDestroy(e);
-    *ms_per_iter = total / static_cast<double>(std::max<int64_t>(iters, 1));
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    SKNR_API_END
-}
-
-// FP64 pipe ceiling on this device: 8 independent DFMA chains per thread, a
-// full grid of 148 x 8 CTAs of 256 threads, timed with CUDA events.
-__global__ void k_fp64_peak(double* out, int iters, double a0, double b0) {
-    // per-thread register operands (3 distinct register pairs per DFMA)
-    const double a = a0 + threadIdx.x * 1e-12, b = b0 * (1.0 + threadIdx.x * 1e-9);
-    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-10, x2 = x0 + 2e-10, x3 = x0 + 3e-10;
-    double x4 = x0 + 4e-10, x5 = x0 + 5e-10, x6 = x0 + 6e-10, x7 = x0 + 7e-10;
-    double y0 = a * 1.5, y1 = a * 1.25, y2 = a * 1.125, y3 = a, y4 = a * 0.5, y5 = a * 0.75, y6 = a * 0.875, y7 = a;
-    for (int i = 0; i < iters; ++i) {
-        x0 = fma(x0, y0, b); x1 = fma(x1, y1, b); x2 = fma(x2, y2, b); x3 = fma(x3, y3, b);
-        x4 = fma(x4, y4, b); x5 = fma(x5, y5, b); x6 = fma(x6, y6, b); x7 = fma(x7, y7, b);
-    }
-    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
-    if (s == 12345.678) out[0] = s;
-}
-
-// Time launch-configuration variant v of the d=2 column-LSE sum kernel on this
-// problem's current packed state (tuning aid; see tools/tune_lse.py).
-int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    const bool block = variant >= 200;
-    if (variant < 100 && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
-    if (variant >= 100 && variant < 200 && P.dim != 0)
-        throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
-    if (block && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
-    const int64_t n = P.n, m = P.m;
-    cudaStream_t s = P.stream;
-    DBuf f, g, V, Wv;
-    f.ensure(n);
-    g.ensure(m);
-    count_launch();
-    k_fill<<<grid_for(n), AUX_NT, 0, s>>>(f.p, n, 0.0);
-    count_launch();
-    k_state_init<<<1, 32, 0, s>>>(P.st, 1, 1.0);
-    plan_for(P, 0, MODE_SUM, 0);
-    plan_for(P, 0, MODE_MAX, 0);
-    lse(P, 0, f.p, g.p, G_NONE);
-    lse(P, 0, f.p, g.p, G_NONE);  // leaves the bound-shift pack in place
-    const int kt = 32;
-    TilePlan tp = plan_tiles(P.dim, block ? MODE_BLOCK : MODE_SUM, block ? kt : 0, m, n, block ? 8 : 0, variant);
-    if (!tp.fn) throw InvalidArgument("sknr_tune_variant: unknown variant");
-    P.partial.ensure(static_cast<size_t>(tp.n_in_blocks) * m * (block ? kt : 1));
-    TileArgs ta = tile_args(P, 0, tp, G_NONE);
-    if (block) {
-        V.ensure(n * kt);
-        Wv.ensure(n * kt);
-        count_launch();
-        k_fill<<<grid_for(n * kt), AUX_NT, 0, s>>>(Wv.p, n * kt, 1.0 / std::sqrt(static_cast<double>(n)));
-        ta.W = Wv.p;
-        P.rsum.ensure(static_cast<size_t>(tp.n_out_tiles) * n);  // for the fused-r variants
-        ta.out_w = P.tgt.w.p;
-        ta.rsum = P.rsum.p;
-    }
-    launch_tiles(tp, ta, s);
-    CK(cudaStreamSynchronize(s));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, s));
-    for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
-    CK(cudaEventRecord(e1, s));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    *kernel_ms = ms / passes;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    CK(cudaGetLastError());
-    SKNR_API_END
-}
-
-// Diagnostics: the first 16 entries of the handle's reduction scratch (sums of the last
-// stopping test / acceptance test / gauge).
-int sknr_debug_sums(sknr_problem h, double* out) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    CK(cudaMemcpyAsync(out, P.sums.p, sizeof(double) * 16, cudaMemcpyDeviceToHost, P.stream));
-    CK(cudaStreamSynchronize(P.stream));
-    SKNR_API_END
-}
-
-// Diagnostics: [exact col, exact row, retry col, retry row] counters since creation.
-int sknr_debug_counters(sknr_problem h, int64_t* out) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, P.stream));
-    CK(cudaStreamSynchronize(P.stream));
-    out[0] = static_cast<int64_t>(P.st_host->n_exact[0]);
-    out[1] = static_cast<int64_t>(P.st_host->n_exact[1]);
-    out[2] = static_cast<int64_t>(P.st_host->n_retry[0]);
-    out[3] = static_cast<int64_t>(P.st_host->n_retry[1]);
-    out[4] = static_cast<int64_t>(P.st_host->n_cull_tested);
-    out[5] = static_cast<int64_t>(P.st_host->n_cull_kept);
-    SKNR_API_END
-}
-
-int sknr_bench_fp64_peak(double* tflops, double* ms) {
-    SKNR_API_BEGIN
-    check_device();
-    int sms = 0, dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    DBuf out;
-    out.ensure(1);
-    const int iters = 16000, grid = sms * 8, block = 256;
-    k_fp64_peak<<<grid, block>>>(out.p, 100, 0.5, 1e-7);
-    CK(cudaDeviceSynchronize());
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0));
-    count_launch();
-    k_fp64_peak<<<grid, block>>>(out.p, iters, 0.5, 1e-7);
-    CK(cudaEventRecord(e1));
-    CK(cudaEventSynchronize(e1));
-    float t = 0;
-    CK(cudaEventElapsedTime(&t, e0, e1));
-    const double flops = 2.0 * 8.0 * iters * static_cast<double>(grid) * block;
-    *tflops = flops / (t * 1e-3) / 1e12;
-    if (ms) *ms = t;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    SKNR_API_END
-}
-
-// ---------------------------------------------------------------- multi-GPU (row sharding)
-int sknr_comm_unique_id(unsigned char id[128]) {
-    SKNR_API_BEGIN
-    g_nccl.load();
-    ncclUniqueId uid;
-    NK(g_nccl.GetUniqueId(&uid));
-    std::memcpy(id, uid.internal, NCCL_UNIQUE_ID_BYTES);
-    SKNR_API_END
-}
-
-int sknr_comm_init(int rank, int world, const unsigned char id[128], int device) {
-    SKNR_API_BEGIN
-    if (world < 1 || rank < 0 || rank >= world) throw InvalidArgument("sknr_comm_init: bad rank/world");
-    check_device();
-    if (device >= 0) CK(cudaSetDevice(device));
-    g_nccl.load();
-    if (g_comm.comm) {
-        g_nccl.CommDestroy(g_comm.comm);
-        g_comm.comm = nullptr;
-    }
-    ncclUniqueId uid;
-    std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
-    NK(g_nccl.CommInitRank(&g_comm.comm, world, uid, rank));
-    g_comm.rank = rank;
-    g_comm.world = world;
-    SKNR_API_END
-}
-
-// Testing: an in-process group of `world` emulated ranks on the current GPU (see
-// EmuGroup). Shards created afterwards route their collectives through it; each
-// rank's calls must come from its own host thread.
-int sknr_comm_init_emulated(int world) {
-    SKNR_API_BEGIN
-    if (world < 1 || world > kEmuMax) throw InvalidArgument("sknr_comm_init_emulated: 1 <= world <= 16 required");
-    check_device();
-    g_emu.init(world);
-    SKNR_API_END
-}
-
-int sknr_comm_destroy(void) {
-    SKNR_API_BEGIN
-    g_emu.destroy();
-    if (g_comm.comm) {
-        g_nccl.CommDestroy(g_comm.comm);
-        g_comm.comm = nullptr;
-    }
-    g_comm.world = 1;
-    g_comm.rank = 0;
-    SKNR_API_END
-}
-
-// Keep only this rank's source rows; column partials, the gauge scalar, the
-// marginal residuals and the Newton inner products are merged with NCCL.
-int sknr_problem_shard(sknr_problem h, int64_t row_begin, int64_t row_end) {
-    SKNR_API_BEGIN
-    Problem& P = get(h);
-    std::lock_guard<std::mutex> lk(P.mu);
-    const bool emu = g_emu.world > 0;
-    if (!g_comm.comm && !emu) throw RuntimeFailure("sknr_problem_shard: call sknr_comm_init first");
-    if (P.shard) throw InvalidArgument("sknr_problem_shard: problem already sharded");
-    const int world = emu ? g_emu.world : g_comm.world;
-    int rank = emu ? -1 : g_comm.rank;
-    if (emu)  // the emulated rank is the one whose standard block this is
-        for (int r = 0; r < world; ++r) {
-            int64_t rb, re;
-            row_partition(P.n_global, world, r, rb, re);
-            if (rb == row_begin && re == row_end) rank = r;
-        }
-    int64_t b = 0, e = 0;
-    if (rank >= 0) row_partition(P.n_global, world, rank, b, e);
-    if (rank < 0 || row_begin != b || row_end != e)
-        throw InvalidArgument("sknr_problem_shard: rows must follow the standard partition [n*r/R, n*(r+1)/R)");
-    const int64_t nl = e - b, n = P.n_global, m = P.m;
-    if (nl < 1) throw InvalidArgument("sknr_problem_shard: empty row block");
-    cudaStream_t s = P.stream;
-    auto slice = [&](DBuf& buf, int64_t cols) {
-        if (!buf.p) return;
-        DBuf tmp;
-        tmp.ensure(nl * cols);
-        for (int64_t c = 0; c < cols; ++c)
-            CK(cudaMemcpyAsync(tmp.p + c * nl, buf.p + c * n + b, sizeof(double) * nl, cudaMemcpyDeviceToDevice, s));
-        CK(cudaStreamSynchronize(s));
-        std::swap(buf.p, tmp.p);
-        std::swap(buf.n, tmp.n);
-    };
-    slice(P.src.w, 1);
-    slice(P.src.lw, 1);
-    slice(P.src.sw, 1);
-    slice(P.src.lsw, 1);
-    slice(P.src.sq, 1);
-    slice(P.src.coords, P.d);
-    if (P.C.p) {
-        DBuf c2, ct2;
-        c2.ensure(nl * m);
-        ct2.ensure(nl * m);
-        CK(cudaMemcpy2DAsync(c2.p, sizeof(double) * nl, P.C.p + b, sizeof(double) * n, sizeof(double) * nl, m,
-                             cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(ct2.p, P.CT.p + b * m, sizeof(double) * nl * m, cudaMemcpyDeviceToDevice, s));
-        CK(cudaStreamSynchronize(s));
-        std::swap(P.C.p, c2.p);
-        std::swap(P.C.n, c2.n);
-        std::swap(P.CT.p, ct2.p);
-        std::swap(P.CT.n, ct2.n);
-    }
-    P.src.count = nl;
-    P.n = nl;
-    P.row_begin = b;
-    P.shard = true;
-    P.emu = emu;
-    P.rank = rank;
-    P.world = world;
-    P.plans.clear();
-    if (P.cull_ready) {  // re-derive the Morton order and group boxes for the local rows
-        P.cull_ready = false;
-        prepare_culling(P);
-    }
-    count_launch();
-    k_invalidate_refs<<<1, 32, 0, s>>>(P.st);
-    CK(cudaStreamSynchronize(s));
-    SKNR_API_END
-}
-
-}  // extern "C"
+#include "engine_capi.cuh"
