@@ -272,7 +272,11 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     cudaStream_t s = P.stream;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    if (!P.shard) {
+    // SKNR_HOST_LOOP=1: one graph per iteration, host-polled (profilers such as ncu do not
+    // see kernels inside conditional-node bodies)
+    static const bool host_loop = std::getenv("SKNR_HOST_LOOP") != nullptr;
+    const bool polled = P.shard || host_loop;
+    if (!polled) {
         // the whole solve as one graph: a WHILE node whose body is one iteration;
         // k_record clears the loop condition once the stopping test (or max_iter) hits
         CK(cudaGraphCreate(&graph, 0));
@@ -300,7 +304,7 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     }
     int64_t batch = 1;
     int64_t launched = 0;
-    while (P.shard) {  // sharded (NCCL in the graph) and emulated shards: host-polled batches
+    while (polled) {  // sharded (NCCL in the graph), emulated shards, SKNR_HOST_LOOP: host-polled batches
         for (int64_t b = 0; b < batch; ++b) {
             if (exec)
                 CK(cudaGraphLaunch(exec, s));
