@@ -73,12 +73,14 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
         a.part[2 * blockIdx.x + 1] = bmin;
     }
     if (!last_block(&a.st->counters[a.dir])) return;
+    double mx = -kInf, mn = kInf;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        mx = fmax(mx, a.part[2 * b]);
+        mn = fmin(mn, a.part[2 * b + 1]);
+    }
+    mx = block_reduce(mx, sh, MaxOp());
+    mn = block_reduce(mn, sh, MinOp());
     if (threadIdx.x == 0) {
-        double mx = -kInf, mn = kInf;
-        for (unsigned b = 0; b < gridDim.x; ++b) {
-            mx = fmax(mx, a.part[2 * b]);
-            mn = fmin(mn, a.part[2 * b + 1]);
-        }
         if (a.defer) {  // sharded: decided by k_decide after the cross-rank max
             a.st->scratch[2 * a.dir] = mx;
             a.st->scratch[2 * a.dir + 1] = -mn;
@@ -143,39 +145,82 @@ __global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk
 }
 
 // ------------------------------------------------------------------ finalize
+// Split-K partials are folded column-wise: a block owns 32 consecutive output
+// entries q (one per lane) and its 8 warps take the partial rows b = w, w+8, ...
+// in increasing order; warp 0 then adds the 8 warp sums in warp order. Every
+// load of a warp is one 256-byte row segment, each thread issues nb/8 independent
+// loads, and the summation order is fixed by (nb, layout) alone: deterministic.
+constexpr int FOLD_W = AUX_NT / 32;
+
+template <bool MAX>
+__device__ __forceinline__ double fold_rows(const double* __restrict__ p, int64_t nb, int64_t stride,
+                                            int64_t q, bool valid, double (*sh)[32]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double s = MAX ? -kInf : 0.0;
+    if (valid) {
+        const double* col = p + q;
+#pragma unroll 4
+        for (int64_t b = w; b < nb; b += FOLD_W) {
+            const double v = col[b * stride];
+            s = MAX ? fmax(s, v) : s + v;
+        }
+    }
+    sh[w][lane] = s;
+    __syncthreads();
+    if (w == 0) {
+        s = sh[0][lane];
+#pragma unroll
+        for (int k = 1; k < FOLD_W; ++k) s = MAX ? fmax(s, sh[k][lane]) : s + sh[k][lane];
+    }
+    __syncthreads();
+    return s;  // valid in warp 0
+}
+
+#define FOLD_LOOP(Q)                                                                      \
+    for (int64_t q0 = static_cast<int64_t>(blockIdx.x) * 32; q0 < (Q);                  \
+         q0 += static_cast<int64_t>(gridDim.x) * 32)
+
 // Exact shift: shift_o += max_u / L64, B_o recomputed from it.
 __global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {
     if (guard_skip(a.st, a.guard)) return;
-    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.n_out;
-         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double M = -kInf;
-        for (int64_t b = 0; b < a.nb; ++b) M = fmax(M, a.partial[b * a.n_out + o]);
-        const double s = a.shift[o] + M * kInvLS;
-        a.shift[o] = s;
-        double e = 0.0;
-        if (a.sq) e -= a.kc * a.sq[o];
-        a.pack[o * a.pk] = kLS * (e - s);
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(a.n_out) {
+        const int64_t o = q0 + (threadIdx.x & 31);
+        const double M = fold_rows<true>(a.partial, a.nb, a.n_out, o, o < a.n_out, sh);
+        if (threadIdx.x < 32 && o < a.n_out) {
+            const double s = a.shift[o] + M * kInvLS;
+            a.shift[o] = s;
+            double e = 0.0;
+            if (a.sq) e -= a.kc * a.sq[o];
+            a.pack[o * a.pk] = kLS * (e - s);
+        }
     }
 }
 
 // L_o = shift_o + log(sum_b partial[b][o]); pot_o = -eps L_o. A sum outside
-// [2^-900, 2^900] means the bound shift was too loose: request the exact path.
+// [2^-900, 2^900] means the bound shift was too loose: request the exact path
+// (n_retry counts the 32-output chunks that saw such a sum).
 __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
     if (guard_skip(a.st, a.guard)) return;
-    bool bad = false;
-    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < a.n_out;
-         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double S = 0.0;
-        for (int64_t b = 0; b < a.nb; ++b) S += a.partial[b * a.n_out + o];
-        const bool ok = S >= 0x1p-900 && S <= 0x1p900;
-        bad |= !ok;
-        const double L = a.shift[o] + log(S);
-        if (a.L) a.L[o] = L;
-        if (a.pot) a.pot[o] = -a.eps * L;
-    }
-    if (bad && !a.retry_phase && !a.st->need_exact[a.dir]) {
-        a.st->retry[a.dir] = 1;
-        atomicAdd(&a.st->n_retry[a.dir], 1ull);
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(a.n_out) {
+        const int64_t o = q0 + (threadIdx.x & 31);
+        const bool valid = o < a.n_out;
+        const double S = fold_rows<false>(a.partial, a.nb, a.n_out, o, valid, sh);
+        if (threadIdx.x < 32) {
+            bool bad = false;
+            if (valid) {
+                bad = !(S >= 0x1p-900 && S <= 0x1p900);
+                const double L = a.shift[o] + log(S);
+                if (a.L) a.L[o] = L;
+                if (a.pot) a.pot[o] = -a.eps * L;
+            }
+            if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0 && !a.retry_phase &&
+                !a.st->need_exact[a.dir]) {
+                a.st->retry[a.dir] = 1;
+                atomicAdd(&a.st->n_retry[a.dir], 1ull);
+            }
+        }
     }
 }
 
@@ -184,11 +229,11 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
 __global__ void __launch_bounds__(AUX_NT) k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n,
                                                           double* out, const DevState* st, unsigned guard) {
     if (guard_skip(st, guard)) return;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (int64_t t = 0; t < n_tiles; ++t) s += rsum[t * n + i];
-        out[i] = s;
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(n) {
+        const int64_t i = q0 + (threadIdx.x & 31);
+        const double s = fold_rows<false>(rsum, n_tiles, n, i, i < n, sh);
+        if (threadIdx.x < 32 && i < n) out[i] = s;
     }
 }
 
@@ -196,11 +241,11 @@ __global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, 
                                                          int64_t n_out, const double* scale,
                                                          double* out, DevState* st, unsigned guard) {
     if (guard_skip(st, guard)) return;
-    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < n_out;
-         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double S = 0.0;
-        for (int64_t b = 0; b < nb; ++b) S += partial[b * n_out + o];
-        out[o] = scale ? scale[o] * S : S;
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(n_out) {
+        const int64_t o = q0 + (threadIdx.x & 31);
+        const double S = fold_rows<false>(partial, nb, n_out, o, o < n_out, sh);
+        if (threadIdx.x < 32 && o < n_out) out[o] = scale ? scale[o] * S : S;
     }
 }
 
@@ -217,19 +262,35 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_commit(const double* in_vec, dou
     }
 }
 
+// partial layout [b][c][o] (c < kt): entry q = c*n_out + o of the first k columns
+// is the contiguous range q < k*n_out of each row b (row stride kt*n_out).
 __global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial, int64_t nb, int kt,
                                                            int k, int64_t n_out, const double* scale,
                                                            double* out, int64_t ld, DevState* st,
                                                            unsigned guard) {
     if (guard_skip(st, guard)) return;
+    __shared__ double sh[FOLD_W][32];
     const int64_t total = n_out * k;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t o = e % n_out;
-        const int64_t c = e / n_out;
-        double S = 0.0;
-        for (int64_t b = 0; b < nb; ++b) S += partial[(b * kt + c) * n_out + o];
-        out[o + c * ld] = scale ? scale[o] * S : S;
+    FOLD_LOOP(total) {
+        const int64_t e = q0 + (threadIdx.x & 31);
+        const double S = fold_rows<false>(partial, nb, kt * n_out, e, e < total, sh);
+        if (threadIdx.x < 32 && e < total) {
+            const int64_t o = e % n_out;
+            const int64_t c = e / n_out;
+            out[o + c * ld] = scale ? scale[o] * S : S;
+        }
+    }
+}
+
+// Column fold of gram partials: out[q] = scale * sum_b part[b*Q + q].
+__global__ void __launch_bounds__(AUX_NT) k_fold_sum(const double* part, int64_t nb, int64_t Q, double scale,
+                                                     double* out, const DevState* st, unsigned guard) {
+    if (guard_skip(st, guard)) return;
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(Q) {
+        const int64_t q = q0 + (threadIdx.x & 31);
+        const double S = fold_rows<false>(part, nb, Q, q, q < Q, sh);
+        if (threadIdx.x < 32 && q < Q) out[q] = scale * S;
     }
 }
 
@@ -298,22 +359,19 @@ __global__ void __launch_bounds__(AUX_NT) k_gram(GramArgs a) {
             acc[q] = s;
         }
     }
+    // one block: the result directly; several: rows of partials for k_fold_sum
+    double* dst = gridDim.x == 1 ? a.out : a.part + static_cast<int64_t>(blockIdx.x) * npairs;
+    const double sc = gridDim.x == 1 ? a.out_scale : 1.0;
 #pragma unroll
     for (int q = 0; q < QMAX; ++q) {
         const int p = threadIdx.x + q * AUX_NT;
-        if (p < npairs) a.part[static_cast<int64_t>(blockIdx.x) * npairs + p] = acc[q];
+        if (p < npairs) dst[p] = sc * acc[q];
     }
-    if (!last_block(a.counter)) return;
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-        double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += a.part[static_cast<int64_t>(b) * npairs + p];
-        a.out[p] = a.out_scale * s;
-    }
-    if (threadIdx.x == 0) *a.counter = 0u;
+    // several blocks: the host folds the partial rows with k_fold_sum
 }
 
 int reduce_blocks(int64_t T) {
-    int64_t b = (T + AUX_NT * 8 - 1) / (AUX_NT * 8);
+    int64_t b = (T + RED_PER_BLOCK - 1) / RED_PER_BLOCK;
     if (b < 1) b = 1;
     if (b > 296) b = 296;
     return static_cast<int>(b);
@@ -357,7 +415,7 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
         const int64_t T = a.T[seg];
         int64_t g = gridDim.x;
         if (seg == 1) {
-            g = (T + AUX_NT * 8 - 1) / (AUX_NT * 8);  // reduce_blocks(T[1])
+            g = (T + RED_PER_BLOCK - 1) / RED_PER_BLOCK;  // reduce_blocks(T[1])
             g = g < 1 ? 1 : (g > 296 ? 296 : g);
             g = g < gridDim.x ? g : gridDim.x;
             if (blockIdx.x >= g) continue;
@@ -400,17 +458,31 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
         is_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!is_last || threadIdx.x != 0) return;
+    if (!is_last) return;
     __threadfence();
+    // last block: warp t folds term t's block partials, lane l taking blocks l, l+32, ...
+    // in order, then a fixed shuffle tree (the same order whatever the timing)
+    __shared__ double rs[RED_MAX_TERMS];
+    if (warp < a.nterms) {
+        const int t = warp;
+        const bool mx = a.op[t] == RED_MAXABS;
+        double v = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) {
+            const double w = a.part[static_cast<int64_t>(b) * a.nterms + t];
+            v = mx ? fmax(v, w) : v + w;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_down_sync(0xffffffffu, v, o);
+            v = mx ? fmax(v, w) : v + w;
+        }
+        if (lane == 0) rs[t] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     double r[RED_MAX_TERMS] = {};
     for (int t = 0; t < a.nterms; ++t) {
-        double v = a.part[t];
-        for (unsigned b = 1; b < gridDim.x; ++b) {
-            const double w = a.part[static_cast<int64_t>(b) * a.nterms + t];
-            v = a.op[t] == RED_MAXABS ? fmax(v, w) : v + w;
-        }
-        r[t] = v;
-        a.out[t] = v;
+        r[t] = rs[t];
+        a.out[t] = rs[t];
     }
     *a.counter = 0u;
     run_epilogue(a.st, a.epilogue, a.newton, r);
@@ -425,11 +497,11 @@ __global__ void k_epilogue(DevState* st, int epilogue, int newton, const double*
 __global__ void __launch_bounds__(AUX_NT) k_max_local(const double* partial, int64_t nb, int64_t n_out,
                                                       double* out, DevState* st, unsigned guard) {
     if (guard_skip(st, guard)) return;
-    for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < n_out;
-         o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double M = -kInf;
-        for (int64_t b = 0; b < nb; ++b) M = fmax(M, partial[b * n_out + o]);
-        out[o] = M;
+    __shared__ double sh[FOLD_W][32];
+    FOLD_LOOP(n_out) {
+        const int64_t o = q0 + (threadIdx.x & 31);
+        const double M = fold_rows<true>(partial, nb, n_out, o, o < n_out, sh);
+        if (threadIdx.x < 32 && o < n_out) out[o] = M;
     }
 }
 

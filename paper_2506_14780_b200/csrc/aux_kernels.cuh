@@ -89,6 +89,16 @@ __global__ void k_lse_commit(const double* in_vec, double* ref, int64_t count, i
 __global__ void k_block_finalize(const double* partial, int64_t nb, int kt, int k, int64_t n_out,
                                  const double* scale, double* out, int64_t ld, DevState* st,
                                  unsigned guard);
+// out[q] = scale * sum_b part[b*Q + q] (column fold of split partial rows, deterministic)
+__global__ void k_fold_sum(const double* part, int64_t nb, int64_t Q, double scale, double* out,
+                           const DevState* st, unsigned guard);
+// grid for the column-fold finalize kernels: one block per 32 outputs
+inline int fold_grid(int64_t Q) {
+    int64_t g = (Q + 31) / 32;
+    if (g < 1) g = 1;
+    if (g > 148 * 8) g = 148 * 8;
+    return static_cast<int>(g);
+}
 __global__ void k_pack_w(const double* X, int64_t n, int64_t ldx, int k, int kt, const double* rowscale,
                          double* W);
 
@@ -120,6 +130,7 @@ int gram_blocks(int64_t T);
 enum { RED_DOT = 0, RED_SQ = 1, RED_MAXABS = 2 };
 enum { EPI_NONE = 0, EPI_GAUGE = 1, EPI_CHECK = 2, EPI_ACCEPT = 3 };
 constexpr int RED_MAX_TERMS = 6;
+constexpr int RED_PER_BLOCK = AUX_NT * 2;  // elements per k_reduce block (up to 296 blocks)
 struct RedArgs {
     int64_t T[2] = {0, 0};
     int nterms = 0;

@@ -747,14 +747,14 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         fa.guard = gmax;
         if (split) {  // local column maxima -> max over ranks -> shift
             count_launch();
-            k_max_local<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tmax.n_in_blocks, nout, P.red_tmp.p,
+            k_max_local<<<fold_grid(nout), AUX_NT, 0, s>>>(P.partial.p, tmax.n_in_blocks, nout, P.red_tmp.p,
                                                          P.st, gmax);
             allreduce(P, P.red_tmp.p, nout, ncclMax);
             fa.partial = P.red_tmp.p;
             fa.nb = 1;
         }
         count_launch();
-        k_max_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
+        k_max_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(fa);
         if (cull) {  // output-group maxima of S with this phase's shift
             unsigned* sched = &P.st->counters[10 + dir];
             cull_group_max(P, out, P.pack_out[dir].p, P.s_go[dir].p, CULL_GO, gsum, sched);
@@ -770,14 +770,14 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         fa.retry_phase = phase;
         if (split) {  // local column sums share one shift per column: plain sum over ranks
             count_launch();
-            k_sum_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tsum.n_in_blocks, nout, nullptr,
+            k_sum_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(P.partial.p, tsum.n_in_blocks, nout, nullptr,
                                                             P.red_tmp.p, P.st, gsum);
             allreduce(P, P.red_tmp.p, nout, ncclSum);
             fa.partial = P.red_tmp.p;
             fa.nb = 1;
         }
         count_launch();
-        k_lse_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(fa);
+        k_lse_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(fa);
     }
     count_launch();
     k_lse_commit<<<grid_for(nin), AUX_NT, 0, s>>>(in_vec, P.ref[dir].p, nin, dir, P.st, guard);
@@ -877,15 +877,15 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     launch_tiles(tp, ta, s);
     if (rs) {
         count_launch();
-        k_rsum_finalize<<<grid_for(nin), AUX_NT, 0, s>>>(P.rsum.p, tp.n_out_tiles, nin, ps.rsum_out, P.st,
+        k_rsum_finalize<<<fold_grid(nin), AUX_NT, 0, s>>>(P.rsum.p, tp.n_out_tiles, nin, ps.rsum_out, P.st,
                                                          ps.guard);
     }
     count_launch();
     if (mode == MODE_SUM)
-        k_sum_finalize<<<grid_for(nout), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, nout, ps.out_scale,
+        k_sum_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, nout, ps.out_scale,
                                                          ps.out, P.st, ps.guard);
     else
-        k_block_finalize<<<grid_for(nout * ps.k), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, ps.kt,
+        k_block_finalize<<<fold_grid(nout * ps.k), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, ps.kt,
                                                                   ps.k, nout, ps.out_scale, ps.out, nout,
                                                                   P.st, ps.guard);
     if (ps.dir == 0)  // column direction reduces over the sharded rows
@@ -914,8 +914,14 @@ static void gram(Problem& P, int64_t T, int ka, int kb, const double* U, int64_t
     ga.counter = &P.st->counters[kGramSlot];
     ga.st = P.st;
     ga.guard = guard;
+    const int G = gram_blocks(T);
     count_launch();
-    k_gram<<<gram_blocks(T), AUX_NT, 0, P.stream>>>(ga);
+    k_gram<<<G, AUX_NT, 0, P.stream>>>(ga);
+    if (G > 1) {
+        const int64_t Q = diag_only ? ka : static_cast<int64_t>(ka) * kb;
+        count_launch();
+        k_fold_sum<<<fold_grid(Q), AUX_NT, 0, P.stream>>>(ga.part, G, Q, scale, out, P.st, guard);
+    }
     CK(cudaGetLastError());
 }
 

@@ -114,20 +114,25 @@ __global__ void k_newton_solve(const double* G1, const double* cross, const doub
         sA[e] = -(0.5 * (h_rc + h_cr));
     }
     __syncthreads();
+    // Right-looking factorisation. Every entry sees the same operations in the same
+    // order as in the left-looking loop of Eigen's unblocked LLT (A_rc -= L_rt L_ct for
+    // t = 0, 1, ..., then / L_cc), so the factor is the same, but each column costs
+    // three barriers instead of a serial dot product.
     for (int c = 0; c < ell; ++c) {
         if (tid == 0) {
-            double x = sA[c + c * ell];
-            for (int t = 0; t < c; ++t) x -= sA[c + t * ell] * sA[c + t * ell];
+            const double x = sA[c + c * ell];
             if (!(x > 0.0)) fail = 1;
             piv = sqrt(x);
             sA[c + c * ell] = piv;
         }
         __syncthreads();
         if (fail) break;
-        for (int r = c + 1 + tid; r < ell; r += blockDim.x) {
-            double v = sA[r + c * ell];
-            for (int t = 0; t < c; ++t) v -= sA[r + t * ell] * sA[c + t * ell];
-            sA[r + c * ell] = v / piv;
+        for (int r = c + 1 + tid; r < ell; r += blockDim.x) sA[r + c * ell] = sA[r + c * ell] / piv;
+        __syncthreads();
+        const int rs = ell - c - 1;
+        for (int e = tid; e < rs * rs; e += blockDim.x) {
+            const int r = c + 1 + e % rs, q = c + 1 + e / rs;
+            if (r >= q) sA[r + q * ell] -= sA[r + c * ell] * sA[q + c * ell];
         }
         __syncthreads();
     }
@@ -135,20 +140,26 @@ __global__ void k_newton_solve(const double* G1, const double* cross, const doub
         if (tid == 0) st->newton_ok = 0;
         return;
     }
-    if (tid == 0) {
-        double y[64];
-        for (int r = 0; r < ell; ++r) {
-            double v = grad[r];
-            for (int t = 0; t < r; ++t) v -= sA[r + t * ell] * y[t];
-            y[r] = v / sA[r + r * ell];
-        }
-        for (int r = ell - 1; r >= 0; --r) {
-            double v = y[r];
-            for (int t = r + 1; t < ell; ++t) v -= sA[t + r * ell] * y[t];
-            y[r] = v / sA[r + r * ell];
-        }
-        for (int r = 0; r < ell; ++r) delta[r] = y[r];
+    // L y = grad, then L^T delta = y, column-oriented on warp 0 (2 rows per lane)
+    __shared__ double sy[64];
+    if (tid >= 32) return;
+    for (int r = tid; r < ell; r += 32) sy[r] = grad[r];
+    __syncwarp();
+    for (int t = 0; t < ell; ++t) {
+        const double yt = sy[t] / sA[t + t * ell];
+        for (int r = t + 1 + tid; r < ell; r += 32) sy[r] -= sA[r + t * ell] * yt;
+        __syncwarp();
+        if (tid == 0) sy[t] = yt;
+        __syncwarp();
     }
+    for (int t = ell - 1; t >= 0; --t) {
+        const double yt = sy[t] / sA[t + t * ell];
+        for (int r = tid; r < t; r += 32) sy[r] -= sA[t + r * ell] * yt;
+        __syncwarp();
+        if (tid == 0) sy[t] = yt;
+        __syncwarp();
+    }
+    for (int r = tid; r < ell; r += 32) delta[r] = sy[r];
 }
 
 // candidate = f + V delta (solver.cpp:45)

@@ -160,7 +160,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
         allreduce(P, grad, l, ncclSum);
         count_launch();
-        k_newton_solve<<<1, 64, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
+        k_newton_solve<<<1, 256, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
                                                             P.st, gn);
         count_launch();
         k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
