@@ -386,9 +386,19 @@ def run_ours(args, world, rank, local):
         t0 = time.perf_counter()
         rsm = sk.solve_small_batch(tup, tol=1e-9)
         t_sm = time.perf_counter() - t0
+        # the same kernel on ONE problem: a cooperative group of CTAs (low-latency single solve)
+        sk.solve_small_batch(tup[:1], tol=1e-9)
+        t1s = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r_one = sk.solve_small_batch(tup[:1], tol=1e-9)[0]
+            t1s.append(time.perf_counter() - t0)
         small = {"problems": len(tup), "ms": t_sm * 1e3, "solves_per_s": len(tup) / t_sm,
                  "all_converged": all(r.converged for r in rsm),
-                 "iterations_equal_first32": all(a.iterations == b.iterations for a, b in zip(rsm, rb))}
+                 "iterations_equal_first32": all(a.iterations == b.iterations for a, b in zip(rsm, rb)),
+                 "single_problem_ms": min(t1s) * 1e3, "single_problem_iterations": r_one.iterations,
+                 "single_problem_note": "C1 seed 1 alone: a group of CTAs with two group barriers per "
+                                        "iteration, host arrays in and potentials out (min of 3)"}
         batch = {"problems": len(probs), "config": "C1 seeds 1..32, SK (ell=0) to marginal error 1e-9",
                  "small_problem_kernel": small,
                  "ms_batch": t_b * 1e3, "solves_per_s": len(probs) / t_b, "ms_per_solve_one_by_one": t_1 * 1e3,

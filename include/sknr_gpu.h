@@ -197,8 +197,11 @@ int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_con
                      int64_t* iterations, int* converged);
 
 /* Small-problem batch (not in the reference): `count` point-cloud problems of one
- * dimension d <= 4 with n, m <= 2048, each solved by plain SK (ell = 0) from f = 0
- * to tol inside one CTA of a single kernel launch (no launch per iteration). Per
+ * dimension d <= 4 with n, m <= 8192 (d <= 2), 6224 (d = 3), 4979 (d = 4), each
+ * solved by plain SK (ell = 0) from f = 0 to tol inside a single kernel launch (no
+ * launch per iteration): one CTA per problem when the batch fills the GPU, a
+ * cooperative group of CTAs per problem when it does not (count = 1 is the
+ * low-latency single solve). Per
  * problem q: n[q], m[q], x[q] (n x d), y[q] (m x d), a[q], b[q], eps[q],
  * cost_scale[q] (NULL: 1); outputs f_out[q], g_out[q], iterations[q], converged[q].
  * Same iteration and stopping test as sknr_solve; sums in a different order. */

@@ -798,8 +798,10 @@ def solve_batch(problems: Sequence[Problem], tol: float = 1e-9, max_iter: int = 
 
 
 def solve_small_batch(problems, tol: float = 1e-9, max_iter: int = 100000) -> list:
-    """Plain SK (ell = 0, from f = 0) for many small point-cloud problems in ONE kernel
-    launch, one CTA per problem (n, m <= 2048, one dimension d <= 4). `problems` holds
+    """Plain SK (ell = 0, from f = 0) for small point-cloud problems in ONE kernel launch
+    (one dimension d <= 4; n, m <= 8192 at d <= 2, 6224 at d = 3, 4979 at d = 4): one
+    CTA per problem when the batch fills the GPU, a cooperative group of CTAs per
+    problem otherwise (a single problem is the low-latency solve). `problems` holds
     PointProblem objects or (x, y, alpha, beta, epsilon[, cost_scale]) tuples. Same
     iteration and stopping test as solve(); reductions run in a different order, so
     potentials agree with solve() to rounding, not bit for bit. Not in the reference."""

@@ -934,8 +934,10 @@ int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_con
 }
 
 // Small-problem batch: every problem solved by plain SK (ell = 0) from f = 0 inside one
-// CTA of one kernel launch (launch_sk_small); point clouds of one dimension d <= 4 with
-// n, m <= 2048 each. Problems may differ in n, m, epsilon and cost scale.
+// kernel launch (launch_sk_small) by a group of G CTAs (G = 1 when the batch fills the
+// GPU; a lone C1 problem gets 32 CTAs); point clouds of one dimension d <= 4 with
+// n, m <= small_max_count(d) (8192 at d <= 2). Problems may differ in n, m, epsilon
+// and cost scale.
 int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int64_t* m, const double* const* x,
                            const double* const* y, const double* const* a, const double* const* b,
                            const double* eps, const double* cost_scale, double tol, int64_t max_iter,
@@ -950,9 +952,14 @@ int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int
         throw InvalidArgument("solve_small_batch: null pointer");
     // one device arena: per problem x (n d), y (m d), a (n), b (m), f (n), g (m), h (m)
     std::vector<size_t> off(static_cast<size_t>(count) + 1, 0);
+    int64_t max_nm = 1;
     for (int64_t q = 0; q < count; ++q) {
-        if (n[q] < 1 || m[q] < 1 || n[q] > kSmallMax || m[q] > kSmallMax)
-            throw InvalidArgument("solve_small_batch: 1 <= n, m <= 2048 required");
+        if (n[q] < 1 || m[q] < 1 || n[q] > small_max_count(static_cast<int>(d)) ||
+            m[q] > small_max_count(static_cast<int>(d)))
+            throw InvalidArgument("solve_small_batch: 1 <= n, m <= " +
+                                  std::to_string(small_max_count(static_cast<int>(d))) + " required at d = " +
+                                  std::to_string(d));
+        max_nm = std::max<int64_t>(max_nm, std::max(n[q], m[q]));
         if (!(eps[q] > 0.0)) throw InvalidArgument("EotProblem: epsilon must be positive");
         validate_measure(a[q], n[q]);
         validate_measure(b[q], m[q]);
@@ -989,8 +996,15 @@ int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     CK(cudaMemcpyAsync(arena.p, host.data(), sizeof(double) * off[count], cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dprobs.p, hp.data(), sizeof(SmallProbDev) * count, cudaMemcpyHostToDevice, s));
-    launch_sk_small(static_cast<int>(d), reinterpret_cast<SmallProbDev*>(dprobs.p), static_cast<int>(count), tol,
-                    max_iter, 0, s);
+    const int G = small_group_size(static_cast<int>(d), static_cast<int>(count), static_cast<int>(max_nm));
+    DBuf gpart, gbar;
+    if (G > 1) {
+        gpart.ensure(static_cast<size_t>(count) * G * 4);
+        gbar.ensure(static_cast<size_t>(count));  // 2 unsigned per problem
+        CK(cudaMemsetAsync(gbar.p, 0, sizeof(double) * count, s));
+    }
+    launch_sk_small(static_cast<int>(d), reinterpret_cast<SmallProbDev*>(dprobs.p), static_cast<int>(count),
+                    static_cast<int>(max_nm), tol, max_iter, 0, G, gpart.p, reinterpret_cast<unsigned*>(gbar.p), s);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(host.data(), arena.p, sizeof(double) * off[count], cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp.data(), dprobs.p, sizeof(SmallProbDev) * count, cudaMemcpyDeviceToHost, s));

@@ -65,9 +65,17 @@ int chunk_inputs(int mode, int kt);
 void count_launch();
 int64_t launch_count();
 
-// Small-problem batch (sknr_solve_small_batch): one CTA runs a whole SK solve of one
-// point-cloud problem (n, m <= kSmallMax, d <= 4) with __syncthreads only.
-constexpr int kSmallMax = 2048;
+// Small-problem batch (sknr_solve_small_batch): a group of CTAs (one CTA when the batch
+// fills the GPU) runs a whole SK solve of one point-cloud problem (n, m <=
+// small_max_count(d), d <= 4) inside one kernel.
+constexpr int kSmallMax = 8192;
+// largest n, m for the small-problem kernel at dimension d: every CTA stages one side's
+// points (d + 1 doubles each) next to the 32 KiB exp2 table in <= 227 KiB of shared memory
+inline int small_max_count(int d) {
+    const int words = 232448 / 8 - (256 * 16) - 64;
+    const int c = words / (d + 1);
+    return c < kSmallMax ? c : kSmallMax;
+}
 struct SmallProbDev {
     const double *x = nullptr, *y = nullptr, *a = nullptr, *b = nullptr;  // col-major coords, weights
     double *f = nullptr, *g = nullptr, *h = nullptr;                     // potentials (f, g in/out), scratch
@@ -76,7 +84,11 @@ struct SmallProbDev {
     long long iters = 0;
     int conv = 0;
 };
-void launch_sk_small(int d, SmallProbDev* probs, int count, double tol, long long max_iter, int warm_g,
-                     cudaStream_t s);
+// Launches the small-problem kernel for `count` problems whose largest side is max_nm;
+// returns the CTAs per problem used (G). gpart: count*G*4 doubles, gbar: 2*count zeroed
+// unsigneds (only touched when G > 1); allocate them for G = small_group_size(...).
+int small_group_size(int d, int count, int max_nm);
+void launch_sk_small(int d, SmallProbDev* probs, int count, int max_nm, double tol, long long max_iter,
+                     int warm_g, int G, double* gpart, unsigned* gbar, cudaStream_t s);
 
 }  // namespace sknr

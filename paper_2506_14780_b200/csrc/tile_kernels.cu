@@ -286,11 +286,15 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
 }
 
 // ------------------------------------------------------------- small-problem batched SK
-// One CTA = one problem, the whole solve loop inside the kernel (no launches per
-// iteration): inputs of each log-sum-exp staged in shared memory, one warp per output,
-// lanes over the inputs, exact max shift then sum (core.cpp:35-82), warp-shuffle and
-// fixed-order block reductions (deterministic). Same iteration as the device loop:
-// row LSE -> gauge (solver.cpp:108-112) -> column LSE -> marginal gap -> stop test.
+// A group of G CTAs = one problem, the whole solve loop inside the kernel (no launches
+// per iteration): the inputs of each log-sum-exp are staged in every CTA's shared
+// memory, one warp per output (warps of the group take outputs round-robin), lanes over
+// the inputs, exact max shift then sum (core.cpp:35-82), warp-shuffle and fixed-order
+// block and group reductions (deterministic for a given G). Same iteration as the
+// device loop: row LSE -> gauge (solver.cpp:108-112) -> column LSE -> marginal gap ->
+// stop test. G = 1 (many problems) needs only __syncthreads; G > 1 (few problems,
+// one problem spread over many SMs) adds two group barriers per iteration, launched
+// cooperatively so every CTA of a group is resident.
 template <int D>
 __device__ __forceinline__ double small_lse(const double* __restrict__ sp, int cnt, const double* yo, double ke,
                                             const unsigned long long* __restrict__ tab, unsigned laneoff,
@@ -334,95 +338,155 @@ __device__ __forceinline__ double small_block_sum(double v, double* red, int tid
     return t;
 }
 
+// Generation barrier of the G CTAs of one group (bar[0] arrivals, bar[1] generation).
+__device__ __forceinline__ void group_barrier(unsigned* bar, int G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = bar + 1;
+        const unsigned gen = *vgen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == static_cast<unsigned>(G - 1)) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Sum over the group of the block totals of v0 (and v1): block totals in fixed order,
+// then the G CTA totals in CTA order (identical in every CTA of the group).
+template <int NV>
+__device__ __forceinline__ void group_sums(double* v, double* red, int tid, int nthreads, int G, int r,
+                                           double* part, int slot, unsigned* bar) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = small_block_sum(v[k], red, tid, nthreads);
+    if (G == 1) return;
+    if (tid == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) part[r * 4 + slot + k] = v[k];
+    group_barrier(bar, G);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double t = __ldcg(part + slot + k);
+        for (int c = 1; c < G; ++c) t += __ldcg(part + c * 4 + slot + k);
+        v[k] = t;
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(512, 1)
-    k_sk_small(SmallProbDev* probs, double tol, long long max_iter, int warm_g) {
+    k_sk_small(SmallProbDev* probs, double tol, long long max_iter, int warm_g, int G, double* gpart,
+               unsigned* gbar) {
     constexpr int P = D + 1;
     constexpr int NT = 512;
+    constexpr int WPB = NT / 32;
     extern __shared__ __align__(16) double sm[];
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
     double* red = sm + kTabWords;
     double* sp = red + 64;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = blockIdx.x / G, r = blockIdx.x % G;
+    const int W = G * WPB, gw = r * WPB + warp;  // warps of the group, this warp's rank in it
+    double* part = gpart ? gpart + static_cast<int64_t>(q) * G * 4 : nullptr;
+    unsigned* bar = gbar ? gbar + 2 * q : nullptr;
     load_exp2_table(tab, tid, NT);
     const unsigned laneoff = (tid & (kTabRep - 1)) << 3;
     const double c3 = pexp_c3();
-    SmallProbDev& pr = probs[blockIdx.x];
+    SmallProbDev& pr = probs[q];
     const int n = pr.n, m = pr.m;
     const double eps = pr.eps, ie = 1.0 / eps, ke = pr.kappa * ie;
     double* f = pr.f;
     double* g = pr.g;
     double* h = pr.h;
-    // column LSE at f into h (ctransform_of_f): inputs i (la_i + f_i/eps, x_i), outputs j
-    auto col_lse = [&]() {
+    // Cross-CTA data (f, g, h, partials) is read with ld.global.cg: L1 is not coherent.
+    // column LSE at f - c into h (ctransform_of_f): inputs i (la_i + (f_i - c)/eps, x_i),
+    // outputs j owned by warp j mod W, whose lane 0 also stores the gauged g_j = gsrc_j + c;
+    // then the CTA's threads form the column residuals b_j expm1((g_j - h_j)/eps) of the
+    // CTA's own columns (j = 16 r + w + k W, w < 16) in parallel.
+    auto col_lse = [&](double c, const double* gsrc, double& csq) {
         __syncthreads();
         for (int i = tid; i < n; i += NT) {
-            sp[i * P] = log(pr.a[i]) + f[i] * ie;
+            sp[i * P] = log(pr.a[i]) + (__ldcg(f + i) - c) * ie;
 #pragma unroll
             for (int d = 0; d < D; ++d) sp[i * P + 1 + d] = pr.x[i + d * n];
         }
         __syncthreads();
-        for (int j = warp; j < m; j += NT / 32) {
+        for (int j = gw; j < m; j += W) {
             double yo[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) yo[d] = pr.y[j + d * m];
+            const double gprev = gsrc ? __ldcg(gsrc + j) : 0.0;  // loaded ahead of the LSE
             const double L = small_lse<D>(sp, n, yo, ke, tab, laneoff, c3, lane);
-            if (lane == 0) h[j] = -eps * L;
+            if (lane == 0) {
+                h[j] = -eps * L;
+                if (gsrc) g[j] = gprev + c;
+            }
         }
+        if (!gsrc) return;
         __syncthreads();
+        for (int t = tid;; t += NT) {
+            const int k = t >> 4;
+            if (static_cast<int64_t>(k) * W >= m) break;
+            const int j = r * WPB + (t & 15) + k * W;
+            if (j >= m) continue;
+            const double cr = pr.b[j] * expm1((g[j] - h[j]) * ie);
+            csq = fma(cr, cr, csq);
+        }
     };
+    double dummy = 0.0;
     if (!warm_g) {  // first sweep's g = f0^{C,eps}
-        col_lse();
-        for (int j = tid; j < m; j += NT) g[j] = h[j];
+        col_lse(0.0, nullptr, dummy);
+        if (G > 1) group_barrier(bar, G);
     }
+    const double* gsrc = warm_g ? g : h;  // g of the coming sweep (previous h, gauged below)
     long long it = 0;
     int conv = 0;
     while (it < max_iter) {
         ++it;
-        // row LSE at g (ctransform_of_g): f_i = -eps L_i; row residual a_i expm1(f_i/eps + L_i)
+        // row LSE at gsrc (ctransform_of_g): f_i = -eps L_i; row residual a_i expm1(f_i/eps + L_i)
         __syncthreads();
         for (int j = tid; j < m; j += NT) {
-            sp[j * P] = log(pr.b[j]) + g[j] * ie;
+            sp[j * P] = log(pr.b[j]) + __ldcg(gsrc + j) * ie;
 #pragma unroll
             for (int d = 0; d < D; ++d) sp[j * P + 1 + d] = pr.y[j + d * m];
         }
         __syncthreads();
-        double rsq = 0.0, af = 0.0;
-        for (int i = warp; i < n; i += NT / 32) {
+        double rs[2] = {0.0, 0.0};  // a.f, |row - a|^2
+        for (int i = gw; i < n; i += W) {
             double xo[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) xo[d] = pr.x[i + d * n];
+            const double ai = pr.a[i];
             const double L = small_lse<D>(sp, m, xo, ke, tab, laneoff, c3, lane);
             if (lane == 0) {
                 const double fi = -eps * L;
-                const double rr = pr.a[i] * expm1(fi * ie + L);
+                const double rr = ai * expm1(fi * ie + L);
                 f[i] = fi;
-                rsq = fma(rr, rr, rsq);
-                af = fma(pr.a[i], fi, af);
+                rs[1] = fma(rr, rr, rs[1]);
+                rs[0] = fma(ai, fi, rs[0]);
             }
         }
-        // gauge (solver.cpp:108-112)
-        const double c = small_block_sum(af, red, tid, NT);
-        const double row2 = small_block_sum(rsq, red, tid, NT);
-        __syncthreads();
-        for (int i = tid; i < n; i += NT) f[i] -= c;
-        for (int j = tid; j < m; j += NT) g[j] += c;
-        // column LSE at the gauged f: the column residual b_j expm1((g_j - h_j)/eps) and next g
-        col_lse();
-        double csq = 0.0;
-        for (int j = tid; j < m; j += NT) {
-            const double cr = pr.b[j] * expm1((g[j] - h[j]) * ie);
-            csq = fma(cr, cr, csq);
-        }
-        const double col2 = small_block_sum(csq, red, tid, NT);
-        if (sqrt(row2) + sqrt(col2) < tol) {
+        // gauge (solver.cpp:108-112): c = a.f over the whole group
+        group_sums<2>(rs, red, tid, NT, G, r, part, 0, bar);
+        const double c = rs[0], row2 = rs[1];
+        // column LSE at the gauged f: next h, column residual, gauged g
+        double cs[1] = {0.0};
+        col_lse(c, gsrc, cs[0]);
+        group_sums<1>(cs, red, tid, NT, G, r, part, 2, bar);
+        // f -= c on the rows this warp owns (lanes split them; the warp writes them again
+        // in the next sweep, after a __syncthreads)
+        for (int i = gw + lane * W; i < n; i += 32 * W) f[i] = f[i] - c;
+        if (sqrt(row2) + sqrt(cs[0]) < tol) {
             conv = 1;
             break;
         }
-        __syncthreads();
-        for (int j = tid; j < m; j += NT) g[j] = h[j];
+        gsrc = h;
     }
-    if (tid == 0) {
+    if (tid == 0 && r == 0) {
         pr.iters = it;
         pr.conv = conv;
     }
@@ -1476,22 +1540,50 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     return p;
 }
 
-void launch_sk_small(int d, SmallProbDev* probs, int count, double tol, long long max_iter, int warm_g,
-                     cudaStream_t s) {
-    int maxcnt = kSmallMax;
-    const void* fn = nullptr;
+static const void* small_kernel(int d) {
     switch (d) {
-        case 1: fn = reinterpret_cast<const void*>(&k_sk_small<1>); break;
-        case 2: fn = reinterpret_cast<const void*>(&k_sk_small<2>); break;
-        case 3: fn = reinterpret_cast<const void*>(&k_sk_small<3>); break;
-        case 4: fn = reinterpret_cast<const void*>(&k_sk_small<4>); break;
-        default: return;
+        case 1: return reinterpret_cast<const void*>(&k_sk_small<1>);
+        case 2: return reinterpret_cast<const void*>(&k_sk_small<2>);
+        case 3: return reinterpret_cast<const void*>(&k_sk_small<3>);
+        case 4: return reinterpret_cast<const void*>(&k_sk_small<4>);
+        default: return nullptr;
     }
-    const int smem = static_cast<int>(sizeof(double)) * (kTabWords + 64 + maxcnt * (d + 1));
+}
+
+static int small_smem(int d, int max_nm) {
+    return static_cast<int>(sizeof(double)) * (kTabWords + 64 + max_nm * (d + 1));
+}
+
+// CTAs per problem: spread few problems over the SMs (all CTAs must be co-resident for
+// the group barriers), at most one warp per output of the larger side.
+int small_group_size(int d, int count, int max_nm) {
+    const void* fn = small_kernel(d);
+    if (!fn || count < 1) return 1;
+    const int smem = small_smem(d, max_nm);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    void* args[] = {&probs, &tol, &max_iter, &warm_g};
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512, smem);
+    const int capacity = sms * (occ > 0 ? occ : 1);
+    int G = capacity / count;
+    const int useful = (max_nm + 15) / 16;
+    if (G > useful) G = useful;
+    return G < 1 ? 1 : G;
+}
+
+void launch_sk_small(int d, SmallProbDev* probs, int count, int max_nm, double tol, long long max_iter,
+                     int warm_g, int G, double* gpart, unsigned* gbar, cudaStream_t s) {
+    const void* fn = small_kernel(d);
+    if (!fn) return;
+    const int smem = small_smem(d, max_nm);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    void* args[] = {&probs, &tol, &max_iter, &warm_g, &G, &gpart, &gbar};
     count_launch();
-    cudaLaunchKernel(fn, dim3(count), dim3(512), args, smem, s);
+    if (G > 1)  // group barriers: every CTA must be resident
+        cudaLaunchCooperativeKernel(fn, dim3(count * G), dim3(512), args, smem, s);
+    else
+        cudaLaunchKernel(fn, dim3(count), dim3(512), args, smem, s);
 }
 
 void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s) {

@@ -425,8 +425,8 @@ def test_culled_sharded_sk_matches_dense_unsharded():
 
 
 def test_solve_small_batch_matches_oracle_and_solve():
-    """One CTA per problem, whole SK loop in one kernel launch: identical iteration
-    counts with the CPU oracle and with solve(), potentials within 1e-9."""
+    """Whole SK loop in one kernel launch (5 problems: a group of CTAs each): identical
+    iteration counts with the CPU oracle and with solve(), potentials within 1e-9."""
     probs, refs = [], []
     for s in range(5):
         inst = G.config("C1", seed=1 + s, n=300 + 40 * s, m=260 + 30 * s)
@@ -440,6 +440,43 @@ def test_solve_small_batch_matches_oracle_and_solve():
         assert rel_err(r.f, ref["f"]) <= 1e-9 and rel_err(r.g, ref["g"]) <= 1e-9
         one = sk.solve(sk.PointProblem(x, y, a, b, e), tol=1e-9)
         assert one.iterations == r.iterations
-    with pytest.raises(ValueError, match="n, m <= 2048"):
-        x = np.random.default_rng(0).uniform(0, 1, (3000, 2))
-        sk.solve_small_batch([(x, x, np.full(3000, 1 / 3000), np.full(3000, 1 / 3000), 0.1)])
+    with pytest.raises(ValueError, match="n, m <= 8192"):
+        x = np.random.default_rng(0).uniform(0, 1, (9000, 2))
+        sk.solve_small_batch([(x, x, np.full(9000, 1 / 9000), np.full(9000, 1 / 9000), 0.1)])
+
+
+def test_solve_small_batch_cta_groups():
+    """A lone problem is spread over a cooperative group of CTAs (group barriers, two per
+    iteration); a full batch runs one CTA per problem. Both give solve()'s iteration
+    count, and the two layouts agree to rounding."""
+    inst = G.config("C1")
+    a = np.full(inst.n, 1 / inst.n)
+    b = np.full(inst.m, 1 / inst.m)
+    tup = (inst.x, inst.y, a, b, inst.epsilon)
+    ref = sk.solve(sk.PointProblem(*tup), tol=1e-9)
+    one = sk.solve_small_batch([tup], tol=1e-9)[0]
+    many = sk.solve_small_batch([tup] * 300, tol=1e-9)
+    assert one.converged and one.iterations == ref.iterations
+    assert rel_err(one.f, ref.f) <= 1e-9 and rel_err(one.g, ref.g) <= 1e-9
+    for r in (many[0], many[150], many[299]):
+        assert r.iterations == one.iterations
+        assert rel_err(r.f, one.f) <= 1e-12 and rel_err(r.g, one.g) <= 1e-12
+    assert np.array_equal(many[0].f, many[299].f)
+    # C2-sized single problem: 4096 x 4096 on (up to) every SM
+    c2 = G.config("C2")
+    p2 = (c2.x, c2.y, c2.alpha, c2.beta, 0.02, c2.cost_scale)
+    r2 = sk.solve_small_batch([p2], tol=1e-9)[0]
+    s2 = sk.solve(sk.PointProblem(c2.x, c2.y, c2.alpha, c2.beta, 0.02, c2.cost_scale), tol=1e-9)
+    assert r2.converged and r2.iterations == s2.iterations
+    assert rel_err(r2.f, s2.f) <= 1e-9 and rel_err(r2.g, s2.g) <= 1e-9
+    # ragged sizes and d = 3 in one batch of two (two groups side by side)
+    rng = np.random.default_rng(7)
+    ps = []
+    for n_, m_ in ((700, 1300), (1901, 33)):
+        ps.append((rng.uniform(0, 1, (n_, 3)), rng.normal(size=(m_, 3)), np.full(n_, 1 / n_),
+                   np.full(m_, 1 / m_), 0.05))
+    outs = sk.solve_small_batch(ps, tol=1e-9)
+    for p, r in zip(ps, outs):
+        s_ = sk.solve(sk.PointProblem(*p), tol=1e-9)
+        assert r.converged and r.iterations == s_.iterations
+        assert rel_err(r.f, s_.f) <= 1e-9
