@@ -47,6 +47,7 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
 
 // ------------------------------------------------------------------ prep
 __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     __shared__ double sh[AUX_NT];
     double lmax = -kInf, lmin = kInf;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
 }
 
 __global__ void __launch_bounds__(AUX_NT) k_prep_out(PrepOutArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     const bool bound = a.shift_mode == SHIFT_BOUND && !a.st->need_exact[a.dir];
     const double dshift = bound ? a.st->dmax[a.dir] * a.inv_eps : 0.0;
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(AUX_NT) k_group_max(const double* pack, int pk
                                                       const int* perm, int64_t count, int gs, double* out,
                                                       const DevState* st, unsigned guard, unsigned* zero_counter,
                                                       const double* sub) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     if (zero_counter && blockIdx.x == 0 && threadIdx.x == 0) *zero_counter = 0u;
     __shared__ double vals[AUX_NT];
@@ -182,6 +185,7 @@ __device__ __forceinline__ double fold_rows(const double* __restrict__ p, int64_
 
 // Exact shift: shift_o += max_u / L64, B_o recomputed from it.
 __global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(a.n_out) {
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(AUX_NT) k_max_finalize(FinalizeArgs a) {
 // [2^-900, 2^900] means the bound shift was too loose: request the exact path
 // (n_retry counts the 32-output chunks that saw such a sum).
 __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(a.n_out) {
@@ -228,6 +233,7 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
 // transposed sums (r = P~ beta), deterministic.
 __global__ void __launch_bounds__(AUX_NT) k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n,
                                                           double* out, const DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(n) {
@@ -240,6 +246,7 @@ __global__ void __launch_bounds__(AUX_NT) k_rsum_finalize(const double* rsum, in
 __global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, int64_t nb,
                                                          int64_t n_out, const double* scale,
                                                          double* out, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(n_out) {
@@ -251,6 +258,7 @@ __global__ void __launch_bounds__(AUX_NT) k_sum_finalize(const double* partial, 
 
 __global__ void __launch_bounds__(AUX_NT) k_lse_commit(const double* in_vec, double* ref, int64_t count,
                                                        int dir, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -268,6 +276,7 @@ __global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial
                                                            int k, int64_t n_out, const double* scale,
                                                            double* out, int64_t ld, DevState* st,
                                                            unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
     const int64_t total = n_out * k;
@@ -285,6 +294,7 @@ __global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial
 // Column fold of gram partials: out[q] = scale * sum_b part[b*Q + q].
 __global__ void __launch_bounds__(AUX_NT) k_fold_sum(const double* part, int64_t nb, int64_t Q, double scale,
                                                      double* out, const DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(Q) {
@@ -297,6 +307,7 @@ __global__ void __launch_bounds__(AUX_NT) k_fold_sum(const double* part, int64_t
 // W[i*kt + c] = rowscale_i * X[i + c*ldx] for c < k, 0 for k <= c < kt.
 __global__ void __launch_bounds__(AUX_NT) k_pack_w(const double* X, int64_t n, int64_t ldx, int k,
                                                    int kt, const double* rowscale, double* W) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * kt;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -319,6 +330,7 @@ int gram_blocks(int64_t T) {  // >= 64 rows per block, up to two CTAs per SM
 // Each block owns a contiguous t-range; rows are staged 32 at a time in shared
 // memory (w folded into U); thread owns pairs p = tid + q*AUX_NT.
 __global__ void __launch_bounds__(AUX_NT) k_gram(GramArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int RB = 32;
     constexpr int KMAXP = 64;
@@ -403,6 +415,7 @@ __device__ void run_epilogue(DevState* st, int epilogue, int newton, const doubl
 }
 
 __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     __shared__ double sh[RED_MAX_TERMS][AUX_NT / 32];
     double acc[RED_MAX_TERMS];
@@ -489,6 +502,7 @@ __global__ void __launch_bounds__(AUX_NT) k_reduce(RedArgs a) {
 }
 
 __global__ void k_epilogue(DevState* st, int epilogue, int newton, const double* r, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     if (threadIdx.x == 0 && blockIdx.x == 0) run_epilogue(st, epilogue, newton, r);
 }
@@ -496,6 +510,7 @@ __global__ void k_epilogue(DevState* st, int epilogue, int newton, const double*
 // max over split-K partials (sharded column LSE: local part before allreduce)
 __global__ void __launch_bounds__(AUX_NT) k_max_local(const double* partial, int64_t nb, int64_t n_out,
                                                       double* out, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
     FOLD_LOOP(n_out) {
@@ -507,6 +522,7 @@ __global__ void __launch_bounds__(AUX_NT) k_max_local(const double* partial, int
 
 // exact-path decision after the cross-rank max of (dmax, -dmin) (sharded prep_in)
 __global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double mx = st->scratch[2 * dir], mn = -st->scratch[2 * dir + 1];

@@ -21,6 +21,7 @@
 #include <condition_variable>
 #include <map>
 #include <tuple>
+#include <unordered_map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -133,6 +134,53 @@ template <typename... KArgs, typename... Args>
 static void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
     count_launch();
     kern<<<grid, block, 0, s>>>(args...);
+}
+
+// Rewrites the plain kernel->kernel edges of a captured graph into programmatic edges
+// (see SKNR_PDL_ENTRY): the successor may launch as soon as every CTA of the predecessor
+// has started, and waits in griddepcontrol.wait for its completion. Only edges into this
+// library's kernels are rewritten (foreign kernels, e.g. NCCL's, do not wait).
+// SKNR_NO_PDL=1 keeps plain edges.
+static bool own_kernel(cudaGraphNode_t node) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, bool> cache;
+    cudaKernelNodeParams kp = {};
+    if (cudaGraphKernelNodeGetParams(node, &kp) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(kp.func);
+    if (it != cache.end()) return it->second;
+    const char* name = nullptr;
+    bool ours = cudaFuncGetName(&name, kp.func) == cudaSuccess && name && std::strstr(name, "4sknr") != nullptr;
+    cudaGetLastError();
+    cache.emplace(kp.func, ours);
+    return ours;
+}
+
+static void make_programmatic(cudaGraph_t g) {
+    static const bool off = std::getenv("SKNR_NO_PDL") != nullptr;
+    if (off || !g) return;
+    size_t ne = 0;
+    CK(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
+    if (ne == 0) return;
+    std::vector<cudaGraphNode_t> from(ne), to(ne);
+    std::vector<cudaGraphEdgeData> ed(ne);
+    CK(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
+    for (size_t e = 0; e < ne; ++e) {
+        if (ed[e].type != cudaGraphDependencyTypeDefault || ed[e].from_port != cudaGraphKernelNodePortDefault)
+            continue;
+        cudaGraphNodeType tf, tt;
+        CK(cudaGraphNodeGetType(from[e], &tf));
+        CK(cudaGraphNodeGetType(to[e], &tt));
+        if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel || !own_kernel(to[e])) continue;
+        CK(cudaGraphRemoveDependencies_v2(g, &from[e], &to[e], &ed[e], 1));
+        cudaGraphEdgeData pe = {};
+        pe.from_port = cudaGraphKernelNodePortProgrammatic;
+        pe.type = cudaGraphDependencyTypeProgrammatic;
+        CK(cudaGraphAddDependencies_v2(g, &from[e], &to[e], &pe, 1));
+    }
 }
 
 static int grid_for(int64_t count, int threads = AUX_NT) {
@@ -458,6 +506,7 @@ struct EmuPtrs {
 };
 
 __global__ void k_emu_allreduce(EmuPtrs p, int world, int64_t count, int op) {
+    SKNR_PDL_ENTRY();
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double acc = p.buf[0][e];

@@ -1203,6 +1203,7 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
     enqueue_iteration(P, S, ell, false, 1);
     if (kernels_per_iter) *kernels_per_iter = launch_count() - l0;
     CK(cudaStreamEndCapture(s, &graph));
+    make_programmatic(graph);
     CK(cudaGraphInstantiate(&exec, graph, 0));
     for (int64_t t = 0; t < std::max<int64_t>(warmup, 1); ++t) CK(cudaGraphLaunch(exec, s));
     CK(cudaStreamSynchronize(s));
@@ -1231,6 +1232,7 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
 // FP64 pipe ceiling on this device: 8 independent DFMA chains per thread, a
 // full grid of 148 x 8 CTAs of 256 threads, timed with CUDA events.
 __global__ void k_fp64_peak(double* out, int iters, double a0, double b0) {
+    SKNR_PDL_ENTRY();
     // per-thread register operands (3 distinct register pairs per DFMA)
     const double a = a0 + threadIdx.x * 1e-12, b = b0 * (1.0 + threadIdx.x * 1e-9);
     double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-10, x2 = x0 + 2e-10, x3 = x0 + 3e-10;

@@ -5,12 +5,14 @@
 
 // ============================================================ small kernels
 __global__ void k_fill(double* x, int64_t n, double v) {
+    SKNR_PDL_ENTRY();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         x[i] = v;
 }
 
 __global__ void k_copy(double* dst, const double* src, int64_t n, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -18,6 +20,7 @@ __global__ void k_copy(double* dst, const double* src, int64_t n, DevState* st, 
 }
 
 __global__ void k_state_init(DevState* st, long long max_iter, double tol) {
+    SKNR_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     st->done = 0;
     st->iter_active = 0;
@@ -37,6 +40,7 @@ __global__ void k_state_init(DevState* st, long long max_iter, double tol) {
 }
 
 __global__ void k_invalidate_refs(DevState* st) {
+    SKNR_PDL_ENTRY();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         st->ref_valid[0] = st->ref_valid[1] = 0;
         st->done = 0;
@@ -45,6 +49,7 @@ __global__ void k_invalidate_refs(DevState* st) {
 }
 
 __global__ void k_iter_begin(DevState* st) {
+    SKNR_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (st->done) {
         st->iter_active = 0;
@@ -61,6 +66,7 @@ __global__ void k_iter_begin(DevState* st) {
 // f = f_pre - c ; rowres_i = a_i expm1(f_pre_i/eps + L_i) ; g += c
 __global__ void k_gauge_apply(double* f, const double* L, const double* a, int64_t n, double* g,
                               int64_t m, double inv_eps, double* rowres, DevState* st) {
+    SKNR_PDL_ENTRY();
     if (st->done) return;
     const double c = st->c_gauge;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
@@ -78,6 +84,7 @@ __global__ void k_gauge_apply(double* f, const double* L, const double* a, int64
 // colres_j = b_j expm1((g_j - h_j)/eps)
 __global__ void k_colres(const double* g, const double* h, const double* b, int64_t m, double inv_eps,
                          double* colres, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -87,6 +94,7 @@ __global__ void k_colres(const double* g, const double* h, const double* b, int6
 // alpha - r = -a_i expm1(f_i/eps + L_i(h)) ; r = a - (alpha - r)
 __global__ void k_newton_r(const double* f, const double* L, const double* a, int64_t n, double inv_eps,
                            double* am, double* r, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -101,6 +109,7 @@ __global__ void k_newton_r(const double* f, const double* L, const double* a, in
 // Eigen's llt_inplace::unblocked); delta = LLT.solve(grad).
 __global__ void k_newton_solve(const double* G1, const double* cross, const double* grad, int ell,
                                double inv_eps, double* delta, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     extern __shared__ double sA[];  // ell*ell
     __shared__ int fail;
@@ -165,6 +174,7 @@ __global__ void k_newton_solve(const double* G1, const double* cross, const doub
 // candidate = f + V delta (solver.cpp:45)
 __global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, const double* delta,
                         double* out, DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sd[64];
     if (threadIdx.x < ell) sd[threadIdx.x] = delta[threadIdx.x];
@@ -180,6 +190,7 @@ __global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, co
 // accepted: f <- candidate, next g <- h(candidate); otherwise next g <- h.
 __global__ void k_select(double* f, const double* fcand, int64_t n, double* gnext, const double* h,
                          const double* hcand, int64_t m, DevState* st) {
+    SKNR_PDL_ENTRY();
     if (st->done) return;
     const bool acc = st->newton_ok && st->accept;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n + m;
@@ -196,6 +207,7 @@ __global__ void k_select(double* f, const double* fcand, int64_t n, double* gnex
 // device-side WHILE loop (conditional graph node) -- the loop condition.
 __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled,
                          cudaGraphConditionalHandle loop) {
+    SKNR_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (!st->iter_active) {
         if (loop) cudaGraphSetConditional(loop, 0);
@@ -220,6 +232,7 @@ __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int tr
 }
 
 __global__ void k_axpby(const double* x, const double* y, int64_t n, double a, double b, double* out) {
+    SKNR_PDL_ENTRY();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[i] = a * x[i] + b * y[i];
@@ -228,6 +241,7 @@ __global__ void k_axpby(const double* x, const double* y, int64_t n, double a, d
 // ---- top_modes helpers
 // Y[:,c] -= u0 * s_c
 __global__ void k_deflate(double* Y, int64_t n, int k, const double* u0, const double* s) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -239,6 +253,7 @@ __global__ void k_deflate(double* Y, int64_t n, int k, const double* u0, const d
 
 // out (n x l) = X (n x k) * W (k x l), W col-major
 __global__ void k_small_gemm(const double* X, int64_t n, int k, const double* W, int l, double* out) {
+    SKNR_PDL_ENTRY();
     extern __shared__ double sW[];
     for (int e = threadIdx.x; e < k * l; e += blockDim.x) sW[e] = W[e];
     __syncthreads();
@@ -255,6 +270,7 @@ __global__ void k_small_gemm(const double* X, int64_t n, int k, const double* W,
 // out (n x l) += sgn * X (n x k) * W (k x l), W col-major
 __global__ void k_small_gemm_acc(const double* X, int64_t n, int k, const double* W, int l, double sgn,
                                  double* out) {
+    SKNR_PDL_ENTRY();
     extern __shared__ double sW[];
     for (int e = threadIdx.x; e < k * l; e += blockDim.x) sW[e] = W[e];
     __syncthreads();
@@ -271,6 +287,7 @@ __global__ void k_small_gemm_acc(const double* X, int64_t n, int k, const double
 // R = YW - theta_a XW
 __global__ void k_resid(const double* YW, const double* XW, const double* theta, int64_t n, int l,
                         double* R) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * l;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -280,6 +297,7 @@ __global__ void k_resid(const double* YW, const double* XW, const double* theta,
 }
 
 __global__ void k_div_rows(const double* X, const double* s, int64_t n, int l, double* out) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * l;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -290,6 +308,7 @@ __global__ void k_div_rows(const double* X, const double* s, int64_t n, int l, d
 // stream seeded 0x73706563 is state seed + (t+1)*gamma -- computed in parallel.
 __global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long seed, int64_t n_global,
                                  int64_t row_begin) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -307,6 +326,7 @@ __global__ void k_splitmix_block(double* X, int64_t n, int k, unsigned long long
 // applyHouseholderOnTheLeft, HouseholderQR + householderQ()*Identity):
 // hh[4c..4c+3] = {tau, beta, 1/(c0-beta), zero_tail}
 __global__ void k_hh_norm(double* X, int64_t n, int c, double* part, double* hh, unsigned* counter) {
+    SKNR_PDL_ENTRY();
     __shared__ double sh[AUX_NT];
     double s = 0.0;
     const double* col = X + static_cast<int64_t>(c) * n;
@@ -354,6 +374,7 @@ __global__ void k_hh_norm(double* X, int64_t n, int c, double* part, double* hh,
 // for c2 in [c2lo, k) of matrix M (M==X for the factorisation, Q for forming Q).
 __global__ void k_hh_w(double* X, const double* M, int64_t n, int k, int c, int c2lo, int scale_v,
                        const double* hh, double* part, double* w, unsigned* counter) {
+    SKNR_PDL_ENTRY();
     constexpr int KM = 64;
     __shared__ double sh[AUX_NT];
     __shared__ double sw[KM];
@@ -402,6 +423,7 @@ __global__ void k_hh_w(double* X, const double* M, int64_t n, int k, int c, int 
 // M[r,c2] -= tau w_c2 v_r for r >= c (v_c = 1), c2 in [c2lo, k)
 __global__ void k_hh_update(const double* X, double* M, int64_t n, int k, int c, int c2lo,
                             const double* hh, const double* w) {
+    SKNR_PDL_ENTRY();
     const double tau = hh[4 * c];
     if (tau == 0.0) return;
     const int nw = k - c2lo;
@@ -418,6 +440,7 @@ __global__ void k_hh_update(const double* X, double* M, int64_t n, int k, int c,
 }
 
 __global__ void k_eye(double* Q, int64_t n, int k) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * k;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -430,6 +453,7 @@ __global__ void k_coupling(const double* C, const double* x, const double* y, in
                            int64_t r0, int64_t rows, int d, double kappa, const double* a,
                            const double* b, const double* f, const double* g, double inv_eps,
                            double* plan) {
+    SKNR_PDL_ENTRY();
     const int64_t total = rows * m;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -453,6 +477,7 @@ __global__ void k_coupling(const double* C, const double* x, const double* y, in
 // written in both layouts.
 __global__ void k_build_cost(const double* x, const double* y, int64_t n, int64_t m, int d,
                              double kappa, double* C, double* CT) {
+    SKNR_PDL_ENTRY();
     const int64_t total = n * m;
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -470,6 +495,7 @@ __global__ void k_build_cost(const double* x, const double* y, int64_t n, int64_
 
 // transpose n x m col-major -> m x n col-major
 __global__ void k_transpose(const double* A, int64_t n, int64_t m, double* AT) {
+    SKNR_PDL_ENTRY();
     __shared__ double tile[32][33];
     for (int64_t bj = blockIdx.y * 32; bj < m; bj += static_cast<int64_t>(gridDim.y) * 32)
         for (int64_t bi = blockIdx.x * 32; bi < n; bi += static_cast<int64_t>(gridDim.x) * 32) {

@@ -293,6 +293,7 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
         CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, loop);
         CK(cudaStreamEndCapture(s, &body));
+        make_programmatic(body);
         CK(cudaGraphInstantiate(&exec, graph, 0));
         CK(cudaGraphLaunch(exec, s));
         CK(cudaStreamSynchronize(s));
@@ -300,6 +301,7 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
         CK(cudaStreamEndCapture(s, &graph));
+        make_programmatic(graph);
         CK(cudaGraphInstantiate(&exec, graph, 0));
     }
     int64_t batch = 1;
@@ -391,6 +393,7 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
             CK(cudaStreamBeginCaptureToGraph(P.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
             enqueue_iteration(P, S(b), ell, false, 1, exact_marginals, loop);
             CK(cudaStreamEndCapture(P.stream, &body));
+            make_programmatic(body);
         }
         CK(cudaGraphInstantiate(&exec, graph, 0));
         CK(cudaGraphLaunch(exec, s0));

@@ -137,6 +137,7 @@ struct QrWork {
 // Cholesky G + shift*I = L L^T (shift = coef * trace(G)), then Rinv = L^{-T}
 // (upper). One CTA; k <= 64. *fail = 1 if a pivot is not positive.
 __global__ void k_chol_inv(const double* G, int k, double coef, double* Rinv, int* fail) {
+    SKNR_PDL_ENTRY();
     extern __shared__ double sL[];  // k*k
     __shared__ double piv;
     __shared__ int bad;
@@ -302,6 +303,7 @@ struct OpWork {
 // sub = (v - vt)/eps (+ lw): log-total lower bound of an operator pass's outputs
 __global__ void k_cull_sub(const double* v, const double* vt, const double* lw, double inv_eps, int64_t count,
                            double* sub) {
+    SKNR_PDL_ENTRY();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         sub[i] = (v[i] - vt[i]) * inv_eps + (lw ? lw[i] : 0.0);
@@ -374,6 +376,7 @@ static void apply_sym_sym(Problem& P, const double* f, const double* g, const do
 // Chebyshev three-term step: out = a * (AY - c * Y) - b * Yprev
 __global__ void k_cheb_step(const double* AY, const double* Y, const double* Yprev, int64_t count, double a,
                             double c, double b, double* out) {
+    SKNR_PDL_ENTRY();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[i] = a * (AY[i] - c * Y[i]) - (Yprev ? b * Yprev[i] : 0.0);

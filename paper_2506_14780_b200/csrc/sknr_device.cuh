@@ -22,6 +22,14 @@
 
 namespace sknr {
 
+// Programmatic dependent launch: the solver's graphs join consecutive kernel nodes with
+// programmatic edges (make_programmatic in engine.cu), so a kernel can be scheduled while
+// its predecessor drains. Every kernel therefore first waits for its prerequisite grids
+// to complete (their writes visible), then lets its own dependents begin launching.
+// Both instructions are no-ops for a kernel launched without a programmatic dependency.
+#define SKNR_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
+
 // Table resolution: SKNR_TB = 8 -> 256 entries x 16 replicas (32 KiB), degree-4
 // polynomial (11 FP64 slots per cell); SKNR_TB = 10 -> 1024 entries x 8 replicas
 // (64 KiB), degree-3 minimax polynomial (10 slots per cell).

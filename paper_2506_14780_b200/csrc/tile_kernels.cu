@@ -73,6 +73,7 @@ __device__ __forceinline__ void acc_init(double* acc) {
 template <int D, int JT, int MODE, int KT, int NTT = NT_of<MODE>::value, int UNR = 2, bool FASTCLAMP = false,
           int MINB = 1>
 __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int NT = NTT;
     constexpr int PK = PK_of<D>::value;
@@ -184,6 +185,7 @@ __device__ __forceinline__ double box_dist2(const double* __restrict__ a, const 
 
 template <int D, int JT, int NTT>
 __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = PK_of<D>::value;
     static_assert(32 * JT == CULL_GO, "one warp owns one output group");
@@ -381,6 +383,7 @@ template <int D>
 __global__ void __launch_bounds__(512, 1)
     k_sk_small(SmallProbDev* probs, double tol, long long max_iter, int warm_g, int G, double* gpart,
                unsigned* gbar) {
+    SKNR_PDL_ENTRY();
     constexpr int P = D + 1;
     constexpr int NT = 512;
     constexpr int WPB = NT / 32;
@@ -525,6 +528,7 @@ constexpr int MMA_CH = 64;   // inputs per shared-memory round
 // MCH: inputs staged per shared-memory round (32 with RS keeps 4 CTAs per SM).
 template <int D, int KT, int MB, bool RS = false, int MCH = MMA_CH>
 __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     constexpr int RS_LD = MCH + 4;  // staging row stride (conflict-free half-warp stores)
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = PK_of<D>::value;
@@ -664,6 +668,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 template <int D, int KT, int MB>
 __global__ void __launch_bounds__(MMA_NT, 3) pts_mma_cull_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = PK_of<D>::value;
     constexpr int NCB = KT / 8;
@@ -807,6 +812,7 @@ __global__ void __launch_bounds__(MMA_NT, 3) pts_mma_cull_kernel(TileArgs a) {
 // the current step's math.
 template <int KT, int MB>
 __global__ void __launch_bounds__(MMA_NT) dense_mma_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int NCB = KT / 8;
     constexpr int WS = WStride<KT>::value;
@@ -908,6 +914,7 @@ constexpr int CT_CH = 64;
 
 template <int DK, int MODE, int KT, int MB>
 __global__ void __launch_bounds__(CT_NT) pts_contract_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = DK + 2;
     constexpr int NK = DK / 4;
@@ -1033,6 +1040,7 @@ __global__ void __launch_bounds__(CT_NT) pts_contract_kernel(TileArgs a) {
 // ------------------------------------------------------------- stored cost
 template <int JT, int MODE, int KT>
 __global__ void __launch_bounds__(NT_of<MODE>::value) dense_tile_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int NT = NT_of<MODE>::value;
     constexpr int CH = Chunk<MODE, KT>::value;
@@ -1143,6 +1151,7 @@ __global__ void __launch_bounds__(NT_of<MODE>::value) dense_tile_kernel(TileArgs
 // streams them with one double2 load per input (requires even ldc and n_out).
 template <int JT2, int U, int NTT, int MODE>
 __global__ void __launch_bounds__(NTT) dense_v2_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int NT = NTT;
     constexpr int CH = 256;
