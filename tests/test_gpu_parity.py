@@ -510,3 +510,44 @@ def test_randomized_transforms_and_marginals_match_oracle(seed):
     assert rel_err(row, row_o) <= 1e-12 and rel_err(col, col_o) <= 1e-12
     # the gap at this near-fixed point is itself rounding noise (~1e-14): absolute floor
     assert abs(l2 - l2_o) <= 1e-12 * l2_o + 1e-13
+
+
+def test_programmatic_launch_changes_nothing():
+    """Programmatic dependent launch only changes scheduling: a solve with programmatic
+    edges (default) and one with plain edges (SKNR_NO_PDL=1, fresh process) give
+    bitwise-identical potentials, traces and iteration counts (SK and SK-NR)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    script = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2506_14780_b200 as sk
+from paper_2506_14780_b200 import generators as G
+c = G.config("C1")
+p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+r0 = sk.solve(p, tol=1e-9)
+w = sk.solve(sk.PointProblem(c.x, c.y, c.alpha, c.beta, 2 * c.epsilon), tol=1e-9)
+b = sk.top_modes(sk.PointProblem(c.x, c.y, c.alpha, c.beta, 2 * c.epsilon), w.f, w.g, 10)
+r1 = sk.solve(p, tol=1e-9, ell=10, basis=b, init=(w.f, w.g))
+h = hashlib.sha256()
+for r in (r0, r1):
+    h.update(np.ascontiguousarray(r.f).tobytes()); h.update(np.ascontiguousarray(r.g).tobytes())
+    h.update(str(r.iterations).encode())
+    h.update(np.array([t.marginal_error for t in r.trace]).tobytes())
+print(h.hexdigest(), r0.iterations, r1.iterations)
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_extra in ({}, {"SKNR_NO_PDL": "1"}):
+        env = dict(os.environ)
+        env.pop("SKNR_NO_PDL", None)
+        env.update(env_extra)
+        res = subprocess.run([sys.executable, "-c", script, root], capture_output=True, text=True, env=env,
+                             timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
