@@ -407,6 +407,25 @@ def test_sharded_path_across_R_matches_unsharded(world):
 TOL_NR = 2e-8  # accept decisions at the rounding level (as TOL_POT_NEWTON in test_gpu_parity)
 
 
+@pytest.mark.parametrize("method,degree", [("chebyshev", 8), ("lanczos", 4)])
+def test_sharded_opt_in_basis_methods_match_unsharded(method, degree):
+    """The opt-in basis methods bench.py runs on row-sharded C4 under torchrun: the
+    Chebyshev-filtered subspace iteration and block Lanczos on R = 3 emulated ranks
+    (ragged rows) give the unsharded rhos to 1e-8 and the same subspace."""
+    inst = G.config("C1", n=601, m=433)
+    a = np.full(601, 1 / 601)
+    b = np.full(433, 1 / 433)
+    mk = lambda: sk.PointProblem(inst.x, inst.y, a, b, inst.basis_eps)
+    warm = sk.solve(mk(), tol=1e-10)
+    ref = sk.top_modes(mk(), warm.f, warm.g, 6, method=method, degree=degree)
+    out = sk.run_emulated_shards(mk, 3, lambda p: sk.top_modes(p, warm.f, warm.g, 6, method=method,
+                                                               degree=degree))
+    for tm in out:
+        assert rel_err(tm.rhos, ref.rhos) <= 1e-8
+        assert sk.projector_distance(tm, ref) <= 1e-6
+        assert np.array_equal(tm.vectors, out[0].vectors)
+
+
 def test_culled_sharded_sk_matches_dense_unsharded():
     """Culling on row-sharded handles (each rank culls its own rows against the global
     LSE bound), R = 4 emulated ranks."""

@@ -1,0 +1,116 @@
+"""C4 (north-star config: n=m=65536, d=2, eps=5e-4, ell=32, tol 1e-9) full SK-NR
+main-solve parity against the CPU oracle.
+
+The oracle cannot run the eps'=1e-3 warm solve (2112 SK iterations at ~30-60 s
+each on the host cores), so both sides start the main solve from the SAME inputs:
+the GPU's warm potentials at eps' and the GPU's top_modes basis (the reference's
+`--basis-from` protocol, main.cpp:131-141, with those two inputs fixed). The main
+solve then runs to tolerance on both sides: iteration counts, accept decisions and
+potentials are compared.
+
+  python tools/c4_full_parity.py gpu      # on the B200: writes gpurun_out/c4_full/inputs.npz
+  python tools/c4_full_parity.py oracle   # here (CPU, all cores): resumable, chunks of
+                                          # CHUNK iterations, progress in gpurun_out/c4_full/
+Writes profiles/c4_full_parity_r01.json when the oracle reaches tolerance.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np
+
+from paper_2506_14780_b200 import generators as G
+
+OUT = os.path.join(ROOT, "gpurun_out", "c4_full")
+CHUNK = 5
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+def run_gpu():
+    import paper_2506_14780_b200 as sk
+
+    c = G.config("C4")
+    os.makedirs(OUT, exist_ok=True)
+    pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
+    t0 = time.perf_counter()
+    warm = sk.solve(pw, tol=1e-9, trace=False)
+    t_warm = time.perf_counter() - t0
+    b = sk.top_modes(pw, warm.f, warm.g, c.ell, method="chebyshev", degree=16, max_power_iters=200000)
+    p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+    t0 = time.perf_counter()
+    r = sk.solve(p, tol=1e-9, ell=c.ell, basis=b, init=(warm.f, warm.g), trace=True)
+    t_main = time.perf_counter() - t0
+    np.savez(os.path.join(OUT, "inputs.npz"), warm_f=warm.f, warm_g=warm.g, V=b.vectors, rhos=b.rhos,
+             f=r.f, g=r.g, iterations=r.iterations, converged=r.converged,
+             marginal_error=np.array([t.marginal_error for t in r.trace]),
+             semi_dual_value=np.array([t.semi_dual_value for t in r.trace]),
+             accepted=np.array([bool(t.newton_accepted) for t in r.trace]),
+             attempted=np.array([bool(t.newton_attempted) for t in r.trace]))
+    info = {"warm_iterations": warm.iterations, "warm_s": t_warm, "basis_sweeps": b.sweeps,
+            "main_iterations": r.iterations, "main_s": t_main, "converged": r.converged,
+            "accepts": int(sum(t.newton_accepted for t in r.trace))}
+    json.dump(info, open(os.path.join(OUT, "gpu_info.json"), "w"), indent=1)
+    print(json.dumps(info), flush=True)
+
+
+def run_oracle():
+    import oracle_ref as O
+
+    c = G.config("C4")
+    d = np.load(os.path.join(OUT, "inputs.npz"))
+    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y)
+    state_path = os.path.join(OUT, "oracle_state.npz")
+    if os.path.exists(state_path):
+        s = np.load(state_path)
+        f, g, done = s["f"], s["g"], int(s["done"])
+        trace = [tuple(t) for t in s["trace"]]
+        secs = float(s["secs"])
+    else:
+        f, g, done, trace, secs = d["warm_f"], d["warm_g"], 0, [], 0.0
+    print("oracle threads", O.max_threads(), "resuming at", done, flush=True)
+    converged = bool(trace) and trace[-1][0] < 1e-9
+    while not converged and done < 400:
+        t0 = time.time()
+        r = O.solve(op, tol=1e-9, max_iter=CHUNK, ell=c.ell, V=d["V"], init=(f, g), trace=True)
+        secs += time.time() - t0
+        f, g = r["f"], r["g"]
+        trace += r["trace"]
+        done += r["iterations"]
+        converged = r["converged"]
+        np.savez(state_path, f=f, g=g, done=done, trace=np.array(trace, dtype=float), secs=secs)
+        print(f"iter {done}: err {trace[-1][0]:.3e} accepted {int(sum(t[4] for t in trace))} "
+              f"({secs:.0f} s)", flush=True)
+    acc_o = [bool(t[4]) for t in trace]
+    acc_g = [bool(a) for a in d["accepted"]]
+    first_diff = next((i for i, (a, b) in enumerate(zip(acc_g, acc_o)) if a != b), None)
+    me_g, me_o = d["marginal_error"], np.array([t[0] for t in trace])
+    k = min(len(me_g), len(me_o))
+    out = {
+        "config": "C4 n=m=65536 d=2 eps=5e-4 ell=32 tol=1e-9; main SK-NR solve from the GPU's eps'=1e-3 "
+                  "warm potentials and chebyshev(16) top_modes basis on both sides",
+        "oracle_threads": O.max_threads(), "oracle_s": secs,
+        "iterations": {"gpu": int(d["iterations"]), "oracle": done},
+        "converged": {"gpu": bool(d["converged"]), "oracle": bool(converged)},
+        "accepts": {"gpu": int(sum(acc_g)), "oracle": int(sum(acc_o))},
+        "first_differing_accept": first_diff,
+        "rel_f": rel(d["f"], f), "rel_g": rel(d["g"], g),
+        "max_rel_marginal_error_diff_common_prefix": float(np.max(np.abs(me_g[:k] - me_o[:k]) / me_o[:k])),
+        "marginal_error_gpu": [float(v) for v in me_g], "marginal_error_oracle": [float(v) for v in me_o],
+        "accepted_gpu": acc_g, "accepted_oracle": acc_o,
+    }
+    gi = os.path.join(OUT, "gpu_info.json")
+    if os.path.exists(gi):
+        out["gpu"] = json.load(open(gi))
+    json.dump(out, open(os.path.join(ROOT, "profiles", "c4_full_parity_r01.json"), "w"), indent=1)
+    print(json.dumps({k: v for k, v in out.items() if not isinstance(v, list)}), flush=True)
+
+
+if __name__ == "__main__":
+    {"gpu": run_gpu, "oracle": run_oracle}[sys.argv[1]]()
