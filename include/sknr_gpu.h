@@ -89,6 +89,15 @@ int sknr_problem_destroy(sknr_problem p);
  * 0 turns culling off). Point clouds with d <= 4 (sharded handles cull their own
  * rows). The sums change by less than n e^-threshold relative (< 1e-21 at 60). */
 int sknr_problem_set_culling(sknr_problem p, double threshold);
+/* Opt-in reduced precision of the column/row LSE sum passes (not in the reference,
+ * which is fp64 throughout; BASELINE north star "1e-5 if an fp32 variant is
+ * offered"): bits = 32 evaluates each cell's exponent in fp32 and its exp2 on the
+ * MUFU unit (accumulation, shifts, potentials and every other pass stay fp64);
+ * bits = 64 (default) restores the fp64 path. Point clouds with d <= 4; culling,
+ * when enabled, takes precedence. Per-term relative error ~2^-24 |u| (u the cell
+ * exponent in bits before the shift cancels), so potentials move by ~eps * 1e-4
+ * at eps = 5e-4; the solver's own marginal test converges to the fp32 fixed point. */
+int sknr_problem_set_precision(sknr_problem p, int bits);
 
 /* ---------------------------------------------------------------- core.hpp
  * core.hpp:16-43 / core.cpp:35-150 on host buffers (upload, device kernels,
@@ -245,6 +254,8 @@ int sknr_bench_iterations(sknr_problem p, const sknr_config* cfg, const double* 
 /* Measured FP64 FMA ceiling of the current device (TFLOP/s, FMA = 2 flops):
  * the denominator of the on-the-fly roofline (MEASURED_PEAKS.json has no FP64 entry). */
 int sknr_bench_fp64_peak(double* tflops, double* ms);
+/* Measured MUFU ex2.approx.f32 ceiling (G ex2/s): the denominator of the fp32 roofline. */
+int sknr_bench_mufu_peak(double* gex2_per_s, double* ms);
 /* Tuning aid: device ms of launch variant `variant` of the d=2 column-LSE sum
  * kernel on this problem (tools/tune_lse.py). */
 int sknr_tune_variant(sknr_problem p, int variant, int passes, double* kernel_ms);

@@ -237,14 +237,24 @@ void restricted_derivatives(const Problem& p, const Vec& f, const Vec& g, const 
     Vec Vr(static_cast<size_t>(n) * ell);  // row-major copy: contiguous per i (same arithmetic)
     for (Index c = 0; c < ell; ++c)
         for (Index i = 0; i < n; ++i) Vr[i * ell + c] = V[i + c * n];
-    par_for(m, [&](Index j) {
-        std::vector<double> s(ell, 0.0);
+    // Columns in blocks of kJB per task: each V row is read once per block instead of
+    // once per column (the n x ell V streams from memory otherwise); every S[c, j] still
+    // accumulates over i in ascending order, so the result is unchanged.
+    constexpr Index kJB = 16;
+    par_for((m + kJB - 1) / kJB, [&](Index jb) {
+        const Index j0 = jb * kJB, jn = std::min(kJB, m - j0);
+        std::vector<double> s(static_cast<size_t>(ell) * kJB, 0.0);
         for (Index i = 0; i < n; ++i) {
-            const double w = p.a[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
             const double* vr = &Vr[i * ell];
-            for (Index c = 0; c < ell; ++c) s[c] += vr[c] * w;
+            for (Index q = 0; q < jn; ++q) {
+                const Index j = j0 + q;
+                const double w = p.a[i] * std::exp((f[i] + g[j] - p.C(i, j)) * inv_eps);
+                double* sq = &s[q * ell];
+                for (Index c = 0; c < ell; ++c) sq[c] += vr[c] * w;
+            }
         }
-        for (Index c = 0; c < ell; ++c) S[c + j * ell] = s[c];
+        for (Index q = 0; q < jn; ++q)
+            for (Index c = 0; c < ell; ++c) S[c + (j0 + q) * ell] = s[q * ell + c];
     });
     // row marginal r += chunk * b_seg, chunk by chunk (objective.cpp:127-128)
     Vec r(n, 0.0);

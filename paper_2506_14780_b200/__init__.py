@@ -84,6 +84,7 @@ _SIGS = {
                           _D, ctypes.POINTER(ctypes.c_int)],
     "sknr_problem_destroy": [_P],
     "sknr_problem_set_culling": [_P, ctypes.c_double],
+    "sknr_problem_set_precision": [_P, ctypes.c_int],
     "sknr_ctransform_of_f": [_P, _D, _D],
     "sknr_ctransform_of_g": [_P, _D, _D],
     "sknr_plan_marginals": [_P, _D, _D, _D, _D, _D, _D],
@@ -122,6 +123,7 @@ _SIGS = {
     "sknr_bench_iterations": [_P, ctypes.POINTER(_Config), _D, _I64, _I64, _I64, ctypes.c_int, _D,
                               ctypes.POINTER(_I64)],
     "sknr_bench_fp64_peak": [_D, _D],
+    "sknr_bench_mufu_peak": [_D, _D],
     "sknr_tune_variant": [_P, ctypes.c_int, ctypes.c_int, _D],
     "sknr_debug_counters": [_P, ctypes.POINTER(_I64)],
     "sknr_comm_unique_id": [ctypes.c_void_p],
@@ -257,6 +259,8 @@ class Problem:
             q = PointProblem(p._x, p._y, p._alpha, p._beta, eps, p._cost_scale, p._cost_mode)
             if getattr(p, "_cull", 0.0) > 0.0:
                 q.set_culling(p._cull)
+            if getattr(p, "_precision", 64) != 64:
+                q.set_precision(p._precision)
             return q
         return Problem(p._cost, p._alpha, p._beta, eps)
 
@@ -316,6 +320,13 @@ class PointProblem(Problem):
         (Morton-ordered group bounds; 0 disables). Not in the reference API."""
         _check(lib().sknr_problem_set_culling(self.handle, float(threshold)))
         self._cull = float(threshold)
+
+    def set_precision(self, bits: int) -> None:
+        """Opt-in: bits=32 runs the LSE sum passes with fp32 cell exponents and MUFU exp2
+        (accumulation and potentials stay fp64; potentials within ~1e-5 relative of the
+        fp64 path); bits=64 (default) is the reference's arithmetic. Not in the reference API."""
+        _check(lib().sknr_problem_set_precision(self.handle, int(bits)))
+        self._precision = int(bits)
 
     @property
     def cost(self) -> np.ndarray:
@@ -998,6 +1009,14 @@ def bench_fp64_peak():
     """(TFLOP/s, ms) of a DFMA-only kernel filling every SM: the measured FP64 ceiling."""
     t, ms = ctypes.c_double(), ctypes.c_double()
     _check(lib().sknr_bench_fp64_peak(ctypes.byref(t), ctypes.byref(ms)))
+    return t.value, ms.value
+
+
+def bench_mufu_peak():
+    """(G ex2/s, ms) of an ex2.approx.f32-only kernel filling every SM: the MUFU ceiling
+    of the fp32 sum pass (set_precision(32))."""
+    t, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().sknr_bench_mufu_peak(ctypes.byref(t), ctypes.byref(ms)))
     return t.value, ms.value
 
 

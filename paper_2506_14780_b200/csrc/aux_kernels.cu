@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
         if (threadIdx.x < 32) {
             bool bad = false;
             if (valid) {
-                bad = !(S >= 0x1p-900 && S <= 0x1p900);
+                bad = !(S >= a.lo_ok && S <= 0x1p900);
                 const double L = a.shift[o] + log(S);
                 if (a.L) a.L[o] = L;
                 if (a.pot) a.pot[o] = -a.eps * L;

@@ -69,6 +69,7 @@ struct FinalizeArgs {
     int retry_phase = 0;
     DevState* st = nullptr;
     unsigned guard = 0;
+    double lo_ok = 0x1p-900;  // lse: a sum below this means the bound shift was too loose
 };
 
 // Culling bounds: over permuted positions, the maximum of pack[i*pk] + lskc*sq[i]

@@ -291,6 +291,8 @@ struct Problem {
     std::shared_ptr<SolveState> solve_cache;  // per-solve device buffers, reused across solves
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
+    // sknr_problem_set_precision: 64 (default) or 32 (LSE sum passes in fp32 on MUFU, points d <= 4)
+    int precision = 64;
     bool cull_ready = false;
     DBuf f_gi[2], s_go[2], f_g32[2], s_g16[2];
     DBuf gram_part, sums, misc;
@@ -715,6 +717,12 @@ static unsigned retry_bit(int dir) { return dir == 0 ? G_RETRY0 : G_RETRY1; }
 // (C,eps)-transform in direction dir (0: g <- f^{C,eps}, core.cpp:35-54; 1: f <-
 // g^{C,eps}, core.cpp:56-82). Writes L (natural-log LSE) into P.L[dir] and, if
 // pot != nullptr, the potential -eps*L.
+// Sum-pass kernel family of an LSE direction: culled (opt-in) before fp32 (opt-in) before fp64.
+static int sum_mode(const Problem& P, int dir) {
+    if (cull_active(P, dir)) return MODE_SUM_CULL;
+    return P.precision == 32 ? MODE_SUM_F32 : MODE_SUM;
+}
+
 static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned guard) {
     Side& in = P.in_side(dir);
     Side& out = P.out_side(dir);
@@ -722,7 +730,8 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     cudaStream_t s = P.stream;
     const TilePlan tmax = plan_for(P, dir, MODE_MAX, 0);
     const bool cull = cull_active(P, dir);
-    const TilePlan tsum = plan_for(P, dir, cull ? MODE_SUM_CULL : MODE_SUM, 0);
+    const bool f32 = sum_mode(P, dir) == MODE_SUM_F32;
+    const TilePlan tsum = plan_for(P, dir, sum_mode(P, dir), 0);
 
     PrepInArgs pi;
     pi.count = nin;
@@ -743,6 +752,9 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     pi.guard = guard;
     const bool split = P.shard && dir == 0;  // column transform reduces over sharded rows
     pi.defer = split ? 1 : 0;
+    // fp32 terms underflow below 2^-126: take the exact shift once the bound could sit
+    // more than 40 nats (58 bits) above the true maximum
+    if (f32) pi.exact_spread = 40.0;
     const int gin = std::min(grid_for(nin), 148 * 8);
     count_launch();
     k_prep_in<<<gin, AUX_NT, 0, s>>>(pi);
@@ -786,6 +798,7 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     fa.pot = pot;
     fa.dir = dir;
     fa.st = P.st;
+    if (f32) fa.lo_ok = 0x1p-60;  // smallest sum whose leading fp32 terms are still normal
 
     for (int phase = 0; phase < 2; ++phase) {
         const unsigned gmax = guard | (phase == 0 ? exact_bit(dir) : retry_bit(dir));

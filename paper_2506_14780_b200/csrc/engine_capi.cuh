@@ -250,6 +250,17 @@ int sknr_problem_set_culling(sknr_problem h, double threshold) {
     SKNR_API_END
 }
 
+int sknr_problem_set_precision(sknr_problem h, int bits) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (bits != 32 && bits != 64) throw InvalidArgument("set_precision: bits must be 32 or 64");
+    if (bits == 32 && (P.dim < 1 || P.dim > 4))
+        throw InvalidArgument("set_precision: fp32 needs a point-cloud problem with d <= 4");
+    P.precision = bits;
+    SKNR_API_END
+}
+
 int sknr_problem_destroy(sknr_problem h) {
     SKNR_API_BEGIN
     delete h;
@@ -1132,7 +1143,9 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    TilePlan tsum = plan_for(P, 0, MODE_SUM, 0);
+    // the plain (unculled) sum kernel of this handle's precision
+    const int smode = P.precision == 32 ? MODE_SUM_F32 : MODE_SUM;
+    TilePlan tsum = plan_for(P, 0, smode, 0);
     auto one = [&]() {
         switch (which) {
             case 0: lse(P, 0, f.p, g.p, G_NONE); break;
@@ -1163,7 +1176,7 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
     *ms_per_pass = ms / passes;
     if (kernel_ms_per_pass) {
         // the dominant tile kernel alone, on the same stream
-        TilePlan tp = which == 1 ? plan_for(P, 1, MODE_SUM, 0)
+        TilePlan tp = which == 1 ? plan_for(P, 1, smode, 0)
                                  : (which >= 3 ? plan_for(P, 0, MODE_BLOCK, kt, 8) : tsum);
         TileArgs ta = tile_args(P, which == 1 ? 1 : 0, tp, G_NONE);
         if (which >= 3) ta.W = Wv.p;
@@ -1246,14 +1259,65 @@ __global__ void k_fp64_peak(double* out, int iters, double a0, double b0) {
     if (s == 12345.678) out[0] = s;
 }
 
+// MUFU ex2 ceiling (the fp32 sum pass's bound): 8 independent ex2.approx chains per
+// thread over the same full grid.
+__global__ void k_mufu_peak(float* out, int iters, float a0) {
+    SKNR_PDL_ENTRY();
+    float x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = -1.0f - (threadIdx.x + c) * 1e-6f;
+    const float a = a0 + threadIdx.x * 1e-9f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            float r;
+            asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x[c]));
+            x[c] = r - a;  // stays in (-1.0, 0): one FADD per ex2 keeps the chain live
+        }
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s += x[c];
+    if (s == 12345.678f) out[0] = s;
+}
+
+int sknr_bench_mufu_peak(double* gex2_per_s, double* ms) {
+    SKNR_API_BEGIN
+    check_device();
+    int sms = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf out;
+    out.ensure(1);
+    float* o = reinterpret_cast<float*>(out.p);
+    const int iters = 8000, grid = sms * 8, block = 256;
+    k_mufu_peak<<<grid, block>>>(o, 100, 1.5f);
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0));
+    count_launch();
+    k_mufu_peak<<<grid, block>>>(o, iters, 1.5f);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    *gex2_per_s = 8.0 * iters * static_cast<double>(grid) * block / (t * 1e-3) / 1e9;
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    SKNR_API_END
+}
+
 // Time launch-configuration variant v of the d=2 column-LSE sum kernel on this
 // problem's current packed state (tuning aid; see tools/tune_lse.py).
 int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    const bool block = variant >= 200;
-    if (variant < 100 && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
+    const bool block = variant >= 200 && variant < 300;
+    if ((variant < 100 || variant >= 300) && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
     if (variant >= 100 && variant < 200 && P.dim != 0)
         throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
     if (block && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");

@@ -239,7 +239,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
     plan_for(P, 0, MODE_MAX, 0);
     plan_for(P, 1, MODE_MAX, 0);
     for (int dir = 0; dir < 2; ++dir)
-        if (cull_active(P, dir)) plan_for(P, dir, MODE_SUM_CULL, 0);
+        if (sum_mode(P, dir) != MODE_SUM) plan_for(P, dir, sum_mode(P, dir), 0);
     if (init_f)
         upload_rows(P, S.f.p, init_f);
     else {

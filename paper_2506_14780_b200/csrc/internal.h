@@ -12,7 +12,10 @@ namespace sknr {
 // MODE_SUM_CULL: sum pass over spatially sorted point clouds that skips (output
 // group, input group) pairs whose every term is provably below e^-T of the
 // output's total (points d <= 4, opt-in; see pts_cull_kernel).
-enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4, MODE_BLOCK_CULL = 5 };
+// MODE_SUM_F32: opt-in fp32 sum pass (sknr_problem_set_precision(p, 32); points d <= 4):
+// the same partial sums with the cell exponent in fp32 and exp2 on the MUFU unit.
+enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4, MODE_BLOCK_CULL = 5,
+       MODE_SUM_F32 = 6 };
 
 // Group sizes of the culling bounds (permuted positions): the sum pass tests input
 // groups of CULL_GI against output groups of CULL_GO (one warp's 32 x 4 outputs);

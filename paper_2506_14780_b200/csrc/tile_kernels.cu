@@ -162,6 +162,140 @@ __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
     }
 }
 
+// ------------------------------------------------------------- fp32 sum pass (opt-in)
+// MODE_SUM_F32 (sknr_problem_set_precision(p, 32)): the sum pass of pts_tile_kernel with
+// the cell exponent in fp32 and 2^v on the MUFU unit (ex2.approx.ftz.f32). The fp64 pack
+// (u = A + B + <X, Y>) is re-expanded around the squared distance, in log2 units:
+//   v = u/256 = A'/256 + B'/256 - |Xs - Ys|^2,  A' = A + |X|^2/2, B' = B + |Y|^2/2,
+//   Xs = X / sqrt(512)
+// and the potential-carrying terms are split on a 2^-8 grid:
+//   A'/256 = Ah + Al, Ah = rint(A')/256, |Al| <= 2^-9   (B' likewise)
+// so that, per cell, s = Ah + Bh is exact in fp32 (|Ah|, |Bh| < 2^15), the squared
+// distance q = |Xs - Ys|^2 depends on the coordinates alone, and v = s - q is one
+// rounding at the ulp of v (< 3e-8 for the terms that carry the sum). 2^Al enters as
+// an fp32 weight per input (FFMA into the partial), 2^Bl as an fp64 factor per output.
+// The coordinate rounding (|Xs| < 2^5: 1e-6 absolute) is a FIXED perturbation of the
+// kernel (a few 1e-6 per term at C4), so the solver converges in its own marginals and
+// the potentials stay within ~1e-6 relative of the fp64 path. Per cell: 7 FP32 ops +
+// 1 MUFU; the MUFU pipe (16 ex2 / clk / SM on sm_100: 4.65 TCells/s at 1.965 GHz) and
+// the issue slot (8 per cell) bound it together. Partials accumulate in fp32 over 32
+// inputs, then in fp64, in the fp64 [ib][n_out] layout: the finalize kernels are shared
+// (with the fp32 validity window FinalizeArgs::lo_ok).
+__device__ __forceinline__ float ex2_mufu(float v) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+// 2^t for |t| <= 2^-9 to fp64 accuracy (truncation below 1e-13)
+__device__ __forceinline__ double exp2_small(double t) {
+    const double z = t * 0.6931471805599453;
+    return 1.0 + z * (1.0 + z * (0.5 + z * (1.0 / 6.0)));
+}
+
+constexpr double kInvSqrt512 = 0.04419417382415922;  // 1/sqrt(512)
+
+template <int D>
+struct PKF_of {  // fp32 input pack: Ah, 2^Al, D coords, padded to a float4 multiple
+    static constexpr int value = ((D + 2 + 3) / 4) * 4;
+};
+
+template <int D, int JT, int NTT>
+__global__ void __launch_bounds__(NTT) pts_f32_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int PKF = PKF_of<D>::value;
+    constexpr int CH = 256;
+    constexpr int SUB = 32;  // inputs per fp32 partial sum
+    extern __shared__ __align__(16) float smf[];
+    const int tid = threadIdx.x;
+    const int64_t out_tile = static_cast<int64_t>(NTT) * JT;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        float B[JT], Y[JT][D];
+        double acc[JT], bscale[JT];
+        int64_t o[JT];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            o[jt] = ot * out_tile + jt * NTT + tid;
+            const int64_t oc = o[jt] < a.n_out ? o[jt] : a.n_out - 1;
+            double bv = a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double yd = a.out_pack[oc * PK + 1 + d];
+                bv = fma(0.5 * yd, yd, bv);
+                Y[jt][d] = static_cast<float>(yd * kInvSqrt512);
+            }
+            const double bh = rint(bv);
+            B[jt] = static_cast<float>(bh * (1.0 / 256.0));
+            bscale[jt] = exp2_small((bv - bh) * (1.0 / 256.0));
+            acc[jt] = 0.0;
+        }
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+            const int cnt = static_cast<int>((i1 - c0) < CH ? (i1 - c0) : CH);
+            const int cnt32 = (cnt + SUB - 1) / SUB * SUB;
+            __syncthreads();
+            for (int t = tid; t < cnt32 * PKF; t += NTT) {
+                const int k = t / PKF, q = t % PKF;
+                float v = 0.0f;
+                if (k >= cnt) {
+                    v = q == 0 ? -1e30f : 0.0f;  // padding inputs: 2^v = 0 and weight 0
+                } else if (q < 2) {
+                    const double* ip = a.in_pack + (c0 + k) * PK;
+                    double av = ip[0];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) av = fma(0.5 * ip[1 + d], ip[1 + d], av);
+                    const double ah = rint(av);
+                    v = q == 0 ? static_cast<float>(ah * (1.0 / 256.0))
+                               : static_cast<float>(exp2_small((av - ah) * (1.0 / 256.0)));
+                } else if (q < 2 + D) {
+                    v = static_cast<float>(a.in_pack[(c0 + k) * PK + q - 1] * kInvSqrt512);
+                }
+                smf[t] = v;
+            }
+            __syncthreads();
+            for (int k0 = 0; k0 < cnt32; k0 += SUB) {
+                float part[JT];
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) part[jt] = 0.0f;
+#pragma unroll 4
+                for (int k = k0; k < k0 + SUB; ++k) {
+                    float x[PKF];
+#pragma unroll
+                    for (int q = 0; q < PKF / 4; ++q) {
+                        const float4 v = reinterpret_cast<const float4*>(smf + k * PKF)[q];
+                        x[4 * q] = v.x;
+                        x[4 * q + 1] = v.y;
+                        x[4 * q + 2] = v.z;
+                        x[4 * q + 3] = v.w;
+                    }
+#pragma unroll
+                    for (int jt = 0; jt < JT; ++jt) {
+                        const float d0 = x[2] - Y[jt][0];
+                        float q = d0 * d0;
+#pragma unroll
+                        for (int d = 1; d < D; ++d) {
+                            const float dd = x[2 + d] - Y[jt][d];
+                            q = fmaf(dd, dd, q);
+                        }
+                        const float v = (x[0] + B[jt]) - q;
+                        part[jt] = fmaf(x[1], ex2_mufu(v), part[jt]);
+                    }
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) acc[jt] += static_cast<double>(part[jt]);
+            }
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+            if (o[jt] < a.n_out) a.partial[ib * a.n_out + o[jt]] = acc[jt] * bscale[jt];
+    }
+}
+
 // ------------------------------------------------------------- culled sum pass (opt-in)
 // Both point clouds are visited in Morton order (perm_in / perm_out), so a warp's
 // 256 outputs and a 64-input group each cover a small box. For every term
@@ -1245,6 +1379,16 @@ KernelInfo make_pts() {
     return k;
 }
 
+template <int D, int JT, int NTT>
+KernelInfo make_f32() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_f32_kernel<D, JT, NTT>);
+    k.jt = JT;
+    k.nt = NTT;
+    k.smem = static_cast<int>(sizeof(float)) * 256 * PKF_of<D>::value;
+    return k;
+}
+
 template <int D>
 KernelInfo make_cull() {
     KernelInfo k;
@@ -1307,7 +1451,8 @@ KernelInfo make_contract() {
 
 template <int DK>
 KernelInfo pick_contract(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL) return KernelInfo{};
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32)
+        return KernelInfo{};
     if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
     if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
     switch (kt) {
@@ -1328,6 +1473,7 @@ KernelInfo pick_pts(int mode, int kt) {
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
     if (mode == MODE_SUM_CULL) return make_cull<D>();
+    if (mode == MODE_SUM_F32) return make_f32<D, 8, 256>();
     if (mode == MODE_BLOCK_CULL) {
         switch (kt) {
             case 8: return make_mma_cull<D, 8>();
@@ -1386,7 +1532,8 @@ KernelInfo make_dense_mma() {
 }
 
 KernelInfo pick_dense(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL) return KernelInfo{};
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32)
+        return KernelInfo{};
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
     switch (kt) {  // FP64 tensor-core (DMMA) block pass
@@ -1450,6 +1597,13 @@ KernelInfo tune_variant(int v) {
         case 205: return make_mma<2, 32, 2, true>();
         case 206: return make_mma<2, 32, 4, true, 32>();
         case 207: return make_mma<2, 32, 4, false, 32>();
+        // fp32 sum pass (MUFU ex2), d=2
+        case 300: return make_f32<2, 8, 256>();
+        case 301: return make_f32<2, 4, 256>();
+        case 302: return make_f32<2, 16, 256>();
+        case 303: return make_f32<2, 8, 128>();
+        case 304: return make_f32<2, 16, 128>();
+        case 305: return make_f32<2, 8, 512>();
         default: return KernelInfo{};
     }
 }
@@ -1503,7 +1657,14 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     // register kernels leave most SMs idle; use 128-output tiles instead.
     const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS || mode == MODE_BLOCK_CULL;
     const bool culled = mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL;
-    if (variant < 0 && dim > 0 && !blk && !culled && n_out * n_in <= (int64_t(1) << 26)) {
+    if (variant < 0 && dim > 0 && mode == MODE_SUM_F32 && n_out * n_in <= (int64_t(1) << 26)) {
+        switch (dim) {
+            case 1: ki = make_f32<1, 1, 128>(); break;
+            case 2: ki = make_f32<2, 1, 128>(); break;
+            case 3: ki = make_f32<3, 1, 128>(); break;
+            default: ki = make_f32<4, 1, 128>(); break;
+        }
+    } else if (variant < 0 && dim > 0 && !blk && !culled && n_out * n_in <= (int64_t(1) << 26)) {
         switch (dim) {
             case 1: ki = mode == MODE_SUM ? make_pts<1, 1, MODE_SUM, 0, 128, 2>() : make_pts<1, 1, MODE_MAX, 0, 128, 2>(); break;
             case 2: ki = mode == MODE_SUM ? make_pts<2, 1, MODE_SUM, 0, 128, 2>() : make_pts<2, 1, MODE_MAX, 0, 128, 2>(); break;
