@@ -314,6 +314,8 @@ def run_ours(args, world, rank, local):
     # ---- time to tolerance: C1 (reference basis method) and C3 (Chebyshev-filtered basis)
     ttt = None
 
+    kept = {}
+
     def ttt_case(name, method, cull=0.0, degree=8):
         # SK and SK-NR(ell) to marginal error 1e-9 from inputs resident on the device;
         # SK-NR end to end = warm SK solve at eps' + top_modes basis + main solve.
@@ -335,6 +337,8 @@ def run_ours(args, world, rank, local):
             return out, dist_max(dist, time.perf_counter() - t0)
 
         r_sk, t_sk = timed(lambda: sk.solve(p1, tol=1e-9, trace=False))
+        if not cull:
+            kept[name] = r_sk
         warm, t_warm = timed(lambda: sk.solve(p1w, tol=1e-9, trace=False))
         b1, t_basis = timed(lambda: sk.top_modes(p1w, warm.f, warm.g, c.ell, method=method, degree=degree,
                                                  max_power_iters=200000))
@@ -375,6 +379,34 @@ def run_ours(args, world, rank, local):
             ttt["C4"] = ttt_case("C4", "chebyshev", degree=16)
             ttt["C4_culled"] = ttt_case("C4", "chebyshev", cull=60.0, degree=16)
             ttt["C4_culled"]["note"] = cull_note
+
+    # ---- opt-in fp32 variant (sknr_problem_set_precision(32), north star "1e-5 if an fp32
+    # variant is offered"): LSE sum passes with fp32 exponents on the MUFU ex2 unit
+    fp32 = None
+    if world == 1 and not args.no_ttt:
+        p32 = make_problem()
+        p32.set_precision(32)
+        gex2, _ = sk.bench_mufu_peak()
+        ms32_pass, ms32_k = sk.bench_pass(p32, 2, 0, passes=10)
+        ms32_it, _ = sk.bench_iterations(p32, 0, None, iters=args.steps, warmup=max(args.warmup, 3),
+                                         flush_l2=True)
+        g32 = cells / (ms32_k * 1e-3) / 1e9
+        fp32 = {"sweep_gcells_per_s": 2.0 * cells / (ms32_it * 1e-3) / 1e9, "ms_per_step": ms32_it,
+                "roofline": {"bound": "mufu", "kernel": "pts_f32_kernel<2,8,256> (column LSE, fp32 exponent, "
+                                                        "ex2.approx)",
+                             "kernel_ms": ms32_k, "achieved": g32, "peak": gex2, "unit": "G ex2/s",
+                             "frac": g32 / gex2, "algorithmic_per_cell": "1 MUFU ex2 + 7 FP32 ops",
+                             "peak_source": "measured ex2-only kernel on this GPU (sknr_bench_mufu_peak)"}}
+        if "C4" in kept:
+            ref = kept["C4"]
+            t0 = time.perf_counter()
+            r32 = sk.solve(p32, tol=1e-9, trace=False)
+            t32 = time.perf_counter() - t0
+            fp32["C4_sk_ttt"] = {"iterations": r32.iterations, "converged": r32.converged, "ms": t32 * 1e3,
+                                 "fp64_iterations": ref.iterations,
+                                 "rel_f_vs_fp64": float(np.max(np.abs(r32.f - ref.f)) / np.max(np.abs(ref.f))),
+                                 "rel_g_vs_fp64": float(np.max(np.abs(r32.g - ref.g)) / np.max(np.abs(ref.g)))}
+        del p32
 
     # ---- batched small problems: 32 C1 instances, SK to 1e-9
     batch = None
@@ -454,6 +486,7 @@ def run_ours(args, world, rank, local):
             "pass_ms": {"column_lse_full": ms_pass, "row_lse_full": ms_row_pass,
                         "row_lse_kernel_gcells_per_s": cells_local / (ms_row_kernel * 1e-3) / 1e9},
             "roofline_stored": stored,
+            "fp32_variant": fp32,
             "time_to_tol": ttt,
             "batch_c1": batch,
             "library": sk.version(),
