@@ -200,8 +200,23 @@ struct PKF_of {  // fp32 input pack: Ah, 2^Al, D coords, padded to a float4 mult
     static constexpr int value = ((D + 2 + 3) / 4) * 4;
 };
 
-template <int D, int JT, int NTT>
-__global__ void __launch_bounds__(NTT) pts_f32_kernel(TileArgs a) {
+// 2^(B'/256 - Bh) of an output: the fp64 factor that completes its fp32 sums
+template <int D, int PK>
+__device__ __forceinline__ double f32_out_split(const double* pk, float& Bh, float* Y) {
+    double bv = pk[0];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const double yd = pk[1 + d];
+        bv = fma(0.5 * yd, yd, bv);
+        if (Y) Y[d] = static_cast<float>(yd * kInvSqrt512);
+    }
+    const double bh = rint(bv);
+    Bh = static_cast<float>(bh * (1.0 / 256.0));
+    return exp2_small((bv - bh) * (1.0 / 256.0));
+}
+
+template <int D, int JT, int NTT, int MINB = 1>
+__global__ void __launch_bounds__(NTT, MINB) pts_f32_kernel(TileArgs a) {
     SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = PK_of<D>::value;
@@ -215,22 +230,12 @@ __global__ void __launch_bounds__(NTT) pts_f32_kernel(TileArgs a) {
     for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
         float B[JT], Y[JT][D];
-        double acc[JT], bscale[JT];
-        int64_t o[JT];
+        double acc[JT];
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
-            o[jt] = ot * out_tile + jt * NTT + tid;
-            const int64_t oc = o[jt] < a.n_out ? o[jt] : a.n_out - 1;
-            double bv = a.out_pack[oc * PK];
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const double yd = a.out_pack[oc * PK + 1 + d];
-                bv = fma(0.5 * yd, yd, bv);
-                Y[jt][d] = static_cast<float>(yd * kInvSqrt512);
-            }
-            const double bh = rint(bv);
-            B[jt] = static_cast<float>(bh * (1.0 / 256.0));
-            bscale[jt] = exp2_small((bv - bh) * (1.0 / 256.0));
+            const int64_t o = ot * out_tile + jt * NTT + tid;
+            const int64_t oc = o < a.n_out ? o : a.n_out - 1;
+            f32_out_split<D, PK>(a.out_pack + oc * PK, B[jt], Y[jt]);
             acc[jt] = 0.0;
         }
         const int64_t i0 = ib * a.in_block;
@@ -291,8 +296,14 @@ __global__ void __launch_bounds__(NTT) pts_f32_kernel(TileArgs a) {
             }
         }
 #pragma unroll
-        for (int jt = 0; jt < JT; ++jt)
-            if (o[jt] < a.n_out) a.partial[ib * a.n_out + o[jt]] = acc[jt] * bscale[jt];
+        for (int jt = 0; jt < JT; ++jt) {
+            const int64_t o = ot * out_tile + jt * NTT + tid;
+            if (o < a.n_out) {
+                float bh;  // the output's split again (not held in registers across the loop)
+                const double scale = f32_out_split<D, PK>(a.out_pack + o * PK, bh, nullptr);
+                a.partial[ib * a.n_out + o] = acc[jt] * scale;
+            }
+        }
     }
 }
 
@@ -1379,10 +1390,10 @@ KernelInfo make_pts() {
     return k;
 }
 
-template <int D, int JT, int NTT>
+template <int D, int JT, int NTT, int MINB = 1>
 KernelInfo make_f32() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_f32_kernel<D, JT, NTT>);
+    k.fn = reinterpret_cast<const void*>(&pts_f32_kernel<D, JT, NTT, MINB>);
     k.jt = JT;
     k.nt = NTT;
     k.smem = static_cast<int>(sizeof(float)) * 256 * PKF_of<D>::value;
@@ -1473,7 +1484,7 @@ KernelInfo pick_pts(int mode, int kt) {
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
     if (mode == MODE_SUM_CULL) return make_cull<D>();
-    if (mode == MODE_SUM_F32) return make_f32<D, 8, 256>();
+    if (mode == MODE_SUM_F32) return make_f32<D, 8, 512, 2>();  // best of tools/fp32_probe.py variants 300-311
     if (mode == MODE_BLOCK_CULL) {
         switch (kt) {
             case 8: return make_mma_cull<D, 8>();
@@ -1604,6 +1615,12 @@ KernelInfo tune_variant(int v) {
         case 303: return make_f32<2, 8, 128>();
         case 304: return make_f32<2, 16, 128>();
         case 305: return make_f32<2, 8, 512>();
+        case 306: return make_f32<2, 8, 256, 3>();
+        case 307: return make_f32<2, 4, 256, 4>();
+        case 308: return make_f32<2, 8, 128, 6>();
+        case 309: return make_f32<2, 16, 128, 3>();
+        case 310: return make_f32<2, 6, 256, 3>();
+        case 311: return make_f32<2, 8, 512, 2>();
         default: return KernelInfo{};
     }
 }

@@ -1,5 +1,6 @@
 """ncu target: the C4 column-LSE sum tile kernel (and the ell-wide block pass).
-Usage: python tools/profile_lse.py [which]   which=2 LSE sum kernel, 3 block pass."""
+Usage: python tools/profile_lse.py [which] [bits]   which=2 LSE sum kernel, 3 block pass;
+bits=32 profiles the opt-in fp32 sum kernel (set_precision(32))."""
 import os
 import sys
 
@@ -11,5 +12,7 @@ from paper_2506_14780_b200 import generators as G
 which = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 inst = G.config("C4")
 p = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, inst.epsilon)
+if len(sys.argv) > 2 and int(sys.argv[2]) == 32:
+    p.set_precision(32)
 ms, kms = sk.bench_pass(p, which, inst.ell, passes=2)
 print(f"which={which} pass {ms:.3f} ms kernel {kms:.3f} ms")
