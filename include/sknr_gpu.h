@@ -93,10 +93,12 @@ int sknr_problem_set_culling(sknr_problem p, double threshold);
  * which is fp64 throughout; BASELINE north star "1e-5 if an fp32 variant is
  * offered"): bits = 32 evaluates each cell's exponent in fp32 and its exp2 on the
  * MUFU unit (accumulation, shifts, potentials and every other pass stay fp64);
- * bits = 64 (default) restores the fp64 path. Point clouds with d <= 4; culling,
- * when enabled, takes precedence. Per-term relative error ~2^-24 |u| (u the cell
- * exponent in bits before the shift cancels), so potentials move by ~eps * 1e-4
- * at eps = 5e-4; the solver's own marginal test converges to the fp32 fixed point. */
+ * bits = 64 (default) restores the fp64 path bit for bit. Point clouds with
+ * d <= 4; combines with culling (the kept groups in fp32). The cell exponent is
+ * re-expanded around the squared distance with the potential terms on a 2^-8 grid
+ * (exact fp32 sums), so the fp32 rounding is a fixed perturbation of the kernel
+ * (~1e-6 per term): the solver still converges to tol in its own marginals and the
+ * potentials stay within ~1e-6 relative of the fp64 path. */
 int sknr_problem_set_precision(sknr_problem p, int bits);
 
 /* ---------------------------------------------------------------- core.hpp

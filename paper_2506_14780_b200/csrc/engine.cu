@@ -717,10 +717,11 @@ static unsigned retry_bit(int dir) { return dir == 0 ? G_RETRY0 : G_RETRY1; }
 // (C,eps)-transform in direction dir (0: g <- f^{C,eps}, core.cpp:35-54; 1: f <-
 // g^{C,eps}, core.cpp:56-82). Writes L (natural-log LSE) into P.L[dir] and, if
 // pot != nullptr, the potential -eps*L.
-// Sum-pass kernel family of an LSE direction: culled (opt-in) before fp32 (opt-in) before fp64.
+// Sum-pass kernel family of an LSE direction: culled and/or fp32 (both opt-in), else fp64.
 static int sum_mode(const Problem& P, int dir) {
-    if (cull_active(P, dir)) return MODE_SUM_CULL;
-    return P.precision == 32 ? MODE_SUM_F32 : MODE_SUM;
+    const bool f32 = P.precision == 32;
+    if (cull_active(P, dir)) return f32 ? MODE_SUM_CULL_F32 : MODE_SUM_CULL;
+    return f32 ? MODE_SUM_F32 : MODE_SUM;
 }
 
 static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned guard) {
@@ -730,7 +731,7 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     cudaStream_t s = P.stream;
     const TilePlan tmax = plan_for(P, dir, MODE_MAX, 0);
     const bool cull = cull_active(P, dir);
-    const bool f32 = sum_mode(P, dir) == MODE_SUM_F32;
+    const bool f32 = P.precision == 32;
     const TilePlan tsum = plan_for(P, dir, sum_mode(P, dir), 0);
 
     PrepInArgs pi;

@@ -14,8 +14,9 @@ namespace sknr {
 // output's total (points d <= 4, opt-in; see pts_cull_kernel).
 // MODE_SUM_F32: opt-in fp32 sum pass (sknr_problem_set_precision(p, 32); points d <= 4):
 // the same partial sums with the cell exponent in fp32 and exp2 on the MUFU unit.
+// MODE_SUM_CULL_F32: both (the culled pass with the fp32 arithmetic on its kept groups).
 enum { MODE_SUM = 0, MODE_MAX = 1, MODE_BLOCK = 2, MODE_BLOCK_RS = 3, MODE_SUM_CULL = 4, MODE_BLOCK_CULL = 5,
-       MODE_SUM_F32 = 6 };
+       MODE_SUM_F32 = 6, MODE_SUM_CULL_F32 = 7 };
 
 // Group sizes of the culling bounds (permuted positions): the sum pass tests input
 // groups of CULL_GI against output groups of CULL_GO (one warp's 32 x 4 outputs);

@@ -328,7 +328,8 @@ __device__ __forceinline__ double box_dist2(const double* __restrict__ a, const 
     return s;
 }
 
-template <int D, int JT, int NTT>
+// F32: the kept groups' terms in the fp32 arithmetic of pts_f32_kernel (opt-in precision).
+template <int D, int JT, int NTT, bool F32 = false>
 __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
     SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
@@ -357,13 +358,18 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
         const int64_t og = unit % a.n_out_tiles, ib = unit / a.n_out_tiles;
         const int64_t wpos = og * CULL_GO;
         double B[JT], Y[JT][D], acc[JT];
+        float Bf[JT], Yf[JT][D];
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
             const int64_t pos = wpos + jt * 32 + lane;
             const int64_t oc = a.perm_out[pos < a.n_out ? pos : a.n_out - 1];
-            B[jt] = a.out_pack[oc * PK];
+            if (F32) {
+                f32_out_split<D, PK>(a.out_pack + oc * PK, Bf[jt], Yf[jt]);
+            } else {
+                B[jt] = a.out_pack[oc * PK];
 #pragma unroll
-            for (int d = 0; d < D; ++d) Y[jt][d] = a.out_pack[oc * PK + 1 + d];
+                for (int d = 0; d < D; ++d) Y[jt][d] = a.out_pack[oc * PK + 1 + d];
+            }
             acc[jt] = 0.0;
         }
         double wbox[2 * D];
@@ -392,6 +398,53 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
             const int64_t g0 = r0 + static_cast<int64_t>(bit) * CULL_GI;
             const int cnt = static_cast<int>((i1 - g0) < CULL_GI ? (i1 - g0) : CULL_GI);
             __syncwarp();
+            if constexpr (F32) {  // fp32 pack (Ah, 2^Al, Xs...) of the group, one input per lane
+                constexpr int PKF = PKF_of<D>::value;
+                static_assert(PKF <= 2 * PK, "fp32 pack fits the fp64 staging row");
+                float* sf = reinterpret_cast<float*>(sin);
+                for (int t = lane; t < cnt; t += 32) {
+                    const double* ip = a.in_pack + static_cast<int64_t>(a.perm_in[g0 + t]) * PK;
+                    double av = ip[0];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) av = fma(0.5 * ip[1 + d], ip[1 + d], av);
+                    const double ah = rint(av);
+                    sf[t * PKF] = static_cast<float>(ah * (1.0 / 256.0));
+                    sf[t * PKF + 1] = static_cast<float>(exp2_small((av - ah) * (1.0 / 256.0)));
+#pragma unroll
+                    for (int d = 0; d < D; ++d) sf[t * PKF + 2 + d] = static_cast<float>(ip[1 + d] * kInvSqrt512);
+#pragma unroll
+                    for (int q = D + 2; q < PKF; ++q) sf[t * PKF + q] = 0.0f;
+                }
+                __syncwarp();
+                float part[JT];
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) part[jt] = 0.0f;
+#pragma unroll 2
+                for (int k = 0; k < cnt; ++k) {
+                    float x[PKF];
+#pragma unroll
+                    for (int q = 0; q < PKF / 4; ++q) {
+                        const float4 v = reinterpret_cast<const float4*>(sf + k * PKF)[q];
+                        x[4 * q] = v.x;
+                        x[4 * q + 1] = v.y;
+                        x[4 * q + 2] = v.z;
+                        x[4 * q + 3] = v.w;
+                    }
+#pragma unroll
+                    for (int jt = 0; jt < JT; ++jt) {
+                        const float d0 = x[2] - Yf[jt][0];
+                        float q2 = d0 * d0;
+#pragma unroll
+                        for (int d = 1; d < D; ++d) {
+                            const float dd = x[2 + d] - Yf[jt][d];
+                            q2 = fmaf(dd, dd, q2);
+                        }
+                        part[jt] = fmaf(x[1], ex2_mufu((x[0] + Bf[jt]) - q2), part[jt]);
+                    }
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) acc[jt] += static_cast<double>(part[jt]);
+            } else {
             for (int t = lane; t < cnt; t += 32) {
                 const double2* src = reinterpret_cast<const double2*>(a.in_pack +
                                                                       static_cast<int64_t>(a.perm_in[g0 + t]) * PK);
@@ -417,12 +470,21 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
                     acc[jt] = pexp_acc<false, false>(u, tab, laneoff, c3, acc[jt]);
                 }
             }
+            }
         }
         }
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
             const int64_t pos = wpos + jt * 32 + lane;
-            if (pos < a.n_out) a.partial[ib * a.n_out + a.perm_out[pos]] = acc[jt];
+            if (pos < a.n_out) {
+                const int64_t o = a.perm_out[pos];
+                double scale = 1.0;
+                if (F32) {
+                    float bh;
+                    scale = f32_out_split<D, PK>(a.out_pack + o * PK, bh, nullptr);
+                }
+                a.partial[ib * a.n_out + o] = acc[jt] * scale;
+            }
         }
         if (lane == 0) {
             DevState* st = const_cast<DevState*>(a.st);
@@ -1400,10 +1462,10 @@ KernelInfo make_f32() {
     return k;
 }
 
-template <int D>
+template <int D, bool F32 = false>
 KernelInfo make_cull() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_cull_kernel<D, 4, 256>);
+    k.fn = reinterpret_cast<const void*>(&pts_cull_kernel<D, 4, 256, F32>);
     k.jt = 4;
     k.nt = 256;
     k.out_tile = CULL_GO;  // work units are per warp
@@ -1462,7 +1524,8 @@ KernelInfo make_contract() {
 
 template <int DK>
 KernelInfo pick_contract(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32)
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32 ||
+        mode == MODE_SUM_CULL_F32)
         return KernelInfo{};
     if (mode == MODE_SUM) return make_contract<DK, MODE_SUM, 0, 2>();
     if (mode == MODE_MAX) return make_contract<DK, MODE_MAX, 0, 2>();
@@ -1484,6 +1547,7 @@ KernelInfo pick_pts(int mode, int kt) {
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
     if (mode == MODE_SUM_CULL) return make_cull<D>();
+    if (mode == MODE_SUM_CULL_F32) return make_cull<D, true>();
     if (mode == MODE_SUM_F32) return make_f32<D, 8, 512, 2>();  // best of tools/fp32_probe.py variants 300-311
     if (mode == MODE_BLOCK_CULL) {
         switch (kt) {
@@ -1543,7 +1607,8 @@ KernelInfo make_dense_mma() {
 }
 
 KernelInfo pick_dense(int mode, int kt) {
-    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32)
+    if (mode == MODE_BLOCK_RS || mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_F32 ||
+        mode == MODE_SUM_CULL_F32)
         return KernelInfo{};
     if (mode == MODE_SUM) return make_dense<2, MODE_SUM, 0>();
     if (mode == MODE_MAX) return make_dense<2, MODE_MAX, 0>();
@@ -1673,7 +1738,7 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     // Small problems (e.g. C1 512^2, C2 4096^2): the 2048-output tiles of the
     // register kernels leave most SMs idle; use 128-output tiles instead.
     const bool blk = mode == MODE_BLOCK || mode == MODE_BLOCK_RS || mode == MODE_BLOCK_CULL;
-    const bool culled = mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL;
+    const bool culled = mode == MODE_SUM_CULL || mode == MODE_BLOCK_CULL || mode == MODE_SUM_CULL_F32;
     if (variant < 0 && dim > 0 && mode == MODE_SUM_F32 && n_out * n_in <= (int64_t(1) << 26)) {
         switch (dim) {
             case 1: ki = make_f32<1, 1, 128>(); break;
@@ -1706,7 +1771,7 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
     p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
     // input-block granularity (the kernels stage up to their chunk size per round)
     const int ch = mode == MODE_BLOCK_CULL ? CULL_GB
-                                          : (blk ? chunk_inputs(MODE_BLOCK, kt) : (mode == MODE_SUM_CULL ? CULL_GI : 32));
+                                          : (blk ? chunk_inputs(MODE_BLOCK, kt) : (mode == MODE_SUM_CULL || mode == MODE_SUM_CULL_F32 ? CULL_GI : 32));
     const int64_t max_blocks_by_chunk = (n_in + ch - 1) / ch;
     // Aim for >= 8 tiles per resident CTA so the last wave's imbalance stays small
     // (culled pass: >= 8 work units per resident warp, taken from a queue).

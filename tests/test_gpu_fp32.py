@@ -133,3 +133,29 @@ def test_fp32_sharded_matches_unsharded():
 def test_mufu_peak_is_measured():
     gex2, ms = sk.bench_mufu_peak()
     assert 1000.0 < gex2 < 20000.0 and ms > 0
+
+
+def test_fp32_culled_matches_fp32_dense():
+    """Both opt-ins together: culling (terms below e^-60 skipped) with the fp32 arithmetic
+    on the kept groups; a 4096^2 C4-shaped problem at eps = 2e-3."""
+    inst = G.config("C4", n=4096, m=4096)
+
+    def mk(cull):
+        p = sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, 2e-3)
+        p.set_precision(32)
+        if cull:
+            p.set_culling(60.0)
+        return p
+
+    ref = sk.solve(mk(False), tol=1e-9)
+    pc = mk(True)
+    r = sk.solve(pc, tol=1e-9)
+    assert sk.debug_counters(pc)["cull_kept"] < sk.debug_counters(pc)["cull_tested"]
+    assert r.converged, (r.iterations, ref.iterations)
+    # fp32 group sums round differently from the dense kernel's: near tol the
+    # stopping iteration can move by a few (as against the oracle, test above)
+    assert abs(r.iterations - ref.iterations) <= 3 + ref.iterations // 100, (r.iterations, ref.iterations)
+    assert rel_err(r.f, ref.f) <= 1e-6 and rel_err(r.g, ref.g) <= 1e-6
+    op = O.Instance(inst.alpha, inst.beta, 2e-3, x=inst.x, y=inst.y)
+    f = random_vector(G.SplitMix64(3), inst.n, 0.01)
+    assert rel_err(sk.ctransform_of_f(pc, f), O.ctransform_of_f(op, f)) <= TOL_F32
