@@ -358,10 +358,12 @@ def run_ours(args, world, rank, local):
 
     cull_note = ("opt-in culling (sknr_problem_set_culling, T=60): terms below e^-60 of their output's "
                  "total skipped under rigorous group bounds")
+    # C4 basis: restarted block Lanczos (12 blocks per cycle; 26 operator applications vs 81
+    # for Chebyshev(16))
     if not args.no_ttt and world > 1 and not args.no_c4_ttt:
         # north-star time-to-tolerance at R GPUs: C4 row-sharded over all ranks (NCCL)
-        ttt = {"C4": ttt_case("C4", "chebyshev", degree=16),
-               "C4_culled": ttt_case("C4", "chebyshev", cull=60.0, degree=16)}
+        ttt = {"C4": ttt_case("C4", "lanczos", degree=12),
+               "C4_culled": ttt_case("C4", "lanczos", cull=60.0, degree=12)}
         ttt["C4_culled"]["note"] = cull_note
     if not args.no_ttt and world == 1:
         ttt = {"C1": ttt_case("C1", "subspace"), "C3": ttt_case("C3", "chebyshev")}
@@ -378,8 +380,8 @@ def run_ours(args, world, rank, local):
                             "converged": all(s.converged for s in stages)}
         del p2c
         if not args.no_c4_ttt:
-            ttt["C4"] = ttt_case("C4", "chebyshev", degree=16)
-            ttt["C4_culled"] = ttt_case("C4", "chebyshev", cull=60.0, degree=16)
+            ttt["C4"] = ttt_case("C4", "lanczos", degree=12)
+            ttt["C4_culled"] = ttt_case("C4", "lanczos", cull=60.0, degree=12)
             ttt["C4_culled"]["note"] = cull_note
 
     # ---- opt-in fp32 variant (sknr_problem_set_precision(32), north star "1e-5 if an fp32
@@ -409,30 +411,37 @@ def run_ours(args, world, rank, local):
                                  "rel_f_vs_fp64": float(np.max(np.abs(r32.f - ref.f)) / np.max(np.abs(ref.f))),
                                  "rel_g_vs_fp64": float(np.max(np.abs(r32.g - ref.g)) / np.max(np.abs(ref.g)))}
         if "C4_nr" in kept:
-            # SK-NR(32) end to end with only the eps' warm solve in fp32: the main solve is
-            # the fp64 path from a warm start / basis that differ at the fp32 level
+            # SK-NR(32) end to end with only the eps' warm solve in fp32: the basis and the
+            # main solve are the fp64 path, from a warm start that differs at the fp32 level
+            # (dense, and with culling on every pass)
             c = G.config("C4")
-            pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
-            pw.set_precision(32)
-            t0 = time.perf_counter()
-            w32 = sk.solve(pw, tol=1e-9, trace=False)
-            t_w = time.perf_counter() - t0
-            pw.set_precision(64)
-            b32 = sk.top_modes(pw, w32.f, w32.g, c.ell, method="chebyshev", degree=16, max_power_iters=200000)
-            t_b = time.perf_counter() - t0 - t_w
-            pm = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
-            t0 = time.perf_counter()
-            rm = sk.solve(pm, tol=1e-9, ell=c.ell, basis=b32, init=(w32.f, w32.g), trace=False)
-            t_m = time.perf_counter() - t0
             ref = kept["C4_nr"]
-            fp32["C4_sknr_fp32_warm"] = {
-                "warm_iterations": w32.iterations, "warm_ms": t_w * 1e3, "basis_ms": t_b * 1e3,
-                "basis_operator_applications": b32.sweeps, "main_iterations": rm.iterations,
-                "main_converged": rm.converged, "main_ms": t_m * 1e3, "ms_end_to_end": (t_w + t_b + t_m) * 1e3,
-                "fp64_pipeline_main_iterations": ref.iterations,
-                "rel_f_vs_fp64_pipeline": float(np.max(np.abs(rm.f - ref.f)) / np.max(np.abs(ref.f))),
-                "note": "eps'=1e-3 warm SK solve in fp32, basis and main SK-NR(32) solve in fp64"}
-            del pw, pm
+            for key, cull in (("C4_sknr_fp32_warm", 0.0), ("C4_sknr_fp32_warm_culled", 60.0)):
+                pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
+                pm = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+                if cull:
+                    pw.set_culling(cull)
+                    pm.set_culling(cull)
+                pw.set_precision(32)
+                t0 = time.perf_counter()
+                w32 = sk.solve(pw, tol=1e-9, trace=False)
+                t_w = time.perf_counter() - t0
+                pw.set_precision(64)
+                b32 = sk.top_modes(pw, w32.f, w32.g, c.ell, method="lanczos", degree=12, max_power_iters=200000)
+                t_b = time.perf_counter() - t0 - t_w
+                t0 = time.perf_counter()
+                rm = sk.solve(pm, tol=1e-9, ell=c.ell, basis=b32, init=(w32.f, w32.g), trace=False)
+                t_m = time.perf_counter() - t0
+                fp32[key] = {
+                    "culling": cull or None, "warm_iterations": w32.iterations, "warm_ms": t_w * 1e3,
+                    "basis_ms": t_b * 1e3, "basis_method": "lanczos(12)",
+                    "basis_operator_applications": b32.sweeps, "main_iterations": rm.iterations,
+                    "main_converged": rm.converged, "main_ms": t_m * 1e3,
+                    "ms_end_to_end": (t_w + t_b + t_m) * 1e3,
+                    "fp64_pipeline_main_iterations": ref.iterations,
+                    "rel_f_vs_fp64_pipeline": float(np.max(np.abs(rm.f - ref.f)) / np.max(np.abs(ref.f))),
+                    "note": "eps'=1e-3 warm SK solve in fp32, basis and main SK-NR(32) solve in fp64"}
+                del pw, pm
         del p32
 
     # ---- batched small problems: 32 C1 instances, SK to 1e-9
