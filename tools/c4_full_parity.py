@@ -112,58 +112,61 @@ def run_oracle():
     print(json.dumps({k: v for k, v in out.items() if not isinstance(v, list)}), flush=True)
 
 
-def run_tail(k0):
-    """On the GPU box (16 host cores): the GPU's main-solve iterate after k0 iterations
-    (same deterministic trajectory as the full solve), then the oracle from that
-    iterate to tolerance. The oracle's own trajectory covers iterations 1..k0 here
-    (run_oracle); together they cover the whole main solve."""
+def run_segment(k0, k1, budget_s=3000.0):
+    """On the GPU box (16 host cores; one gpurun call is capped at an hour): the GPU's
+    main-solve iterates after k0 and k1 iterations (the same deterministic trajectory
+    as the full solve), then the oracle from iterate k0 for up to k1 - k0 iterations
+    (or to tolerance, or until budget_s): accept decisions and marginal errors per
+    iteration and the potentials at the segment's end are compared with the GPU's.
+    Segments [35,60), [60,85), [85,end) plus the oracle's own trajectory over [0,35)
+    (run_oracle, here) cover the whole main solve."""
     import oracle_ref as O
     import paper_2506_14780_b200 as sk
 
     c = G.config("C4")
-    src = os.path.join(ROOT, "c4_full_inputs", "inputs.npz")
-    d = np.load(src)
+    d = np.load(os.path.join(ROOT, "c4_full_inputs", "inputs.npz"))
     os.makedirs(OUT, exist_ok=True)
     p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
     basis = sk.SpectralBasis(np.asfortranarray(d["V"]), np.asfortranarray(d["V"]), d["rhos"], c.basis_eps)
-    rk = sk.solve(p, tol=1e-9, max_iter=k0, ell=c.ell, basis=basis, init=(d["warm_f"], d["warm_g"]), trace=True)
-    np.savez(os.path.join(OUT, f"gpu_iterate_{k0}.npz"), f=rk.f, g=rk.g)
-    same = [bool(t.newton_accepted) for t in rk.trace] == [bool(a) for a in d["accepted"][:k0]]
+    init = (d["warm_f"], d["warm_g"])
+    r0 = sk.solve(p, tol=1e-9, max_iter=k0, ell=c.ell, basis=basis, init=init, trace=True)
+    same = [bool(t.newton_accepted) for t in r0.trace] == [bool(a) for a in d["accepted"][:k0]]
     print("gpu iterate", k0, "same accepts as the full solve:", same, flush=True)
     op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y)
-    f, g, done, trace, secs = rk.f, rk.g, k0, [], 0.0
-    converged = False
-    while not converged and done < 400:
+    f, g, done, trace, secs = r0.f, r0.g, k0, [], 0.0
+    converged, last = False, 0.0
+    while not converged and done < k1 and secs + 1.2 * last < budget_s:
         t0 = time.time()
-        r = O.solve(op, tol=1e-9, max_iter=CHUNK, ell=c.ell, V=d["V"], init=(f, g), trace=True)
-        secs += time.time() - t0
+        r = O.solve(op, tol=1e-9, max_iter=min(CHUNK, k1 - done), ell=c.ell, V=d["V"], init=(f, g), trace=True)
+        last = time.time() - t0
+        secs += last
         f, g = r["f"], r["g"]
         trace += r["trace"]
         done += r["iterations"]
         converged = r["converged"]
         print(f"iter {done}: err {trace[-1][0]:.3e} ({secs:.0f} s)", flush=True)
+    r1 = sk.solve(p, tol=1e-9, max_iter=done, ell=c.ell, basis=basis, init=init, trace=False)
     acc_o = [bool(t[4]) for t in trace]
-    acc_g = [bool(a) for a in d["accepted"][k0:]]
-    me_g = d["marginal_error"][k0:]
+    acc_g = [bool(a) for a in d["accepted"][k0:done]]
+    me_g = d["marginal_error"][k0:done]
     me_o = np.array([t[0] for t in trace])
     k = min(len(me_g), len(me_o))
-    out = {"k0": k0, "oracle_threads": O.max_threads(), "oracle_s": secs,
+    out = {"k0": k0, "end": done, "oracle_threads": O.max_threads(), "oracle_s": secs,
            "gpu_iterate_same_accepts": same,
-           "iterations": {"gpu": int(d["iterations"]), "oracle_from_gpu_iterate": done},
-           "converged": {"gpu": bool(d["converged"]), "oracle": bool(converged)},
-           "accepts_after_k0": {"gpu": int(sum(acc_g)), "oracle": int(sum(acc_o))},
-           "first_differing_accept_after_k0": next((k0 + i for i, (a, b) in enumerate(zip(acc_g, acc_o))
-                                                    if a != b), None),
-           "rel_f": rel(d["f"], f), "rel_g": rel(d["g"], g),
-           "max_rel_marginal_error_diff": float(np.max(np.abs(me_g[:k] - me_o[:k]) / me_o[:k])),
+           "gpu_total_iterations": int(d["iterations"]), "oracle_converged_at": done if converged else None,
+           "gpu_converged_at_end": bool(r1.converged),
+           "accepts": {"gpu": int(sum(acc_g)), "oracle": int(sum(acc_o))},
+           "same_accepts": acc_g == acc_o[:len(acc_g)],
+           "rel_f_end": rel(r1.f, f), "rel_g_end": rel(r1.g, g),
+           "max_rel_marginal_error_diff": float(np.max(np.abs(me_g[:k] - me_o[:k]) / me_o[:k])) if k else None,
            "marginal_error_gpu": [float(v) for v in me_g], "marginal_error_oracle": [float(v) for v in me_o],
            "accepted_gpu": acc_g, "accepted_oracle": acc_o}
-    json.dump(out, open(os.path.join(OUT, "tail.json"), "w"), indent=1)
+    json.dump(out, open(os.path.join(OUT, f"seg_{k0}.json"), "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if not isinstance(v, list)}), flush=True)
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "tail":
-        run_tail(int(sys.argv[2]))
+    if sys.argv[1] == "segment":
+        run_segment(int(sys.argv[2]), int(sys.argv[3]))
     else:
         {"gpu": run_gpu, "oracle": run_oracle}[sys.argv[1]]()
