@@ -72,14 +72,25 @@ def load_instance(a, epsilon: float) -> Problem:
 
 
 def cmd_solve(a) -> int:
-    """cmd_solve (main.cpp:120-157)."""
+    """cmd_solve (main.cpp:120-157). Opt-in additions (point clouds only, not in the
+    reference CLI): --cull T (skip terms below e^-T), --warm-fp32 (the --basis-from warm
+    solve with fp32 LSE passes), --basis-method (chebyshev / lanczos top_modes)."""
     problem = load_instance(a, a.epsilon)
+    if (a.cull or a.warm_fp32) and not isinstance(problem, PointProblem):
+        raise ValueError("--cull / --warm-fp32 need a point-cloud instance (--points or --synthetic)")
+    if a.cull:
+        problem.set_culling(a.cull)
     basis, init = None, None
     if a.ell > 0:
         warm_eps = a.basis_from if a.basis_from is not None else a.epsilon
         warm_problem = problem.with_epsilon(warm_eps)
+        if a.warm_fp32:
+            warm_problem.set_precision(32)
         warm = solve(warm_problem, tol=a.tol, max_iter=a.max_iter, ell=0, trace=not a.no_trace)
-        basis = top_modes(warm_problem, warm.f, warm.g, a.ell)
+        if a.warm_fp32:
+            warm_problem.set_precision(64)
+        degree = 12 if a.basis_method == "lanczos" else 8
+        basis = top_modes(warm_problem, warm.f, warm.g, a.ell, method=a.basis_method, degree=degree)
         if a.basis_from is not None:
             init = (warm.f, warm.g)
     result = solve(problem, tol=a.tol, max_iter=a.max_iter, ell=a.ell, basis=basis, init=init,
@@ -145,6 +156,12 @@ def build_parser() -> argparse.ArgumentParser:
                    help="Build the basis (and warm start) from the solution at this epsilon")
     s.add_argument("--out", default=".", help="Output directory")
     s.add_argument("--no-trace", action="store_true", help="Skip the per-iteration trace file")
+    s.add_argument("--cull", type=float, default=0.0,
+                   help="Opt-in: skip LSE terms below e^-T of their output's total (point clouds, T >= 40)")
+    s.add_argument("--warm-fp32", action="store_true",
+                   help="Opt-in: run the --basis-from warm solve with fp32 LSE passes (point clouds)")
+    s.add_argument("--basis-method", choices=["subspace", "chebyshev", "lanczos"], default="subspace",
+                   help="top_modes method (subspace = the reference's)")
     s.set_defaults(fn=cmd_solve)
     p = sub.add_parser("spectrum", help="Eigen-structure reports across epsilons")
     _add_instance_flags(p)

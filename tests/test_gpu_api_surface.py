@@ -224,6 +224,25 @@ def test_cli_solve_spectrum_anneal(tmp_path, capsys):  # main.cpp:120-218
     assert rc == 2
 
 
+def test_cli_opt_in_flags(tmp_path, capsys):
+    """--cull / --warm-fp32 / --basis-method (additions beyond the reference CLI) give the
+    reference pipeline's potentials to the solve tolerance's resolution."""
+    base = ["solve", "--synthetic", "gauss2d", "--n", "300", "--m", "280", "--epsilon", "0.01", "--ell", "6",
+            "--basis-from", "0.02", "--no-trace"]
+    assert cli.main(base + ["--out", str(tmp_path / "ref")]) == 0
+    assert cli.main(base + ["--cull", "60", "--warm-fp32", "--basis-method", "lanczos",
+                            "--out", str(tmp_path / "opt")]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert all(line.startswith("converged=true") for line in out[-2:])
+    read = lambda d: np.array([float(l.split(",")[2]) for l in open(tmp_path / d / "potentials.csv").read()
+                               .splitlines()[1:]])
+    assert rel_err(read("opt"), read("ref")) <= 1e-7
+    np.savetxt(tmp_path / "c.csv", np.ones((3, 3)), delimiter=",")
+    rc = cli.main(["solve", "--cost", str(tmp_path / "c.csv"), "--epsilon", "0.5", "--cull", "60", "--out",
+                   str(tmp_path / "x")])
+    assert rc == 1 and "point-cloud" in capsys.readouterr().err
+
+
 def test_cli_zero_cost_exact_outer_product(tmp_path):  # test_cli.cpp:74-90
     (tmp_path / "zero3x3.csv").write_text("0,0,0\n0,0,0\n0,0,0\n")
     rc = cli.main(["solve", "--cost", str(tmp_path / "zero3x3.csv"), "--epsilon", "0.5", "--out",
