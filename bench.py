@@ -410,38 +410,41 @@ def run_ours(args, world, rank, local):
                                  "fp64_iterations": ref.iterations,
                                  "rel_f_vs_fp64": float(np.max(np.abs(r32.f - ref.f)) / np.max(np.abs(ref.f))),
                                  "rel_g_vs_fp64": float(np.max(np.abs(r32.g - ref.g)) / np.max(np.abs(ref.g)))}
-        if "C4_nr" in kept:
-            # SK-NR(32) end to end with only the eps' warm solve in fp32: the basis and the
-            # main solve are the fp64 path, from a warm start that differs at the fp32 level
-            # (dense, and with culling on every pass)
-            c = G.config("C4")
-            ref = kept["C4_nr"]
-            for key, cull in (("C4_sknr_fp32_warm", 0.0), ("C4_sknr_fp32_warm_culled", 60.0)):
-                pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
-                pm = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
-                if cull:
-                    pw.set_culling(cull)
-                    pm.set_culling(cull)
-                pw.set_precision(32)
-                t0 = time.perf_counter()
-                w32 = sk.solve(pw, tol=1e-9, trace=False)
-                t_w = time.perf_counter() - t0
-                pw.set_precision(64)
-                b32 = sk.top_modes(pw, w32.f, w32.g, c.ell, method="lanczos", degree=12, max_power_iters=200000)
-                t_b = time.perf_counter() - t0 - t_w
-                t0 = time.perf_counter()
-                rm = sk.solve(pm, tol=1e-9, ell=c.ell, basis=b32, init=(w32.f, w32.g), trace=False)
-                t_m = time.perf_counter() - t0
-                fp32[key] = {
-                    "culling": cull or None, "warm_iterations": w32.iterations, "warm_ms": t_w * 1e3,
-                    "basis_ms": t_b * 1e3, "basis_method": "lanczos(12)",
-                    "basis_operator_applications": b32.sweeps, "main_iterations": rm.iterations,
-                    "main_converged": rm.converged, "main_ms": t_m * 1e3,
-                    "ms_end_to_end": (t_w + t_b + t_m) * 1e3,
-                    "fp64_pipeline_main_iterations": ref.iterations,
-                    "rel_f_vs_fp64_pipeline": float(np.max(np.abs(rm.f - ref.f)) / np.max(np.abs(ref.f))),
-                    "note": "eps'=1e-3 warm SK solve in fp32, basis and main SK-NR(32) solve in fp64"}
-                del pw, pm
+        # SK-NR(ell) end to end with only the eps' warm solve in fp32: the basis and the main
+        # solve are the fp64 path, from a warm start that differs at the fp32 level (C4 dense
+        # and culled on every pass, Lanczos basis; C3 with the Chebyshev basis of its fp64 leg)
+        cases = [("C4_sknr_fp32_warm", "C4", 0.0, "lanczos", 12), ("C4_sknr_fp32_warm_culled", "C4", 60.0, "lanczos", 12),
+                 ("C3_sknr_fp32_warm", "C3", 0.0, "chebyshev", 8)]
+        for key, name, cull, method, degree in cases:
+            if name + "_nr" not in kept:
+                continue
+            c = G.config(name)
+            ref = kept[name + "_nr"]
+            pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps, c.cost_scale)
+            pm = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale)
+            if cull:
+                pw.set_culling(cull)
+                pm.set_culling(cull)
+            pw.set_precision(32)
+            t0 = time.perf_counter()
+            w32 = sk.solve(pw, tol=1e-9, trace=False)
+            t_w = time.perf_counter() - t0
+            pw.set_precision(64)
+            b32 = sk.top_modes(pw, w32.f, w32.g, c.ell, method=method, degree=degree, max_power_iters=200000)
+            t_b = time.perf_counter() - t0 - t_w
+            t0 = time.perf_counter()
+            rm = sk.solve(pm, tol=1e-9, ell=c.ell, basis=b32, init=(w32.f, w32.g), trace=False)
+            t_m = time.perf_counter() - t0
+            fp32[key] = {
+                "culling": cull or None, "warm_iterations": w32.iterations, "warm_ms": t_w * 1e3,
+                "basis_ms": t_b * 1e3, "basis_method": f"{method}({degree})",
+                "basis_operator_applications": b32.sweeps, "main_iterations": rm.iterations,
+                "main_converged": rm.converged, "main_ms": t_m * 1e3,
+                "ms_end_to_end": (t_w + t_b + t_m) * 1e3,
+                "fp64_pipeline_main_iterations": ref.iterations,
+                "rel_f_vs_fp64_pipeline": float(np.max(np.abs(rm.f - ref.f)) / np.max(np.abs(ref.f))),
+                "note": f"eps'={c.basis_eps} warm SK solve in fp32, basis and main SK-NR({c.ell}) solve in fp64"}
+            del pw, pm
         del p32
 
     # ---- batched small problems: 32 C1 instances, SK to 1e-9
