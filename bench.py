@@ -167,8 +167,8 @@ def oracle_sweep_rate(O, inst, ms, threads, reps, warm=0):
     return 2.0 * inst.n * ms / t / 1e9, t, times
 
 
-def read_profile_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_lse_sum_kernel.json")
+def read_profile_traffic(name="ncu_lse_sum_kernel.json"):
+    path = os.path.join(ROOT, "profiles", name)
     if os.path.exists(path):
         try:
             return json.load(open(path)).get("dram_bytes_per_launch")
@@ -400,6 +400,7 @@ def run_ours(args, world, rank, local):
                                                         "ex2.approx)",
                              "kernel_ms": ms32_k, "achieved": g32, "peak": gex2, "unit": "G ex2/s",
                              "frac": g32 / gex2, "algorithmic_per_cell": "1 MUFU ex2 + 7 FP32 ops",
+                             "traffic": read_profile_traffic("ncu_lse_f32_kernel_r01.json"),
                              "peak_source": "measured ex2-only kernel on this GPU (sknr_bench_mufu_peak)"}}
         if "C4" in kept:
             ref = kept["C4"]
