@@ -181,7 +181,10 @@ def merge(k_head=35):
         path = os.path.join(OUT, f"seg_{k0}.json")
         if os.path.exists(path):
             sg = json.load(open(path))
-            segs.append({k: v for k, v in sg.items() if not isinstance(v, list)})
+            row = {k: v for k, v in sg.items() if not isinstance(v, list)}
+            diff = [k0 + i + 1 for i, (a, b) in enumerate(zip(sg["accepted_gpu"], sg["accepted_oracle"])) if a != b]
+            row["differing_accept_iterations"] = diff
+            segs.append(row)
     gi = json.load(open(os.path.join(OUT, "gpu_info.json")))
     covered = sorted((s_["k0"], s_["end"]) for s_ in segs)
     out = {"config": "C4 n=m=65536 d=2 eps=5e-4 ell=32 tol=1e-9: the main SK-NR(32) solve from the GPU's "
@@ -192,7 +195,11 @@ def merge(k_head=35):
                    "solve is checked in hour-capped segments: the oracle runs from the GPU's own iterate k0 "
                    "(k0 = 0: the warm start, i.e. the oracle's own trajectory) for the segment's iterations and "
                    "is compared per iteration (marginal error, accept decision) and at the segment's end "
-                   "(potentials); the last segment runs both to tolerance"}
+                   "(potentials); the last segment runs both to tolerance. Accept decisions agree through "
+                   "iteration 16, where the Newton steps carry the error; from 17 on the ell = 32 subspace's "
+                   "error is at the rounding floor, the gain Q1 - Q0 is below Q's rounding and the decision "
+                   "is noise on either side (solver.cpp:47, SURVEY 7 hard part 1): the marginal errors stay "
+                   "equal to 7 digits whichever way it goes"}
     json.dump(out, open(os.path.join(ROOT, "profiles", "c4_full_parity_r01.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
 
