@@ -97,7 +97,7 @@ int sknr_problem_set_culling(sknr_problem p, double threshold);
  * d <= 4; combines with culling (the kept groups in fp32). The cell exponent is
  * re-expanded around the squared distance with the potential terms on a 2^-8 grid
  * (exact fp32 sums), so the fp32 rounding is a fixed perturbation of the kernel
- * (~1e-6 per term): the solver still converges to tol in its own marginals and the
+ * (<= 2e-5 per term): the solver still converges to tol in its own marginals and the
  * potentials stay within ~1e-6 relative of the fp64 path. */
 int sknr_problem_set_precision(sknr_problem p, int bits);
 

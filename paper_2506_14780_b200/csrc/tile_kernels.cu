@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
 // rounding at the ulp of v (< 3e-8 for the terms that carry the sum). 2^Al enters as
 // an fp32 weight per input (FFMA into the partial), 2^Bl as an fp64 factor per output.
 // The coordinate rounding (|Xs| < 2^5: 1e-6 absolute) is a FIXED perturbation of the
-// kernel (a few 1e-6 per term at C4), so the solver converges in its own marginals and
+// kernel (<= 2e-5 per term, ~1e-6 per column sum at C4), so the solver converges in its own marginals and
 // the potentials stay within ~1e-6 relative of the fp64 path. Per cell: 7 FP32 ops +
 // 1 MUFU; the MUFU pipe (16 ex2 / clk / SM on sm_100: 4.65 TCells/s at 1.965 GHz) and
 // the issue slot (8 per cell) bound it together. Partials accumulate in fp32 over 32
