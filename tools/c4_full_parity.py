@@ -8,10 +8,13 @@ the GPU's warm potentials at eps' and the GPU's top_modes basis (the reference's
 solve then runs to tolerance on both sides: iteration counts, accept decisions and
 potentials are compared.
 
-  python tools/c4_full_parity.py gpu      # on the B200: writes gpurun_out/c4_full/inputs.npz
-  python tools/c4_full_parity.py oracle   # here (CPU, all cores): resumable, chunks of
-                                          # CHUNK iterations, progress in gpurun_out/c4_full/
-Writes profiles/c4_full_parity_r01.json when the oracle reaches tolerance.
+  python tools/c4_full_parity.py gpu            # on the B200: gpurun_out/c4_full/inputs.npz
+                                                # (copied to c4_full_inputs/ to travel back)
+  bash tools/gpurun_c4_seg.sh K0 K1             # on the box: oracle from the GPU iterate K0
+                                                # (segments 0-50, 50-85, 85-end; < 1 h each)
+  python tools/c4_full_parity.py merge          # here: profiles/c4_full_parity_r01.json
+  python tools/c4_full_parity.py oracle         # optional local cross-check of the head
+                                                # (resumable, chunks of CHUNK iterations)
 """
 import json
 import os
