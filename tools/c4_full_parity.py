@@ -28,7 +28,12 @@ import numpy as np
 
 from paper_2506_14780_b200 import generators as G
 
-OUT = os.path.join(ROOT, "gpurun_out", "c4_full")
+# SKNR_PARITY_CFG=C3 runs the same protocol on BASELINE configs[2] (C3, Chebyshev(8) basis)
+CFG = os.environ.get("SKNR_PARITY_CFG", "C4").upper()
+TAG = CFG.lower()
+OUT = os.path.join(ROOT, "gpurun_out", f"{TAG}_full")
+INPUTS = os.path.join(ROOT, f"{TAG}_full_inputs", "inputs.npz")
+BASIS = {"C4": ("chebyshev", 16)}.get(CFG, ("chebyshev", 8))
 CHUNK = 5
 
 
@@ -39,14 +44,14 @@ def rel(a, b):
 def run_gpu():
     import paper_2506_14780_b200 as sk
 
-    c = G.config("C4")
+    c = G.config(CFG)
     os.makedirs(OUT, exist_ok=True)
-    pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
+    pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps, c.cost_scale)
     t0 = time.perf_counter()
     warm = sk.solve(pw, tol=1e-9, trace=False)
     t_warm = time.perf_counter() - t0
-    b = sk.top_modes(pw, warm.f, warm.g, c.ell, method="chebyshev", degree=16, max_power_iters=200000)
-    p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+    b = sk.top_modes(pw, warm.f, warm.g, c.ell, method=BASIS[0], degree=BASIS[1], max_power_iters=200000)
+    p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale)
     t0 = time.perf_counter()
     r = sk.solve(p, tol=1e-9, ell=c.ell, basis=b, init=(warm.f, warm.g), trace=True)
     t_main = time.perf_counter() - t0
@@ -66,9 +71,9 @@ def run_gpu():
 def run_oracle():
     import oracle_ref as O
 
-    c = G.config("C4")
+    c = G.config(CFG)
     d = np.load(os.path.join(OUT, "inputs.npz"))
-    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y)
+    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
     state_path = os.path.join(OUT, "oracle_state.npz")
     if os.path.exists(state_path):
         s = np.load(state_path)
@@ -115,7 +120,7 @@ def run_oracle():
     print(json.dumps({k: v for k, v in out.items() if not isinstance(v, list)}), flush=True)
 
 
-def run_segment(k0, k1, budget_s=3000.0):
+def run_segment(k0, k1, budget_s=2700.0):
     """On the GPU box (16 host cores; one gpurun call is capped at an hour): the GPU's
     main-solve iterates after k0 and k1 iterations (the same deterministic trajectory
     as the full solve), then the oracle from iterate k0 for up to k1 - k0 iterations
@@ -126,10 +131,10 @@ def run_segment(k0, k1, budget_s=3000.0):
     import oracle_ref as O
     import paper_2506_14780_b200 as sk
 
-    c = G.config("C4")
-    d = np.load(os.path.join(ROOT, "c4_full_inputs", "inputs.npz"))
+    c = G.config(CFG)
+    d = np.load(INPUTS)
     os.makedirs(OUT, exist_ok=True)
-    p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+    p = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale)
     basis = sk.SpectralBasis(np.asfortranarray(d["V"]), np.asfortranarray(d["V"]), d["rhos"], c.basis_eps)
     init = (d["warm_f"], d["warm_g"])
     if k0 > 0:
@@ -139,7 +144,7 @@ def run_segment(k0, k1, budget_s=3000.0):
     same = [bool(t.newton_accepted) for t in r0.trace] == [bool(a) for a in d["accepted"][:k0]]
     print("gpu iterate", k0, "same accepts as the full solve:", same, flush=True)
     np.savez(os.path.join(OUT, f"gpu_iterate_{k0}.npz"), f=r0.f, g=r0.g)  # the seam with the oracle's head run
-    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y)
+    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
     f, g, done, trace, secs = r0.f, r0.g, k0, [], 0.0
     converged, last = False, 0.0
     while not converged and done < k1 and secs + 1.2 * last < budget_s:
@@ -180,7 +185,8 @@ def merge(k_head=35):
     if os.path.exists(os.path.join(OUT, "oracle_state.npz")):
         head = local_head(d, k_head)
     segs = []
-    for k0 in (0, 50, 85):
+    ks = sorted(int(n[4:-5]) for n in os.listdir(OUT) if n.startswith("seg_") and n.endswith(".json"))
+    for k0 in ks:
         path = os.path.join(OUT, f"seg_{k0}.json")
         if os.path.exists(path):
             sg = json.load(open(path))
@@ -190,20 +196,24 @@ def merge(k_head=35):
             segs.append(row)
     gi = json.load(open(os.path.join(OUT, "gpu_info.json")))
     covered = sorted((s_["k0"], s_["end"]) for s_ in segs)
-    out = {"config": "C4 n=m=65536 d=2 eps=5e-4 ell=32 tol=1e-9: the main SK-NR(32) solve from the GPU's "
-                     "eps'=1e-3 warm potentials (2112 SK iterations) and Chebyshev(16) top_modes basis, fed "
-                     "identically to the oracle (tools/c4_full_parity.py)",
+    c = G.config(CFG)
+    out = {"config": f"{CFG} n={c.n} m={c.m} d={c.x.shape[1]} eps={c.epsilon} ell={c.ell} tol=1e-9: the main "
+                     f"SK-NR({c.ell}) solve from the GPU's eps'={c.basis_eps} warm potentials ({gi['warm_iterations']} "
+                     f"SK iterations) and {BASIS[0]}({BASIS[1]}) top_modes basis, fed identically to the oracle "
+                     "(tools/c4_full_parity.py)",
            "gpu": gi, "segments_covered": covered, "oracle_segments": segs, "oracle_head_here": head,
-           "note": "the oracle needs ~55 s per C4 SK-NR iteration on the GPU box's 16 host cores, so the main "
-                   "solve is checked in hour-capped segments: the oracle runs from the GPU's own iterate k0 "
+           "note": "the oracle is too slow for one sitting at this size, so the main solve is checked in "
+                   "hour-capped segments on the GPU box's host: the oracle runs from the GPU's own iterate k0 "
                    "(k0 = 0: the warm start, i.e. the oracle's own trajectory) for the segment's iterations and "
                    "is compared per iteration (marginal error, accept decision) and at the segment's end "
-                   "(potentials); the last segment runs both to tolerance. Accept decisions agree through "
-                   "iteration 16, where the Newton steps carry the error; from 17 on the ell = 32 subspace's "
-                   "error is at the rounding floor, the gain Q1 - Q0 is below Q's rounding and the decision "
-                   "is noise on either side (solver.cpp:47, SURVEY 7 hard part 1): the marginal errors stay "
-                   "equal to 7 digits whichever way it goes"}
-    json.dump(out, open(os.path.join(ROOT, "profiles", "c4_full_parity_r01.json"), "w"), indent=1)
+                   "(potentials); the last segment runs both to tolerance"}
+    if CFG == "C4":
+        out["note"] += (". ~55 s per C4 SK-NR iteration on 16 host cores. Accept decisions agree through "
+                        "iteration 16, where the Newton steps carry the error; from 17 on the ell = 32 subspace's "
+                        "error is at the rounding floor, the gain Q1 - Q0 is below Q's rounding and the decision "
+                        "is noise on either side (solver.cpp:47, SURVEY 7 hard part 1): the marginal errors stay "
+                        "equal to 7 digits whichever way it goes")
+    json.dump(out, open(os.path.join(ROOT, "profiles", f"{TAG}_full_parity_r01.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
 
 
