@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
                 float part[JT];
 #pragma unroll
                 for (int jt = 0; jt < JT; ++jt) part[jt] = 0.0f;
-#pragma unroll 2
+#pragma unroll 8
                 for (int k = 0; k < cnt; ++k) {
                     float x[PKF];
 #pragma unroll
