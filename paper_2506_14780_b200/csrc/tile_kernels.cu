@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(NTT, 2) pts_cull_kernel(TileArgs a) {
                 for (int q = 0; q < PK / 2; ++q) dst[q] = src[q];
             }
             __syncwarp();
-#pragma unroll 1
+#pragma unroll 4
             for (int k = 0; k < cnt; ++k) {
                 double x[PK];
 #pragma unroll
