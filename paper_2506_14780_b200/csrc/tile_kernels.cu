@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NTT, MINB) pts_f32_kernel(TileArgs a) {
                 float part[JT];
 #pragma unroll
                 for (int jt = 0; jt < JT; ++jt) part[jt] = 0.0f;
-#pragma unroll 4
+#pragma unroll 8
                 for (int k = k0; k < k0 + SUB; ++k) {
                     float x[PKF];
 #pragma unroll
