@@ -9,7 +9,8 @@ solve then runs to tolerance on both sides: iteration counts, accept decisions a
 potentials are compared.
 
   python tools/c4_full_parity.py gpu            # on the B200: gpurun_out/c4_full/inputs.npz
-                                                # (copied to c4_full_inputs/ to travel back)
+                                                # (copied to c4_full_inputs/ to travel back;
+                                                # drop it from .gpurunignore for segment calls)
   bash tools/gpurun_c4_seg.sh K0 K1             # on the box: oracle from the GPU iterate K0
                                                 # (segments 0-50, 50-85, 85-end; < 1 h each)
   python tools/c4_full_parity.py merge          # here: profiles/c4_full_parity_r01.json
