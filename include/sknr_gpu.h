@@ -172,7 +172,16 @@ typedef struct {
     int32_t exact_marginals; /* 0: column marginal from the fused transform
                                 (beta_j expm1((g_j-h_j)/eps)); 1: explicit
                                 plan-sum passes as core.cpp:120-143 */
-    int32_t reserved;
+    int32_t accept_test;   /* Newton accept test of try_newton (solver.cpp:46-47).
+                              0 (default, the reference): Q(f') > Q(f) with both values
+                              evaluated in full -- once the step's gain falls below
+                              ulp(Q) the decision is rounding noise on any platform.
+                              1 (stable): the same predicate as dQ = Q(f') - Q(f) > 0,
+                              dQ = a.d + b.(h' - h), d = f' - f, h'_j - h_j =
+                              -eps log1p(sum_i P~_ij expm1(d_i/eps) / sum_i P~_ij) at the
+                              anchor h = f^{C,eps}: rounding scales with the step, so
+                              decisions are reproducible (steps with max|d| > 600 eps
+                              use the literal test). */
 } sknr_config;
 
 void sknr_config_default(sknr_config* c);
@@ -194,6 +203,11 @@ int sknr_solve(sknr_problem p, const sknr_config* cfg, const double* basis, int6
                const double* init_f, const double* init_g, double* f_out, double* g_out,
                int64_t* iterations, int* converged, sknr_record* trace, int64_t trace_cap,
                int64_t* trace_len);
+
+/* The full trace of the last sknr_solve / sknr_anneal on this handle (concatenated over
+ * anneal stages): lets a caller size its record array from the trace_len the solve
+ * returned instead of from max_iter (the reference push_back()s the iterations run). */
+int sknr_last_trace(sknr_problem p, sknr_record* trace, int64_t cap, int64_t* len);
 
 /* Batched solve (not in the reference): `count` independent
  * problems (any sizes / cost kinds, distinct unsharded handles) solved with the
@@ -226,6 +240,9 @@ int sknr_solve_small_batch(int64_t count, int64_t d, const int64_t* n, const int
  * from f with basis vectors (n x ell). f_out = accepted ? f + V delta : f. */
 int sknr_newton_step(sknr_problem p, const double* f, const double* vectors, int64_t ell, double* f_out,
                      int* accepted, int* factorization_failed);
+/* Same with the accept test selected as in sknr_config.accept_test (0 literal, 1 stable). */
+int sknr_newton_step_ex(sknr_problem p, const double* f, const double* vectors, int64_t ell, int accept_test,
+                        double* f_out, int* accepted, int* factorization_failed);
 
 /* anneal (solver.cpp:158-222). warm_mode 0 none, 1 potentials, 2 spectral.
  * Per stage s: f_out[s*n ..], g_out[s*m ..], iterations[s], converged[s];

@@ -731,7 +731,11 @@ TopModesResult top_modes(const Problem& p, const Vec& f, const Vec& g, Index ell
 struct Record {
     double marginal_error, marginal_error_inf, semi_dual_value;
     int newton_attempted, newton_accepted;
+    double newton_gain, newton_step_max;  // diagnostics: Q(f') - Q(f) as tested, max_i |f'_i - f_i|
 };
+
+// diagnostics of the last try_newton (copied into the trace record)
+static thread_local double g_last_gain = 0.0, g_last_step_max = 0.0;
 
 struct SolveOut {
     Vec f, g;
@@ -787,6 +791,44 @@ double semi_dual_hessian_quadform(const Problem& p, const Vec& f, const Vec& u) 
     return -acc * inv_eps;
 }
 
+// Accept test of try_newton. 0 (literal, the reference): Q(f') > Q(f) with both
+// values evaluated in full (solver.cpp:46-47, objective.cpp:42-45). 1 (stable): the
+// same predicate as Q(f') - Q(f) > 0, with the difference evaluated directly so its
+// rounding scales with the step, not with |Q|:
+//   d = f' - f,  P~_ij = a_i exp((f_i + h_j - C_ij)/eps)   (h = f^{C,eps}, the anchor)
+//   h'_j - h_j = -eps log1p(t_j / s_j),  s_j = sum_i P~_ij,  t_j = sum_i P~_ij expm1(d_i/eps)
+//   dQ = a.d + b.(h' - h)
+// (exact algebra: sum_i a_i e^{(f'_i - C_ij)/eps} = e^{-h_j/eps} (s_j + t_j)). Steps with
+// max|d|/eps > kStableSpan fall back to the literal test (expm1 would overflow; such
+// steps are never rounding-decided).
+static int g_accept_mode = 0;
+constexpr double kStableSpan = 600.0;
+
+static bool stable_delta_q(const Problem& p, const Vec& f, const Vec& h, const Vec& cand, double& dq) {
+    const Index n = p.n, m = p.m;
+    const double inv_eps = 1.0 / p.eps;
+    Vec dv(n), ev(n);
+    double dmax = 0.0;
+    for (Index i = 0; i < n; ++i) {
+        dv[i] = cand[i] - f[i];
+        dmax = std::max(dmax, std::abs(dv[i]));
+        ev[i] = std::expm1(dv[i] * inv_eps);
+    }
+    if (!(dmax * inv_eps <= kStableSpan)) return false;
+    Vec dh(m);
+    par_for(m, [&](Index j) {
+        double s = 0.0, t = 0.0;
+        for (Index i = 0; i < n; ++i) {
+            const double w = p.a[i] * std::exp((f[i] + h[j] - p.C(i, j)) * inv_eps);
+            s += w;
+            t += w * ev[i];
+        }
+        dh[j] = -p.eps * std::log1p(t / s);
+    });
+    dq = dot(p.a, dv) + dot(p.b, dh);
+    return true;
+}
+
 // try_newton (solver.cpp:30-56)
 static bool try_newton(const Problem& p, Vec& f, const Vec& h, double value_at_f,
                        const double* V, Index ell, double& value_out, Vec* g_cand) {
@@ -805,7 +847,21 @@ static bool try_newton(const Problem& p, Vec& f, const Vec& h, double value_at_f
         for (Index c = 0; c < ell; ++c) s += V[i + c * p.n] * delta[c];
         cand[i] = f[i] + s;
     }
+    double dq = 0.0;
+    g_last_step_max = 0.0;
+    for (Index i = 0; i < p.n; ++i) g_last_step_max = std::max(g_last_step_max, std::abs(cand[i] - f[i]));
+    if (g_accept_mode == 1 && !g_cand && stable_delta_q(p, f, h, cand, dq)) {
+        g_last_gain = dq;
+        if (dq > 0.0) {
+            f = std::move(cand);
+            value_out = value_at_f + dq;
+            return true;
+        }
+        value_out = value_at_f;
+        return false;
+    }
     const double cv = semi_dual_value(p, cand, g_cand);
+    g_last_gain = cv - value_at_f;
     if (cv > value_at_f) {
         f = std::move(cand);
         value_out = cv;
@@ -855,7 +911,10 @@ SolveOut solve(const Problem& p, double tol, long max_iter, Index ell, const dou
             const double value_sweep = dot(p.a, out.f) + dot(p.b, h);
             rec.newton_attempted = 1;
             double value;
+            g_last_gain = g_last_step_max = 0.0;
             rec.newton_accepted = try_newton(p, out.f, h, value_sweep, V, ell, value, nullptr);
+            rec.newton_gain = g_last_gain;
+            rec.newton_step_max = g_last_step_max;
             rec.semi_dual_value = value;
         } else if (trace_enabled) {
             rec.semi_dual_value = semi_dual_value(p, out.f);
@@ -894,6 +953,9 @@ const char* oracle_last_error(void) { return g_err.c_str(); }
 void oracle_set_threads(int t) {
     g_threads = t > 0 ? t : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
 }
+
+/* Accept test of try_newton: 0 literal Q(f') > Q(f) (the reference), 1 stable dQ > 0. */
+void oracle_set_accept_mode(int mode) { g_accept_mode = mode == 1 ? 1 : 0; }
 
 int oracle_max_threads(void) {
     return static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
@@ -1109,6 +1171,8 @@ typedef struct {
     double semi_dual_value;
     int newton_attempted;
     int newton_accepted;
+    double newton_gain;     /* Q(f') - Q(f) as the accept test evaluated it (0 if no candidate) */
+    double newton_step_max; /* max_i |f'_i - f_i| of the candidate */
 } oracle_record;
 
 int oracle_solve(const oracle_problem* q, double tol, long max_iter, long ell, const double* V,
@@ -1130,6 +1194,8 @@ int oracle_solve(const oracle_problem* q, double tol, long max_iter, long ell, c
             trace[t].semi_dual_value = o.trace[t].semi_dual_value;
             trace[t].newton_attempted = o.trace[t].newton_attempted;
             trace[t].newton_accepted = o.trace[t].newton_accepted;
+            trace[t].newton_gain = o.trace[t].newton_gain;
+            trace[t].newton_step_max = o.trace[t].newton_step_max;
         }
     })
 }

@@ -48,7 +48,7 @@ class _Config(ctypes.Structure):
         ("newton_enabled", ctypes.c_int32),
         ("trace_enabled", ctypes.c_int32),
         ("exact_marginals", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("accept_test", ctypes.c_int32),
     ]
 
 
@@ -102,6 +102,9 @@ _SIGS = {
     "sknr_dual_value": [_P, _D, _D, _D],
     "sknr_semi_dual_hessian_quadform": [_P, _D, _D, _D],
     "sknr_newton_step": [_P, _D, _D, _I64, _D, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
+    "sknr_newton_step_ex": [_P, _D, _D, _I64, ctypes.c_int, _D, ctypes.POINTER(ctypes.c_int),
+                            ctypes.POINTER(ctypes.c_int)],
+    "sknr_last_trace": [_P, ctypes.POINTER(_Record), _I64, ctypes.POINTER(_I64)],
     "sknr_spectrum_report": [_P, _D, _D, _I64, ctypes.c_int, ctypes.c_double, _I64, _D, _D, _D, _D, _D],
     "sknr_projector_distance": [_I64, _I64, _D, _D, _D],
     "sknr_semi_dual_value": [_P, _D, _D],
@@ -691,8 +694,8 @@ def sk_sweep(problem: Problem, f, g=None):
     return ctransform_of_g(problem, g1), g1
 
 
-def newton_step(problem: Problem, f, basis: SpectralBasis) -> NewtonOutcome:
-    """One restricted Newton step from f (solver.cpp:59-69)."""
+def newton_step(problem: Problem, f, basis: SpectralBasis, accept: str = "literal") -> NewtonOutcome:
+    """One restricted Newton step from f (solver.cpp:59-69); `accept` as in solve()."""
     if basis.ell < 1:
         raise ValueError("newton_step: empty basis")
     f = _checked(f, problem.n, "ctransform_of_f")
@@ -701,12 +704,34 @@ def newton_step(problem: Problem, f, basis: SpectralBasis) -> NewtonOutcome:
         raise ValueError("restricted_derivatives: basis dimension mismatch")
     fo = np.empty(problem.n)
     acc, fail = ctypes.c_int(), ctypes.c_int()
-    _check(lib().sknr_newton_step(problem.handle, _ptr(f), _ptr(V), V.shape[1], _ptr(fo), ctypes.byref(acc),
-                                  ctypes.byref(fail)))
+    _check(lib().sknr_newton_step_ex(problem.handle, _ptr(f), _ptr(V), V.shape[1], _accept_code(accept),
+                                     _ptr(fo), ctypes.byref(acc), ctypes.byref(fail)))
     return NewtonOutcome(fo, bool(acc.value), bool(fail.value))
 
 
-def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False) -> _Config:
+_ACCEPT = {"literal": 0, "stable": 1}
+
+
+def _accept_code(accept) -> int:
+    if accept not in _ACCEPT:
+        raise ValueError("accept must be 'literal' or 'stable'")
+    return _ACCEPT[accept]
+
+
+# records preallocated per solve; longer traces are fetched whole afterwards (sknr_last_trace)
+_TRACE_PREALLOC = 4096
+
+
+def _full_trace(problem, recs, cap, total):
+    if total <= cap:
+        return _records(recs, total)
+    buf = (_Record * total)()
+    got = _I64()
+    _check(lib().sknr_last_trace(problem.handle, buf, total, ctypes.byref(got)))
+    return _records(buf, min(total, got.value))
+
+
+def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False, accept="literal") -> _Config:
     c = _Config()
     lib().sknr_config_default(ctypes.byref(c))
     c.tol_omega = float(tol)
@@ -715,16 +740,23 @@ def _config(tol, max_iter, ell, trace, newton=True, exact_marginals=False) -> _C
     c.trace_enabled = 1 if trace else 0
     c.newton_enabled = 1 if newton else 0
     c.exact_marginals = 1 if exact_marginals else 0
+    c.accept_test = _accept_code(accept)
     return c
 
 
 def solve(problem: Problem, tol: float = 1e-9, max_iter: int = 100000, ell: int = 0,
           basis: Optional[SpectralBasis] = None, init=None, trace: bool = True,
-          exact_marginals: bool = False) -> SolveResult:
+          exact_marginals: bool = False, accept: str = "literal") -> SolveResult:
     """SK-NR(ell) (Alg. 1; solver.cpp:71-156). exact_marginals=True evaluates the
     stopping test from explicit plan row/column sums (core.cpp:120-143) instead
-    of the fused transform (2 extra passes per iteration)."""
-    cfg = _config(tol, max_iter, ell, trace, exact_marginals=exact_marginals)
+    of the fused transform (2 extra passes per iteration).
+
+    accept: the Newton accept test (solver.cpp:46-47). "literal" (the reference)
+    compares Q(f') > Q(f) evaluated in full; once the gain of a step falls below
+    ulp(Q) that comparison is rounding noise on any platform. "stable" evaluates the
+    same predicate as dQ = a.(f'-f) + b.(h'-h) > 0 with h'-h = -eps log1p(...) from an
+    anchor pass, whose rounding scales with the step (sknr_config.accept_test)."""
+    cfg = _config(tol, max_iter, ell, trace, exact_marginals=exact_marginals, accept=accept)
     V = None
     bell = 0
     if ell > 0:
@@ -745,26 +777,26 @@ def solve(problem: Problem, tol: float = 1e-9, max_iter: int = 100000, ell: int 
     g = np.empty(problem.m)
     iters = _I64()
     conv = ctypes.c_int()
-    cap = int(max_iter) if trace else 0
+    cap = min(int(max_iter), _TRACE_PREALLOC) if trace else 0
     recs = (_Record * max(cap, 1))()
     tlen = _I64()
     _check(lib().sknr_solve(problem.handle, ctypes.byref(cfg), _ptr(V), bell, _ptr(f0), _ptr(g0),
                             _ptr(f), _ptr(g), ctypes.byref(iters), ctypes.byref(conv), recs, cap,
                             ctypes.byref(tlen)))
-    return SolveResult(f, g, bool(conv.value), int(iters.value), _records(recs, min(tlen.value, cap)),
-                       problem)
+    tr = _full_trace(problem, recs, cap, int(tlen.value)) if trace else []
+    return SolveResult(f, g, bool(conv.value), int(iters.value), tr, problem, problem.epsilon)
 
 
 def solve_batch(problems: Sequence[Problem], tol: float = 1e-9, max_iter: int = 100000, ell: int = 0,
                 bases: Optional[Sequence[SpectralBasis]] = None, inits=None,
-                exact_marginals: bool = False) -> list:
+                exact_marginals: bool = False, accept: str = "literal") -> list:
     """Solve independent problems together (one CUDA graph per iteration, one
     concurrent branch per problem; not in the reference API). Each result equals
     solve(problems[b], ...) bit for bit; traces are not recorded."""
     B = len(problems)
     if B < 1:
         raise ValueError("solve_batch: empty batch")
-    cfg = _config(tol, max_iter, ell, False, exact_marginals=exact_marginals)
+    cfg = _config(tol, max_iter, ell, False, exact_marginals=exact_marginals, accept=accept)
     handles = (_P * B)(*[p.handle for p in problems])
     keep = []
 
@@ -805,7 +837,8 @@ def solve_batch(problems: Sequence[Problem], tol: float = 1e-9, max_iter: int = 
     conv = (ctypes.c_int * B)()
     _check(lib().sknr_solve_batch(handles, B, ctypes.byref(cfg), bptr, int(ell), fptr, gptr, arr(fo), arr(go),
                                   iters, conv))
-    return [SolveResult(fo[b], go[b], bool(conv[b]), int(iters[b]), [], problems[b]) for b in range(B)]
+    return [SolveResult(fo[b], go[b], bool(conv[b]), int(iters[b]), [], problems[b], problems[b].epsilon)
+            for b in range(B)]
 
 
 def solve_small_batch(problems, tol: float = 1e-9, max_iter: int = 100000) -> list:
@@ -864,8 +897,9 @@ def solve_small_batch(problems, tol: float = 1e-9, max_iter: int = 100000) -> li
 
 
 def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", ell: int = 8,
-           refresh_basis: bool = False, tol: float = 1e-9, max_iter: int = 100000) -> list:
-    """Epsilon-annealing driver (solver.cpp:158-222)."""
+           refresh_basis: bool = False, tol: float = 1e-9, max_iter: int = 100000,
+           accept: str = "literal") -> list:
+    """Epsilon-annealing driver (solver.cpp:158-222); `accept` as in solve()."""
     modes = {"none": 0, "potentials": 1, "spectral": 2}
     if warm not in modes:
         raise ValueError("warm must be none|potentials|spectral")
@@ -873,20 +907,24 @@ def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", 
     S = eps.size
     if S == 0:
         raise ValueError("anneal: empty schedule")
-    cfg = _config(tol, max_iter, ell, True)
+    cfg = _config(tol, max_iter, ell, True, accept=accept)
     n, m = problem.n, problem.m
     F = np.empty(S * n)
     G = np.empty(S * m)
     iters = (_I64 * S)()
     conv = (ctypes.c_int * S)()
-    cap = int(max_iter) * S
-    cap = min(cap, 2_000_000)
+    cap = min(int(max_iter), _TRACE_PREALLOC) * S
     recs = (_Record * max(cap, 1))()
     offs = (_I64 * S)()
     tlen = _I64()
     _check(lib().sknr_anneal(problem.handle, _ptr(eps), S, modes[warm], 1 if refresh_basis else 0,
                              ctypes.byref(cfg), _ptr(F), _ptr(G), iters, conv, recs, cap, offs,
                              ctypes.byref(tlen)))
+    if tlen.value > cap:
+        cap = int(tlen.value)
+        recs = (_Record * cap)()
+        got = _I64()
+        _check(lib().sknr_last_trace(problem.handle, recs, cap, ctypes.byref(got)))
     out = []
     for s in range(S):
         lo = offs[s]
@@ -906,10 +944,10 @@ def bench_pass(problem: Problem, which: int, ell: int = 0, passes: int = 5):
 
 
 def bench_iterations(problem: Problem, ell: int = 0, basis: Optional[SpectralBasis] = None,
-                     iters: int = 5, warmup: int = 1, flush_l2: bool = True):
+                     iters: int = 5, warmup: int = 1, flush_l2: bool = True, accept: str = "literal"):
     """Device ms per SK-NR(ell) iteration (CUDA events per iteration, L2 flushed
     between iterations) and the number of kernels in one iteration."""
-    cfg = _config(1e-9, 1 << 40, ell, False)
+    cfg = _config(1e-9, 1 << 40, ell, False, accept=accept)
     V = _mat_f(basis.vectors) if (basis is not None and ell > 0) else None
     ms = ctypes.c_double()
     kpi = _I64()

@@ -411,6 +411,18 @@ __device__ void run_epilogue(DevState* st, int epilogue, int newton, const doubl
         if (st->done || !st->newton_ok) return;
         st->q1 = r[0] + r[1];
         st->accept = st->q1 > st->q0 ? 1 : 0;
+    } else if (epilogue == EPI_STEP) {
+        // stable accept test, first half: r = (a.d, max|d|), d = f' - f
+        if (st->done || !st->newton_ok) return;
+        st->adq = r[0];
+        st->lit = r[1] <= st->lit_dmax ? 0 : 1;
+    } else if (epilogue == EPI_ACCEPT_DQ) {
+        // dQ = a.d + b.(h' - h) > 0: the predicate Q1 > Q0 of solver.cpp:46-47 evaluated
+        // as a difference whose rounding scales with the step, not with |Q|
+        if (st->done || !st->newton_ok || st->lit) return;
+        const double dq = st->adq + r[0];
+        st->q1 = st->q0 + dq;
+        st->accept = dq > 0.0 ? 1 : 0;
     }
 }
 

@@ -129,7 +129,7 @@ int gram_blocks(int64_t T);
 // sum x*x, or max |x|. Results land in out[t]; the last block merges block
 // partials in block order, then runs an optional epilogue on DevState.
 enum { RED_DOT = 0, RED_SQ = 1, RED_MAXABS = 2 };
-enum { EPI_NONE = 0, EPI_GAUGE = 1, EPI_CHECK = 2, EPI_ACCEPT = 3 };
+enum { EPI_NONE = 0, EPI_GAUGE = 1, EPI_CHECK = 2, EPI_ACCEPT = 3, EPI_STEP = 4, EPI_ACCEPT_DQ = 5 };
 constexpr int RED_MAX_TERMS = 6;
 constexpr int RED_PER_BLOCK = AUX_NT * 2;  // elements per k_reduce block (up to 296 blocks)
 struct RedArgs {

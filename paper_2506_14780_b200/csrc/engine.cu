@@ -313,6 +313,7 @@ struct Problem {
     int64_t n_global = 0, row_begin = 0;
     DBuf red_tmp, gather_buf;
     std::vector<double> h_alpha, h_beta;  // full host copies (validation, host-side dots)
+    std::vector<sknr_record> last_trace;  // trace of the last solve / anneal (sknr_last_trace)
 
     bool otf() const { return dim != 0; }  // on-the-fly cost (dim > 0: registers, dim < 0: DMMA contraction)
     double inv_eps() const { return 1.0 / eps; }

@@ -86,7 +86,7 @@ void sknr_config_default(sknr_config* c) {
     c->newton_enabled = 1;
     c->trace_enabled = 1;
     c->exact_marginals = 0;
-    c->reserved = 0;
+    c->accept_test = 0;
 }
 
 int sknr_problem_create_dense(const double* cost, int64_t n, int64_t m, const double* alpha,
@@ -733,14 +733,18 @@ static bool host_llt_solve(std::vector<double> A, int l, const double* b, double
 }
 
 // ---- newton_step (solver.cpp:59-69 with try_newton :30-56): g = f^{C,eps}, Q0 = a.f + b.g,
-// restricted derivatives, LLT(-H) (reject on failure), delta, f' = f + V delta, accept iff Q(f') > Q0.
-int sknr_newton_step(sknr_problem h, const double* f, const double* vectors, int64_t ell, double* f_out,
-                     int* accepted, int* factorization_failed) {
+// restricted derivatives, LLT(-H) (reject on failure), delta, f' = f + V delta, accept iff Q(f') > Q0
+// (accept_test 0) or dQ > 0 (accept_test 1, see sknr_config): s = R^T(1), t = R^T(expm1(d/eps))
+// at the anchor (f, g), h' - h = -eps log1p(t/s).
+int sknr_newton_step_ex(sknr_problem h, const double* f, const double* vectors, int64_t ell, int accept_test,
+                        double* f_out, int* accepted, int* factorization_failed) {
     SKNR_API_BEGIN
     Problem& P = get(h);
     if (ell < 1) throw InvalidArgument("newton_step: empty basis");
     if (!vectors || !f_out || !accepted || !factorization_failed)
         throw InvalidArgument("newton_step: null pointer");
+    if (accept_test != 0 && accept_test != 1)
+        throw InvalidArgument("newton_step: accept_test must be 0 (literal) or 1 (stable)");
     const int64_t n = P.n_global, m = P.m;
     const int l = static_cast<int>(ell);
     std::vector<double> g(m), grad(l), hess(static_cast<size_t>(l) * l);
@@ -767,14 +771,41 @@ int sknr_newton_step(sknr_problem h, const double* f, const double* vectors, int
         for (int c = 0; c < l; ++c) s += vectors[i + c * n] * delta[c];
         cand[i] = f[i] + s;
     }
-    double q1 = 0.0;
-    rc = sknr_semi_dual_value(h, cand.data(), &q1);
-    if (rc != SKNR_OK) return rc;
-    if (q1 > value) {
+    const double inv_eps = 1.0 / P.eps;
+    double dmax = 0.0;
+    std::vector<double> dv(n), ev(n);
+    for (int64_t i = 0; i < n; ++i) {
+        dv[i] = cand[i] - f[i];
+        dmax = std::max(dmax, std::abs(dv[i]));
+        ev[i] = std::expm1(dv[i] * inv_eps);
+    }
+    bool acc = false;
+    if (accept_test == 1 && dmax * inv_eps <= kStableSpan) {
+        std::vector<double> ones(n, 1.0), sv(m), tv(m);
+        rc = sknr_apply_Rt(h, f, g.data(), ones.data(), sv.data());
+        if (rc != SKNR_OK) return rc;
+        rc = sknr_apply_Rt(h, f, g.data(), ev.data(), tv.data());
+        if (rc != SKNR_OK) return rc;
+        double dq = 0.0, bdh = 0.0;
+        for (int64_t i = 0; i < n; ++i) dq += P.h_alpha[i] * dv[i];
+        for (int64_t j = 0; j < m; ++j) bdh += P.h_beta[j] * (-P.eps * std::log1p(tv[j] / sv[j]));
+        acc = dq + bdh > 0.0;
+    } else {
+        double q1 = 0.0;
+        rc = sknr_semi_dual_value(h, cand.data(), &q1);
+        if (rc != SKNR_OK) return rc;
+        acc = q1 > value;
+    }
+    if (acc) {
         std::memcpy(f_out, cand.data(), sizeof(double) * n);
         *accepted = 1;
     }
     SKNR_API_END
+}
+
+int sknr_newton_step(sknr_problem h, const double* f, const double* vectors, int64_t ell, double* f_out,
+                     int* accepted, int* factorization_failed) {
+    return sknr_newton_step_ex(h, f, vectors, ell, 0, f_out, accepted, factorization_failed);
 }
 
 // ---- projector_distance (spectral.cpp:230-242): ||(I - A A^T) B||_2 for n x k column blocks,
@@ -880,6 +911,8 @@ static void validate_config(const sknr_config* cfg, const double* basis, int64_t
         if (basis == nullptr) throw InvalidArgument("solve: ell > 0 requires a basis");
         if (basis_ell != cfg->ell) throw InvalidArgument("solve: basis has wrong column count");
     }
+    if (cfg->accept_test != 0 && cfg->accept_test != 1)
+        throw InvalidArgument("solve: accept_test must be 0 (literal) or 1 (stable)");
     (void)n;
 }
 
@@ -897,7 +930,7 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     const int64_t ell = use_newton ? cfg->ell : 0;
     SolveOut o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, basis, init_f, cfg->trace_enabled != 0,
                            std::max<int64_t>(trace_cap, cfg->trace_enabled ? cfg->max_iter : 1),
-                           cfg->exact_marginals != 0);
+                           cfg->exact_marginals != 0, cfg->accept_test);
     std::memcpy(f_out, o.f.data(), sizeof(double) * P.n_global);
     std::memcpy(g_out, o.g.data(), sizeof(double) * P.m);
     if (iterations) *iterations = o.iterations;
@@ -906,6 +939,7 @@ int sknr_solve(sknr_problem h, const sknr_config* cfg, const double* basis, int6
     if (trace_len) *trace_len = len;
     if (trace)
         for (int64_t t = 0; t < len && t < trace_cap; ++t) trace[t] = o.trace[t];
+    P.last_trace = std::move(o.trace);
     SKNR_API_END
 }
 
@@ -934,7 +968,7 @@ int sknr_solve_batch(const sknr_problem* problems, int64_t count, const sknr_con
     }
     const bool use_newton = cfg->newton_enabled && cfg->ell > 0;
     std::vector<SolveOut> o = run_solve_batch(items, cfg->tol_omega, cfg->max_iter, use_newton ? cfg->ell : 0,
-                                              cfg->exact_marginals != 0);
+                                              cfg->exact_marginals != 0, cfg->accept_test);
     for (int64_t b = 0; b < count; ++b) {
         std::memcpy(f_out[b], o[b].f.data(), sizeof(double) * items[b].P->n_global);
         std::memcpy(g_out[b], o[b].g.data(), sizeof(double) * items[b].P->m);
@@ -1048,6 +1082,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
     const double eps0 = P.eps;
     const int64_t n = P.n_global, m = P.m;
     int64_t tl = 0;
+    P.last_trace.clear();
     Basis basis;
     bool have_basis = false;
     std::vector<double> prev_f, prev_g;
@@ -1083,7 +1118,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
             SolveOut o;
             try {
                 o = run_solve(P, cfg->tol_omega, cfg->max_iter, ell, bptr, init, cfg->trace_enabled != 0,
-                              cfg->max_iter, cfg->exact_marginals != 0);
+                              cfg->max_iter, cfg->exact_marginals != 0, cfg->accept_test);
             } catch (const InvalidArgument& e) {
                 throw RuntimeFailure("anneal stage " + std::to_string(s) + ": " + e.what());
             }
@@ -1094,6 +1129,7 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
             trace_offsets[s] = tl;
             for (size_t t = 0; t < o.trace.size(); ++t, ++tl)
                 if (trace && tl < trace_cap) trace[tl] = o.trace[t];
+            P.last_trace.insert(P.last_trace.end(), o.trace.begin(), o.trace.end());
             prev_f = std::move(o.f);
             prev_g = std::move(o.g);
         }
@@ -1104,6 +1140,17 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
     if (trace_len) *trace_len = tl;
     set_eps(eps0);
     CK(cudaStreamSynchronize(P.stream));
+    SKNR_API_END
+}
+
+int sknr_last_trace(sknr_problem h, sknr_record* trace, int64_t cap, int64_t* len) {
+    SKNR_API_BEGIN
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    const int64_t L = static_cast<int64_t>(P.last_trace.size());
+    if (len) *len = L;
+    if (trace)
+        for (int64_t t = 0; t < L && t < cap; ++t) trace[t] = P.last_trace[t];
     SKNR_API_END
 }
 
@@ -1205,7 +1252,7 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
     const int64_t ell = use_newton ? cfg->ell : 0;
     if (P.emu) throw InvalidArgument("sknr_bench_iterations: not available on emulated shards");
     SolveState S;
-    prepare_solve(P, S, ell, basis, nullptr, warmup + iters + 1000000, 1e-300, 1);
+    prepare_solve(P, S, ell, basis, nullptr, warmup + iters + 1000000, 1e-300, 1, cfg->accept_test);
     cudaStream_t s = P.stream;
     DBuf flush;
     if (flush_l2) flush.ensure((256ull << 20) / sizeof(double));  // 256 MiB > 126 MB L2
@@ -1213,7 +1260,7 @@ int sknr_bench_iterations(sknr_problem h, const sknr_config* cfg, const double* 
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     const int64_t l0 = launch_count();
-    enqueue_iteration(P, S, ell, false, 1);
+    enqueue_iteration(P, S, ell, false, 1, false, 0, cfg->accept_test);
     if (kernels_per_iter) *kernels_per_iter = launch_count() - l0;
     CK(cudaStreamEndCapture(s, &graph));
     make_programmatic(graph);

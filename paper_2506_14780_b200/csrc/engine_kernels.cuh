@@ -19,9 +19,12 @@ __global__ void k_copy(double* dst, const double* src, int64_t n, DevState* st, 
         dst[i] = src[i];
 }
 
-__global__ void k_state_init(DevState* st, long long max_iter, double tol) {
+__global__ void k_state_init(DevState* st, long long max_iter, double tol, double lit_dmax = 0.0) {
     SKNR_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    st->lit = 0;
+    st->lit_dmax = lit_dmax;
+    st->trace_base = 0;
     st->done = 0;
     st->iter_active = 0;
     st->conv = 0;
@@ -187,6 +190,44 @@ __global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, co
     }
 }
 
+// Stable accept test, per row: candidate f' = f + V delta, d = f' - f (exact: f' and f
+// are close), and the block-pass weights W[i] = (1, expm1(d_i/eps), 0, ...) of the
+// anchor pass s_j = sum_i P~_ij, t_j = sum_i P~_ij expm1(d_i/eps).
+__global__ void k_fcand_step(const double* f, const double* V, int64_t n, int ell, const double* delta,
+                             double inv_eps, double* out, double* dvec, double* W, int kt, DevState* st,
+                             unsigned guard) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(st, guard)) return;
+    __shared__ double sd[64];
+    if (threadIdx.x < ell) sd[threadIdx.x] = delta[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < ell; ++c) s += V[i + c * n] * sd[c];
+        const double fc = f[i] + s;
+        const double d = fc - f[i];
+        out[i] = fc;
+        dvec[i] = d;
+        W[i * kt] = 1.0;
+        W[i * kt + 1] = expm1(fmin(d * inv_eps, 700.0));
+    }
+}
+
+// h'_j - h_j = -eps log1p(t_j / s_j) from the anchor pass (ST = [s | t], m x 2), and
+// the candidate's transform h' = h + (h' - h) (the next sweep's g if accepted).
+__global__ void k_dh(const double* ST, const double* h, int64_t m, double eps, double* dh, double* hcand,
+                     DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(st, guard)) return;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = -eps * log1p(ST[m + j] / ST[j]);
+        dh[j] = v;
+        hcand[j] = h[j] + v;
+    }
+}
+
 // accepted: f <- candidate, next g <- h(candidate); otherwise next g <- h.
 __global__ void k_select(double* f, const double* fcand, int64_t n, double* gnext, const double* h,
                          const double* hcand, int64_t m, DevState* st) {
@@ -204,7 +245,9 @@ __global__ void k_select(double* f, const double* fcand, int64_t n, double* gnex
 }
 
 // End of an iteration: trace record, max_iter stop and -- when the solve runs as a
-// device-side WHILE loop (conditional graph node) -- the loop condition.
+// device-side WHILE loop (conditional graph node) -- the loop condition. The device
+// trace holds `cap` records starting at iteration trace_base + 1; when it is full the
+// loop pauses (condition 0 without `done`) so the host can drain it and relaunch.
 __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int trace_enabled,
                          cudaGraphConditionalHandle loop) {
     SKNR_PDL_ENTRY();
@@ -215,7 +258,8 @@ __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int tr
     }
     st->iter_active = 0;
     const long long k = st->iter;
-    if (trace_enabled && k - 1 < cap) {
+    const long long slot = k - 1 - st->trace_base;
+    if (trace_enabled && slot >= 0 && slot < cap) {
         sknr_record r;
         r.index = k;
         r.marginal_error = st->gap_l2;
@@ -225,10 +269,15 @@ __global__ void k_record(DevState* st, sknr_record* trace, long long cap, int tr
         r.newton_attempted = st->attempted;
         r.newton_accepted = acc ? 1 : 0;
         r.wall_time_ms = static_cast<double>(globaltimer_ns() - st->t_iter0) * 1e-6;
-        trace[k - 1] = r;
+        trace[slot] = r;
     }
     if (k >= st->max_iter) st->done = 1;
-    if (loop) cudaGraphSetConditional(loop, st->done ? 0 : 1);
+    const bool full = trace_enabled && slot + 1 >= cap;
+    if (loop) cudaGraphSetConditional(loop, (st->done || full) ? 0 : 1);
+}
+
+__global__ void k_trace_rebase(DevState* st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) st->trace_base = st->iter;
 }
 
 __global__ void k_axpby(const double* x, const double* y, int64_t n, double a, double b, double* out) {

@@ -6,6 +6,7 @@
 // ============================================================ solve
 struct SolveState {
     DBuf f, g, gnext, h, fcand, hcand, rowres, colres, am, r, Lr, V, Wv, S, delta, G;
+    DBuf dvec, Wst, ST, dh;  // stable accept test: d = f' - f, anchor-pass weights/sums, h' - h
     DBuf trace_raw;  // sknr_record array (as doubles)
 };
 
@@ -16,10 +17,14 @@ struct SolveOut {
     std::vector<sknr_record> trace;
 };
 
+// Largest max_i |f'_i - f_i| / eps the stable accept test evaluates (expm1 stays finite).
+constexpr double kStableSpan = 600.0;
+
 // Enqueue one SK-NR(ell) iteration (solver.cpp:104-151).
+// accept: 0 literal Q1 > Q0 (the reference), 1 stable dQ > 0 (ACCEPT_STABLE below).
 static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace_enabled,
                               int64_t trace_cap, bool exact_marginals = false,
-                              cudaGraphConditionalHandle loop = 0) {
+                              cudaGraphConditionalHandle loop = 0, int accept = 0) {
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     const bool newton = ell > 0;
@@ -162,9 +167,77 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         count_launch();
         k_newton_solve<<<1, 256, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
                                                             P.st, gn);
-        count_launch();
-        k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
-        lse(P, 0, S.fcand.p, S.hcand.p, gn);
+        // accept test. Literal (solver.cpp:45-47): Q1 = a.f' + b.f'^{C,eps} from a full
+        // column LSE of the candidate, accept iff Q1 > Q0. Stable (accept = 1): the same
+        // predicate as dQ = Q1 - Q0 > 0 evaluated directly -- one anchor pass at (f, h)
+        // gives s_j = sum_i P~_ij and t_j = sum_i P~_ij expm1(d_i/eps), d = f' - f, and
+        // h'_j - h_j = -eps log1p(t_j/s_j) (exact algebra), so dQ = a.d + b.(h' - h) rounds
+        // at the size of the step instead of at ulp(Q) (oracle stable_delta_q). Steps with
+        // max|d| > 600 eps take the literal path (guard bits G_LIT / G_NOLIT).
+        const bool stable = accept == 1;
+        const unsigned glit = stable ? (gn | G_LIT) : gn;
+        if (stable) {
+            const unsigned gst = gn | G_NOLIT;
+            count_launch();
+            k_fcand_step<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, P.inv_eps(), S.fcand.p,
+                                                        S.dvec.p, S.Wst.p, 8, P.st, gn);
+            {
+                RedArgs ra;
+                ra.T[0] = n;
+                ra.nterms = 2;
+                ra.x[0] = P.src.w.p;
+                ra.y[0] = S.dvec.p;
+                ra.op[0] = RED_DOT;
+                ra.x[1] = S.dvec.p;
+                ra.op[1] = RED_MAXABS;
+                ra.out = sums + 10;
+                ra.part = P.gram_part.p;
+                ra.counter = &P.st->counters[6];
+                ra.epilogue = P.shard ? EPI_NONE : EPI_STEP;
+                ra.st = P.st;
+                ra.guard = gn;
+                count_launch();
+                k_reduce<<<reduce_blocks(n), AUX_NT, 0, s>>>(ra);
+                if (P.shard) {
+                    allreduce(P, sums + 10, 1, ncclSum);
+                    allreduce(P, sums + 11, 1, ncclMax);
+                    count_launch();
+                    k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_STEP, 0, sums + 10, gn);
+                }
+            }
+            PassSpec tp;
+            tp.dir = 0;
+            tp.in_v = S.f.p;
+            tp.in_lw = P.src.lw.p;
+            tp.out_v = S.h.p;
+            tp.W = S.Wst.p;
+            tp.k = 2;
+            tp.kt = 8;
+            tp.out = S.ST.p;
+            tp.guard = gst;
+            plan_pass(P, tp);  // sums over the row shards
+            count_launch();
+            k_dh<<<grid_for(m), AUX_NT, 0, s>>>(S.ST.p, S.h.p, m, P.eps, S.dh.p, S.hcand.p, P.st, gst);
+            RedArgs ra;
+            ra.T[1] = m;
+            ra.nterms = 1;
+            ra.x[0] = P.tgt.w.p;
+            ra.y[0] = S.dh.p;
+            ra.op[0] = RED_DOT;
+            ra.seg[0] = 1;  // replicated on every rank: same layout, no exchange
+            ra.out = sums + 12;
+            ra.part = P.gram_part.p;
+            ra.counter = &P.st->counters[6];
+            ra.epilogue = EPI_ACCEPT_DQ;
+            ra.st = P.st;
+            ra.guard = gst;
+            count_launch();
+            k_reduce<<<reduce_blocks(m), AUX_NT, 0, s>>>(ra);
+        } else {
+            count_launch();
+            k_fcand<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, S.fcand.p, P.st, gn);
+        }
+        lse(P, 0, S.fcand.p, S.hcand.p, glit);
         {
             RedArgs ra;
             ra.T[0] = n;
@@ -181,13 +254,13 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             ra.counter = &P.st->counters[6];
             ra.epilogue = P.shard ? EPI_NONE : EPI_ACCEPT;
             ra.st = P.st;
-            ra.guard = gn;
+            ra.guard = glit;
             count_launch();
             k_reduce<<<reduce_blocks(n + m), AUX_NT, 0, s>>>(ra);
             if (P.shard) {
                 allreduce(P, sums + 6, 1, ncclSum);
                 count_launch();
-                k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_ACCEPT, 0, sums + 6, gn);
+                k_epilogue<<<1, 32, 0, s>>>(P.st, EPI_ACCEPT, 0, sums + 6, glit);
             }
         }
         count_launch();
@@ -204,7 +277,8 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
 }
 
 static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* basis_host,
-                          const double* init_f, int64_t max_iter, double tol, int64_t trace_cap) {
+                          const double* init_f, int64_t max_iter, double tol, int64_t trace_cap,
+                          int accept = 0) {
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     S.f.ensure(n);
@@ -233,6 +307,13 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         // pre-size the block-pass partials outside graph capture
         const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
         plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
+        if (accept == 1) {  // stable accept test: anchor pass with W = (1, expm1(d/eps))
+            S.dvec.ensure(n);
+            S.Wst.ensure(n * 8);
+            S.ST.ensure(2 * m);
+            S.dh.ensure(m);
+            plan_for(P, 0, MODE_BLOCK, 8, 8);
+        }
     }
     plan_for(P, 0, MODE_SUM, 0);
     plan_for(P, 1, MODE_SUM, 0);
@@ -247,7 +328,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         k_fill<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, n, 0.0);
     }
     count_launch();
-    k_state_init<<<1, 32, 0, s>>>(P.st, max_iter, tol);
+    k_state_init<<<1, 32, 0, s>>>(P.st, max_iter, tol, kStableSpan * P.eps);
     // first sweep's g = f0^{C,eps} (exact shift: no reference state yet)
     lse(P, 0, S.f.p, S.gnext.p, G_NONE);
     CK(cudaGetLastError());
@@ -259,68 +340,124 @@ static bool poll_done(Problem& P) {
     return P.st_host->done != 0;
 }
 
+// Device trace capacity per chunk: long solves pause the device loop when it fills, the
+// host drains it and relaunches (the host copy grows with the iterations actually run,
+// like the reference's push_back, never with max_iter).
+constexpr int64_t kTraceChunk = 1 << 14;
+
+// Ends a pending stream capture on unwind (an exception between Begin/EndCapture would
+// otherwise leave the handle's stream in capture mode) and frees the graph objects.
+struct GraphGuard {
+    cudaStream_t s = nullptr;
+    bool capturing = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~GraphGuard() {
+        if (capturing) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+        }
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+};
+
 static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell, const double* basis,
                           const double* init_f, bool trace_enabled, int64_t trace_cap_hint,
-                          bool exact_marginals = false) {
+                          bool exact_marginals = false, int accept = 0) {
     if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
-    const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, std::max<int64_t>(trace_cap_hint, 1)) : 1;
+    (void)trace_cap_hint;
+    const int64_t trace_cap = trace_enabled ? std::min<int64_t>(max_iter, kTraceChunk) : 1;
     if (!P.solve_cache) P.solve_cache = std::make_shared<SolveState>();
     SolveState& S = *P.solve_cache;
-    prepare_solve(P, S, ell, basis, init_f, max_iter, tol, trace_cap);
+    prepare_solve(P, S, ell, basis, init_f, max_iter, tol, trace_cap, accept);
     cudaStream_t s = P.stream;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
+    GraphGuard gg;
+    gg.s = s;
+    SolveOut out;
+    // copies the device trace records of iterations (trace_base, iter] to the host
+    auto drain = [&]() {
+        if (!trace_enabled) return;
+        CK(cudaMemcpyAsync(P.st_host, P.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t len = std::min<int64_t>(P.st_host->iter - P.st_host->trace_base, trace_cap);
+        if (len > 0) {
+            const size_t old = out.trace.size();
+            out.trace.resize(old + static_cast<size_t>(len));
+            CK(cudaMemcpyAsync(out.trace.data() + old, S.trace_raw.p, sizeof(sknr_record) * len,
+                               cudaMemcpyDeviceToHost, s));
+        }
+        count_launch();
+        k_trace_rebase<<<1, 32, 0, s>>>(P.st);
+        CK(cudaStreamSynchronize(s));
+    };
     // SKNR_HOST_LOOP=1: one graph per iteration, host-polled (profilers such as ncu do not
     // see kernels inside conditional-node bodies)
     static const bool host_loop = std::getenv("SKNR_HOST_LOOP") != nullptr;
     const bool polled = P.shard || host_loop;
     if (!polled) {
         // the whole solve as one graph: a WHILE node whose body is one iteration;
-        // k_record clears the loop condition once the stopping test (or max_iter) hits
-        CK(cudaGraphCreate(&graph, 0));
+        // k_record clears the loop condition once the stopping test (or max_iter) hits,
+        // or pauses it when the device trace chunk is full
+        CK(cudaGraphCreate(&gg.graph, 0));
         cudaGraphConditionalHandle loop = 0;
-        CK(cudaGraphConditionalHandleCreate(&loop, graph, 1, cudaGraphCondAssignDefault));
+        CK(cudaGraphConditionalHandleCreate(&loop, gg.graph, 1, cudaGraphCondAssignDefault));
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
         cp.conditional.handle = loop;
         cp.conditional.type = cudaGraphCondTypeWhile;
         cp.conditional.size = 1;
         cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+        CK(cudaGraphAddNode(&node, gg.graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, loop);
+        gg.capturing = true;
+        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, loop, accept);
+        gg.capturing = false;
         CK(cudaStreamEndCapture(s, &body));
         make_programmatic(body);
-        CK(cudaGraphInstantiate(&exec, graph, 0));
-        CK(cudaGraphLaunch(exec, s));
-        CK(cudaStreamSynchronize(s));
+        CK(cudaGraphInstantiate(&gg.exec, gg.graph, 0));
+        while (true) {
+            CK(cudaGraphLaunch(gg.exec, s));
+            if (!trace_enabled) {
+                CK(cudaStreamSynchronize(s));
+                break;
+            }
+            drain();  // pauses only to drain a full trace chunk
+            if (P.st_host->done) break;
+        }
     } else if (!P.emu) {
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
-        CK(cudaStreamEndCapture(s, &graph));
-        make_programmatic(graph);
-        CK(cudaGraphInstantiate(&exec, graph, 0));
+        gg.capturing = true;
+        enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, 0, accept);
+        gg.capturing = false;
+        CK(cudaStreamEndCapture(s, &gg.graph));
+        make_programmatic(gg.graph);
+        CK(cudaGraphInstantiate(&gg.exec, gg.graph, 0));
     }
     int64_t batch = 1;
     int64_t launched = 0;
     while (polled) {  // sharded (NCCL in the graph), emulated shards, SKNR_HOST_LOOP: host-polled batches
+        // batches never outrun the trace chunk: they are drained at every poll
         for (int64_t b = 0; b < batch; ++b) {
-            if (exec)
-                CK(cudaGraphLaunch(exec, s));
+            if (gg.exec)
+                CK(cudaGraphLaunch(gg.exec, s));
             else  // emulated shards: the same kernels and collectives, launched eagerly
-                enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals);
+                enqueue_iteration(P, S, ell, trace_enabled, trace_cap, exact_marginals, 0, accept);
             ++launched;
         }
-        if (poll_done(P)) break;
+        const bool done = poll_done(P);
+        drain();
+        if (done) break;
         if (launched >= max_iter + 2) break;
-        batch = std::min<int64_t>(batch * 2, 64);
+        // once converged every further launch is a guard-skipped no-op (collectives
+        // included): keep batches short so few of them are issued past the stop
+        batch = std::min<int64_t>({batch * 2, 64, std::max<int64_t>(trace_cap, 1)});
     }
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    SolveOut out;
     out.f.resize(P.n_global);
     out.g.resize(P.m);
     gather_rows(P, S.f.p, out.f.data());
@@ -329,13 +466,6 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     CK(cudaStreamSynchronize(s));
     out.iterations = P.st_host->iter;
     out.converged = P.st_host->conv != 0;
-    if (trace_enabled) {
-        const int64_t len = std::min<int64_t>(out.iterations, trace_cap);
-        out.trace.resize(len);
-        CK(cudaMemcpyAsync(out.trace.data(), S.trace_raw.p, sizeof(sknr_record) * len,
-                           cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
     return out;
 }
 
@@ -352,7 +482,7 @@ struct BatchItem {
 };
 
 static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, double tol, int64_t max_iter,
-                                             int64_t ell, bool exact_marginals) {
+                                             int64_t ell, bool exact_marginals, int accept = 0) {
     if (!(tol > 0.0)) throw InvalidArgument("solve: tol_omega must be positive");
     if (max_iter < 1) throw InvalidArgument("solve: max_iter must be >= 1");
     if (ell > 64) throw InvalidArgument("solve: ell > 64 is not supported by sknr_b200");
@@ -365,7 +495,7 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
     }
     auto S = [&](size_t b) -> SolveState& { return *Sp[b]; };
     for (size_t b = 0; b < B; ++b) {
-        prepare_solve(*items[b].P, S(b), ell, items[b].basis, items[b].init_f, max_iter, tol, 1);
+        prepare_solve(*items[b].P, S(b), ell, items[b].basis, items[b].init_f, max_iter, tol, 1, accept);
         CK(cudaStreamSynchronize(items[b].P->stream));
     }
     cudaStream_t s0 = nullptr;
@@ -391,7 +521,7 @@ static std::vector<SolveOut> run_solve_batch(std::vector<BatchItem>& items, doub
             CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
             cudaGraph_t body = cp.conditional.phGraph_out[0];
             CK(cudaStreamBeginCaptureToGraph(P.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals, loop);
+            enqueue_iteration(P, S(b), ell, false, 1, exact_marginals, loop, accept);
             CK(cudaStreamEndCapture(P.stream, &body));
             make_programmatic(body);
         }

@@ -91,6 +91,11 @@ struct DevState {
     unsigned long long n_exact[2];  // diagnostics: exact-shift passes per direction
     unsigned long long n_retry[2];  // diagnostics: bound-shift validation failures
     unsigned long long n_cull_tested, n_cull_kept;  // diagnostics: culling group tests / kept groups
+    // stable accept test (sknr_config.accept_test = 1): dQ = a.d + b.(h' - h), see engine_solver.cuh
+    int lit;            // this step falls back to the literal Q1 > Q0 test (max|d| > lit_dmax)
+    double lit_dmax;    // largest max|f' - f| the stable evaluation takes (600 eps)
+    double adq;         // a.(f' - f) of the current step
+    long long trace_base;  // iteration index of the device trace buffer's first slot (chunked trace)
 };
 
 enum Guard : unsigned {
@@ -103,6 +108,8 @@ enum Guard : unsigned {
     G_RETRY1 = 32u,     // skip unless st->retry[1]
     G_ACTIVE = 64u,     // skip unless st->iter_active
     G_ACCEPT = 128u,    // skip unless st->accept
+    G_LIT = 256u,       // skip unless st->lit (stable accept test fell back to literal)
+    G_NOLIT = 512u,     // skip if st->lit
 };
 
 __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
@@ -115,6 +122,8 @@ __device__ __forceinline__ bool guard_skip(const DevState* st, unsigned g) {
     if ((g & G_RETRY1) && !st->retry[1]) return true;
     if ((g & G_ACTIVE) && !st->iter_active) return true;
     if ((g & G_ACCEPT) && !st->accept) return true;
+    if ((g & G_LIT) && !st->lit) return true;
+    if ((g & G_NOLIT) && st->lit) return true;
     return false;
 }
 

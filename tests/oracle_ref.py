@@ -41,6 +41,8 @@ class OracleRecord(ctypes.Structure):
         ("semi_dual_value", ctypes.c_double),
         ("newton_attempted", ctypes.c_int),
         ("newton_accepted", ctypes.c_int),
+        ("newton_gain", ctypes.c_double),
+        ("newton_step_max", ctypes.c_double),
     ]
 
 
@@ -62,6 +64,27 @@ def lib():
 
 def set_threads(t: int):
     lib().oracle_set_threads(int(t))
+
+
+def set_accept_mode(mode) -> None:
+    """Accept test of try_newton: "literal" (the reference's Q(f') > Q(f)) or "stable"
+    (the same predicate evaluated as dQ > 0, sknr_oracle.cpp stable_delta_q)."""
+    lib().oracle_set_accept_mode(1 if mode in ("stable", 1) else 0)
+
+
+class accept_mode:
+    """Context manager: run oracle calls under one accept mode, restore literal after."""
+
+    def __init__(self, mode):
+        self.mode = mode
+
+    def __enter__(self):
+        set_accept_mode(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        set_accept_mode("literal")
+        return False
 
 
 def max_threads() -> int:
@@ -264,7 +287,7 @@ def solve(P: Instance, tol=1e-9, max_iter=100000, ell=0, V=None, init=None, trac
                               _p(f), _p(g), ctypes.byref(iters), ctypes.byref(conv), recs,
                               ctypes.c_long(cap), ctypes.byref(tlen)))
     tr = [(r.marginal_error, r.marginal_error_inf, r.semi_dual_value, r.newton_attempted,
-           r.newton_accepted) for r in recs[:min(tlen.value, cap)]]
+           r.newton_accepted, r.newton_gain, r.newton_step_max) for r in recs[:min(tlen.value, cap)]]
     return {"f": f, "g": g, "iterations": iters.value, "converged": bool(conv.value), "trace": tr}
 
 

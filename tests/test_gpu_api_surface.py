@@ -398,23 +398,28 @@ def test_sharded_path_across_R_matches_unsharded(world):
     ref_sk = sk.solve(mk(), tol=1e-9)
     warm = sk.solve(mk().with_epsilon(inst.basis_eps), tol=1e-10)
     basis = sk.top_modes(mk().with_epsilon(inst.basis_eps), warm.f, warm.g, 6)
-    ref_nr = sk.solve(mk(), tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g))
+    ref_nr = sk.solve(mk(), tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g), accept="stable")
     ref_tm = sk.top_modes(mk(), ref_sk.f, ref_sk.g, 6)
     sched = [0.05, 0.025, 0.0125]
-    ref_an = sk.anneal(mk(), sched, warm="spectral", ell=4)
+    ref_an = sk.anneal(mk(), sched, warm="spectral", ell=4, accept="stable")
     out = sk.run_emulated_shards(mk, world, lambda p: (
         sk.solve(p, tol=1e-9),
-        sk.solve(p, tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g)),
+        sk.solve(p, tol=1e-9, ell=6, basis=basis, init=(warm.f, warm.g), accept="stable"),
         sk.top_modes(p, ref_sk.f, ref_sk.g, 6),
-        sk.anneal(p, sched, warm="spectral", ell=4)))
+        sk.anneal(p, sched, warm="spectral", ell=4, accept="stable")))
     for _, _, _, an in out:
         assert [s.iterations for s in an] == [s.iterations for s in ref_an]
-        assert all(rel_err(s.f, q.f) <= TOL_NR for s, q in zip(an, ref_an))
+        assert [[t.newton_accepted for t in s.trace] for s in an] == \
+            [[t.newton_accepted for t in s.trace] for s in ref_an]
+        # stages >= 1 run on a basis each side computed (sharded vs unsharded top_modes,
+        # residual tol 1e-8): the Newton directions agree to that resolution only
+        assert all(rel_err(s.f, q.f) <= TOL_ANNEAL_BASIS for s, q in zip(an, ref_an))
     out = [o[:3] for o in out]
     for r_sk, r_nr, tm in out:
         assert r_sk.iterations == ref_sk.iterations
         assert rel_err(r_sk.f, ref_sk.f) <= 1e-12 and rel_err(r_sk.g, ref_sk.g) <= 1e-12
         assert r_nr.iterations == ref_nr.iterations
+        assert [t.newton_accepted for t in r_nr.trace] == [t.newton_accepted for t in ref_nr.trace]
         assert rel_err(r_nr.f, ref_nr.f) <= TOL_NR
         assert rel_err(tm.rhos, ref_tm.rhos) <= 1e-8
         assert sk.projector_distance(tm, ref_tm) <= 1e-6
@@ -423,7 +428,8 @@ def test_sharded_path_across_R_matches_unsharded(world):
         assert np.array_equal(r_sk.f, out[0][0].f) and np.array_equal(r_nr.g, out[0][1].g)
 
 
-TOL_NR = 2e-8  # accept decisions at the rounding level (as TOL_POT_NEWTON in test_gpu_parity)
+TOL_NR = 1e-9  # stable accept test: identical decisions across R
+TOL_ANNEAL_BASIS = 2e-8
 
 
 @pytest.mark.parametrize("method,degree", [("chebyshev", 8), ("lanczos", 4)])
