@@ -13,6 +13,15 @@
 //    copy-free variant.
 //  * SolveResult::coupling is materialised only on request (coupling_from);
 //    the reference always builds the n x m plan at the end of solve.
+//  * EotProblem can also be built from two harness::PointCloud's
+//    (generators.hpp:12-19) without the dense n x m cost the reference builds at
+//    main.cpp:86: C_ij = cost_scale * ||x_i - y_j||^2 is evaluated on the fly on the
+//    device (the north star's "problem = point clouds or cost"). Such a problem has no
+//    host cost(); everything else is the same.
+//  * Extensions beyond the reference (all off by default): SolverConfig::accept_test
+//    (stable Newton accept test), EotProblem::set_culling / set_precision / shard,
+//    top_modes with the Chebyshev / block-Lanczos methods, and the NCCL communicator
+//    functions comm_unique_id / comm_init / comm_destroy for row sharding.
 #pragma once
 
 #include <algorithm>
@@ -100,38 +109,138 @@ private:
     Matrix c_;
 };
 
-// EotProblem (types.hpp:47-69) backed by a device handle.
+namespace harness {
+// PointCloud (harness/generators.hpp:12-19): points are rows (count x d, column-major),
+// one weight per row.
+struct PointCloud {
+    Matrix points;
+    DiscreteMeasure weights;
+    Index count() const { return points.rows(); }
+    Index dim() const { return points.cols(); }
+};
+
+// sq_euclidean_cost (generators.cpp:94-103): dense host C_ij = ||x_i - y_j||^2 (direct
+// difference). For small problems only; large ones use EotProblem(source, target, eps).
+inline CostMatrix sq_euclidean_cost(const PointCloud& source, const PointCloud& target) {
+    if (source.dim() != target.dim()) throw std::invalid_argument("sq_euclidean_cost: dimension mismatch");
+    Matrix c(source.count(), target.count());
+    for (Index j = 0; j < target.count(); ++j)
+        for (Index i = 0; i < source.count(); ++i) {
+            double s = 0.0;
+            for (Index k = 0; k < source.dim(); ++k) {
+                const double t = source.points(i, k) - target.points(j, k);
+                s += t * t;
+            }
+            c(i, j) = s;
+        }
+    return CostMatrix(std::move(c));
+}
+}  // namespace harness
+
+// How an on-the-fly problem evaluates its cost (sknr_problem_create_points_ex).
+enum class CostMode { automatic = 0, stored = 1, on_the_fly = 2 };
+
+// EotProblem (types.hpp:47-69) backed by a device handle: either a dense cost
+// (the reference's constructor) or two point clouds (cost evaluated on the fly).
 class EotProblem {
 public:
     EotProblem(CostMatrix cost, DiscreteMeasure alpha, DiscreteMeasure beta, double epsilon)
-        : cost_(std::move(cost)), alpha_(std::move(alpha)), beta_(std::move(beta)), eps_(epsilon) {
-        if (alpha_.size() != cost_.rows() || beta_.size() != cost_.cols())
+        : cost_(std::make_shared<CostMatrix>(std::move(cost))), alpha_(std::move(alpha)),
+          beta_(std::move(beta)), eps_(epsilon), n_(cost_->rows()), m_(cost_->cols()) {
+        if (alpha_.size() != cost_->rows() || beta_.size() != cost_->cols())
             throw std::invalid_argument("EotProblem: measure sizes must match cost shape");
         sknr_problem h = nullptr;
-        detail::check(sknr_problem_create_dense(cost_.entries().data(), cost_.rows(), cost_.cols(),
-                                                alpha_.weights().data(), beta_.weights().data(), eps_,
-                                                &h));
+        detail::check(sknr_problem_create_dense(cost_->entries().data(), n_, m_, alpha_.weights().data(),
+                                                beta_.weights().data(), eps_, &h));
         h_ = std::shared_ptr<sknr_problem_s>(h, detail::HandleDeleter());
     }
-    Index n() const { return cost_.rows(); }
-    Index m() const { return cost_.cols(); }
-    const Matrix& cost() const { return cost_.entries(); }
+    // Point-cloud problem: C_ij = cost_scale * ||x_i - y_j||^2 never stored (d <= 4 in
+    // registers, larger d stored on device when it fits or contracted on FP64 tensor
+    // cores); alpha/beta are the clouds' weights.
+    EotProblem(const harness::PointCloud& source, const harness::PointCloud& target, double epsilon,
+               double cost_scale = 1.0, CostMode mode = CostMode::automatic)
+        : src_(std::make_shared<harness::PointCloud>(source)), tgt_(std::make_shared<harness::PointCloud>(target)),
+          alpha_(source.weights), beta_(target.weights), eps_(epsilon), n_(source.count()), m_(target.count()),
+          cost_scale_(cost_scale), mode_(mode) {
+        if (source.dim() != target.dim()) throw std::invalid_argument("EotProblem: point dimensions differ");
+        if (alpha_.size() != n_ || beta_.size() != m_)
+            throw std::invalid_argument("EotProblem: measure sizes must match cost shape");
+        sknr_problem h = nullptr;
+        detail::check(sknr_problem_create_points_ex(src_->points.data(), tgt_->points.data(), n_, m_, source.dim(),
+                                                    cost_scale, alpha_.weights().data(), beta_.weights().data(),
+                                                    eps_, static_cast<int>(mode), &h));
+        h_ = std::shared_ptr<sknr_problem_s>(h, detail::HandleDeleter());
+    }
+    Index n() const { return n_; }
+    Index m() const { return m_; }
+    bool has_stored_cost() const { return cost_ != nullptr; }
+    // The dense cost of a dense problem; a point-cloud problem has none on the host.
+    const Matrix& cost() const {
+        if (!cost_) throw std::logic_error("EotProblem::cost: point-cloud problem (cost evaluated on the fly)");
+        return cost_->entries();
+    }
+    const harness::PointCloud* source() const { return src_.get(); }
+    const harness::PointCloud* target() const { return tgt_.get(); }
     const DiscreteMeasure& alpha() const { return alpha_; }
     const DiscreteMeasure& beta() const { return beta_; }
     double epsilon() const { return eps_; }
-    EotProblem with_epsilon(double epsilon) const { return EotProblem(cost_, alpha_, beta_, epsilon); }
+    double cost_scale() const { return cost_scale_; }
+    // Same instance at a different regularization (types.hpp:60-62): a new device handle.
+    EotProblem with_epsilon(double epsilon) const {
+        EotProblem p = cost_ ? EotProblem(*cost_, alpha_, beta_, epsilon)
+                             : EotProblem(*src_, *tgt_, epsilon, cost_scale_, mode_);
+        if (cull_ > 0.0) p.set_culling(cull_);
+        if (bits_ != 64) p.set_precision(bits_);
+        return p;
+    }
+    // In place and copy-free (every copy of this problem shares the handle).
     void set_epsilon(double epsilon) {
         detail::check(sknr_problem_set_epsilon(h_.get(), epsilon));
         eps_ = epsilon;
     }
+    // Opt-in culling of negligible terms (sknr_problem_set_culling; threshold 0 = off).
+    void set_culling(double threshold) {
+        detail::check(sknr_problem_set_culling(h_.get(), threshold));
+        cull_ = threshold;
+    }
+    // Opt-in fp32 LSE sum passes (sknr_problem_set_precision; 64 = the fp64 default).
+    void set_precision(int bits) {
+        detail::check(sknr_problem_set_precision(h_.get(), bits));
+        bits_ = bits;
+    }
+    // Row sharding under the communicator of comm_init(): keep rows [row_begin, row_end).
+    void shard(Index row_begin, Index row_end) { detail::check(sknr_problem_shard(h_.get(), row_begin, row_end)); }
     sknr_problem handle() const { return h_.get(); }
 
 private:
-    CostMatrix cost_;
+    std::shared_ptr<CostMatrix> cost_;
+    std::shared_ptr<harness::PointCloud> src_, tgt_;
     DiscreteMeasure alpha_, beta_;
     double eps_;
+    Index n_ = 0, m_ = 0;
+    double cost_scale_ = 1.0;
+    CostMode mode_ = CostMode::automatic;
+    double cull_ = 0.0;
+    int bits_ = 64;
     std::shared_ptr<sknr_problem_s> h_;
 };
+
+// Standard contiguous row block of rank r among `world` (as the library partitions rows).
+inline std::pair<Index, Index> row_block(Index n, int world, int rank) {
+    return {n * rank / world, n * (rank + 1) / world};
+}
+
+// ---- multi-GPU plumbing (one process per GPU; NCCL over NVLink)
+inline std::vector<unsigned char> comm_unique_id() {
+    std::vector<unsigned char> id(128);
+    detail::check(sknr_comm_unique_id(id.data()));
+    return id;
+}
+inline void comm_init(int rank, int world, const std::vector<unsigned char>& id, int device = -1) {
+    if (id.size() != 128) throw std::invalid_argument("comm_init: unique id must be 128 bytes");
+    detail::check(sknr_comm_init(rank, world, id.data(), device));
+}
+inline void comm_destroy() { detail::check(sknr_comm_destroy()); }
 
 struct Potentials {
     Vector f, g;
@@ -148,12 +257,17 @@ struct SpectralBasis {
     Index dim() const { return vectors.rows(); }
 };
 
+// Newton accept test (extension): literal = the reference's Q(f') > Q(f); stable = the
+// same predicate evaluated as dQ > 0 (sknr_config.accept_test).
+enum class AcceptTest { literal = 0, stable = 1 };
+
 struct SolverConfig {
     double tol_omega = 1e-9;
     Index max_iter = 100000;
     Index ell = 0;
     bool newton_enabled = true;
     bool trace_enabled = true;
+    AcceptTest accept_test = AcceptTest::literal;  // extension (not in solver.hpp:13-19)
 };
 
 struct IterationRecord {
@@ -316,6 +430,17 @@ inline SpectralBasis top_modes(const EotProblem& p, const Potentials& anchor, In
     return b;
 }
 
+// Extension: accelerated basis methods with the same residual test (sknr_top_modes_ex).
+enum class TopModesMethod { subspace = 0, chebyshev = 1, lanczos = 2 };
+inline SpectralBasis top_modes(const EotProblem& p, const Potentials& anchor, Index ell, double tol,
+                               Index max_power_iters, TopModesMethod method, int degree) {
+    SpectralBasis b{Matrix(p.n(), ell), Matrix(p.n(), ell), Vector(ell), p.epsilon()};
+    detail::check(sknr_top_modes_ex(p.handle(), anchor.f.data(), anchor.g.data(), ell, tol, max_power_iters,
+                                    static_cast<int>(method), degree, b.vectors.data(), b.vectors_sym.data(),
+                                    b.rhos.data(), nullptr));
+    return b;
+}
+
 // SinkhornOperator (spectral.hpp:14-42): matrix-free view of K_eps at (f, g); keeps a
 // pointer to the problem, which must outlive it (as in the reference).
 class SinkhornOperator {
@@ -419,19 +544,21 @@ struct NewtonOutcome {  // solver.hpp:50-57
     bool accepted = false;
     bool factorization_failed = false;
 };
-inline NewtonOutcome newton_step(const EotProblem& p, const Vector& f, const SpectralBasis& basis) {
+inline NewtonOutcome newton_step(const EotProblem& p, const Vector& f, const SpectralBasis& basis,
+                                 AcceptTest accept = AcceptTest::literal) {
     if (basis.ell() < 1) throw std::invalid_argument("newton_step: empty basis");
     if (basis.dim() != p.n()) throw std::invalid_argument("restricted_derivatives: basis dimension mismatch");
     NewtonOutcome o{Vector(p.n())};
     int acc = 0, fail = 0;
-    detail::check(sknr_newton_step(p.handle(), f.data(), basis.vectors.data(), basis.ell(), o.f.data(), &acc, &fail));
+    detail::check(sknr_newton_step_ex(p.handle(), f.data(), basis.vectors.data(), basis.ell(),
+                                      static_cast<int>(accept), o.f.data(), &acc, &fail));
     o.accepted = acc != 0;
     o.factorization_failed = fail != 0;
     return o;
 }
 
-inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
-                         const SpectralBasis* basis = nullptr, const Potentials* init = nullptr) {
+namespace detail {
+inline sknr_config to_c(const SolverConfig& config) {
     sknr_config c;
     sknr_config_default(&c);
     c.tol_omega = config.tol_omega;
@@ -439,6 +566,28 @@ inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
     c.ell = config.ell;
     c.newton_enabled = config.newton_enabled ? 1 : 0;
     c.trace_enabled = config.trace_enabled ? 1 : 0;
+    c.accept_test = static_cast<int32_t>(config.accept_test);
+    return c;
+}
+constexpr Index kTracePrealloc = 4096;  // longer traces are fetched whole (sknr_last_trace)
+inline std::vector<sknr_record> fetch_trace(sknr_problem h, std::vector<sknr_record> recs, int64_t tlen) {
+    if (tlen > static_cast<int64_t>(recs.size())) {
+        recs.resize(static_cast<size_t>(tlen));
+        int64_t got = 0;
+        check(sknr_last_trace(h, recs.data(), tlen, &got));
+    }
+    recs.resize(static_cast<size_t>(std::min<int64_t>(tlen, static_cast<int64_t>(recs.size()))));
+    return recs;
+}
+inline IterationRecord to_record(const sknr_record& s) {
+    return IterationRecord{s.index, s.marginal_error, s.marginal_error_inf, s.semi_dual_value,
+                           s.newton_attempted != 0, s.newton_accepted != 0, s.wall_time_ms};
+}
+}  // namespace detail
+
+inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
+                         const SpectralBasis* basis = nullptr, const Potentials* init = nullptr) {
+    sknr_config c = detail::to_c(config);
     if (config.newton_enabled && config.ell > 0 && basis && basis->dim() != p.n())
         throw std::invalid_argument("solve: basis dimension mismatch");
     if (init && (init->f.size() != p.n() || init->g.size() != p.m()))
@@ -446,7 +595,7 @@ inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
     SolveResult r;
     r.potentials.f = Vector(p.n());
     r.potentials.g = Vector(p.m());
-    const Index cap = config.trace_enabled ? config.max_iter : 0;
+    const Index cap = config.trace_enabled ? std::min(config.max_iter, detail::kTracePrealloc) : 0;
     std::vector<sknr_record> recs(static_cast<size_t>(cap > 0 ? cap : 1));
     int64_t iters = 0, tlen = 0;
     int conv = 0;
@@ -456,10 +605,10 @@ inline SolveResult solve(const EotProblem& p, const SolverConfig& config,
                              &iters, &conv, recs.data(), cap, &tlen));
     r.iterations = iters;
     r.converged = conv != 0;
-    for (int64_t t = 0; t < tlen && t < cap; ++t) {
-        const sknr_record& s = recs[static_cast<size_t>(t)];
-        r.trace.push_back(IterationRecord{s.index, s.marginal_error, s.marginal_error_inf, s.semi_dual_value,
-                                          s.newton_attempted != 0, s.newton_accepted != 0, s.wall_time_ms});
+    if (config.trace_enabled) {
+        recs.resize(static_cast<size_t>(cap));
+        for (const sknr_record& s : detail::fetch_trace(p.handle(), std::move(recs), tlen))
+            r.trace.push_back(detail::to_record(s));
     }
     return r;
 }
@@ -471,12 +620,7 @@ inline std::vector<SolveResult> solve_batch(const std::vector<const EotProblem*>
                                             const std::vector<const SpectralBasis*>& bases = {},
                                             const std::vector<const Potentials*>& inits = {}) {
     const size_t B = problems.size();
-    sknr_config c;
-    sknr_config_default(&c);
-    c.tol_omega = config.tol_omega;
-    c.max_iter = config.max_iter;
-    c.ell = config.ell;
-    c.newton_enabled = config.newton_enabled ? 1 : 0;
+    sknr_config c = detail::to_c(config);
     c.trace_enabled = 0;
     std::vector<sknr_problem> h(B);
     std::vector<const double*> bp(B, nullptr), fi(B, nullptr), gi(B, nullptr);
@@ -510,23 +654,22 @@ inline std::vector<SolveResult> solve_batch(const std::vector<const EotProblem*>
 inline std::vector<SolveResult> anneal(const EotProblem& p, const AnnealSchedule& schedule,
                                        const SolverConfig& config) {
     const Index S = static_cast<Index>(schedule.epsilons.size());
-    sknr_config c;
-    sknr_config_default(&c);
-    c.tol_omega = config.tol_omega;
-    c.max_iter = config.max_iter;
-    c.ell = config.ell;
-    c.newton_enabled = config.newton_enabled ? 1 : 0;
-    c.trace_enabled = config.trace_enabled ? 1 : 0;
+    sknr_config c = detail::to_c(config);
     std::vector<double> F(static_cast<size_t>(S * p.n())), G(static_cast<size_t>(S * p.m()));
     std::vector<int64_t> iters(static_cast<size_t>(S)), offs(static_cast<size_t>(S));
     std::vector<int> conv(static_cast<size_t>(S));
-    const Index cap = config.trace_enabled ? config.max_iter * S : 0;
+    Index cap = config.trace_enabled ? std::min(config.max_iter, detail::kTracePrealloc) * S : 0;
     std::vector<sknr_record> recs(static_cast<size_t>(cap > 0 ? cap : 1));
     int64_t tlen = 0;
     const int warm = schedule.warm_mode == WarmMode::none ? 0 : schedule.warm_mode == WarmMode::potentials ? 1 : 2;
     detail::check(sknr_anneal(p.handle(), schedule.epsilons.data(), S, warm, schedule.refresh_basis ? 1 : 0, &c,
                               F.data(), G.data(), iters.data(), conv.data(), recs.data(), cap, offs.data(),
                               &tlen));
+    if (config.trace_enabled && tlen > cap) {
+        recs.resize(static_cast<size_t>(cap));
+        recs = detail::fetch_trace(p.handle(), std::move(recs), tlen);
+        cap = tlen;
+    }
     std::vector<SolveResult> out(static_cast<size_t>(S));
     for (Index s = 0; s < S; ++s) {
         SolveResult& r = out[static_cast<size_t>(s)];
@@ -536,9 +679,7 @@ inline std::vector<SolveResult> anneal(const EotProblem& p, const AnnealSchedule
         r.converged = conv[static_cast<size_t>(s)] != 0;
         const int64_t hi = s + 1 < S ? offs[static_cast<size_t>(s + 1)] : tlen;
         for (int64_t t = offs[static_cast<size_t>(s)]; t < hi && t < cap; ++t) {
-            const sknr_record& q = recs[static_cast<size_t>(t)];
-            r.trace.push_back(IterationRecord{q.index, q.marginal_error, q.marginal_error_inf, q.semi_dual_value,
-                                              q.newton_attempted != 0, q.newton_accepted != 0, q.wall_time_ms});
+            r.trace.push_back(detail::to_record(recs[static_cast<size_t>(t)]));
         }
     }
     return out;

@@ -299,6 +299,10 @@ int sknr_comm_init(int rank, int world, const unsigned char id[128], int device)
  * ends it. Used to check the sharded path at R > 1 on a single GPU. */
 int sknr_comm_init_emulated(int world);
 int sknr_comm_destroy(void);
+/* Collectives this process issued for sharded handles since the last reset: calls and
+ * payload bytes (allreduce counts once per call with its buffer size; a row gather
+ * counts the full gathered vector). reset != 0 zeroes the counters after reading. */
+int sknr_comm_stats(int64_t* calls, int64_t* bytes, int reset);
 /* Restrict a freshly created problem to rows [row_begin,row_end) of this rank
  * under the attached communicator. */
 int sknr_problem_shard(sknr_problem p, int64_t row_begin, int64_t row_end);

@@ -134,6 +134,7 @@ _SIGS = {
     "sknr_comm_destroy": [],
     "sknr_comm_init_emulated": [ctypes.c_int],
     "sknr_problem_shard": [_P, _I64, _I64],
+    "sknr_comm_stats": [ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.c_int],
 }
 _RET = {
     "sknr_last_error": ctypes.c_char_p,
@@ -971,6 +972,13 @@ def comm_init(rank: int, world: int, uid: bytes, device: int = -1) -> None:
         raise ValueError("comm_init: unique id must be 128 bytes")
     buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
     _check(lib().sknr_comm_init(int(rank), int(world), buf, int(device)))
+
+
+def comm_stats(reset: bool = False):
+    """(calls, bytes) of the collectives this process issued for sharded handles."""
+    c, b = _I64(), _I64()
+    _check(lib().sknr_comm_stats(ctypes.byref(c), ctypes.byref(b), 1 if reset else 0))
+    return int(c.value), int(b.value)
 
 
 def comm_destroy() -> None:

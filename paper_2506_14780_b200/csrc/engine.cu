@@ -576,9 +576,17 @@ static EmuGroup g_emu;
 
 static int nccl_op_code(ncclRedOp_t op) { return op == ncclMax ? 1 : 0; }
 
+// Collective accounting (sknr_comm_stats): calls and payload bytes issued by this process.
+static std::atomic<int64_t> g_coll_calls{0}, g_coll_bytes{0};
+static void count_collective(size_t bytes) {
+    g_coll_calls.fetch_add(1, std::memory_order_relaxed);
+    g_coll_bytes.fetch_add(static_cast<int64_t>(bytes), std::memory_order_relaxed);
+}
+
 // In-place allreduce on the problem's stream; a no-op unless the handle is row-sharded.
 static void allreduce(Problem& P, double* buf, size_t count, ncclRedOp_t op) {
     if (!P.shard || count == 0) return;
+    count_collective(count * sizeof(double));
     if (P.emu) {
         std::unique_lock<std::mutex> lk(g_emu.mu);
         g_emu.bufs.buf[P.rank] = buf;
@@ -628,6 +636,7 @@ static void gather_rows(Problem& P, const double* dev_local, double* host_full) 
         CK(cudaStreamSynchronize(P.stream));
         return;
     }
+    count_collective(static_cast<size_t>(P.n_global) * sizeof(double));
     NK(g_nccl.GroupStart());
     for (int r = 0; r < g_comm.world; ++r) {
         int64_t b, e;

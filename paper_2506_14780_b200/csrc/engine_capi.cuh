@@ -1143,6 +1143,17 @@ int sknr_anneal(sknr_problem h, const double* epsilons, int64_t stages, int warm
     SKNR_API_END
 }
 
+int sknr_comm_stats(int64_t* calls, int64_t* bytes, int reset) {
+    SKNR_API_BEGIN
+    if (calls) *calls = g_coll_calls.load();
+    if (bytes) *bytes = g_coll_bytes.load();
+    if (reset) {
+        g_coll_calls.store(0);
+        g_coll_bytes.store(0);
+    }
+    SKNR_API_END
+}
+
 int sknr_last_trace(sknr_problem h, sknr_record* trace, int64_t cap, int64_t* len) {
     SKNR_API_BEGIN
     Problem& P = get(h);

@@ -441,6 +441,8 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
     }
     int64_t batch = 1;
     int64_t launched = 0;
+    double gap_prev = 0.0;
+    int64_t iter_prev = 0;
     while (polled) {  // sharded (NCCL in the graph), emulated shards, SKNR_HOST_LOOP: host-polled batches
         // batches never outrun the trace chunk: they are drained at every poll
         for (int64_t b = 0; b < batch; ++b) {
@@ -451,12 +453,24 @@ static SolveOut run_solve(Problem& P, double tol, int64_t max_iter, int64_t ell,
             ++launched;
         }
         const bool done = poll_done(P);
+        const double gap = P.st_host->gap_l2;
+        const int64_t it = P.st_host->iter;
         drain();
         if (done) break;
         if (launched >= max_iter + 2) break;
-        // once converged every further launch is a guard-skipped no-op (collectives
-        // included): keep batches short so few of them are issued past the stop
-        batch = std::min<int64_t>({batch * 2, 64, std::max<int64_t>(trace_cap, 1)});
+        // Launches past the stop are guard-skipped no-ops, but their collectives still run:
+        // size the next batch from the observed contraction of the marginal error, so the
+        // batch that crosses tol overshoots by a few iterations instead of up to 63.
+        int64_t next = std::min<int64_t>(batch * 2, 64);
+        if (gap_prev > 0.0 && gap > 0.0 && gap < gap_prev && it > iter_prev) {
+            const double rate = std::log(gap / gap_prev) / static_cast<double>(it - iter_prev);  // < 0
+            const double remaining = std::log(tol / gap) / rate;
+            if (std::isfinite(remaining))
+                next = std::min<int64_t>(next, std::max<int64_t>(1, static_cast<int64_t>(remaining) + 1));
+        }
+        gap_prev = gap;
+        iter_prev = it;
+        batch = std::min<int64_t>(next, std::max<int64_t>(trace_cap, 1));
     }
     out.f.resize(P.n_global);
     out.g.resize(P.m);

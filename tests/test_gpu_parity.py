@@ -424,6 +424,37 @@ def test_cpp_facade_demo_runs():
     assert "converged=1" in out.stdout and "rho1=" in out.stdout
 
 
+@pytest.mark.parametrize("mode", ["stable", "literal"])
+def test_cpp_facade_points_c4(tmp_path, mode):
+    """BASELINE C4 (n = m = 65536, d = 2) through the C++ facade's point-cloud
+    EotProblem (no dense cost): warm SK at eps' = 1e-3, block-Lanczos basis, SK-NR(32)
+    at eps = 5e-4 -- the same iterations and bit-identical potentials as the same
+    protocol through the Python API."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "facade_points_demo")
+    if not os.path.exists(exe):
+        pytest.skip("facade points demo not built")
+    c = G.config("C4")
+    for name, arr in (("x", c.x), ("y", c.y), ("a", c.alpha), ("b", c.beta)):
+        np.asfortranarray(arr, dtype=np.float64).ravel(order="F").tofile(tmp_path / f"{name}.bin")
+    (tmp_path / "meta.txt").write_text(f"{c.n} {c.m} 2 {c.epsilon!r} {c.basis_eps!r} {c.ell}\n")
+    out = subprocess.run([exe, str(tmp_path), mode], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    f_cpp = np.fromfile(tmp_path / "f.bin")
+    g_cpp = np.fromfile(tmp_path / "g.bin")
+    pw = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.basis_eps)
+    warm = sk.solve(pw, tol=1e-9, trace=False)
+    basis = sk.top_modes(pw, warm.f, warm.g, c.ell, method="lanczos", degree=12)
+    r = sk.solve(sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon), tol=1e-9, ell=c.ell, basis=basis,
+                 init=(warm.f, warm.g), accept=mode)
+    assert r.converged
+    assert f"iterations={r.iterations} " in out.stdout.splitlines()[-1]
+    assert np.array_equal(f_cpp, r.f) and np.array_equal(g_cpp, r.g)
+
+
 def test_sharded_code_path_single_rank_is_bitwise_identical():
     """World-size-1 NCCL communicator: every collective of the row-sharded path
     runs (allreduce of column partials, gauge scalar, residuals, Newton inner

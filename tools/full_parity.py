@@ -32,7 +32,8 @@ CFG = os.environ.get("SKNR_PARITY_CFG", "C4").upper()
 TAG = CFG.lower()
 INPUTS = os.path.join(ROOT, f"{TAG}_full_inputs", "inputs.npz")
 OUT = os.path.join(ROOT, "gpurun_out", f"{TAG}_r02")
-STATE = os.path.join(ROOT, f"{TAG}_full_inputs")  # oracle checkpoints live beside the inputs
+# oracle checkpoints: beside the inputs here; under gpurun_out/ on the GPU box's host
+STATE = os.environ.get("SKNR_PARITY_STATE", os.path.join(ROOT, f"{TAG}_full_inputs"))
 CHUNK = int(os.environ.get("SKNR_PARITY_CHUNK", "5"))
 MAX_ITER = 5000
 
@@ -71,6 +72,7 @@ def run_oracle(mode):
     c = G.config(CFG)
     d = np.load(INPUTS)
     op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+    os.makedirs(STATE, exist_ok=True)
     path = os.path.join(STATE, f"oracle_{mode}.npz")
     if os.path.exists(path):
         s = np.load(path)
@@ -127,9 +129,10 @@ def merge():
                "oracle_newton_gain": [float(t[5]) for t in tr],
                "marginal_error_gpu": [float(v) for v in me_g], "marginal_error_oracle": [float(v) for v in me_o],
                "accepted_gpu": acc_g, "accepted_oracle": acc_o}
-        if bool(o["converged"]) and int(o["done"]) == int(g["iterations"]):
-            row["rel_f"] = rel(g["f"], o["f"])
-            row["rel_g"] = rel(g["g"], o["g"])
+        # potentials at each side's stopping iteration (the same iteration when the counts agree)
+        row["same_iteration_count"] = int(o["done"]) == int(g["iterations"])
+        row["rel_f"] = rel(g["f"], o["f"])
+        row["rel_g"] = rel(g["g"], o["g"])
         out["modes"][mode] = row
     gi = os.path.join(OUT, "gpu_info.json")
     if os.path.exists(gi):
