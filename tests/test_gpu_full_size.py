@@ -1,0 +1,102 @@
+"""Full-size BASELINE configs against the oracle (-m gpu; about 8 minutes on the GPU
+box's 16 host cores, most of it oracle time).
+
+* C2 (configs[1]): the whole anneal, eps 0.1 -> 0.001, spectral warm start, ell = 16,
+  each side computing its own bases (solver.cpp:158-222).
+* C3, C4, C5 stored, C5 on the fly (configs[2..4]) at their full sizes: K SK iterations
+  from f = 0, then K_NR SK-NR(ell) iterations with a smooth L2(alpha)-orthonormal basis
+  from the oracle's iterate -- the same start on both sides, compared per iteration.
+* C4 with the opt-in fp32 LSE passes: both transforms within the 1e-5 fp32 bar.
+
+The main solves to tolerance at C3 / C4 (hundreds to thousands of oracle-hours of host
+time) are in profiles/c{3,4}_full_parity_r02.json (tools/full_parity.py)."""
+import numpy as np
+import pytest
+
+import oracle_ref as O
+import paper_2506_14780_b200 as sk
+from paper_2506_14780_b200 import generators as G
+from support import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_POT = 1e-9
+
+
+def smooth_basis(x, alpha, ell):
+    """ell low-frequency cosine modes of a 2-D projection of the sources, orthonormal in
+    L2(alpha) and alpha-mean-zero (the deflated direction removed): a Newton basis whose
+    steps are large and well decided, with no top_modes run needed on either side."""
+    rng = np.random.default_rng(0)
+    z = x @ rng.standard_normal((x.shape[1], 2))
+    z = (z - z.min(0)) / (z.max(0) - z.min(0))
+    cols = [np.cos(np.pi * a * z[:, 0]) * np.cos(np.pi * b * z[:, 1])
+            for a in range(8) for b in range(8) if (a, b) != (0, 0)]
+    w = np.sqrt(alpha)[:, None]
+    Vs = np.stack(cols[:ell], 1) * w
+    Vs -= w * (w[:, 0] @ Vs)[None, :]
+    Q, _ = np.linalg.qr(Vs)
+    return np.asfortranarray(Q / w)
+
+
+@pytest.mark.parametrize("name,mode,K,KN", [("C3", "auto", 6, 3), ("C4", "auto", 2, 2),
+                                            ("C5", "stored", 2, 2), ("C5", "onthefly", 2, 2)])
+def test_full_size_trajectory(name, mode, K, KN):
+    c = G.config(name)
+    gp = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale, cost_mode=mode)
+    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+    rg = sk.solve(gp, tol=1e-300, max_iter=K)
+    ro = O.solve(op, tol=1e-300, max_iter=K)
+    assert rel_err(rg.f, ro["f"]) <= TOL_POT and rel_err(rg.g, ro["g"]) <= TOL_POT
+    for tg, to in zip(rg.trace, ro["trace"]):
+        assert abs(tg.marginal_error - to[0]) <= 1e-9 * to[0]
+    V = smooth_basis(c.x, c.alpha, c.ell)
+    basis = sk.SpectralBasis(V, V, np.zeros(c.ell), c.epsilon)
+    init = (ro["f"], ro["g"])
+    ng = sk.solve(gp, tol=1e-300, max_iter=KN, ell=c.ell, basis=basis, init=init, accept="stable")
+    with O.accept_mode("stable"):
+        no = O.solve(op, tol=1e-300, max_iter=KN, ell=c.ell, V=V, init=init)
+    assert [t.newton_accepted for t in ng.trace] == [bool(t[4]) for t in no["trace"]]
+    assert rel_err(ng.f, no["f"]) <= TOL_POT and rel_err(ng.g, no["g"]) <= TOL_POT
+    for tg, to in zip(ng.trace, no["trace"]):
+        assert abs(tg.marginal_error - to[0]) <= 1e-9 * to[0]
+        assert abs(tg.semi_dual_value - to[2]) <= 1e-13 * abs(to[2])
+
+
+@pytest.mark.parametrize("accept", ["stable", "literal"])
+def test_c2_anneal_full(accept):
+    """BASELINE C2 end to end: 8 stages, spectral warm start (the basis is built once
+    from stage 0's potentials by each side's own top_modes), ell = 16, tol 1e-9."""
+    c = G.config("C2")
+    eps = list(c.epsilons)
+    gp = sk.PointProblem(c.x, c.y, c.alpha, c.beta, eps[0], c.cost_scale)
+    sg = sk.anneal(gp, eps, warm="spectral", ell=c.ell, accept=accept)
+    op = O.Instance(c.alpha, c.beta, eps[0], x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+    with O.accept_mode(accept):
+        so = O.anneal(op, eps, warm="spectral", ell=c.ell)
+    its_g = [s.iterations for s in sg]
+    its_o = [s["iterations"] for s in so]
+    rel = [rel_err(a.f, b["f"]) for a, b in zip(sg, so)]
+    print(accept, "iterations gpu", its_g, "oracle", its_o, "rel_f", ["%.1e" % r for r in rel])
+    assert all(s.converged for s in sg) and all(s["converged"] for s in so)
+    assert rel[0] <= TOL_POT and its_g[0] == its_o[0]  # stage 0: plain SK
+    if accept == "stable":
+        assert its_g == its_o
+        assert max(rel) <= TOL_POT
+
+
+def test_c4_fp32_transforms_full_size():
+    """The opt-in fp32 LSE passes at the full C4 shape: both transforms within 1e-5 of
+    the fp64 oracle (north star: 1e-5 if an fp32 variant is offered)."""
+    c = G.config("C4")
+    gp = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon)
+    gp.set_precision(32)
+    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y)
+    rng = np.random.default_rng(4)
+    f = 0.02 * rng.standard_normal(c.n)
+    g32 = sk.ctransform_of_f(gp, f)
+    go = O.ctransform_of_f(op, f)
+    assert rel_err(g32, go) <= 1e-5
+    f32 = sk.ctransform_of_g(gp, go)
+    fo = O.ctransform_of_g(op, go)
+    assert rel_err(f32, fo) <= 1e-5
