@@ -82,12 +82,6 @@ __global__ void __launch_bounds__(AUX_NT) k_prep_in(PrepInArgs a) {
     mx = block_reduce(mx, sh, MaxOp());
     mn = block_reduce(mn, sh, MinOp());
     if (threadIdx.x == 0) {
-        if (a.defer) {  // sharded: decided by k_decide after the cross-rank max
-            a.st->scratch[2 * a.dir] = mx;
-            a.st->scratch[2 * a.dir + 1] = -mn;
-            a.st->counters[a.dir] = 0u;
-            return;
-        }
         a.st->dmax[a.dir] = mx;
         a.st->dmin[a.dir] = mn;
         const bool ok = a.st->ref_valid[a.dir] && (mx - mn) * a.inv_eps <= a.exact_spread &&
@@ -218,6 +212,7 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
                 bad = !(S >= a.lo_ok && S <= 0x1p900);
                 const double L = a.shift[o] + log(S);
                 if (a.L) a.L[o] = L;
+                if (a.S) a.S[o] = S;
                 if (a.pot) a.pot[o] = -a.eps * L;
             }
             if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0 && !a.retry_phase &&
@@ -226,6 +221,22 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_finalize(FinalizeArgs a) {
                 atomicAdd(&a.st->n_retry[a.dir], 1ull);
             }
         }
+    }
+}
+
+__global__ void __launch_bounds__(AUX_NT) k_lse_merge(const double* X, int world, int64_t m, double eps,
+                                                      double* L, double* pot, const DevState* st, unsigned guard) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(st, guard)) return;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double M = X[j];
+        for (int r = 1; r < world; ++r) M = fmax(M, X[r * 2 * m + j]);
+        double T = 0.0;
+        for (int r = 0; r < world; ++r) T += X[r * 2 * m + m + j] * exp(X[r * 2 * m + j] - M);
+        const double v = M + log(T);
+        L[j] = v;
+        if (pot) pot[j] = -eps * v;
     }
 }
 
@@ -517,33 +528,6 @@ __global__ void k_epilogue(DevState* st, int epilogue, int newton, const double*
     SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     if (threadIdx.x == 0 && blockIdx.x == 0) run_epilogue(st, epilogue, newton, r);
-}
-
-// max over split-K partials (sharded column LSE: local part before allreduce)
-__global__ void __launch_bounds__(AUX_NT) k_max_local(const double* partial, int64_t nb, int64_t n_out,
-                                                      double* out, DevState* st, unsigned guard) {
-    SKNR_PDL_ENTRY();
-    if (guard_skip(st, guard)) return;
-    __shared__ double sh[FOLD_W][32];
-    FOLD_LOOP(n_out) {
-        const int64_t o = q0 + (threadIdx.x & 31);
-        const double M = fold_rows<true>(partial, nb, n_out, o, o < n_out, sh);
-        if (threadIdx.x < 32 && o < n_out) out[o] = M;
-    }
-}
-
-// exact-path decision after the cross-rank max of (dmax, -dmin) (sharded prep_in)
-__global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, unsigned guard) {
-    SKNR_PDL_ENTRY();
-    if (guard_skip(st, guard)) return;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const double mx = st->scratch[2 * dir], mn = -st->scratch[2 * dir + 1];
-    st->dmax[dir] = mx;
-    st->dmin[dir] = mn;
-    const bool ok = st->ref_valid[dir] && (mx - mn) * inv_eps <= spread && isfinite(mx) && isfinite(mn);
-    st->need_exact[dir] = ok ? 0 : 1;
-    st->retry[dir] = 0;
-    if (!ok) st->n_exact[dir] += 1;
 }
 
 }  // namespace sknr

@@ -26,7 +26,6 @@ struct PrepInArgs {
     int dir = 0;
     double* part = nullptr;       // 2*gridDim doubles
     double exact_spread = 600.0;  // (max-min)(v-ref)/eps above which the exact path is forced
-    int defer = 0;                // sharded: leave the decision to k_decide
     DevState* st = nullptr;
     unsigned guard = 0;
 };
@@ -70,6 +69,7 @@ struct FinalizeArgs {
     DevState* st = nullptr;
     unsigned guard = 0;
     double lo_ok = 0x1p-900;  // lse: a sum below this means the bound shift was too loose
+    double* S = nullptr;      // lse (row-sharded column transform): the local sums S_o
 };
 
 // Culling bounds: over permuted positions, the maximum of pack[i*pk] + lskc*sq[i]
@@ -80,6 +80,10 @@ __global__ void k_group_max(const double* pack, int pk, const double* sq, double
                             unsigned* zero_counter, const double* sub = nullptr);
 
 __global__ void k_max_finalize(FinalizeArgs a);
+// Row-sharded column LSE: merge the gathered rank rows X[r] = [shift (m) | S (m)] in rank
+// order: L_j = M_j + log(sum_r S_rj exp(shift_rj - M_j)), M_j = max_r shift_rj; pot = -eps L.
+__global__ void k_lse_merge(const double* X, int world, int64_t m, double eps, double* L, double* pot,
+                            const DevState* st, unsigned guard);
 __global__ void k_lse_finalize(FinalizeArgs a);
 __global__ void k_rsum_finalize(const double* rsum, int64_t n_tiles, int64_t n, double* out, const DevState* st,
                                 unsigned guard);
@@ -149,9 +153,6 @@ struct RedArgs {
 };
 __global__ void k_reduce(RedArgs a);
 __global__ void k_epilogue(DevState* st, int epilogue, int newton, const double* r, unsigned guard);
-__global__ void k_max_local(const double* partial, int64_t nb, int64_t n_out, double* out, DevState* st,
-                            unsigned guard);
-__global__ void k_decide(DevState* st, int dir, double inv_eps, double spread, unsigned guard);
 int reduce_blocks(int64_t T);
 
 }  // namespace sknr

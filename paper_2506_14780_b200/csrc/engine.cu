@@ -77,6 +77,7 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -97,6 +98,7 @@ struct NcclApi {
         CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
         AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
         Broadcast = reinterpret_cast<decltype(Broadcast)>(sym("ncclBroadcast"));
+        AllGather = reinterpret_cast<decltype(AllGather)>(sym("ncclAllGather"));
         GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
         GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
         CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
@@ -312,6 +314,9 @@ struct Problem {
     int rank = 0, world = 1;
     int64_t n_global = 0, row_begin = 0;
     DBuf red_tmp, gather_buf;
+    // sharded column LSE: rank-local LSE of the last pass (bound-shift reference), the
+    // exchange row [shift | S] (2m) and the gathered rows of every rank [R][2m]
+    DBuf L_loc, xrow, xall;
     std::vector<double> h_alpha, h_beta;  // full host copies (validation, host-side dots)
     std::vector<sknr_record> last_trace;  // trace of the last solve / anneal (sknr_last_trace)
 
@@ -603,6 +608,26 @@ static void allreduce(Problem& P, double* buf, size_t count, ncclRedOp_t op) {
     NK(g_nccl.AllReduce(buf, buf, count, ncclDouble, op, g_comm.comm, P.stream));
 }
 
+// All-gather `count` doubles per rank into recv[R][count] (rank order), on the problem's stream.
+static void allgather(Problem& P, const double* send, double* recv, size_t count) {
+    count_collective(count * sizeof(double) * static_cast<size_t>(P.world));
+    if (P.emu) {
+        {
+            std::lock_guard<std::mutex> lk(g_emu.mu);
+            g_emu.locals[P.rank] = send;
+            g_emu.bufs.buf[P.rank] = recv;
+        }
+        g_emu.meet(P.rank, P.stream, [&] {
+            for (int q = 0; q < g_emu.world; ++q)
+                for (int r = 0; r < g_emu.world; ++r)
+                    CK(cudaMemcpyAsync(g_emu.bufs.buf[r] + q * count, g_emu.locals[q], sizeof(double) * count,
+                                       cudaMemcpyDeviceToDevice, g_emu.red));
+        });
+        return;
+    }
+    NK(g_nccl.AllGather(send, recv, count, ncclDouble, g_comm.comm, P.stream));
+}
+
 // Upload the local row block of a full-length, `cols`-column column-major host array.
 static void upload_rows(Problem& P, double* dev, const double* host_full, int64_t cols = 1) {
     for (int64_t c = 0; c < cols; ++c)
@@ -743,6 +768,22 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     const bool cull = cull_active(P, dir);
     const bool f32 = P.precision == 32;
     const TilePlan tsum = plan_for(P, dir, sum_mode(P, dir), 0);
+    // Row-sharded column transform: every rank runs the whole single-GPU
+    // pipeline on its own rows -- its own bound-shift / exact-max decision, shift and
+    // validity retry, all rank-local (no collective inside the guarded branches) -- and
+    // ends with its (shift_j, S_j) per column. ONE all-gather of those 2m doubles per rank
+    // and a fixed rank-order merge L_j = M_j + log(sum_r S_rj e^{shift_rj - M_j}),
+    // M_j = max_r shift_rj, give every rank the same global transform.
+    const bool split = P.shard && dir == 0;
+    double* Lbuf = P.L[dir].p;
+    double* shift = P.shift[dir].p;
+    if (split) {
+        P.L_loc.ensure(nout);
+        P.xrow.ensure(2 * nout);
+        P.xall.ensure(2 * nout * P.world);
+        Lbuf = P.L_loc.p;
+        shift = P.xrow.p;
+    }
 
     PrepInArgs pi;
     pi.count = nin;
@@ -761,19 +802,12 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     pi.part = P.stats.p;
     pi.st = P.st;
     pi.guard = guard;
-    const bool split = P.shard && dir == 0;  // column transform reduces over sharded rows
-    pi.defer = split ? 1 : 0;
     // fp32 terms underflow below 2^-126: take the exact shift once the bound could sit
     // more than 40 nats (58 bits) above the true maximum
     if (f32) pi.exact_spread = 40.0;
     const int gin = std::min(grid_for(nin), 148 * 8);
     count_launch();
     k_prep_in<<<gin, AUX_NT, 0, s>>>(pi);
-    if (split) {
-        allreduce(P, &P.st->scratch[2 * dir], 2, ncclMax);  // (max df, -min df) over all rows
-        count_launch();
-        k_decide<<<1, 32, 0, s>>>(P.st, dir, P.inv_eps(), pi.exact_spread, guard);
-    }
 
     PrepOutArgs po;
     po.count = nout;
@@ -785,8 +819,8 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     po.kc = P.kc();
     po.sigma = P.sigma();
     po.shift_mode = SHIFT_BOUND;
-    po.Lref = P.L[dir].p;
-    po.shift = P.shift[dir].p;
+    po.Lref = Lbuf;
+    po.shift = shift;
     po.pack = P.pack_out[dir].p;
     po.dir = dir;
     po.st = P.st;
@@ -799,14 +833,15 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
     FinalizeArgs fa;
     fa.partial = P.partial.p;
     fa.n_out = nout;
-    fa.shift = P.shift[dir].p;
+    fa.shift = shift;
     fa.pack = P.pack_out[dir].p;
     fa.pk = P.pk();
     fa.sq = P.otf() ? out.sq.p : nullptr;
     fa.kc = P.kc();
     fa.eps = P.eps;
-    fa.L = P.L[dir].p;
-    fa.pot = pot;
+    fa.L = Lbuf;
+    fa.pot = split ? nullptr : pot;
+    fa.S = split ? P.xrow.p + nout : nullptr;
     fa.dir = dir;
     fa.st = P.st;
     if (f32) fa.lo_ok = 0x1p-60;  // smallest sum whose leading fp32 terms are still normal
@@ -818,14 +853,6 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         fa.partial = P.partial.p;
         fa.nb = tmax.n_in_blocks;
         fa.guard = gmax;
-        if (split) {  // local column maxima -> max over ranks -> shift
-            count_launch();
-            k_max_local<<<fold_grid(nout), AUX_NT, 0, s>>>(P.partial.p, tmax.n_in_blocks, nout, P.red_tmp.p,
-                                                         P.st, gmax);
-            allreduce(P, P.red_tmp.p, nout, ncclMax);
-            fa.partial = P.red_tmp.p;
-            fa.nb = 1;
-        }
         count_launch();
         k_max_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(fa);
         if (cull) {  // output-group maxima of S with this phase's shift
@@ -841,16 +868,14 @@ static void lse(Problem& P, int dir, const double* in_vec, double* pot, unsigned
         fa.nb = tsum.n_in_blocks;
         fa.guard = gsum;
         fa.retry_phase = phase;
-        if (split) {  // local column sums share one shift per column: plain sum over ranks
-            count_launch();
-            k_sum_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(P.partial.p, tsum.n_in_blocks, nout, nullptr,
-                                                            P.red_tmp.p, P.st, gsum);
-            allreduce(P, P.red_tmp.p, nout, ncclSum);
-            fa.partial = P.red_tmp.p;
-            fa.nb = 1;
-        }
         count_launch();
         k_lse_finalize<<<fold_grid(nout), AUX_NT, 0, s>>>(fa);
+    }
+    if (split) {
+        allgather(P, P.xrow.p, P.xall.p, static_cast<size_t>(2 * nout));
+        count_launch();
+        k_lse_merge<<<grid_for(nout), AUX_NT, 0, s>>>(P.xall.p, P.world, nout, P.eps, P.L[dir].p, pot, P.st,
+                                                      guard);
     }
     count_launch();
     k_lse_commit<<<grid_for(nin), AUX_NT, 0, s>>>(in_vec, P.ref[dir].p, nin, dir, P.st, guard);
@@ -876,6 +901,15 @@ struct PassSpec {
     unsigned guard = 0;
 };
 
+// Input-block cap of a pass's split-K partials: the ell-wide block passes keep at most 8
+// (their partials are kt x n_out each); sum passes and the 2-column register pass are
+// split like the LSE sums (enough tiles for every SM).
+static int64_t anchor_in_blocks(int kt) { return kt > 2 ? 8 : 0; }
+
+// Columns of the stable accept test's anchor pass W = (1, expm1(d/eps)): the register
+// point kernels take 2 columns with DFMA; the DMMA kernels need a multiple of 8.
+static int anchor_kt(const Problem& P) { return P.dim >= 1 && P.dim <= 4 ? 2 : 8; }
+
 // Whether the block pass can fuse r = P~ beta (register point kernels, d <= 4).
 static bool block_rs_fusable(const Problem& P) { return P.dim >= 1 && P.dim <= 4; }
 
@@ -888,7 +922,7 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     if (rs && (ps.dir != 0 || !block_rs_fusable(P))) throw InvalidArgument("sknr_b200: fused row sums unsupported here");
     const bool bcull = ps.W && !rs && ps.cull && cull_block_active(P, ps.dir);
     const int mode = ps.W ? (rs ? MODE_BLOCK_RS : (bcull ? MODE_BLOCK_CULL : MODE_BLOCK)) : MODE_SUM;
-    const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, ps.W ? 8 : 0);
+    const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, anchor_in_blocks(ps.W ? ps.kt : 0));
 
     PrepInArgs pi;
     pi.count = nin;

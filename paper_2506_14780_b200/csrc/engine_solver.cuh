@@ -179,8 +179,9 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         if (stable) {
             const unsigned gst = gn | G_NOLIT;
             count_launch();
+            const int akt = anchor_kt(P);
             k_fcand_step<<<grid_for(n), AUX_NT, 0, s>>>(S.f.p, S.V.p, n, l, S.delta.p, P.inv_eps(), S.fcand.p,
-                                                        S.dvec.p, S.Wst.p, 8, P.st, gn);
+                                                        S.dvec.p, S.Wst.p, akt, P.st, gn);
             {
                 RedArgs ra;
                 ra.T[0] = n;
@@ -212,7 +213,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             tp.out_v = S.h.p;
             tp.W = S.Wst.p;
             tp.k = 2;
-            tp.kt = 8;
+            tp.kt = akt;
             tp.out = S.ST.p;
             tp.guard = gst;
             plan_pass(P, tp);  // sums over the row shards
@@ -308,11 +309,12 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
         plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
         if (accept == 1) {  // stable accept test: anchor pass with W = (1, expm1(d/eps))
+            const int akt = anchor_kt(P);
             S.dvec.ensure(n);
-            S.Wst.ensure(n * 8);
+            S.Wst.ensure(n * akt);
             S.ST.ensure(2 * m);
             S.dh.ensure(m);
-            plan_for(P, 0, MODE_BLOCK, 8, 8);
+            plan_for(P, 0, MODE_BLOCK, akt, anchor_in_blocks(akt));
         }
     }
     plan_for(P, 0, MODE_SUM, 0);

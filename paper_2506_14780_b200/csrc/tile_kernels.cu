@@ -25,6 +25,8 @@
 // transform, C^T for the column transform), so a warp's 32 loads of one input
 // are one coalesced 256 B request and every fp64 cost element is read once per
 // pass: 8 B/cell, the HBM roofline of BASELINE.md section 4.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace sknr {
@@ -36,6 +38,15 @@ __constant__ unsigned long long c_exp2_tab[kTabEntries] = {
 #include "exp2_table.inc"
 #endif
 };
+
+#if SKNR_TB != 10
+// 2^(e/1024) mantissas for the 1024-entry LSE sum kernel (pts_sum10_kernel)
+__constant__ unsigned long long c_exp2_tab10[1024] = {
+#include "exp2_table1024.inc"
+};
+#else
+#define c_exp2_tab10 c_exp2_tab
+#endif
 
 // Fill the replicated table: tab[e*kTabRep + r] = mantissa bits of 2^(e/2^kTB).
 __device__ __forceinline__ void load_exp2_table(unsigned long long* tab, int tid, int nthreads) {
@@ -159,6 +170,108 @@ __global__ void __launch_bounds__(NTT, MINB) pts_tile_kernel(TileArgs a) {
                 a.partial[ib * a.n_out + o[jt]] = acc[jt][0];
             }
         }
+    }
+}
+
+// ------------------------------------------------------------- LSE sum pass, 1024-entry table
+// MODE_SUM with one FP64 slot fewer per cell than pts_tile_kernel: 2^(u/256) is evaluated
+// as 2^(u'/1024), u' = 4u, from a 1024-entry table of 2^(e/1024) and a degree-3 minimax
+// polynomial of 2^(r/1024), |r| <= 1/2 (max rel. error 1.4e-16; the degree-4 Taylor form
+// of the 256-entry table is 4e-17):
+//   per cell 1 DADD + D DFMA (u') + 3 DADD (Cody-Waite) + 3 DFMA (p) + 1 DFMA (acc) = 10 (d=2)
+// u' costs nothing extra: the inputs are scaled by (4, 2, 2, ..) while they are staged into
+// shared memory (A' = 4A, X' = 2X) and the outputs by the same factors when loaded into
+// registers (B' = 4B, Y' = 2Y) -- powers of two, exact. The table is replicated 16x (one
+// copy per lane of a half-warp: conflict-free LDS.64), which takes 128 KiB of shared
+// memory: one 512-thread CTA per SM (16 warps, as two 256-thread CTAs of the 256-entry
+// kernel). Partials are the same sums in the same [ib][n_out] layout.
+constexpr int kTab10Rep = 16;
+constexpr int kTab10Words = 1024 * kTab10Rep;
+constexpr double kMagic10 = 6755399442103296.0;  // 1.5 * 2^52 + 1023 * 1024
+constexpr double kQ1 = 0.0006769015435155716;   // minimax 2^(r/1024) = 1 + r(q1 + r(q2 + r q3))
+constexpr double kQ2 = 2.29097851993791e-07;
+constexpr double kQ3 = 5.1692229383458926e-11;
+static __constant__ double c_pexp10_k[4] = {kMagic10, kQ1, kQ2, kQ3};
+
+__device__ __forceinline__ double pexp10_acc(double u, const unsigned long long* __restrict__ tab,
+                                             unsigned laneoff, double q2, double acc) {
+    const double t = u + c_pexp10_k[0];
+    const double kf = t - c_pexp10_k[0];
+    const double r = u - kf;
+    double p = fma(r, c_pexp10_k[3], q2);
+    p = fma(p, r, c_pexp10_k[1]);
+    p = fma(p, r, 1.0);
+    // biased k = round(u') + 1023*1024 from the magic sum's low word, flushed at 0 (terms
+    // below 2^-1023 underflow to zero, as in pexp_parts)
+    const int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
+    const unsigned s = static_cast<unsigned>(kc) << 10;
+    const unsigned off = ((static_cast<unsigned>(kc) << 7) & (1023u << 7)) | laneoff;
+    const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
+    const double Tp = __hiloint2double(static_cast<int>((s & 0xFFF00000u) | T.y), static_cast<int>(T.x));
+    return fma(Tp, p, acc);
+}
+
+template <int D, int JT, int NTT>
+__global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int NT = NTT;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int CH = 256;
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + kTab10Words;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < kTab10Words; t += NT) tab[t] = c_exp2_tab10[t / kTab10Rep];
+    const unsigned laneoff = (tid & (kTab10Rep - 1)) << 3;
+    double q2 = kQ2;
+    asm volatile("" : "+d"(q2));
+    const int64_t out_tile = static_cast<int64_t>(NT) * JT;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        double B[JT], Y[JT][D], acc[JT];
+        int64_t o[JT];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            o[jt] = ot * out_tile + jt * NT + tid;
+            const int64_t oc = o[jt] < a.n_out ? o[jt] : a.n_out - 1;
+            B[jt] = 4.0 * a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Y[jt][d] = 2.0 * a.out_pack[oc * PK + 1 + d];
+            acc[jt] = 0.0;
+        }
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+            const int cnt = static_cast<int>((i1 - c0) < CH ? (i1 - c0) : CH);
+            __syncthreads();
+            for (int t = tid; t < cnt * PK; t += NT) {
+                const int q = t % PK;
+                sin[t] = (q == 0 ? 4.0 : 2.0) * a.in_pack[c0 * PK + t];
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int k = 0; k < cnt; ++k) {
+                double x[PK];
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(sin + k * PK)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    double u = x[0] + B[jt];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
+                    acc[jt] = pexp10_acc(u, tab, laneoff, q2, acc[jt]);
+                }
+            }
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+            if (o[jt] < a.n_out) a.partial[ib * a.n_out + o[jt]] = acc[jt];
     }
 }
 
@@ -855,6 +968,202 @@ __global__ void __launch_bounds__(MMA_NT) pts_mma_kernel(TileArgs a) {
     }
 }
 
+// ------------------------------------------------------------- block pass v2 (double-buffered)
+// Same arithmetic as pts_mma_kernel (DMMA m8n8k4 over the cell values e(o, in) generated in
+// registers, optional fused RS row sums), restructured for the FP64 pipe:
+//  * the input chunks (pack rows and W rows) are staged with cp.async into a double
+//    buffer, so chunk c+1 streams in from L2 while chunk c is multiplied (one barrier per
+//    chunk; the staging latency no longer stalls the CTA's warps);
+//  * the work stream runs across tiles (the next tile's first chunk is prefetched during
+//    the current tile's last chunk);
+//  * NW warps per CTA share each staged chunk (NW = 8: 256-output tiles, half the
+//    r-partial rows of the 128-output v1 tiles);
+//  * RS warp sums are double-buffered by chunk parity, so the cross-warp combine of chunk
+//    c (after the next barrier) never races the warps writing chunk c+1.
+// Tail chunks are zero-filled (cp.async src-size 0): padded inputs have W = 0 and add 0
+// to S; their RS slots are never written.
+__device__ __forceinline__ void cp_async16_zfill(double* smem_dst, const double* gmem_src, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "r"(src_bytes)
+                 : "memory");
+}
+
+template <int D, int KT, int MB, bool RS, int MCH, int NW>
+struct Mma2Layout {
+    static constexpr int PK = PK_of<D>::value;
+    static constexpr int WS = WStride<KT>::value;
+    static constexpr int BUF = MCH * PK + MCH * WS;  // doubles per stage
+    static constexpr int RS_LD = MCH + 4;
+    static constexpr int words = kTabWords + 2 * BUF + (RS ? NW * 8 * RS_LD + 2 * NW * MCH : 0);
+};
+
+template <int D, int KT, int MB, bool RS, int MCH, int NW>
+__global__ void __launch_bounds__(NW * 32) pts_mma2_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(a.st, a.guard)) return;
+    using L = Mma2Layout<D, KT, MB, RS, MCH, NW>;
+    constexpr int NT = NW * 32;
+    constexpr int PK = L::PK;
+    constexpr int WS = L::WS;
+    constexpr int NCB = KT / 8;
+    constexpr int OUT_WARP = 8 * MB;
+    constexpr int OUT_CTA = OUT_WARP * NW;
+    constexpr int RS_LD = L::RS_LD;
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* stage = sm + kTabWords;
+    double* srs = stage + 2 * L::BUF;     // RS: [NW*8][RS_LD] per-lane partials of one chunk
+    double* srw = srs + NW * 8 * RS_LD;   // RS: [2][NW][MCH] warp sums, by chunk parity
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = lane >> 2, kq = lane & 3;
+    if (static_cast<int64_t>(blockIdx.x) >= a.n_tiles) return;
+    load_exp2_table(tab, tid, NT);
+    const unsigned laneoff = (lane & (kTabRep - 1)) << 3;
+    const double c3 = pexp_c3();
+
+    auto blk_begin = [&](int64_t t) { return (t / a.n_out_tiles) * a.in_block; };
+    auto blk_end = [&](int64_t t) {
+        const int64_t e = blk_begin(t) + a.in_block;
+        return e < a.n_in ? e : a.n_in;
+    };
+    auto issue = [&](int64_t t, int64_t c0, int b) {
+        const int64_t c1 = blk_end(t);
+        const int cnt = static_cast<int>((c1 - c0) < MCH ? (c1 - c0) : MCH);
+        double* sin = stage + b * L::BUF;
+        double* sw = sin + MCH * PK;
+        for (int g = tid; g < MCH * PK / 2; g += NT) {
+            const int k = g / (PK / 2);
+            const bool ok = k < cnt;
+            cp_async16_zfill(sin + 2 * g, a.in_pack + (c0 + (ok ? k : 0)) * PK + 2 * (g % (PK / 2)), ok ? 16 : 0);
+        }
+        for (int g = tid; g < MCH * KT / 2; g += NT) {
+            const int k = g / (KT / 2), c2 = g % (KT / 2);
+            const bool ok = k < cnt;
+            cp_async16_zfill(sw + k * WS + 2 * c2, a.W + (c0 + (ok ? k : 0)) * KT + 2 * c2, ok ? 16 : 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    int64_t tile = blockIdx.x, c0 = blk_begin(tile);
+    issue(tile, c0, 0);
+    int buf = 0;
+    double Bo[MB], Yo[MB][D], Bw[MB];
+    double acc[MB][NCB][2];
+    auto begin_tile = [&](int64_t t) {
+        const int64_t obase = (t % a.n_out_tiles) * OUT_CTA + warp * OUT_WARP;
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            int64_t o = obase + mb * 8 + row;
+            if (RS) Bw[mb] = o < a.n_out ? a.out_w[o] : 0.0;
+            o = o < a.n_out ? o : a.n_out - 1;
+            Bo[mb] = a.out_pack[o * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Yo[mb][d] = a.out_pack[o * PK + 1 + d];
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) acc[mb][cb][0] = acc[mb][cb][1] = 0.0;
+        }
+    };
+    begin_tile(tile);
+    // RS: the chunk whose warp sums (srw[parity]) await the cross-warp combine
+    int pend = 0, pbuf = 0;
+    int64_t pbase = 0, pot = 0;
+    auto rs_combine = [&]() {
+        const double* w = srw + pbuf * NW * MCH;
+        for (int k = tid; k < pend; k += NT) {
+            double v = w[k];
+#pragma unroll
+            for (int q = 1; q < NW; ++q) v += w[q * MCH + k];
+            a.rsum[pot * a.n_in + pbase + k] = v;
+        }
+        pend = 0;
+    };
+
+    while (true) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // chunk `buf` landed for every thread; all reads of buf^1 are done
+        if (RS && pend) rs_combine();
+        // next work item: the following chunk of this tile, else the first chunk of the next tile
+        const int64_t c1 = blk_end(tile);
+        int64_t ntile = tile, nc0 = c0 + MCH;
+        if (nc0 >= c1) {
+            ntile = tile + gridDim.x;
+            nc0 = ntile < a.n_tiles ? blk_begin(ntile) : 0;
+        }
+        if (ntile < a.n_tiles) issue(ntile, nc0, buf ^ 1);
+        const int cnt = static_cast<int>((c1 - c0) < MCH ? (c1 - c0) : MCH);
+        const int cnt4 = (cnt + 3) & ~3;
+        const double* sin = stage + buf * L::BUF;
+        const double* sw = sin + MCH * PK;
+        double* srs_w = srs + warp * 8 * RS_LD;
+        for (int k4 = 0; k4 < cnt4; k4 += 4) {
+            const double* xin = sin + (k4 + kq) * PK;
+            double x[PK];
+#pragma unroll
+            for (int q = 0; q < PK / 2; ++q) {
+                const double2 v = reinterpret_cast<const double2*>(xin)[q];
+                x[2 * q] = v.x;
+                x[2 * q + 1] = v.y;
+            }
+            double bf[NCB];
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) bf[cb] = sw[(k4 + kq) * WS + cb * 8 + row];
+            double rt = 0.0;
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+                double u = x[0] + Bo[mb];
+#pragma unroll
+                for (int d = 0; d < D; ++d) u = fma(x[1 + d], Yo[mb][d], u);
+                const double e = pexp<true>(u, tab, laneoff, c3);
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) dmma_8x8x4(acc[mb][cb][0], acc[mb][cb][1], e, bf[cb]);
+                if (RS) rt = mb == 0 ? e * Bw[0] : fma(e, Bw[mb], rt);
+            }
+            if (RS) srs_w[row * RS_LD + k4 + kq] = rt;
+        }
+        if (RS) {
+            __syncwarp();
+            double* w = srw + buf * NW * MCH + warp * MCH;
+#pragma unroll
+            for (int h = 0; h < MCH / 32; ++h) {
+                const int k = lane + 32 * h;
+                const double s01 = srs_w[k] + srs_w[RS_LD + k], s23 = srs_w[2 * RS_LD + k] + srs_w[3 * RS_LD + k];
+                const double s45 = srs_w[4 * RS_LD + k] + srs_w[5 * RS_LD + k];
+                const double s67 = srs_w[6 * RS_LD + k] + srs_w[7 * RS_LD + k];
+                w[k] = (s01 + s23) + (s45 + s67);
+            }
+            __syncwarp();
+            pend = cnt;
+            pbuf = buf;
+            pbase = c0;
+            pot = tile % a.n_out_tiles;
+        }
+        if (ntile != tile) {  // tile done: its split-K partial of S
+            const int64_t ib = tile / a.n_out_tiles;
+            const int64_t obase = (tile % a.n_out_tiles) * OUT_CTA + warp * OUT_WARP;
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+                const int64_t o = obase + mb * 8 + row;
+                if (o >= a.n_out) continue;
+#pragma unroll
+                for (int cb = 0; cb < NCB; ++cb) {
+                    const int c = cb * 8 + kq * 2;
+                    a.partial[(ib * KT + c) * a.n_out + o] = acc[mb][cb][0];
+                    a.partial[(ib * KT + c + 1) * a.n_out + o] = acc[mb][cb][1];
+                }
+            }
+            if (ntile >= a.n_tiles) break;
+            begin_tile(ntile);
+        }
+        tile = ntile;
+        c0 = nc0;
+        buf ^= 1;
+    }
+    if (RS) {
+        __syncthreads();
+        rs_combine();
+    }
+}
+
 // Culled block pass (opt-in, see pts_cull_kernel): work unit = (32 Morton-ordered
 // outputs, input block), taken from a queue by each warp; inputs are tested in
 // groups of 32 against the unit's box with the output-normalised bound
@@ -1452,6 +1761,16 @@ KernelInfo make_pts() {
     return k;
 }
 
+template <int D, int JT, int NTT>
+KernelInfo make_sum10() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_sum10_kernel<D, JT, NTT>);
+    k.jt = JT;
+    k.nt = NTT;
+    k.smem = static_cast<int>(sizeof(double)) * (kTab10Words + 256 * PK_of<D>::value);
+    return k;
+}
+
 template <int D, int JT, int NTT, int MINB = 1>
 KernelInfo make_f32() {
     KernelInfo k;
@@ -1494,6 +1813,17 @@ KernelInfo make_mma() {
     k.out_tile = 8 * MB * (MMA_NT / 32);
     k.smem = static_cast<int>(sizeof(double)) * (kTabWords + MCH * PK_of<D>::value + MCH * WStride<KT>::value +
                                                  (RS ? (MMA_NT / 32) * (8 * (MCH + 4) + MCH) : 0));
+    return k;
+}
+
+template <int D, int KT, int MB, bool RS, int MCH, int NW>
+KernelInfo make_mma2() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_mma2_kernel<D, KT, MB, RS, MCH, NW>);
+    k.jt = 1;
+    k.nt = NW * 32;
+    k.out_tile = 8 * MB * NW;
+    k.smem = static_cast<int>(sizeof(double)) * Mma2Layout<D, KT, MB, RS, MCH, NW>::words;
     return k;
 }
 
@@ -1561,26 +1891,55 @@ KernelInfo pick_pts(int mode, int kt) {
             default: return KernelInfo{};
         }
     }
-    if (mode == MODE_BLOCK_RS) {  // 32-input rounds: 4 CTAs/SM fit (C4 ell=32: 13.9 ms vs 14.1 ms at 64)
+    if (mode == MODE_BLOCK && kt == 2)  // two-column block (stable accept test's anchor pass): DFMA
+        return make_pts<D, 8, MODE_BLOCK, 2, 256, 1>();
+    // FP64 tensor-core (DMMA) block passes. Default: the double-buffered v2 kernel (8 warps,
+    // 256-output tiles, 32-input chunks); SKNR_BLOCK_V1=1 selects the round-1 kernel.
+    static const bool v1 = std::getenv("SKNR_BLOCK_V1") != nullptr;
+    if (mode == MODE_BLOCK_RS) {
+        if (v1) {  // 32-input rounds: 4 CTAs/SM fit (C4 ell=32: 13.9 ms vs 14.1 ms at 64)
+            switch (kt) {
+                case 8: return make_mma<D, 8, 4, true, 32>();
+                case 16: return make_mma<D, 16, 4, true, 32>();
+                case 24: return make_mma<D, 24, 4, true, 32>();
+                case 32: return make_mma<D, 32, 4, true, 32>();
+                case 40: return make_mma<D, 40, 4, true, 32>();
+                case 48: return make_mma<D, 48, 2, true, 32>();
+                case 64: return make_mma<D, 64, 2, true, 32>();
+                default: return KernelInfo{};
+            }
+        }
         switch (kt) {
-            case 8: return make_mma<D, 8, 4, true, 32>();
-            case 16: return make_mma<D, 16, 4, true, 32>();
-            case 24: return make_mma<D, 24, 4, true, 32>();
-            case 32: return make_mma<D, 32, 4, true, 32>();
-            case 40: return make_mma<D, 40, 4, true, 32>();
-            case 48: return make_mma<D, 48, 2, true, 32>();
-            case 64: return make_mma<D, 64, 2, true, 32>();
+            case 8: return make_mma2<D, 8, 4, true, 32, 8>();
+            case 16: return make_mma2<D, 16, 4, true, 32, 8>();
+            case 24: return make_mma2<D, 24, 4, true, 32, 8>();
+            case 32: return make_mma2<D, 32, 4, true, 32, 8>();
+            case 40: return make_mma2<D, 40, 4, true, 32, 8>();
+            case 48: return make_mma2<D, 48, 2, true, 32, 8>();
+            case 64: return make_mma2<D, 64, 2, true, 32, 8>();
             default: return KernelInfo{};
         }
     }
-    switch (kt) {  // FP64 tensor-core (DMMA) block pass, 4 x 8-output blocks per warp
-        case 8: return make_mma<D, 8, 4>();
-        case 16: return make_mma<D, 16, 4>();
-        case 24: return make_mma<D, 24, 4>();
-        case 32: return make_mma<D, 32, 4>();
-        case 40: return make_mma<D, 40, 4>();
-        case 48: return make_mma<D, 48, 2>();
-        case 64: return make_mma<D, 64, 2>();
+    if (v1) {
+        switch (kt) {  // 4 x 8-output blocks per warp
+            case 8: return make_mma<D, 8, 4>();
+            case 16: return make_mma<D, 16, 4>();
+            case 24: return make_mma<D, 24, 4>();
+            case 32: return make_mma<D, 32, 4>();
+            case 40: return make_mma<D, 40, 4>();
+            case 48: return make_mma<D, 48, 2>();
+            case 64: return make_mma<D, 64, 2>();
+            default: return KernelInfo{};
+        }
+    }
+    switch (kt) {
+        case 8: return make_mma2<D, 8, 4, false, 32, 8>();
+        case 16: return make_mma2<D, 16, 4, false, 32, 8>();
+        case 24: return make_mma2<D, 24, 4, false, 32, 8>();
+        case 32: return make_mma2<D, 32, 4, false, 32, 8>();
+        case 40: return make_mma2<D, 40, 4, false, 32, 8>();
+        case 48: return make_mma2<D, 48, 2, false, 32, 8>();
+        case 64: return make_mma2<D, 64, 2, false, 32, 8>();
         default: return KernelInfo{};
     }
 }
@@ -1655,6 +2014,13 @@ KernelInfo tune_variant(int v) {
         case 24: return make_pts<2, 8, MODE_SUM, 0, 256, 1, false, 2>();
         case 25: return make_pts<2, 8, MODE_SUM, 0, 128, 1, false, 4>();
         case 26: return make_pts<2, 6, MODE_SUM, 0, 256, 1, false, 2>();
+        // 1024-entry table, 10 FP64 slots per cell (pts_sum10_kernel <D, JT, threads>)
+        case 40: return make_sum10<2, 8, 512>();
+        case 41: return make_sum10<2, 4, 512>();
+        case 42: return make_sum10<2, 8, 256>();
+        case 43: return make_sum10<2, 6, 512>();
+        case 44: return make_sum10<2, 12, 256>();
+        case 45: return make_sum10<2, 8, 384>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();
@@ -1673,6 +2039,14 @@ KernelInfo tune_variant(int v) {
         case 205: return make_mma<2, 32, 2, true>();
         case 206: return make_mma<2, 32, 4, true, 32>();
         case 207: return make_mma<2, 32, 4, false, 32>();
+        // double-buffered v2 (pts_mma2_kernel): <D, KT, MB, RS, MCH, NW>
+        case 210: return make_mma2<2, 32, 4, true, 32, 8>();
+        case 211: return make_mma2<2, 32, 4, true, 32, 4>();
+        case 212: return make_mma2<2, 32, 2, true, 32, 8>();
+        case 213: return make_mma2<2, 32, 4, false, 32, 8>();
+        case 214: return make_mma2<2, 32, 4, true, 64, 4>();
+        case 215: return make_mma2<2, 32, 2, true, 64, 8>();
+        case 216: return make_mma2<2, 32, 4, false, 64, 4>();
         // fp32 sum pass (MUFU ex2), d=2
         case 300: return make_f32<2, 8, 256>();
         case 301: return make_f32<2, 4, 256>();
