@@ -13,8 +13,8 @@
 // (3 DADD), a degree-4 polynomial for 2^(r/256), |r| <= 1/2 (4 DFMA,
 // truncation < 4e-17), and a 256-entry table of 2^(e/256) whose biased
 // exponent field (k>>8)+1023 is OR-ed in with integer ops (no FP64 slot).
-// The table is stored with the exponent field cleared and replicated 16x in
-// shared memory, so the 16 lanes of each half-warp hit 16 distinct 8-byte bank
+// The table is stored with the exponent field cleared (and the hi word pre-biased
+// by -(e << (20 - kTB)), see pexp_parts) and replicated 16x in shared memory, so the 16 lanes of each half-warp hit 16 distinct 8-byte bank
 // pairs: a warp's table read is always the minimum 2 wavefronts.
 #pragma once
 #include <cuda_runtime.h>
@@ -159,10 +159,13 @@ __device__ __forceinline__ void pexp_parts(double u, const unsigned long long* _
     int kc = FASTCLAMP ? max(__double2loint(t), 0)
                        : ((__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0);
     if (HI_CLAMP) kc = min(kc, kKcMax);
-    const unsigned s = static_cast<unsigned>(kc) << (20 - kTB);
-    const unsigned off = ((s >> (20 - kTB - kRepShift)) & (((1u << kTB) - 1u) << kRepShift)) | laneoff;
+    const unsigned off = ((static_cast<unsigned>(kc) << kRepShift) & (((1u << kTB) - 1u) << kRepShift)) | laneoff;
     const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
-    Tp = __hiloint2double(static_cast<int>((s & 0xFFF00000u) | T.y), static_cast<int>(T.x));
+    // hi word = biased exponent (kc >> kTB) << 20 | mantissa bits of 2^(e/2^kTB), e = kc mod 2^kTB.
+    // The table's hi words are stored minus e << (20 - kTB) (load_exp2_table), so one IMAD
+    // kc * 2^(20 - kTB) + T.y assembles it (the e part cancels; arithmetic mod 2^32).
+    Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * (1u << (20 - kTB)) + T.y),
+                          static_cast<int>(T.x));
 }
 
 // register-resident first Horner constant for pexp_parts

@@ -49,8 +49,15 @@ __constant__ unsigned long long c_exp2_tab10[1024] = {
 #endif
 
 // Fill the replicated table: tab[e*kTabRep + r] = mantissa bits of 2^(e/2^kTB).
+// The hi word is pre-biased by -(e << (20 - kTB)) (mod 2^32) so that pexp_parts assembles
+// exponent and mantissa with one IMAD.
 __device__ __forceinline__ void load_exp2_table(unsigned long long* tab, int tid, int nthreads) {
-    for (int t = tid; t < kTabWords; t += nthreads) tab[t] = c_exp2_tab[t / kTabRep];
+    for (int t = tid; t < kTabWords; t += nthreads) {
+        const unsigned e = static_cast<unsigned>(t / kTabRep);
+        const unsigned long long v = c_exp2_tab[e];
+        const unsigned hi = static_cast<unsigned>(v >> 32) - (e << (20 - kTB));
+        tab[t] = (static_cast<unsigned long long>(hi) << 32) | (v & 0xFFFFFFFFull);
+    }
 }
 
 namespace {
@@ -204,10 +211,13 @@ __device__ __forceinline__ double pexp10_acc(double u, const unsigned long long*
     // biased k = round(u') + 1023*1024 from the magic sum's low word, flushed at 0 (terms
     // below 2^-1023 underflow to zero, as in pexp_parts)
     const int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
-    const unsigned s = static_cast<unsigned>(kc) << 10;
     const unsigned off = ((static_cast<unsigned>(kc) << 7) & (1023u << 7)) | laneoff;
     const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
-    const double Tp = __hiloint2double(static_cast<int>((s & 0xFFF00000u) | T.y), static_cast<int>(T.x));
+    // hi word = biased exponent (kc >> 10) << 20 | mantissa bits of 2^(e/1024), e = kc & 1023:
+    // the table's hi words are stored minus e << 10, so kc * 1024 + T.y is that word in one
+    // IMAD (the e << 10 part of kc * 1024 cancels; arithmetic mod 2^32)
+    const double Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * 1024u + T.y),
+                                       static_cast<int>(T.x));
     return fma(Tp, p, acc);
 }
 
@@ -222,7 +232,12 @@ __global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
     unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
     double* sin = sm + kTab10Words;
     const int tid = threadIdx.x;
-    for (int t = tid; t < kTab10Words; t += NT) tab[t] = c_exp2_tab10[t / kTab10Rep];
+    for (int t = tid; t < kTab10Words; t += NT) {  // hi word pre-biased by -(e << 10), see pexp10_acc
+        const unsigned e = static_cast<unsigned>(t / kTab10Rep);
+        const unsigned long long v = c_exp2_tab10[e];
+        const unsigned hi = static_cast<unsigned>(v >> 32) - (e << 10);
+        tab[t] = (static_cast<unsigned long long>(hi) << 32) | (v & 0xFFFFFFFFull);
+    }
     const unsigned laneoff = (tid & (kTab10Rep - 1)) << 3;
     double q2 = kQ2;
     asm volatile("" : "+d"(q2));
