@@ -124,6 +124,10 @@ int sknr_restricted_derivatives(sknr_problem p, const double* f, const double* g
                                 double* grad /* ell */, double* hess /* ell x ell */);
 /* dual_value (objective.cpp:10-40): a.f + b.g - eps*expm1(log sum_ij a_i b_j e^{(f_i+g_j-C_ij)/eps}). */
 int sknr_dual_value(sknr_problem p, const double* f, const double* g, double* value);
+/* full_semi_dual_hessian (objective.cpp:150-171): the dense n x n semi-dual Hessian
+ * -(1/eps)(diag(r) - P~ diag(b) P~^T), symmetrised, at g = f^{C,eps}; SKNR_EINVAL when
+ * n > dense_limit (the reference's guard). The plan and the n^2 m product run on the device. */
+int sknr_full_semi_dual_hessian(sknr_problem p, const double* f, int64_t dense_limit, double* hess);
 /* semi_dual_hessian_quadform (objective.cpp:53-77): u^T H(f) u. */
 int sknr_semi_dual_hessian_quadform(sknr_problem p, const double* f, const double* u, double* value);
 

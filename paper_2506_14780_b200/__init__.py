@@ -101,6 +101,7 @@ _SIGS = {
     "sknr_apply_Rt": [_P, _D, _D, _D, _D],
     "sknr_dual_value": [_P, _D, _D, _D],
     "sknr_semi_dual_hessian_quadform": [_P, _D, _D, _D],
+    "sknr_full_semi_dual_hessian": [_P, _D, _I64, _D],
     "sknr_newton_step": [_P, _D, _D, _I64, _D, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
     "sknr_newton_step_ex": [_P, _D, _D, _I64, ctypes.c_int, _D, ctypes.POINTER(ctypes.c_int),
                             ctypes.POINTER(ctypes.c_int)],

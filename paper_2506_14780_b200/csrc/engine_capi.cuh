@@ -407,6 +407,51 @@ int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan
     return sknr_coupling_rows(h, f, g, 0, h && h->p ? h->p->n : 0, plan);
 }
 
+// full_semi_dual_hessian (objective.cpp:150-171): H = -(1/eps)(diag(r) - P~ diag(b) P~^T),
+// symmetrised, with g = f^{C,eps}. The plan and the O(n^2 m) product run on the device.
+int sknr_full_semi_dual_hessian(sknr_problem h, const double* f, int64_t dense_limit, double* hess) {
+    SKNR_API_BEGIN
+    Problem& P0 = get(h);
+    if (P0.n_global > dense_limit) throw InvalidArgument("full_semi_dual_hessian: dense Hessian too large");
+    if (P0.shard) throw RuntimeFailure("full_semi_dual_hessian: not available on a row-sharded problem");
+    std::vector<double> g(P0.m);
+    int rc = sknr_ctransform_of_f(h, f, g.data());
+    if (rc != SKNR_OK) return rc;
+    Problem& P = get(h);
+    std::lock_guard<std::mutex> lk(P.mu);
+    const int64_t n = P.n, m = P.m;
+    DBuf df, dg, dp, dr, dout;
+    df.ensure(n);
+    dg.ensure(m);
+    dp.ensure(n * m);
+    dr.ensure(n);
+    dout.ensure(n * n);
+    upload(df.p, f, n, P.stream);
+    upload(dg.p, g.data(), m, P.stream);
+    count_launch();
+    k_coupling<<<grid_for(n * m), AUX_NT, 0, P.stream>>>(P.kind == 0 || P.C.p ? P.C.p : nullptr, P.src.coords.p,
+                                                         P.tgt.coords.p, n, m, 0, n, static_cast<int>(P.d), P.kappa,
+                                                         P.src.w.p, P.tgt.w.p, df.p, dg.p, P.inv_eps(), dp.p);
+    count_launch();
+    k_row_sums<<<grid_for(n), AUX_NT, 0, P.stream>>>(dp.p, n, m, dr.p);
+    count_launch();
+    k_plan_outer<<<dim3(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((n + 31) / 32)), 256, 0,
+                   P.stream>>>(dp.p, n, m, P.tgt.w.p, dout.p);
+    CK(cudaGetLastError());
+    std::vector<double> outer(static_cast<size_t>(n * n)), r(n);
+    download(outer.data(), dout.p, n * n, P.stream);
+    download(r.data(), dr.p, n, P.stream);
+    CK(cudaStreamSynchronize(P.stream));
+    const double c = -1.0 / P.eps;
+    for (int64_t k = 0; k < n; ++k)
+        for (int64_t i = 0; i < n; ++i) {
+            const double hik = c * ((i == k ? r[i] : 0.0) - outer[i + k * n]);
+            const double hki = c * ((i == k ? r[i] : 0.0) - outer[k + i * n]);
+            hess[i + k * n] = 0.5 * (hik + hki);
+        }
+    SKNR_API_END
+}
+
 int sknr_semi_dual_value(sknr_problem h, const double* f, double* value) {
     SKNR_API_BEGIN
     std::vector<double> g(get(h).m);  // f^{C,eps}, then Q = a.f + b.g (objective.cpp:42-45)

@@ -543,6 +543,51 @@ __global__ void k_build_cost(const double* x, const double* y, int64_t n, int64_
 }
 
 // transpose n x m col-major -> m x n col-major
+// full_semi_dual_hessian (objective.cpp:150-171) on a materialised plan (col-major n x m,
+// plan_ij = P~_ij b_j): out_ik = sum_j plan_ij plan_kj / b_j (= P~ diag(b) P~^T), j ascending
+// within each 32-wide chunk, chunks in order. 32 x 32 output tiles, 256 threads, 4 outputs each.
+__global__ void __launch_bounds__(256) k_plan_outer(const double* plan, int64_t n, int64_t m, const double* b,
+                                                    double* out) {
+    SKNR_PDL_ENTRY();
+    __shared__ double sa[32][33], sb[32][33];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, k0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j0 = 0; j0 < m; j0 += 32) {
+        __syncthreads();
+        for (int q = ty; q < 32; q += 8) {
+            const int64_t j = j0 + q;
+            const bool jv = j < m;
+            const double ib = jv ? 1.0 / b[j] : 0.0;
+            sa[q][tx] = (jv && i0 + tx < n) ? plan[i0 + tx + j * n] : 0.0;
+            sb[q][tx] = (jv && k0 + tx < n) ? plan[k0 + tx + j * n] * ib : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const double av = sa[q][tx];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[t] = fma(av, sb[q][ty + 8 * t], acc[t]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int64_t i = i0 + tx, k = k0 + ty + 8 * t;
+        if (i < n && k < n) out[i + k * n] = acc[t];
+    }
+}
+
+// row sums of a col-major n x m matrix, j ascending
+__global__ void k_row_sums(const double* A, int64_t n, int64_t m, double* out) {
+    SKNR_PDL_ENTRY();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int64_t j = 0; j < m; ++j) s += A[i + j * n];
+        out[i] = s;
+    }
+}
+
 __global__ void k_transpose(const double* A, int64_t n, int64_t m, double* AT) {
     SKNR_PDL_ENTRY();
     __shared__ double tile[32][33];

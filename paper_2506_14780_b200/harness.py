@@ -11,25 +11,20 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import (Problem, coupling, ctransform_of_f, ctransform_of_g, gauge_normalized, marginal_error,
-               plan_marginals, semi_dual_gradient, semi_dual_value)
+from . import (Problem, _check, _ptr, coupling, ctransform_of_f, ctransform_of_g, gauge_normalized, lib,
+               marginal_error, plan_marginals, semi_dual_gradient, semi_dual_value)
 
 
 def full_semi_dual_hessian(problem: Problem, f, dense_limit: int = 2000) -> np.ndarray:
     """Dense n x n semi-dual Hessian -(1/eps)(diag(r) - P~ diag(b) P~^T), symmetrised
-    (objective.cpp:150-171). P~_ij = a_i e^{(f_i+g_j-C_ij)/eps} comes from the
-    device coupling (plan_ij = P~_ij b_j)."""
+    (objective.cpp:150-171): the plan P~_ij b_j and the O(n^2 m) product are computed on
+    the device (sknr_full_semi_dual_hessian); the n x n result comes back to the host."""
     if problem.n > dense_limit:
         raise ValueError("full_semi_dual_hessian: dense Hessian too large")
-    f = np.asarray(f, dtype=np.float64)
-    g = ctransform_of_f(problem, f)
-    plan = coupling(problem, f, g)
-    b = problem.beta
-    pt = plan / b[None, :]
-    r = plan.sum(axis=1)
-    outer = plan @ pt.T
-    hess = (-1.0 / problem.epsilon) * (np.diag(r) - outer)
-    return 0.5 * (hess + hess.T)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.empty((problem.n, problem.n), order="F")
+    _check(lib().sknr_full_semi_dual_hessian(problem.handle, _ptr(f), int(dense_limit), _ptr(out)))
+    return out
 
 
 @dataclass
