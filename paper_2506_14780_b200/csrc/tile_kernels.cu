@@ -200,6 +200,7 @@ constexpr double kQ2 = 2.29097851993791e-07;
 constexpr double kQ3 = 5.1692229383458926e-11;
 static __constant__ double c_pexp10_k[4] = {kMagic10, kQ1, kQ2, kQ3};
 
+template <bool FASTCLAMP = false>
 __device__ __forceinline__ double pexp10_acc(double u, const unsigned long long* __restrict__ tab,
                                              unsigned laneoff, double q2, double acc) {
     const double t = u + c_pexp10_k[0];
@@ -210,7 +211,9 @@ __device__ __forceinline__ double pexp10_acc(double u, const unsigned long long*
     p = fma(p, r, 1.0);
     // biased k = round(u') + 1023*1024 from the magic sum's low word, flushed at 0 (terms
     // below 2^-1023 underflow to zero, as in pexp_parts)
-    const int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
+    // (FASTCLAMP: one IMNMX on the low word, valid while |u'| < 2^31 - 2^20)
+    const int kc = FASTCLAMP ? max(__double2loint(t), 0)
+                             : ((__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0);
     const unsigned off = ((static_cast<unsigned>(kc) << 7) & (1023u << 7)) | laneoff;
     const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
     // hi word = biased exponent (kc >> 10) << 20 | mantissa bits of 2^(e/1024), e = kc & 1023:
@@ -221,7 +224,7 @@ __device__ __forceinline__ double pexp10_acc(double u, const unsigned long long*
     return fma(Tp, p, acc);
 }
 
-template <int D, int JT, int NTT>
+template <int D, int JT, int NTT, bool FC = false>
 __global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
     SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
                     double u = x[0] + B[jt];
 #pragma unroll
                     for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
-                    acc[jt] = pexp10_acc(u, tab, laneoff, q2, acc[jt]);
+                    acc[jt] = pexp10_acc<FC>(u, tab, laneoff, q2, acc[jt]);
                 }
             }
         }
@@ -1776,10 +1779,10 @@ KernelInfo make_pts() {
     return k;
 }
 
-template <int D, int JT, int NTT>
+template <int D, int JT, int NTT, bool FC = false>
 KernelInfo make_sum10() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_sum10_kernel<D, JT, NTT>);
+    k.fn = reinterpret_cast<const void*>(&pts_sum10_kernel<D, JT, NTT, FC>);
     k.jt = JT;
     k.nt = NTT;
     k.smem = static_cast<int>(sizeof(double)) * (kTab10Words + 256 * PK_of<D>::value);
@@ -2036,6 +2039,8 @@ KernelInfo tune_variant(int v) {
         case 43: return make_sum10<2, 6, 512>();
         case 44: return make_sum10<2, 12, 256>();
         case 45: return make_sum10<2, 8, 384>();
+        case 46: return make_sum10<2, 8, 512, true>();
+        case 47: return make_sum10<2, 6, 512, true>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();
