@@ -640,7 +640,7 @@ def run_ours(args, world, rank, local):
                                "note": "2 sweep LSEs + fused V^T P~ / P~ beta pass + candidate column LSE",
                                "stable_accept": {"ms": ms_nr_st, "kernels": kpi_nr_st,
                                                  "note": "candidate column LSE replaced by the anchor pass "
-                                                         "s, t = P~^T (1, expm1(d/eps))"}},
+                                                         "s, t, u = P~^T (1, expm1(d/eps), exp(d/eps))"}},
             "collectives": comm,
             "cpu_time_to_tol": cpu_ttt,
             "pass_ms": {"column_lse_full": ms_pass, "row_lse_full": ms_row_pass,

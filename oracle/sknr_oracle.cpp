@@ -796,34 +796,41 @@ double semi_dual_hessian_quadform(const Problem& p, const Vec& f, const Vec& u) 
 // same predicate as Q(f') - Q(f) > 0, with the difference evaluated directly so its
 // rounding scales with the step, not with |Q|:
 //   d = f' - f,  P~_ij = a_i exp((f_i + h_j - C_ij)/eps)   (h = f^{C,eps}, the anchor)
-//   h'_j - h_j = -eps log1p(t_j / s_j),  s_j = sum_i P~_ij,  t_j = sum_i P~_ij expm1(d_i/eps)
+//   h'_j - h_j = -eps log(u_j / s_j) = -eps log1p(t_j / s_j),
+//   s_j = sum_i P~_ij,  t_j = sum_i P~_ij expm1(d_i/eps),  u_j = sum_i P~_ij exp(d_i/eps)
 //   dQ = a.d + b.(h' - h)
+// log1p(t/s) when |t/s| <= 1/2 (u - s would cancel for small steps), log(u/s) otherwise
+// (1 + t/s cancels when the step moves a column's mass away: t/s -> -1).
 // (exact algebra: sum_i a_i e^{(f'_i - C_ij)/eps} = e^{-h_j/eps} (s_j + t_j)). Steps with
 // max|d|/eps > kStableSpan fall back to the literal test (expm1 would overflow; such
 // steps are never rounding-decided).
 static int g_accept_mode = 0;
 constexpr double kStableSpan = 600.0;
+constexpr double kDhSwitch = 0.5;
 
 static bool stable_delta_q(const Problem& p, const Vec& f, const Vec& h, const Vec& cand, double& dq) {
     const Index n = p.n, m = p.m;
     const double inv_eps = 1.0 / p.eps;
-    Vec dv(n), ev(n);
+    Vec dv(n), ev(n), xv(n);
     double dmax = 0.0;
     for (Index i = 0; i < n; ++i) {
         dv[i] = cand[i] - f[i];
         dmax = std::max(dmax, std::abs(dv[i]));
         ev[i] = std::expm1(dv[i] * inv_eps);
+        xv[i] = std::exp(dv[i] * inv_eps);
     }
-    if (!(dmax * inv_eps <= kStableSpan)) return false;
+    if (!(dmax <= kStableSpan * p.eps)) return false;  // as the GPU (lit_dmax = 600 eps)
     Vec dh(m);
     par_for(m, [&](Index j) {
-        double s = 0.0, t = 0.0;
+        double s = 0.0, t = 0.0, u = 0.0;
         for (Index i = 0; i < n; ++i) {
             const double w = p.a[i] * std::exp((f[i] + h[j] - p.C(i, j)) * inv_eps);
             s += w;
             t += w * ev[i];
+            u += w * xv[i];
         }
-        dh[j] = -p.eps * std::log1p(t / s);
+        const double ts = t / s;
+        dh[j] = -p.eps * (std::abs(ts) <= kDhSwitch ? std::log1p(ts) : std::log(u / s));
     });
     dq = dot(p.a, dv) + dot(p.b, dh);
     return true;

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <map>
+#include <set>
 #include <tuple>
 #include <unordered_map>
 #include <cmath>
@@ -214,19 +215,42 @@ static cudaStream_t alloc_stream() {
     return s;
 }
 
+// Frees are stream-ordered on the stream of the problem that used the buffer (no
+// device-wide barrier): every API entry point makes its problem's stream this thread's
+// owner stream (own_stream), and a buffer allocated under it is returned to the pool
+// after the work already queued there. Streams are registered while alive, so a buffer
+// never frees on a destroyed stream (unowned buffers -- host-synchronised temporaries --
+// free on the allocation stream).
+static std::mutex g_live_mu;
+static std::set<cudaStream_t> g_live_streams;
+static thread_local cudaStream_t tl_owner = nullptr;
+static void own_stream(cudaStream_t s) { tl_owner = s; }
+static cudaStream_t live_owner() {
+    if (!tl_owner) return nullptr;
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    return g_live_streams.count(tl_owner) ? tl_owner : nullptr;
+}
+
 struct DBuf {
     double* p = nullptr;
     size_t n = 0;
+    cudaStream_t owner = nullptr;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { release(); }
-    // Returns the memory to the pool once no stream can still use it.
+    // Returns the memory to the pool after the work queued on the owner stream.
     void release() {
         if (!p) return;
-        if (cudaDeviceSynchronize() == cudaSuccess) cudaFreeAsync(p, alloc_stream());
+        cudaStream_t o = owner;
+        if (o) {
+            std::lock_guard<std::mutex> lk(g_live_mu);
+            if (!g_live_streams.count(o)) o = nullptr;  // its problem is gone (and was synchronised)
+        }
+        cudaFreeAsync(p, o ? o : alloc_stream());
         p = nullptr;
         n = 0;
+        owner = nullptr;
     }
     // Grows (never inside stream capture). The zero fill is complete before
     // returning: the problem streams are non-blocking, so the allocation stream's
@@ -240,6 +264,7 @@ struct DBuf {
         CK(cudaMemsetAsync(p, 0, bytes, s));
         CK(cudaStreamSynchronize(s));
         n = count;
+        owner = live_owner();
     }
 };
 
@@ -276,7 +301,15 @@ struct Side {
 
 struct SolveState;
 
+struct StreamReaper {
+    cudaStream_t s = nullptr;
+    ~StreamReaper() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
 struct Problem {
+    StreamReaper reaper;  // first member: destroyed after every DBuf member
     int kind = 0;  // 0 dense, 1 points
     int64_t n = 0, m = 0, d = 0;
     double eps = 1.0, kappa = 1.0;
@@ -301,7 +334,14 @@ struct Problem {
     std::mutex mu;
 
     ~Problem() {
-        if (stream) cudaStreamDestroy(stream);
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            std::lock_guard<std::mutex> lk(g_live_mu);
+            g_live_streams.erase(stream);
+        }
+        if (tl_owner == stream) tl_owner = nullptr;
+        // the member buffers free after this body (the stream is idle and unregistered, so
+        // on the allocation stream); the stream itself goes last (StreamReaper)
         if (st) cudaFree(st);
         if (st_host) cudaFreeHost(st_host);
     }
@@ -387,6 +427,12 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     p->m = m;
     p->eps = eps;
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->reaper.s = p->stream;
+    {
+        std::lock_guard<std::mutex> lk(g_live_mu);
+        g_live_streams.insert(p->stream);
+    }
+    own_stream(p->stream);
     CK(cudaMalloc(&p->st, sizeof(DevState)));
     CK(cudaMemset(p->st, 0, sizeof(DevState)));
     CK(cudaDeviceSynchronize());
@@ -906,9 +952,9 @@ struct PassSpec {
 // split like the LSE sums (enough tiles for every SM).
 static int64_t anchor_in_blocks(int kt) { return kt > 2 ? 8 : 0; }
 
-// Columns of the stable accept test's anchor pass W = (1, expm1(d/eps)): the register
-// point kernels take 2 columns with DFMA; the DMMA kernels need a multiple of 8.
-static int anchor_kt(const Problem& P) { return P.dim >= 1 && P.dim <= 4 ? 2 : 8; }
+// Columns of the stable accept test's anchor pass W = (1, expm1(d/eps), exp(d/eps), 0):
+// the register point kernels take 4 columns with DFMA; the DMMA kernels need a multiple of 8.
+static int anchor_kt(const Problem& P) { return P.dim >= 1 && P.dim <= 4 ? 4 : 8; }
 
 // Whether the block pass can fuse r = P~ beta (register point kernels, d <= 4).
 static bool block_rs_fusable(const Problem& P) { return P.dim >= 1 && P.dim <= 4; }

@@ -45,6 +45,7 @@ static thread_local double g_best_residual = 0.0;
 
 static Problem& get(sknr_problem h) {
     if (!h || !h->p) throw InvalidArgument("sknr: null problem handle");
+    own_stream(h->p->stream);  // this call's buffers free stream-ordered on the problem's stream
     return *h->p;
 }
 
@@ -818,22 +819,28 @@ int sknr_newton_step_ex(sknr_problem h, const double* f, const double* vectors, 
     }
     const double inv_eps = 1.0 / P.eps;
     double dmax = 0.0;
-    std::vector<double> dv(n), ev(n);
+    std::vector<double> dv(n), ev(n), xv(n);
     for (int64_t i = 0; i < n; ++i) {
         dv[i] = cand[i] - f[i];
         dmax = std::max(dmax, std::abs(dv[i]));
         ev[i] = std::expm1(dv[i] * inv_eps);
+        xv[i] = std::exp(std::min(dv[i] * inv_eps, 700.0));
     }
     bool acc = false;
-    if (accept_test == 1 && dmax * inv_eps <= kStableSpan) {
-        std::vector<double> ones(n, 1.0), sv(m), tv(m);
+    if (accept_test == 1 && dmax <= kStableSpan * P.eps) {
+        std::vector<double> ones(n, 1.0), sv(m), tv(m), uv(m);
         rc = sknr_apply_Rt(h, f, g.data(), ones.data(), sv.data());
         if (rc != SKNR_OK) return rc;
         rc = sknr_apply_Rt(h, f, g.data(), ev.data(), tv.data());
         if (rc != SKNR_OK) return rc;
+        rc = sknr_apply_Rt(h, f, g.data(), xv.data(), uv.data());
+        if (rc != SKNR_OK) return rc;
         double dq = 0.0, bdh = 0.0;
         for (int64_t i = 0; i < n; ++i) dq += P.h_alpha[i] * dv[i];
-        for (int64_t j = 0; j < m; ++j) bdh += P.h_beta[j] * (-P.eps * std::log1p(tv[j] / sv[j]));
+        for (int64_t j = 0; j < m; ++j) {
+            const double ts = tv[j] / sv[j];  // as k_dh
+            bdh += P.h_beta[j] * (-P.eps * (std::abs(ts) <= kDhSwitch ? std::log1p(ts) : std::log(uv[j] / sv[j])));
+        }
         acc = dq + bdh > 0.0;
     } else {
         double q1 = 0.0;

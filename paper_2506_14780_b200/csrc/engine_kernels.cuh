@@ -126,10 +126,14 @@ __global__ void k_newton_solve(const double* G1, const double* cross, const doub
         sA[e] = -(0.5 * (h_rc + h_cr));
     }
     __syncthreads();
-    // Right-looking factorisation. Every entry sees the same operations in the same
-    // order as in the left-looking loop of Eigen's unblocked LLT (A_rc -= L_rt L_ct for
-    // t = 0, 1, ..., then / L_cc), so the factor is the same, but each column costs
-    // three barriers instead of a serial dot product.
+    // Right-looking factorisation. Every entry sees the same scalar operations in the
+    // same order as the oracle's left-looking loop (A_rc -= L_rt L_ct for t = 0, 1, ...,
+    // then / L_cc), so the factor is the oracle's, but each column costs three barriers
+    // instead of a serial dot product. Eigen itself differs at the rounding level: its
+    // LLT::compute runs llt_inplace::blocked, which is the unblocked loop only below 32
+    // columns (and even then with SIMD dot products); for ell >= 32 (C4: 32, C5: 24 -> no)
+    // it factors in blocks with GEMM trailing updates. The reference's Cholesky order is
+    // therefore parity-unpinned; only the oracle's is matched.
     for (int c = 0; c < ell; ++c) {
         if (tid == 0) {
             const double x = sA[c + c * ell];
@@ -191,8 +195,9 @@ __global__ void k_fcand(const double* f, const double* V, int64_t n, int ell, co
 }
 
 // Stable accept test, per row: candidate f' = f + V delta, d = f' - f (exact: f' and f
-// are close), and the block-pass weights W[i] = (1, expm1(d_i/eps), 0, ...) of the
-// anchor pass s_j = sum_i P~_ij, t_j = sum_i P~_ij expm1(d_i/eps).
+// are close), and the block-pass weights W[i] = (1, expm1(d_i/eps), exp(d_i/eps), 0, ...)
+// of the anchor pass s_j = sum_i P~_ij, t_j = sum_i P~_ij expm1(d_i/eps),
+// u_j = sum_i P~_ij exp(d_i/eps) (|d|/eps <= 600 here: the larger steps take the literal test).
 __global__ void k_fcand_step(const double* f, const double* V, int64_t n, int ell, const double* delta,
                              double inv_eps, double* out, double* dvec, double* W, int kt, DevState* st,
                              unsigned guard) {
@@ -211,18 +216,24 @@ __global__ void k_fcand_step(const double* f, const double* V, int64_t n, int el
         dvec[i] = d;
         W[i * kt] = 1.0;
         W[i * kt + 1] = expm1(fmin(d * inv_eps, 700.0));
+        W[i * kt + 2] = exp(fmin(d * inv_eps, 700.0));
     }
 }
 
-// h'_j - h_j = -eps log1p(t_j / s_j) from the anchor pass (ST = [s | t], m x 2), and
-// the candidate's transform h' = h + (h' - h) (the next sweep's g if accepted).
+// h'_j - h_j = -eps log(u_j / s_j) from the anchor pass (ST = [s | t | u], m x 3), and
+// the candidate's transform h' = h + (h' - h) (the next sweep's g if accepted). The ratio
+// u/s = 1 + t/s is taken as log1p(t/s) when |t/s| <= 1/2 (small steps: u - s would cancel)
+// and as log(u/s) otherwise (t/s -> -1 would cancel: a column whose mass the step moves
+// away); both forms are accurate to rounding on their side of the switch (kDhSwitch).
+constexpr double kDhSwitch = 0.5;
 __global__ void k_dh(const double* ST, const double* h, int64_t m, double eps, double* dh, double* hcand,
                      DevState* st, unsigned guard) {
     SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < m;
          j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double v = -eps * log1p(ST[m + j] / ST[j]);
+        const double ts = ST[m + j] / ST[j];
+        const double v = -eps * (fabs(ts) <= kDhSwitch ? log1p(ts) : log(ST[2 * m + j] / ST[j]));
         dh[j] = v;
         hcand[j] = h[j] + v;
     }

@@ -170,8 +170,9 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         // accept test. Literal (solver.cpp:45-47): Q1 = a.f' + b.f'^{C,eps} from a full
         // column LSE of the candidate, accept iff Q1 > Q0. Stable (accept = 1): the same
         // predicate as dQ = Q1 - Q0 > 0 evaluated directly -- one anchor pass at (f, h)
-        // gives s_j = sum_i P~_ij and t_j = sum_i P~_ij expm1(d_i/eps), d = f' - f, and
-        // h'_j - h_j = -eps log1p(t_j/s_j) (exact algebra), so dQ = a.d + b.(h' - h) rounds
+        // gives s_j = sum_i P~_ij, t_j = sum_i P~_ij expm1(d_i/eps) and u_j = sum_i P~_ij
+        // exp(d_i/eps), d = f' - f, and h'_j - h_j = -eps log(u_j/s_j) = -eps log1p(t_j/s_j)
+        // (exact algebra; k_dh picks the form that does not cancel), so dQ = a.d + b.(h' - h) rounds
         // at the size of the step instead of at ulp(Q) (oracle stable_delta_q). Steps with
         // max|d| > 600 eps take the literal path (guard bits G_LIT / G_NOLIT).
         const bool stable = accept == 1;
@@ -212,7 +213,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             tp.in_lw = P.src.lw.p;
             tp.out_v = S.h.p;
             tp.W = S.Wst.p;
-            tp.k = 2;
+            tp.k = 3;
             tp.kt = akt;
             tp.out = S.ST.p;
             tp.guard = gst;
@@ -280,6 +281,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
 static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* basis_host,
                           const double* init_f, int64_t max_iter, double tol, int64_t trace_cap,
                           int accept = 0) {
+    own_stream(P.stream);
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
     S.f.ensure(n);
@@ -312,7 +314,7 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
             const int akt = anchor_kt(P);
             S.dvec.ensure(n);
             S.Wst.ensure(n * akt);
-            S.ST.ensure(2 * m);
+            S.ST.ensure(3 * m);
             S.dh.ensure(m);
             plan_for(P, 0, MODE_BLOCK, akt, anchor_in_blocks(akt));
         }

@@ -1909,8 +1909,8 @@ KernelInfo pick_pts(int mode, int kt) {
             default: return KernelInfo{};
         }
     }
-    if (mode == MODE_BLOCK && kt == 2)  // two-column block (stable accept test's anchor pass): DFMA
-        return make_pts<D, 8, MODE_BLOCK, 2, 256, 1>();
+    if (mode == MODE_BLOCK && kt == 4)  // 4-column block (stable accept test's anchor pass): DFMA
+        return make_pts<D, 4, MODE_BLOCK, 4, 256, 1>();
     // FP64 tensor-core (DMMA) block passes. Default: the double-buffered v2 kernel (8 warps,
     // 256-output tiles, 32-input chunks); SKNR_BLOCK_V1=1 selects the round-1 kernel.
     static const bool v1 = std::getenv("SKNR_BLOCK_V1") != nullptr;

@@ -16,27 +16,11 @@ import pytest
 import oracle_ref as O
 import paper_2506_14780_b200 as sk
 from paper_2506_14780_b200 import generators as G
-from support import rel_err
+from support import rel_err, smooth_basis
 
 pytestmark = pytest.mark.gpu
 
 TOL_POT = 1e-9
-
-
-def smooth_basis(x, alpha, ell):
-    """ell low-frequency cosine modes of a 2-D projection of the sources, orthonormal in
-    L2(alpha) and alpha-mean-zero (the deflated direction removed): a Newton basis whose
-    steps are large and well decided, with no top_modes run needed on either side."""
-    rng = np.random.default_rng(0)
-    z = x @ rng.standard_normal((x.shape[1], 2))
-    z = (z - z.min(0)) / (z.max(0) - z.min(0))
-    cols = [np.cos(np.pi * a * z[:, 0]) * np.cos(np.pi * b * z[:, 1])
-            for a in range(8) for b in range(8) if (a, b) != (0, 0)]
-    w = np.sqrt(alpha)[:, None]
-    Vs = np.stack(cols[:ell], 1) * w
-    Vs -= w * (w[:, 0] @ Vs)[None, :]
-    Q, _ = np.linalg.qr(Vs)
-    return np.asfortranarray(Q / w)
 
 
 @pytest.mark.parametrize("name,mode,K,KN", [("C3", "auto", 6, 3), ("C4", "auto", 2, 2),

@@ -216,3 +216,30 @@ def test_points_kind_matches_dense_cost():
     Pp = O.Instance(a, b, 0.05, x=x, y=y)
     f = random_vector(rng, 11, 0.1)
     assert np.max(np.abs(O.ctransform_of_f(Pd, f) - O.ctransform_of_f(Pp, f))) <= 1e-14
+
+
+@pytest.mark.parametrize("k_sk", [1, 2, 3, 4, 6])
+def test_stable_delta_q_matches_literal_gain(k_sk):
+    """The stable accept test evaluates Q(f') - Q(f) directly (sknr_oracle.cpp
+    stable_delta_q); wherever the literal difference is well above Q's rounding the two
+    must agree -- including large steps (|d|/eps up to the 600 literal-fallback span) that
+    move a column's mass away, where log1p(t/s) would cancel to -inf (t/s -> -1) and the
+    log(u/s) form takes over. BASELINE C3 shape (d = 3, Dirichlet weights, eps = 1e-3)."""
+    from paper_2506_14780_b200 import generators as G
+    from support import smooth_basis
+
+    c = G.config("C3", n=500, m=450)
+    P = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+    r0 = O.solve(P, tol=1e-300, max_iter=k_sk)
+    V = smooth_basis(c.x, c.alpha, c.ell)
+    gains = {}
+    for mode in ("literal", "stable"):
+        with O.accept_mode(mode):
+            r = O.solve(P, tol=1e-300, max_iter=1, ell=c.ell, V=V, init=(r0["f"], r0["g"]))
+        gains[mode] = r["trace"][0]
+    lit, st = gains["literal"], gains["stable"]
+    step_over_eps = lit[6] / c.epsilon
+    assert math.isfinite(st[5]) and math.isfinite(st[2])
+    q_ulp = 4 * np.spacing(abs(lit[2]))
+    assert abs(st[5] - lit[5]) <= 1e-9 * abs(lit[5]) + q_ulp, (step_over_eps, st[5], lit[5])
+    assert st[4] == lit[4]
