@@ -108,11 +108,13 @@ int sknr_ctransform_of_f(sknr_problem p, const double* f, double* g);
 int sknr_ctransform_of_g(sknr_problem p, const double* g, double* f);
 int sknr_plan_marginals(sknr_problem p, const double* f, const double* g, double* row,
                         double* col, double* gap_l2, double* gap_inf);
-/* coupling_from (core.cpp:84-103): n x m col-major into a host buffer. */
+/* coupling_from (core.cpp:84-103): n x m col-major into a host buffer. On a row-sharded
+ * handle: this rank's rows only (n_local x m), f full length. */
 int sknr_coupling(sknr_problem p, const double* f, const double* g, double* plan);
 /* Rows [row_begin, row_end) of the same plan, col-major with leading dimension
  * row_end - row_begin: lets a caller stream an n x m coupling (e.g. the CLI's
- * coupling.csv, main.cpp:149-154) without holding it whole. */
+ * coupling.csv, main.cpp:149-154) without holding it whole. Row-sharded handle: global row
+ * indices inside this rank's block [row_begin, row_begin + n_local) (sknr_problem_shard). */
 int sknr_coupling_rows(sknr_problem p, const double* f, const double* g, int64_t row_begin, int64_t row_end,
                        double* plan_rows);
 

@@ -459,9 +459,12 @@ def plan_marginals(problem: Problem, f, g):
 
 
 def coupling(problem: Problem, f, g) -> np.ndarray:
+    """coupling_from (core.cpp:84-103); on a row-sharded problem, this rank's rows
+    (row_partition) -- each rank materialises its own block of the n x m plan."""
     f = _checked(f, problem.n, "coupling_from(f)")
     g = _checked(g, problem.m, "coupling_from(g)")
-    plan = np.empty((problem.n, problem.m), order="F")
+    b, e = getattr(problem, "_rows", (0, problem.n))
+    plan = np.empty((e - b, problem.m), order="F")
     _check(lib().sknr_coupling(problem.handle, _ptr(f), _ptr(g), _ptr(plan)))
     return plan
 
@@ -1037,6 +1040,7 @@ def shard(problem: Problem, rank: int, world: int) -> None:
     Inputs and outputs of every call stay full length on every rank."""
     b, e = row_partition(problem.n, world, rank)
     _check(lib().sknr_problem_shard(problem.handle, b, e))
+    problem._rows = (b, e)
 
 
 def debug_counters(problem: Problem) -> dict:

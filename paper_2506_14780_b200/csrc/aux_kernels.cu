@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(AUX_NT) k_lse_commit(const double* in_vec, dou
 __global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial, int64_t nb, int kt,
                                                            int k, int64_t n_out, const double* scale,
                                                            double* out, int64_t ld, DevState* st,
-                                                           unsigned guard) {
+                                                           unsigned guard, int64_t blk_rows) {
     SKNR_PDL_ENTRY();
     if (guard_skip(st, guard)) return;
     __shared__ double sh[FOLD_W][32];
@@ -297,7 +297,11 @@ __global__ void __launch_bounds__(AUX_NT) k_block_finalize(const double* partial
         if (threadIdx.x < 32 && e < total) {
             const int64_t o = e % n_out;
             const int64_t c = e / n_out;
-            out[o + c * ld] = scale ? scale[o] * S : S;
+            // blk_rows > 0: rank-blocked layout for a reduce-scatter -- block q = rows
+            // [q * blk_rows, (q + 1) * blk_rows), its k columns contiguous (ld = blk_rows)
+            const int64_t at = blk_rows > 0 ? (o / blk_rows) * (k * blk_rows) + c * blk_rows + o % blk_rows
+                                            : o + c * ld;
+            out[at] = scale ? scale[o] * S : S;
         }
     }
 }

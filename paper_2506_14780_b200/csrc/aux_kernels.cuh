@@ -93,7 +93,7 @@ __global__ void k_lse_commit(const double* in_vec, double* ref, int64_t count, i
                              unsigned guard);
 __global__ void k_block_finalize(const double* partial, int64_t nb, int kt, int k, int64_t n_out,
                                  const double* scale, double* out, int64_t ld, DevState* st,
-                                 unsigned guard);
+                                 unsigned guard, int64_t blk_rows);
 // out[q] = scale * sum_b part[b*Q + q] (column fold of split partial rows, deterministic)
 __global__ void k_fold_sum(const double* part, int64_t nb, int64_t Q, double scale, double* out,
                            const DevState* st, unsigned guard);

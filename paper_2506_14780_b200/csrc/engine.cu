@@ -79,6 +79,8 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                  cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -100,6 +102,7 @@ struct NcclApi {
         AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
         Broadcast = reinterpret_cast<decltype(Broadcast)>(sym("ncclBroadcast"));
         AllGather = reinterpret_cast<decltype(AllGather)>(sym("ncclAllGather"));
+        ReduceScatter = reinterpret_cast<decltype(ReduceScatter)>(sym("ncclReduceScatter"));
         GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
         GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
         CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
@@ -572,6 +575,18 @@ __global__ void k_emu_allreduce(EmuPtrs p, int world, int64_t count, int op) {
     }
 }
 
+// recv[q][e] = sum_r send[r][q * count + e], ranks in order (reduce-scatter)
+__global__ void k_emu_reduce_scatter(EmuPtrs send, EmuPtrs recv, int world, int64_t count) {
+    SKNR_PDL_ENTRY();
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count * world;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int q = static_cast<int>(t / count);
+        double acc = send.buf[0][t];
+        for (int r = 1; r < world; ++r) acc += send.buf[r][t];
+        recv.buf[q][t - q * count] = acc;
+    }
+}
+
 struct EmuGroup {
     int world = 0;
     std::mutex mu;
@@ -673,6 +688,75 @@ static void allgather(Problem& P, const double* send, double* recv, size_t count
     }
     NK(g_nccl.AllGather(send, recv, count, ncclDouble, g_comm.comm, P.stream));
 }
+
+// Reduce-scatter (sum): send holds R blocks of `count` doubles, rank q receives the sum of
+// block q over all ranks (NCCL's layout), on the problem's stream.
+static void reduce_scatter(Problem& P, const double* send, double* recv, size_t count) {
+    count_collective(count * sizeof(double) * static_cast<size_t>(P.world));
+    if (P.emu) {
+        {
+            std::lock_guard<std::mutex> lk(g_emu.mu);
+            g_emu.locals[P.rank] = send;
+            g_emu.bufs.buf[P.rank] = recv;
+        }
+        g_emu.meet(P.rank, P.stream, [&] {
+            EmuPtrs sp{};
+            for (int r = 0; r < g_emu.world; ++r) sp.buf[r] = const_cast<double*>(g_emu.locals[r]);
+            const int64_t tot = static_cast<int64_t>(count) * g_emu.world;
+            count_launch();
+            k_emu_reduce_scatter<<<static_cast<int>(std::min<int64_t>((tot + 255) / 256, 1184)), 256, 0, g_emu.red>>>(
+                sp, g_emu.bufs, g_emu.world, static_cast<int64_t>(count));
+            CK(cudaGetLastError());
+        });
+        return;
+    }
+    NK(g_nccl.ReduceScatter(send, recv, count, ncclDouble, ncclSum, g_comm.comm, P.stream));
+}
+
+// All-gather of an n_local x k column-major row block (ld = n_local) into the full
+// n_global x k block (ld = n_global) on every rank: one NCCL broadcast per rank (ragged
+// row blocks) into a staging buffer, then a strided copy into place.
+static void gather_row_block(Problem& P, const double* X, int k, double* full) {
+    const size_t pitch = sizeof(double) * static_cast<size_t>(P.n_global);
+    if (P.emu) {
+        {
+            std::lock_guard<std::mutex> lk(g_emu.mu);
+            g_emu.locals[P.rank] = X;
+            g_emu.bufs.buf[P.rank] = full;
+        }
+        g_emu.meet(P.rank, P.stream, [&] {
+            for (int q = 0; q < g_emu.world; ++q) {
+                int64_t b, e;
+                row_partition(P.n_global, g_emu.world, q, b, e);
+                if (e == b) continue;
+                for (int r = 0; r < g_emu.world; ++r)
+                    CK(cudaMemcpy2DAsync(g_emu.bufs.buf[r] + b, pitch, g_emu.locals[q], sizeof(double) * (e - b),
+                                         sizeof(double) * (e - b), k, cudaMemcpyDeviceToDevice, g_emu.red));
+            }
+        });
+        return;
+    }
+    P.gather_buf.ensure(static_cast<size_t>(P.n_global) * k);
+    count_collective(static_cast<size_t>(P.n_global) * k * sizeof(double));
+    NK(g_nccl.GroupStart());
+    for (int r = 0; r < g_comm.world; ++r) {
+        int64_t b, e;
+        row_partition(P.n_global, g_comm.world, r, b, e);
+        NK(g_nccl.Broadcast(X, P.gather_buf.p + b * k, (e - b) * k, ncclDouble, r, g_comm.comm, P.stream));
+    }
+    NK(g_nccl.GroupEnd());
+    for (int r = 0; r < g_comm.world; ++r) {
+        int64_t b, e;
+        row_partition(P.n_global, g_comm.world, r, b, e);
+        if (e == b) continue;
+        CK(cudaMemcpy2DAsync(full + b, pitch, P.gather_buf.p + b * k, sizeof(double) * (e - b), sizeof(double) * (e - b),
+                             k, cudaMemcpyDeviceToDevice, P.stream));
+    }
+}
+
+// Column blocks of the m-side for the reduce-scattered S = V^T P~: rank q
+// owns target rows [q * mb, min(m, (q + 1) * mb)), mb = ceil(m / R) (NCCL needs equal blocks).
+static int64_t scatter_rows(const Problem& P) { return (P.m + P.world - 1) / P.world; }
 
 // Upload the local row block of a full-length, `cols`-column column-major host array.
 static void upload_rows(Problem& P, double* dev, const double* host_full, int64_t cols = 1) {
@@ -942,6 +1026,10 @@ struct PassSpec {
     const double* out_scale = nullptr;
     double* out = nullptr;  // sum: [nout]; block: col-major nout x k (ld = nout)
     double* rsum_out = nullptr;  // block, dir 0 only: r_i = sum_j e(j, i) b_j fused into the pass
+    // block, dir 0, sharded: reduce-scatter instead of allreduce -- `out` (R * scatter_rows
+    // x k, rank-blocked) is summed over the shards and this rank receives its block
+    // (scatter_rows x k, ld = scatter_rows) here
+    double* scatter_out = nullptr;
     bool cull = false;                 // block pass may skip negligible terms (culling enabled)
     const double* cull_logtot = nullptr;  // per-output log of sum_in e (nullptr: 0, i.e. sums are 1)
     unsigned guard = 0;
@@ -966,6 +1054,7 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     cudaStream_t s = P.stream;
     const bool rs = ps.W && ps.rsum_out;
     if (rs && (ps.dir != 0 || !block_rs_fusable(P))) throw InvalidArgument("sknr_b200: fused row sums unsupported here");
+    const bool scatter = ps.scatter_out && P.shard && ps.W && ps.dir == 0;
     const bool bcull = ps.W && !rs && ps.cull && cull_block_active(P, ps.dir);
     const int mode = ps.W ? (rs ? MODE_BLOCK_RS : (bcull ? MODE_BLOCK_CULL : MODE_BLOCK)) : MODE_SUM;
     const TilePlan tp = plan_for(P, ps.dir, mode, ps.W ? ps.kt : 0, anchor_in_blocks(ps.W ? ps.kt : 0));
@@ -1040,8 +1129,10 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     else
         k_block_finalize<<<fold_grid(nout * ps.k), AUX_NT, 0, s>>>(P.partial.p, tp.n_in_blocks, ps.kt,
                                                                   ps.k, nout, ps.out_scale, ps.out, nout,
-                                                                  P.st, ps.guard);
-    if (ps.dir == 0)  // column direction reduces over the sharded rows
+                                                                  P.st, ps.guard, scatter ? scatter_rows(P) : 0);
+    if (scatter)  // column direction, this rank's block of the sum over the sharded rows
+        reduce_scatter(P, ps.out, ps.scatter_out, static_cast<size_t>(scatter_rows(P)) * ps.k);
+    else if (ps.dir == 0)  // column direction reduces over the sharded rows
         allreduce(P, ps.out, static_cast<size_t>(nout) * (mode == MODE_SUM ? 1 : ps.k), ncclSum);
     CK(cudaGetLastError());
 }

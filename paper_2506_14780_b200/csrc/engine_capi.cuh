@@ -366,20 +366,24 @@ int sknr_coupling_rows(sknr_problem h, const double* f, const double* g, int64_t
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    if (P.shard) throw RuntimeFailure("coupling_from: not available on a row-sharded problem");
-    if (row_begin < 0 || row_end > P.n || row_begin > row_end)
-        throw InvalidArgument("coupling_rows: row range out of bounds");
-    check_finite_vec(f, P.n, "coupling_from(f)");
+    // row-sharded: global row indices inside this rank's block [P.row_begin, P.row_begin + n);
+    // each rank materialises its own rows of the plan (the n x m output is never gathered)
+    if (row_begin < P.row_begin || row_end > P.row_begin + P.n || row_begin > row_end)
+        throw InvalidArgument(P.shard ? "coupling_rows: row range outside this rank's row block"
+                                      : "coupling_rows: row range out of bounds");
+    check_finite_vec(f, P.n_global, "coupling_from(f)");
     check_finite_vec(g, P.m, "coupling_from(g)");
     const int64_t rows = row_end - row_begin;
     if (rows == 0) return SKNR_OK;
+    row_begin -= P.row_begin;  // local from here on
+    row_end -= P.row_begin;
     // host-side block size bounded to 1 GiB of device scratch per launch
     const int64_t m = P.m;
     const int64_t cap_rows = std::max<int64_t>(1, (int64_t(1) << 27) / std::max<int64_t>(m, 1));
     DBuf df, dg, dp;
     df.ensure(P.n);
     dg.ensure(m);
-    upload(df.p, f, P.n, P.stream);
+    upload_rows(P, df.p, f);
     upload(dg.p, g, m, P.stream);
     const bool whole = rows <= cap_rows;
     dp.ensure((whole ? rows : cap_rows) * m);
@@ -405,7 +409,8 @@ int sknr_coupling_rows(sknr_problem h, const double* f, const double* g, int64_t
 }
 
 int sknr_coupling(sknr_problem h, const double* f, const double* g, double* plan) {
-    return sknr_coupling_rows(h, f, g, 0, h && h->p ? h->p->n : 0, plan);
+    const int64_t b = h && h->p ? h->p->row_begin : 0;
+    return sknr_coupling_rows(h, f, g, b, b + (h && h->p ? h->p->n : 0), plan);
 }
 
 // full_semi_dual_hessian (objective.cpp:150-171): H = -(1/eps)(diag(r) - P~ diag(b) P~^T),

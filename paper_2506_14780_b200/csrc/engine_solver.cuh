@@ -6,6 +6,7 @@
 // ============================================================ solve
 struct SolveState {
     DBuf f, g, gnext, h, fcand, hcand, rowres, colres, am, r, Lr, V, Wv, S, delta, G;
+    DBuf Sloc;  // sharded: this rank's reduce-scattered block of S (scatter_rows x ell)
     DBuf dvec, Wst, ST, dh;  // stable accept test: d = f' - f, anchor-pass weights/sums, h' - h
     DBuf trace_raw;  // sknr_record array (as doubles)
 };
@@ -147,6 +148,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         sp.k = l;
         sp.kt = block_kt_for(l);
         sp.out = S.S.p;
+        sp.scatter_out = P.shard ? S.Sloc.p : nullptr;
         sp.rsum_out = fuse_r ? S.r.p : nullptr;
         sp.cull = cull_nr;  // P~ columns sum to 1 at h = f^{C,eps}: no normalisation needed
         sp.guard = gn;
@@ -155,15 +157,28 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
             count_launch();
             k_axpby<<<grid_for(n), AUX_NT, 0, s>>>(P.src.w.p, S.r.p, n, 1.0, -1.0, S.am.p);
         }
-        // (plan_pass has already summed S = V^T P~ over the row shards)
         double* G1 = S.G.p;
         double* cross = G1 + l * l;
         double* grad = cross + l * l;
         gram(P, n, l, l, S.V.p, n, S.V.p, n, S.r.p, G1, gn);
-        gram(P, m, l, l, S.S.p, m, S.S.p, m, P.tgt.w.p, cross, gn);
-        gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
-        allreduce(P, G1, static_cast<size_t>(l) * l, ncclSum);
-        allreduce(P, grad, l, ncclSum);
+        if (P.shard) {
+            // S = V^T P~ was reduce-scattered: this rank holds target rows
+            // [q mb, q mb + rows) and adds its part of cross = S diag(b) S^T; one allreduce
+            // sums [G1 | cross | grad] (contiguous) over the shards
+            const int64_t mb = scatter_rows(P);
+            const int64_t j0 = std::min<int64_t>(m, mb * P.rank), rows = std::min<int64_t>(m, j0 + mb) - j0;
+            if (rows > 0)
+                gram(P, rows, l, l, S.Sloc.p, mb, S.Sloc.p, mb, P.tgt.w.p + j0, cross, gn);
+            else {
+                count_launch();
+                k_fill<<<1, AUX_NT, 0, s>>>(cross, static_cast<int64_t>(l) * l, 0.0);
+            }
+            gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
+            allreduce(P, G1, static_cast<size_t>(2 * l * l + l), ncclSum);
+        } else {
+            gram(P, m, l, l, S.S.p, m, S.S.p, m, P.tgt.w.p, cross, gn);
+            gram(P, n, l, 1, S.V.p, n, S.am.p, n, nullptr, grad, gn);
+        }
         count_launch();
         k_newton_solve<<<1, 256, sizeof(double) * l * l, s>>>(G1, cross, grad, l, P.inv_eps(), S.delta.p,
                                                             P.st, gn);
@@ -302,7 +317,12 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
         const int kt = block_kt_for(static_cast<int>(ell));
         S.V.ensure(n * ell);
         S.Wv.ensure(n * kt);
-        S.S.ensure(m * ell);
+        if (P.shard) {
+            S.S.ensure(P.world * scatter_rows(P) * ell);  // rank-blocked, padded rows stay 0
+            S.Sloc.ensure(scatter_rows(P) * ell);
+        } else {
+            S.S.ensure(m * ell);
+        }
         upload_rows(P, S.V.p, basis_host, ell);
         count_launch();
         k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(S.V.p, n, n, static_cast<int>(ell), kt, nullptr,

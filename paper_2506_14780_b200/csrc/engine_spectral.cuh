@@ -130,8 +130,10 @@ static void host_sym_eig(const std::vector<double>& A, int k, std::vector<double
 }
 
 struct QrWork {
-    DBuf hh, w, part, Q, backup, flag;
-    bool force_householder = false;
+    DBuf hh, w, part, Q, backup, flag, full;
+    // SKNR_FORCE_HOUSEHOLDER=1: every round takes the Householder path (tests of the
+    // fallback, sharded and not)
+    bool force_householder = std::getenv("SKNR_FORCE_HOUSEHOLDER") != nullptr;
 };
 
 // Cholesky G + shift*I = L L^T (shift = coef * trace(G)), then Rinv = L^{-T}
@@ -262,23 +264,32 @@ static void device_orth_deflated(Problem& P, double* X, int64_t n, int k, const 
             device_cholqr_step(P, X, n, k, true, qw, fail);
             device_cholqr_step(P, X, n, k, false, qw, fail);
             device_cholqr_step(P, X, n, k, false, qw, fail);
+            int hfail = 0;
+            CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
+            CK(cudaStreamSynchronize(P.stream));
+            if (hfail) {  // restore the deflated block and redo this round with Householder
+                CK(cudaMemcpyAsync(X, qw.backup.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
+                use_householder = true;
+            }
+        }
+        if (use_householder) {
+            if (P.shard) {
+                // row-sharded: every rank gathers the whole n x k block, runs the same
+                // device Householder QR on it (identical inputs -> identical Q on every
+                // rank) and keeps its own rows
+                qw.full.ensure(static_cast<size_t>(P.n_global) * k);
+                gather_row_block(P, X, k, qw.full.p);
+                device_householder_q(P, qw.full.p, P.n_global, k, qw);
+                CK(cudaMemcpy2DAsync(X, sizeof(double) * n, qw.full.p + P.row_begin, sizeof(double) * P.n_global,
+                                     sizeof(double) * n, k, cudaMemcpyDeviceToDevice, P.stream));
+            } else {
+                device_householder_q(P, X, n, k, qw);
+            }
         }
         gram_all(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
         std::vector<double> hs(k + 1);
         download(hs.data(), s, k, P.stream);
-        int hfail = 0;
-        if (!use_householder) CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, P.stream));
         CK(cudaStreamSynchronize(P.stream));
-        if (hfail) {  // restore the deflated block and redo this round with Householder
-            if (P.shard)
-                throw EigenFailure("top_modes: CholeskyQR breakdown on a row-sharded problem (no sharded "
-                                   "Householder fallback)", std::numeric_limits<double>::infinity());
-            CK(cudaMemcpyAsync(X, qw.backup.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, P.stream));
-            device_householder_q(P, X, n, k, qw);
-            gram(P, n, k, 1, X, n, u0, n, nullptr, s, 0);
-            download(hs.data(), s, k, P.stream);
-            CK(cudaStreamSynchronize(P.stream));
-        }
         double worst = 0.0;
         for (int c = 0; c < k; ++c) worst = std::max(worst, std::abs(hs[c]));
         if (worst < 1e-13) break;

@@ -48,6 +48,12 @@ __constant__ unsigned long long c_exp2_tab10[1024] = {
 #define c_exp2_tab10 c_exp2_tab
 #endif
 
+// 2^(e/4096) mantissas for the 4096-entry LSE sum kernel (pts_sum12_kernel); global
+// memory (32 KiB would crowd the constant bank), copied into shared memory per CTA
+__device__ const unsigned long long g_exp2_tab12[4096] = {
+#include "exp2_table4096.inc"
+};
+
 // Fill the replicated table: tab[e*kTabRep + r] = mantissa bits of 2^(e/2^kTB).
 // The hi word is pre-biased by -(e << (20 - kTB)) (mod 2^32) so that pexp_parts assembles
 // exponent and mantissa with one IMAD.
@@ -284,6 +290,113 @@ __global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
 #pragma unroll
                     for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
                     acc[jt] = pexp10_acc<FC>(u, tab, laneoff, q2, acc[jt]);
+                }
+            }
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+            if (o[jt] < a.n_out) a.partial[ib * a.n_out + o[jt]] = acc[jt];
+    }
+}
+
+// ------------------------------------------------------------- LSE sum pass, 4096-entry table
+// MODE_SUM in 10 FP64 slots per cell with the 32 KiB shared-memory footprint of the
+// 256-entry kernel: 2^(u/256) = 2^(u'/4096), u' = 16u, from a 4096-entry table of
+// 2^(e/4096) held ONCE per CTA (REP copies; REP = 1: lanes read random entries and pay the
+// bank conflicts -- the shared-memory pipe has the slack, the FP64 pipe does not) and a
+// degree-3 Taylor polynomial of 2^(r/4096), |r| <= 1/2 (truncation 2e-18):
+//   per cell 1 DADD + D DFMA (u') + 3 DADD (Cody-Waite) + 3 DFMA (p) + 1 DFMA (acc) = 10 (d=2)
+// u' is exact: inputs are staged as (16A, 4X), outputs loaded as (16B, 4Y) -- powers of two.
+// Same partial sums in the same [ib][n_out] layout as pts_tile_kernel<SUM>.
+constexpr double kMagic12 = 6755399445250048.0;  // 1.5 * 2^52 + 1023 * 4096
+constexpr double kR1 = 0.0001692253858788929;    // (ln2/4096)^k / k!
+constexpr double kR2 = 1.4318615612930102e-08;
+constexpr double kR3 = 8.076910841165457e-13;
+static __constant__ double c_pexp12_k[4] = {kMagic12, kR1, kR2, kR3};
+
+template <int REP, bool FASTCLAMP>
+__device__ __forceinline__ double pexp12_acc(double u, const unsigned long long* __restrict__ tab,
+                                             unsigned laneoff, double r2, double acc) {
+    const double t = u + c_pexp12_k[0];
+    const double kf = t - c_pexp12_k[0];
+    const double r = u - kf;
+    double p = fma(r, c_pexp12_k[3], r2);
+    p = fma(p, r, c_pexp12_k[1]);
+    p = fma(p, r, 1.0);
+    // biased k = round(u') + 1023*4096 (low word of the magic sum), flushed at 0
+    const int kc = FASTCLAMP ? max(__double2loint(t), 0)
+                             : ((__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0);
+    constexpr int SH = REP == 1 ? 3 : (REP == 2 ? 4 : 5);
+    const unsigned off = ((static_cast<unsigned>(kc) << SH) & (4095u << SH)) | laneoff;
+    const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
+    // hi word = (kc >> 12) << 20 | mantissa bits of 2^(e/4096); table hi words pre-biased
+    // by -(e << 8), so kc * 256 + T.y assembles it in one IMAD (mod 2^32)
+    const double Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * 256u + T.y),
+                                       static_cast<int>(T.x));
+    return fma(Tp, p, acc);
+}
+
+template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1>
+__global__ void __launch_bounds__(NTT, MINB) pts_sum12_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int NT = NTT;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int CH = 256;
+    constexpr int TW = 4096 * REP;
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + TW;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < TW; t += NT) {  // hi word pre-biased by -(e << 8), see pexp12_acc
+        const unsigned e = static_cast<unsigned>(t / REP);
+        const unsigned long long v = g_exp2_tab12[e];
+        const unsigned hi = static_cast<unsigned>(v >> 32) - (e << 8);
+        tab[t] = (static_cast<unsigned long long>(hi) << 32) | (v & 0xFFFFFFFFull);
+    }
+    const unsigned laneoff = (tid & (REP - 1)) << 3;
+    double r2 = kR2;
+    asm volatile("" : "+d"(r2));
+    const int64_t out_tile = static_cast<int64_t>(NT) * JT;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        double B[JT], Y[JT][D], acc[JT];
+        int64_t o[JT];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            o[jt] = ot * out_tile + jt * NT + tid;
+            const int64_t oc = o[jt] < a.n_out ? o[jt] : a.n_out - 1;
+            B[jt] = 16.0 * a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Y[jt][d] = 4.0 * a.out_pack[oc * PK + 1 + d];
+            acc[jt] = 0.0;
+        }
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+            const int cnt = static_cast<int>((i1 - c0) < CH ? (i1 - c0) : CH);
+            __syncthreads();
+            for (int t = tid; t < cnt * PK; t += NT) {
+                const int q = t % PK;
+                sin[t] = (q == 0 ? 16.0 : 4.0) * a.in_pack[c0 * PK + t];
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int k = 0; k < cnt; ++k) {
+                double x[PK];
+#pragma unroll
+                for (int q = 0; q < PK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(sin + k * PK)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    double u = x[0] + B[jt];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
+                    acc[jt] = pexp12_acc<REP, FC>(u, tab, laneoff, r2, acc[jt]);
                 }
             }
         }
@@ -1789,6 +1902,16 @@ KernelInfo make_sum10() {
     return k;
 }
 
+template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1>
+KernelInfo make_sum12() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_sum12_kernel<D, JT, NTT, REP, FC, MINB>);
+    k.jt = JT;
+    k.nt = NTT;
+    k.smem = static_cast<int>(sizeof(double)) * (4096 * REP + 256 * PK_of<D>::value);
+    return k;
+}
+
 template <int D, int JT, int NTT, int MINB = 1>
 KernelInfo make_f32() {
     KernelInfo k;
@@ -1889,8 +2012,14 @@ KernelInfo pick_contract(int mode, int kt) {
     }
 }
 
+KernelInfo tune_variant(int v);
+
 template <int D>
 KernelInfo pick_pts(int mode, int kt) {
+    // SKNR_SUM_VARIANT=v (d = 2): run the sum passes with tune variant v (numerics checks of
+    // the variants, tools/tune_lse.py)
+    static const int sum_variant = std::getenv("SKNR_SUM_VARIANT") ? std::atoi(std::getenv("SKNR_SUM_VARIANT")) : -1;
+    if (mode == MODE_SUM && D == 2 && sum_variant >= 0 && sum_variant < 100) return tune_variant(sum_variant);
     // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
     if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
@@ -2041,6 +2170,16 @@ KernelInfo tune_variant(int v) {
         case 45: return make_sum10<2, 8, 384>();
         case 46: return make_sum10<2, 8, 512, true>();
         case 47: return make_sum10<2, 6, 512, true>();
+        // 4096-entry table, 10 FP64 slots per cell (pts_sum12_kernel <D, JT, threads, REP, FC>)
+        case 50: return make_sum12<2, 8, 256, 1, false, 2>();
+        case 51: return make_sum12<2, 8, 256, 2, false, 2>();
+        case 52: return make_sum12<2, 8, 256, 1, true, 2>();
+        case 53: return make_sum12<2, 8, 256, 2, true, 2>();
+        case 54: return make_sum12<2, 8, 512, 4>();
+        case 55: return make_sum12<2, 6, 256, 1, false, 2>();
+        case 56: return make_sum12<2, 4, 256, 1, false, 3>();
+        case 57: return make_sum12<2, 8, 128, 1, false, 4>();
+        case 58: return make_sum12<2, 8, 256, 1, false, 1>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();

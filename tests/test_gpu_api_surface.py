@@ -429,6 +429,53 @@ def test_sharded_path_across_R_matches_unsharded(world):
 
 
 TOL_NR = 1e-9  # stable accept test: identical decisions across R
+
+
+def test_coupling_sharded_rows():
+    """coupling_from on R = 3 emulated row shards (core.cpp:84-103): each rank returns its
+    own rows of the plan, bitwise equal to the unsharded plan's rows; global row ranges
+    outside the rank's block are rejected."""
+    inst = G.config("C1", n=301, m=233)
+    mk = lambda: sk.PointProblem(inst.x, inst.y, inst.alpha[:301] / inst.alpha[:301].sum(),
+                                 inst.beta[:233] / inst.beta[:233].sum(), inst.epsilon)
+    ref = sk.solve(mk(), tol=1e-9)
+    full = sk.coupling(mk(), ref.f, ref.g)
+
+    def per_rank(p):
+        b, e = p._rows
+        blk = sk.coupling(p, ref.f, ref.g)
+        part = sk.coupling_rows(p, ref.f, ref.g, b + 1, e)
+        with pytest.raises(ValueError, match="outside this rank"):
+            sk.coupling_rows(p, ref.f, ref.g, max(0, b - 1), e) if b > 0 else \
+                sk.coupling_rows(p, ref.f, ref.g, b, e + 1)
+        return b, e, blk, part
+
+    for b, e, blk, part in sk.run_emulated_shards(mk, 3, per_rank):
+        assert np.array_equal(blk, full[b:e]) and np.array_equal(part, full[b + 1:e])
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_householder_fallback_sharded(world, monkeypatch):
+    """orthonormalize_deflated's Householder path (spectral.cpp:116-117) forced on every
+    round (SKNR_FORCE_HOUSEHOLDER=1), unsharded and on R = 3 emulated row shards (each
+    rank gathers the n x k block, runs the same device QR and keeps its rows): the same
+    modes as the CholeskyQR3 default."""
+    inst = G.config("C1", n=601, m=433)
+    a = np.full(601, 1 / 601)
+    b = np.full(433, 1 / 433)
+    mk = lambda: sk.PointProblem(inst.x, inst.y, a, b, inst.epsilon)
+    ref_sk = sk.solve(mk(), tol=1e-9)
+    ref_tm = sk.top_modes(mk(), ref_sk.f, ref_sk.g, 6)
+    monkeypatch.setenv("SKNR_FORCE_HOUSEHOLDER", "1")
+    if world == 1:
+        out = [sk.top_modes(mk(), ref_sk.f, ref_sk.g, 6)]
+    else:
+        out = sk.run_emulated_shards(mk, world, lambda p: sk.top_modes(p, ref_sk.f, ref_sk.g, 6))
+    for tm in out:
+        assert rel_err(tm.rhos, ref_tm.rhos) <= 1e-8
+        assert sk.projector_distance(tm, ref_tm) <= 1e-6
+    for tm in out[1:]:
+        assert np.array_equal(tm.vectors, out[0].vectors)
 TOL_ANNEAL_BASIS = 2e-8
 
 

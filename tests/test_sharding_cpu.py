@@ -95,3 +95,66 @@ def test_row_partition_is_contiguous_and_complete():
             assert blocks[0][0] == 0 and blocks[-1][1] == n
             for (b0, e0), (b1, _) in zip(blocks, blocks[1:]):
                 assert e0 == b1 and b0 <= e0
+
+
+def _newton_worker(rank, world, port, q):
+    """Newton exchange (engine_solver.cuh): each rank forms its partial
+    S_r = V_r^T P~_r (m x ell) over its rows, writes it rank-blocked (block q = target rows
+    [q mb, (q+1) mb), mb = ceil(m/R), zero-padded: k_block_finalize blk_rows), one
+    reduce-scatter leaves rank q the summed block q, the rank adds its rows of
+    cross = S diag(b) S^T to its partial G1 = V_r^T diag(r_r) V_r and grad, and ONE
+    allreduce of [G1 | cross | grad] completes the ell x ell system on every rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, m, ell, eps = 90, 77, 5, 0.05
+    inst = G.config("C1", n=n, m=m)
+    rng = np.random.default_rng(3)
+    f = 0.05 * rng.standard_normal(n)
+    V = rng.standard_normal((n, ell))
+    P = O.Instance(inst.alpha, inst.beta, eps, x=inst.x, y=inst.y)
+    h = O.ctransform_of_f(P, f)
+    C = ((inst.x[:, None, :] - inst.y[None, :, :]) ** 2).sum(-1)
+    Pt = inst.alpha[:, None] * np.exp((f[:, None] + h[None, :] - C) / eps)  # P~ (n x m)
+    b0, b1 = row_partition(n, world, rank)
+    S_r = Pt[b0:b1].T @ V[b0:b1]                      # m x ell, this rank's rows
+    r_r = Pt[b0:b1] @ inst.beta                       # r = P~ beta on this rank's rows
+    mb = (m + world - 1) // world
+    blocked = np.zeros((world, ell, mb))              # rank-blocked send buffer
+    for j in range(m):
+        blocked[j // mb, :, j % mb] = S_r[j]
+    send = torch.from_numpy(blocked.reshape(-1).copy())
+    recv = torch.zeros(ell * mb, dtype=torch.float64)
+    # gloo has no reduce_scatter: an all-reduce then this rank's block is the same sum
+    dist.all_reduce(send)
+    recv.copy_(send[rank * ell * mb:(rank + 1) * ell * mb])
+    S_loc = recv.numpy().reshape(ell, mb).T           # mb x ell, ld = mb
+    j0 = min(m, rank * mb)
+    rows = min(m, j0 + mb) - j0
+    G1 = V[b0:b1].T @ (r_r[:, None] * V[b0:b1])
+    cross = S_loc[:rows].T @ (inst.beta[j0:j0 + rows, None] * S_loc[:rows])
+    grad = V[b0:b1].T @ (inst.alpha[b0:b1] - r_r)
+    buf = torch.from_numpy(np.concatenate([G1.ravel(), cross.ravel(), grad]))
+    dist.all_reduce(buf)
+    if rank == 0:
+        q.put((buf.numpy(), Pt, V, inst.alpha, inst.beta))
+    dist.destroy_process_group()
+
+
+def test_two_rank_newton_exchange_matches_unsharded():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_newton_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    buf, Pt, V, a, b = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ell = V.shape[1]
+    r = Pt @ b
+    S = Pt.T @ V
+    ref = np.concatenate([(V.T @ (r[:, None] * V)).ravel(), (S.T @ (b[:, None] * S)).ravel(), V.T @ (a - r)])
+    assert np.max(np.abs(buf - ref)) <= 1e-13 * np.max(np.abs(ref))
+    assert buf.size == 2 * ell * ell + ell
