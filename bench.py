@@ -37,10 +37,13 @@ import numpy as np  # noqa: E402
 
 METRIC = "GCells/s of LSE sweeps (C4 Sinkhorn sweep = 2 LSE passes over n*m cells)"
 UNIT = "GCells/s"
-# FP64 pipe instructions per cell of the on-the-fly d=2 LSE sum kernel:
-# exponent 1 DADD + 2 DFMA; exp2 3 DADD (Cody-Waite) + 5 DFMA (poly) + 1 DFMA (table x poly
-# fused with the accumulate) = 11 issue slots, counted as 2 flops each (FMA-equivalent).
-FP64_SLOTS_PER_CELL = 11
+# FP64 pipe instructions per cell of the on-the-fly d=2 LSE sum kernel (pts_sum12_kernel):
+# exponent 1 DADD + 2 DFMA; exp2 3 DADD (Cody-Waite) + 3 DFMA (degree-3 polynomial, 4096-entry
+# table) + 1 DFMA (table x poly fused with the accumulate) = 10 issue slots, counted as 2
+# flops each (FMA-equivalent).
+FP64_SLOTS_PER_CELL = 10
+SUM_KERNEL = "pts_sum12_kernel<2,8,512,4> (column LSE, on-the-fly d=2, 4096-entry exp2 table)"
+SUM_KERNEL_PROFILE = "ncu_lse_sum12_r02.json"
 
 
 def parse():
@@ -170,7 +173,7 @@ def oracle_sweep_rate(O, inst, ms, threads, reps, warm=0):
     return 2.0 * inst.n * ms / t / 1e9, t, times
 
 
-def read_profile_traffic(name="ncu_lse_sum_kernel.json"):
+def read_profile_traffic(name=SUM_KERNEL_PROFILE):
     path = os.path.join(ROOT, "profiles", name)
     if os.path.exists(path):
         try:
@@ -281,13 +284,14 @@ def cpu_time_to_tol(O):
 
 
 def run_ours(args, world, rank, local):
+    gpu = local
+    if world > 1:
+        # one process per GPU: this rank's GPU is the only one the library sees (set before
+        # anything can initialise CUDA in this process)
+        os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
     import paper_2506_14780_b200 as sk
     from paper_2506_14780_b200 import generators as G
 
-    gpu = local
-    if world > 1:
-        # one process per GPU: this rank's GPU is the only one the library sees
-        os.environ["CUDA_VISIBLE_DEVICES"] = str(local)
     dist = dist_init(world)
     inst = G.config(args.config)
     n, m = inst.n, inst.m
@@ -345,7 +349,7 @@ def run_ours(args, world, rank, local):
     gcells_kernel = cells_local / (ms_kernel * 1e-3) / 1e9
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_nominal, "unit": "TFLOP/s",
                 "frac": achieved / peak_nominal, "traffic": read_profile_traffic(),
-                "kernel": "pts_tile_kernel<2,8,SUM> (column LSE, on-the-fly d=2)",
+                "kernel": SUM_KERNEL,
                 "kernel_ms": ms_kernel, "kernel_gcells_per_s": gcells_kernel,
                 "algorithmic_per_cell": f"{FP64_SLOTS_PER_CELL} FP64 issue slots (x2 flops)",
                 "peak_source": "nominal FP64 pipe: 148 SM x 64 FMA/clk x 2 flops x sm_max_mhz "
@@ -354,7 +358,7 @@ def run_ours(args, world, rank, local):
                 "survey_8d_ceiling_gcells_per_s": 886.0,
                 "frac_vs_survey_8d": gcells_kernel / 886.0,
                 "survey_8d_note": "SURVEY 8(d) counts 21 FP64 slots per cell (exp pinned at 12); this kernel "
-                                  "spends 11 (table-driven exp2), so its 21-slot reading exceeds 1"}
+                                  f"spends {FP64_SLOTS_PER_CELL} (table-driven exp2), so its 21-slot reading exceeds 1"}
 
     # ---- row LSE separately (K1 vs K2)
     ms_row_pass, ms_row_kernel = sk.bench_pass(prob, 1, 0, passes=5)

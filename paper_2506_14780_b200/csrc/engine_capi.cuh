@@ -1229,7 +1229,7 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
     std::lock_guard<std::mutex> lk(P.mu);
     const int64_t n = P.n, m = P.m;
     cudaStream_t s = P.stream;
-    DBuf f, g, V, Wv, Sm;
+    DBuf f, g, V, Wv, Sm, rr;
     f.ensure(n);
     g.ensure(m);
     count_launch();
@@ -1252,7 +1252,8 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
         k_fill<<<grid_for(n * l), AUX_NT, 0, s>>>(V.p, n * l, 1.0 / std::sqrt(static_cast<double>(n)));
         count_launch();
         k_pack_w<<<grid_for(n * kt), AUX_NT, 0, s>>>(V.p, n, n, l, kt, nullptr, Wv.p);
-        plan_for(P, 0, MODE_BLOCK, kt, 8);
+        plan_for(P, 0, which == 4 ? MODE_BLOCK_RS : MODE_BLOCK, kt, 8);
+        if (which == 4) rr.ensure(n);  // 4: the fused S / r = P~ beta pass of the Newton step
     }
     CK(cudaStreamSynchronize(s));
     cudaEvent_t e0, e1;
@@ -1276,6 +1277,7 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
                 sp.k = l;
                 sp.kt = kt;
                 sp.out = Sm.p;
+                if (which == 4) sp.rsum_out = rr.p;
                 plan_pass(P, sp);
             }
         }
@@ -1292,9 +1294,13 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
     if (kernel_ms_per_pass) {
         // the dominant tile kernel alone, on the same stream
         TilePlan tp = which == 1 ? plan_for(P, 1, smode, 0)
-                                 : (which >= 3 ? plan_for(P, 0, MODE_BLOCK, kt, 8) : tsum);
+                                 : (which >= 3 ? plan_for(P, 0, which == 4 ? MODE_BLOCK_RS : MODE_BLOCK, kt, 8) : tsum);
         TileArgs ta = tile_args(P, which == 1 ? 1 : 0, tp, G_NONE);
         if (which >= 3) ta.W = Wv.p;
+        if (which == 4) {
+            ta.out_w = P.tgt.w.p;
+            ta.rsum = P.rsum.p;
+        }
         CK(cudaEventRecord(e0, s));
         for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
         CK(cudaEventRecord(e1, s));

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NTT, 1) pts_sum10_kernel(TileArgs a) {
 //   per cell 1 DADD + D DFMA (u') + 3 DADD (Cody-Waite) + 3 DFMA (p) + 1 DFMA (acc) = 10 (d=2)
 // u' is exact: inputs are staged as (16A, 4X), outputs loaded as (16B, 4Y) -- powers of two.
 // Same partial sums in the same [ib][n_out] layout as pts_tile_kernel<SUM>.
-constexpr double kMagic12 = 6755399445250048.0;  // 1.5 * 2^52 + 1023 * 4096
+constexpr double kMagic12 = 6755399445245952.0;  // 1.5 * 2^52 + 1023 * 4096
 constexpr double kR1 = 0.0001692253858788929;    // (ln2/4096)^k / k!
 constexpr double kR2 = 1.4318615612930102e-08;
 constexpr double kR3 = 8.076910841165457e-13;
@@ -336,7 +336,7 @@ __device__ __forceinline__ double pexp12_acc(double u, const unsigned long long*
     return fma(Tp, p, acc);
 }
 
-template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1>
+template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1, int UNR = 1>
 __global__ void __launch_bounds__(NTT, MINB) pts_sum12_kernel(TileArgs a) {
     SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(NTT, MINB) pts_sum12_kernel(TileArgs a) {
                 sin[t] = (q == 0 ? 16.0 : 4.0) * a.in_pack[c0 * PK + t];
             }
             __syncthreads();
-#pragma unroll 1
+#pragma unroll UNR
             for (int k = 0; k < cnt; ++k) {
                 double x[PK];
 #pragma unroll
@@ -1902,10 +1902,10 @@ KernelInfo make_sum10() {
     return k;
 }
 
-template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1>
+template <int D, int JT, int NTT, int REP, bool FC = false, int MINB = 1, int UNR = 1>
 KernelInfo make_sum12() {
     KernelInfo k;
-    k.fn = reinterpret_cast<const void*>(&pts_sum12_kernel<D, JT, NTT, REP, FC, MINB>);
+    k.fn = reinterpret_cast<const void*>(&pts_sum12_kernel<D, JT, NTT, REP, FC, MINB, UNR>);
     k.jt = JT;
     k.nt = NTT;
     k.smem = static_cast<int>(sizeof(double)) * (4096 * REP + 256 * PK_of<D>::value);
@@ -2020,8 +2020,11 @@ KernelInfo pick_pts(int mode, int kt) {
     // the variants, tools/tune_lse.py)
     static const int sum_variant = std::getenv("SKNR_SUM_VARIANT") ? std::atoi(std::getenv("SKNR_SUM_VARIANT")) : -1;
     if (mode == MODE_SUM && D == 2 && sum_variant >= 0 && sum_variant < 100) return tune_variant(sum_variant);
-    // JT=8, 256 threads, no extra unroll: best of the launch sweep (tools/tune_lse.py)
-    if (mode == MODE_SUM) return make_pts<D, 8, MODE_SUM, 0, 256, 1>();
+    // 4096-entry table (10 FP64 slots per cell), JT=8, 512 threads, 4 table copies, inner
+    // loop unrolled 2x: best of the launch sweep (tools/tune_lse.py, variants 4-69: C4
+    // column LSE 3.08 ms vs 3.57 ms for the 256-entry pts_tile_kernel)
+    if (mode == MODE_SUM) return D == 4 ? make_sum12<4, 6, 512, 4, false, 1, 2>()  // 8 outputs spill at d = 4
+                                        : make_sum12<D, 8, 512, 4, false, 1, 2>();
     if (mode == MODE_MAX) return make_pts<D, 4, MODE_MAX, 0>();
     if (mode == MODE_SUM_CULL) return make_cull<D>();
     if (mode == MODE_SUM_CULL_F32) return make_cull<D, true>();
@@ -2180,6 +2183,17 @@ KernelInfo tune_variant(int v) {
         case 56: return make_sum12<2, 4, 256, 1, false, 3>();
         case 57: return make_sum12<2, 8, 128, 1, false, 4>();
         case 58: return make_sum12<2, 8, 256, 1, false, 1>();
+        case 59: return make_sum12<2, 8, 256, 1, false, 2, 2>();
+        case 60: return make_sum12<2, 8, 256, 1, true, 2, 2>();
+        case 61: return make_sum12<2, 8, 256, 2, false, 2, 2>();
+        case 62: return make_sum12<2, 8, 512, 4, false, 1, 2>();
+        case 63: return make_sum12<2, 8, 512, 1, false, 1, 2>();
+        case 64: return make_sum12<2, 8, 512, 1, false, 1>();
+        case 65: return make_sum12<2, 8, 512, 2, false, 1, 2>();
+        case 66: return make_sum12<2, 8, 512, 4, false, 1, 4>();
+        case 67: return make_sum12<2, 8, 512, 4, true, 1, 2>();
+        case 68: return make_sum12<2, 6, 512, 4, false, 1, 2>();
+        case 69: return make_sum12<2, 8, 384, 4, false, 1, 2>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();

@@ -23,28 +23,42 @@ pytestmark = pytest.mark.gpu
 TOL_POT = 1e-9
 
 
+_ORACLE = {}
+
+
+def _oracle_trajectory(name, K, KN):
+    """The oracle's K SK + KN stable SK-NR iterations (cached: C5's stored and on-the-fly
+    cost modes are checked against the same oracle run)."""
+    if (name, K, KN) not in _ORACLE:
+        c = G.config(name)
+        op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+        ro = O.solve(op, tol=1e-300, max_iter=K)
+        V = smooth_basis(c.x, c.alpha, c.ell)
+        with O.accept_mode("stable"):
+            no = O.solve(op, tol=1e-300, max_iter=KN, ell=c.ell, V=V, init=(ro["f"], ro["g"]))
+        _ORACLE[(name, K, KN)] = (ro, V, no)
+    return _ORACLE[(name, K, KN)]
+
+
 @pytest.mark.parametrize("name,mode,K,KN", [("C3", "auto", 6, 3), ("C4", "auto", 2, 2),
-                                            ("C5", "stored", 2, 2), ("C5", "onthefly", 2, 2)])
+                                            ("C5", "stored", 1, 1), ("C5", "onthefly", 1, 1)])
 def test_full_size_trajectory(name, mode, K, KN):
     c = G.config(name)
     gp = sk.PointProblem(c.x, c.y, c.alpha, c.beta, c.epsilon, c.cost_scale, cost_mode=mode)
-    op = O.Instance(c.alpha, c.beta, c.epsilon, x=c.x, y=c.y, cost_div=1.0 / c.cost_scale)
+    ro, V, no = _oracle_trajectory(name, K, KN)
     rg = sk.solve(gp, tol=1e-300, max_iter=K)
-    ro = O.solve(op, tol=1e-300, max_iter=K)
     assert rel_err(rg.f, ro["f"]) <= TOL_POT and rel_err(rg.g, ro["g"]) <= TOL_POT
     for tg, to in zip(rg.trace, ro["trace"]):
         assert abs(tg.marginal_error - to[0]) <= 1e-9 * to[0]
-    V = smooth_basis(c.x, c.alpha, c.ell)
     basis = sk.SpectralBasis(V, V, np.zeros(c.ell), c.epsilon)
     init = (ro["f"], ro["g"])
     ng = sk.solve(gp, tol=1e-300, max_iter=KN, ell=c.ell, basis=basis, init=init, accept="stable")
-    with O.accept_mode("stable"):
-        no = O.solve(op, tol=1e-300, max_iter=KN, ell=c.ell, V=V, init=init)
     assert [t.newton_accepted for t in ng.trace] == [bool(t[4]) for t in no["trace"]]
     assert rel_err(ng.f, no["f"]) <= TOL_POT and rel_err(ng.g, no["g"]) <= TOL_POT
     for tg, to in zip(ng.trace, no["trace"]):
         assert abs(tg.marginal_error - to[0]) <= 1e-9 * to[0]
-        assert abs(tg.semi_dual_value - to[2]) <= 1e-13 * abs(to[2])
+        # Q = a.f + b.h at the potentials' 1e-12 agreement (literal steps: Q from full LSEs)
+        assert abs(tg.semi_dual_value - to[2]) <= 1e-12 * abs(to[2])
 
 
 @pytest.mark.parametrize("accept", ["stable", "literal"])

@@ -4,7 +4,7 @@ For C1-shaped problems (n = m = 512, eps = 1e-2, ell = 10, eps' = 2e-2 warm star
 basis from the oracle, shared by both sides) and seeds 1..S, run the SK-NR main solve on
 the GPU and on the oracle in both accept modes and count: iterations, iterations where
 the two sides' decisions differ, and those differences above the step noise floor
-(the oracle's step max|f'-f| > 1e-10 max|f|). Writes profiles/accept_modes_r02.json.
+(the oracle's step max|f'-f| > 1e-10 max|f|). Writes gpurun_out/accept_modes_r02.json (copied to profiles/ by hand).
 
   python tools/accept_modes.py [S]
 """
@@ -61,7 +61,8 @@ def main(S):
     out = {"config": "C1 shape (n = m = 512, eps = 1e-2, ell = 10, tol 1e-9), seeds 1..%d; warm start and basis "
                      "from the oracle at eps' = 2e-2, shared" % S,
            "summary": summ, "seeds": rows}
-    json.dump(out, open(os.path.join(ROOT, "profiles", "accept_modes_r02.json"), "w"), indent=1)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(out, open(os.path.join(ROOT, "gpurun_out", "accept_modes_r02.json"), "w"), indent=1)
     print(json.dumps(summ, indent=1))
 
 

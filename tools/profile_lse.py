@@ -1,5 +1,5 @@
 """ncu target: the C4 column-LSE sum tile kernel (and the ell-wide block pass).
-Usage: python tools/profile_lse.py [which] [bits]   which=2 LSE sum kernel, 3 block pass;
+Usage: python tools/profile_lse.py [which] [bits]   which=2 LSE sum kernel, 3 block pass, 4 fused S / r block pass (Newton step);
 bits=32 profiles the opt-in fp32 sum kernel (set_precision(32)); a third argument "cull"
 turns culling on (use which=0: the full column LSE, whose sum pass is then pts_cull_kernel)."""
 import os
