@@ -1036,9 +1036,9 @@ struct PassSpec {
 };
 
 // Input-block cap of a pass's split-K partials: the ell-wide block passes keep at most 8
-// (their partials are kt x n_out each); sum passes and the 2-column register pass are
+// (their partials are kt x n_out each); sum passes and the 4-column anchor pass are
 // split like the LSE sums (enough tiles for every SM).
-static int64_t anchor_in_blocks(int kt) { return kt > 2 ? 8 : 0; }
+static int64_t anchor_in_blocks(int kt) { return kt > 4 ? 8 : 0; }
 
 // Columns of the stable accept test's anchor pass W = (1, expm1(d/eps), exp(d/eps), 0):
 // the register point kernels take 4 columns with DFMA; the DMMA kernels need a multiple of 8.

@@ -1437,7 +1437,8 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     SKNR_API_BEGIN
     Problem& P = get(h);
     std::lock_guard<std::mutex> lk(P.mu);
-    const bool block = variant >= 200 && variant < 300;
+    const bool anchor = variant >= 400 && variant < 500;  // 4-column anchor pass (stable accept test)
+    const bool block = (variant >= 200 && variant < 300) || anchor;
     if ((variant < 100 || variant >= 300) && P.dim != 2) throw InvalidArgument("sknr_tune_variant: needs a d=2 point problem");
     if (variant >= 100 && variant < 200 && P.dim != 0)
         throw InvalidArgument("sknr_tune_variant: needs a stored-cost problem");
@@ -1455,8 +1456,8 @@ int sknr_tune_variant(sknr_problem h, int variant, int passes, double* kernel_ms
     plan_for(P, 0, MODE_MAX, 0);
     lse(P, 0, f.p, g.p, G_NONE);
     lse(P, 0, f.p, g.p, G_NONE);  // leaves the bound-shift pack in place
-    const int kt = 32;
-    TilePlan tp = plan_tiles(P.dim, block ? MODE_BLOCK : MODE_SUM, block ? kt : 0, m, n, block ? 8 : 0, variant);
+    const int kt = anchor ? 4 : 32;
+    TilePlan tp = plan_tiles(P.dim, block ? MODE_BLOCK : MODE_SUM, block ? kt : 0, m, n, block && !anchor ? 8 : 0, variant);
     if (!tp.fn) throw InvalidArgument("sknr_tune_variant: unknown variant");
     P.partial.ensure(static_cast<size_t>(tp.n_in_blocks) * m * (block ? kt : 1));
     TileArgs ta = tile_args(P, 0, tp, G_NONE);

@@ -406,6 +406,105 @@ __global__ void __launch_bounds__(NTT, MINB) pts_sum12_kernel(TileArgs a) {
     }
 }
 
+// ------------------------------------------------------------- stable-accept anchor pass
+// The three column sums of the stable accept test (engine_solver.cuh, k_dh): for each
+// output j, s = sum_i e, t = sum_i e w1_i, u = sum_i e w2_i, with e = P~_ij (unshifted
+// pack: P~ <= 1 by construction) and W = (1, expm1(d/eps), exp(d/eps), 0) in the KT = 4
+// layout of MODE_BLOCK. The exponential is pexp12's (4096-entry table), so a cell costs
+// u' 3 + Cody-Waite 3 + polynomial 3 + s 1 + e 1 + t, u 2 = 13 FP64 slots (the generic
+// 4-column register block pass: 16, at lower occupancy). Partials in the MODE_BLOCK
+// layout [ib][c][n_out], c = 0..2 (column 3 of W is zero and is not written).
+template <int D, int JT, int NTT, int REP, int UNR = 1>
+__global__ void __launch_bounds__(NTT, 1) pts_anchor12_kernel(TileArgs a) {
+    SKNR_PDL_ENTRY();
+    if (guard_skip(a.st, a.guard)) return;
+    constexpr int NT = NTT;
+    constexpr int PK = PK_of<D>::value;
+    constexpr int SK = PK + 2;  // staged row: 16A, 4X[D] (+ pad), w1, w2
+    constexpr int CH = 256;
+    constexpr int TW = 4096 * REP;
+    extern __shared__ __align__(16) double sm[];
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);
+    double* sin = sm + TW;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < TW; t += NT) {
+        const unsigned e = static_cast<unsigned>(t / REP);
+        const unsigned long long v = g_exp2_tab12[e];
+        const unsigned hi = static_cast<unsigned>(v >> 32) - (e << 8);
+        tab[t] = (static_cast<unsigned long long>(hi) << 32) | (v & 0xFFFFFFFFull);
+    }
+    const unsigned laneoff = (tid & (REP - 1)) << 3;
+    double r2 = kR2;
+    asm volatile("" : "+d"(r2));
+    const int64_t out_tile = static_cast<int64_t>(NT) * JT;
+
+    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
+        double B[JT], Y[JT][D], as[JT], at[JT], au[JT];
+        int64_t o[JT];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            o[jt] = ot * out_tile + jt * NT + tid;
+            const int64_t oc = o[jt] < a.n_out ? o[jt] : a.n_out - 1;
+            B[jt] = 16.0 * a.out_pack[oc * PK];
+#pragma unroll
+            for (int d = 0; d < D; ++d) Y[jt][d] = 4.0 * a.out_pack[oc * PK + 1 + d];
+            as[jt] = at[jt] = au[jt] = 0.0;
+        }
+        const int64_t i0 = ib * a.in_block;
+        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+        for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+            const int cnt = static_cast<int>((i1 - c0) < CH ? (i1 - c0) : CH);
+            __syncthreads();
+            for (int t = tid; t < cnt * SK; t += NT) {
+                const int k = t / SK, q = t % SK;
+                sin[t] = q < PK ? (q == 0 ? 16.0 : 4.0) * a.in_pack[(c0 + k) * PK + q]
+                                : a.W[(c0 + k) * 4 + (q - PK + 1)];
+            }
+            __syncthreads();
+#pragma unroll UNR
+            for (int k = 0; k < cnt; ++k) {
+                double x[SK];
+#pragma unroll
+                for (int q = 0; q < SK / 2; ++q) {
+                    const double2 v = reinterpret_cast<const double2*>(sin + k * SK)[q];
+                    x[2 * q] = v.x;
+                    x[2 * q + 1] = v.y;
+                }
+#pragma unroll
+                for (int jt = 0; jt < JT; ++jt) {
+                    double u = x[0] + B[jt];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) u = fma(x[1 + d], Y[jt][d], u);
+                    const double t = u + c_pexp12_k[0];
+                    const double kf = t - c_pexp12_k[0];
+                    const double r = u - kf;
+                    double p = fma(r, c_pexp12_k[3], r2);
+                    p = fma(p, r, c_pexp12_k[1]);
+                    p = fma(p, r, 1.0);
+                    const int kc = (__double2hiint(t) >= kMagicHi) ? __double2loint(t) : 0;
+                    constexpr int SH = REP == 1 ? 3 : (REP == 2 ? 4 : 5);
+                    const unsigned off = ((static_cast<unsigned>(kc) << SH) & (4095u << SH)) | laneoff;
+                    const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
+                    const double Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * 256u + T.y),
+                                                       static_cast<int>(T.x));
+                    as[jt] = fma(Tp, p, as[jt]);
+                    const double e = Tp * p;
+                    at[jt] = fma(e, x[PK], at[jt]);
+                    au[jt] = fma(e, x[PK + 1], au[jt]);
+                }
+            }
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+            if (o[jt] >= a.n_out) continue;
+            a.partial[(ib * 4 + 0) * a.n_out + o[jt]] = as[jt];
+            a.partial[(ib * 4 + 1) * a.n_out + o[jt]] = at[jt];
+            a.partial[(ib * 4 + 2) * a.n_out + o[jt]] = au[jt];
+        }
+    }
+}
+
 // ------------------------------------------------------------- fp32 sum pass (opt-in)
 // MODE_SUM_F32 (sknr_problem_set_precision(p, 32)): the sum pass of pts_tile_kernel with
 // the cell exponent in fp32 and 2^v on the MUFU unit (ex2.approx.ftz.f32). The fp64 pack
@@ -1912,6 +2011,16 @@ KernelInfo make_sum12() {
     return k;
 }
 
+template <int D, int JT, int NTT, int REP, int UNR = 1>
+KernelInfo make_anchor12() {
+    KernelInfo k;
+    k.fn = reinterpret_cast<const void*>(&pts_anchor12_kernel<D, JT, NTT, REP, UNR>);
+    k.jt = JT;
+    k.nt = NTT;
+    k.smem = static_cast<int>(sizeof(double)) * (4096 * REP + 256 * (PK_of<D>::value + 2));
+    return k;
+}
+
 template <int D, int JT, int NTT, int MINB = 1>
 KernelInfo make_f32() {
     KernelInfo k;
@@ -2041,8 +2150,8 @@ KernelInfo pick_pts(int mode, int kt) {
             default: return KernelInfo{};
         }
     }
-    if (mode == MODE_BLOCK && kt == 4)  // 4-column block (stable accept test's anchor pass): DFMA
-        return make_pts<D, 4, MODE_BLOCK, 4, 256, 1>();
+    if (mode == MODE_BLOCK && kt == 4)  // the stable accept test's anchor pass (s, t, u)
+        return D == 4 ? make_anchor12<4, 4, 512, 4, 1>() : make_anchor12<D, 4, 512, 4, 2>();  // tune 400-405
     // FP64 tensor-core (DMMA) block passes. Default: the double-buffered v2 kernel (8 warps,
     // 256-output tiles, 32-input chunks); SKNR_BLOCK_V1=1 selects the round-1 kernel.
     static const bool v1 = std::getenv("SKNR_BLOCK_V1") != nullptr;
@@ -2194,6 +2303,13 @@ KernelInfo tune_variant(int v) {
         case 67: return make_sum12<2, 8, 512, 4, true, 1, 2>();
         case 68: return make_sum12<2, 6, 512, 4, false, 1, 2>();
         case 69: return make_sum12<2, 8, 384, 4, false, 1, 2>();
+        // stable-accept anchor pass, d=2 (timed with W = 1/sqrt(n) in every column)
+        case 400: return make_pts<2, 4, MODE_BLOCK, 4, 256, 1>();
+        case 401: return make_anchor12<2, 6, 512, 4, 1>();
+        case 402: return make_anchor12<2, 4, 512, 4, 1>();
+        case 403: return make_anchor12<2, 6, 512, 4, 2>();
+        case 404: return make_anchor12<2, 8, 512, 4, 1>();
+        case 405: return make_anchor12<2, 4, 512, 4, 2>();
         // stored cost (dim 0)
         case 100: return make_dense<2, MODE_SUM, 0>();
         case 101: return make_dense_v2<1, 4, 256, MODE_SUM>();
