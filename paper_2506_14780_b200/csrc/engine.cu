@@ -437,8 +437,7 @@ static Problem* new_problem(int64_t n, int64_t m, const double* alpha, const dou
     }
     own_stream(p->stream);
     CK(cudaMalloc(&p->st, sizeof(DevState)));
-    CK(cudaMemset(p->st, 0, sizeof(DevState)));
-    CK(cudaDeviceSynchronize());
+    CK(cudaMemsetAsync(p->st, 0, sizeof(DevState), p->stream));
     CK(cudaMallocHost(&p->st_host, sizeof(DevState)));
     setup_side(p->src, alpha, n, p->stream);
     setup_side(p->tgt, beta, m, p->stream);
