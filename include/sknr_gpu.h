@@ -284,6 +284,16 @@ int sknr_bench_mufu_peak(double* gex2_per_s, double* ms);
 /* Tuning aid: device ms of launch variant `variant` of the d=2 column-LSE sum
  * kernel on this problem (tools/tune_lse.py). */
 int sknr_tune_variant(sknr_problem p, int variant, int passes, double* kernel_ms);
+/* Newton block pass S = V^T P~, r = P~ beta (objective.cpp:127-131) on the tensor cores:
+ * tcgen05 int8 GEMMs over exact byte slices of P~ and V (i8_kernels.cu), on by default
+ * for point clouds (d <= 4), ell <= 32 and n*m >= 2^22; 0 selects the FP64 DMMA pass.
+ * Process-wide; applies to plans made afterwards (each setting keeps its own plans). */
+int sknr_set_tensor_block_pass(int on);
+int sknr_get_tensor_block_pass(void);
+/* Testing aid: D[128][n] = A[128][k] (uint8, row-major) x B (int8, given as Bt[n][k]) with
+ * one tcgen05.mma.kind::i8 per 32 inputs, in the block pass's operand layouts (A MN-major,
+ * B K-major); 32 <= n <= 256 and 32 <= k <= 256, multiples of 32. Returns 0 on success. */
+int sknr_probe_i8_mma(const uint8_t* A, const int8_t* Bt, int n, int k, int32_t* D);
 /* Diagnostics: out[0..3] = exact-shift passes (column, row), bound-shift
  * validation failures that triggered the exact retry (column, row); out[4..5] =
  * culling group tests and kept groups (sknr_problem_set_culling). */

@@ -130,6 +130,9 @@ _SIGS = {
     "sknr_bench_mufu_peak": [_D, _D],
     "sknr_tune_variant": [_P, ctypes.c_int, ctypes.c_int, _D],
     "sknr_debug_counters": [_P, ctypes.POINTER(_I64)],
+    "sknr_set_tensor_block_pass": [ctypes.c_int],
+    "sknr_get_tensor_block_pass": [],
+    "sknr_probe_i8_mma": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p],
     "sknr_comm_unique_id": [ctypes.c_void_p],
     "sknr_comm_init": [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int],
     "sknr_comm_destroy": [],
@@ -941,6 +944,28 @@ def anneal(problem: Problem, epsilons: Sequence[float], warm: str = "spectral", 
 
 
 # ---------------------------------------------------------------- measurement
+def set_tensor_block_pass(on: bool) -> bool:
+    """Select the tensor-core (tcgen05 int8 slice) Newton block pass (default) or the FP64
+    DMMA pass for plans made afterwards; returns the previous setting."""
+    prev = bool(lib().sknr_get_tensor_block_pass())
+    _check(lib().sknr_set_tensor_block_pass(1 if on else 0))
+    return prev
+
+
+def probe_i8_mma(A: np.ndarray, Bt: np.ndarray) -> np.ndarray:
+    """D = A @ Bt.T on one tcgen05 int8 GEMM (A: 128 x k uint8, Bt: n x k int8)."""
+    A = np.ascontiguousarray(A, dtype=np.uint8)
+    Bt = np.ascontiguousarray(Bt, dtype=np.int8)
+    n, k = Bt.shape
+    if A.shape != (128, k):
+        raise ValueError("probe_i8_mma: A must be 128 x k")
+    D = np.zeros((128, n), dtype=np.int32)
+    rc = lib().sknr_probe_i8_mma(A.ctypes.data, Bt.ctypes.data, n, k, D.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"probe_i8_mma failed ({rc})")
+    return D
+
+
 def bench_pass(problem: Problem, which: int, ell: int = 0, passes: int = 5):
     ms, kms = ctypes.c_double(), ctypes.c_double()
     _check(lib().sknr_bench_pass(problem.handle, int(which), int(ell), int(passes), ctypes.byref(ms),

@@ -326,6 +326,7 @@ struct Problem {
     // per-direction LSE state
     DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
     DBuf partial, rsum;
+    DBuf vsl, vexp;  // tensor-core block pass: V digit tiles, column exponents (i8_kernels.cu)
     std::shared_ptr<SolveState> solve_cache;  // per-solve device buffers, reused across solves
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
@@ -349,7 +350,7 @@ struct Problem {
         if (st_host) cudaFreeHost(st_host);
     }
 
-    std::map<std::tuple<int, int, int, int64_t>, TilePlan> plans;
+    std::map<std::tuple<int, int, int, int64_t, bool>, TilePlan> plans;
 
     // row sharding: this handle holds source rows [row_begin, row_begin + n)
     bool shard = false;
@@ -805,7 +806,7 @@ static void gather_rows(Problem& P, const double* dev_local, double* host_full) 
 // ============================================================ passes
 static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_blocks = 0) {
     const int64_t nout = dir == 0 ? P.m : P.n, nin = dir == 0 ? P.n : P.m;
-    const auto key = std::make_tuple(dir, mode, kt, max_in_blocks);
+    const auto key = std::make_tuple(dir, mode, kt, max_in_blocks, i8_block_enabled());
     auto it = P.plans.find(key);
     if (it != P.plans.end()) return it->second;
     TilePlan tp = plan_tiles(P.dim, mode, kt, nout, nin, max_in_blocks);
@@ -815,6 +816,10 @@ static TilePlan plan_for(Problem& P, int dir, int mode, int kt, int64_t max_in_b
     const size_t need = static_cast<size_t>(tp.n_in_blocks) * nout * (blk ? kt : 1);
     P.partial.ensure(need);
     if (mode == MODE_BLOCK_RS) P.rsum.ensure(static_cast<size_t>(tp.n_out_tiles) * nin);
+    if (tp.i8) {
+        P.vsl.ensure(static_cast<size_t>(i8_vslice_bytes(nin) / 8));
+        P.vexp.ensure(16);
+    }
     return tp;
 }
 
@@ -1114,6 +1119,14 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
     if (rs) {
         ta.out_w = out.w.p;
         ta.rsum = P.rsum.p;
+    }
+    if (tp.i8) {  // tensor-core pass: V as exact int8 digit tiles (rebuilt per pass, O(n kt))
+        uint8_t* vsl = reinterpret_cast<uint8_t*>(P.vsl.p);
+        unsigned* vexp = reinterpret_cast<unsigned*>(P.vexp.p);
+        launch_i8_vprep(ps.W, ps.kt, nin, vsl, vexp, P.st, ps.guard, s);
+        ta.vsl = vsl;
+        ta.vexp = vexp;
+        ta.kt = ps.kt;
     }
     launch_tiles(tp, ta, s);
     if (rs) {

@@ -1301,6 +1301,11 @@ int sknr_bench_pass(sknr_problem h, int which, int64_t ell, int passes, double* 
             ta.out_w = P.tgt.w.p;
             ta.rsum = P.rsum.p;
         }
+        if (tp.i8) {  // digit tiles of Wv, built by the plan_pass calls above
+            ta.vsl = reinterpret_cast<const uint8_t*>(P.vsl.p);
+            ta.vexp = reinterpret_cast<const unsigned*>(P.vexp.p);
+            ta.kt = kt;
+        }
         CK(cudaEventRecord(e0, s));
         for (int t = 0; t < passes; ++t) launch_tiles(tp, ta, s);
         CK(cudaEventRecord(e1, s));
@@ -1401,6 +1406,14 @@ __global__ void k_mufu_peak(float* out, int iters, float a0) {
     for (int c = 0; c < 8; ++c) s += x[c];
     if (s == 12345.678f) out[0] = s;
 }
+
+int sknr_set_tensor_block_pass(int on) {
+    SKNR_API_BEGIN
+    set_i8_block_enabled(on != 0);
+    SKNR_API_END
+}
+
+int sknr_get_tensor_block_pass(void) { return i8_block_enabled() ? 1 : 0; }
 
 int sknr_bench_mufu_peak(double* gex2_per_s, double* ms) {
     SKNR_API_BEGIN

@@ -51,10 +51,15 @@ struct TileArgs {
     int dir = 0;
     int retry_phase = 0;
     unsigned* sched = nullptr;         // dynamic tile counter (zeroed by the preceding k_group_max)
+    // tensor-core (int8 slice) block pass, i8_kernels.cu
+    const uint8_t* vsl = nullptr;      // V digit tiles, 7168 bytes per 32-input chunk
+    const unsigned* vexp = nullptr;    // per column: 2048 + largest exponent (0: zero column)
+    int kt = 0;                        // columns of W (<= 32)
 };
 
 struct TilePlan {
     const void* fn = nullptr;
+    bool i8 = false;                   // pts_i8_kernel: needs launch_i8_vprep on W first
     int grid = 0, smem = 0, occ = 0, nt = 128;
     int64_t out_tile = 0, in_block = 0, n_out_tiles = 0, n_in_blocks = 0, n_tiles = 0;
 };
@@ -65,6 +70,18 @@ TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int6
 void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s);
 int block_kt_for(int k);
 int chunk_inputs(int mode, int kt);
+
+// Newton block pass S = V^T P~ / r = P~ beta on the tensor cores (i8_kernels.cu)
+const void* i8_block_kernel(int d);
+bool i8_block_enabled();
+void set_i8_block_enabled(bool on);
+int i8_block_smem();
+int i8_block_threads();
+int i8_block_out_tile();
+int i8_max_in_block();
+int64_t i8_vslice_bytes(int64_t n_in);
+void launch_i8_vprep(const double* W, int kt, int64_t n_in, uint8_t* vsl, unsigned* vexp, const DevState* st,
+                     unsigned guard, cudaStream_t s);
 
 void count_launch();
 int64_t launch_count();

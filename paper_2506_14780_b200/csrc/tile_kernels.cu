@@ -25,6 +25,7 @@
 // transform, C^T for the column transform), so a warp's 32 loads of one input
 // are one coalesced 256 B request and every fp64 cost element is read once per
 // pass: 8 B/cell, the HBM roofline of BASELINE.md section 4.
+#include <atomic>
 #include <cstdlib>
 
 #include "internal.h"
@@ -2392,9 +2393,63 @@ int chunk_inputs(int mode, int kt) {
     return kt > 32 ? 32 : 64;
 }
 
+// Tensor-core Newton block pass (i8_kernels.cu): on unless SKNR_BLOCK_I8=0.
+static std::atomic<int> g_i8_on{-1};
+bool i8_block_enabled() {
+    int v = g_i8_on.load();
+    if (v < 0) {
+        const char* e = std::getenv("SKNR_BLOCK_I8");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_i8_on.store(v);
+    }
+    return v != 0;
+}
+void set_i8_block_enabled(bool on) { g_i8_on.store(on ? 1 : 0); }
+
+static int sm_count_cached() {
+    static thread_local int sm_count = 0;
+    if (sm_count == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (sm_count <= 0) sm_count = 148;
+    }
+    return sm_count;
+}
+
+// 128-output tiles x input blocks of <= 8192 inputs (int32 level bound), multiples of 32;
+// one CTA per SM (persistent).
+static TilePlan plan_i8(int dim, int64_t n_out, int64_t n_in, int64_t max_in_blocks) {
+    TilePlan p;
+    p.fn = i8_block_kernel(dim);
+    if (!p.fn) return p;
+    p.i8 = true;
+    p.smem = i8_block_smem();
+    p.nt = i8_block_threads();
+    cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+    p.occ = 1;
+    const int64_t resident = sm_count_cached();
+    p.out_tile = i8_block_out_tile();
+    p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
+    int64_t want = (8 * resident + p.n_out_tiles - 1) / p.n_out_tiles;
+    if (max_in_blocks > 0 && want > max_in_blocks) want = max_in_blocks;
+    if (want < 1) want = 1;
+    int64_t in_block = (n_in + want - 1) / want;
+    in_block = ((in_block + 31) / 32) * 32;
+    if (in_block > i8_max_in_block()) in_block = i8_max_in_block();
+    p.in_block = in_block;
+    p.n_in_blocks = (n_in + in_block - 1) / in_block;
+    p.n_tiles = p.n_out_tiles * p.n_in_blocks;
+    p.grid = static_cast<int>(p.n_tiles < resident ? p.n_tiles : resident);
+    return p;
+}
+
 TilePlan plan_tiles(int dim, int mode, int kt, int64_t n_out, int64_t n_in, int64_t max_in_blocks,
                     int variant) {
     TilePlan p;
+    if (variant < 0 && mode == MODE_BLOCK_RS && dim >= 1 && dim <= 4 && kt <= 32 && i8_block_enabled() &&
+        n_out * n_in >= (int64_t(1) << 22))
+        return plan_i8(dim, n_out, n_in, max_in_blocks);
     // the stored cost's leading dimension equals n_out in both directions
     KernelInfo ki = variant >= 0 ? tune_variant(variant) : pick(dim, mode, kt, n_out % 2 == 0);
     if (!ki.fn) return p;
