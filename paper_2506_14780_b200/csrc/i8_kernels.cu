@@ -20,22 +20,23 @@
 // (below the rounding of an FP64 product), and P~'s own representation error is 2^-52.
 // One int32 level accumulates at most 7 * 8192 * 255 * 128 < 2^31 per tile (in_block <= 8192).
 //
-// Work unit: 128 outputs j (MMA M) x an input block; per 32-input chunk (MMA K) the 8 warps
-// generate the 128 x 32 cells of P~ (warp w: outputs 16w..16w+15, lane: input) with the
-// FP64 exponential of pts_sum12_kernel (4096-entry table, u' = 16u exact), accumulate
-// r_i += P~_ij beta_j in FP64, and store the 7 byte slices as MN-major (j contiguous) int8
-// tiles into a 4-stage shared-memory ring; one elected thread then issues 7 tcgen05.mma
-// (A = slice a, B = the chunk's V digit tile [7 x 32 columns, K-major, fetched by a bulk
-// copy], D = TMEM columns 32a.. so that product (a, b) lands on level a + b) and commits
-// them to the stage's mbarrier. The tile's 8 levels x 32 columns of int32 live in TMEM
-// (256 columns); at the end of the tile warps 0-3 read them back (tcgen05.ld), combine the
-// levels in FP64 and write the split-K partial in the layout of the FP64 kernels.
+// Tile: 128 outputs j (MMA M) x an input block; per 32-input chunk (MMA K) the producer
+// warps generate the 128 x 32 cells of P~ with the FP64 exponential of pts_sum12_kernel
+// (4096-entry table, u' = 16u exact), accumulate r_i += P~_ij beta_j in FP64, and store the
+// byte slices as MN-major (j contiguous) int8 tiles into a 4-stage shared-memory ring; one
+// elected thread then issues 8 tcgen05.mma (A = slice a, B = the chunk's V digit tile
+// [7 x 32 columns, K-major, fetched by a bulk copy], D = TMEM columns 32a.. so that product
+// (a, b) lands on level a + b) and commits them to the stage's mbarrier. A tile's 8 levels
+// x 32 columns of int32 live in TMEM (256 columns); after every input block they are read
+// back (tcgen05.ld) and combined in FP64 into the split-K partial. See pts_i8w_kernel for
+// the warp roles and the work units.
 //
 // Precondition: P~_ij <= 1 (+ rounding), i.e. the pass is taken at the anchor h = f^{C,eps}
 // whose columns of P~ sum to 1 (objective.cpp:127-131); engine.cu only routes the Newton S
 // pass here.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -47,10 +48,8 @@ __device__ const unsigned long long g_exp2_tab12_i8[4096] = {
 };
 
 namespace i8 {
-constexpr int NT = 256;              // 8 warps
-constexpr int NW = NT / 32;
-constexpr int MT = 128;              // outputs per tile (MMA M); warp w: outputs 16w..16w+15
-constexpr int KC = 32;               // inputs per chunk (MMA K for kind::i8); lane = input
+constexpr int MT = 128;              // outputs per tile (MMA M)
+constexpr int KC = 32;               // inputs per chunk (MMA K for kind::i8)
 constexpr int NSL = 7;               // byte slices of P~ and digits of V
 constexpr int NLEV = 8;              // levels kept
 constexpr int A_SLICE = MT * KC;     // 4096 bytes per slice tile
@@ -58,10 +57,6 @@ constexpr int A_BYTES = (NSL + 1) * A_SLICE;  // + the signed low slice (slot 7)
 constexpr int B_BYTES = NSL * 32 * KC;  // 7 digits x 32 columns x 32 inputs = 7168
 constexpr int STAGES = 4;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int OFF_TAB = STAGES * STAGE_BYTES;
-constexpr int OFF_RS = OFF_TAB + 4096 * 8;
-constexpr int OFF_BAR = OFF_RS + 2 * NW * 32 * 8;
-constexpr int SMEM = OFF_BAR + 256;
 constexpr int TMEM_COLS = 256;
 constexpr int MAX_IN_BLOCK = 8192;
 // instruction descriptor: D s32 (bits 4-5 = 2), A u8 (7-9 = 0), B s8 (10-12 = 1),
@@ -104,15 +99,17 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
 }
 
+// try_wait with a suspend-time hint (ns): a waiting warp sleeps in hardware instead of
+// re-issuing the test (the producers' and service warps' polls took 14 % of the issue slots)
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@P1 bra DONE_%=;\n\t"
         "bra WAIT_%=;\n"
         "DONE_%=:\n\t}\n" ::"r"(mbar),
-        "r"(parity)
+        "r"(parity), "r"(2000u)
         : "memory");
 }
 
@@ -299,28 +296,82 @@ constexpr double kI8R3 = 8.076910841165457e-13;
 constexpr int kI8MagicHi = 0x43380000;
 constexpr double kI8MagicLo = 6755399441055744.0;  // 1.5 * 2^52: low word = rint(x), |x| < 2^31
 
+// ------------------------------------------------------------- fused block pass, warp-specialised
+// No CTA-wide barrier sits in the chunk loop (the first version -- 8 warps of 16 outputs, one
+// __syncthreads per chunk, r sums and MMA issue on the compute warps -- left the FP64 pipe
+// idle two thirds of the time, profiles/ncu_block_i8_v1_r02.json):
+//   16 producer warps (warp w: 16 outputs x 16 inputs of the chunk, a lane pair per input, 8
+//     outputs per lane) generate P~, the byte slices (one 8-byte store per slice: half a
+//     16-output core-matrix row, a warp's stores contiguous) and the r terms, then arrive
+//     on the stage's `full` mbarrier (one arrival per warp);
+//   4 service warps: one waits for `full` and the V tile and issues the chunk's 8
+//     tcgen05.mma, committed to the stage's `free` mbarrier; two add the 16 r terms of each
+//     input in a fixed order (even / odd chunks) and arrive on `free` as well; one fetches
+//     the V digit tiles. (With the r sums on the MMA warp its serial latency, ~2000 cycles
+//     per chunk, set the pace of the whole CTA.)
+// Producers only wait for `free` of the stage they are about to refill, so they run up to
+// STAGES chunks ahead of the tensor cores and of each other. At the end of a tile all 16
+// producer warps read the levels back (lane group w % 4, columns 8 (w / 4)..+7), and the
+// MMA warp waits for their `drained` arrivals before the next tile's first MMA.
+namespace i8w {
+constexpr int NPW = 16;                       // producer warps
+constexpr int NT = (NPW + 4) * 32;            // + the MMA warp's warpgroup (setmaxnreg is per warpgroup)
+constexpr int OW = i8::MT / NPW;              // outputs per producer warp = 8
+constexpr int OFF_TAB = i8::STAGES * i8::STAGE_BYTES;
+constexpr int OFF_RS = OFF_TAB + 4096 * 8;
+constexpr int OFF_BAR = OFF_RS + i8::STAGES * NPW * 32 * 8;
+constexpr int SMEM = OFF_BAR + 256;
+// barriers: [0..3] free, [4..7] V tile landed, [8..11] full, [12] accumulators ready, [13] drained
+constexpr int B_FREE = 0, B_VT = i8::STAGES, B_FULL = 2 * i8::STAGES, B_ACC = 3 * i8::STAGES, B_DRAIN = B_ACC + 1;
+}  // namespace i8w
+
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z)
+                 : "memory");
+}
+
 template <int D>
-__global__ void __launch_bounds__(i8::NT, 1) pts_i8_kernel(TileArgs a) {
+__global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
     SKNR_PDL_ENTRY();
     if (guard_skip(a.st, a.guard)) return;
     constexpr int PK = ((D + 2) / 2) * 2;
+    constexpr int OW = i8w::OW;
     extern __shared__ __align__(1024) uint8_t sm8[];
     uint8_t* stages = sm8;
-    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm8 + i8::OFF_TAB);
-    double* rs = reinterpret_cast<double*>(sm8 + i8::OFF_RS);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm8 + i8::OFF_BAR);
-    // bars[0..3] stage free (MMA done), bars[4..7] V tile landed, bars[8] tile accumulators ready
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * i8::STAGES + 1);
+    unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm8 + i8w::OFF_TAB);
+    double* rs = reinterpret_cast<double*>(sm8 + i8w::OFF_RS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm8 + i8w::OFF_BAR);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + i8w::B_DRAIN + 1);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    for (int t = tid; t < 4096; t += i8::NT) {  // 2^(e/4096), hi word pre-biased by -(e << 8)
+    for (int t = tid; t < 4096; t += i8w::NT) {  // 2^(e/4096), hi word pre-biased by -(e << 8)
         const unsigned e = static_cast<unsigned>(t);
         const unsigned long long v = g_exp2_tab12_i8[e];
         const unsigned hi = static_cast<unsigned>(v >> 32) - (e << 8);
         tab[t] = (static_cast<unsigned long long>(hi) << 32) | (v & 0xFFFFFFFFull);
     }
     if (tid == 0) {
-        for (int q = 0; q < 2 * i8::STAGES + 1; ++q) mbar_init(smem_u32(bars + q), 1);
+        for (int q = 0; q < i8::STAGES; ++q) {
+            mbar_init(smem_u32(bars + i8w::B_FREE + q), 2);  // MMAs completed + r terms read
+            mbar_init(smem_u32(bars + i8w::B_VT + q), 1);
+            mbar_init(smem_u32(bars + i8w::B_FULL + q), i8w::NPW);
+        }
+        mbar_init(smem_u32(bars + i8w::B_ACC), 1);
+        mbar_init(smem_u32(bars + i8w::B_DRAIN), i8w::NPW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tmem_alloc(smem_u32(tslot));
@@ -328,165 +379,247 @@ __global__ void __launch_bounds__(i8::NT, 1) pts_i8_kernel(TileArgs a) {
     __syncthreads();
     tc_after_sync();
     const uint32_t tbase = *tslot;
-    const uint32_t trow = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    if (warp < 4) {  // TMEM starts undefined: zero this warp's 32 lanes x 256 columns
+    // this producer warp's part of the accumulators: lanes 32 (w % 4).., columns 8 (w / 4)..+7 per level
+    const uint32_t tmine = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16) + static_cast<uint32_t>((warp >> 2) * 8);
+    if (warp < i8w::NPW) {  // TMEM starts undefined
 #pragma unroll
-        for (int w = 0; w < i8::NLEV; ++w) tmem_zero32(trow + w * 32);
+        for (int w = 0; w < i8::NLEV; ++w) tmem_zero8(tmine + w * 32);
         tmem_wait_st();
     }
     tc_before_sync();
     __syncthreads();
+    tc_after_sync();
 
-    const double r2 = reg_const(kI8R2);
-    const double c59 = reg_const(0x1p59), cm59 = reg_const(-0x1p59), c60 = reg_const(0x1p60);
-    // A-slice address of this thread's row: input `lane`, the warp's 16 outputs (one
-    // 16-byte row of an MN-major core matrix of 16 outputs x 8 inputs); a warp's stores
-    // cover 512 contiguous bytes
-    uint32_t g = 0;        // chunks issued by this CTA
-    uint32_t ntile = 0;    // tiles finished by this CTA
-    for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x, ++ntile) {
-        const int64_t ot = tile % a.n_out_tiles, ib = tile / a.n_out_tiles;
-        // this warp's 16 outputs: (16B, 4Y) exact, beta
-        double Bj[16], Yj[16][D], Wj[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            int64_t o = ot * i8::MT + warp * 16 + q;
-            Wj[q] = o < a.n_out ? a.out_w[o] : 0.0;
-            o = o < a.n_out ? o : a.n_out - 1;
-            Bj[q] = 16.0 * a.out_pack[o * PK];
-#pragma unroll
-            for (int d = 0; d < D; ++d) Yj[q][d] = 4.0 * a.out_pack[o * PK + 1 + d];
-        }
-        const int64_t i0 = ib * a.in_block;
-        const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
-        double xn0, Xn[D];
-        {
-            const int64_t ic = (i0 + lane < i1) ? i0 + lane : i1 - 1;
-            xn0 = 16.0 * a.in_pack[ic * PK];
-#pragma unroll
-            for (int d = 0; d < D; ++d) Xn[d] = 4.0 * a.in_pack[ic * PK + 1 + d];
-        }
-        for (int64_t c0 = i0; c0 < i1; c0 += i8::KC, ++g) {
-            const uint32_t s = g % i8::STAGES, use = g / i8::STAGES;
-            uint8_t* sA = stages + s * i8::STAGE_BYTES;
-            uint8_t* sB = sA + i8::A_BYTES;
-            const int64_t i = c0 + lane;
-            const bool ok = i < i1;
-            double x0 = xn0, X[D];
-#pragma unroll
-            for (int d = 0; d < D; ++d) X[d] = Xn[d];
-            if (!ok) x0 = -1.0e300;  // e = 0: every byte slice 0, no contribution
-            if (c0 + i8::KC < i1) {  // prefetch the next chunk's inputs (hidden by this chunk)
-                const int64_t inx = (i + i8::KC < i1) ? i + i8::KC : i1 - 1;
-                xn0 = 16.0 * a.in_pack[inx * PK];
-#pragma unroll
-                for (int d = 0; d < D; ++d) Xn[d] = 4.0 * a.in_pack[inx * PK + 1 + d];
-            }
-            if (use > 0) mbar_wait(smem_u32(bars + s), (use - 1) & 1u);
-            if (tid == 0) {
-                mbar_expect_tx(smem_u32(bars + i8::STAGES + s), i8::B_BYTES);
-                bulk_g2s(smem_u32(sB), a.vsl + (c0 >> 5) * i8::B_BYTES, i8::B_BYTES, smem_u32(bars + i8::STAGES + s));
-            }
-            double rt = 0.0;
-            uint32_t wl[4][4], wh[4][3], wq[4];  // [group of 4 outputs][byte], low slice
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t lo[4], hi[4], ql[4];
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq) {
-                    const int q = q4 * 4 + qq;
-                    double u = x0 + Bj[q];
-#pragma unroll
-                    for (int d = 0; d < D; ++d) u = fma(X[d], Yj[q][d], u);
-                    const double t = u + kI8Magic;
-                    const double kf = t - kI8Magic;
-                    const double r = u - kf;
-                    double p = fma(r, kI8R3, r2);
-                    p = fma(p, r, kI8R1);
-                    p = fma(p, r, 1.0);
-                    const int kc = (__double2hiint(t) >= kI8MagicHi) ? __double2loint(t) : 0;
-                    const unsigned off = (static_cast<unsigned>(kc) << 3) & (4095u << 3);
-                    const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
-                    const double Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * 256u + T.y),
-                                                       static_cast<int>(T.x));
-                    const double e = Tp * p;
-                    rt = fma(e, Wj[q], rt);
-                    const double tf = e + 2.0;  // mantissa = P~ in 2^-51 units
-                    lo[qq] = static_cast<uint32_t>(__double2loint(tf));
-                    hi[qq] = static_cast<uint32_t>(__double2hiint(tf));
-                    // residual e - (tf - 2), exact, as rint(. 2^59) in the low word of tq
-                    const double nh = fma(tf, cm59, c60);  // -(tf - 2) 2^59, exact
-                    const double tq = fma(e, c59, nh) + kI8MagicLo;
-                    ql[qq] = static_cast<uint32_t>(min(__double2loint(tq), 127));
-                }
-                byte_transpose<4>(lo[0], lo[1], lo[2], lo[3], wl[q4]);
-                byte_transpose<3>(hi[0], hi[1], hi[2], hi[3], wh[q4]);
-                wq[q4] = prmt(prmt(ql[0], ql[1], 0x40), prmt(ql[2], ql[3], 0x40), 0x5410);
-            }
-            // slice tiles: byte k of t at sA + k*4096, the signed low slice at slot 7
-            uint8_t* dst = sA + warp * 512 + lane * 16;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                *reinterpret_cast<uint4*>(dst + k * i8::A_SLICE) = make_uint4(wl[0][k], wl[1][k], wl[2][k], wl[3][k]);
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                *reinterpret_cast<uint4*>(dst + (4 + k) * i8::A_SLICE) =
-                    make_uint4(wh[0][k], wh[1][k], wh[2][k], wh[3][k]);
-            *reinterpret_cast<uint4*>(dst + 7 * i8::A_SLICE) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
-            rs[(g & 1u) * (i8::NW * 32) + warp * 32 + lane] = rt;
-            fence_proxy_async();
-            __syncthreads();
-            if (warp == i8::NW - 1 && ok) {  // r partial of this chunk: the warps' sums in fixed order
-                const double* rr = rs + (g & 1u) * (i8::NW * 32) + lane;
-                double v = rr[0];
-#pragma unroll
-                for (int w = 1; w < i8::NW; ++w) v += rr[w * 32];
-                a.rsum[ot * a.n_in + i] = v;
-            }
-            if (tid == 0) {
-                mbar_wait(smem_u32(bars + i8::STAGES + s), use & 1u);
+    uint32_t g = 0;      // chunks seen by this CTA
+    uint32_t ntile = 0;  // (output tile, input block) pairs finished by this CTA
+    // work units: i8_og output tiles x i8_ig input blocks; n_out_tiles / n_in_blocks count the
+    // unit rows (= rows of rsum / partial), i8_out_tiles / i8_in_blocks the tiles themselves
+    const int64_t n_units = a.n_out_tiles * a.n_in_blocks;
+    if (warp >= i8w::NPW) {
+        // ------------------------------------------------------------------ service warps
+        // (their warpgroup gives registers back to the producers: 640 x 96 at launch ->
+        // 512 x 112 + 128 x 32). Each walks the CTA's chunk sequence on its own:
+        //   warp 16    tcgen05.mma issue (one elected lane)
+        //   warp 17/18 r terms of the even / odd chunks
+        //   warp 19    V digit tiles (bulk copies) one ring round ahead
+        // A stage is free again when its MMAs have completed AND its r terms have been
+        // read (`free` counts two arrivals).
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
+        const int role = warp - i8w::NPW;
+        for (int64_t unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+            const int64_t ogi = unit % a.n_out_tiles, igi = unit / a.n_out_tiles;
+            const int64_t ot0 = ogi * a.i8_og, ot1 = (ot0 + a.i8_og < a.i8_out_tiles) ? ot0 + a.i8_og : a.i8_out_tiles;
+            const int64_t ib0 = igi * a.i8_ig, ib1 = (ib0 + a.i8_ig < a.i8_in_blocks) ? ib0 + a.i8_ig : a.i8_in_blocks;
+            double* rrow = a.rsum + ogi * a.n_in;  // this unit's r terms: row ogi, inputs of blocks ib0..ib1-1
+            for (int64_t ot = ot0; ot < ot1; ++ot)
+            for (int64_t ib = ib0; ib < ib1; ++ib, ++ntile) {
+            const int64_t i0 = ib * a.in_block;
+            const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+            if (role == 0 && ntile > 0) {  // the previous tile's levels have been read and zeroed
+                mbar_wait(smem_u32(bars + i8w::B_DRAIN), (ntile - 1) & 1u);
                 tc_after_sync();
-                const uint64_t bd = umma_desc(smem_u32(sB), 128, 256);
+            }
+            for (int64_t c0 = i0; c0 < i1; c0 += i8::KC, ++g) {
+                const uint32_t s = g % i8::STAGES, use = g / i8::STAGES;
+                uint8_t* sA = stages + s * i8::STAGE_BYTES;
+                uint8_t* sB = sA + i8::A_BYTES;
+                if (role == 0) {
+                    if (lane == 0) {
+                        mbar_wait(smem_u32(bars + i8w::B_FULL + s), use & 1u);
+                        mbar_wait(smem_u32(bars + i8w::B_VT + s), use & 1u);
+                        tc_after_sync();
+                        const uint64_t bd = umma_desc(smem_u32(sB), 128, 256);
 #pragma unroll
-                for (int sa = 0; sa < i8::NSL; ++sa) {  // P~ slice sa = byte 6 - sa
-                    const int nb = (i8::NLEV - sa) < i8::NSL ? (i8::NLEV - sa) : i8::NSL;
-                    const uint64_t ad = umma_desc(smem_u32(sA + (6 - sa) * i8::A_SLICE), 128, 512);
-                    mma_i8(tbase + sa * 32, ad, bd, i8::IDESC | (static_cast<uint32_t>(nb * 32 >> 3) << 17), 1u);
+                        for (int sa = 0; sa < i8::NSL; ++sa) {  // P~ slice sa = byte 6 - sa
+                            const int nb = (i8::NLEV - sa) < i8::NSL ? (i8::NLEV - sa) : i8::NSL;
+                            const uint64_t ad = umma_desc(smem_u32(sA + (6 - sa) * i8::A_SLICE), 128, 512);
+                            mma_i8(tbase + sa * 32, ad, bd, i8::IDESC | (static_cast<uint32_t>(nb * 32 >> 3) << 17), 1u);
+                        }
+                        mma_i8(tbase + 7 * 32, umma_desc(smem_u32(sA + 7 * i8::A_SLICE), 128, 512), bd, i8::IDESC_LO,
+                               1u);
+                        mma_commit(smem_u32(bars + i8w::B_FREE + s));
+                        if (c0 + i8::KC >= i1) mma_commit(smem_u32(bars + i8w::B_ACC));
+                    }
+                    __syncwarp();
+                } else if (role == 3) {
+                    if (lane == 0) {
+                        if (use > 0) mbar_wait(smem_u32(bars + i8w::B_FREE + s), (use - 1) & 1u);
+                        mbar_expect_tx(smem_u32(bars + i8w::B_VT + s), i8::B_BYTES);
+                        bulk_g2s(smem_u32(sB), a.vsl + (c0 >> 5) * i8::B_BYTES, i8::B_BYTES,
+                                 smem_u32(bars + i8w::B_VT + s));
+                    }
+                    __syncwarp();
+                } else if (static_cast<int>(g & 1u) == role - 1) {
+                    // r accumulates over the unit's output tiles in this row (L2-resident
+                    // read-modify-write; the load overlaps the wait below)
+                    const bool rok = c0 + lane < i1;
+                    double rold = 0.0;
+                    if (rok && ot > ot0) rold = rrow[c0 + lane];
+                    mbar_wait(smem_u32(bars + i8w::B_FULL + s), use & 1u);
+                    // r of input `lane` over the tile's 128 outputs: the 16 producer terms
+                    // (output group 0..7, half 0..1) as a fixed pairwise tree; producer warp
+                    // 2 og + (lane >> 4) holds them in lanes 2 (lane & 15) + half
+                    const double* rr = rs + s * (i8w::NPW * 32) + (lane >> 4) * 32 + 2 * (lane & 15);
+                    double q[i8w::NPW / 2];
+#pragma unroll
+                    for (int og = 0; og < i8w::NPW / 2; ++og) {
+                        const double2 pr = *reinterpret_cast<const double2*>(rr + og * 64);
+                        q[og] = pr.x + pr.y;
+                    }
+                    const double v = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+                    if (rok) rrow[c0 + lane] = rold + v;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_FREE + s));
                 }
-                // signed low slice x V's leading digit -> level 7
-                mma_i8(tbase + 7 * 32, umma_desc(smem_u32(sA + 7 * i8::A_SLICE), 128, 512), bd, i8::IDESC_LO, 1u);
-                mma_commit(smem_u32(bars + s));
-                if (c0 + i8::KC >= i1) mma_commit(smem_u32(bars + 2 * i8::STAGES));
+            }
             }
         }
-        // tile done: levels -> FP64 split-K partial (warps 0-3, lane = output row)
-        if (warp < 4) {
-            mbar_wait(smem_u32(bars + 2 * i8::STAGES), ntile & 1u);
-            tc_after_sync();
-            double acc[32];
+    } else {
+        // ------------------------------------------------------------------ producer warps
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+        const double r2 = reg_const(kI8R2);
+        const double c59 = reg_const(0x1p59), cm59 = reg_const(-0x1p59);
+        // 2^60 + 1.5 * 2^52: -(tf - 2) 2^59 + this is exact (a multiple of 2^8 below 2^60)
+        const double c60m = reg_const(0x1p60 + kI8MagicLo);
+        // warp w: output group w >> 1 (16 outputs) x input half w & 1 (16 inputs); lane:
+        // input lane >> 1 of that half, outputs 8 (lane & 1)..+7 of the group. A lane pair
+        // then writes one 16-byte core-matrix row and a warp 256 contiguous bytes per slice
+        // (conflict-free 8-byte stores; a lane = input mapping strides them by 16 bytes).
+        const int og16 = warp >> 1;
+        const int kin = (warp & 1) * 16 + (lane >> 1);   // input within the chunk
+        const int oh = lane & 1;
+        for (int64_t unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+            const int64_t ogi = unit % a.n_out_tiles, igi = unit / a.n_out_tiles;
+            const int64_t ot0 = ogi * a.i8_og, ot1 = (ot0 + a.i8_og < a.i8_out_tiles) ? ot0 + a.i8_og : a.i8_out_tiles;
+            const int64_t ib0 = igi * a.i8_ig, ib1 = (ib0 + a.i8_ig < a.i8_in_blocks) ? ib0 + a.i8_ig : a.i8_in_blocks;
+            for (int64_t ot = ot0; ot < ot1; ++ot) {
+            // Operands stay unscaled in registers: u = A_i + B_j + x.y, and the exact factor 16
+            // of u' = 16 u (table step 2^(1/4096)) rides on the Cody-Waite FMAs below -- the
+            // same values as staging (16A, 4X), (16B, 4Y), without a multiply on the loaded
+            // inputs (which made every chunk wait for its own prefetch).
+            double Bj[OW], Yj[OW][D], Wj[OW];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-#pragma unroll 1
+            for (int q = 0; q < OW; ++q) {
+                int64_t o = ot * i8::MT + og16 * 16 + oh * 8 + q;
+                Wj[q] = o < a.n_out ? a.out_w[o] : 0.0;
+                o = o < a.n_out ? o : a.n_out - 1;
+                Bj[q] = a.out_pack[o * PK];
+#pragma unroll
+                for (int d = 0; d < D; ++d) Yj[q][d] = a.out_pack[o * PK + 1 + d];
+            }
+            for (int64_t ib = ib0; ib < ib1; ++ib, ++ntile) {
+            const int64_t i0 = ib * a.in_block;
+            const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
+            double xn0, Xn[D];
+            {
+                const int64_t ic = (i0 + kin < i1) ? i0 + kin : i1 - 1;
+                xn0 = a.in_pack[ic * PK];
+#pragma unroll
+                for (int d = 0; d < D; ++d) Xn[d] = a.in_pack[ic * PK + 1 + d];
+            }
+            for (int64_t c0 = i0; c0 < i1; c0 += i8::KC, ++g) {
+                const uint32_t s = g % i8::STAGES, use = g / i8::STAGES;
+                uint8_t* sA = stages + s * i8::STAGE_BYTES;
+                const int64_t i = c0 + kin;
+                double x0 = xn0, X[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) X[d] = Xn[d];
+                if (i >= i1) x0 = -1.0e300;  // e = 0: every byte slice 0, no contribution
+                if (c0 + i8::KC < i1) {  // prefetch the next chunk's inputs (used one chunk later)
+                    const int64_t inx = (i + i8::KC < i1) ? i + i8::KC : i1 - 1;
+                    xn0 = a.in_pack[inx * PK];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) Xn[d] = a.in_pack[inx * PK + 1 + d];
+                }
+                if (use > 0) mbar_wait(smem_u32(bars + i8w::B_FREE + s), (use - 1) & 1u);
+                double rt = 0.0;
+                uint32_t wl[2][4], wh[2][3], wq[2];  // [group of 4 outputs][byte], low slice
+#pragma unroll
+                for (int q4 = 0; q4 < 2; ++q4) {
+                    uint32_t lo[4], hi[4], ql[4];
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        const int q = q4 * 4 + qq;
+                        double u = x0 + Bj[q];
+#pragma unroll
+                        for (int d = 0; d < D; ++d) u = fma(X[d], Yj[q][d], u);
+                        const double t = fma(u, 16.0, kI8Magic);  // u' + magic, u' = 16 u exact
+                        const double kf = t - kI8Magic;
+                        const double r = fma(u, 16.0, -kf);
+                        double p = fma(r, kI8R3, r2);
+                        p = fma(p, r, kI8R1);
+                        p = fma(p, r, 1.0);
+                        const int kc = (__double2hiint(t) >= kI8MagicHi) ? __double2loint(t) : 0;
+                        const unsigned off = (static_cast<unsigned>(kc) << 3) & (4095u << 3);
+                        const uint2 T = *reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(tab) + off);
+                        const double Tp = __hiloint2double(static_cast<int>(static_cast<unsigned>(kc) * 256u + T.y),
+                                                           static_cast<int>(T.x));
+                        const double e = Tp * p;
+                        rt = fma(e, Wj[q], rt);
+                        const double tf = e + 2.0;  // mantissa = P~ in 2^-51 units
+                        lo[qq] = static_cast<uint32_t>(__double2loint(tf));
+                        hi[qq] = static_cast<uint32_t>(__double2hiint(tf));
+                        // residual e - (tf - 2), exact, as rint(. 2^59) in the low word of tq
+                        const double nh = fma(tf, cm59, c60m);  // -(tf - 2) 2^59 + 1.5 2^52, exact
+                        const double tq = fma(e, c59, nh);
+                        ql[qq] = static_cast<uint32_t>(min(__double2loint(tq), 127));
+                    }
+                    byte_transpose<4>(lo[0], lo[1], lo[2], lo[3], wl[q4]);
+                    byte_transpose<3>(hi[0], hi[1], hi[2], hi[3], wh[q4]);
+                    wq[q4] = prmt(prmt(ql[0], ql[1], 0x40), prmt(ql[2], ql[3], 0x40), 0x5410);
+                }
+                // core matrix (og16, kin >> 3): 16 bytes (outputs) per input row kin & 7
+                uint8_t* dst = sA + og16 * 512 + kin * 16 + oh * 8;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    *reinterpret_cast<uint2*>(dst + k * i8::A_SLICE) = make_uint2(wl[0][k], wl[1][k]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    *reinterpret_cast<uint2*>(dst + (4 + k) * i8::A_SLICE) = make_uint2(wh[0][k], wh[1][k]);
+                *reinterpret_cast<uint2*>(dst + 7 * i8::A_SLICE) = make_uint2(wq[0], wq[1]);
+                rs[s * (i8w::NPW * 32) + warp * 32 + lane] = rt;
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_FULL + s));
+            }
+            // input block done: levels -> FP64; warp w: rows 32 (w % 4) + lane, columns 8 (w / 4)..+7
+            mbar_wait(smem_u32(bars + i8w::B_ACC), ntile & 1u);
+            tc_after_sync();
+            double acc[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+#pragma unroll
             for (int w = i8::NLEV - 1; w >= 0; --w) {  // smallest level first
-                uint32_t v[32];
-                tmem_ld32(trow + w * 32, v);
+                uint32_t v[8];
+                tmem_ld8(tmine + w * 32, v);
                 const double sc = __hiloint2double((1023 + 45 - 8 * w) << 20, 0);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) acc[c] = fma(static_cast<double>(static_cast<int32_t>(v[c])), sc, acc[c]);
-                tmem_zero32(trow + w * 32);
+                for (int c = 0; c < 8; ++c) acc[c] = fma(static_cast<double>(static_cast<int32_t>(v[c])), sc, acc[c]);
+                tmem_zero8(tmine + w * 32);
             }
             tmem_wait_st();
             tc_before_sync();
-            const int64_t o = ot * i8::MT + warp * 32 + lane;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_DRAIN));
+            // the unit's split-K partial of this output tile (row igi of [n_ig][kt][n_out]) sums
+            // its input blocks in order: read-modify-write by the owning thread (L2-resident;
+            // the scale is a power of two, so scaling each block's term is exact)
+            const int64_t o = ot * i8::MT + (warp & 3) * 32 + lane;
             if (o < a.n_out) {
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
+                for (int cc = 0; cc < 8; ++cc) {
+                    const int c = (warp >> 2) * 8 + cc;
                     if (c < a.kt) {
                         const unsigned ve = a.vexp[c];
                         const double sc = ve ? scalbn(1.0, -(53 - (static_cast<int>(ve) - 2048))) : 0.0;
-                        a.partial[(ib * a.kt + c) * a.n_out + o] = acc[c] * sc;
+                        double* pp = a.partial + (igi * a.kt + c) * a.n_out + o;
+                        double v = acc[cc] * sc;
+                        if (ib > ib0) v += *pp;
+                        *pp = v;
                     }
                 }
+            }
+            }
             }
         }
     }
@@ -498,15 +631,15 @@ __global__ void __launch_bounds__(i8::NT, 1) pts_i8_kernel(TileArgs a) {
 
 const void* i8_block_kernel(int d) {
     switch (d) {
-        case 1: return reinterpret_cast<const void*>(&pts_i8_kernel<1>);
-        case 2: return reinterpret_cast<const void*>(&pts_i8_kernel<2>);
-        case 3: return reinterpret_cast<const void*>(&pts_i8_kernel<3>);
-        case 4: return reinterpret_cast<const void*>(&pts_i8_kernel<4>);
+        case 1: return reinterpret_cast<const void*>(&pts_i8w_kernel<1>);
+        case 2: return reinterpret_cast<const void*>(&pts_i8w_kernel<2>);
+        case 3: return reinterpret_cast<const void*>(&pts_i8w_kernel<3>);
+        case 4: return reinterpret_cast<const void*>(&pts_i8w_kernel<4>);
         default: return nullptr;
     }
 }
-int i8_block_smem() { return i8::SMEM; }
-int i8_block_threads() { return i8::NT; }
+int i8_block_smem() { return i8w::SMEM; }
+int i8_block_threads() { return i8w::NT; }
 int i8_block_out_tile() { return i8::MT; }
 int i8_max_in_block() { return i8::MAX_IN_BLOCK; }
 int64_t i8_vslice_bytes(int64_t n_in) { return ((n_in + 31) / 32) * i8::B_BYTES; }

@@ -55,6 +55,9 @@ struct TileArgs {
     const uint8_t* vsl = nullptr;      // V digit tiles, 7168 bytes per 32-input chunk
     const unsigned* vexp = nullptr;    // per column: 2048 + largest exponent (0: zero column)
     int kt = 0;                        // columns of W (<= 32)
+    // pts_i8w_kernel work units: i8_og output tiles x i8_ig input blocks of the
+    // i8_out_tiles x i8_in_blocks tiling (n_out_tiles / n_in_blocks then count unit rows)
+    int64_t i8_og = 1, i8_ig = 1, i8_out_tiles = 0, i8_in_blocks = 0;
 };
 
 struct TilePlan {
@@ -62,6 +65,7 @@ struct TilePlan {
     bool i8 = false;                   // pts_i8_kernel: needs launch_i8_vprep on W first
     int grid = 0, smem = 0, occ = 0, nt = 128;
     int64_t out_tile = 0, in_block = 0, n_out_tiles = 0, n_in_blocks = 0, n_tiles = 0;
+    int64_t i8_og = 1, i8_ig = 1, i8_out_tiles = 0, i8_in_blocks = 0;  // pts_i8w_kernel work units
 };
 
 // dim: 0 = stored cost, 1..4 = point-cloud dimension. kt: block width (8..64) for MODE_BLOCK.

@@ -2419,6 +2419,12 @@ static int sm_count_cached() {
 
 // 128-output tiles x input blocks of <= 8192 inputs (int32 level bound), multiples of 32;
 // one CTA per SM (persistent).
+// pts_i8w_kernel: a CTA takes a work unit of og output tiles x ig input blocks. S is summed
+// over the unit's input blocks in registers (one partial row per ig-group instead of one per
+// input block) and r over its output tiles (one row per og-group instead of one per output
+// tile), so the split-K partials shrink from (NI S-rows, NO r-rows) to (ceil(NI/ig),
+// ceil(NO/og)). The shape is the one with the smallest makespan (cells on the busiest CTA)
+// over the input-block counts NI and ig; ties go to fewer partial bytes.
 static TilePlan plan_i8(int dim, int64_t n_out, int64_t n_in, int64_t max_in_blocks) {
     TilePlan p;
     p.fn = i8_block_kernel(dim);
@@ -2430,16 +2436,45 @@ static TilePlan plan_i8(int dim, int64_t n_out, int64_t n_in, int64_t max_in_blo
     p.occ = 1;
     const int64_t resident = sm_count_cached();
     p.out_tile = i8_block_out_tile();
-    p.n_out_tiles = (n_out + p.out_tile - 1) / p.out_tile;
-    int64_t want = (8 * resident + p.n_out_tiles - 1) / p.n_out_tiles;
-    if (max_in_blocks > 0 && want > max_in_blocks) want = max_in_blocks;
-    if (want < 1) want = 1;
-    int64_t in_block = (n_in + want - 1) / want;
-    in_block = ((in_block + 31) / 32) * 32;
-    if (in_block > i8_max_in_block()) in_block = i8_max_in_block();
-    p.in_block = in_block;
-    p.n_in_blocks = (n_in + in_block - 1) / in_block;
-    p.n_tiles = p.n_out_tiles * p.n_in_blocks;
+    const int64_t NO = (n_out + p.out_tile - 1) / p.out_tile;
+    const int64_t ni_min = (n_in + i8_max_in_block() - 1) / i8_max_in_block();
+    double best_span = 0.0, best_bytes = 0.0;
+    bool have = false;
+    for (int64_t want = ni_min; want <= ni_min + 24; ++want) {
+        int64_t in_block = (n_in + want - 1) / want;
+        in_block = ((in_block + 31) / 32) * 32;
+        if (in_block > i8_max_in_block()) continue;
+        const int64_t NI = (n_in + in_block - 1) / in_block;
+        for (int64_t ig = 1; ig <= NI; ++ig) {
+            const int64_t n_ig = (NI + ig - 1) / ig;
+            if (max_in_blocks > 0 && n_ig > max_in_blocks) continue;
+            // og so that the units fit the resident CTAs in one or two waves, or og = 1
+            // (many small units, round-robin: the fallback when NO does not split well)
+            for (int waves = 0; waves <= 2; ++waves) {
+                const int64_t per_ig = waves == 0 ? NO : (resident * waves) / n_ig;  // og-groups per ig-group
+                if (per_ig < 1) continue;
+                const int64_t og = (NO + per_ig - 1) / per_ig;
+                const int64_t n_og = (NO + og - 1) / og;
+                const int64_t units = n_og * n_ig;
+                const int64_t rounds = (units + resident - 1) / resident;
+                const double span = static_cast<double>(rounds) * og * ig * in_block;
+                const double bytes = static_cast<double>(n_ig) * n_out * 32 + static_cast<double>(n_og) * n_in;
+                if (!have || span < best_span * 0.99 || (span <= best_span * 1.01 && bytes < best_bytes)) {
+                    have = true;
+                    best_span = span;
+                    best_bytes = bytes;
+                    p.in_block = in_block;
+                    p.i8_in_blocks = NI;
+                    p.i8_ig = ig;
+                    p.i8_og = og;
+                    p.n_in_blocks = n_ig;
+                    p.n_out_tiles = n_og;
+                }
+            }
+        }
+    }
+    p.i8_out_tiles = NO;
+    p.n_tiles = p.n_out_tiles * p.n_in_blocks;  // work units
     p.grid = static_cast<int>(p.n_tiles < resident ? p.n_tiles : resident);
     return p;
 }
@@ -2561,6 +2596,10 @@ void launch_tiles(const TilePlan& p, TileArgs a, cudaStream_t s) {
     a.n_in_blocks = p.n_in_blocks;
     a.n_tiles = p.n_tiles;
     a.in_block = p.in_block;
+    a.i8_og = p.i8_og;
+    a.i8_ig = p.i8_ig;
+    a.i8_out_tiles = p.i8_out_tiles;
+    a.i8_in_blocks = p.i8_in_blocks;
     void* args[] = {&a};
     count_launch();
     cudaLaunchKernel(p.fn, dim3(p.grid), dim3(p.nt), args, p.smem, s);

@@ -49,7 +49,9 @@ def _both_paths(fn):
 
 
 @pytest.mark.parametrize("d,n,m,ell", [(2, 3000, 2500, 24), (1, 2100, 2049, 16), (3, 2047, 2300, 32),
-                                        (4, 2500, 1800, 5), (2, 4096, 4096, 32)])
+                                        (4, 2500, 1800, 5), (2, 4096, 4096, 32),
+                                        # work units of 2 output tiles x 2 input blocks (plan_i8)
+                                        (2, 30000, 12000, 12)])
 def test_tensor_block_pass_matches_fp64_and_oracle(d, n, m, ell):
     rng, x, y, a, b = _points(d, n, m, d * 7919 + n + ell)
     eps = 0.02
