@@ -401,6 +401,28 @@ def run_ours(args, world, rank, local):
         comm["sknr_iteration_stable"] = {"calls": calls / (1 + max(3, args.steps // 10)),
                                          "bytes": nbytes / (1 + max(3, args.steps // 10))}
 
+    # ---- the Newton derivative pass alone (S = V^T P~, r = P~ beta): tensor-core slices vs FP64 DMMA
+    newton_pass = None
+    if world == 1 and inst.ell <= 32:
+        ms_i8, k_i8 = sk.bench_pass(prob, 4, inst.ell, passes=5)
+        prev = sk.set_tensor_block_pass(False)
+        try:
+            ms_f64, k_f64 = sk.bench_pass(prob, 4, inst.ell, passes=5)
+        finally:
+            sk.set_tensor_block_pass(prev)
+        slots = 14.0  # FP64 issue slots per cell of pts_i8w_kernel (DESIGN 4.1)
+        newton_pass = {"ell": inst.ell,
+                       "tensor_core": {"kernel": "pts_i8w_kernel (tcgen05.mma.kind::i8 over exact byte slices)",
+                                       "pass_ms": ms_i8, "kernel_ms": k_i8,
+                                       "gcells_per_s": cells / (k_i8 * 1e-3) / 1e9,
+                                       "fp64_slots_per_cell": slots,
+                                       "int8_macs_per_cell": 1120,
+                                       "frac_of_nominal_fp64": slots * 2 * cells / (k_i8 * 1e-3) / 1e12 / peak_nominal,
+                                       "int8_tmacs_per_s": 1120 * cells / (k_i8 * 1e-3) / 1e12},
+                       "fp64_dmma": {"kernel": "pts_mma2_kernel<.., RS> (mma.sync m8n8k4 f64)",
+                                     "pass_ms": ms_f64, "kernel_ms": k_f64,
+                                     "gcells_per_s": cells / (k_f64 * 1e-3) / 1e9}}
+
     # ---- e2e: public C ABI with host buffers (problem upload + solve + potentials download)
     # Five complete runs (each: new problem from host arrays, K iterations, download);
     # the median is reported, all five are listed (host-side allocation jitter).
@@ -645,6 +667,7 @@ def run_ours(args, world, rank, local):
                                "stable_accept": {"ms": ms_nr_st, "kernels": kpi_nr_st,
                                                  "note": "candidate column LSE replaced by the anchor pass "
                                                          "s, t, u = P~^T (1, expm1(d/eps), exp(d/eps))"}},
+            "newton_pass": newton_pass,
             "collectives": comm,
             "cpu_time_to_tol": cpu_ttt,
             "pass_ms": {"column_lse_full": ms_pass, "row_lse_full": ms_row_pass,

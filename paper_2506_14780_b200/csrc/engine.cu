@@ -327,6 +327,7 @@ struct Problem {
     DBuf L[2], ref[2], shift[2], pack_in[2], pack_out[2], stats;
     DBuf partial, rsum;
     DBuf vsl, vexp;  // tensor-core block pass: V digit tiles, column exponents (i8_kernels.cu)
+    const double* vsl_src = nullptr;  // the static W whose digit tiles vsl holds (a solve's basis), or nullptr
     std::shared_ptr<SolveState> solve_cache;  // per-solve device buffers, reused across solves
     // culling (sknr_problem_set_culling): threshold T (0 = off) and per-direction group bounds
     double cull_t = 0.0;
@@ -1034,6 +1035,7 @@ struct PassSpec {
     // x k, rank-blocked) is summed over the shards and this rank receives its block
     // (scatter_rows x k, ld = scatter_rows) here
     double* scatter_out = nullptr;
+    bool w_static = false;             // W is the solve's packed basis: its int8 digit tiles are made once per solve
     bool cull = false;                 // block pass may skip negligible terms (culling enabled)
     const double* cull_logtot = nullptr;  // per-output log of sum_in e (nullptr: 0, i.e. sums are 1)
     unsigned guard = 0;
@@ -1120,10 +1122,14 @@ static void plan_pass(Problem& P, const PassSpec& ps) {
         ta.out_w = out.w.p;
         ta.rsum = P.rsum.p;
     }
-    if (tp.i8) {  // tensor-core pass: V as exact int8 digit tiles (rebuilt per pass, O(n kt))
+    if (tp.i8) {  // tensor-core pass: V as exact int8 digit tiles, O(n kt); a solve's basis keeps
+                  // the tiles made by prepare_solve, any other W is converted per pass
         uint8_t* vsl = reinterpret_cast<uint8_t*>(P.vsl.p);
         unsigned* vexp = reinterpret_cast<unsigned*>(P.vexp.p);
-        launch_i8_vprep(ps.W, ps.kt, nin, vsl, vexp, P.st, ps.guard, s);
+        if (!(ps.w_static && P.vsl_src == ps.W)) {
+            launch_i8_vprep(ps.W, ps.kt, nin, vsl, vexp, P.st, ps.guard, s);
+            P.vsl_src = nullptr;
+        }
         ta.vsl = vsl;
         ta.vexp = vexp;
         ta.kt = ps.kt;

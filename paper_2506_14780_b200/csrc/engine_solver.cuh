@@ -150,6 +150,7 @@ static void enqueue_iteration(Problem& P, SolveState& S, int64_t ell, bool trace
         sp.out = S.S.p;
         sp.scatter_out = P.shard ? S.Sloc.p : nullptr;
         sp.rsum_out = fuse_r ? S.r.p : nullptr;
+        sp.w_static = true;
         sp.cull = cull_nr;  // P~ columns sum to 1 at h = f^{C,eps}: no normalisation needed
         sp.guard = gn;
         plan_pass(P, sp);
@@ -329,7 +330,14 @@ static void prepare_solve(Problem& P, SolveState& S, int64_t ell, const double* 
                                                      S.Wv.p);
         // pre-size the block-pass partials outside graph capture
         const bool cull_nr = cull_block_active(P, 0) && cull_active(P, 1);
-        plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
+        const TilePlan bp =
+            plan_for(P, 0, cull_nr ? MODE_BLOCK_CULL : (block_rs_fusable(P) ? MODE_BLOCK_RS : MODE_BLOCK), kt, 8);
+        P.vsl_src = nullptr;
+        if (bp.i8) {  // the basis is fixed for the solve: its int8 digit tiles are made once, here
+            launch_i8_vprep(S.Wv.p, kt, n, reinterpret_cast<uint8_t*>(P.vsl.p),
+                            reinterpret_cast<unsigned*>(P.vexp.p), P.st, 0, s);
+            P.vsl_src = S.Wv.p;
+        }
         if (accept == 1) {  // stable accept test: anchor pass with W = (1, expm1(d/eps))
             const int akt = anchor_kt(P);
             S.dvec.ensure(n);
