@@ -99,17 +99,15 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
 }
 
-// try_wait with a suspend-time hint (ns): a waiting warp sleeps in hardware instead of
-// re-issuing the test (the producers' and service warps' polls took 14 % of the issue slots)
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@P1 bra DONE_%=;\n\t"
         "bra WAIT_%=;\n"
         "DONE_%=:\n\t}\n" ::"r"(mbar),
-        "r"(parity), "r"(2000u)
+        "r"(parity)
         : "memory");
 }
 
@@ -357,8 +355,6 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm8 + i8w::OFF_BAR);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + i8w::B_DRAIN + 1);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint32_t bar0 = smem_u32(bars);  // shared-window address of bars[0]; bars[q] = bar0 + 8 q
-    asm volatile("" : "+r"(bar0));   // opaque: keep it in a register instead of re-deriving it per chunk
 
     for (int t = tid; t < 4096; t += i8w::NT) {  // 2^(e/4096), hi word pre-biased by -(e << 8)
         const unsigned e = static_cast<unsigned>(t);
@@ -368,12 +364,12 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
     }
     if (tid == 0) {
         for (int q = 0; q < i8::STAGES; ++q) {
-            mbar_init((bar0 + 8u * (i8w::B_FREE + q)), 2);  // MMAs completed + r terms read
-            mbar_init((bar0 + 8u * (i8w::B_VT + q)), 1);
-            mbar_init((bar0 + 8u * (i8w::B_FULL + q)), i8w::NPW);
+            mbar_init(smem_u32(bars + i8w::B_FREE + q), 2);  // MMAs completed + r terms read
+            mbar_init(smem_u32(bars + i8w::B_VT + q), 1);
+            mbar_init(smem_u32(bars + i8w::B_FULL + q), i8w::NPW);
         }
-        mbar_init((bar0 + 8u * (i8w::B_ACC)), 1);
-        mbar_init((bar0 + 8u * (i8w::B_DRAIN)), i8w::NPW);
+        mbar_init(smem_u32(bars + i8w::B_ACC), 1);
+        mbar_init(smem_u32(bars + i8w::B_DRAIN), i8w::NPW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tmem_alloc(smem_u32(tslot));
@@ -418,7 +414,7 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
             const int64_t i0 = ib * a.in_block;
             const int64_t i1 = (i0 + a.in_block < a.n_in) ? i0 + a.in_block : a.n_in;
             if (role == 0 && ntile > 0) {  // the previous tile's levels have been read and zeroed
-                mbar_wait((bar0 + 8u * (i8w::B_DRAIN)), (ntile - 1) & 1u);
+                mbar_wait(smem_u32(bars + i8w::B_DRAIN), (ntile - 1) & 1u);
                 tc_after_sync();
             }
             for (int64_t c0 = i0; c0 < i1; c0 += i8::KC, ++g) {
@@ -427,8 +423,8 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
                 uint8_t* sB = sA + i8::A_BYTES;
                 if (role == 0) {
                     if (lane == 0) {
-                        mbar_wait((bar0 + 8u * (i8w::B_FULL + s)), use & 1u);
-                        mbar_wait((bar0 + 8u * (i8w::B_VT + s)), use & 1u);
+                        mbar_wait(smem_u32(bars + i8w::B_FULL + s), use & 1u);
+                        mbar_wait(smem_u32(bars + i8w::B_VT + s), use & 1u);
                         tc_after_sync();
                         const uint64_t bd = umma_desc(smem_u32(sB), 128, 256);
 #pragma unroll
@@ -439,16 +435,16 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
                         }
                         mma_i8(tbase + 7 * 32, umma_desc(smem_u32(sA + 7 * i8::A_SLICE), 128, 512), bd, i8::IDESC_LO,
                                1u);
-                        mma_commit((bar0 + 8u * (i8w::B_FREE + s)));
-                        if (c0 + i8::KC >= i1) mma_commit((bar0 + 8u * (i8w::B_ACC)));
+                        mma_commit(smem_u32(bars + i8w::B_FREE + s));
+                        if (c0 + i8::KC >= i1) mma_commit(smem_u32(bars + i8w::B_ACC));
                     }
                     __syncwarp();
                 } else if (role == 3) {
                     if (lane == 0) {
-                        if (use > 0) mbar_wait((bar0 + 8u * (i8w::B_FREE + s)), (use - 1) & 1u);
-                        mbar_expect_tx((bar0 + 8u * (i8w::B_VT + s)), i8::B_BYTES);
+                        if (use > 0) mbar_wait(smem_u32(bars + i8w::B_FREE + s), (use - 1) & 1u);
+                        mbar_expect_tx(smem_u32(bars + i8w::B_VT + s), i8::B_BYTES);
                         bulk_g2s(smem_u32(sB), a.vsl + (c0 >> 5) * i8::B_BYTES, i8::B_BYTES,
-                                 (bar0 + 8u * (i8w::B_VT + s)));
+                                 smem_u32(bars + i8w::B_VT + s));
                     }
                     __syncwarp();
                 } else if (static_cast<int>(g & 1u) == role - 1) {
@@ -457,7 +453,7 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
                     const bool rok = c0 + lane < i1;
                     double rold = 0.0;
                     if (rok && ot > ot0) rold = rrow[c0 + lane];
-                    mbar_wait((bar0 + 8u * (i8w::B_FULL + s)), use & 1u);
+                    mbar_wait(smem_u32(bars + i8w::B_FULL + s), use & 1u);
                     // r of input `lane` over the tile's 128 outputs: the 16 producer terms
                     // (output group 0..7, half 0..1) as a fixed pairwise tree; producer warp
                     // 2 og + (lane >> 4) holds them in lanes 2 (lane & 15) + half
@@ -471,7 +467,7 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
                     const double v = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
                     if (rok) rrow[c0 + lane] = rold + v;
                     __syncwarp();
-                    if (lane == 0) mbar_arrive((bar0 + 8u * (i8w::B_FREE + s)));
+                    if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_FREE + s));
                 }
             }
             }
@@ -533,7 +529,7 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
 #pragma unroll
                     for (int d = 0; d < D; ++d) Xn[d] = a.in_pack[inx * PK + 1 + d];
                 }
-                if (use > 0) mbar_wait((bar0 + 8u * (i8w::B_FREE + s)), (use - 1) & 1u);
+                if (use > 0) mbar_wait(smem_u32(bars + i8w::B_FREE + s), (use - 1) & 1u);
                 double rt = 0.0;
                 uint32_t wl[2][4], wh[2][3], wq[2];  // [group of 4 outputs][byte], low slice
 #pragma unroll
@@ -582,10 +578,10 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
                 rs[s * (i8w::NPW * 32) + warp * 32 + lane] = rt;
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) mbar_arrive((bar0 + 8u * (i8w::B_FULL + s)));
+                if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_FULL + s));
             }
             // input block done: levels -> FP64; warp w: rows 32 (w % 4) + lane, columns 8 (w / 4)..+7
-            mbar_wait((bar0 + 8u * (i8w::B_ACC)), ntile & 1u);
+            mbar_wait(smem_u32(bars + i8w::B_ACC), ntile & 1u);
             tc_after_sync();
             double acc[8];
 #pragma unroll
@@ -602,7 +598,7 @@ __global__ void __launch_bounds__(i8w::NT, 1) pts_i8w_kernel(TileArgs a) {
             tmem_wait_st();
             tc_before_sync();
             __syncwarp();
-            if (lane == 0) mbar_arrive((bar0 + 8u * (i8w::B_DRAIN)));
+            if (lane == 0) mbar_arrive(smem_u32(bars + i8w::B_DRAIN));
             // the unit's split-K partial of this output tile (row igi of [n_ig][kt][n_out]) sums
             // its input blocks in order: read-modify-write by the owning thread (L2-resident;
             // the scale is a power of two, so scaling each block's term is exact)
