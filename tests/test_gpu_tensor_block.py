@@ -92,3 +92,33 @@ def test_tensor_block_pass_sknr_solve_matches_fp64_and_oracle():
     acc_o = [bool(t[4]) for t in ro["trace"]]
     assert acc_t == [t.newton_accepted for t in rf.trace] == acc_o
     assert rel_err(rt.f, ro["f"]) <= 1e-9 and rel_err(rt.g, ro["g"]) <= 1e-9
+
+
+def test_basis_digit_tiles_follow_the_solve():
+    """The basis' int8 digit tiles are made once per solve (prepare_solve) and reused by every
+    Newton pass of that solve; a second solve on the same handle with another basis, and a
+    restricted_derivatives call in between (its own W), must not see stale tiles."""
+    inst = G.config("C4", n=2048, m=2048)
+    eps = 4e-3
+    rng = np.random.default_rng(5)
+    Va = np.asfortranarray(smooth_basis(inst.x, inst.alpha, 8))
+    Vb = np.asfortranarray(np.linalg.qr(rng.standard_normal((2048, 8)))[0] * np.sqrt(2048.0))
+    ba = sk.SpectralBasis(Va, Va, np.zeros(8), eps)
+    bb = sk.SpectralBasis(Vb, Vb, np.zeros(8), eps)
+
+    def make():
+        return sk.PointProblem(inst.x, inst.y, inst.alpha, inst.beta, eps, inst.cost_scale)
+
+    def run(p, basis):
+        return sk.solve(p, tol=1e-9, max_iter=40, ell=8, basis=basis, trace=True, accept="stable")
+
+    p = make()
+    ra = run(p, ba)
+    f0 = rng.uniform(-0.01, 0.01, 2048)
+    sk.restricted_derivatives(p, f0, bb)
+    rb = run(p, bb)
+    ra2 = run(p, ba)
+    rb_fresh = run(make(), bb)
+    assert np.array_equal(rb.f, rb_fresh.f) and np.array_equal(rb.g, rb_fresh.g)
+    assert np.array_equal(ra.f, ra2.f) and ra.iterations == ra2.iterations
+    assert [t.newton_accepted for t in rb.trace] == [t.newton_accepted for t in rb_fresh.trace]
