@@ -15,6 +15,3 @@ timeout 600 python bench.py --steps 3 --warmup 3 --no-ttt > gpurun_out/bench_sma
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/launches_r02.csv \
   python bench.py --steps 3 --warmup 3 --no-ttt > gpurun_out/ncu_launch_r02.log 2>&1
 echo "launch list rc=$?"
-# memcheck of the tensor-core pass on one small case (smem / global bounds, mbarrier misuse)
-timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_tensor_block.py -q -x \
-  -p no:cacheprovider -k "2500-1800 or probe" > gpurun_out/memcheck_i8.log 2>&1; echo "memcheck rc=$?"; tail -4 gpurun_out/memcheck_i8.log
